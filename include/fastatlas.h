@@ -1,0 +1,184 @@
+/*
+ * fastatlas.h — C ABI of the B200 (sm_100a) per-frame atlasing library.
+ *
+ * The reference (`atlaspack`, pure Python/numpy) has no FFI; its boundary is
+ * the Python API re-exported by /root/reference/pkg/src/atlaspack/__init__.py:3-64
+ * plus `run_scene_pipeline` (cli.py:360-406).  Each entry point below replaces
+ * one reference function on the per-frame path; the comment names it.  The
+ * Python mirror (paper_2502_17712_b200/) binds these through ctypes, exactly
+ * as INTEGRATION.md shows for the reference package.
+ *
+ * Conventions
+ *   - All array pointers are DEVICE pointers unless the parameter says host.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *   - A context is bound to one device, owns its scratch and frame outputs
+ *     (valid until the next call on the same context) and is not thread safe.
+ *   - Return value: FA_OK or one of the status codes, which map 1:1 onto the
+ *     reference's exceptions (ValueError, PackFailure, NothingVisible,
+ *     HeightOverflow, DegenerateChart); negative codes are CUDA / internal
+ *     errors.  fa_last_error() gives a message.
+ *   - Triangles are int32 (T,3) row-major; positions float64 (V,3) row-major;
+ *     camera matrices are the 16 row-major float64 of CameraFrame.view_proj
+ *     (geometry.py:90-92), passed by HOST pointer.
+ */
+#ifndef FASTATLAS_H
+#define FASTATLAS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FA_ABI_VERSION 1
+
+enum fa_status {
+    FA_OK = 0,
+    FA_VALUE_ERROR = 1,       /* ValueError (packing.py:313-323,365-367, charts.py:294-295, ...) */
+    FA_PACK_FAILURE = 2,      /* PackFailure (packing.py:328-332,345) */
+    FA_NOTHING_VISIBLE = 3,   /* NothingVisible (cli.py:366-368) */
+    FA_HEIGHT_OVERFLOW = 4,   /* HeightOverflow (packing.py:127-129) */
+    FA_DEGENERATE_CHART = 5,  /* DegenerateChart (geometry.py:320-321) */
+    FA_CUDA_ERROR = -1,
+    FA_INTERNAL_ERROR = -2
+};
+
+typedef struct fa_ctx fa_ctx;
+
+/* ---- context ---------------------------------------------------------- */
+int fa_abi_version(void);
+const char *fa_last_error(void);
+int fa_create(fa_ctx **out, int device);
+void fa_destroy(fa_ctx *ctx);
+
+/* Bind a resident mesh (Mesh, charts.py:29-61).  The caller keeps both
+ * buffers alive while the context uses them. */
+int fa_set_mesh(fa_ctx *ctx, const double *positions, int64_t n_vertices,
+                const int32_t *triangles, int64_t n_triangles);
+
+/* ---- per-stage entry points (reference functions) ----------------------- */
+
+/* homo @ view_proj.T for every vertex (charts.py:273-274); clip_out is (V,4). */
+int fa_project(fa_ctx *ctx, const double *vp_host, double *clip_out, void *stream);
+
+/* depth_prepass (charts.py:285-299): depth_out (H,W) float64, +inf uncovered. */
+int fa_depth_prepass(fa_ctx *ctx, const double *vp_host, int width, int height, int backface_cull,
+                     double *depth_out, void *stream);
+
+/* mark_visible (charts.py:302-313): flags_out (T,) uint8. */
+int fa_mark_visible(fa_ctx *ctx, const double *vp_host, const double *depth, int width, int height,
+                    int backface_cull, uint8_t *flags_out, void *stream);
+
+/* connected_charts (charts.py:343-359): labels_out (T,) int32, -1 invisible. */
+int fa_connected_charts(fa_ctx *ctx, const int32_t *adjacency, const uint8_t *flags,
+                        int32_t *labels_out, void *stream);
+
+/* merge_shared_vertices (charts.py:362-386): labels_out (T,), vertex_to_chart_out (V,) int32. */
+int fa_merge_shared_vertices(fa_ctx *ctx, const int32_t *labels_in, int32_t *labels_out,
+                             int32_t *vertex_to_chart_out, void *stream);
+
+/* Per-chart chart_bbox (geometry.py:281-322) + viewport_box (geometry.py:352-362)
+ * + prescale (cli.py:379-384) for every chart of `labels` in ascending-root
+ * order.  Outputs are sized for the worst case (T charts); *n_charts_host
+ * receives the count (synchronises the stream). */
+int fa_chart_boxes(fa_ctx *ctx, const double *vp_host, const int32_t *labels, int width, int height,
+                   double prescale, int32_t *roots_out, double *ndc_out, int32_t *px_out,
+                   int64_t *target_out, int64_t *n_charts_host, void *stream);
+
+/* Batched forms of the scalar geometry helpers on the chart_bbox path:
+ * blinn_clamped_ndc (geometry.py:185-200) over (n,4) points -> (n,2);
+ * select_side_plane (geometry.py:257-278) over (n,3,4) clip triangles ->
+ * plane index 0..3 (left, right, bottom, top) or -1 for None;
+ * chart_bbox (geometry.py:281-322) of (n,3,3) world triangles -> box_host[4]
+ * (FA_DEGENERATE_CHART when nothing survives);
+ * viewport_box (geometry.py:352-362) over (n,4) boxes -> (n,2) int64. */
+int fa_blinn_clamped_ndc(fa_ctx *ctx, const double *points4, int64_t n, double *out2, void *stream);
+int fa_select_side_plane(fa_ctx *ctx, const double *tris12, int64_t n, int32_t *out, void *stream);
+int fa_chart_bbox(fa_ctx *ctx, const double *vp_host, const double *tris_xyz, int64_t n, double *box_host,
+                  void *stream);
+int fa_viewport_box(fa_ctx *ctx, const double *boxes4, int64_t n, int width, int height, int64_t *out2,
+                    void *stream);
+
+/* orient (packing.py:109-117): rotate boxes wider than tall. */
+int fa_orient(fa_ctx *ctx, const int64_t *target_w, const int64_t *target_h, int64_t n, int64_t *ow_out,
+              int64_t *oh_out, uint8_t *rot_out, void *stream);
+
+/* orient + order (packing.py:109-130): perm_out[i] = input index of the i-th
+ * ordered box; ow/oh oriented dims, rot rotated flag. */
+int fa_orient_order(fa_ctx *ctx, const int64_t *target_w, const int64_t *target_h,
+                    const int64_t *min_tri, int64_t n, int64_t max_h, int32_t *perm_out,
+                    int64_t *ow_out, int64_t *oh_out, uint8_t *rot_out, void *stream);
+
+/* fold (packing.py:133-158). *m_host receives overflow_m (synchronises). */
+int fa_fold(fa_ctx *ctx, const int64_t *widths, int64_t n, int64_t omega, int64_t *rows_out,
+            int64_t *x_out, int64_t *m_host, void *stream);
+
+/* push_up (packing.py:170-215). *used_host receives the frontline maximum. */
+int fa_push_up(fa_ctx *ctx, const int64_t *rows, const int64_t *x, const int64_t *widths,
+               const int64_t *heights, int64_t n, int64_t omega, int64_t *y_out, int64_t *used_host,
+               void *stream);
+
+/* pack_at_scale / _pack_arrays (packing.py:218-292) on ordered oriented
+ * boxes.  *accepted_host = 1 and xywh_out (n,4), scale_host[2] on accept. */
+int fa_pack_at_scale(fa_ctx *ctx, const int64_t *ow, const int64_t *oh, int64_t n, int64_t num,
+                     int64_t den, int64_t omega, int64_t min_dim, int64_t padding, int64_t *xywh_out,
+                     int64_t *scale_host, int *accepted_host, void *stream);
+
+/* pack (packing.py:295-345).  placements_out (n,8) int64 in packing order:
+ * chart_id x y w h rotated target_w target_h.  scale_host[2] = num, den.
+ * accept_out (optional, n_scales bytes, device) receives the accept vector. */
+int fa_pack(fa_ctx *ctx, const int64_t *target_w, const int64_t *target_h, const int64_t *chart_id,
+            const int64_t *min_tri, int64_t n, int64_t omega, int64_t n_scales, int64_t min_dim,
+            int64_t padding, int64_t *placements_out, int64_t *scale_host, uint8_t *accept_out,
+            void *stream);
+
+/* ---- whole frame: run_scene_pipeline (cli.py:360-406) -------------------- */
+typedef struct fa_frame_params {
+    int width, height;       /* SceneConfig.screen */
+    int64_t omega;           /* SceneConfig.omega (power of two) */
+    int64_t n_scales;        /* SceneConfig.n_scales */
+    int64_t min_dim;         /* SceneConfig.min_dim */
+    int64_t padding;         /* SceneConfig.padding */
+    double prescale;         /* SceneConfig.prescale */
+    int backface_cull;       /* SceneConfig.backface_cull */
+    int uv_f64;              /* 1: emit float64 UVs (bit-exact), 0: float32 */
+    int want_depth;          /* 1: decode the depth buffer into float64 */
+    int use_graph;           /* 1: replay a captured CUDA graph per shape */
+} fa_frame_params;
+
+typedef struct fa_frame_result {
+    int status;                   /* fa_status of the frame */
+    int32_t n_visible;            /* visible triangles */
+    int32_t n_charts;             /* charts (= boxes = placements) */
+    int64_t scale_num, scale_den; /* AtlasLayout.scale */
+    int64_t screen_fragments;     /* cli.py:390 */
+    int64_t texels_allocated;     /* cli.py:391-393 */
+    /* device pointers owned by the context, valid until its next frame */
+    const double *depth;            /* (H,W) float64 when want_depth */
+    const uint8_t *flags;           /* (T,) visibility */
+    const int32_t *visible;         /* (n_visible,) ascending triangle ids */
+    const int32_t *chart_of_triangle; /* (T,) -1 invisible */
+    const int32_t *vertex_to_chart; /* (V,) -1 unmapped */
+    const int32_t *roots;           /* (n_charts,) ascending chart ids */
+    const double *ndc;              /* (n_charts,4) min_x min_y max_x max_y */
+    const int32_t *px;              /* (n_charts,2) viewport w_px h_px */
+    const int64_t *target;          /* (n_charts,2) target_w target_h */
+    const int64_t *placements;      /* (n_charts,8) packing order */
+    const void *uv;                 /* (n_visible,6) float32 or float64, NaN = no UV */
+} fa_frame_result;
+
+/* Enqueue a whole frame on `stream` (no host synchronisation). */
+int fa_frame_launch(fa_ctx *ctx, const double *vp_host, const fa_frame_params *params, void *stream);
+/* Wait for the frame and fill `out` (synchronises the stream). */
+int fa_frame_finish(fa_ctx *ctx, fa_frame_result *out, void *stream);
+/* launch + finish */
+int fa_frame(fa_ctx *ctx, const double *vp_host, const fa_frame_params *params, fa_frame_result *out,
+             void *stream);
+
+/* Number of kernels the last fa_frame_launch enqueued (benchmark accounting). */
+int fa_last_launch_count(fa_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FASTATLAS_H */

@@ -1,0 +1,874 @@
+// fa_api.cu — C ABI (include/fastatlas.h): contexts, per-stage entry
+// points and the whole-frame pipeline (run_scene_pipeline, cli.py:360-406).
+//
+// The frame is a fixed sequence of kernels whose work sizes are read from a
+// device status block (fa_dstat), so the whole frame needs no host round
+// trip and is captured once per shape into a CUDA graph; per frame only the
+// 128-byte camera matrix is uploaded before the graph launch.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+
+#include "fa_internal.h"
+#include "fa_raster.cuh"
+
+static thread_local std::string g_err;
+
+static int set_err(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(x)                                                                                    \
+    do {                                                                                         \
+        cudaError_t e_ = (x);                                                                    \
+        if (e_ != cudaSuccess) return set_err(FA_CUDA_ERROR, "%s: %s", #x, cudaGetErrorString(e_)); \
+    } while (0)
+
+#define CKL()                                                                                    \
+    do {                                                                                         \
+        cudaError_t e_ = cudaGetLastError();                                                     \
+        if (e_ != cudaSuccess) return set_err(FA_CUDA_ERROR, "launch: %s", cudaGetErrorString(e_)); \
+    } while (0)
+
+size_t fa_trisetup_bytes() { return sizeof(TriSetup); }
+
+bool fa_ensure(fa_ctx* ctx, fa_buf& b, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (b.bytes >= bytes) return true;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    size_t alloc = bytes + bytes / 4 + 256;
+    if (cudaMalloc(&b.p, alloc) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    b.bytes = alloc;
+    ctx->gen++;
+    return true;
+}
+
+#define ENSURE(buf, n)                                                                     \
+    do {                                                                                   \
+        if (!fa_ensure(ctx, ctx->buf, (size_t)(n)))                                        \
+            return set_err(FA_CUDA_ERROR, "out of device memory allocating " #buf " (%zu B)", (size_t)(n)); \
+    } while (0)
+
+template <typename T>
+static T* P(const fa_buf& b) {
+    return reinterpret_cast<T*>(b.p);
+}
+
+static void free_buf(fa_buf& b) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+}
+
+extern "C" {
+
+int fa_abi_version(void) { return FA_ABI_VERSION; }
+const char* fa_last_error(void) { return g_err.c_str(); }
+
+int fa_create(fa_ctx** out, int device) {
+    if (!out) return set_err(FA_VALUE_ERROR, "null output pointer");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) return set_err(FA_CUDA_ERROR, "no CUDA device: %s", cudaGetErrorString(e));
+    if (device < 0 || device >= n) return set_err(FA_VALUE_ERROR, "bad device %d", device);
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+        return set_err(FA_CUDA_ERROR, "device %s is sm_%d%d; this library is built for sm_100a", prop.name,
+                       prop.major, prop.minor);
+    fa_ctx* c = new fa_ctx();
+    c->device = device;
+    c->max_large = 1 << 16;
+    c->max_tiles = 1 << 18;
+    c->pack_batch = 148;
+    if (cudaMallocHost(&c->hstat, sizeof(fa_dstat)) != cudaSuccess ||
+        cudaMallocHost(&c->hvp, 16 * sizeof(double)) != cudaSuccess) {
+        delete c;
+        return set_err(FA_CUDA_ERROR, "cudaMallocHost failed");
+    }
+    memset(c->hstat, 0, sizeof(fa_dstat));
+    *out = c;
+    return FA_OK;
+}
+
+void fa_destroy(fa_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+    fa_buf* bufs[] = {&c->clip, &c->depth_keys, &c->depth_f64, &c->flags, &c->vis_list, &c->small_list, &c->large,
+                      &c->tiles, &c->label, &c->vmin, &c->v2c, &c->cidx, &c->roots, &c->ndc_keys, &c->ndc, &c->px,
+                      &c->target, &c->survived, &c->okey, &c->oidx, &c->ow, &c->oh, &c->orot, &c->sortk, &c->sortv,
+                      &c->pinv, &c->cand, &c->cand_p, &c->cand_w, &c->cand_h, &c->cand_y, &c->rowstart,
+                      &c->placements, &c->uv, &c->vp_dev, &c->blocks, &c->dstat, &c->aux, &c->in_tw, &c->in_th,
+                      &c->in_cid, &c->in_mt};
+    for (fa_buf* b : bufs) free_buf(*b);
+    if (c->hstat) cudaFreeHost(c->hstat);
+    if (c->hvp) cudaFreeHost(c->hvp);
+    delete c;
+}
+
+int fa_set_mesh(fa_ctx* ctx, const double* positions, int64_t n_vertices, const int32_t* triangles,
+                int64_t n_triangles) {
+    if (!ctx) return set_err(FA_VALUE_ERROR, "null context");
+    if (n_vertices < 0 || n_triangles < 0 || n_vertices >= (1ll << 31) - 1 || n_triangles >= (1ll << 31) / 4)
+        return set_err(FA_VALUE_ERROR, "mesh too large for 32-bit indices");
+    if ((n_vertices > 0 && !positions) || (n_triangles > 0 && !triangles))
+        return set_err(FA_VALUE_ERROR, "null mesh buffer");
+    ctx->pos = positions;
+    ctx->tris = triangles;
+    ctx->V = n_vertices;
+    ctx->T = n_triangles;
+    return FA_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// internal helpers
+// ---------------------------------------------------------------------------
+static int ensure_raster(fa_ctx* ctx, int W, int H, bool depth) {
+    int64_t T = ctx->T, V = ctx->V;
+    ENSURE(clip, (V > 0 ? V : 1) * sizeof(double4));
+    if (depth) ENSURE(depth_keys, (size_t)W * H * 8);
+    ENSURE(flags, ((T + 15) / 16 + 1) * 16);
+    ENSURE(small_list, (T + 1) * 4);
+    long long want_tiles = (long long)W * H / 32;
+    if (want_tiles > ctx->max_tiles) ctx->max_tiles = (int)(want_tiles < (1ll << 30) ? want_tiles : (1 << 30));
+    ENSURE(large, (size_t)ctx->max_large * sizeof(TriSetup));
+    ENSURE(tiles, (size_t)ctx->max_tiles * sizeof(int2));
+    ENSURE(dstat, sizeof(fa_dstat));
+    ENSURE(vp_dev, 16 * sizeof(double));
+    return FA_OK;
+}
+
+static int ensure_charts(fa_ctx* ctx) {
+    int64_t T = ctx->T, V = ctx->V;
+    ENSURE(vis_list, (T + 1) * 4);
+    ENSURE(label, (T + 1) * 4);
+    ENSURE(vmin, (V + 1) * 4);
+    ENSURE(v2c, (V + 1) * 4);
+    ENSURE(cidx, (T + 1) * 4);
+    ENSURE(aux, (T + 1) * 4);
+    ENSURE(roots, (T + 1) * 4);
+    ENSURE(ndc_keys, (T + 1) * 32);
+    ENSURE(survived, (T + 1) * 4);
+    ENSURE(ndc, (T + 1) * 32);
+    ENSURE(px, (T + 1) * 8);
+    ENSURE(target, (T + 1) * 16);
+    ENSURE(blocks, (size_t)fa_compact_blocks(T + 1) * 4 + 64);
+    return FA_OK;
+}
+
+// pack scratch for n_cap boxes, batch candidates, n_scales records
+static int ensure_pack(fa_ctx* ctx, int64_t n_cap, int64_t n_scales, int64_t omega, int batch) {
+    int64_t n = n_cap > 0 ? n_cap : 1;
+    if (n < ctx->pack_cap) n = ctx->pack_cap;  // never shrink the capacity
+    ctx->pack_cap = n;
+    ENSURE(in_tw, n * 8);
+    ENSURE(in_th, n * 8);
+    ENSURE(in_cid, n * 8);
+    ENSURE(ow, n * 8);
+    ENSURE(oh, n * 8);
+    ENSURE(orot, n + 16);
+    ENSURE(oidx, n * 4);  // perm
+    ENSURE(pinv, n * 4);
+    ENSURE(sortk, 2 * n * 8);
+    ENSURE(sortv, 2 * n * 4);
+    ENSURE(cand, (size_t)n_scales * FA_CAND_REC * 8);
+    ENSURE(cand_p, (size_t)batch * n * 8);
+    ENSURE(cand_w, (size_t)batch * n * 4);
+    ENSURE(cand_h, (size_t)batch * n * 4);
+    ENSURE(cand_y, (size_t)batch * n * 4);
+    ENSURE(rowstart, (size_t)batch * n * 4);
+    ENSURE(placements, n * 64);
+    if (!fa_front_in_smem(omega)) ENSURE(okey, (size_t)batch * (omega + 1) * 4);
+    return FA_OK;
+}
+
+static fa_pack_bufs pack_bufs(fa_ctx* ctx, const long long* tw, const long long* th, const long long* cid,
+                              long long* placements, unsigned char* accept_out) {
+    fa_pack_bufs b;
+    b.tw = tw;
+    b.th = th;
+    b.chart_id = cid;
+    b.ow = P<long long>(ctx->ow);
+    b.oh = P<long long>(ctx->oh);
+    b.rot = P<unsigned char>(ctx->orot);
+    b.perm = P<int>(ctx->oidx);
+    b.pinv = P<int>(ctx->pinv);
+    b.sortk = P<unsigned long long>(ctx->sortk);
+    b.sortv = P<int>(ctx->sortv);
+    b.cand = P<long long>(ctx->cand);
+    b.cand_p = P<long long>(ctx->cand_p);
+    b.cand_w = P<int>(ctx->cand_w);
+    b.cand_h = P<int>(ctx->cand_h);
+    b.cand_y = P<int>(ctx->cand_y);
+    b.rowstart = P<int>(ctx->rowstart);
+    b.placements = placements;
+    b.accept_out = accept_out;
+    b.gfront = P<int>(ctx->okey);
+    return b;
+}
+
+static int check_omega(int64_t omega) {
+    if (omega < 1 || (omega & (omega - 1)) != 0) return set_err(FA_VALUE_ERROR, "omega must be a power of two >= 1");
+    if (omega > (1ll << 30)) return set_err(FA_VALUE_ERROR, "omega above 2^30 is not supported");
+    return FA_OK;
+}
+
+static int status_from_flags(const fa_dstat* h) {
+    if (h->flags & FA_DFLAG_POLY_OVERFLOW) return set_err(FA_INTERNAL_ERROR, "clipped polygon exceeded capacity");
+    if (h->flags & FA_DFLAG_QUEUE_OVERFLOW) return set_err(FA_INTERNAL_ERROR, "work queue overflow");
+    if (h->flags & FA_DFLAG_KEY_RANGE) return set_err(FA_VALUE_ERROR, "box key range exceeds 64 bits");
+    if (h->flags & FA_DFLAG_DUPLICATE_MIN_TRI) return set_err(FA_VALUE_ERROR, "duplicate min_tri in pack request");
+    if (h->flags & FA_DFLAG_HEIGHT_OVERFLOW) return set_err(FA_HEIGHT_OVERFLOW, "box height exceeds capacity");
+    return FA_OK;
+}
+
+static void grow_queues(fa_ctx* ctx, const fa_dstat* h) {
+    if (h->n_large > ctx->max_large) ctx->max_large = h->n_large + h->n_large / 2;
+    if (h->n_tiles > ctx->max_tiles) ctx->max_tiles = h->n_tiles + h->n_tiles / 2;
+}
+
+static int read_stat(fa_ctx* ctx, cudaStream_t s) {
+    CK(cudaMemcpyAsync(ctx->hstat, ctx->dstat.p, sizeof(fa_dstat), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return FA_OK;
+}
+
+static int upload_vp(fa_ctx* ctx, const double* vp_host, cudaStream_t s) {
+    // pageable source: the copy is staged before the call returns, so the
+    // caller may reuse its matrix immediately
+    CK(cudaMemcpyAsync(ctx->vp_dev.p, vp_host, 16 * sizeof(double), cudaMemcpyHostToDevice, s));
+    return FA_OK;
+}
+
+// depth pass (shared by fa_depth_prepass and the frame)
+static int launch_depth(fa_ctx* ctx, int W, int H, int cull, unsigned char* flags_out, cudaStream_t s, int& nl) {
+    int T = (int)ctx->T, V = (int)ctx->V;
+    fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), P<int>(ctx->vmin),
+                         P<unsigned long long>(ctx->depth_keys), (long long)W * H, flags_out, T, s);
+    fa_launch_raster_setup(true, P<double4>(ctx->clip), ctx->tris, T, W, H, cull,
+                           P<unsigned long long>(ctx->depth_keys), P<int>(ctx->small_list), P<TriSetup>(ctx->large),
+                           ctx->max_large, P<int2>(ctx->tiles), ctx->max_tiles, P<fa_dstat>(ctx->dstat), s);
+    fa_launch_raster_depth_tiles(P<TriSetup>(ctx->large), P<int2>(ctx->tiles), ctx->max_tiles, W,
+                                 P<unsigned long long>(ctx->depth_keys), P<fa_dstat>(ctx->dstat), s);
+    nl += 3;
+    return FA_OK;
+}
+
+extern "C" {
+
+int fa_project(fa_ctx* ctx, const double* vp_host, double* clip_out, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || !vp_host || (!clip_out && ctx->V)) return set_err(FA_VALUE_ERROR, "bad arguments");
+    CK(cudaSetDevice(ctx->device));
+    ENSURE(vp_dev, 16 * sizeof(double));
+    int r = upload_vp(ctx, vp_host, s);
+    if (r) return r;
+    fa_launch_frame_init(ctx->pos, (int)ctx->V, P<double>(ctx->vp_dev), (double4*)clip_out, nullptr, nullptr, 0,
+                         nullptr, 0, s);
+    CKL();
+    return FA_OK;
+}
+
+int fa_depth_prepass(fa_ctx* ctx, const double* vp_host, int width, int height, int backface_cull, double* depth_out,
+                     void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || !vp_host) return set_err(FA_VALUE_ERROR, "bad arguments");
+    if (width < 1 || height < 1) return set_err(FA_VALUE_ERROR, "resolution must be at least 1x1");
+    CK(cudaSetDevice(ctx->device));
+    for (int attempt = 0; attempt < 4; attempt++) {
+        int r = ensure_raster(ctx, width, height, true);
+        if (!r) r = ensure_charts(ctx);
+        if (r) return r;
+        CK(cudaMemsetAsync(ctx->dstat.p, 0, sizeof(fa_dstat), s));
+        r = upload_vp(ctx, vp_host, s);
+        if (r) return r;
+        int nl = 0;
+        launch_depth(ctx, width, height, backface_cull, nullptr, s, nl);
+        fa_launch_decode_depth(P<unsigned long long>(ctx->depth_keys), depth_out, (long long)width * height, s);
+        CKL();
+        r = read_stat(ctx, s);
+        if (r) return r;
+        if (ctx->hstat->flags & FA_DFLAG_QUEUE_OVERFLOW) {
+            grow_queues(ctx, ctx->hstat);
+            continue;
+        }
+        return status_from_flags(ctx->hstat);
+    }
+    return set_err(FA_INTERNAL_ERROR, "raster queue kept overflowing");
+}
+
+int fa_mark_visible(fa_ctx* ctx, const double* vp_host, const double* depth, int width, int height,
+                    int backface_cull, uint8_t* flags_out, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || !vp_host || !depth) return set_err(FA_VALUE_ERROR, "bad arguments");
+    if (width < 1 || height < 1) return set_err(FA_VALUE_ERROR, "resolution must be at least 1x1");
+    CK(cudaSetDevice(ctx->device));
+    int T = (int)ctx->T, V = (int)ctx->V;
+    for (int attempt = 0; attempt < 4; attempt++) {
+        int r = ensure_raster(ctx, width, height, true);
+        if (!r) r = ensure_charts(ctx);
+        if (r) return r;
+        CK(cudaMemsetAsync(ctx->dstat.p, 0, sizeof(fa_dstat), s));
+        r = upload_vp(ctx, vp_host, s);
+        if (r) return r;
+        fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), nullptr, nullptr, 0,
+                             P<unsigned char>(ctx->flags), T, s);
+        fa_launch_encode_depth(depth, P<unsigned long long>(ctx->depth_keys), (long long)width * height, s);
+        fa_launch_raster_setup(false, P<double4>(ctx->clip), ctx->tris, T, width, height, backface_cull, nullptr,
+                               P<int>(ctx->small_list), P<TriSetup>(ctx->large), ctx->max_large, P<int2>(ctx->tiles),
+                               ctx->max_tiles, P<fa_dstat>(ctx->dstat), s);
+        fa_launch_raster_vis(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->small_list), P<TriSetup>(ctx->large),
+                             P<int2>(ctx->tiles), ctx->max_tiles, T, width, height, backface_cull,
+                             P<unsigned long long>(ctx->depth_keys), P<unsigned char>(ctx->flags),
+                             P<fa_dstat>(ctx->dstat), s);
+        CKL();
+        r = read_stat(ctx, s);
+        if (r) return r;
+        if (ctx->hstat->flags & FA_DFLAG_QUEUE_OVERFLOW) {
+            grow_queues(ctx, ctx->hstat);
+            continue;
+        }
+        if (T) CK(cudaMemcpyAsync(flags_out, ctx->flags.p, T, cudaMemcpyDeviceToDevice, s));
+        return status_from_flags(ctx->hstat);
+    }
+    return set_err(FA_INTERNAL_ERROR, "raster queue kept overflowing");
+}
+
+int fa_connected_charts(fa_ctx* ctx, const int32_t* adjacency, const uint8_t* flags, int32_t* labels_out,
+                        void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || (ctx->T && (!adjacency || !flags || !labels_out))) return set_err(FA_VALUE_ERROR, "bad arguments");
+    CK(cudaSetDevice(ctx->device));
+    int T = (int)ctx->T;
+    int r = ensure_charts(ctx);
+    if (r) return r;
+    ENSURE(dstat, sizeof(fa_dstat));
+    CK(cudaMemsetAsync(ctx->dstat.p, 0, sizeof(fa_dstat), s));
+    fa_dstat* st = P<fa_dstat>(ctx->dstat);
+    // flags may not be 16-byte padded: stage a padded copy
+    ENSURE(flags, ((T + 15) / 16 + 1) * 16);
+    if (T) CK(cudaMemcpyAsync(ctx->flags.p, flags, T, cudaMemcpyDeviceToDevice, s));
+    fa_launch_compact_visible(P<unsigned char>(ctx->flags), T, P<int>(ctx->blocks), P<int>(ctx->vis_list), labels_out,
+                              st, s);
+    fa_launch_uf_edges(adjacency, P<unsigned char>(ctx->flags), P<int>(ctx->vis_list), labels_out, T, st, s);
+    fa_launch_uf_compress(P<int>(ctx->vis_list), labels_out, T, st, s);
+    CKL();
+    return FA_OK;
+}
+
+int fa_merge_shared_vertices(fa_ctx* ctx, const int32_t* labels_in, int32_t* labels_out, int32_t* v2c_out,
+                             void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || (ctx->T && (!labels_in || !labels_out))) return set_err(FA_VALUE_ERROR, "bad arguments");
+    CK(cudaSetDevice(ctx->device));
+    int T = (int)ctx->T, V = (int)ctx->V;
+    int r = ensure_charts(ctx);
+    if (r) return r;
+    ENSURE(dstat, sizeof(fa_dstat));
+    ENSURE(flags, ((T + 15) / 16 + 1) * 16);
+    CK(cudaMemsetAsync(ctx->dstat.p, 0, sizeof(fa_dstat), s));
+    fa_dstat* st = P<fa_dstat>(ctx->dstat);
+    unsigned char* fl = P<unsigned char>(ctx->flags);
+    fa_launch_flags_from_labels(labels_in, fl, T, s);
+    fa_launch_compact_visible(fl, T, P<int>(ctx->blocks), P<int>(ctx->vis_list), labels_out, st, s);
+    // general chart sets: every node starts as its own root (charts.py:371-374)
+    fa_launch_uf_labels(labels_in, P<int>(ctx->vis_list), labels_out, T, st, s);
+    fa_launch_fill(P<int>(ctx->vmin), V, 0x7fffffff, s);
+    fa_launch_uf_vertex(ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->vmin), labels_out, T, st, s);
+    fa_launch_uf_compress(P<int>(ctx->vis_list), labels_out, T, st, s);
+    fa_launch_canonicalize(P<int>(ctx->vis_list), labels_out, P<int>(ctx->aux), T, st, s);
+    fa_launch_canon_apply(fl, labels_out, P<int>(ctx->aux), T, s);
+    if (v2c_out) fa_launch_v2c(P<int>(ctx->vmin), labels_out, v2c_out, V, s);
+    CKL();
+    return FA_OK;
+}
+
+int fa_chart_boxes(fa_ctx* ctx, const double* vp_host, const int32_t* labels, int width, int height, double prescale,
+                   int32_t* roots_out, double* ndc_out, int32_t* px_out, int64_t* target_out, int64_t* n_charts_host,
+                   void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || !vp_host || (ctx->T && !labels)) return set_err(FA_VALUE_ERROR, "bad arguments");
+    if (width < 1 || height < 1) return set_err(FA_VALUE_ERROR, "screen dimensions must be >= 1");
+    CK(cudaSetDevice(ctx->device));
+    int T = (int)ctx->T, V = (int)ctx->V;
+    int r = ensure_charts(ctx);
+    if (!r) r = ensure_raster(ctx, 1, 1, false);
+    if (!r) r = ensure_pack(ctx, T, 1, 1, 1);
+    if (r) return r;
+    CK(cudaMemsetAsync(ctx->dstat.p, 0, sizeof(fa_dstat), s));
+    r = upload_vp(ctx, vp_host, s);
+    if (r) return r;
+    fa_dstat* st = P<fa_dstat>(ctx->dstat);
+    unsigned char* fl = P<unsigned char>(ctx->flags);
+    fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), nullptr, nullptr, 0, nullptr, 0,
+                         s);
+    fa_launch_flags_from_labels(labels, fl, T, s);
+    fa_launch_compact_visible(fl, T, P<int>(ctx->blocks), P<int>(ctx->vis_list), P<int>(ctx->aux), st, s);
+    fa_launch_compact_roots(P<int>(ctx->vis_list), labels, T, P<int>(ctx->blocks), P<int>(ctx->roots),
+                            P<int>(ctx->cidx), P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), st, s);
+    fa_launch_chart_bounds(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->vis_list), labels, P<int>(ctx->cidx), T,
+                           P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), st, s);
+    fa_launch_box_dims(P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), P<int>(ctx->roots), T, width,
+                       height, prescale, P<double>(ctx->ndc), P<int>(ctx->px), P<long long>(ctx->target),
+                       P<long long>(ctx->in_tw), P<long long>(ctx->in_th), P<long long>(ctx->in_cid),
+                       (int)ctx->pack_cap, st, s);
+    CKL();
+    r = read_stat(ctx, s);
+    if (r) return r;
+    int C = ctx->hstat->n_charts;
+    if (ctx->hstat->flags & FA_DFLAG_DEGENERATE_CHART)
+        return set_err(FA_DEGENERATE_CHART, "a chart has no triangle surviving clipping");
+    if (C) {
+        CK(cudaMemcpyAsync(roots_out, ctx->roots.p, (size_t)C * 4, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(ndc_out, ctx->ndc.p, (size_t)C * 32, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(px_out, ctx->px.p, (size_t)C * 8, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(target_out, ctx->target.p, (size_t)C * 16, cudaMemcpyDeviceToDevice, s));
+    }
+    if (n_charts_host) *n_charts_host = C;
+    CK(cudaStreamSynchronize(s));
+    return FA_OK;
+}
+
+int fa_orient_order(fa_ctx* ctx, const int64_t* target_w, const int64_t* target_h, const int64_t* min_tri, int64_t n,
+                    int64_t max_h, int32_t* perm_out, int64_t* ow_out, int64_t* oh_out, uint8_t* rot_out,
+                    void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || n < 0 || n >= (1ll << 30)) return set_err(FA_VALUE_ERROR, "bad arguments");
+    if (n == 0) return FA_OK;
+    CK(cudaSetDevice(ctx->device));
+    int r = ensure_pack(ctx, n, 1, 1, 1);
+    if (r) return r;
+    ENSURE(dstat, sizeof(fa_dstat));
+    CK(cudaMemsetAsync(ctx->dstat.p, 0, sizeof(fa_dstat), s));
+    fa_launch_orient_sort_mt((const long long*)target_w, (const long long*)target_h, (const long long*)min_tri, (int)n,
+                             max_h, (long long*)ow_out, (long long*)oh_out, rot_out, perm_out, P<int>(ctx->pinv),
+                             P<unsigned long long>(ctx->sortk), P<int>(ctx->sortv), 0, P<fa_dstat>(ctx->dstat), s);
+    CKL();
+    r = read_stat(ctx, s);
+    if (r) return r;
+    return status_from_flags(ctx->hstat);
+}
+
+int fa_fold(fa_ctx* ctx, const int64_t* widths, int64_t n, int64_t omega, int64_t* rows_out, int64_t* x_out,
+            int64_t* m_host, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || n <= 0 || n >= (1ll << 31)) return set_err(FA_VALUE_ERROR, "fold requires a non-empty width sequence");
+    int r = check_omega(omega);
+    if (r) return r;
+    CK(cudaSetDevice(ctx->device));
+    ENSURE(aux, 64);
+    fa_launch_fold((const long long*)widths, (int)n, omega, (long long*)rows_out, (long long*)x_out,
+                   P<long long>(ctx->aux), s);
+    CKL();
+    long long m = 0;
+    CK(cudaMemcpyAsync(&m, ctx->aux.p, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (m < 0) return set_err(FA_VALUE_ERROR, "widths must be in [1, omega]");
+    if (m_host) *m_host = m;
+    return FA_OK;
+}
+
+int fa_push_up(fa_ctx* ctx, const int64_t* rows, const int64_t* x, const int64_t* widths, const int64_t* heights,
+               int64_t n, int64_t omega, int64_t* y_out, int64_t* used_host, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || n < 0 || n >= (1ll << 31)) return set_err(FA_VALUE_ERROR, "bad arguments");
+    int r = check_omega(omega);
+    if (r) return r;
+    CK(cudaSetDevice(ctx->device));
+    if (n == 0) {
+        if (used_host) *used_host = 0;
+        return FA_OK;
+    }
+    ENSURE(rowstart, (size_t)n * 4 + 64);
+    ENSURE(aux, 64);
+    int* gfront = nullptr;
+    if (!fa_front_in_smem(omega)) {
+        ENSURE(okey, (size_t)(omega + 1) * 4);
+        gfront = P<int>(ctx->okey);
+    }
+    fa_launch_push_up_impl((const long long*)rows, (const long long*)x, (const long long*)widths,
+                           (const long long*)heights, (int)n, omega, P<int>(ctx->rowstart), (long long*)y_out,
+                           P<long long>(ctx->aux), gfront, s);
+    CKL();
+    long long used = 0;
+    CK(cudaMemcpyAsync(&used, ctx->aux.p, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (used_host) *used_host = used;
+    return FA_OK;
+}
+
+int fa_pack_at_scale(fa_ctx* ctx, const int64_t* ow, const int64_t* oh, int64_t n, int64_t num, int64_t den,
+                     int64_t omega, int64_t min_dim, int64_t padding, int64_t* xywh_out, int64_t* scale_host,
+                     int* accepted_host, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    int r = check_omega(omega);
+    if (r) return r;
+    if (!ctx || n < 0 || n >= (1ll << 30)) return set_err(FA_VALUE_ERROR, "bad arguments");
+    if (!(num > 0 && den > 0 && num <= den)) return set_err(FA_VALUE_ERROR, "scale must be in (0, 1]");
+    if (min_dim < 1 || padding < 0 || min_dim > (1 << 28) || padding > (1 << 28))
+        return set_err(FA_VALUE_ERROR, "min_dim must be >= 1 and padding >= 0");
+    CK(cudaSetDevice(ctx->device));
+    if (n == 0) {
+        long long g = num, b = den;
+        while (b) { long long t = g % b; g = b; b = t; }
+        if (scale_host) { scale_host[0] = num / g; scale_host[1] = den / g; }
+        if (accepted_host) *accepted_host = 1;
+        return FA_OK;
+    }
+    r = ensure_pack(ctx, n, 1, omega, 1);
+    if (r) return r;
+    CK(cudaMemsetAsync(ctx->cand.p, 0, FA_CAND_REC * 8, s));
+    fa_launch_pack_at_scale((const long long*)ow, (const long long*)oh, (int)n, num, den, omega, min_dim, padding,
+                            P<long long>(ctx->cand), P<long long>(ctx->cand_p), P<int>(ctx->cand_w),
+                            P<int>(ctx->cand_h), P<int>(ctx->cand_y), P<int>(ctx->rowstart), P<int>(ctx->okey), s);
+    fa_launch_xywh(P<long long>(ctx->cand), P<long long>(ctx->cand_p), P<int>(ctx->cand_w), P<int>(ctx->cand_h),
+                   P<int>(ctx->cand_y), (int)n, omega, (long long*)xywh_out, s);
+    CKL();
+    long long rec[FA_CAND_REC];
+    CK(cudaMemcpyAsync(rec, ctx->cand.p, sizeof(rec), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (accepted_host) *accepted_host = (int)rec[0];
+    if (scale_host && rec[0]) {
+        scale_host[0] = rec[1];
+        scale_host[1] = rec[2];
+    }
+    return FA_OK;
+}
+
+int fa_pack(fa_ctx* ctx, const int64_t* target_w, const int64_t* target_h, const int64_t* chart_id,
+            const int64_t* min_tri, int64_t n, int64_t omega, int64_t n_scales, int64_t min_dim, int64_t padding,
+            int64_t* placements_out, int64_t* scale_host, uint8_t* accept_out, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    int r = check_omega(omega);
+    if (r) return r;
+    if (!ctx) return set_err(FA_VALUE_ERROR, "null context");
+    if (!(1 <= n_scales && n_scales <= (1 << 20))) return set_err(FA_VALUE_ERROR, "n_scales must be in [1, 2^20]");
+    if (min_dim < 1 || padding < 0 || min_dim > (1 << 28) || padding > (1 << 28))
+        return set_err(FA_VALUE_ERROR, "min_dim must be >= 1 and padding >= 0");
+    if (n < 0 || n >= (1ll << 30)) return set_err(FA_VALUE_ERROR, "bad box count");
+    if (n == 0) {
+        if (scale_host) { scale_host[0] = 1; scale_host[1] = 1; }
+        return FA_OK;
+    }
+    CK(cudaSetDevice(ctx->device));
+    int batch = (int)(n_scales < ctx->pack_batch ? n_scales : ctx->pack_batch);
+    r = ensure_pack(ctx, n, n_scales, omega, batch);
+    if (r) return r;
+    ENSURE(dstat, sizeof(fa_dstat));
+    CK(cudaMemsetAsync(ctx->dstat.p, 0, sizeof(fa_dstat), s));
+    CK(cudaMemsetAsync(ctx->cand.p, 0, (size_t)n_scales * FA_CAND_REC * 8, s));
+    fa_dstat* st = P<fa_dstat>(ctx->dstat);
+    fa_launch_orient_sort_mt((const long long*)target_w, (const long long*)target_h, (const long long*)min_tri, (int)n,
+                             FA_MAX_BOX_DIM, P<long long>(ctx->ow), P<long long>(ctx->oh), P<unsigned char>(ctx->orot),
+                             P<int>(ctx->oidx), P<int>(ctx->pinv), P<unsigned long long>(ctx->sortk),
+                             P<int>(ctx->sortv), 1, st, s);
+    fa_pack_bufs b = pack_bufs(ctx, (const long long*)target_w, (const long long*)target_h,
+                               (const long long*)chart_id, (long long*)placements_out, accept_out);
+    fa_launch_pack(b, (int)n, nullptr, omega, n_scales, min_dim, padding, batch, st, s);
+    CKL();
+    r = read_stat(ctx, s);
+    if (r) return r;
+    r = status_from_flags(ctx->hstat);
+    if (r) return r;
+    if (ctx->hstat->flags & FA_DFLAG_PACK_FAILURE) return set_err(FA_PACK_FAILURE, "every candidate scale was rejected");
+    if (scale_host) {
+        scale_host[0] = ctx->hstat->scale_num;
+        scale_host[1] = ctx->hstat->scale_den;
+    }
+    return FA_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// whole frame
+// ---------------------------------------------------------------------------
+static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s, int& nl) {
+    int T = (int)ctx->T, V = (int)ctx->V, W = p->width, H = p->height;
+    fa_dstat* st = P<fa_dstat>(ctx->dstat);
+    int64_t n_cap = ctx->pack_cap;
+    int batch = (int)(p->n_scales < ctx->pack_batch ? p->n_scales : ctx->pack_batch);
+    CK(cudaMemsetAsync(ctx->dstat.p, 0, sizeof(fa_dstat), s));
+    CK(cudaMemsetAsync(ctx->cand.p, 0, (size_t)p->n_scales * FA_CAND_REC * 8, s));
+    nl = 0;
+    unsigned char* flags = P<unsigned char>(ctx->flags);
+    launch_depth(ctx, W, H, p->backface_cull, flags, s, nl);
+    fa_launch_raster_vis(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->small_list), P<TriSetup>(ctx->large),
+                         P<int2>(ctx->tiles), ctx->max_tiles, T, W, H, p->backface_cull,
+                         P<unsigned long long>(ctx->depth_keys), flags, st, s);
+    nl += 2;
+    fa_launch_compact_visible(flags, T, P<int>(ctx->blocks), P<int>(ctx->vis_list), P<int>(ctx->label), st, s);
+    nl += 2;
+    fa_launch_uf_vertex(ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->vmin), P<int>(ctx->label), T, st, s);
+    fa_launch_uf_compress(P<int>(ctx->vis_list), P<int>(ctx->label), T, st, s);
+    fa_launch_v2c(P<int>(ctx->vmin), P<int>(ctx->label), P<int>(ctx->v2c), V, s);
+    nl += 4;
+    fa_launch_compact_roots(P<int>(ctx->vis_list), P<int>(ctx->label), T, P<int>(ctx->blocks), P<int>(ctx->roots),
+                            P<int>(ctx->cidx), P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), st, s);
+    fa_launch_chart_bounds(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->label),
+                           P<int>(ctx->cidx), T, P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), st, s);
+    fa_launch_box_dims(P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), P<int>(ctx->roots), T, W, H,
+                       p->prescale, P<double>(ctx->ndc), P<int>(ctx->px), P<long long>(ctx->target),
+                       P<long long>(ctx->in_tw), P<long long>(ctx->in_th), P<long long>(ctx->in_cid), (int)n_cap,
+                       st, s);
+    nl += 4;
+    fa_pack_bufs b = pack_bufs(ctx, P<long long>(ctx->in_tw), P<long long>(ctx->in_th), P<long long>(ctx->in_cid),
+                               P<long long>(ctx->placements), nullptr);
+    fa_launch_orient_sort(b, (int)n_cap, &st->n_charts, FA_MAX_BOX_DIM, st, s);
+    nl += 1;
+    nl += fa_launch_pack(b, (int)n_cap, &st->n_charts, p->omega, p->n_scales, p->min_dim, p->padding, batch, st, s);
+    fa_launch_uv(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->label), P<int>(ctx->cidx),
+                 P<int>(ctx->pinv), P<double>(ctx->ndc), P<int>(ctx->px), P<long long>(ctx->placements), T, W, H,
+                 p->padding, p->uv_f64 != 0, ctx->uv.p, st, s);
+    nl += 1;
+    if (p->want_depth) {
+        fa_launch_decode_depth(P<unsigned long long>(ctx->depth_keys), P<double>(ctx->depth_f64), (long long)W * H, s);
+        nl += 1;
+    }
+    CK(cudaMemcpyAsync(ctx->hstat, ctx->dstat.p, sizeof(fa_dstat), cudaMemcpyDeviceToHost, s));
+    CKL();
+    return FA_OK;
+}
+
+static int frame_prepare(fa_ctx* ctx, const fa_frame_params* p) {
+    if (p->width < 1 || p->height < 1) return set_err(FA_VALUE_ERROR, "screen must be at least 1x1");
+    int r = check_omega(p->omega);
+    if (r) return r;
+    if (!(1 <= p->n_scales && p->n_scales <= (1 << 20))) return set_err(FA_VALUE_ERROR, "n_scales must be in [1, 2^20]");
+    if (p->min_dim < 1 || p->padding < 0 || p->min_dim > (1 << 28) || p->padding > (1 << 28))
+        return set_err(FA_VALUE_ERROR, "min_dim must be >= 1 and padding >= 0");
+    if (!(p->prescale > 0)) return set_err(FA_VALUE_ERROR, "prescale must be positive");
+    if (ctx->T > 0 && (!ctx->pos || !ctx->tris)) return set_err(FA_VALUE_ERROR, "no mesh bound");
+    r = ensure_raster(ctx, p->width, p->height, true);
+    if (!r) r = ensure_charts(ctx);
+    if (r) return r;
+    int64_t cap = ctx->pack_cap;
+    if (cap < 16384) cap = 16384;
+    if (cap > ctx->T + 1) cap = ctx->T + 1;
+    int batch = (int)(p->n_scales < ctx->pack_batch ? p->n_scales : ctx->pack_batch);
+    r = ensure_pack(ctx, cap, p->n_scales, p->omega, batch);
+    if (r) return r;
+    ENSURE(uv, (size_t)(ctx->T + 1) * 6 * (p->uv_f64 ? 8 : 4));
+    if (p->want_depth) ENSURE(depth_f64, (size_t)p->width * p->height * 8);
+    return FA_OK;
+}
+
+extern "C" {
+
+int fa_frame_launch(fa_ctx* ctx, const double* vp_host, const fa_frame_params* p, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || !vp_host || !p) return set_err(FA_VALUE_ERROR, "bad arguments");
+    CK(cudaSetDevice(ctx->device));
+    int r = frame_prepare(ctx, p);
+    if (r) return r;
+    ctx->last_params = *p;
+    r = upload_vp(ctx, vp_host, s);
+    if (r) return r;
+    if (!p->use_graph) {
+        int nl = 0;
+        r = frame_sequence(ctx, p, s, nl);
+        ctx->last_launches = nl;
+        return r;
+    }
+    fa_graph_key key;
+    key.width = p->width;
+    key.height = p->height;
+    key.cull = p->backface_cull;
+    key.uv_f64 = p->uv_f64;
+    key.want_depth = p->want_depth;
+    key.omega = p->omega;
+    key.n_scales = p->n_scales;
+    key.min_dim = p->min_dim;
+    key.padding = p->padding;
+    key.prescale = p->prescale;
+    key.T = ctx->T;
+    key.V = ctx->V;
+    key.pos = ctx->pos;
+    key.tris = ctx->tris;
+    key.gen = ctx->gen;
+    if (!ctx->graph_exec || !(key == ctx->graph_key)) {
+        if (ctx->graph_exec) {
+            cudaGraphExecDestroy(ctx->graph_exec);
+            ctx->graph_exec = nullptr;
+        }
+        cudaStream_t cap;
+        CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+        CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+        int nl = 0;
+        int rr = frame_sequence(ctx, p, cap, nl);
+        cudaGraph_t g;
+        cudaError_t e = cudaStreamEndCapture(cap, &g);
+        cudaStreamDestroy(cap);
+        if (rr) return rr;
+        if (e != cudaSuccess) return set_err(FA_CUDA_ERROR, "graph capture: %s", cudaGetErrorString(e));
+        e = cudaGraphInstantiate(&ctx->graph_exec, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return set_err(FA_CUDA_ERROR, "graph instantiate: %s", cudaGetErrorString(e));
+        ctx->graph_key = key;
+        ctx->last_launches = nl;
+    }
+    CK(cudaGraphLaunch(ctx->graph_exec, s));
+    return FA_OK;
+}
+
+int fa_frame_finish(fa_ctx* ctx, fa_frame_result* out, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || !out) return set_err(FA_VALUE_ERROR, "bad arguments");
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamSynchronize(s));
+    const fa_dstat* h = ctx->hstat;
+    memset(out, 0, sizeof(*out));
+    out->n_visible = h->n_vis;
+    out->n_charts = h->n_charts;
+    out->scale_num = h->scale_num;
+    out->scale_den = h->scale_den;
+    out->screen_fragments = h->screen_fragments;
+    out->texels_allocated = h->texels_allocated;
+    out->depth = ctx->last_params.want_depth ? P<double>(ctx->depth_f64) : nullptr;
+    out->flags = P<uint8_t>(ctx->flags);
+    out->visible = P<int32_t>(ctx->vis_list);
+    out->chart_of_triangle = P<int32_t>(ctx->label);
+    out->vertex_to_chart = P<int32_t>(ctx->v2c);
+    out->roots = P<int32_t>(ctx->roots);
+    out->ndc = P<double>(ctx->ndc);
+    out->px = P<int32_t>(ctx->px);
+    out->target = P<int64_t>(ctx->target);
+    out->placements = P<int64_t>(ctx->placements);
+    out->uv = ctx->uv.p;
+    int64_t n_cap = ctx->pack_cap;
+    ctx->needs_rerun = false;
+    if (h->flags & FA_DFLAG_QUEUE_OVERFLOW || h->n_charts > n_cap) {
+        grow_queues(ctx, h);
+        if (h->n_charts > n_cap) {
+            int batch = (int)(ctx->last_params.n_scales < ctx->pack_batch ? ctx->last_params.n_scales : ctx->pack_batch);
+            int r = ensure_pack(ctx, (int64_t)h->n_charts * 2, ctx->last_params.n_scales, ctx->last_params.omega, batch);
+            if (r) return r;
+        }
+        out->status = FA_INTERNAL_ERROR;
+        ctx->needs_rerun = true;
+        return set_err(FA_INTERNAL_ERROR, "work queue overflow (capacity grown; rerun the frame)");
+    }
+    int r = status_from_flags(h);
+    if (r) {
+        out->status = r;
+        return r;
+    }
+    if (h->n_vis == 0) {
+        out->status = FA_NOTHING_VISIBLE;
+        return set_err(FA_NOTHING_VISIBLE, "no triangle covers a depth-passing sample");
+    }
+    if (h->flags & FA_DFLAG_DEGENERATE_CHART) {
+        out->status = FA_DEGENERATE_CHART;
+        return set_err(FA_DEGENERATE_CHART, "a visible chart has no surviving triangle");
+    }
+    if (h->flags & FA_DFLAG_PACK_FAILURE) {
+        out->status = FA_PACK_FAILURE;
+        return set_err(FA_PACK_FAILURE, "every candidate scale was rejected");
+    }
+    out->status = FA_OK;
+    return FA_OK;
+}
+
+int fa_frame(fa_ctx* ctx, const double* vp_host, const fa_frame_params* p, fa_frame_result* out, void* stream) {
+    for (int attempt = 0; attempt < 4; attempt++) {
+        int r = fa_frame_launch(ctx, vp_host, p, stream);
+        if (r) return r;
+        r = fa_frame_finish(ctx, out, stream);
+        if (r == FA_INTERNAL_ERROR && ctx->needs_rerun) continue;
+        return r;
+    }
+    return set_err(FA_INTERNAL_ERROR, "frame kept overflowing its work queues");
+}
+
+int fa_last_launch_count(fa_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// batched geometry helpers backing the scalar reference API
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int fa_blinn_clamped_ndc(fa_ctx* ctx, const double* points4, int64_t n, double* out2, void* stream) {
+    if (!ctx || n < 0 || n >= (1ll << 31)) return set_err(FA_VALUE_ERROR, "bad arguments");
+    if (n == 0) return FA_OK;
+    CK(cudaSetDevice(ctx->device));
+    fa_launch_blinn_points(points4, (int)n, out2, (cudaStream_t)stream);
+    CKL();
+    return FA_OK;
+}
+
+int fa_select_side_plane(fa_ctx* ctx, const double* tris12, int64_t n, int32_t* out, void* stream) {
+    if (!ctx || n < 0 || n >= (1ll << 31)) return set_err(FA_VALUE_ERROR, "bad arguments");
+    if (n == 0) return FA_OK;
+    CK(cudaSetDevice(ctx->device));
+    fa_launch_select_side_plane(tris12, (int)n, out, (cudaStream_t)stream);
+    CKL();
+    return FA_OK;
+}
+
+int fa_chart_bbox(fa_ctx* ctx, const double* vp_host, const double* tris_xyz, int64_t n, double* box_host,
+                  void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || !vp_host || n < 0 || n >= (1ll << 31)) return set_err(FA_VALUE_ERROR, "bad arguments");
+    if (n == 0) return set_err(FA_DEGENERATE_CHART, "chart has no triangles");
+    CK(cudaSetDevice(ctx->device));
+    ENSURE(vp_dev, 16 * sizeof(double));
+    ENSURE(aux, 128);
+    int r = upload_vp(ctx, vp_host, s);
+    if (r) return r;
+    unsigned long long* keys = P<unsigned long long>(ctx->aux);
+    int* surv = reinterpret_cast<int*>(keys + 4);
+    double* box = reinterpret_cast<double*>(keys + 6);
+    fa_launch_chart_bbox_world(tris_xyz, (int)n, P<double>(ctx->vp_dev), keys, surv, box, s);
+    CKL();
+    double hb[4];
+    int hs = 0;
+    CK(cudaMemcpyAsync(hb, box, 32, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&hs, surv, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (!hs) return set_err(FA_DEGENERATE_CHART, "no triangle survives clipping");
+    memcpy(box_host, hb, sizeof(hb));
+    return FA_OK;
+}
+
+int fa_viewport_box(fa_ctx* ctx, const double* boxes4, int64_t n, int width, int height, int64_t* out2,
+                    void* stream) {
+    if (!ctx || n < 0 || n >= (1ll << 31)) return set_err(FA_VALUE_ERROR, "bad arguments");
+    if (width < 1 || height < 1) return set_err(FA_VALUE_ERROR, "screen dimensions must be >= 1");
+    if (n == 0) return FA_OK;
+    CK(cudaSetDevice(ctx->device));
+    fa_launch_viewport_box(boxes4, (int)n, width, height, (long long*)out2, (cudaStream_t)stream);
+    CKL();
+    return FA_OK;
+}
+
+int fa_orient(fa_ctx* ctx, const int64_t* target_w, const int64_t* target_h, int64_t n, int64_t* ow_out,
+              int64_t* oh_out, uint8_t* rot_out, void* stream) {
+    if (!ctx || n < 0 || n >= (1ll << 31)) return set_err(FA_VALUE_ERROR, "bad arguments");
+    if (n == 0) return FA_OK;
+    CK(cudaSetDevice(ctx->device));
+    fa_launch_orient((const long long*)target_w, (const long long*)target_h, (int)n, (long long*)ow_out,
+                     (long long*)oh_out, rot_out, (cudaStream_t)stream);
+    CKL();
+    return FA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,344 @@
+// fa_charts.cu — visible-list compaction and lock-free union-find
+// chartification on sm_100a.
+//
+// Reference: connected_charts + merge_shared_vertices (charts.py:343-406).
+// The merged charts are the connected components of the visible-triangle /
+// vertex incidence graph (edge adjacency is subsumed because edge neighbours
+// share two vertices).  Per vertex v we keep vmin[v] = the smallest visible
+// triangle touching v (which is exactly the reference's first_chart[v],
+// charts.py:375-380), then union every visible triangle with vmin of its
+// three vertices.  Hooking always puts the larger root under the smaller
+// (atomicCAS), so each component's root is its minimum triangle index —
+// the reference's canonical chart id (charts.py:335-340, 394-402).
+#include "fa_internal.h"
+
+#define CMP_THREADS 256
+#define CMP_ITEMS 16
+#define CMP_TILE (CMP_THREADS * CMP_ITEMS)
+
+int fa_compact_blocks(long long n) { return (int)((n + CMP_TILE - 1) / CMP_TILE) > 0 ? (int)((n + CMP_TILE - 1) / CMP_TILE) : 1; }
+
+__device__ __forceinline__ int byte_sum4(unsigned int v) { return (int)((v * 0x01010101u) >> 24); }
+
+// sum of blocks[0..b-1] computed cooperatively by the block
+__device__ __forceinline__ int block_prefix_of(const int* blocks, int b, int* smem32) {
+    int s = 0;
+    for (int i = threadIdx.x; i < b; i += blockDim.x) s += blocks[i];
+    s = warp_sum(s);
+    if (lane_id() == 0) smem32[threadIdx.x >> 5] = s;
+    __syncthreads();
+    int tot = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); i++) tot += smem32[i];
+    __syncthreads();
+    return tot;
+}
+
+// ---- visible compaction ----------------------------------------------------
+__global__ void __launch_bounds__(CMP_THREADS) k_count_flags(const unsigned char* __restrict__ flags, int T,
+                                                             int* __restrict__ blocks) {
+    __shared__ int sm[32];
+    int base = blockIdx.x * CMP_TILE + threadIdx.x * CMP_ITEMS;
+    int c = 0;
+    if (base + CMP_ITEMS <= T) {
+        uint4 v = *reinterpret_cast<const uint4*>(flags + base);
+        c = byte_sum4(v.x) + byte_sum4(v.y) + byte_sum4(v.z) + byte_sum4(v.w);
+    } else {
+        for (int i = base; i < T; i++) c += flags[i] != 0;
+    }
+    c = warp_sum(c);
+    if (lane_id() == 0) sm[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int s = 0;
+        for (int i = 0; i < CMP_THREADS / 32; i++) s += sm[i];
+        blocks[blockIdx.x] = s;
+    }
+}
+
+__global__ void __launch_bounds__(CMP_THREADS) k_scatter_visible(const unsigned char* __restrict__ flags, int T,
+                                                                 const int* __restrict__ blocks, int nblocks,
+                                                                 int* __restrict__ vis_list, int* __restrict__ label,
+                                                                 fa_dstat* __restrict__ st) {
+    __shared__ int sm[32];
+    int offset = block_prefix_of(blocks, blockIdx.x, sm);
+    int base = blockIdx.x * CMP_TILE + threadIdx.x * CMP_ITEMS;
+    unsigned char f[CMP_ITEMS];
+    if (base + CMP_ITEMS <= T) {
+        uint4 v = *reinterpret_cast<const uint4*>(flags + base);
+        unsigned int w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < CMP_ITEMS; i++) f[i] = (w[i >> 2] >> (8 * (i & 3))) & 0xffu;
+    } else {
+#pragma unroll
+        for (int i = 0; i < CMP_ITEMS; i++) f[i] = (base + i < T) ? flags[base + i] : 0;
+    }
+    int c = 0;
+#pragma unroll
+    for (int i = 0; i < CMP_ITEMS; i++) c += f[i] != 0;
+    int total;
+    int pos = offset + block_exclusive_scan(c, sm, &total);
+#pragma unroll
+    for (int i = 0; i < CMP_ITEMS; i++) {
+        int t = base + i;
+        if (t < T) {
+            if (f[i]) vis_list[pos++] = t;
+            label[t] = f[i] ? t : -1;
+        }
+    }
+    if (blockIdx.x == nblocks - 1 && threadIdx.x == 0) st->n_vis = offset + total;
+}
+
+void fa_launch_compact_visible(const unsigned char* flags, int T, int* blocks, int* vis_list, int* label,
+                               fa_dstat* st, cudaStream_t s) {
+    int nb = fa_compact_blocks(T);
+    k_count_flags<<<nb, CMP_THREADS, 0, s>>>(flags, T, blocks);
+    k_scatter_visible<<<nb, CMP_THREADS, 0, s>>>(flags, T, blocks, nb, vis_list, label, st);
+}
+
+// ---- union-find ---------------------------------------------------------------
+// parent[x] <= x always holds; find with pointer jumping (ECL-CC style)
+__device__ __forceinline__ int uf_find(int* parent, int x) {
+    volatile int* p = parent;
+    int cur = p[x];
+    if (cur != x) {
+        int next, prev = x;
+        while (cur > (next = p[cur])) {
+            p[prev] = next;
+            prev = cur;
+            cur = next;
+        }
+    }
+    return cur;
+}
+
+__device__ __forceinline__ void uf_union(int* parent, int a, int b) {
+    int ra = uf_find(parent, a), rb = uf_find(parent, b);
+    while (ra != rb) {
+        if (ra < rb) { int t = ra; ra = rb; rb = t; }
+        int old = atomicCAS(parent + ra, ra, rb);
+        if (old == ra) break;
+        ra = uf_find(parent, old);
+        rb = uf_find(parent, rb);
+    }
+}
+
+__global__ void k_vmin(const int* __restrict__ tris, const int* __restrict__ vis_list, int* __restrict__ vmin,
+                       const fa_dstat* __restrict__ st) {
+    int n = st->n_vis;
+    int stride = gridDim.x * blockDim.x;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+        int t = vis_list[k];
+#pragma unroll
+        for (int j = 0; j < 3; j++) {
+            int v = __ldg(tris + 3 * t + j);
+            if (*(volatile int*)(vmin + v) > t) atomicMin(vmin + v, t);
+        }
+    }
+}
+
+__global__ void k_hook_vertex(const int* __restrict__ tris, const int* __restrict__ vis_list,
+                              const int* __restrict__ vmin, int* label, const fa_dstat* __restrict__ st) {
+    int n = st->n_vis;
+    int stride = gridDim.x * blockDim.x;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+        int t = vis_list[k];
+#pragma unroll
+        for (int j = 0; j < 3; j++) {
+            int u = vmin[__ldg(tris + 3 * t + j)];
+            if (u != t) uf_union(label, t, u);
+        }
+    }
+}
+
+__global__ void k_hook_edges(const int* __restrict__ adj, const unsigned char* __restrict__ flags,
+                             const int* __restrict__ vis_list, int* label, const fa_dstat* __restrict__ st) {
+    int n = st->n_vis;
+    int stride = gridDim.x * blockDim.x;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+        int t = vis_list[k];
+#pragma unroll
+        for (int e = 0; e < 3; e++) {
+            int nb = __ldg(adj + 3 * t + e);
+            if (nb >= 0 && flags[nb]) uf_union(label, t, nb);
+        }
+    }
+}
+
+__global__ void k_hook_labels(const int* __restrict__ labels_in, const int* __restrict__ vis_list, int* label,
+                              const fa_dstat* __restrict__ st) {
+    int n = st->n_vis;
+    int stride = gridDim.x * blockDim.x;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+        int t = vis_list[k];
+        int r = labels_in[t];
+        if (r != t) uf_union(label, t, r);
+    }
+}
+
+__global__ void k_compress(const int* __restrict__ vis_list, int* label, const fa_dstat* __restrict__ st) {
+    int n = st->n_vis;
+    int stride = gridDim.x * blockDim.x;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+        int t = vis_list[k];
+        label[t] = uf_find(label, t);
+    }
+}
+
+__global__ void k_iota(int* a, int n) {
+    int stride = gridDim.x * blockDim.x;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) a[i] = i;
+}
+
+__global__ void k_fill(int* a, int n, int v) {
+    int stride = gridDim.x * blockDim.x;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) a[i] = v;
+}
+
+// canonical label = minimum VISIBLE member of each union-find root
+// (charts.py:396-402).  tmp must be pre-filled with INT_MAX.
+__global__ void k_canon_min(const int* __restrict__ vis_list, const int* __restrict__ label, int* tmp,
+                            const fa_dstat* __restrict__ st) {
+    int n = st->n_vis;
+    int stride = gridDim.x * blockDim.x;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+        int t = vis_list[k];
+        atomicMin(tmp + label[t], t);
+    }
+}
+
+__global__ void k_canon_apply(const unsigned char* __restrict__ flags, int* label, const int* __restrict__ tmp, int T) {
+    int stride = gridDim.x * blockDim.x;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += stride)
+        label[t] = flags[t] ? tmp[label[t]] : -1;
+}
+
+__global__ void k_v2c(const int* __restrict__ vmin, const int* __restrict__ label, int* __restrict__ v2c, int V) {
+    int stride = gridDim.x * blockDim.x;
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += stride) {
+        int m = vmin[v];
+        v2c[v] = m == 0x7fffffff ? -1 : label[m];
+    }
+}
+
+__global__ void k_flags_from_labels(const int* __restrict__ labels, unsigned char* __restrict__ flags, int T) {
+    int stride = gridDim.x * blockDim.x;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += stride) flags[t] = labels[t] >= 0;
+}
+
+static inline int uf_grid(int T) { return fa_grid(T, 256, FA_NUM_SMS * 8); }
+
+void fa_launch_uf_vertex(const int* tris, const int* vis_list, int* vmin, int* label, int T, const fa_dstat* st,
+                         cudaStream_t s) {
+    k_vmin<<<uf_grid(T), 256, 0, s>>>(tris, vis_list, vmin, st);
+    k_hook_vertex<<<uf_grid(T), 256, 0, s>>>(tris, vis_list, vmin, label, st);
+}
+
+void fa_launch_uf_edges(const int* adjacency, const unsigned char* flags, const int* vis_list, int* label, int T,
+                        const fa_dstat* st, cudaStream_t s) {
+    k_hook_edges<<<uf_grid(T), 256, 0, s>>>(adjacency, flags, vis_list, label, st);
+}
+
+void fa_launch_uf_labels(const int* labels_in, const int* vis_list, int* label, int T, const fa_dstat* st,
+                         cudaStream_t s) {
+    k_iota<<<uf_grid(T), 256, 0, s>>>(label, T);
+    k_hook_labels<<<uf_grid(T), 256, 0, s>>>(labels_in, vis_list, label, st);
+}
+
+void fa_launch_uf_compress(const int* vis_list, int* label, int T, const fa_dstat* st, cudaStream_t s) {
+    k_compress<<<uf_grid(T), 256, 0, s>>>(vis_list, label, st);
+}
+
+void fa_launch_canonicalize(const int* vis_list, int* label, int* tmp, int T, const fa_dstat* st, cudaStream_t s) {
+    // label holds roots for visible triangles; flags are recovered from the vis list
+    k_fill<<<uf_grid(T), 256, 0, s>>>(tmp, T, 0x7fffffff);
+    k_canon_min<<<uf_grid(T), 256, 0, s>>>(vis_list, label, tmp, st);
+}
+
+void fa_launch_canon_apply(const unsigned char* flags, int* label, const int* tmp, int T, cudaStream_t s) {
+    k_canon_apply<<<uf_grid(T), 256, 0, s>>>(flags, label, tmp, T);
+}
+
+void fa_launch_v2c(const int* vmin, const int* label, int* v2c, int V, cudaStream_t s) {
+    k_v2c<<<fa_grid(V, 256, FA_NUM_SMS * 8), 256, 0, s>>>(vmin, label, v2c, V);
+}
+
+void fa_launch_flags_from_labels(const int* labels, unsigned char* flags, int T, cudaStream_t s) {
+    k_flags_from_labels<<<uf_grid(T), 256, 0, s>>>(labels, flags, T);
+}
+
+void fa_launch_fill(int* a, int n, int v, cudaStream_t s) { k_fill<<<uf_grid(n), 256, 0, s>>>(a, n, v); }
+
+// ---- chart roots: ordered compaction of label[t] == t over the vis list -------
+__global__ void __launch_bounds__(CMP_THREADS) k_count_roots(const int* __restrict__ vis_list,
+                                                             const int* __restrict__ label, int* __restrict__ blocks,
+                                                             const fa_dstat* __restrict__ st) {
+    __shared__ int sm[32];
+    int n = st->n_vis;
+    int base = blockIdx.x * CMP_TILE + threadIdx.x * CMP_ITEMS;
+    int c = 0;
+#pragma unroll 4
+    for (int i = 0; i < CMP_ITEMS; i++) {
+        int k = base + i;
+        if (k < n) {
+            int t = vis_list[k];
+            c += label[t] == t;
+        }
+    }
+    c = warp_sum(c);
+    if (lane_id() == 0) sm[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int s = 0;
+        for (int i = 0; i < CMP_THREADS / 32; i++) s += sm[i];
+        blocks[blockIdx.x] = s;
+    }
+}
+
+__global__ void __launch_bounds__(CMP_THREADS) k_scatter_roots(const int* __restrict__ vis_list,
+                                                               const int* __restrict__ label,
+                                                               const int* __restrict__ blocks, int nblocks,
+                                                               int* __restrict__ roots, int* __restrict__ cidx,
+                                                               unsigned long long* __restrict__ ndc_keys,
+                                                               int* __restrict__ survived, fa_dstat* __restrict__ st) {
+    __shared__ int sm[32];
+    int n = st->n_vis;
+    int last = (n + CMP_TILE - 1) / CMP_TILE - 1;
+    if (last < 0) last = 0;
+    if ((int)blockIdx.x > last) return;
+    int offset = block_prefix_of(blocks, blockIdx.x, sm);
+    int base = blockIdx.x * CMP_TILE + threadIdx.x * CMP_ITEMS;
+    int tv[CMP_ITEMS];
+    int c = 0;
+#pragma unroll
+    for (int i = 0; i < CMP_ITEMS; i++) {
+        int k = base + i;
+        tv[i] = -1;
+        if (k < n) {
+            int t = vis_list[k];
+            if (label[t] == t) { tv[i] = t; c++; }
+        }
+    }
+    int total;
+    int pos = offset + block_exclusive_scan(c, sm, &total);
+#pragma unroll
+    for (int i = 0; i < CMP_ITEMS; i++) {
+        if (tv[i] >= 0) {
+            roots[pos] = tv[i];
+            cidx[tv[i]] = pos;
+            ndc_keys[4 * pos + 0] = FA_KEY_POS_INF;
+            ndc_keys[4 * pos + 1] = FA_KEY_POS_INF;
+            ndc_keys[4 * pos + 2] = FA_KEY_NEG_INF;
+            ndc_keys[4 * pos + 3] = FA_KEY_NEG_INF;
+            survived[pos] = 0;
+            pos++;
+        }
+    }
+    if ((int)blockIdx.x == last && threadIdx.x == 0) st->n_charts = offset + total;
+}
+
+void fa_launch_compact_roots(const int* vis_list, const int* label, int T, int* blocks, int* roots, int* cidx,
+                             unsigned long long* ndc_keys, int* survived, fa_dstat* st, cudaStream_t s) {
+    int nb = fa_compact_blocks(T);
+    k_count_roots<<<nb, CMP_THREADS, 0, s>>>(vis_list, label, blocks, st);
+    k_scatter_roots<<<nb, CMP_THREADS, 0, s>>>(vis_list, label, blocks, nb, roots, cidx, ndc_keys, survived, st);
+}

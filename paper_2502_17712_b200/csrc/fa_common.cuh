@@ -1,0 +1,205 @@
+// fa_common.cuh — shared device helpers for the B200 atlas path.
+//
+// Every kernel in this library is compiled with -fmad=false: the reference
+// computes in numpy float64 with one rounding per operation, so contraction
+// of a*b+c into DFMA would change bits.  The only FMAs are the explicit
+// __fma_rn() calls that restate OpenBLAS' dgemm chain.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/fastatlas.h"
+
+#define FA_W_EPSILON 1e-9       // geometry.py:19
+#define FA_DEPTH_EPSILON 1e-6   // charts.py:26
+#define FA_MAX_BOX_DIM (1 << 23)  // packing.py:25
+#define FA_SCALE_GRID_BITS 24   // packing.py:29
+#define FA_DIRECTION_PERIOD 3   // packing.py:32
+#define FA_MAX_OVERFLOW_ITERS 8 // packing.py:34
+#define FA_MAXV 16              // clipped polygon capacity (real max is 10)
+
+#define FA_NUM_SMS 148
+
+// device status bits (fa_ctx::dstat->flags)
+#define FA_DFLAG_POLY_OVERFLOW 1u
+#define FA_DFLAG_HEIGHT_OVERFLOW 2u
+#define FA_DFLAG_DEGENERATE_CHART 4u
+#define FA_DFLAG_PACK_FAILURE 8u
+#define FA_DFLAG_QUEUE_OVERFLOW 16u
+#define FA_DFLAG_DUPLICATE_MIN_TRI 32u
+#define FA_DFLAG_KEY_RANGE 64u
+#define FA_DFLAG_BAD_ARGS 128u
+
+// Per-frame device counters and status (one 256-byte struct, zeroed per frame).
+struct fa_dstat {
+    unsigned int flags;
+    int n_vis;            // visible triangles
+    int n_charts;         // chart roots (ascending)
+    int n_small;          // small-raster triangle list length (pass 2 input)
+    int n_large;          // large-raster triangle setups
+    int n_tiles;          // large-raster tile work items
+    int best;             // selected candidate (1-based), 0 = none
+    int floor_fail;       // pack floor-width failure
+    long long screen_fragments;
+    long long texels_allocated;
+    long long scale_num;
+    long long scale_den;
+    int n_rows_max;
+    int max_h;            // max oriented height (sort key range)
+    unsigned int done;    // pack batch early-exit
+    int pad[45];
+};
+
+// ---- float64 <-> order-preserving u64 key --------------------------------
+__device__ __forceinline__ unsigned long long f64_key(double x) {
+    unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double key_f64(unsigned long long k) {
+    unsigned long long b = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
+    return __longlong_as_double((long long)b);
+}
+#define FA_KEY_POS_INF 0xfff0000000000000ull   // f64_key(+inf)
+#define FA_KEY_NEG_INF 0x000fffffffffffffull   // f64_key(-inf)
+
+// ---- projection (charts.py:273-274): OpenBLAS dgemm FMA chain -------------
+struct vp_mat { double m[16]; };
+
+__device__ __forceinline__ double4 project_point(double x, double y, double z, const double* __restrict__ m) {
+    double4 o;
+    double a;
+    a = __dmul_rn(x, m[0]);  a = __fma_rn(y, m[1], a);  a = __fma_rn(z, m[2], a);  a = __fma_rn(1.0, m[3], a);  o.x = a;
+    a = __dmul_rn(x, m[4]);  a = __fma_rn(y, m[5], a);  a = __fma_rn(z, m[6], a);  a = __fma_rn(1.0, m[7], a);  o.y = a;
+    a = __dmul_rn(x, m[8]);  a = __fma_rn(y, m[9], a);  a = __fma_rn(z, m[10], a); a = __fma_rn(1.0, m[11], a); o.z = a;
+    a = __dmul_rn(x, m[12]); a = __fma_rn(y, m[13], a); a = __fma_rn(z, m[14], a); a = __fma_rn(1.0, m[15], a); o.w = a;
+    return o;
+}
+
+// ---- warp helpers ---------------------------------------------------------
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ int warp_max_i(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__device__ __forceinline__ long long warp_max_ll(long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        long long w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = v > w ? v : w;
+    }
+    return v;
+}
+
+// warp-aggregated append: returns the slot of this lane when pred is true
+__device__ __forceinline__ int warp_append(int* counter, bool pred) {
+    unsigned mask = __ballot_sync(0xffffffffu, pred);
+    if (!mask) return -1;
+    int leader = __ffs(mask) - 1;
+    int base = 0;
+    if (lane_id() == leader) base = atomicAdd(counter, __popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    return pred ? base + __popc(mask & ((1u << lane_id()) - 1u)) : -1;
+}
+
+// block-wide exclusive scan of one int per thread (blockDim multiple of 32, <= 1024)
+__device__ __forceinline__ int block_exclusive_scan(int v, int* smem32, int* total) {
+    int lane = lane_id(), wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) smem32[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        int s = lane < nw ? smem32[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < nw) smem32[lane] = s;
+    }
+    __syncthreads();
+    int base = wid > 0 ? smem32[wid - 1] : 0;
+    int tot = smem32[nw - 1];
+    __syncthreads();
+    if (total) *total = tot;
+    return base + x - v;
+}
+
+// same for int64
+__device__ __forceinline__ long long block_exclusive_scan_ll(long long v, long long* smem32, long long* total) {
+    int lane = lane_id(), wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) smem32[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        long long s = lane < nw ? smem32[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            long long y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < nw) smem32[lane] = s;
+    }
+    __syncthreads();
+    long long base = wid > 0 ? smem32[wid - 1] : 0;
+    long long tot = smem32[nw - 1];
+    __syncthreads();
+    if (total) *total = tot;
+    return base + x - v;
+}
+
+__device__ __forceinline__ long long block_max_ll(long long v, long long* smem32) {
+    int lane = lane_id(), wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_max_ll(v);
+    if (lane == 0) smem32[wid] = v;
+    __syncthreads();
+    long long r = smem32[0];
+    for (int i = 1; i < nw; i++) r = r > smem32[i] ? r : smem32[i];
+    __syncthreads();
+    return r;
+}
+
+__device__ __forceinline__ long long block_sum_ll(long long v, long long* smem32) {
+    int lane = lane_id(), wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_sum(v);
+    if (lane == 0) smem32[wid] = v;
+    __syncthreads();
+    long long r = 0;
+    for (int i = 0; i < nw; i++) r += smem32[i];
+    __syncthreads();
+    return r;
+}
+
+static inline int fa_grid(long long n, int block, int max_blocks) {
+    long long g = (n + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > max_blocks) g = max_blocks;
+    return (int)g;
+}
+
+// 32-byte read-only load of a clip-space vertex (two 128-bit LDG.NC)
+__device__ __forceinline__ double4 ldg4(const double4* p) {
+    const double2* q = reinterpret_cast<const double2*>(p);
+    double2 a = __ldg(q), b = __ldg(q + 1);
+    return make_double4(a.x, a.y, b.x, b.y);
+}

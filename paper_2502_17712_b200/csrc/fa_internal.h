@@ -1,0 +1,162 @@
+// fa_internal.h — context layout and kernel launchers (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/fastatlas.h"
+#include "fa_common.cuh"
+
+struct TriSetup;
+
+// growable device buffer
+struct fa_buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+struct fa_graph_key {
+    int width = 0, height = 0, cull = 0, uv_f64 = 0, want_depth = 0;
+    long long omega = 0, n_scales = 0, min_dim = 0, padding = 0;
+    double prescale = 0;
+    long long T = 0, V = 0;
+    const void* pos = nullptr;
+    const void* tris = nullptr;
+    size_t gen = 0;  // buffer generation (graph invalid after any regrow)
+    bool operator==(const fa_graph_key& o) const {
+        return width == o.width && height == o.height && cull == o.cull && uv_f64 == o.uv_f64 &&
+               want_depth == o.want_depth && omega == o.omega && n_scales == o.n_scales && min_dim == o.min_dim &&
+               padding == o.padding && prescale == o.prescale && T == o.T && V == o.V && pos == o.pos &&
+               tris == o.tris && gen == o.gen;
+    }
+};
+
+struct fa_ctx {
+    int device = 0;
+    // resident mesh (caller-owned)
+    const double* pos = nullptr;
+    const int* tris = nullptr;
+    int64_t V = 0, T = 0;
+
+    // scratch (grown on demand)
+    fa_buf clip, depth_keys, depth_f64, flags, vis_list, small_list, large, tiles, label, vmin, v2c, cidx;
+    fa_buf roots, ndc_keys, ndc, px, target, survived, okey, oidx, ow, oh, orot, sortk, sortv, pinv;
+    fa_buf cand, cand_p, cand_w, cand_h, cand_y, rowstart, placements, uv, vp_dev, blocks, dstat, aux;
+    fa_buf in_tw, in_th, in_cid, in_mt;
+    size_t gen = 0;
+    int max_large = 0, max_tiles = 0;
+    int pack_batch = 0;  // candidates per pack launch
+    int64_t pack_cap = 0;  // boxes the pack scratch holds
+    bool needs_rerun = false;
+
+    fa_dstat* hstat = nullptr;  // pinned mirror of the device status
+    double* hvp = nullptr;      // pinned camera staging
+    fa_frame_params last_params{};
+    int last_launches = 0;
+
+    // CUDA graph per frame shape
+    cudaGraphExec_t graph_exec = nullptr;
+    fa_graph_key graph_key{};
+};
+
+// growth helper: ensures buf has >= bytes; returns false on allocation failure
+bool fa_ensure(fa_ctx* ctx, fa_buf& b, size_t bytes);
+
+// ---- raster (fa_raster.cu) ------------------------------------------------
+void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* clip, int* vmin,
+                          unsigned long long* depth, long long npx, unsigned char* flags, int T, cudaStream_t s);
+void fa_launch_raster_setup(bool write_depth, const double4* clip, const int* tris, int T, int W, int H, int cull,
+                            unsigned long long* depth, int* small_list, TriSetup* large, int max_large, int2* tiles,
+                            int max_tiles, fa_dstat* st, cudaStream_t s);
+void fa_launch_raster_depth_tiles(const TriSetup* large, const int2* tiles, int max_tiles, int W,
+                                  unsigned long long* depth, fa_dstat* st, cudaStream_t s);
+void fa_launch_raster_vis(const double4* clip, const int* tris, const int* small_list, const TriSetup* large,
+                          const int2* tiles, int max_tiles, int T, int W, int H, int cull,
+                          const unsigned long long* depth, unsigned char* flags, const fa_dstat* st, cudaStream_t s);
+void fa_launch_decode_depth(const unsigned long long* keys, double* out, long long n, cudaStream_t s);
+void fa_launch_encode_depth(const double* in, unsigned long long* keys, long long n, cudaStream_t s);
+size_t fa_trisetup_bytes();
+
+// ---- charts (fa_charts.cu) -----------------------------------------------
+// ordered compaction of flags -> vis list; label[t] = flag ? t : -1
+void fa_launch_compact_visible(const unsigned char* flags, int T, int* blocks, int* vis_list, int* label,
+                               fa_dstat* st, cudaStream_t s);
+int fa_compact_blocks(long long n);
+void fa_launch_uf_vertex(const int* tris, const int* vis_list, int* vmin, int* label, int T, const fa_dstat* st,
+                         cudaStream_t s);
+void fa_launch_uf_edges(const int* adjacency, const unsigned char* flags, const int* vis_list, int* label, int T,
+                        const fa_dstat* st, cudaStream_t s);
+void fa_launch_uf_labels(const int* labels_in, const int* vis_list, int* label, int T, const fa_dstat* st,
+                         cudaStream_t s);
+void fa_launch_uf_compress(const int* vis_list, int* label, int T, const fa_dstat* st, cudaStream_t s);
+void fa_launch_canonicalize(const int* vis_list, int* label, int* tmp, int T, const fa_dstat* st, cudaStream_t s);
+void fa_launch_v2c(const int* vmin, const int* label, int* v2c, int V, cudaStream_t s);
+void fa_launch_flags_from_labels(const int* labels, unsigned char* flags, int T, cudaStream_t s);
+// ordered compaction of roots (label[t]==t over the vis list) -> roots, cidx, chart init
+void fa_launch_compact_roots(const int* vis_list, const int* label, int T, int* blocks, int* roots, int* cidx,
+                             unsigned long long* ndc_keys, int* survived, fa_dstat* st, cudaStream_t s);
+void fa_launch_canon_apply(const unsigned char* flags, int* label, const int* tmp, int T, cudaStream_t s);
+void fa_launch_fill(int* a, int n, int v, cudaStream_t s);
+
+// ---- bounds (fa_bounds.cu) -----------------------------------------------
+void fa_launch_chart_bounds(const double4* clip, const int* tris, const int* vis_list, const int* label,
+                            const int* cidx, int T, unsigned long long* ndc_keys, int* survived, const fa_dstat* st,
+                            cudaStream_t s);
+void fa_launch_box_dims(const unsigned long long* ndc_keys, const int* survived, const int* roots, int T, int W, int H,
+                        double prescale, double* ndc, int* px, long long* target, long long* tw, long long* th,
+                        long long* cid, int cap, fa_dstat* st, cudaStream_t s);
+
+// ---- pack (fa_pack.cu) ---------------------------------------------------
+struct fa_pack_bufs {
+    const long long* tw;       // target dims, input order
+    const long long* th;
+    const long long* chart_id; // per input box
+    long long* ow;             // ordered oriented dims
+    long long* oh;
+    unsigned char* rot;        // ordered rotated flag
+    int* perm;                 // ordered -> input index
+    int* pinv;                 // input index -> ordered position
+    unsigned long long* sortk; // radix ping-pong
+    int* sortv;
+    long long* cand;           // per-candidate results (4 x int64 each)
+    long long* cand_p;         // per-candidate prefix sums (n each)
+    int* cand_w;
+    int* cand_h;
+    int* cand_y;
+    int* rowstart;             // per-candidate row starts (n each)
+    long long* placements;     // (n,8) packing order
+    unsigned char* accept_out; // optional
+    int* gfront;               // global frontline (batch x (omega+1)) when omega is too big for smem
+};
+void fa_launch_orient_sort(const fa_pack_bufs& b, int n_max, const int* n_dev, long long max_h, fa_dstat* st,
+                           cudaStream_t s);
+int fa_launch_pack(const fa_pack_bufs& b, int n_max, const int* n_dev, long long omega, long long n_scales,
+                   long long min_dim, long long pad, int batch, fa_dstat* st, cudaStream_t s);
+void fa_launch_orient_sort_mt(const long long* tw, const long long* th, const long long* mt, int n, long long max_h,
+                              long long* ow, long long* oh, unsigned char* rot, int* perm, int* pinv,
+                              unsigned long long* sk, int* sv, int reject_dups, fa_dstat* st, cudaStream_t s);
+void fa_launch_pack_at_scale(const long long* ow, const long long* oh, int n, long long num, long long den,
+                             long long omega, long long min_dim, long long pad, long long* cand, long long* cand_p,
+                             int* cand_w, int* cand_h, int* cand_y, int* rowstart, int* gfront, cudaStream_t s);
+void fa_launch_xywh(const long long* cand, const long long* cand_p, const int* cand_w, const int* cand_h,
+                    const int* cand_y, int n, long long omega, long long* out, cudaStream_t s);
+void fa_launch_push_up_impl(const long long* rows, const long long* x, const long long* w, const long long* h, int n,
+                            long long omega, int* rowstart, long long* y, long long* used, int* gfront,
+                            cudaStream_t s);
+bool fa_front_in_smem(long long omega);
+#define FA_CAND_REC 5
+void fa_launch_fold(const long long* w, int n, long long omega, long long* rows, long long* x, long long* m,
+                    cudaStream_t s);
+
+// ---- uv (fa_uv.cu) -------------------------------------------------------
+void fa_launch_uv(const double4* clip, const int* tris, const int* vis_list, const int* label, const int* cidx,
+                  const int* pinv, const double* ndc, const int* px, const long long* placements, int T, int W, int H,
+                  long long pad, bool f64, void* uv, const fa_dstat* st, cudaStream_t s);
+
+// ---- standalone helpers (fa_bounds.cu / fa_pack.cu) -------------------------
+void fa_launch_blinn_points(const double* p4, int n, double* out, cudaStream_t s);
+void fa_launch_select_side_plane(const double* t12, int n, int* out, cudaStream_t s);
+void fa_launch_chart_bbox_world(const double* xyz, int n, const double* vp, unsigned long long* keys, int* surv,
+                                double* box_out, cudaStream_t s);
+void fa_launch_viewport_box(const double* box, int n, int W, int H, long long* out, cudaStream_t s);
+void fa_launch_orient(const long long* tw, const long long* th, int n, long long* ow, long long* oh,
+                      unsigned char* rot, cudaStream_t s);

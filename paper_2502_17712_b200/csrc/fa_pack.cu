@@ -1,0 +1,714 @@
+// fa_pack.cu — orient/order, candidate-parallel fold + push-up packing.
+//
+// Reference: packing.py:109-362.
+//   * orient/order (packing.py:109-130): one CTA; stable LSD radix sort
+//     (8-bit digits, warp match_any ranking) on the composite key
+//     (h descending, min_tri ascending).  In the frame path the boxes
+//     arrive in ascending-root order, so only the height digits are sorted.
+//   * pack (packing.py:295-345): one CTA per scale candidate.  Each CTA runs
+//     up to 9 rounds of [scaled dims -> block max -> block prefix-sum fold
+//     -> overflow m -> exact dyadic snap] (packing.py:245-268), the
+//     pigeonhole check, and push_up (packing.py:170-215) against a
+//     shared-memory frontline: rows in order, each row's boxes handled by
+//     thread groups sized to the row population (max over the column span,
+//     then write back the new top; boxes of one row never overlap when
+//     m == 0, so no intra-row barrier is needed).
+//   * selection (packing.py:342-345): the largest accepted candidate index.
+// All scale arithmetic is exact integer arithmetic with numpy int64
+// semantics; the snap uses 128-bit intermediates.
+#include "fa_internal.h"
+
+#define PK_THREADS 1024
+#define SORT_THREADS 1024
+
+// numpy int64 semantics of -((-num * t) // den) (packing.py:349)
+__device__ __forceinline__ long long np_ceil_scaled(long long num, long long t, long long den) {
+    unsigned long long prod = (0ull - (unsigned long long)num) * (unsigned long long)t;  // wrapping
+    long long a = (long long)prod;
+    long long q = a / den;
+    if ((a % den != 0) && ((a < 0) != (den < 0))) q -= 1;  // floor
+    return (long long)(0ull - (unsigned long long)q);
+}
+
+__device__ __forceinline__ long long scaled_dim(long long t, long long num, long long den, long long min_dim,
+                                                long long pad) {
+    long long s = np_ceil_scaled(num, t, den);
+    if (s < min_dim) s = min_dim;
+    return s + 2 * pad;
+}
+
+__device__ __forceinline__ long long gcd_ll(long long a, long long b) {
+    if (a < 0) a = -a;
+    if (b < 0) b = -b;
+    while (b) {
+        long long t = a % b;
+        a = b;
+        b = t;
+    }
+    return a;
+}
+
+// u128 helpers for the snap (packing.py:353-362)
+struct u128 {
+    unsigned long long hi, lo;
+};
+__device__ __forceinline__ u128 mul64(unsigned long long a, unsigned long long b) {
+    u128 r;
+    r.lo = a * b;
+    r.hi = __umul64hi(a, b);
+    return r;
+}
+__device__ __forceinline__ bool ge128(u128 a, u128 b) { return a.hi != b.hi ? a.hi > b.hi : a.lo >= b.lo; }
+__device__ __forceinline__ u128 sub128(u128 a, u128 b) {
+    u128 r;
+    r.lo = a.lo - b.lo;
+    r.hi = a.hi - b.hi - (a.lo < b.lo ? 1ull : 0ull);
+    return r;
+}
+__device__ __forceinline__ u128 shl128(u128 a, int s) {
+    if (s == 0) return a;
+    u128 r;
+    if (s >= 64) { r.hi = a.lo << (s - 64); r.lo = 0; }
+    else { r.hi = (a.hi << s) | (a.lo >> (64 - s)); r.lo = a.lo << s; }
+    return r;
+}
+// floor(n / d) for d != 0, restoring division
+__device__ u128 div128(u128 n, u128 d) {
+    u128 q = {0, 0}, r = {0, 0};
+    for (int i = 127; i >= 0; i--) {
+        r = shl128(r, 1);
+        unsigned long long bit = i >= 64 ? (n.hi >> (i - 64)) & 1ull : (n.lo >> i) & 1ull;
+        r.lo |= bit;
+        if (ge128(r, d)) {
+            r = sub128(r, d);
+            if (i >= 64) q.hi |= 1ull << (i - 64); else q.lo |= 1ull << i;
+        }
+    }
+    return q;
+}
+
+// (num, den) <- reduce(floor(num*omega*2^24 / (den*(omega+m))), 2^24)
+__device__ __forceinline__ void snap_scale(long long& num, long long& den, long long omega, long long m) {
+    u128 n = mul64((unsigned long long)num, (unsigned long long)omega);  // < 2^116 overall after shift
+    n = shl128(n, FA_SCALE_GRID_BITS);
+    u128 d = mul64((unsigned long long)den, (unsigned long long)(omega + m));
+    u128 f = div128(n, d);
+    long long fn = (long long)f.lo;  // < 2^24 since scale <= 1
+    if (fn == 0) { num = 0; den = 1; return; }
+    int tz = __ffsll(fn) - 1;
+    if (tz > FA_SCALE_GRID_BITS) tz = FA_SCALE_GRID_BITS;
+    num = fn >> tz;
+    den = (1ll << FA_SCALE_GRID_BITS) >> tz;
+}
+
+// ============================================================================
+// orient + order: single CTA stable LSD radix sort
+// ============================================================================
+struct SortSmem {
+    int hist[256];
+    int base[256];
+    int wcnt[32][257];
+    long long red[32];
+    int flag;
+};
+
+// one stable pass on digit `shift` of 64-bit keys: (ki,vi) -> (ko,vo)
+__device__ void radix_pass(const unsigned long long* ki, const int* vi, unsigned long long* ko, int* vo, int n,
+                           int shift, SortSmem& sm) {
+    int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+    for (int i = tid; i < 256; i += blockDim.x) sm.hist[i] = 0;
+    for (int i = tid; i < 32 * 257; i += blockDim.x) (&sm.wcnt[0][0])[i] = 0;
+    __syncthreads();
+    for (int i = tid; i < n; i += blockDim.x) atomicAdd(&sm.hist[(ki[i] >> shift) & 255ull], 1);
+    __syncthreads();
+    if (tid < 32) {
+        // exclusive scan of 256 bins by one warp (8 per lane)
+        int loc[8], s = 0;
+        for (int j = 0; j < 8; j++) { loc[j] = sm.hist[lane * 8 + j]; s += loc[j]; }
+        int incl = s;
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        int run = incl - s;
+        for (int j = 0; j < 8; j++) { sm.base[lane * 8 + j] = run; run += loc[j]; }
+    }
+    __syncthreads();
+    for (int t0 = 0; t0 < n; t0 += blockDim.x) {
+        int i = t0 + tid;
+        bool valid = i < n;
+        unsigned long long k = valid ? ki[i] : 0ull;
+        int v = valid ? vi[i] : 0;
+        int d = valid ? (int)((k >> shift) & 255ull) : 256;
+        unsigned peers = __match_any_sync(0xffffffffu, d);
+        int rank = __popc(peers & ((1u << lane) - 1u));
+        if (rank == 0) sm.wcnt[warp][d] = __popc(peers);
+        __syncthreads();
+        if (valid) {
+            int off = 0;
+            for (int w = 0; w < warp; w++) off += sm.wcnt[w][d];
+            int pos = sm.base[d] + off + rank;
+            ko[pos] = k;
+            vo[pos] = v;
+        }
+        __syncthreads();
+        if (tid < 256) {
+            int s = 0;
+            for (int w = 0; w < 32; w++) { s += sm.wcnt[w][tid]; sm.wcnt[w][tid] = 0; }
+            sm.base[tid] += s;
+        }
+        if (tid < 32) sm.wcnt[tid][256] = 0;
+        __syncthreads();
+    }
+}
+
+// Frame mode (mt == nullptr): input order already ascending min_tri.
+__global__ void __launch_bounds__(SORT_THREADS) k_orient_sort(const long long* __restrict__ tw,
+                                                              const long long* __restrict__ th,
+                                                              const long long* __restrict__ mt, int n_max,
+                                                              const int* __restrict__ n_dev, long long max_h,
+                                                              long long* __restrict__ ow, long long* __restrict__ oh,
+                                                              unsigned char* __restrict__ rot, int* __restrict__ perm,
+                                                              int* __restrict__ pinv, unsigned long long* sk,
+                                                              int* sv, int reject_dups, fa_dstat* __restrict__ st) {
+    __shared__ SortSmem sm;
+    int n = n_dev ? *n_dev : n_max;
+    if (n > n_max) {
+        if (threadIdx.x == 0) atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW);
+        return;
+    }
+    int tid = threadIdx.x;
+    long long hmax = 0, hmin = 0x7fffffffffffffffll, mmin = 0x7fffffffffffffffll, mmax = 0;
+    bool overflow = false;
+    for (int i = tid; i < n; i += blockDim.x) {
+        long long w = tw[i], h = th[i];
+        long long oh_ = w > h ? w : h;
+        if (oh_ > max_h) overflow = true;
+        hmax = oh_ > hmax ? oh_ : hmax;
+        hmin = oh_ < hmin ? oh_ : hmin;
+        if (mt) {
+            mmin = mt[i] < mmin ? mt[i] : mmin;
+            mmax = mt[i] > mmax ? mt[i] : mmax;
+        }
+    }
+    if (tid == 0) sm.flag = 0;
+    __syncthreads();
+    if (overflow) sm.flag = 1;
+    hmax = block_max_ll(hmax, sm.red);
+    hmin = -block_max_ll(-hmin, sm.red);
+    if (mt) {
+        mmax = block_max_ll(mmax, sm.red);
+        mmin = -block_max_ll(-mmin, sm.red);
+    }
+    if (sm.flag) {
+        if (tid == 0) atomicOr(&st->flags, FA_DFLAG_HEIGHT_OVERFLOW);
+        return;
+    }
+    if (n == 0) return;
+    if (tid == 0) st->max_h = (int)hmax;
+    int hbits = 0;
+    while (hbits < 63 && ((hmax - hmin) >> hbits) != 0) hbits++;
+    int mbits = 0;
+    if (mt)
+        while (mbits < 63 && ((unsigned long long)(mmax - mmin) >> mbits) != 0) mbits++;
+    if (hbits + mbits > 64) {
+        if (tid == 0) atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW);  // key range unsupported
+        return;
+    }
+    // composite key: (hmax - h) above a byte-aligned (mt - mmin) field, so the
+    // first ceil(mbits/8) LSD passes leave the array ordered by min_tri alone
+    int mfield = 8 * ((mbits + 7) / 8);
+    if (hbits + mfield > 64) {
+        if (tid == 0) atomicOr(&st->flags, FA_DFLAG_KEY_RANGE);
+        return;
+    }
+    unsigned long long* ka = sk;
+    unsigned long long* kb = sk + n_max;
+    int* va = sv;
+    int* vb = sv + n_max;
+    for (int i = tid; i < n; i += blockDim.x) {
+        long long w = tw[i], h = th[i];
+        long long oh_ = w > h ? w : h;
+        unsigned long long key = mfield < 64 ? ((unsigned long long)(hmax - oh_) << mfield) : 0ull;
+        if (mt) key |= (unsigned long long)(mt[i] - mmin);
+        ka[i] = key;
+        va[i] = i;
+    }
+    __syncthreads();
+    int mpasses = mfield / 8;
+    int passes = mpasses + (hbits + 7) / 8;
+    for (int p = 0; p < passes; p++) {
+        radix_pass(ka, va, kb, vb, n, 8 * p, sm);
+        unsigned long long* tk = ka; ka = kb; kb = tk;
+        int* tv = va; va = vb; vb = tv;
+        if (mt && reject_dups && p == mpasses - 1) {
+            // ordered by min_tri: adjacent equal ids are duplicates (packing.py:319-323)
+            for (int j = tid + 1; j < n; j += blockDim.x)
+                if (mt[va[j - 1]] == mt[va[j]]) sm.flag = 1;
+            __syncthreads();
+            if (sm.flag) {
+                if (tid == 0) atomicOr(&st->flags, FA_DFLAG_DUPLICATE_MIN_TRI);
+                return;
+            }
+        }
+    }
+    __syncthreads();
+    for (int j = tid; j < n; j += blockDim.x) {
+        int i = va[j];
+        long long w = tw[i], h = th[i];
+        bool r = w > h;
+        perm[j] = i;
+        pinv[i] = j;
+        ow[j] = r ? h : w;
+        oh[j] = r ? w : h;
+        rot[j] = r;
+    }
+}
+
+// ============================================================================
+// packing candidates
+// ============================================================================
+struct PackSmem {
+    long long red[32];
+    int red_i[32];
+    int flag;
+};
+
+// One candidate: returns accept; fills cand_w/h/p/y/rowstart for the CTA.
+__device__ bool pack_candidate(const long long* __restrict__ ow, const long long* __restrict__ oh, int n,
+                               long long num, long long den, long long omega, int kbits, long long min_dim,
+                               long long pad, int* cw, int* ch, long long* cp, int* cy, int* rowstart, int* front,
+                               long long& out_num, long long& out_den, long long& out_used, PackSmem& sm) {
+    int tid = threadIdx.x;
+    bool have_fold = false;
+    long long m = 0;
+    for (int it = 0; it < FA_MAX_OVERFLOW_ITERS + 1; it++) {
+        long long wmax = 0;
+        for (int b = tid; b < n; b += blockDim.x) {
+            long long w = scaled_dim(ow[b], num, den, min_dim, pad);
+            cw[b] = (int)w;
+            wmax = w > wmax ? w : wmax;
+        }
+        // note: widths <= omega + ... stay well inside int32 (checked by host)
+        wmax = block_max_ll(wmax, sm.red);
+        if (wmax > omega) {
+            m = wmax - omega;
+            have_fold = false;
+        } else {
+            long long carry = 0, mloc = -(1ll << 62);
+            for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+                int b = c0 + tid;
+                long long w = b < n ? (long long)cw[b] : 0;
+                long long tot;
+                long long p = carry + block_exclusive_scan_ll(w, sm.red, &tot);
+                if (b < n) {
+                    cp[b] = p;
+                    long long q = p & (omega - 1);
+                    long long over = q + w - omega;
+                    mloc = over > mloc ? over : mloc;
+                }
+                carry += tot;
+            }
+            mloc = block_max_ll(mloc, sm.red);
+            m = mloc > 0 ? mloc : 0;
+            have_fold = true;
+        }
+        if (m == 0) break;
+        have_fold = false;
+        snap_scale(num, den, omega, m);
+    }
+    if (!have_fold || m != 0) return false;
+    // heights + pigeonhole (packing.py:271-274), int64 wrapping sum
+    unsigned long long area = 0;
+    for (int b = tid; b < n; b += blockDim.x) {
+        long long h = scaled_dim(oh[b], num, den, min_dim, pad);
+        ch[b] = (int)h;
+        area += (unsigned long long)cw[b] * (unsigned long long)h;
+    }
+    area = (unsigned long long)block_sum_ll((long long)area, sm.red);
+    if ((long long)area > omega * omega) return false;
+    // row starts
+    for (int b = tid; b < n; b += blockDim.x) {
+        long long r = cp[b] >> kbits;
+        if (b == 0 || (cp[b - 1] >> kbits) != r) rowstart[r] = b;
+    }
+    for (int c = tid; c <= omega; c += blockDim.x) front[c] = 0;
+    if (tid == 0) sm.flag = 0;
+    __syncthreads();
+    int n_rows = (int)(cp[n - 1] >> kbits) + 1;
+    long long used = 0;
+    for (int r = 0; r < n_rows; r++) {
+        int b0 = rowstart[r];
+        int b1 = (r + 1 < n_rows) ? rowstart[r + 1] : n;
+        int nb = b1 - b0;
+        bool left = (r % FA_DIRECTION_PERIOD) == 0;
+        int G = 32;
+        while (G > 1 && G * nb > (int)blockDim.x) G >>= 1;
+        int groups = blockDim.x / G;
+        int g = tid / G, gl = tid % G;
+        // block-uniform trip count: the group shuffles below are full-warp
+        for (int gbase = 0; gbase < nb; gbase += groups) {
+            int gb = gbase + g;
+            bool act = gb < nb;
+            int b = b0 + (act ? gb : 0);
+            long long q = cp[b] & (omega - 1);
+            int w = act ? cw[b] : 0;
+            int x = left ? (int)q : (int)(omega - q - w);
+            int rest = 0;
+            for (int c = x + gl; c < x + w; c += G) rest = max(rest, front[c]);
+            for (int o = G >> 1; o > 0; o >>= 1) rest = max(rest, __shfl_xor_sync(0xffffffffu, rest, o, G));
+            // saturate above omega: any such top already rejects the candidate
+            long long top64 = (long long)rest + ch[b];
+            int top = top64 > omega ? (int)(omega + 1) : (int)top64;
+            if (act) {
+                for (int c = x + gl; c < x + w; c += G) front[c] = top;
+                if (gl == 0) cy[b] = rest;
+                used = top > used ? top : used;
+            }
+        }
+        // groups are warp-aligned (G divides 32), so shuffles above are full-warp;
+        // the barrier orders this row's writes before the next row's reads
+        __syncthreads();
+    }
+    used = block_max_ll(used, sm.red);
+    out_used = used;
+    if (used > omega) return false;
+    long long g2 = gcd_ll(num, den);
+    if (g2 == 0) g2 = 1;
+    out_num = num / g2;
+    out_den = den / g2;
+    return true;
+}
+
+// cand record: [accept, num, den, used, slot]
+#define CAND_REC FA_CAND_REC
+
+__global__ void __launch_bounds__(PK_THREADS) k_pack(const long long* __restrict__ ow, const long long* __restrict__ oh,
+                                                     int n_max, const int* __restrict__ n_dev, long long omega,
+                                                     int kbits, long long n_scales, long long first,
+                                                     long long explicit_num, long long explicit_den, long long min_dim,
+                                                     long long pad, long long* __restrict__ cand,
+                                                     long long* __restrict__ cand_p, int* __restrict__ cand_w,
+                                                     int* __restrict__ cand_h, int* __restrict__ cand_y,
+                                                     int* __restrict__ rowstart, int* __restrict__ gfront,
+                                                     fa_dstat* __restrict__ st) {
+    extern __shared__ int dyn_front[];
+    __shared__ PackSmem sm;
+    int n = n_dev ? *n_dev : n_max;
+    if (n > n_max) {
+        if (st && threadIdx.x == 0) atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW);
+        return;
+    }
+    long long i = first - blockIdx.x;  // candidates descending within a batch
+    if (i < 1) return;
+    if (st && st->done) return;
+    if (n <= 0) return;
+    if (st && (st->flags & (FA_DFLAG_HEIGHT_OVERFLOW | FA_DFLAG_KEY_RANGE | FA_DFLAG_DUPLICATE_MIN_TRI))) return;
+    long long num, den;
+    if (explicit_den > 0) {
+        long long g = gcd_ll(explicit_num, explicit_den);
+        num = explicit_num / g;
+        den = explicit_den / g;
+    } else {
+        long long g = gcd_ll(i, n_scales);
+        num = i / g;
+        den = n_scales / g;
+    }
+    size_t slot = blockIdx.x;
+    int* front = gfront ? gfront + slot * (size_t)(omega + 1) : dyn_front;
+    long long rn = 0, rd = 1, used = 0;
+    bool ok = pack_candidate(ow, oh, n, num, den, omega, kbits, min_dim, pad, cand_w + slot * n_max,
+                             cand_h + slot * n_max, cand_p + slot * n_max, cand_y + slot * n_max,
+                             rowstart + slot * n_max, front, rn, rd, used, sm);
+    if (threadIdx.x == 0) {
+        long long* rec = cand + CAND_REC * (i - 1);
+        rec[0] = ok;
+        rec[1] = rn;
+        rec[2] = rd;
+        rec[3] = used;
+        rec[4] = (long long)slot;
+    }
+}
+
+// after a batch: done |= any accepted in [lo, hi]
+__global__ void k_batch_done(const long long* __restrict__ cand, long long lo, long long hi, fa_dstat* st) {
+    bool any = false;
+    for (long long i = lo + threadIdx.x; i <= hi; i += blockDim.x) any |= cand[CAND_REC * (i - 1)] != 0;
+    if (__syncthreads_or(any) && threadIdx.x == 0) st->done = 1;
+}
+
+// selection (packing.py:327-345) + placements in packing order
+__global__ void __launch_bounds__(1024) k_select(const long long* __restrict__ ow, const long long* __restrict__ tw,
+                                                 const long long* __restrict__ th, const long long* __restrict__ chart_id,
+                                                 const unsigned char* __restrict__ rot, const int* __restrict__ perm,
+                                                 int n_max, const int* __restrict__ n_dev, long long omega,
+                                                 long long n_scales, long long min_dim, long long pad,
+                                                 const long long* __restrict__ cand, const long long* __restrict__ cand_p,
+                                                 const int* __restrict__ cand_w, const int* __restrict__ cand_h,
+                                                 const int* __restrict__ cand_y, long long* __restrict__ placements,
+                                                 unsigned char* __restrict__ accept_out, fa_dstat* __restrict__ st) {
+    __shared__ long long red[32];
+    __shared__ long long s_best;
+    int n = n_dev ? *n_dev : n_max;
+    int tid = threadIdx.x;
+    if (st->flags & (FA_DFLAG_HEIGHT_OVERFLOW | FA_DFLAG_KEY_RANGE | FA_DFLAG_DUPLICATE_MIN_TRI |
+                     FA_DFLAG_QUEUE_OVERFLOW))
+        return;
+    if (n <= 0) {
+        if (tid == 0) { st->scale_num = 1; st->scale_den = 1; st->best = -1; }
+        return;
+    }
+    // floor-scale width check (packing.py:327-332)
+    long long fmax = 0;
+    for (int b = tid; b < n; b += blockDim.x) {
+        long long f = scaled_dim(ow[b], 1, n_scales, min_dim, pad);
+        fmax = f > fmax ? f : fmax;
+    }
+    fmax = block_max_ll(fmax, red);
+    long long best = 0;
+    for (long long i = tid + 1; i <= n_scales; i += blockDim.x) {
+        bool acc = cand[CAND_REC * (i - 1)] != 0 && cand[CAND_REC * (i - 1) + 4] >= 0;
+        if (accept_out) accept_out[i - 1] = acc;
+        if (acc && i > best) best = i;
+    }
+    best = block_max_ll(best, red);
+    if (fmax > omega) best = 0;
+    if (tid == 0) s_best = best;
+    __syncthreads();
+    best = s_best;
+    if (best == 0) {
+        if (tid == 0) { atomicOr(&st->flags, FA_DFLAG_PACK_FAILURE); st->best = 0; }
+        return;
+    }
+    const long long* rec = cand + CAND_REC * (best - 1);
+    size_t slot = (size_t)rec[4];
+    const long long* p = cand_p + slot * n_max;
+    const int* w = cand_w + slot * n_max;
+    const int* h = cand_h + slot * n_max;
+    const int* y = cand_y + slot * n_max;
+    int kbits = 63 - __clzll(omega);
+    long long tex = 0;
+    for (int j = tid; j < n; j += blockDim.x) {
+        long long q = p[j] & (omega - 1);
+        long long r = p[j] >> kbits;
+        long long x = (r % FA_DIRECTION_PERIOD == 0) ? q : omega - q - w[j];
+        int src = perm[j];
+        long long* P = placements + 8 * (long long)j;
+        P[0] = chart_id ? chart_id[src] : src;
+        P[1] = x;
+        P[2] = y[j];
+        P[3] = w[j];
+        P[4] = h[j];
+        P[5] = rot[j];
+        P[6] = tw[src];
+        P[7] = th[src];
+        long long cw = w[j] - 2 * pad, chh = h[j] - 2 * pad;
+        tex += (cw > 0 ? cw : 0) * (chh > 0 ? chh : 0);
+    }
+    tex = block_sum_ll(tex, red);
+    if (tid == 0) {
+        st->best = (int)best;
+        st->scale_num = rec[1];
+        st->scale_den = rec[2];
+        st->texels_allocated = tex;
+    }
+}
+
+// ---- standalone fold (packing.py:133-158) --------------------------------
+__global__ void __launch_bounds__(1024) k_fold(const long long* __restrict__ w, int n, long long omega,
+                                               long long* __restrict__ rows, long long* __restrict__ xs,
+                                               long long* __restrict__ m_out) {
+    __shared__ long long red[32];
+    int kbits = 63 - __clzll(omega);
+    long long carry = 0, mloc = -(1ll << 62);
+    for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+        int b = c0 + threadIdx.x;
+        long long wb = b < n ? w[b] : 0;
+        long long tot;
+        long long p = carry + block_exclusive_scan_ll(wb, red, &tot);
+        if (b < n) {
+            long long r = p >> kbits, q = p & (omega - 1);
+            rows[b] = r;
+            xs[b] = (r % FA_DIRECTION_PERIOD == 0) ? q : omega - q - wb;
+            long long over = q + wb - omega;
+            mloc = over > mloc ? over : mloc;
+        }
+        carry += tot;
+    }
+    mloc = block_max_ll(mloc, red);
+    if (threadIdx.x == 0) *m_out = mloc > 0 ? mloc : 0;
+}
+
+// ---- standalone push_up (packing.py:170-215) -------------------------------
+__global__ void __launch_bounds__(1024) k_push_up(const long long* __restrict__ rows, const long long* __restrict__ xs,
+                                                  const long long* __restrict__ w, const long long* __restrict__ h,
+                                                  int n, long long omega, int* __restrict__ rowstart,
+                                                  long long* __restrict__ y, long long* __restrict__ used_out,
+                                                  int* gfront) {
+    extern __shared__ int dyn_front[];
+    __shared__ long long red[32];
+    int* front = gfront ? gfront : dyn_front;
+    int tid = threadIdx.x;
+    for (int c = tid; c <= omega; c += blockDim.x) front[c] = 0;
+    // segments of equal consecutive rows (np.split at np.diff(rows) != 0)
+    __shared__ int nseg;
+    if (tid == 0) nseg = 0;
+    __syncthreads();
+    for (int b = tid; b < n; b += blockDim.x) {
+        if (b == 0 || rows[b - 1] != rows[b]) {
+            // segments are numbered by order of appearance; rows are
+            // nondecreasing for a genuine fold so row index works as id
+            rowstart[rows[b] - rows[0]] = b;
+            atomicAdd(&nseg, 1);
+        }
+    }
+    __syncthreads();
+    int nsegs = nseg;
+    long long usedl = 0;
+    for (int r = 0; r < nsegs; r++) {
+        int b0 = rowstart[r];
+        int b1 = (r + 1 < nsegs) ? rowstart[r + 1] : n;
+        int nb = b1 - b0;
+        int G = 32;
+        while (G > 1 && G * nb > (int)blockDim.x) G >>= 1;
+        int groups = blockDim.x / G;
+        int g = tid / G, gl = tid % G;
+        for (int gbase = 0; gbase < nb; gbase += groups) {
+            int gb = gbase + g;
+            bool act = gb < nb;
+            int b = b0 + (act ? gb : 0);
+            int x = (int)xs[b], wb = act ? (int)w[b] : 0;
+            long long rest = 0;
+            for (int c = x + gl; c < x + wb; c += G) rest = max(rest, (long long)front[c]);
+            for (int o = G >> 1; o > 0; o >>= 1) {
+                long long oth = __shfl_xor_sync(0xffffffffu, rest, o, G);
+                rest = oth > rest ? oth : rest;
+            }
+            long long top = rest + h[b];
+            if (act) {
+                for (int c = x + gl; c < x + wb; c += G) front[c] = (int)top;
+                if (gl == 0) y[b] = rest;
+                usedl = top > usedl ? top : usedl;
+            }
+        }
+        __syncthreads();
+    }
+    usedl = block_max_ll(usedl, red);
+    if (tid == 0) *used_out = usedl;
+}
+
+// ---- pack_at_scale xywh output ---------------------------------------------
+__global__ void k_xywh(const long long* __restrict__ cand, const long long* __restrict__ cand_p,
+                       const int* __restrict__ cand_w, const int* __restrict__ cand_h, const int* __restrict__ cand_y,
+                       int n, long long omega, long long* __restrict__ out) {
+    if (cand[0] == 0) return;
+    int kbits = 63 - __clzll(omega);
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        long long q = cand_p[j] & (omega - 1), r = cand_p[j] >> kbits;
+        out[4 * j] = (r % FA_DIRECTION_PERIOD == 0) ? q : omega - q - cand_w[j];
+        out[4 * j + 1] = cand_y[j];
+        out[4 * j + 2] = cand_w[j];
+        out[4 * j + 3] = cand_h[j];
+    }
+}
+
+// ============================================================================
+// host launchers
+// ============================================================================
+static size_t front_smem(long long omega) { return (size_t)(omega + 1) * sizeof(int); }
+static const size_t kMaxFrontSmem = 200 * 1024;
+
+static void ensure_smem_attr() {
+    static bool done = false;
+    if (done) return;
+    cudaFuncSetAttribute(k_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxFrontSmem);
+    cudaFuncSetAttribute(k_push_up, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxFrontSmem);
+    done = true;
+}
+
+void fa_launch_orient_sort(const fa_pack_bufs& b, int n_max, const int* n_dev, long long max_h, fa_dstat* st,
+                           cudaStream_t s) {
+    k_orient_sort<<<1, SORT_THREADS, 0, s>>>(b.tw, b.th, nullptr, n_max, n_dev, max_h, b.ow, b.oh, b.rot, b.perm,
+                                              b.pinv, b.sortk, b.sortv, 0, st);
+}
+
+void fa_launch_orient_sort_mt(const long long* tw, const long long* th, const long long* mt, int n, long long max_h,
+                              long long* ow, long long* oh, unsigned char* rot, int* perm, int* pinv,
+                              unsigned long long* sk, int* sv, int reject_dups, fa_dstat* st, cudaStream_t s) {
+    k_orient_sort<<<1, SORT_THREADS, 0, s>>>(tw, th, mt, n, nullptr, max_h, ow, oh, rot, perm, pinv, sk, sv,
+                                              reject_dups, st);
+}
+
+// returns number of kernel launches
+int fa_launch_pack(const fa_pack_bufs& b, int n_max, const int* n_dev, long long omega, long long n_scales,
+                   long long min_dim, long long pad, int batch, fa_dstat* st, cudaStream_t s) {
+    ensure_smem_attr();
+    int kbits = 63 - __builtin_clzll((unsigned long long)omega);
+    bool smem_front = front_smem(omega) <= kMaxFrontSmem;
+    size_t dyn = smem_front ? front_smem(omega) : 0;
+    int launches = 0;
+    for (long long hi = n_scales; hi >= 1; hi -= batch) {
+        long long lo = hi - batch + 1;
+        if (lo < 1) lo = 1;
+        int grid = (int)(hi - lo + 1);
+        k_pack<<<grid, PK_THREADS, dyn, s>>>(b.ow, b.oh, n_max, n_dev, omega, kbits, n_scales, hi, 0, 0, min_dim, pad,
+                                             b.cand, b.cand_p, b.cand_w, b.cand_h, b.cand_y, b.rowstart,
+                                             smem_front ? nullptr : b.gfront, st);
+        launches++;
+        if (lo > 1) {
+            k_batch_done<<<1, 256, 0, s>>>(b.cand, lo, hi, st);
+            launches++;
+        }
+    }
+    k_select<<<1, 1024, 0, s>>>(b.ow, b.tw, b.th, b.chart_id, b.rot, b.perm, n_max, n_dev, omega, n_scales, min_dim,
+                                pad, b.cand, b.cand_p, b.cand_w, b.cand_h, b.cand_y, b.placements, b.accept_out, st);
+    return launches + 1;
+}
+
+void fa_launch_pack_at_scale(const long long* ow, const long long* oh, int n, long long num, long long den,
+                             long long omega, long long min_dim, long long pad, long long* cand, long long* cand_p,
+                             int* cand_w, int* cand_h, int* cand_y, int* rowstart, int* gfront, cudaStream_t s) {
+    ensure_smem_attr();
+    int kbits = 63 - __builtin_clzll((unsigned long long)omega);
+    bool smem_front = front_smem(omega) <= kMaxFrontSmem;
+    k_pack<<<1, PK_THREADS, smem_front ? front_smem(omega) : 0, s>>>(ow, oh, n, nullptr, omega, kbits, 1, 1, num, den,
+                                                                     min_dim, pad, cand, cand_p, cand_w, cand_h, cand_y,
+                                                                     rowstart, smem_front ? nullptr : gfront, nullptr);
+}
+
+void fa_launch_xywh(const long long* cand, const long long* cand_p, const int* cand_w, const int* cand_h,
+                    const int* cand_y, int n, long long omega, long long* out, cudaStream_t s) {
+    k_xywh<<<fa_grid(n, 256, FA_NUM_SMS), 256, 0, s>>>(cand, cand_p, cand_w, cand_h, cand_y, n, omega, out);
+}
+
+void fa_launch_fold(const long long* w, int n, long long omega, long long* rows, long long* x, long long* m,
+                    cudaStream_t s) {
+    k_fold<<<1, 1024, 0, s>>>(w, n, omega, rows, x, m);
+}
+
+void fa_launch_push_up_impl(const long long* rows, const long long* x, const long long* w, const long long* h, int n,
+                            long long omega, int* rowstart, long long* y, long long* used, int* gfront,
+                            cudaStream_t s) {
+    ensure_smem_attr();
+    size_t dyn = gfront ? 0 : front_smem(omega);
+    k_push_up<<<1, 1024, dyn, s>>>(rows, x, w, h, n, omega, rowstart, y, used, gfront);
+}
+
+bool fa_front_in_smem(long long omega) { return front_smem(omega) <= kMaxFrontSmem; }
+
+// orient (packing.py:109-117): rotate boxes wider than tall
+__global__ void k_orient(const long long* __restrict__ tw, const long long* __restrict__ th, int n,
+                         long long* __restrict__ ow, long long* __restrict__ oh, unsigned char* __restrict__ rot) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        long long w = tw[i], h = th[i];
+        bool r = w > h;
+        ow[i] = r ? h : w;
+        oh[i] = r ? w : h;
+        rot[i] = r;
+    }
+}
+
+void fa_launch_orient(const long long* tw, const long long* th, int n, long long* ow, long long* oh,
+                      unsigned char* rot, cudaStream_t s) {
+    k_orient<<<fa_grid(n, 256, FA_NUM_SMS * 4), 256, 0, s>>>(tw, th, n, ow, oh, rot);
+}

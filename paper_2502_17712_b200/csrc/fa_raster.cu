@@ -1,0 +1,290 @@
+// fa_raster.cu — projection, depth pre-pass and visibility pass on sm_100a.
+//
+// Reference: charts.py:269-313 (depth_prepass / mark_visible) over the
+// per-triangle clip + raster of charts.py:160-266.
+//
+// Work split (load balance): one thread per triangle computes the clip /
+// screen setup; triangles whose sample window is at most FA_SMALL_PX pixels
+// are rasterized in that thread, larger ones store their setup in a queue
+// and reserve 16x8-pixel tiles that a warp each rasterizes (4 px per lane).
+// The depth buffer holds order-preserving u64 keys of the float64 NDC depth
+// so the per-pixel minimum is a single 64-bit atomicMin in L2 (checked with
+// a plain load first).  Pass 2 revisits only triangles that covered a sample
+// in pass 1 (small list) and the stored large setups.
+#include "fa_internal.h"
+#include "fa_raster.cuh"
+
+#define FA_SMALL_PX 48
+#define TILE_W 16
+#define TILE_H 8
+
+// warp-aggregated single-slot append among the currently active lanes
+__device__ __forceinline__ int active_append1(int* counter) {
+    unsigned mask = __activemask();
+    int lane = lane_id();
+    int leader = __ffs(mask) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(counter, __popc(mask));
+    base = __shfl_sync(mask, base, leader);
+    return base + __popc(mask & ((1u << lane) - 1u));
+}
+
+// ---- frame init: projection + buffer clears ------------------------------
+__global__ void k_frame_init(const double* __restrict__ pos, int V, const double* __restrict__ vp_dev,
+                             double4* __restrict__ clip,
+                             int* __restrict__ vmin, unsigned long long* __restrict__ depth, long long npx,
+                             unsigned int* __restrict__ flags32, int nflag32) {
+    long long stride = (long long)gridDim.x * blockDim.x;
+    long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double m[16];
+#pragma unroll
+    for (int i = 0; i < 16; i++) m[i] = __ldg(vp_dev + i);
+    for (long long v = i0; v < V; v += stride) {
+        double x = pos[3 * v], y = pos[3 * v + 1], z = pos[3 * v + 2];
+        clip[v] = project_point(x, y, z, m);
+        if (vmin) vmin[v] = 0x7fffffff;
+    }
+    if (depth) {
+        ulonglong2* d2 = reinterpret_cast<ulonglong2*>(depth);
+        long long n2 = npx >> 1;
+        for (long long i = i0; i < n2; i += stride) d2[i] = make_ulonglong2(FA_KEY_POS_INF, FA_KEY_POS_INF);
+        if ((npx & 1) && i0 == 0) depth[npx - 1] = FA_KEY_POS_INF;
+    }
+    if (flags32)
+        for (long long i = i0; i < nflag32; i += stride) flags32[i] = 0u;
+}
+
+// keys -> float64 depth (debug / standalone depth_prepass output)
+__global__ void k_decode_depth(const unsigned long long* __restrict__ keys, double* __restrict__ out, long long n) {
+    long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = key_f64(keys[i]);
+}
+
+// float64 depth -> keys (standalone mark_visible input)
+__global__ void k_encode_depth(const double* __restrict__ in, unsigned long long* __restrict__ keys, long long n) {
+    long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) keys[i] = f64_key(in[i]);
+}
+
+// ---- pass 1: setup + small raster + large enqueue -------------------------
+// WRITE_DEPTH=false builds the work lists only (standalone mark_visible).
+template <bool WRITE_DEPTH>
+__global__ void __launch_bounds__(256) k_raster_setup(const double4* __restrict__ clip, const int* __restrict__ tris,
+                                                      int T, int W, int H, int cull,
+                                                      unsigned long long* __restrict__ depth,
+                                                      int* __restrict__ small_list, TriSetup* __restrict__ large,
+                                                      int max_large, int2* __restrict__ tiles, int max_tiles,
+                                                      fa_dstat* __restrict__ st) {
+    long long frags = 0;
+    int stride = gridDim.x * blockDim.x;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += stride) {
+        TriSetup s;
+        int r = tri_setup(clip, tris, t, W, H, cull != 0, s);
+        if (r < 0) { atomicOr(&st->flags, FA_DFLAG_POLY_OVERFLOW); continue; }
+        if (r == 0) continue;
+        int bw = s.max_x - s.min_x + 1, bh = s.max_y - s.min_y + 1;
+        if (bw * bh <= FA_SMALL_PX) {
+            bool covered = false;
+            for (int iy = s.min_y; iy <= s.max_y; iy++) {
+                double py = (double)iy + 0.5;
+                for (int ix = s.min_x; ix <= s.max_x; ix++) {
+                    double px = (double)ix + 0.5;
+                    if (!sample_inside(s, px, py)) continue;
+                    covered = true;
+                    if (WRITE_DEPTH) {
+                        unsigned long long key = f64_key(sample_depth(s, px, py));
+                        unsigned long long* d = depth + (long long)iy * W + ix;
+                        if (key < *d) {
+                            unsigned long long old = atomicMin(d, key);
+                            if (old == FA_KEY_POS_INF && key < old) frags++;
+                        }
+                    } else {
+                        break;
+                    }
+                }
+                if (!WRITE_DEPTH && covered) break;
+            }
+            if (covered) {
+                int slot = active_append1(&st->n_small);
+                small_list[slot] = t;
+            }
+        } else {
+            int slot = active_append1(&st->n_large);
+            if (slot >= max_large) { atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW); continue; }
+            large[slot] = s;
+            int tx = (bw + TILE_W - 1) / TILE_W, ty = (bh + TILE_H - 1) / TILE_H;
+            int nt = tx * ty;
+            int base = atomicAdd(&st->n_tiles, nt);
+            // on overflow write the part that fits (no unwritten records below
+            // capacity) and flag the frame; the host grows the queue and reruns
+            int end = base + nt;
+            if (end > max_tiles) { atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW); end = max_tiles; }
+            for (int k = base; k < end; k++) tiles[k] = make_int2(slot, k - base);
+        }
+    }
+    if (WRITE_DEPTH) {
+        frags = warp_sum(frags);
+        if (lane_id() == 0 && frags) atomicAdd((unsigned long long*)&st->screen_fragments, (unsigned long long)frags);
+    }
+}
+
+// copy one TriSetup into warp-private shared memory
+__device__ __forceinline__ void load_setup_warp(const TriSetup* __restrict__ g, TriSetup* sm) {
+    const int nwords = sizeof(TriSetup) / 8;
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(g);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(sm);
+    for (int i = lane_id(); i < nwords; i += 32) dst[i] = __ldg(src + i);
+    __syncwarp();
+}
+
+// ---- pass 1 large: one warp per 16x8 tile --------------------------------
+__global__ void __launch_bounds__(256) k_raster_depth_tiles(const TriSetup* __restrict__ large,
+                                                            const int2* __restrict__ tiles, int W,
+                                                            unsigned long long* __restrict__ depth,
+                                                            fa_dstat* __restrict__ st, int max_tiles) {
+    __shared__ TriSetup sm[8];
+    int warp = threadIdx.x >> 5, lane = lane_id();
+    int nwarps = gridDim.x * 8;
+    int n_tiles = min(st->n_tiles, max_tiles);
+    long long frags = 0;
+    for (int w = blockIdx.x * 8 + warp; w < n_tiles; w += nwarps) {
+        int2 rec = tiles[w];
+        __syncwarp();
+        load_setup_warp(large + rec.x, &sm[warp]);
+        const TriSetup& s = sm[warp];
+        int bw = s.max_x - s.min_x + 1;
+        int tx = (bw + TILE_W - 1) / TILE_W;
+        int x = s.min_x + (rec.y % tx) * TILE_W + (lane & 15);
+        int y0 = s.min_y + (rec.y / tx) * TILE_H + (lane >> 4);
+        if (x <= s.max_x) {
+            double px = (double)x + 0.5;
+            for (int k = 0; k < TILE_H / 2; k++) {
+                int y = y0 + 2 * k;
+                if (y > s.max_y) break;
+                double py = (double)y + 0.5;
+                if (!sample_inside(s, px, py)) continue;
+                unsigned long long key = f64_key(sample_depth(s, px, py));
+                unsigned long long* d = depth + (long long)y * W + x;
+                if (key < *d) {
+                    unsigned long long old = atomicMin(d, key);
+                    if (old == FA_KEY_POS_INF && key < old) frags++;
+                }
+            }
+        }
+    }
+    frags = warp_sum(frags);
+    if (lane == 0 && frags) atomicAdd((unsigned long long*)&st->screen_fragments, (unsigned long long)frags);
+}
+
+// ---- pass 2 small: one thread per covering triangle -----------------------
+__global__ void __launch_bounds__(256) k_raster_vis_small(const double4* __restrict__ clip, const int* __restrict__ tris,
+                                                          const int* __restrict__ small_list, int W, int H, int cull,
+                                                          const unsigned long long* __restrict__ depth,
+                                                          unsigned char* __restrict__ flags,
+                                                          const fa_dstat* __restrict__ st) {
+    int n = st->n_small;
+    int stride = gridDim.x * blockDim.x;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        int t = small_list[i];
+        TriSetup s;
+        if (tri_setup(clip, tris, t, W, H, cull != 0, s) <= 0) continue;
+        bool vis = false;
+        for (int iy = s.min_y; iy <= s.max_y && !vis; iy++) {
+            double py = (double)iy + 0.5;
+            for (int ix = s.min_x; ix <= s.max_x; ix++) {
+                double px = (double)ix + 0.5;
+                if (!sample_inside(s, px, py)) continue;
+                double z = sample_depth(s, px, py);
+                double stored = key_f64(depth[(long long)iy * W + ix]);
+                if (depth_passes(z, stored)) { vis = true; break; }
+            }
+        }
+        if (vis) flags[t] = 1;
+    }
+}
+
+// ---- pass 2 large: one warp per tile --------------------------------------
+__global__ void __launch_bounds__(256) k_raster_vis_tiles(const TriSetup* __restrict__ large,
+                                                          const int2* __restrict__ tiles, int W,
+                                                          const unsigned long long* __restrict__ depth,
+                                                          unsigned char* __restrict__ flags,
+                                                          const fa_dstat* __restrict__ st, int max_tiles) {
+    __shared__ TriSetup sm[8];
+    int warp = threadIdx.x >> 5, lane = lane_id();
+    int nwarps = gridDim.x * 8;
+    int n_tiles = min(st->n_tiles, max_tiles);
+    for (int w = blockIdx.x * 8 + warp; w < n_tiles; w += nwarps) {
+        int2 rec = tiles[w];
+        int t = __ldg(&large[rec.x].tri);
+        int seen = 0;
+        if (lane == 0) seen = *(volatile unsigned char*)(flags + t);
+        if (__shfl_sync(0xffffffffu, seen, 0)) continue;  // already visible (warp-uniform)
+        __syncwarp();
+        load_setup_warp(large + rec.x, &sm[warp]);
+        const TriSetup& s = sm[warp];
+        int bw = s.max_x - s.min_x + 1;
+        int tx = (bw + TILE_W - 1) / TILE_W;
+        int x = s.min_x + (rec.y % tx) * TILE_W + (lane & 15);
+        int y0 = s.min_y + (rec.y / tx) * TILE_H + (lane >> 4);
+        bool vis = false;
+        if (x <= s.max_x) {
+            double px = (double)x + 0.5;
+            for (int k = 0; k < TILE_H / 2; k++) {
+                int y = y0 + 2 * k;
+                if (y > s.max_y) break;
+                double py = (double)y + 0.5;
+                if (!sample_inside(s, px, py)) continue;
+                double z = sample_depth(s, px, py);
+                double stored = key_f64(depth[(long long)y * W + x]);
+                if (depth_passes(z, stored)) { vis = true; break; }
+            }
+        }
+        if (__any_sync(0xffffffffu, vis) && lane == 0) flags[t] = 1;
+    }
+}
+
+// ---- host launchers -------------------------------------------------------
+void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* clip, int* vmin,
+                          unsigned long long* depth, long long npx, unsigned char* flags, int T,
+                          cudaStream_t s) {
+    long long work = V;
+    if (depth && npx / 2 > work) work = npx / 2;
+    int nflag32 = flags ? (T + 3) / 4 : 0;
+    if (nflag32 > work) work = nflag32;
+    k_frame_init<<<fa_grid(work, 256, FA_NUM_SMS * 8), 256, 0, s>>>(
+        pos, V, vp, clip, vmin, depth, npx, reinterpret_cast<unsigned int*>(flags), nflag32);
+}
+
+void fa_launch_raster_setup(bool write_depth, const double4* clip, const int* tris, int T, int W, int H, int cull,
+                            unsigned long long* depth, int* small_list, TriSetup* large, int max_large, int2* tiles,
+                            int max_tiles, fa_dstat* st, cudaStream_t s) {
+    int grid = fa_grid(T, 256, FA_NUM_SMS * 16);
+    if (write_depth)
+        k_raster_setup<true><<<grid, 256, 0, s>>>(clip, tris, T, W, H, cull, depth, small_list, large, max_large,
+                                                  tiles, max_tiles, st);
+    else
+        k_raster_setup<false><<<grid, 256, 0, s>>>(clip, tris, T, W, H, cull, depth, small_list, large, max_large,
+                                                   tiles, max_tiles, st);
+}
+
+void fa_launch_raster_depth_tiles(const TriSetup* large, const int2* tiles, int max_tiles, int W,
+                                  unsigned long long* depth, fa_dstat* st, cudaStream_t s) {
+    k_raster_depth_tiles<<<FA_NUM_SMS * 8, 256, 0, s>>>(large, tiles, W, depth, st, max_tiles);
+}
+
+void fa_launch_raster_vis(const double4* clip, const int* tris, const int* small_list, const TriSetup* large,
+                          const int2* tiles, int max_tiles, int T, int W, int H, int cull,
+                          const unsigned long long* depth, unsigned char* flags, const fa_dstat* st,
+                          cudaStream_t s) {
+    k_raster_vis_small<<<fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s>>>(clip, tris, small_list, W, H, cull, depth,
+                                                                       flags, st);
+    k_raster_vis_tiles<<<FA_NUM_SMS * 8, 256, 0, s>>>(large, tiles, W, depth, flags, st, max_tiles);
+}
+
+void fa_launch_decode_depth(const unsigned long long* keys, double* out, long long n, cudaStream_t s) {
+    k_decode_depth<<<fa_grid(n, 256, FA_NUM_SMS * 8), 256, 0, s>>>(keys, out, n);
+}
+
+void fa_launch_encode_depth(const double* in, unsigned long long* keys, long long n, cudaStream_t s) {
+    k_encode_depth<<<fa_grid(n, 256, FA_NUM_SMS * 8), 256, 0, s>>>(in, keys, n);
+}

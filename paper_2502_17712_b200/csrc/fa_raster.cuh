@@ -1,0 +1,262 @@
+// fa_raster.cuh — per-triangle raster setup shared by the depth and
+// visibility passes.  Restates charts.py:160-266 with identical float64
+// operation order (compiled with -fmad=false).
+#pragma once
+#include "fa_common.cuh"
+
+#define FA_SETUP_MAXV 12   // stored-setup polygon capacity (convex max is 10)
+
+struct TriSetup {
+    int tri;
+    int n;
+    int min_x, max_x, min_y, max_y;
+    int use_plane;
+    int incl_mask;
+    double p0x, p0y, p0z, gx, gy, zmean;
+    double ex[FA_SETUP_MAXV], ey[FA_SETUP_MAXV], edx[FA_SETUP_MAXV], edy[FA_SETUP_MAXV];
+};
+
+struct Poly4 {
+    double v[FA_MAXV][4];
+    int n;
+};
+
+// charts.py:178-189 — keep d >= 0; returns false on capacity overflow
+__device__ __forceinline__ bool clip_halfspace_ge(const Poly4& in, const double* d, Poly4& out) {
+    int n = in.n, m = 0;
+    for (int i = 0; i < n; i++) {
+        int j = (i + 1 == n) ? 0 : i + 1;
+        double da = d[i], db = d[j];
+        if (da >= 0) {
+            if (m >= FA_MAXV) return false;
+            out.v[m][0] = in.v[i][0]; out.v[m][1] = in.v[i][1];
+            out.v[m][2] = in.v[i][2]; out.v[m][3] = in.v[i][3];
+            m++;
+        }
+        if ((da >= 0) != (db >= 0)) {
+            double t = __ddiv_rn(da, __dsub_rn(da, db));
+            if (m >= FA_MAXV) return false;
+#pragma unroll
+            for (int k = 0; k < 4; k++)
+                out.v[m][k] = __dadd_rn(in.v[i][k], __dmul_rn(t, __dsub_rn(in.v[j][k], in.v[i][k])));
+            m++;
+        }
+    }
+    out.n = m;
+    return true;
+}
+
+// charts.py:160-175 (slow path: some plane clips).  Returns false on overflow.
+static __device__ __noinline__ bool clip_triangle_frustum_slow(const double4 c0, const double4 c1, const double4 c2,
+                                                        Poly4& out) {
+    Poly4 tmp;
+    double d[FA_MAXV];
+    Poly4* cur = &out;
+    Poly4* nxt = &tmp;
+    cur->n = 3;
+    cur->v[0][0] = c0.x; cur->v[0][1] = c0.y; cur->v[0][2] = c0.z; cur->v[0][3] = c0.w;
+    cur->v[1][0] = c1.x; cur->v[1][1] = c1.y; cur->v[1][2] = c1.z; cur->v[1][3] = c1.w;
+    cur->v[2][0] = c2.x; cur->v[2][1] = c2.y; cur->v[2][2] = c2.z; cur->v[2][3] = c2.w;
+    bool any_pos = false, any_nonpos = false;
+    for (int i = 0; i < 3; i++) {
+        d[i] = __dsub_rn(cur->v[i][3], FA_W_EPSILON);
+        if (d[i] > 0) any_pos = true;
+        if (d[i] <= 0) any_nonpos = true;
+    }
+    if (!any_pos) { out.n = 0; return true; }
+    if (any_nonpos) {
+        if (!clip_halfspace_ge(*cur, d, *nxt)) return false;
+        Poly4* t = cur; cur = nxt; nxt = t;
+    }
+    for (int p = 0; p < 6; p++) {
+        if (cur->n == 0) break;
+        int axis = p >> 1;
+        bool neg = p & 1;
+        bool all_ge = true;
+        for (int i = 0; i < cur->n; i++) {
+            double c = cur->v[i][axis];
+            d[i] = neg ? __dsub_rn(cur->v[i][3], c) : __dadd_rn(cur->v[i][3], c);
+            if (!(d[i] >= 0)) all_ge = false;
+        }
+        if (all_ge) continue;
+        if (!clip_halfspace_ge(*cur, d, *nxt)) return false;
+        Poly4* t = cur; cur = nxt; nxt = t;
+    }
+    if (cur != &out) {
+        out.n = cur->n;
+        for (int i = 0; i < cur->n; i++)
+            for (int k = 0; k < 4; k++) out.v[i][k] = cur->v[i][k];
+    }
+    return true;
+}
+
+// OpenBLAS SkylakeX strided ddot (charts.py:253)
+__device__ __forceinline__ double ddot_ob(const double* x, const double* y, int n) {
+    double t1 = 0.0, t2 = 0.0;
+    int i = 0, n1 = n & -4;
+    for (; i < n1; i += 4) {
+        double m3 = __dmul_rn(y[i + 2], x[i + 2]);
+        double m4 = __dmul_rn(y[i + 3], x[i + 3]);
+        t1 = __dadd_rn(t1, __fma_rn(y[i], x[i], m3));
+        t2 = __dadd_rn(t2, __fma_rn(y[i + 1], x[i + 1], m4));
+    }
+    for (; i < n; i++) t1 = __fma_rn(y[i], x[i], t1);
+    return __dadd_rn(t1, t2);
+}
+
+__device__ __forceinline__ double screen_x(double c, double w, int W) {
+    double n = __ddiv_rn(c, w);
+    return __dmul_rn(__dmul_rn(__dadd_rn(n, 1.0), 0.5), (double)W);
+}
+
+// Finish a setup from screen-space polygon (x,y,z arrays of n vertices):
+// signed area / cull / flip, bbox, edges, depth plane.  charts.py:205-266.
+// Returns 1 = samples possible, 0 = none, -1 = setup capacity overflow.
+__device__ __forceinline__ int finish_setup(double* sx, double* sy, double* sz, int n, int W, int H,
+                                            bool cull, TriSetup& s) {
+    double ry[FA_MAXV], rx[FA_MAXV];
+    for (int i = 0; i < n; i++) {
+        int j = (i + 1 == n) ? 0 : i + 1;
+        ry[i] = sy[j];
+        rx[i] = sx[j];
+    }
+    double area2 = __dsub_rn(ddot_ob(sx, ry, n), ddot_ob(sy, rx, n));
+    if (area2 == 0.0) return 0;
+    if (area2 < 0.0) {
+        if (cull) return 0;
+        for (int i = 0; i < n / 2; i++) {
+            double t;
+            t = sx[i]; sx[i] = sx[n - 1 - i]; sx[n - 1 - i] = t;
+            t = sy[i]; sy[i] = sy[n - 1 - i]; sy[n - 1 - i] = t;
+            t = sz[i]; sz[i] = sz[n - 1 - i]; sz[n - 1 - i] = t;
+        }
+    }
+    double mnx = sx[0], mxx = sx[0], mny = sy[0], mxy = sy[0];
+    for (int i = 1; i < n; i++) {
+        mnx = sx[i] < mnx ? sx[i] : mnx;
+        mxx = sx[i] > mxx ? sx[i] : mxx;
+        mny = sy[i] < mny ? sy[i] : mny;
+        mxy = sy[i] > mxy ? sy[i] : mxy;
+    }
+    long long fx = (long long)floor(__dsub_rn(mnx, 0.5)), cx = (long long)ceil(mxx);
+    long long fy = (long long)floor(__dsub_rn(mny, 0.5)), cy = (long long)ceil(mxy);
+    s.min_x = fx > 0 ? (int)fx : 0;
+    s.max_x = cx < W - 1 ? (int)cx : W - 1;
+    s.min_y = fy > 0 ? (int)fy : 0;
+    s.max_y = cy < H - 1 ? (int)cy : H - 1;
+    if (s.min_x > s.max_x || s.min_y > s.max_y) return 0;
+    if (n > FA_SETUP_MAXV) return -1;
+    s.n = n;
+    int mask = 0;
+    for (int i = 0; i < n; i++) {
+        int j = (i + 1 == n) ? 0 : i + 1;
+        double dx = __dsub_rn(sx[j], sx[i]);
+        double dy = __dsub_rn(sy[j], sy[i]);
+        s.ex[i] = sx[i];
+        s.ey[i] = sy[i];
+        s.edx[i] = dx;
+        s.edy[i] = dy;
+        if (dy > 0 || (dy == 0 && dx < 0)) mask |= 1 << i;
+    }
+    s.incl_mask = mask;
+    s.use_plane = 0;
+    double p0x = sx[0], p0y = sy[0], p0z = sz[0];
+    for (int j = 1; j < n - 1; j++) {
+        double a1x = __dsub_rn(sx[j], p0x), a1y = __dsub_rn(sy[j], p0y), a1z = __dsub_rn(sz[j], p0z);
+        double a2x = __dsub_rn(sx[j + 1], p0x), a2y = __dsub_rn(sy[j + 1], p0y), a2z = __dsub_rn(sz[j + 1], p0z);
+        double det = __dsub_rn(__dmul_rn(a1x, a2y), __dmul_rn(a2x, a1y));
+        if (fabs(det) > 1e-12) {
+            s.gx = __ddiv_rn(__dsub_rn(__dmul_rn(a1z, a2y), __dmul_rn(a2z, a1y)), det);
+            s.gy = __ddiv_rn(__dsub_rn(__dmul_rn(a2z, a1x), __dmul_rn(a1z, a2x)), det);
+            s.p0x = p0x; s.p0y = p0y; s.p0z = p0z;
+            s.use_plane = 1;
+            break;
+        }
+    }
+    if (!s.use_plane) {
+        // numpy pairwise mean (charts.py:266)
+        double res;
+        if (n < 8) {
+            res = -0.0;
+            for (int i = 0; i < n; i++) res = __dadd_rn(res, sz[i]);
+        } else {
+            double r[8];
+            int i;
+            for (i = 0; i < 8; i++) r[i] = sz[i];
+            for (i = 8; i < n - (n % 8); i += 8)
+                for (int k = 0; k < 8; k++) r[k] = __dadd_rn(r[k], sz[i + k]);
+            res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                            __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+            for (; i < n; i++) res = __dadd_rn(res, sz[i]);
+        }
+        s.zmean = __ddiv_rn(res, (double)n);
+    }
+    return 1;
+}
+
+// Full per-triangle setup (charts.py:269-282 for one triangle).
+// Returns 1 when the triangle yields a non-empty sample window, 0 otherwise,
+// -1 on polygon-capacity overflow.
+__device__ __forceinline__ int tri_setup(const double4* __restrict__ clip, const int* __restrict__ tris,
+                                         int t, int W, int H, bool cull, TriSetup& s) {
+    int ia = __ldg(tris + 3 * t), ib = __ldg(tris + 3 * t + 1), ic = __ldg(tris + 3 * t + 2);
+    double4 c0 = ldg4(clip + ia), c1 = ldg4(clip + ib), c2 = ldg4(clip + ic);
+    double sx[FA_MAXV], sy[FA_MAXV], sz[FA_MAXV];
+    int n;
+    // fast path: every vertex strictly in front and inside all six planes,
+    // so _clip_triangle_frustum returns the triangle unchanged
+    bool inside =
+        __dsub_rn(c0.w, FA_W_EPSILON) > 0 && __dsub_rn(c1.w, FA_W_EPSILON) > 0 && __dsub_rn(c2.w, FA_W_EPSILON) > 0 &&
+        __dadd_rn(c0.w, c0.x) >= 0 && __dsub_rn(c0.w, c0.x) >= 0 && __dadd_rn(c0.w, c0.y) >= 0 &&
+        __dsub_rn(c0.w, c0.y) >= 0 && __dadd_rn(c0.w, c0.z) >= 0 && __dsub_rn(c0.w, c0.z) >= 0 &&
+        __dadd_rn(c1.w, c1.x) >= 0 && __dsub_rn(c1.w, c1.x) >= 0 && __dadd_rn(c1.w, c1.y) >= 0 &&
+        __dsub_rn(c1.w, c1.y) >= 0 && __dadd_rn(c1.w, c1.z) >= 0 && __dsub_rn(c1.w, c1.z) >= 0 &&
+        __dadd_rn(c2.w, c2.x) >= 0 && __dsub_rn(c2.w, c2.x) >= 0 && __dadd_rn(c2.w, c2.y) >= 0 &&
+        __dsub_rn(c2.w, c2.y) >= 0 && __dadd_rn(c2.w, c2.z) >= 0 && __dsub_rn(c2.w, c2.z) >= 0;
+    if (inside) {
+        n = 3;
+        sx[0] = screen_x(c0.x, c0.w, W); sy[0] = screen_x(c0.y, c0.w, H); sz[0] = __ddiv_rn(c0.z, c0.w);
+        sx[1] = screen_x(c1.x, c1.w, W); sy[1] = screen_x(c1.y, c1.w, H); sz[1] = __ddiv_rn(c1.z, c1.w);
+        sx[2] = screen_x(c2.x, c2.w, W); sy[2] = screen_x(c2.y, c2.w, H); sz[2] = __ddiv_rn(c2.z, c2.w);
+    } else {
+        // reject early when no vertex is in front (charts.py:163-165)
+        if (!(__dsub_rn(c0.w, FA_W_EPSILON) > 0 || __dsub_rn(c1.w, FA_W_EPSILON) > 0 ||
+              __dsub_rn(c2.w, FA_W_EPSILON) > 0))
+            return 0;
+        Poly4 p;
+        if (!clip_triangle_frustum_slow(c0, c1, c2, p)) return -1;
+        if (p.n < 3) return 0;
+        n = p.n;
+        for (int i = 0; i < n; i++) {
+            sx[i] = screen_x(p.v[i][0], p.v[i][3], W);
+            sy[i] = screen_x(p.v[i][1], p.v[i][3], H);
+            sz[i] = __ddiv_rn(p.v[i][2], p.v[i][3]);
+        }
+    }
+    int r = finish_setup(sx, sy, sz, n, W, H, cull, s);
+    if (r <= 0) return r;
+    s.tri = t;
+    return 1;
+}
+
+__device__ __forceinline__ bool sample_inside(const TriSetup& s, double px, double py) {
+    for (int i = 0; i < s.n; i++) {
+        double e = __dsub_rn(__dmul_rn(s.edx[i], __dsub_rn(py, s.ey[i])), __dmul_rn(s.edy[i], __dsub_rn(px, s.ex[i])));
+        bool ok = ((s.incl_mask >> i) & 1) ? (e >= 0) : (e > 0);
+        if (!ok) return false;
+    }
+    return true;
+}
+
+__device__ __forceinline__ double sample_depth(const TriSetup& s, double px, double py) {
+    if (s.use_plane)
+        return __dadd_rn(__dadd_rn(s.p0z, __dmul_rn(s.gx, __dsub_rn(px, s.p0x))), __dmul_rn(s.gy, __dsub_rn(py, s.p0y)));
+    return s.zmean;
+}
+
+// charts.py:309-311: z <= stored + 1e-6 * max(1, |stored|)
+__device__ __forceinline__ bool depth_passes(double z, double stored) {
+    double a = fabs(stored);
+    double slack = __dmul_rn(FA_DEPTH_EPSILON, 1.0 > a ? 1.0 : a);
+    return z <= __dadd_rn(stored, slack);
+}

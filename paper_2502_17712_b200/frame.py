@@ -1,0 +1,173 @@
+"""Resident per-frame atlas engine: run_scene_pipeline (cli.py:360-406) as
+one CUDA-graph replay per frame.
+
+A `FrameEngine` binds one mesh to one device context.  Each frame uploads
+only the 4x4 camera matrix, replays the captured kernel graph
+(project -> depth pass -> visibility pass -> visible compaction ->
+union-find charts -> per-chart bounds -> box dims -> radix order ->
+64-candidate pack -> selection -> UVs) and exposes the outputs as zero-copy
+device tensors.  Reference-typed objects (ChartSet dicts, Placement tuples,
+NdcBox dicts) are materialised lazily, outside any timed region.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from fractions import Fraction
+
+import numpy as np
+
+from . import _native as nat
+from .charts import ChartSet, Mesh
+from .geometry import NdcBox
+from .packing import AtlasLayout, ChartBox, placements_from_array
+
+
+@dataclass
+class FrameSettings:
+    screen: tuple = (1920, 1080)
+    omega: int = 2048
+    n_scales: int = 64
+    min_dim: int = 1
+    padding: int = 0
+    prescale: float = 1.0
+    backface_cull: bool = True
+    uv_f64: bool = False
+    want_depth: bool = False
+    use_graph: bool = True
+
+    def params(self) -> nat.FrameParams:
+        p = nat.FrameParams()
+        p.width, p.height = int(self.screen[0]), int(self.screen[1])
+        p.omega, p.n_scales = int(self.omega), int(self.n_scales)
+        p.min_dim, p.padding = int(self.min_dim), int(self.padding)
+        p.prescale = float(self.prescale)
+        p.backface_cull = int(bool(self.backface_cull))
+        p.uv_f64 = int(bool(self.uv_f64))
+        p.want_depth = int(bool(self.want_depth))
+        p.use_graph = int(bool(self.use_graph))
+        return p
+
+
+class FrameOutput:
+    """Device views of one frame's results (valid until the engine's next frame)."""
+
+    def __init__(self, res: nat.FrameResult, settings: FrameSettings, T: int, V: int, device):
+        self.status = int(res.status)
+        self.n_visible = int(res.n_visible)
+        self.n_charts = int(res.n_charts)
+        self.scale = Fraction(int(res.scale_num), int(res.scale_den)) if res.scale_den else None
+        self.screen_fragments = int(res.screen_fragments)
+        self.texels_allocated = int(res.texels_allocated)
+        self.settings = settings
+        C, nv = self.n_charts, self.n_visible
+        W, H = settings.screen
+        v = nat.device_view
+        self.flags = v(res.flags, (T,), np.uint8, device)
+        self.visible = v(res.visible, (nv,), np.int32, device)
+        self.chart_of_triangle = v(res.chart_of_triangle, (T,), np.int32, device)
+        self.vertex_to_chart = v(res.vertex_to_chart, (V,), np.int32, device)
+        self.roots = v(res.roots, (C,), np.int32, device)
+        self.ndc = v(res.ndc, (C, 4), np.float64, device)
+        self.px = v(res.px, (C, 2), np.int32, device)
+        self.target = v(res.target, (C, 2), np.int64, device)
+        self.placements = v(res.placements, (C, 8), np.int64, device)
+        self.uv = v(res.uv, (nv, 6), np.float64 if settings.uv_f64 else np.float32, device)
+        self.depth = v(res.depth, (H, W), np.float64, device) if settings.want_depth and res.depth else None
+
+    # tensors that a caller may want to keep past the next frame
+    TENSORS = ("flags", "visible", "chart_of_triangle", "vertex_to_chart", "roots", "ndc", "px", "target",
+               "placements", "uv", "depth")
+
+    def clone(self) -> "FrameOutput":
+        out = object.__new__(FrameOutput)
+        out.__dict__.update(self.__dict__)
+        for k in self.TENSORS:
+            t = getattr(self, k)
+            setattr(out, k, None if t is None else t.clone())
+        return out
+
+    def to_host(self) -> dict:
+        d = {k: (None if getattr(self, k) is None else getattr(self, k).cpu().numpy()) for k in self.TENSORS}
+        d.update(status=self.status, n_visible=self.n_visible, n_charts=self.n_charts, scale=self.scale,
+                 screen_fragments=self.screen_fragments, texels_allocated=self.texels_allocated)
+        return d
+
+    # -- reference-typed views (materialised on demand) --------------------
+    def chart_set(self) -> ChartSet:
+        return ChartSet(self.chart_of_triangle.cpu().numpy().astype(np.int64),
+                        vertex_chart_array=self.vertex_to_chart.cpu().numpy().astype(np.int64))
+
+    def boxes(self) -> list:
+        r = self.roots.cpu().numpy()
+        t = self.target.cpu().numpy()
+        return [ChartBox(target_w=int(t[i, 0]), target_h=int(t[i, 1]), chart_id=int(r[i]), min_tri=int(r[i]))
+                for i in range(len(r))]
+
+    def layout(self) -> AtlasLayout:
+        return AtlasLayout(omega=int(self.settings.omega), scale=self.scale,
+                           placements=placements_from_array(self.placements.cpu().numpy()))
+
+    def chart_ndc(self) -> dict:
+        r = self.roots.cpu().numpy()
+        b = self.ndc.cpu().numpy()
+        return {int(r[i]): NdcBox(*map(float, b[i])) for i in range(len(r))}
+
+    def chart_px(self) -> dict:
+        r = self.roots.cpu().numpy()
+        p = self.px.cpu().numpy()
+        return {int(r[i]): (int(p[i, 0]), int(p[i, 1])) for i in range(len(r))}
+
+
+class FrameEngine:
+    """One mesh resident on one GPU; `run(camera)` produces one atlas."""
+
+    def __init__(self, mesh: Mesh, device: int | None = None, settings: FrameSettings | None = None):
+        torch = nat.require_device()
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.ctx = nat.Context(self.device)  # private context: outputs survive other API calls
+        self.mesh = mesh
+        self.pos, self.tris = mesh.device_arrays(self.ctx.torch_device)
+        self.ctx.set_mesh(self.pos, self.tris)
+        self.settings = settings or FrameSettings()
+        self._res = nat.FrameResult()
+
+    @property
+    def n_triangles(self) -> int:
+        return self.mesh.n_triangles
+
+    def launch(self, view_proj, settings: FrameSettings | None = None, stream=None) -> None:
+        """Enqueue one frame (asynchronous)."""
+        s = settings or self.settings
+        self._last_settings = s
+        vp = nat.vp_host(view_proj)
+        self._params = s.params()
+        st = ctypes.c_void_p(stream.cuda_stream) if stream is not None else self.ctx.stream_ptr()
+        self._stream = st
+        self.ctx.set_mesh(self.pos, self.tris)
+        nat.raise_for_status(self.ctx.L.fa_frame_launch(self.ctx.h, vp.ctypes.data_as(ctypes.c_void_p),
+                                                        ctypes.byref(self._params), st))
+
+    def finish(self, check: bool = True) -> FrameOutput:
+        """Wait for the launched frame; raise the reference exception on failure."""
+        code = self.ctx.L.fa_frame_finish(self.ctx.h, ctypes.byref(self._res), self._stream)
+        if check:
+            nat.raise_for_status(code)
+        return FrameOutput(self._res, self._last_settings, self.mesh.n_triangles, len(self.mesh.positions),
+                           self.ctx.torch_device)
+
+    def run(self, view_proj, settings: FrameSettings | None = None, stream=None, check: bool = True) -> FrameOutput:
+        for _ in range(4):
+            self.launch(view_proj, settings, stream)
+            code = self.ctx.L.fa_frame_finish(self.ctx.h, ctypes.byref(self._res), self._stream)
+            if code == nat.FA_INTERNAL_ERROR and "rerun" in nat.last_error():
+                continue
+            if check:
+                nat.raise_for_status(code)
+            return FrameOutput(self._res, self._last_settings, self.mesh.n_triangles, len(self.mesh.positions),
+                               self.ctx.torch_device)
+        raise RuntimeError("frame work queues kept overflowing")
+
+    def launch_count(self) -> int:
+        return int(self.ctx.L.fa_last_launch_count(self.ctx.h))
