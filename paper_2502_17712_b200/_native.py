@@ -21,7 +21,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfastatlas.so")
+LIB_PATH = os.environ.get("FASTATLAS_LIB") or os.path.join(_HERE, "libfastatlas.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 FA_OK = 0

@@ -97,6 +97,7 @@ void fa_launch_compact_visible(const unsigned char* flags, int T, int* blocks, i
 
 // ---- union-find ---------------------------------------------------------------
 // parent[x] <= x always holds; find with pointer jumping (ECL-CC style)
+// (only while hooking: every jump keeps a node inside its own set)
 __device__ __forceinline__ int uf_find(int* parent, int x) {
     volatile int* p = parent;
     int cur = p[x];
@@ -108,6 +109,16 @@ __device__ __forceinline__ int uf_find(int* parent, int x) {
             cur = next;
         }
     }
+    return cur;
+}
+
+// Read-only find for the flatten pass.  Pointer jumping must not run there:
+// a jump computed from a stale read can overwrite a label another thread
+// has already finalised with an intermediate (non-root) ancestor.
+__device__ __forceinline__ int uf_find_ro(const int* parent, int x) {
+    const volatile int* p = parent;
+    int cur = x, next;
+    while (cur > (next = p[cur])) cur = next;
     return cur;
 }
 
@@ -180,7 +191,7 @@ __global__ void k_compress(const int* __restrict__ vis_list, int* label, const f
     int stride = gridDim.x * blockDim.x;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
         int t = vis_list[k];
-        label[t] = uf_find(label, t);
+        label[t] = uf_find_ro(label, t);
     }
 }
 

@@ -237,6 +237,11 @@ __global__ void __launch_bounds__(SORT_THREADS) k_orient_sort(const long long* _
     __syncthreads();
     int mpasses = mfield / 8;
     int passes = mpasses + (hbits + 7) / 8;
+    if (mt && reject_dups && mpasses == 0 && n > 1) {
+        // every min_tri equal: duplicates (packing.py:319-323)
+        if (tid == 0) atomicOr(&st->flags, FA_DFLAG_DUPLICATE_MIN_TRI);
+        return;
+    }
     for (int p = 0; p < passes; p++) {
         radix_pass(ka, va, kb, vb, n, 8 * p, sm);
         unsigned long long* tk = ka; ka = kb; kb = tk;

@@ -53,7 +53,8 @@ class FrameSettings:
 class FrameOutput:
     """Device views of one frame's results (valid until the engine's next frame)."""
 
-    def __init__(self, res: nat.FrameResult, settings: FrameSettings, T: int, V: int, device):
+    def __init__(self, res: nat.FrameResult, settings: FrameSettings, T: int, V: int, device, owner=None):
+        self._owner = owner  # keeps the context (and its buffers) alive while the views exist
         self.status = int(res.status)
         self.n_visible = int(res.n_visible)
         self.n_charts = int(res.n_charts)
@@ -155,7 +156,7 @@ class FrameEngine:
         if check:
             nat.raise_for_status(code)
         return FrameOutput(self._res, self._last_settings, self.mesh.n_triangles, len(self.mesh.positions),
-                           self.ctx.torch_device)
+                           self.ctx.torch_device, owner=self)
 
     def run(self, view_proj, settings: FrameSettings | None = None, stream=None, check: bool = True) -> FrameOutput:
         for _ in range(4):
@@ -166,7 +167,7 @@ class FrameEngine:
             if check:
                 nat.raise_for_status(code)
             return FrameOutput(self._res, self._last_settings, self.mesh.n_triangles, len(self.mesh.positions),
-                               self.ctx.torch_device)
+                               self.ctx.torch_device, owner=self)
         raise RuntimeError("frame work queues kept overflowing")
 
     def launch_count(self) -> int:

@@ -329,3 +329,18 @@ def test_full_size_vs_oracle(cfg):
     for q in p:
         grid[q[2]:q[2] + q[4], q[1]:q[1] + q[3]] += 1
     assert grid.max() <= 1
+
+
+@pytest.mark.parametrize("frac", [0.18, 0.5])
+def test_union_find_under_contention(frac):
+    """Random visibility on the 4M-triangle mesh: many small components and
+    heavy hook contention; repeated runs must equal the oracle every time."""
+    spec = scenes.build_scene("C3")
+    T = len(spec.triangles)
+    lab0 = np.where(np.random.default_rng(0).random(T) < frac, np.arange(T), -1)
+    ref, ref_v2c = oracle.merge_shared_vertices(spec.triangles, len(spec.positions), lab0)
+    mesh = fa.Mesh(spec.positions, spec.triangles)
+    for _ in range(3):
+        cs = fa.merge_shared_vertices(fa.ChartSet(lab0), mesh)
+        assert np.array_equal(cs.chart_of_triangle, ref)
+        assert np.array_equal(cs.vertex_chart_array, ref_v2c)
