@@ -1,0 +1,368 @@
+"""Benchmark: per-frame atlasing of a 1M-triangle scene, 1080p view -> 2K^2 atlas.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One step = one frame (one view) per GPU through the CUDA path: visibility
+(depth + visibility raster passes), chartification, chart bounds, order,
+64-candidate pack, UVs.  Workload (BASELINE.json configs[1] / SURVEY §8d):
+scene C2 (1,000,040 triangles, 500,302 vertices), 1920x1080, omega 2048,
+64 scale candidates; each step renders the next C5 golden-angle view, rank r
+taking views r*K.. (weak scaling: K views per GPU).  The mesh is resident
+(uploaded once); L2 is flushed (256 MiB write) between timed frames.
+
+`--impl reference` times the reference algorithm on the host cores: the C
+oracle port (oracle/fa_oracle.c, a restatement of the reference pinned to
+its golden vectors; the reference itself is pure Python and ~6 min/frame),
+one frame per worker process across all host cores per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "ms/frame (atlases/s) @1M tris 1080p→2K² atlas; views/s at 1/2/4/8 GPUs"
+WORKLOAD = ("C2: synthetic sphere-field + ground-plane scene, 1,000,040 tris / 500,302 verts, 1920x1080 view, "
+            "2048^2 atlas, 64 scale candidates, prescale 1; C5 golden-angle camera per step")
+
+
+def _views(n=64):
+    from paper_2502_17712_b200 import scenes
+    return scenes.views_c5(n)
+
+
+def _vp(pose, screen):
+    from paper_2502_17712_b200.geometry import CameraFrame
+    cam = CameraFrame.from_params(math.radians(pose.fov_y_deg), screen[0] / screen[1], pose.near, pose.far,
+                                  position=pose.position, look_at=pose.look_at, up=pose.up)
+    return cam.view_proj
+
+
+# --------------------------------------------------------------------- clocks --
+REASONS = {
+    "clocks_event_reasons.hw_slowdown": "hw_slowdown",
+    "clocks_event_reasons.hw_thermal_slowdown": "hw_thermal_slowdown",
+    "clocks_event_reasons.sw_thermal_slowdown": "sw_thermal_slowdown",
+    "clocks_event_reasons.sw_power_cap": "sw_power_cap",
+}
+
+
+class ClockSampler:
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = "clocks.sm,clocks.max.sm," + ",".join(REASONS)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 2 + len(REASONS):
+                    continue
+                try:
+                    sm.append(float(parts[0]))
+                    mx.append(float(parts[1]))
+                except ValueError:
+                    continue
+                for val, name in zip(parts[2:], REASONS.values()):
+                    if val.lower().startswith("active"):
+                        reasons.add(name)
+        finally:
+            if self.path and os.path.exists(self.path):
+                os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------- roofline --
+def stage_bytes(stage: str, T: int, V: int, W: int, H: int, n_vis: int, C: int) -> int:
+    """Algorithmic (compulsory) bytes per launch of each stage."""
+    table = {
+        "project+clear": 24 * V + 32 * V + 4 * V + 8 * W * H + T,
+        "depth pass": 12 * T + 32 * V + 16 * W * H,
+        "visibility pass": 12 * T + 32 * V + 8 * W * H + T,
+        "visible compaction": 2 * T + 4 * T + 4 * n_vis,
+        "union-find": 4 * n_vis + 12 * n_vis + 4 * V + 4 * n_vis + 4 * V,
+        "chart roots": 8 * n_vis + 4 * C,
+        "bounds+dims": 4 * n_vis + 12 * n_vis + 32 * V + 64 * C,
+        "order": 32 * C,
+        "pack+select": 64 * C,
+        "uv": 4 * n_vis + 12 * n_vis + 32 * V + 24 * n_vis,
+    }
+    return int(table.get(stage, 0))
+
+
+def frame_bytes(T, V, W, H, n_vis, C) -> int:
+    """SURVEY §8(d) per-frame compulsory traffic (f32 UVs)."""
+    return 24 * V + 12 * T + 16 * W * H + 2 * T + 4 * T + 4 * V + 24 * n_vis + 64 * C
+
+
+def _peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------ CPU baseline leg --
+_W_STATE = {}
+
+
+def _worker_init():
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    from paper_2502_17712_b200 import scenes
+    s = scenes.scene_c2()
+    _W_STATE["scene"] = s
+
+
+def _worker_frame(view_idx):
+    import oracle
+    s = _W_STATE["scene"]
+    pose = _views()[view_idx % 64]
+    vp = _vp(pose, s.screen)
+    t0 = time.perf_counter()
+    r = oracle.run_frame(s.positions, s.triangles, vp, s.screen, s.omega)
+    return time.perf_counter() - t0, int(r.status)
+
+
+def cpu_reference_run(steps: int, warmup: int, workers: int):
+    """Oracle port over all host cores: each step = one frame per worker."""
+    import multiprocessing as mp
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle
+    oracle.build()
+    ctx = mp.get_context("fork")
+    with ctx.Pool(workers, initializer=_worker_init) as pool:
+        for w in range(warmup):
+            pool.map(_worker_frame, range(w * workers, (w + 1) * workers))
+        t0 = time.perf_counter()
+        frames = 0
+        for s in range(steps):
+            res = pool.map(_worker_frame, range(s * workers, (s + 1) * workers))
+            frames += len(res)
+        wall = time.perf_counter() - t0
+    return frames, wall
+
+
+def cpu_baseline_sample(n_frames: int = 6):
+    """Single-threaded oracle on a bounded sample of the same workload (rank 0, N=1)."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle
+    from paper_2502_17712_b200 import scenes
+    oracle.build()
+    s = scenes.scene_c2()
+    views = _views()
+    oracle.run_frame(s.positions, s.triangles, _vp(views[0], s.screen), s.screen, s.omega)  # warm
+    t0 = time.perf_counter()
+    for k in range(n_frames):
+        oracle.run_frame(s.positions, s.triangles, _vp(views[k], s.screen), s.screen, s.omega)
+    wall = time.perf_counter() - t0
+    return {"value": n_frames / wall, "unit": "atlases/s", "cores": 1, "kind": "port",
+            "sample": f"{n_frames} C2 frames (views 0..{n_frames - 1}), single-threaded C oracle "
+                      f"(oracle/fa_oracle.c), {1000 * wall / n_frames:.0f} ms/frame"}
+
+
+# ------------------------------------------------------------------------ main --
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-frames", type=int, default=5)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        workers = len(os.sched_getaffinity(0))
+        frames, wall = cpu_reference_run(args.steps, args.warmup, workers)
+        v = frames / wall
+        line = {"metric": METRIC, "value": v, "unit": "atlases/s", "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": 1000 * wall / args.steps, "ms_per_frame": 1000 * wall / frames,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "impl": "reference",
+                "config": {"workload": WORKLOAD, "host": f"{workers} processes, one frame each per step"},
+                "cpu_baseline": {"value": v, "unit": "atlases/s", "cores": workers, "kind": "port",
+                                 "sample": f"{frames} C2 frames, {workers} concurrent single-threaded oracle "
+                                           f"frames per step"},
+                "e2e": {"value": v, "unit": "atlases/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    import paper_2502_17712_b200 as fa
+    from paper_2502_17712_b200 import FrameEngine, FrameSettings, scenes
+
+    spec = scenes.scene_c2()
+    W, H = spec.screen
+    T, V = len(spec.triangles), len(spec.positions)
+    mesh = fa.Mesh(spec.positions, spec.triangles)
+    settings = FrameSettings(screen=spec.screen, omega=spec.omega, n_scales=64, prescale=1.0)
+    eng = FrameEngine(mesh, device=local, settings=settings)
+    views = _views()
+    K = args.steps
+    vps = [_vp(views[(rank * K + s) % 64], spec.screen) for s in range(K)]
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    for w in range(args.warmup):
+        eng.run(vps[w % K])
+    launches_per_frame = eng.launch_count()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---------------- device-timed frames (inputs resident) ----------------
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    stats = []
+    barrier()
+    with ClockSampler(local) as clocks:
+        for s in range(K):
+            flush.zero_()
+            evs[s][0].record(stream)
+            eng.launch(vps[s])
+            evs[s][1].record(stream)
+            out = eng.finish()  # host sync outside the event pair
+            stats.append((out.n_visible, out.n_charts))
+        barrier()
+    dev_ms = sum(a.elapsed_time(b) for a, b in evs)
+    clock = clocks.summary()
+
+    # ---------------- end to end through the public API, host buffers --------
+    pin_cam = torch.empty((K, 16), dtype=torch.float64).pin_memory()
+    pin_cam.copy_(torch.as_tensor(np.stack([v.reshape(-1) for v in vps])))
+    h_chart = torch.empty(T, dtype=torch.int32).pin_memory()
+    h_vis = torch.empty(T, dtype=torch.int32).pin_memory()
+    h_uv = torch.empty((T, 6), dtype=torch.float32).pin_memory()
+    h_plc = torch.empty((T, 8), dtype=torch.int64).pin_memory()
+    eevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    d2h = 0
+    barrier()
+    for s in range(K):
+        flush.zero_()
+        eevs[s][0].record(stream)
+        eng.launch(pin_cam[s].numpy().reshape(4, 4))
+        out = eng.finish()
+        nv, C = out.n_visible, out.n_charts
+        h_chart.copy_(out.chart_of_triangle, non_blocking=True)
+        h_vis[:nv].copy_(out.visible, non_blocking=True)
+        h_uv[:nv].copy_(out.uv, non_blocking=True)
+        h_plc[:C].copy_(out.placements, non_blocking=True)
+        eevs[s][1].record(stream)
+        d2h += 4 * T + 4 * nv + 24 * nv + 64 * C
+    barrier()
+    e2e_ms = sum(a.elapsed_time(b) for a, b in eevs)
+
+    # ---------------- per-stage timing (same stream, CUDA events) ------------
+    prof = FrameSettings(screen=spec.screen, omega=spec.omega, n_scales=64, profile=True, use_graph=False)
+    acc = {}
+    for s in range(args.profile_frames):
+        flush.zero_()
+        eng.run(vps[s % K], settings=prof)
+        for k, v in eng.stage_times().items():
+            acc.setdefault(k, []).append(v)
+    stage_ms = {k: float(np.mean(v)) for k, v in acc.items()}
+
+    # ---------------- reduce over ranks ----------------
+    t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms, e2e_ms = float(t[0]), float(t[1])
+    frames_total = K * world
+    if rank == 0:
+        n_vis = int(np.mean([a for a, _ in stats]))
+        C = int(np.mean([b for _, b in stats]))
+        top = max(stage_ms, key=stage_ms.get) if stage_ms else None
+        peak, peak_kind = _peaks()
+        roof = None
+        if top:
+            b = stage_bytes(top, T, V, W, H, n_vis, C)
+            gbs = b / (stage_ms[top] * 1e-3) / 1e9
+            roof = {"bound": "hbm", "kernel": top, "achieved": gbs, "peak": peak, "unit": "GB/s",
+                    "frac": gbs / peak, "peak_source": peak_kind, "traffic": None,
+                    "algorithmic_bytes": b, "kernel_ms": stage_ms[top],
+                    "frame_bytes": frame_bytes(T, V, W, H, n_vis, C),
+                    "frame_frac": frame_bytes(T, V, W, H, n_vis, C) / (dev_ms / K * 1e-3) / 1e9 / peak}
+        line = {
+            "metric": METRIC, "value": frames_total / (dev_ms * 1e-3), "unit": "atlases/s", "n_gpus": world,
+            "steps": K, "warmup": args.warmup, "ms_per_step": dev_ms / K, "ms_per_frame": dev_ms / K,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD, "l2": "flushed with a 256 MiB write between timed frames",
+                       "views_per_gpu": K, "mean_visible": n_vis, "mean_charts": C,
+                       "parallelism": f"{world} independent view streams (no collective)"},
+            "e2e": {"value": frames_total / (e2e_ms * 1e-3), "unit": "atlases/s", "h2d_bytes_per_step": 128,
+                    "d2h_bytes_per_step": int(d2h / K),
+                    "what": "camera H2D (pageable, staged by the driver) + frame + D2H of chart ids, visible "
+                            "list, f32 UVs, placements into pinned host buffers"},
+            "gpu_launches": launches_per_frame * K,
+            "launches_per_frame": launches_per_frame,
+            "stage_ms": stage_ms,
+            "roofline": roof,
+            "clocks": clock,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline_sample()
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

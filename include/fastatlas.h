@@ -144,6 +144,7 @@ typedef struct fa_frame_params {
     int uv_f64;              /* 1: emit float64 UVs (bit-exact), 0: float32 */
     int want_depth;          /* 1: decode the depth buffer into float64 */
     int use_graph;           /* 1: replay a captured CUDA graph per shape */
+    int profile;             /* 1: record CUDA events between stages (implies use_graph = 0) */
 } fa_frame_params;
 
 typedef struct fa_frame_result {
@@ -177,6 +178,12 @@ int fa_frame(fa_ctx *ctx, const double *vp_host, const fa_frame_params *params, 
 
 /* Number of kernels the last fa_frame_launch enqueued (benchmark accounting). */
 int fa_last_launch_count(fa_ctx *ctx);
+
+/* Per-stage device times (ms, CUDA events on the frame stream) of the last
+ * frame launched with params.profile = 1; returns the stage count (<= max).
+ * Synchronises the stream.  fa_stage_name(i) names stage i. */
+int fa_stage_times(fa_ctx *ctx, float *ms_out, int max, void *stream);
+const char *fa_stage_name(int i);
 
 #ifdef __cplusplus
 }

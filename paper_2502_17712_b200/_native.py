@@ -40,6 +40,7 @@ EXPORTS = (
     "fa_chart_boxes", "fa_blinn_clamped_ndc", "fa_select_side_plane", "fa_chart_bbox",
     "fa_viewport_box", "fa_orient", "fa_orient_order", "fa_fold", "fa_push_up", "fa_pack_at_scale",
     "fa_pack", "fa_frame_launch", "fa_frame_finish", "fa_frame", "fa_last_launch_count",
+    "fa_stage_times", "fa_stage_name",
 )
 
 
@@ -54,7 +55,7 @@ class FrameParams(ctypes.Structure):
         ("min_dim", ctypes.c_int64), ("padding", ctypes.c_int64),
         ("prescale", ctypes.c_double),
         ("backface_cull", ctypes.c_int), ("uv_f64", ctypes.c_int),
-        ("want_depth", ctypes.c_int), ("use_graph", ctypes.c_int),
+        ("want_depth", ctypes.c_int), ("use_graph", ctypes.c_int), ("profile", ctypes.c_int),
     ]
 
 
@@ -121,6 +122,8 @@ def load_library():
             "fa_frame_finish": ([vp, ctypes.POINTER(FrameResult), vp], ci),
             "fa_frame": ([vp, vp, ctypes.POINTER(FrameParams), ctypes.POINTER(FrameResult), vp], ci),
             "fa_last_launch_count": ([vp], ci),
+            "fa_stage_times": ([vp, ctypes.POINTER(ctypes.c_float), ci, vp], ci),
+            "fa_stage_name": ([ci], ctypes.c_char_p),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)

@@ -608,36 +608,68 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     CK(cudaMemsetAsync(ctx->dstat.p, 0, sizeof(fa_dstat), s));
     CK(cudaMemsetAsync(ctx->cand.p, 0, (size_t)p->n_scales * FA_CAND_REC * 8, s));
     nl = 0;
+    bool prof = p->profile && !p->use_graph;
+    ctx->n_stage_marks = 0;
+    auto mark = [&]() -> int {
+        if (!prof) return FA_OK;
+        if (!ctx->ev[ctx->n_stage_marks]) CK(cudaEventCreate(&ctx->ev[ctx->n_stage_marks]));
+        CK(cudaEventRecord(ctx->ev[ctx->n_stage_marks], s));
+        ctx->n_stage_marks++;
+        return FA_OK;
+    };
     unsigned char* flags = P<unsigned char>(ctx->flags);
-    launch_depth(ctx, W, H, p->backface_cull, flags, s, nl);
+    int T_ = T;
+    (void)T_;
+    int V_ = V;
+    mark();  // 0: start
+    fa_launch_frame_init(ctx->pos, V_, P<double>(ctx->vp_dev), P<double4>(ctx->clip), P<int>(ctx->vmin),
+                         P<unsigned long long>(ctx->depth_keys), (long long)W * H, flags, T, s);
+    nl += 1;
+    mark();  // 1: project + clears
+    fa_launch_raster_setup(true, P<double4>(ctx->clip), ctx->tris, T, W, H, p->backface_cull,
+                           P<unsigned long long>(ctx->depth_keys), P<int>(ctx->small_list), P<TriSetup>(ctx->large),
+                           ctx->max_large, P<int2>(ctx->tiles), ctx->max_tiles, st, s);
+    fa_launch_raster_depth_tiles(P<TriSetup>(ctx->large), P<int2>(ctx->tiles), ctx->max_tiles, W,
+                                 P<unsigned long long>(ctx->depth_keys), st, s);
+    nl += 2;
+    mark();  // 2: depth pass
     fa_launch_raster_vis(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->small_list), P<TriSetup>(ctx->large),
                          P<int2>(ctx->tiles), ctx->max_tiles, T, W, H, p->backface_cull,
                          P<unsigned long long>(ctx->depth_keys), flags, st, s);
     nl += 2;
+    mark();  // 3: visibility pass
     fa_launch_compact_visible(flags, T, P<int>(ctx->blocks), P<int>(ctx->vis_list), P<int>(ctx->label), st, s);
     nl += 2;
+    mark();  // 4: visible compaction
     fa_launch_uf_vertex(ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->vmin), P<int>(ctx->label), T, st, s);
     fa_launch_uf_compress(P<int>(ctx->vis_list), P<int>(ctx->label), T, st, s);
     fa_launch_v2c(P<int>(ctx->vmin), P<int>(ctx->label), P<int>(ctx->v2c), V, s);
     nl += 4;
+    mark();  // 5: union-find charts
     fa_launch_compact_roots(P<int>(ctx->vis_list), P<int>(ctx->label), T, P<int>(ctx->blocks), P<int>(ctx->roots),
                             P<int>(ctx->cidx), P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), st, s);
+    nl += 2;
+    mark();  // 6: chart roots
     fa_launch_chart_bounds(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->label),
                            P<int>(ctx->cidx), T, P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), st, s);
     fa_launch_box_dims(P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), P<int>(ctx->roots), T, W, H,
                        p->prescale, P<double>(ctx->ndc), P<int>(ctx->px), P<long long>(ctx->target),
                        P<long long>(ctx->in_tw), P<long long>(ctx->in_th), P<long long>(ctx->in_cid), (int)n_cap,
                        st, s);
-    nl += 4;
+    nl += 2;
+    mark();  // 7: chart bounds + box dims
     fa_pack_bufs b = pack_bufs(ctx, P<long long>(ctx->in_tw), P<long long>(ctx->in_th), P<long long>(ctx->in_cid),
                                P<long long>(ctx->placements), nullptr);
     fa_launch_orient_sort(b, (int)n_cap, &st->n_charts, FA_MAX_BOX_DIM, st, s);
     nl += 1;
+    mark();  // 8: orient + radix order
     nl += fa_launch_pack(b, (int)n_cap, &st->n_charts, p->omega, p->n_scales, p->min_dim, p->padding, batch, st, s);
+    mark();  // 9: candidate pack + select
     fa_launch_uv(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->label), P<int>(ctx->cidx),
                  P<int>(ctx->pinv), P<double>(ctx->ndc), P<int>(ctx->px), P<long long>(ctx->placements), T, W, H,
                  p->padding, p->uv_f64 != 0, ctx->uv.p, st, s);
     nl += 1;
+    mark();  // 10: uv
     if (p->want_depth) {
         fa_launch_decode_depth(P<unsigned long long>(ctx->depth_keys), P<double>(ctx->depth_f64), (long long)W * H, s);
         nl += 1;
@@ -681,7 +713,10 @@ int fa_frame_launch(fa_ctx* ctx, const double* vp_host, const fa_frame_params* p
     ctx->last_params = *p;
     r = upload_vp(ctx, vp_host, s);
     if (r) return r;
-    if (!p->use_graph) {
+    if (!p->use_graph || p->profile) {
+        fa_frame_params q = *p;
+        q.use_graph = 0;
+        p = &q;
         int nl = 0;
         r = frame_sequence(ctx, p, s, nl);
         ctx->last_launches = nl;
@@ -798,6 +833,28 @@ int fa_frame(fa_ctx* ctx, const double* vp_host, const fa_frame_params* p, fa_fr
 }
 
 int fa_last_launch_count(fa_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
+
+static const char* kStageNames[] = {"project+clear", "depth pass",   "visibility pass", "visible compaction",
+                                    "union-find",    "chart roots",  "bounds+dims",     "order",
+                                    "pack+select",   "uv"};
+
+const char* fa_stage_name(int i) {
+    return (i >= 0 && i < (int)(sizeof(kStageNames) / sizeof(kStageNames[0]))) ? kStageNames[i] : "";
+}
+
+int fa_stage_times(fa_ctx* ctx, float* ms_out, int max, void* stream) {
+    if (!ctx || !ms_out) return 0;
+    cudaStreamSynchronize((cudaStream_t)stream);
+    int n = ctx->n_stage_marks - 1;
+    if (n < 0) n = 0;
+    if (n > max) n = max;
+    for (int i = 0; i < n; i++) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev[i], ctx->ev[i + 1]);
+        ms_out[i] = ms;
+    }
+    return n;
+}
 
 }  // extern "C"
 

@@ -56,6 +56,11 @@ struct fa_ctx {
     // CUDA graph per frame shape
     cudaGraphExec_t graph_exec = nullptr;
     fa_graph_key graph_key{};
+
+    // stage timing (params.profile)
+    static const int kMaxStages = 12;
+    cudaEvent_t ev[kMaxStages + 1] = {};
+    int n_stage_marks = 0;
 };
 
 // growth helper: ensures buf has >= bytes; returns false on allocation failure

@@ -36,6 +36,7 @@ class FrameSettings:
     uv_f64: bool = False
     want_depth: bool = False
     use_graph: bool = True
+    profile: bool = False
 
     def params(self) -> nat.FrameParams:
         p = nat.FrameParams()
@@ -47,6 +48,7 @@ class FrameSettings:
         p.uv_f64 = int(bool(self.uv_f64))
         p.want_depth = int(bool(self.want_depth))
         p.use_graph = int(bool(self.use_graph))
+        p.profile = int(bool(self.profile))
         return p
 
 
@@ -172,3 +174,9 @@ class FrameEngine:
 
     def launch_count(self) -> int:
         return int(self.ctx.L.fa_last_launch_count(self.ctx.h))
+
+    def stage_times(self) -> dict:
+        """{stage name: ms} of the last frame run with settings.profile=True."""
+        buf = (ctypes.c_float * 16)()
+        n = self.ctx.L.fa_stage_times(self.ctx.h, buf, 16, self._stream)
+        return {self.ctx.L.fa_stage_name(i).decode(): float(buf[i]) for i in range(n)}

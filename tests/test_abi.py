@@ -42,8 +42,8 @@ def test_abi_version(lib):
 
 def test_struct_layouts_match_header():
     from paper_2502_17712_b200 import _native
-    # fa_frame_params: 2 int, 4 int64, double, 4 int  -> 2*4 + 4*8 + 8 + 4*4 = 64
-    assert ctypes.sizeof(_native.FrameParams) == 64
+    # fa_frame_params: 2 int, 4 int64, double, 5 int (+4 pad) -> 8 + 32 + 8 + 20 + 4 = 72
+    assert ctypes.sizeof(_native.FrameParams) == 72
     # fa_frame_result: int + 2 int32 (+pad to 8) + 4 int64 + 11 pointers
     assert ctypes.sizeof(_native.FrameResult) == 16 + 4 * 8 + 11 * 8
 
