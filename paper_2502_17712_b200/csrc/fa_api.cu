@@ -388,10 +388,11 @@ int fa_merge_shared_vertices(fa_ctx* ctx, const int32_t* labels_in, int32_t* lab
     unsigned char* fl = P<unsigned char>(ctx->flags);
     fa_launch_flags_from_labels(labels_in, fl, T, s);
     fa_launch_compact_visible(fl, T, P<int>(ctx->blocks), P<int>(ctx->vis_list), labels_out, st, s);
-    // general chart sets: every node starts as its own root (charts.py:371-374)
-    fa_launch_uf_labels(labels_in, P<int>(ctx->vis_list), labels_out, T, st, s);
+    // general chart sets: every node starts as its own root (charts.py:371)
+    fa_launch_iota(labels_out, T, s);
     fa_launch_fill(P<int>(ctx->vmin), V, 0x7fffffff, s);
     fa_launch_uf_vertex(ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->vmin), labels_out, T, st, s);
+    fa_launch_uf_labels(labels_in, P<int>(ctx->vis_list), labels_out, T, st, s);
     fa_launch_uf_compress(P<int>(ctx->vis_list), labels_out, T, st, s);
     fa_launch_canonicalize(P<int>(ctx->vis_list), labels_out, P<int>(ctx->aux), T, st, s);
     fa_launch_canon_apply(fl, labels_out, P<int>(ctx->aux), T, s);
@@ -631,7 +632,8 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
                            ctx->max_large, P<int2>(ctx->tiles), ctx->max_tiles, st, s);
     fa_launch_raster_depth_tiles(P<TriSetup>(ctx->large), P<int2>(ctx->tiles), ctx->max_tiles, W,
                                  P<unsigned long long>(ctx->depth_keys), st, s);
-    nl += 2;
+    fa_launch_count_finite(P<unsigned long long>(ctx->depth_keys), (long long)W * H, st, s);
+    nl += 3;
     mark();  // 2: depth pass
     fa_launch_raster_vis(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->small_list), P<TriSetup>(ctx->large),
                          P<int2>(ctx->tiles), ctx->max_tiles, T, W, H, p->backface_cull,
@@ -644,7 +646,7 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     fa_launch_uf_vertex(ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->vmin), P<int>(ctx->label), T, st, s);
     fa_launch_uf_compress(P<int>(ctx->vis_list), P<int>(ctx->label), T, st, s);
     fa_launch_v2c(P<int>(ctx->vmin), P<int>(ctx->label), P<int>(ctx->v2c), V, s);
-    nl += 4;
+    nl += 5;
     mark();  // 5: union-find charts
     fa_launch_compact_roots(P<int>(ctx->vis_list), P<int>(ctx->label), T, P<int>(ctx->blocks), P<int>(ctx->roots),
                             P<int>(ctx->cidx), P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), st, s);

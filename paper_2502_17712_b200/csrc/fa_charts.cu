@@ -147,6 +147,23 @@ __global__ void k_vmin(const int* __restrict__ tris, const int* __restrict__ vis
     }
 }
 
+// ECL-CC style initialisation: parent[t] = smallest triangle sharing a vertex
+// with t (<= t, same component), so hooking starts from shallow trees.
+// Must run as its own kernel: a plain store racing a hooking CAS could lose it.
+__global__ void k_uf_init_vmin(const int* __restrict__ tris, const int* __restrict__ vis_list,
+                               const int* __restrict__ vmin, int* __restrict__ label,
+                               const fa_dstat* __restrict__ st) {
+    int n = st->n_vis;
+    int stride = gridDim.x * blockDim.x;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+        int t = vis_list[k];
+        int m = t;
+#pragma unroll
+        for (int j = 0; j < 3; j++) m = min(m, vmin[__ldg(tris + 3 * t + j)]);
+        label[t] = m;
+    }
+}
+
 __global__ void k_hook_vertex(const int* __restrict__ tris, const int* __restrict__ vis_list,
                               const int* __restrict__ vmin, int* label, const fa_dstat* __restrict__ st) {
     int n = st->n_vis;
@@ -241,6 +258,7 @@ static inline int uf_grid(int T) { return fa_grid(T, 256, FA_NUM_SMS * 8); }
 void fa_launch_uf_vertex(const int* tris, const int* vis_list, int* vmin, int* label, int T, const fa_dstat* st,
                          cudaStream_t s) {
     k_vmin<<<uf_grid(T), 256, 0, s>>>(tris, vis_list, vmin, st);
+    k_uf_init_vmin<<<uf_grid(T), 256, 0, s>>>(tris, vis_list, vmin, label, st);
     k_hook_vertex<<<uf_grid(T), 256, 0, s>>>(tris, vis_list, vmin, label, st);
 }
 
@@ -249,9 +267,12 @@ void fa_launch_uf_edges(const int* adjacency, const unsigned char* flags, const 
     k_hook_edges<<<uf_grid(T), 256, 0, s>>>(adjacency, flags, vis_list, label, st);
 }
 
+void fa_launch_iota(int* label, int T, cudaStream_t s) { k_iota<<<uf_grid(T), 256, 0, s>>>(label, T); }
+
+// union(t, labels_in[t]) for every visible t (charts.py:372-374); run after
+// fa_launch_uf_vertex, whose initialisation overwrites parent pointers
 void fa_launch_uf_labels(const int* labels_in, const int* vis_list, int* label, int T, const fa_dstat* st,
                          cudaStream_t s) {
-    k_iota<<<uf_grid(T), 256, 0, s>>>(label, T);
     k_hook_labels<<<uf_grid(T), 256, 0, s>>>(labels_in, vis_list, label, st);
 }
 

@@ -78,6 +78,7 @@ void fa_launch_raster_vis(const double4* clip, const int* tris, const int* small
                           const int2* tiles, int max_tiles, int T, int W, int H, int cull,
                           const unsigned long long* depth, unsigned char* flags, const fa_dstat* st, cudaStream_t s);
 void fa_launch_decode_depth(const unsigned long long* keys, double* out, long long n, cudaStream_t s);
+void fa_launch_count_finite(const unsigned long long* depth, long long npx, fa_dstat* st, cudaStream_t s);
 void fa_launch_encode_depth(const double* in, unsigned long long* keys, long long n, cudaStream_t s);
 size_t fa_trisetup_bytes();
 
@@ -92,6 +93,7 @@ void fa_launch_uf_edges(const int* adjacency, const unsigned char* flags, const 
                         const fa_dstat* st, cudaStream_t s);
 void fa_launch_uf_labels(const int* labels_in, const int* vis_list, int* label, int T, const fa_dstat* st,
                          cudaStream_t s);
+void fa_launch_iota(int* label, int T, cudaStream_t s);
 void fa_launch_uf_compress(const int* vis_list, int* label, int T, const fa_dstat* st, cudaStream_t s);
 void fa_launch_canonicalize(const int* vis_list, int* label, int* tmp, int T, const fa_dstat* st, cudaStream_t s);
 void fa_launch_v2c(const int* vmin, const int* label, int* v2c, int V, cudaStream_t s);

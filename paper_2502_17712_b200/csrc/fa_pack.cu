@@ -30,9 +30,23 @@ __device__ __forceinline__ long long np_ceil_scaled(long long num, long long t, 
     return (long long)(0ull - (unsigned long long)q);
 }
 
+// exact ceil(p / d) for 0 <= p < 2^53, 0 < d < 2^53: a float64 quotient is
+// within one of the true floor, fixed by one integer remainder check
+__device__ __forceinline__ long long ceil_div_small(long long p, long long d) {
+    long long q = (long long)__ddiv_rz((double)p, (double)d);
+    long long r = p - q * d;
+    if (r < 0) { q -= 1; r += d; }
+    else if (r >= d) { q += 1; r -= d; }
+    return q + (r != 0);
+}
+
 __device__ __forceinline__ long long scaled_dim(long long t, long long num, long long den, long long min_dim,
                                                 long long pad) {
-    long long s = np_ceil_scaled(num, t, den);
+    long long s;
+    if (num >= 0 && num < (1ll << 26) && t >= 0 && t < (1ll << 26) && den > 0 && den < (1ll << 53))
+        s = ceil_div_small(num * t, den);  // num*t < 2^52: same value as the numpy expression
+    else
+        s = np_ceil_scaled(num, t, den);
     if (s < min_dim) s = min_dim;
     return s + 2 * pad;
 }
@@ -89,11 +103,20 @@ __device__ u128 div128(u128 n, u128 d) {
 
 // (num, den) <- reduce(floor(num*omega*2^24 / (den*(omega+m))), 2^24)
 __device__ __forceinline__ void snap_scale(long long& num, long long& den, long long omega, long long m) {
-    u128 n = mul64((unsigned long long)num, (unsigned long long)omega);  // < 2^116 overall after shift
-    n = shl128(n, FA_SCALE_GRID_BITS);
-    u128 d = mul64((unsigned long long)den, (unsigned long long)(omega + m));
-    u128 f = div128(n, d);
-    long long fn = (long long)f.lo;  // < 2^24 since scale <= 1
+    long long fn;
+    unsigned long long nw = (unsigned long long)num * (unsigned long long)omega;
+    unsigned long long dd = (unsigned long long)den * (unsigned long long)(omega + m);
+    if (num >= 0 && num < (1ll << 31) && omega < (1ll << 31) && (nw >> 40) == 0 && den > 0 &&
+        den < (1ll << 31) && (omega + m) < (1ll << 32)) {
+        // common case: numerator fits in 64 bits, one u64 division
+        fn = (long long)((nw << FA_SCALE_GRID_BITS) / dd);
+    } else {
+        u128 n = mul64((unsigned long long)num, (unsigned long long)omega);  // < 2^116 overall after shift
+        n = shl128(n, FA_SCALE_GRID_BITS);
+        u128 d = mul64((unsigned long long)den, (unsigned long long)(omega + m));
+        u128 f = div128(n, d);
+        fn = (long long)f.lo;  // < 2^24 since scale <= 1
+    }
     if (fn == 0) { num = 0; den = 1; return; }
     int tz = __ffsll(fn) - 1;
     if (tz > FA_SCALE_GRID_BITS) tz = FA_SCALE_GRID_BITS;

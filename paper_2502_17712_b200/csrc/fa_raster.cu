@@ -75,15 +75,52 @@ __global__ void __launch_bounds__(256) k_raster_setup(const double4* __restrict_
                                                       int* __restrict__ small_list, TriSetup* __restrict__ large,
                                                       int max_large, int2* __restrict__ tiles, int max_tiles,
                                                       fa_dstat* __restrict__ st) {
-    long long frags = 0;
     int stride = gridDim.x * blockDim.x;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += stride) {
+        Setup3 f;
+        int r3 = tri_setup3(clip, tris, t, W, H, cull != 0, f);
+        if (r3 == 0) continue;
+        if (r3 == 1) {
+            int bw = f.max_x - f.min_x + 1, bh = f.max_y - f.min_y + 1;
+            if (bw * bh <= FA_SMALL_PX) {
+                // unclipped small triangle: registers only, fire-and-forget RED.MIN
+                bool covered = false;
+                for (int iy = f.min_y; iy <= f.max_y; iy++) {
+                    double py = (double)iy + 0.5;
+                    unsigned long long* row = depth + (long long)iy * W;
+                    for (int ix = f.min_x; ix <= f.max_x; ix++) {
+                        double px = (double)ix + 0.5;
+                        if (!sample_inside3(f, px, py)) continue;
+                        covered = true;
+                        if (WRITE_DEPTH) {
+                            unsigned long long key = f64_key(sample_depth3(f, px, py));
+                            if (key < row[ix]) atomicMin(row + ix, key);
+                        } else {
+                            break;
+                        }
+                    }
+                    if (!WRITE_DEPTH && covered) break;
+                }
+                if (covered) {
+                    int slot = active_append1(&st->n_small);
+                    small_list[slot] = t;
+                }
+                continue;
+            }
+        }
         TriSetup s;
-        int r = tri_setup(clip, tris, t, W, H, cull != 0, s);
+        int r;
+        if (r3 == 1) {
+            setup3_to_generic(f, t, s);
+            r = 1;
+        } else {
+            r = tri_setup(clip, tris, t, W, H, cull != 0, s);
+        }
         if (r < 0) { atomicOr(&st->flags, FA_DFLAG_POLY_OVERFLOW); continue; }
         if (r == 0) continue;
         int bw = s.max_x - s.min_x + 1, bh = s.max_y - s.min_y + 1;
         if (bw * bh <= FA_SMALL_PX) {
+            // clipped small polygon (generic setup)
             bool covered = false;
             for (int iy = s.min_y; iy <= s.max_y; iy++) {
                 double py = (double)iy + 0.5;
@@ -94,10 +131,7 @@ __global__ void __launch_bounds__(256) k_raster_setup(const double4* __restrict_
                     if (WRITE_DEPTH) {
                         unsigned long long key = f64_key(sample_depth(s, px, py));
                         unsigned long long* d = depth + (long long)iy * W + ix;
-                        if (key < *d) {
-                            unsigned long long old = atomicMin(d, key);
-                            if (old == FA_KEY_POS_INF && key < old) frags++;
-                        }
+                        if (key < *d) atomicMin(d, key);
                     } else {
                         break;
                     }
@@ -122,10 +156,24 @@ __global__ void __launch_bounds__(256) k_raster_setup(const double4* __restrict_
             for (int k = base; k < end; k++) tiles[k] = make_int2(slot, k - base);
         }
     }
-    if (WRITE_DEPTH) {
-        frags = warp_sum(frags);
-        if (lane_id() == 0 && frags) atomicAdd((unsigned long long*)&st->screen_fragments, (unsigned long long)frags);
+}
+
+// screen_fragments = #finite depth samples (cli.py:390), one pass over the keys
+__global__ void k_count_finite(const unsigned long long* __restrict__ depth, long long npx, fa_dstat* __restrict__ st) {
+    long long c = 0;
+    long long stride = (long long)gridDim.x * blockDim.x;
+    const ulonglong2* d2 = reinterpret_cast<const ulonglong2*>(depth);
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < npx / 2; i += stride) {
+        ulonglong2 v = d2[i];
+        // finite <=> key strictly between key(-inf) and key(+inf)
+        c += (v.x > FA_KEY_NEG_INF && v.x < FA_KEY_POS_INF) + (v.y > FA_KEY_NEG_INF && v.y < FA_KEY_POS_INF);
     }
+    if ((npx & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long v = depth[npx - 1];
+        c += (v > FA_KEY_NEG_INF && v < FA_KEY_POS_INF);
+    }
+    c = warp_sum(c);
+    if (lane_id() == 0 && c) atomicAdd((unsigned long long*)&st->screen_fragments, (unsigned long long)c);
 }
 
 // copy one TriSetup into warp-private shared memory
@@ -146,7 +194,6 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const TriSetup* __re
     int warp = threadIdx.x >> 5, lane = lane_id();
     int nwarps = gridDim.x * 8;
     int n_tiles = min(st->n_tiles, max_tiles);
-    long long frags = 0;
     for (int w = blockIdx.x * 8 + warp; w < n_tiles; w += nwarps) {
         int2 rec = tiles[w];
         __syncwarp();
@@ -165,15 +212,10 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const TriSetup* __re
                 if (!sample_inside(s, px, py)) continue;
                 unsigned long long key = f64_key(sample_depth(s, px, py));
                 unsigned long long* d = depth + (long long)y * W + x;
-                if (key < *d) {
-                    unsigned long long old = atomicMin(d, key);
-                    if (old == FA_KEY_POS_INF && key < old) frags++;
-                }
+                if (key < *d) atomicMin(d, key);
             }
         }
     }
-    frags = warp_sum(frags);
-    if (lane == 0 && frags) atomicAdd((unsigned long long*)&st->screen_fragments, (unsigned long long)frags);
 }
 
 // ---- pass 2 small: one thread per covering triangle -----------------------
@@ -186,9 +228,25 @@ __global__ void __launch_bounds__(256) k_raster_vis_small(const double4* __restr
     int stride = gridDim.x * blockDim.x;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         int t = small_list[i];
+        Setup3 f;
+        int r3 = tri_setup3(clip, tris, t, W, H, cull != 0, f);
+        if (r3 == 0) continue;
+        bool vis = false;
+        if (r3 == 1) {
+            for (int iy = f.min_y; iy <= f.max_y && !vis; iy++) {
+                double py = (double)iy + 0.5;
+                const unsigned long long* row = depth + (long long)iy * W;
+                for (int ix = f.min_x; ix <= f.max_x; ix++) {
+                    double px = (double)ix + 0.5;
+                    if (!sample_inside3(f, px, py)) continue;
+                    if (depth_passes(sample_depth3(f, px, py), key_f64(row[ix]))) { vis = true; break; }
+                }
+            }
+            if (vis) flags[t] = 1;
+            continue;
+        }
         TriSetup s;
         if (tri_setup(clip, tris, t, W, H, cull != 0, s) <= 0) continue;
-        bool vis = false;
         for (int iy = s.min_y; iy <= s.max_y && !vis; iy++) {
             double py = (double)iy + 0.5;
             for (int ix = s.min_x; ix <= s.max_x; ix++) {
@@ -279,6 +337,10 @@ void fa_launch_raster_vis(const double4* clip, const int* tris, const int* small
     k_raster_vis_small<<<fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s>>>(clip, tris, small_list, W, H, cull, depth,
                                                                        flags, st);
     k_raster_vis_tiles<<<FA_NUM_SMS * 8, 256, 0, s>>>(large, tiles, W, depth, flags, st, max_tiles);
+}
+
+void fa_launch_count_finite(const unsigned long long* depth, long long npx, fa_dstat* st, cudaStream_t s) {
+    k_count_finite<<<fa_grid(npx / 2 + 1, 256, FA_NUM_SMS * 4), 256, 0, s>>>(depth, npx, st);
 }
 
 void fa_launch_decode_depth(const unsigned long long* keys, double* out, long long n, cudaStream_t s) {

@@ -239,6 +239,110 @@ __device__ __forceinline__ int tri_setup(const double4* __restrict__ clip, const
     return 1;
 }
 
+// ---- register-resident setup for unclipped triangles (the common case) ----
+// Same arithmetic as tri_setup + finish_setup for n == 3, with every array
+// indexed by compile-time constants so nothing lands in local memory.
+struct Setup3 {
+    double ax0, ay0, dx0, dy0, ax1, ay1, dx1, dy1, ax2, ay2, dx2, dy2;
+    double p0x, p0y, p0z, gx, gy, zmean;
+    int incl, use_plane;
+    int min_x, max_x, min_y, max_y;
+};
+
+// 1 = Setup3 filled, 0 = no samples, 2 = needs the generic (clipping) path
+__device__ __forceinline__ int tri_setup3(const double4* __restrict__ clip, const int* __restrict__ tris, int t,
+                                          int W, int H, bool cull, Setup3& s) {
+    int ia = __ldg(tris + 3 * t), ib = __ldg(tris + 3 * t + 1), ic = __ldg(tris + 3 * t + 2);
+    double4 c0 = ldg4(clip + ia), c1 = ldg4(clip + ib), c2 = ldg4(clip + ic);
+    bool inside =
+        __dsub_rn(c0.w, FA_W_EPSILON) > 0 && __dsub_rn(c1.w, FA_W_EPSILON) > 0 && __dsub_rn(c2.w, FA_W_EPSILON) > 0 &&
+        __dadd_rn(c0.w, c0.x) >= 0 && __dsub_rn(c0.w, c0.x) >= 0 && __dadd_rn(c0.w, c0.y) >= 0 &&
+        __dsub_rn(c0.w, c0.y) >= 0 && __dadd_rn(c0.w, c0.z) >= 0 && __dsub_rn(c0.w, c0.z) >= 0 &&
+        __dadd_rn(c1.w, c1.x) >= 0 && __dsub_rn(c1.w, c1.x) >= 0 && __dadd_rn(c1.w, c1.y) >= 0 &&
+        __dsub_rn(c1.w, c1.y) >= 0 && __dadd_rn(c1.w, c1.z) >= 0 && __dsub_rn(c1.w, c1.z) >= 0 &&
+        __dadd_rn(c2.w, c2.x) >= 0 && __dsub_rn(c2.w, c2.x) >= 0 && __dadd_rn(c2.w, c2.y) >= 0 &&
+        __dsub_rn(c2.w, c2.y) >= 0 && __dadd_rn(c2.w, c2.z) >= 0 && __dsub_rn(c2.w, c2.z) >= 0;
+    if (!inside) {
+        bool anyp = __dsub_rn(c0.w, FA_W_EPSILON) > 0 || __dsub_rn(c1.w, FA_W_EPSILON) > 0 ||
+                    __dsub_rn(c2.w, FA_W_EPSILON) > 0;
+        return anyp ? 2 : 0;
+    }
+    double x0 = screen_x(c0.x, c0.w, W), y0 = screen_x(c0.y, c0.w, H), z0 = __ddiv_rn(c0.z, c0.w);
+    double x1 = screen_x(c1.x, c1.w, W), y1 = screen_x(c1.y, c1.w, H), z1 = __ddiv_rn(c1.z, c1.w);
+    double x2 = screen_x(c2.x, c2.w, W), y2 = screen_x(c2.y, c2.w, H), z2 = __ddiv_rn(c2.z, c2.w);
+    // OpenBLAS ddot tail (n = 3): t1 = fma(y_i, x_i, t1) from 0, then + t2 (= 0)
+    double A = __dadd_rn(__fma_rn(y0, x2, __fma_rn(y2, x1, __fma_rn(y1, x0, 0.0))), 0.0);
+    double B = __dadd_rn(__fma_rn(x0, y2, __fma_rn(x2, y1, __fma_rn(x1, y0, 0.0))), 0.0);
+    double area2 = __dsub_rn(A, B);
+    if (area2 == 0.0) return 0;
+    if (area2 < 0.0) {
+        if (cull) return 0;
+        double t;
+        t = x0; x0 = x2; x2 = t;
+        t = y0; y0 = y2; y2 = t;
+        t = z0; z0 = z2; z2 = t;
+    }
+    double mnx = x0, mxx = x0, mny = y0, mxy = y0;
+    mnx = x1 < mnx ? x1 : mnx; mxx = x1 > mxx ? x1 : mxx; mny = y1 < mny ? y1 : mny; mxy = y1 > mxy ? y1 : mxy;
+    mnx = x2 < mnx ? x2 : mnx; mxx = x2 > mxx ? x2 : mxx; mny = y2 < mny ? y2 : mny; mxy = y2 > mxy ? y2 : mxy;
+    long long fx = (long long)floor(__dsub_rn(mnx, 0.5)), cx = (long long)ceil(mxx);
+    long long fy = (long long)floor(__dsub_rn(mny, 0.5)), cy = (long long)ceil(mxy);
+    s.min_x = fx > 0 ? (int)fx : 0;
+    s.max_x = cx < W - 1 ? (int)cx : W - 1;
+    s.min_y = fy > 0 ? (int)fy : 0;
+    s.max_y = cy < H - 1 ? (int)cy : H - 1;
+    if (s.min_x > s.max_x || s.min_y > s.max_y) return 0;
+    s.ax0 = x0; s.ay0 = y0; s.dx0 = __dsub_rn(x1, x0); s.dy0 = __dsub_rn(y1, y0);
+    s.ax1 = x1; s.ay1 = y1; s.dx1 = __dsub_rn(x2, x1); s.dy1 = __dsub_rn(y2, y1);
+    s.ax2 = x2; s.ay2 = y2; s.dx2 = __dsub_rn(x0, x2); s.dy2 = __dsub_rn(y0, y2);
+    s.incl = ((s.dy0 > 0 || (s.dy0 == 0 && s.dx0 < 0)) ? 1 : 0) | ((s.dy1 > 0 || (s.dy1 == 0 && s.dx1 < 0)) ? 2 : 0) |
+             ((s.dy2 > 0 || (s.dy2 == 0 && s.dx2 < 0)) ? 4 : 0);
+    double a1x = s.dx0, a1y = s.dy0, a1z = __dsub_rn(z1, z0);
+    double a2x = __dsub_rn(x2, x0), a2y = __dsub_rn(y2, y0), a2z = __dsub_rn(z2, z0);
+    double det = __dsub_rn(__dmul_rn(a1x, a2y), __dmul_rn(a2x, a1y));
+    s.p0x = x0; s.p0y = y0; s.p0z = z0;
+    if (fabs(det) > 1e-12) {
+        s.gx = __ddiv_rn(__dsub_rn(__dmul_rn(a1z, a2y), __dmul_rn(a2z, a1y)), det);
+        s.gy = __ddiv_rn(__dsub_rn(__dmul_rn(a2z, a1x), __dmul_rn(a1z, a2x)), det);
+        s.use_plane = 1;
+        s.zmean = 0.0;
+    } else {
+        s.use_plane = 0;
+        s.gx = s.gy = 0.0;
+        s.zmean = __ddiv_rn(__dadd_rn(__dadd_rn(__dadd_rn(-0.0, z0), z1), z2), 3.0);
+    }
+    return 1;
+}
+
+__device__ __forceinline__ bool edge_ok(double ax, double ay, double dx, double dy, bool incl, double px, double py) {
+    double e = __dsub_rn(__dmul_rn(dx, __dsub_rn(py, ay)), __dmul_rn(dy, __dsub_rn(px, ax)));
+    return incl ? (e >= 0) : (e > 0);
+}
+
+__device__ __forceinline__ bool sample_inside3(const Setup3& s, double px, double py) {
+    return edge_ok(s.ax0, s.ay0, s.dx0, s.dy0, s.incl & 1, px, py) &&
+           edge_ok(s.ax1, s.ay1, s.dx1, s.dy1, s.incl & 2, px, py) &&
+           edge_ok(s.ax2, s.ay2, s.dx2, s.dy2, s.incl & 4, px, py);
+}
+
+__device__ __forceinline__ double sample_depth3(const Setup3& s, double px, double py) {
+    if (s.use_plane)
+        return __dadd_rn(__dadd_rn(s.p0z, __dmul_rn(s.gx, __dsub_rn(px, s.p0x))), __dmul_rn(s.gy, __dsub_rn(py, s.p0y)));
+    return s.zmean;
+}
+
+__device__ __forceinline__ void setup3_to_generic(const Setup3& a, int t, TriSetup& s) {
+    s.tri = t;
+    s.n = 3;
+    s.min_x = a.min_x; s.max_x = a.max_x; s.min_y = a.min_y; s.max_y = a.max_y;
+    s.use_plane = a.use_plane;
+    s.incl_mask = a.incl;
+    s.p0x = a.p0x; s.p0y = a.p0y; s.p0z = a.p0z; s.gx = a.gx; s.gy = a.gy; s.zmean = a.zmean;
+    s.ex[0] = a.ax0; s.ey[0] = a.ay0; s.edx[0] = a.dx0; s.edy[0] = a.dy0;
+    s.ex[1] = a.ax1; s.ey[1] = a.ay1; s.edx[1] = a.dx1; s.edy[1] = a.dy1;
+    s.ex[2] = a.ax2; s.ey[2] = a.ay2; s.edx[2] = a.dx2; s.edy[2] = a.dy2;
+}
+
 __device__ __forceinline__ bool sample_inside(const TriSetup& s, double px, double py) {
     for (int i = 0; i < s.n; i++) {
         double e = __dsub_rn(__dmul_rn(s.edx[i], __dsub_rn(py, s.ey[i])), __dmul_rn(s.edy[i], __dsub_rn(px, s.ex[i])));
