@@ -109,7 +109,7 @@ void fa_destroy(fa_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
-    fa_buf* bufs[] = {&c->clip, &c->depth_keys, &c->depth_f64, &c->flags, &c->vis_list, &c->small_list, &c->large,
+    fa_buf* bufs[] = {&c->small_rec, &c->clip, &c->depth_keys, &c->depth_f64, &c->flags, &c->vis_list, &c->small_list, &c->large,
                       &c->tiles, &c->label, &c->vmin, &c->v2c, &c->cidx, &c->roots, &c->ndc_keys, &c->ndc, &c->px,
                       &c->target, &c->survived, &c->okey, &c->oidx, &c->ow, &c->oh, &c->orot, &c->sortk, &c->sortv,
                       &c->pinv, &c->cand, &c->cand_p, &c->cand_w, &c->cand_h, &c->cand_y, &c->rowstart,
@@ -146,6 +146,7 @@ static int ensure_raster(fa_ctx* ctx, int W, int H, bool depth) {
     if (depth) ENSURE(depth_keys, (size_t)W * H * 8);
     ENSURE(flags, ((T + 15) / 16 + 1) * 16);
     ENSURE(small_list, (T + 1) * 4);
+    ENSURE(small_rec, (T + 1) * sizeof(SmallRec));
     long long want_tiles = (long long)W * H / 32;
     if (want_tiles > ctx->max_tiles) ctx->max_tiles = (int)(want_tiles < (1ll << 30) ? want_tiles : (1 << 30));
     ENSURE(large, (size_t)ctx->max_large * sizeof(TriSetup));
@@ -263,7 +264,7 @@ static int launch_depth(fa_ctx* ctx, int W, int H, int cull, unsigned char* flag
     fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), P<int>(ctx->vmin),
                          P<unsigned long long>(ctx->depth_keys), (long long)W * H, flags_out, T, s);
     fa_launch_raster_setup(true, P<double4>(ctx->clip), ctx->tris, T, W, H, cull,
-                           P<unsigned long long>(ctx->depth_keys), P<int>(ctx->small_list), P<TriSetup>(ctx->large),
+                           P<unsigned long long>(ctx->depth_keys), P<int>(ctx->small_list), P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large),
                            ctx->max_large, P<int2>(ctx->tiles), ctx->max_tiles, P<fa_dstat>(ctx->dstat), s);
     fa_launch_raster_depth_tiles(P<TriSetup>(ctx->large), P<int2>(ctx->tiles), ctx->max_tiles, W,
                                  P<unsigned long long>(ctx->depth_keys), P<fa_dstat>(ctx->dstat), s);
@@ -332,9 +333,9 @@ int fa_mark_visible(fa_ctx* ctx, const double* vp_host, const double* depth, int
                              P<unsigned char>(ctx->flags), T, s);
         fa_launch_encode_depth(depth, P<unsigned long long>(ctx->depth_keys), (long long)width * height, s);
         fa_launch_raster_setup(false, P<double4>(ctx->clip), ctx->tris, T, width, height, backface_cull, nullptr,
-                               P<int>(ctx->small_list), P<TriSetup>(ctx->large), ctx->max_large, P<int2>(ctx->tiles),
+                               P<int>(ctx->small_list), P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large), ctx->max_large, P<int2>(ctx->tiles),
                                ctx->max_tiles, P<fa_dstat>(ctx->dstat), s);
-        fa_launch_raster_vis(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->small_list), P<TriSetup>(ctx->large),
+        fa_launch_raster_vis(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->small_list), P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large),
                              P<int2>(ctx->tiles), ctx->max_tiles, T, width, height, backface_cull,
                              P<unsigned long long>(ctx->depth_keys), P<unsigned char>(ctx->flags),
                              P<fa_dstat>(ctx->dstat), s);
@@ -628,14 +629,14 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     nl += 1;
     mark();  // 1: project + clears
     fa_launch_raster_setup(true, P<double4>(ctx->clip), ctx->tris, T, W, H, p->backface_cull,
-                           P<unsigned long long>(ctx->depth_keys), P<int>(ctx->small_list), P<TriSetup>(ctx->large),
+                           P<unsigned long long>(ctx->depth_keys), P<int>(ctx->small_list), P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large),
                            ctx->max_large, P<int2>(ctx->tiles), ctx->max_tiles, st, s);
     fa_launch_raster_depth_tiles(P<TriSetup>(ctx->large), P<int2>(ctx->tiles), ctx->max_tiles, W,
                                  P<unsigned long long>(ctx->depth_keys), st, s);
     fa_launch_count_finite(P<unsigned long long>(ctx->depth_keys), (long long)W * H, st, s);
     nl += 3;
     mark();  // 2: depth pass
-    fa_launch_raster_vis(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->small_list), P<TriSetup>(ctx->large),
+    fa_launch_raster_vis(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->small_list), P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large),
                          P<int2>(ctx->tiles), ctx->max_tiles, T, W, H, p->backface_cull,
                          P<unsigned long long>(ctx->depth_keys), flags, st, s);
     nl += 2;

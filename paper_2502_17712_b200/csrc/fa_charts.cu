@@ -122,14 +122,51 @@ __device__ __forceinline__ int uf_find_ro(const int* parent, int x) {
     return cur;
 }
 
+#ifdef FA_UF_STATS
+// debug build only: [unions, cas attempts, cas failures, find hops, max hops]
+__device__ unsigned long long g_uf_stats[5];
+__device__ __forceinline__ int uf_find_count(int* parent, int x) {
+    volatile int* p = parent;
+    int cur = p[x], hops = 0;
+    if (cur != x) {
+        int next, prev = x;
+        while (cur > (next = p[cur])) {
+            p[prev] = next;
+            prev = cur;
+            cur = next;
+            hops++;
+        }
+    }
+    atomicAdd(&g_uf_stats[3], (unsigned long long)hops);
+    atomicMax(&g_uf_stats[4], (unsigned long long)hops);
+    return cur;
+}
+#define UF_FIND uf_find_count
+extern "C" void fa_debug_uf_stats(unsigned long long* out) {
+    cudaMemcpyFromSymbol(out, g_uf_stats, sizeof(g_uf_stats));
+    unsigned long long z[5] = {0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_uf_stats, z, sizeof(z));
+}
+#else
+#define UF_FIND uf_find
+#endif
+
 __device__ __forceinline__ void uf_union(int* parent, int a, int b) {
-    int ra = uf_find(parent, a), rb = uf_find(parent, b);
+    int ra = UF_FIND(parent, a), rb = UF_FIND(parent, b);
+#ifdef FA_UF_STATS
+    atomicAdd(&g_uf_stats[0], 1ull);
+#endif
+    // ECL-CC hooking: a failed CAS returns the root's new parent, so the
+    // loser climbs one level per round trip instead of re-running finds
     while (ra != rb) {
         if (ra < rb) { int t = ra; ra = rb; rb = t; }
         int old = atomicCAS(parent + ra, ra, rb);
+#ifdef FA_UF_STATS
+        atomicAdd(&g_uf_stats[1], 1ull);
+        if (old != ra) atomicAdd(&g_uf_stats[2], 1ull);
+#endif
         if (old == ra) break;
-        ra = uf_find(parent, old);
-        rb = uf_find(parent, rb);
+        ra = old;
     }
 }
 
@@ -170,11 +207,12 @@ __global__ void k_hook_vertex(const int* __restrict__ tris, const int* __restric
     int stride = gridDim.x * blockDim.x;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
         int t = vis_list[k];
-#pragma unroll
-        for (int j = 0; j < 3; j++) {
-            int u = vmin[__ldg(tris + 3 * t + j)];
-            if (u != t) uf_union(label, t, u);
-        }
+        int u0 = vmin[__ldg(tris + 3 * t)], u1 = vmin[__ldg(tris + 3 * t + 1)], u2 = vmin[__ldg(tris + 3 * t + 2)];
+        // the init already linked t to min(t, u0, u1, u2)
+        int m = min(min(t, u0), min(u1, u2));
+        if (u0 != m && u0 != t) uf_union(label, t, u0);
+        if (u1 != m && u1 != t && u1 != u0) uf_union(label, t, u1);
+        if (u2 != m && u2 != t && u2 != u0 && u2 != u1) uf_union(label, t, u2);
     }
 }
 

@@ -48,7 +48,8 @@ struct fa_dstat {
     int n_rows_max;
     int max_h;            // max oriented height (sort key range)
     unsigned int done;    // pack batch early-exit
-    int pad[45];
+    int n_small3;         // stored small-triangle records (pass 2 input)
+    int pad[44];
 };
 
 // ---- float64 <-> order-preserving u64 key --------------------------------

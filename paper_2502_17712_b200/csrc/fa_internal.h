@@ -7,6 +7,7 @@
 #include "fa_common.cuh"
 
 struct TriSetup;
+struct SmallRec;
 
 // growable device buffer
 struct fa_buf {
@@ -38,7 +39,7 @@ struct fa_ctx {
     int64_t V = 0, T = 0;
 
     // scratch (grown on demand)
-    fa_buf clip, depth_keys, depth_f64, flags, vis_list, small_list, large, tiles, label, vmin, v2c, cidx;
+    fa_buf small_rec, clip, depth_keys, depth_f64, flags, vis_list, small_list, large, tiles, label, vmin, v2c, cidx;
     fa_buf roots, ndc_keys, ndc, px, target, survived, okey, oidx, ow, oh, orot, sortk, sortv, pinv;
     fa_buf cand, cand_p, cand_w, cand_h, cand_y, rowstart, placements, uv, vp_dev, blocks, dstat, aux;
     fa_buf in_tw, in_th, in_cid, in_mt;
@@ -70,11 +71,12 @@ bool fa_ensure(fa_ctx* ctx, fa_buf& b, size_t bytes);
 void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* clip, int* vmin,
                           unsigned long long* depth, long long npx, unsigned char* flags, int T, cudaStream_t s);
 void fa_launch_raster_setup(bool write_depth, const double4* clip, const int* tris, int T, int W, int H, int cull,
-                            unsigned long long* depth, int* small_list, TriSetup* large, int max_large, int2* tiles,
-                            int max_tiles, fa_dstat* st, cudaStream_t s);
+                            unsigned long long* depth, int* small_list, SmallRec* small_rec, TriSetup* large,
+                            int max_large, int2* tiles, int max_tiles, fa_dstat* st, cudaStream_t s);
 void fa_launch_raster_depth_tiles(const TriSetup* large, const int2* tiles, int max_tiles, int W,
                                   unsigned long long* depth, fa_dstat* st, cudaStream_t s);
-void fa_launch_raster_vis(const double4* clip, const int* tris, const int* small_list, const TriSetup* large,
+void fa_launch_raster_vis(const double4* clip, const int* tris, const int* small_list, const SmallRec* small_rec,
+                          const TriSetup* large,
                           const int2* tiles, int max_tiles, int T, int W, int H, int cull,
                           const unsigned long long* depth, unsigned char* flags, const fa_dstat* st, cudaStream_t s);
 void fa_launch_decode_depth(const unsigned long long* keys, double* out, long long n, cudaStream_t s);

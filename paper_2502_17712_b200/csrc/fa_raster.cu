@@ -69,18 +69,20 @@ __global__ void k_encode_depth(const double* __restrict__ in, unsigned long long
 // ---- pass 1: setup + small raster + large enqueue -------------------------
 // WRITE_DEPTH=false builds the work lists only (standalone mark_visible).
 template <bool WRITE_DEPTH>
-__global__ void __launch_bounds__(256) k_raster_setup(const double4* __restrict__ clip, const int* __restrict__ tris,
+__global__ void __launch_bounds__(256, 3) k_raster_setup(const double4* __restrict__ clip, const int* __restrict__ tris,
                                                       int T, int W, int H, int cull,
                                                       unsigned long long* __restrict__ depth,
-                                                      int* __restrict__ small_list, TriSetup* __restrict__ large,
+                                                      int* __restrict__ small_list, SmallRec* __restrict__ small_rec,
+                                                      TriSetup* __restrict__ large,
                                                       int max_large, int2* __restrict__ tiles, int max_tiles,
                                                       fa_dstat* __restrict__ st) {
     int stride = gridDim.x * blockDim.x;
+    const bool rec_ok = W <= 32767 && H <= 32767;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += stride) {
         Setup3 f;
         int r3 = tri_setup3(clip, tris, t, W, H, cull != 0, f);
         if (r3 == 0) continue;
-        if (r3 == 1) {
+        if (r3 == 1 && rec_ok) {
             int bw = f.max_x - f.min_x + 1, bh = f.max_y - f.min_y + 1;
             if (bw * bh <= FA_SMALL_PX) {
                 // unclipped small triangle: registers only, fire-and-forget RED.MIN
@@ -93,8 +95,7 @@ __global__ void __launch_bounds__(256) k_raster_setup(const double4* __restrict_
                         if (!sample_inside3(f, px, py)) continue;
                         covered = true;
                         if (WRITE_DEPTH) {
-                            unsigned long long key = f64_key(sample_depth3(f, px, py));
-                            if (key < row[ix]) atomicMin(row + ix, key);
+                            atomicMin(row + ix, f64_key(sample_depth3(f, px, py)));
                         } else {
                             break;
                         }
@@ -102,8 +103,8 @@ __global__ void __launch_bounds__(256) k_raster_setup(const double4* __restrict_
                     if (!WRITE_DEPTH && covered) break;
                 }
                 if (covered) {
-                    int slot = active_append1(&st->n_small);
-                    small_list[slot] = t;
+                    int slot = active_append1(&st->n_small3);
+                    store_rec(f, t, small_rec + slot);
                 }
                 continue;
             }
@@ -220,31 +221,47 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const TriSetup* __re
 
 // ---- pass 2 small: one thread per covering triangle -----------------------
 __global__ void __launch_bounds__(256) k_raster_vis_small(const double4* __restrict__ clip, const int* __restrict__ tris,
-                                                          const int* __restrict__ small_list, int W, int H, int cull,
-                                                          const unsigned long long* __restrict__ depth,
+                                                          const int* __restrict__ small_list,
+                                                          const SmallRec* __restrict__ small_rec, int W, int H,
+                                                          int cull, const unsigned long long* __restrict__ depth,
                                                           unsigned char* __restrict__ flags,
                                                           const fa_dstat* __restrict__ st) {
+    int n3 = st->n_small3;
     int n = st->n_small;
     int stride = gridDim.x * blockDim.x;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        int t = small_list[i];
+    // stored records: gather up to 4 covered samples, then issue their depth
+    // loads together (independent loads instead of one round trip each)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n3; i += stride) {
         Setup3 f;
-        int r3 = tri_setup3(clip, tris, t, W, H, cull != 0, f);
-        if (r3 == 0) continue;
+        int t;
+        load_rec(small_rec + i, f, t);
         bool vis = false;
-        if (r3 == 1) {
-            for (int iy = f.min_y; iy <= f.max_y && !vis; iy++) {
-                double py = (double)iy + 0.5;
-                const unsigned long long* row = depth + (long long)iy * W;
-                for (int ix = f.min_x; ix <= f.max_x; ix++) {
-                    double px = (double)ix + 0.5;
-                    if (!sample_inside3(f, px, py)) continue;
-                    if (depth_passes(sample_depth3(f, px, py), key_f64(row[ix]))) { vis = true; break; }
+        double zq[4];
+        const unsigned long long* aq[4];
+        int nq = 0;
+        for (int iy = f.min_y; iy <= f.max_y && !vis; iy++) {
+            double py = (double)iy + 0.5;
+            const unsigned long long* row = depth + (long long)iy * W;
+            for (int ix = f.min_x; ix <= f.max_x; ix++) {
+                double px = (double)ix + 0.5;
+                if (!sample_inside3(f, px, py)) continue;
+                zq[nq] = sample_depth3(f, px, py);
+                aq[nq] = row + ix;
+                if (++nq == 4) {
+                    unsigned long long k0 = aq[0][0], k1 = aq[1][0], k2 = aq[2][0], k3 = aq[3][0];
+                    vis = depth_passes(zq[0], key_f64(k0)) || depth_passes(zq[1], key_f64(k1)) ||
+                          depth_passes(zq[2], key_f64(k2)) || depth_passes(zq[3], key_f64(k3));
+                    nq = 0;
+                    if (vis) break;
                 }
             }
-            if (vis) flags[t] = 1;
-            continue;
         }
+        for (int q = 0; q < nq && !vis; q++) vis = depth_passes(zq[q], key_f64(*aq[q]));
+        if (vis) flags[t] = 1;
+    }
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        int t = small_list[i];
+        bool vis = false;
         TriSetup s;
         if (tri_setup(clip, tris, t, W, H, cull != 0, s) <= 0) continue;
         for (int iy = s.min_y; iy <= s.max_y && !vis; iy++) {
@@ -314,14 +331,14 @@ void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* c
 }
 
 void fa_launch_raster_setup(bool write_depth, const double4* clip, const int* tris, int T, int W, int H, int cull,
-                            unsigned long long* depth, int* small_list, TriSetup* large, int max_large, int2* tiles,
-                            int max_tiles, fa_dstat* st, cudaStream_t s) {
+                            unsigned long long* depth, int* small_list, SmallRec* small_rec, TriSetup* large,
+                            int max_large, int2* tiles, int max_tiles, fa_dstat* st, cudaStream_t s) {
     int grid = fa_grid(T, 256, FA_NUM_SMS * 16);
     if (write_depth)
-        k_raster_setup<true><<<grid, 256, 0, s>>>(clip, tris, T, W, H, cull, depth, small_list, large, max_large,
+        k_raster_setup<true><<<grid, 256, 0, s>>>(clip, tris, T, W, H, cull, depth, small_list, small_rec, large, max_large,
                                                   tiles, max_tiles, st);
     else
-        k_raster_setup<false><<<grid, 256, 0, s>>>(clip, tris, T, W, H, cull, depth, small_list, large, max_large,
+        k_raster_setup<false><<<grid, 256, 0, s>>>(clip, tris, T, W, H, cull, depth, small_list, small_rec, large, max_large,
                                                    tiles, max_tiles, st);
 }
 
@@ -330,12 +347,13 @@ void fa_launch_raster_depth_tiles(const TriSetup* large, const int2* tiles, int 
     k_raster_depth_tiles<<<FA_NUM_SMS * 8, 256, 0, s>>>(large, tiles, W, depth, st, max_tiles);
 }
 
-void fa_launch_raster_vis(const double4* clip, const int* tris, const int* small_list, const TriSetup* large,
+void fa_launch_raster_vis(const double4* clip, const int* tris, const int* small_list, const SmallRec* small_rec,
+                          const TriSetup* large,
                           const int2* tiles, int max_tiles, int T, int W, int H, int cull,
                           const unsigned long long* depth, unsigned char* flags, const fa_dstat* st,
                           cudaStream_t s) {
-    k_raster_vis_small<<<fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s>>>(clip, tris, small_list, W, H, cull, depth,
-                                                                       flags, st);
+    k_raster_vis_small<<<fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s>>>(clip, tris, small_list, small_rec, W, H, cull,
+                                                                       depth, flags, st);
     k_raster_vis_tiles<<<FA_NUM_SMS * 8, 256, 0, s>>>(large, tiles, W, depth, flags, st, max_tiles);
 }
 

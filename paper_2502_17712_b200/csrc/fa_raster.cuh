@@ -263,9 +263,45 @@ __device__ __forceinline__ int tri_setup3(const double4* __restrict__ clip, cons
         __dadd_rn(c2.w, c2.x) >= 0 && __dsub_rn(c2.w, c2.x) >= 0 && __dadd_rn(c2.w, c2.y) >= 0 &&
         __dsub_rn(c2.w, c2.y) >= 0 && __dadd_rn(c2.w, c2.z) >= 0 && __dsub_rn(c2.w, c2.z) >= 0;
     if (!inside) {
-        bool anyp = __dsub_rn(c0.w, FA_W_EPSILON) > 0 || __dsub_rn(c1.w, FA_W_EPSILON) > 0 ||
-                    __dsub_rn(c2.w, FA_W_EPSILON) > 0;
-        return anyp ? 2 : 0;
+        bool f0 = __dsub_rn(c0.w, FA_W_EPSILON) > 0, f1 = __dsub_rn(c1.w, FA_W_EPSILON) > 0,
+             f2 = __dsub_rn(c2.w, FA_W_EPSILON) > 0;
+        if (!(f0 || f1 || f2)) return 0;
+        if (f0 && f1 && f2) {
+            // Exact trivial reject (charts.py:168-174): find the first plane in
+            // L,R,B,T,N,F order that is not passed by all three vertices; every
+            // earlier plane leaves the triangle untouched, so if all three
+            // vertices fail this one, Sutherland-Hodgman returns an empty polygon.
+            const double4 c[3] = {c0, c1, c2};
+#pragma unroll
+            for (int p = 0; p < 6; p++) {
+                int ge = 0, lt = 0;
+#pragma unroll
+                for (int i = 0; i < 3; i++) {
+                    double a = (p >> 1) == 0 ? c[i].x : ((p >> 1) == 1 ? c[i].y : c[i].z);
+                    double d = (p & 1) ? __dsub_rn(c[i].w, a) : __dadd_rn(c[i].w, a);
+                    ge += d >= 0;
+                    lt += d < 0;
+                }
+                if (ge == 3) continue;
+                if (lt == 3) return 0;
+                break;
+            }
+        }
+        return 2;
+    }
+    if (cull) {
+        // Back-face pre-filter.  For w_i > 0 the screen shoelace sign equals
+        // sign(D), D = det[x y w] of the clip vertices (screen area =
+        // W*H/4 * D/(w0 w1 w2)).  Inside the frustum |x|,|y| <= w, so both D's
+        // rounding error (~20 eps |w0w1w2|) and the reference shoelace's
+        // (~1e-13 W*H) are far below the 1e-8 |w0w1w2| margin: a D under the
+        // margin is certainly culled by the exact test (charts.py:213-218).
+        double m0 = __dsub_rn(__dmul_rn(c1.y, c2.w), __dmul_rn(c2.y, c1.w));
+        double m1 = __dsub_rn(__dmul_rn(c0.y, c2.w), __dmul_rn(c2.y, c0.w));
+        double m2 = __dsub_rn(__dmul_rn(c0.y, c1.w), __dmul_rn(c1.y, c0.w));
+        double D = __dadd_rn(__dsub_rn(__dmul_rn(c0.x, m0), __dmul_rn(c1.x, m1)), __dmul_rn(c2.x, m2));
+        double wp = __dmul_rn(__dmul_rn(c0.w, c1.w), c2.w);
+        if (D < -1e-8 * wp) return 0;
     }
     double x0 = screen_x(c0.x, c0.w, W), y0 = screen_x(c0.y, c0.w, H), z0 = __ddiv_rn(c0.z, c0.w);
     double x1 = screen_x(c1.x, c1.w, W), y1 = screen_x(c1.y, c1.w, H), z1 = __ddiv_rn(c1.z, c1.w);
@@ -312,6 +348,43 @@ __device__ __forceinline__ int tri_setup3(const double4* __restrict__ clip, cons
         s.zmean = __ddiv_rn(__dadd_rn(__dadd_rn(__dadd_rn(-0.0, z0), z1), z2), 3.0);
     }
     return 1;
+}
+
+// Compact record of a covered small unclipped triangle, written by pass 1 so
+// pass 2 never repeats the projection divides.  Edges are re-derived from the
+// vertices with the same DSUBs, so the sample tests are bit-identical.
+struct __align__(16) SmallRec {
+    double x0, y0, x1, y1, x2, y2;  // screen vertices after the cull/flip
+    double z0, g0, g1;              // plane (gx, gy) or (zmean, unused)
+    int t;
+    short min_x, max_x, min_y, max_y;
+    int flags;                      // bits 0-2 incl, bit 3 use_plane
+};
+
+__device__ __forceinline__ void store_rec(const Setup3& s, int t, SmallRec* r) {
+    SmallRec q;
+    q.x0 = s.ax0; q.y0 = s.ay0; q.x1 = s.ax1; q.y1 = s.ay1; q.x2 = s.ax2; q.y2 = s.ay2;
+    q.z0 = s.p0z;
+    q.g0 = s.use_plane ? s.gx : s.zmean;
+    q.g1 = s.gy;
+    q.t = t;
+    q.min_x = (short)s.min_x; q.max_x = (short)s.max_x; q.min_y = (short)s.min_y; q.max_y = (short)s.max_y;
+    q.flags = s.incl | (s.use_plane ? 8 : 0);
+    *r = q;
+}
+
+__device__ __forceinline__ void load_rec(const SmallRec* __restrict__ r, Setup3& s, int& t) {
+    SmallRec q = *r;
+    s.ax0 = q.x0; s.ay0 = q.y0; s.ax1 = q.x1; s.ay1 = q.y1; s.ax2 = q.x2; s.ay2 = q.y2;
+    s.dx0 = __dsub_rn(q.x1, q.x0); s.dy0 = __dsub_rn(q.y1, q.y0);
+    s.dx1 = __dsub_rn(q.x2, q.x1); s.dy1 = __dsub_rn(q.y2, q.y1);
+    s.dx2 = __dsub_rn(q.x0, q.x2); s.dy2 = __dsub_rn(q.y0, q.y2);
+    s.incl = q.flags & 7;
+    s.use_plane = (q.flags >> 3) & 1;
+    s.p0x = q.x0; s.p0y = q.y0; s.p0z = q.z0;
+    s.gx = q.g0; s.gy = q.g1; s.zmean = q.g0;
+    s.min_x = q.min_x; s.max_x = q.max_x; s.min_y = q.min_y; s.max_y = q.max_y;
+    t = q.t;
 }
 
 __device__ __forceinline__ bool edge_ok(double ax, double ay, double dx, double dy, bool incl, double px, double py) {
