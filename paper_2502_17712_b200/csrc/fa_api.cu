@@ -268,7 +268,7 @@ static int launch_depth(fa_ctx* ctx, int W, int H, int cull, unsigned char* flag
                            ctx->max_large, P<int2>(ctx->tiles), ctx->max_tiles, P<fa_dstat>(ctx->dstat), s);
     fa_launch_raster_depth_tiles(P<TriSetup>(ctx->large), P<int2>(ctx->tiles), ctx->max_tiles, W,
                                  P<unsigned long long>(ctx->depth_keys), P<fa_dstat>(ctx->dstat), s);
-    nl += 3;
+    nl += 4;
     return FA_OK;
 }
 
@@ -336,7 +336,7 @@ int fa_mark_visible(fa_ctx* ctx, const double* vp_host, const double* depth, int
                                P<int>(ctx->small_list), P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large), ctx->max_large, P<int2>(ctx->tiles),
                                ctx->max_tiles, P<fa_dstat>(ctx->dstat), s);
         fa_launch_raster_vis(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->small_list), P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large),
-                             P<int2>(ctx->tiles), ctx->max_tiles, T, width, height, backface_cull,
+                             P<int2>(ctx->tiles), ctx->max_tiles, ctx->max_large, T,width, height, backface_cull,
                              P<unsigned long long>(ctx->depth_keys), P<unsigned char>(ctx->flags),
                              P<fa_dstat>(ctx->dstat), s);
         CKL();
@@ -634,12 +634,12 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     fa_launch_raster_depth_tiles(P<TriSetup>(ctx->large), P<int2>(ctx->tiles), ctx->max_tiles, W,
                                  P<unsigned long long>(ctx->depth_keys), st, s);
     fa_launch_count_finite(P<unsigned long long>(ctx->depth_keys), (long long)W * H, st, s);
-    nl += 3;
+    nl += 4;
     mark();  // 2: depth pass
     fa_launch_raster_vis(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->small_list), P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large),
-                         P<int2>(ctx->tiles), ctx->max_tiles, T, W, H, p->backface_cull,
+                         P<int2>(ctx->tiles), ctx->max_tiles, ctx->max_large, T,W, H, p->backface_cull,
                          P<unsigned long long>(ctx->depth_keys), flags, st, s);
-    nl += 2;
+    nl += 3;  // records + generic small, centre tiles, remaining tiles
     mark();  // 3: visibility pass
     fa_launch_compact_visible(flags, T, P<int>(ctx->blocks), P<int>(ctx->vis_list), P<int>(ctx->label), st, s);
     nl += 2;

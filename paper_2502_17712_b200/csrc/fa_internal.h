@@ -77,10 +77,12 @@ void fa_launch_raster_depth_tiles(const TriSetup* large, const int2* tiles, int 
                                   unsigned long long* depth, fa_dstat* st, cudaStream_t s);
 void fa_launch_raster_vis(const double4* clip, const int* tris, const int* small_list, const SmallRec* small_rec,
                           const TriSetup* large,
-                          const int2* tiles, int max_tiles, int T, int W, int H, int cull,
+                          const int2* tiles, int max_tiles, int max_large, int T, int W, int H, int cull,
                           const unsigned long long* depth, unsigned char* flags, const fa_dstat* st, cudaStream_t s);
 void fa_launch_decode_depth(const unsigned long long* keys, double* out, long long n, cudaStream_t s);
 void fa_launch_count_finite(const unsigned long long* depth, long long npx, fa_dstat* st, cudaStream_t s);
+void fa_launch_small_coop(bool vis, const SmallRec* recs, int T, int W, unsigned long long* depth,
+                          unsigned char* flags, const fa_dstat* st, cudaStream_t s);
 void fa_launch_encode_depth(const double* in, unsigned long long* keys, long long n, cudaStream_t s);
 size_t fa_trisetup_bytes();
 

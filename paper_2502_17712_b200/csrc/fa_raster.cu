@@ -85,27 +85,9 @@ __global__ void __launch_bounds__(256, 3) k_raster_setup(const double4* __restri
         if (r3 == 1 && rec_ok) {
             int bw = f.max_x - f.min_x + 1, bh = f.max_y - f.min_y + 1;
             if (bw * bh <= FA_SMALL_PX) {
-                // unclipped small triangle: registers only, fire-and-forget RED.MIN
-                bool covered = false;
-                for (int iy = f.min_y; iy <= f.max_y; iy++) {
-                    double py = (double)iy + 0.5;
-                    unsigned long long* row = depth + (long long)iy * W;
-                    for (int ix = f.min_x; ix <= f.max_x; ix++) {
-                        double px = (double)ix + 0.5;
-                        if (!sample_inside3(f, px, py)) continue;
-                        covered = true;
-                        if (WRITE_DEPTH) {
-                            atomicMin(row + ix, f64_key(sample_depth3(f, px, py)));
-                        } else {
-                            break;
-                        }
-                    }
-                    if (!WRITE_DEPTH && covered) break;
-                }
-                if (covered) {
-                    int slot = active_append1(&st->n_small3);
-                    store_rec(f, t, small_rec + slot);
-                }
+                // unclipped small triangle: record it; k_small_coop samples it
+                int slot = active_append1(&st->n_small3);
+                store_rec(f, t, small_rec + slot);
                 continue;
             }
         }
@@ -219,6 +201,143 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const TriSetup* __re
     }
 }
 
+// ---- small unclipped triangles: warp-cooperative sampling ------------------
+// A warp stages 32 records in shared memory, prefix-sums their bbox sample
+// counts, and gives every lane one contiguous, equal chunk of the combined
+// sample space, so per-triangle size differences no longer diverge the warp.
+// VIS = false: depth pass (RED.MIN.64 per covered sample).
+// VIS = true: visibility pass (any covered sample passing the slack test sets
+// the flag; a per-record shared "done" bit lets other lanes skip the rest).
+#define COOP_WARPS 8
+struct CoopWarp {
+    SmallRec rec[32];
+    int prefix[33];
+    int done[32];
+};
+
+__device__ __forceinline__ void coop_locate(const Setup3& f, int li, int bw, double& px, double& py, int& ix, int& iy) {
+    int dy = li / bw;
+    iy = f.min_y + dy;
+    ix = f.min_x + (li - dy * bw);
+    px = (double)ix + 0.5;
+    py = (double)iy + 0.5;
+}
+
+template <bool VIS>
+__global__ void __launch_bounds__(COOP_WARPS * 32) k_small_coop(const SmallRec* __restrict__ recs, int W,
+                                                                unsigned long long* __restrict__ depth,
+                                                                unsigned char* __restrict__ flags,
+                                                                const fa_dstat* __restrict__ st) {
+    __shared__ CoopWarp sh[COOP_WARPS];
+    const int warp = threadIdx.x >> 5, lane = lane_id();
+    CoopWarp& cw = sh[warp];
+    const int n = st->n_small3;
+    const int total_warps = gridDim.x * COOP_WARPS;
+    for (int base = (blockIdx.x * COOP_WARPS + warp) * 32; base < n; base += total_warps * 32) {
+        const int cnt = min(32, n - base);
+        int np = 0;
+        if (lane < cnt) {
+            const uint4* src = reinterpret_cast<const uint4*>(recs + base + lane);
+            uint4* dst = reinterpret_cast<uint4*>(&cw.rec[lane]);
+#pragma unroll
+            for (int q = 0; q < (int)(sizeof(SmallRec) / 16); q++) dst[q] = __ldg(src + q);
+            const SmallRec& r = cw.rec[lane];
+            np = (r.max_x - r.min_x + 1) * (r.max_y - r.min_y + 1);
+        }
+        int incl = np;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        cw.prefix[lane + 1] = incl;
+        if (lane == 0) cw.prefix[0] = 0;
+        cw.done[lane] = 0;
+        __syncwarp();
+        const int S = __shfl_sync(0xffffffffu, incl, 31);
+        const int chunk = (S + 31) >> 5;
+        int s = lane * chunk;
+        const int s_end = min(S, s + chunk);
+        if (s < s_end) {
+            // record holding sample s: largest r with prefix[r] <= s
+            int lo = 0, hi = cnt - 1;
+            while (lo < hi) {
+                int mid = (lo + hi + 1) >> 1;
+                if (cw.prefix[mid] <= s) lo = mid; else hi = mid - 1;
+            }
+            int r = lo;
+            Setup3 f;
+            int t;
+            load_rec(&cw.rec[r], f, t);
+            int bw = f.max_x - f.min_x + 1;
+            int pr = cw.prefix[r], pe = cw.prefix[r + 1];
+            if (!VIS) {
+                for (; s < s_end; s++) {
+                    while (s >= pe) {
+                        r++;
+                        load_rec(&cw.rec[r], f, t);
+                        bw = f.max_x - f.min_x + 1;
+                        pr = pe;
+                        pe = cw.prefix[r + 1];
+                    }
+                    double px, py;
+                    int ix, iy;
+                    coop_locate(f, s - pr, bw, px, py, ix, iy);
+                    if (sample_inside3(f, px, py))
+                        atomicMin(depth + (long long)iy * W + ix, f64_key(sample_depth3(f, px, py)));
+                }
+            } else {
+                // gather up to 4 covered samples (possibly of different
+                // records), then issue their depth loads together
+                double zq[4];
+                const unsigned long long* aq[4];
+                int rq[4], tq[4];
+                int nq = 0;
+                bool skip = cw.done[r] != 0;
+                for (; s < s_end; s++) {
+                    while (s >= pe) {
+                        r++;
+                        load_rec(&cw.rec[r], f, t);
+                        bw = f.max_x - f.min_x + 1;
+                        pr = pe;
+                        pe = cw.prefix[r + 1];
+                        skip = cw.done[r] != 0;
+                    }
+                    if (skip) { s = pe - 1; continue; }
+                    double px, py;
+                    int ix, iy;
+                    coop_locate(f, s - pr, bw, px, py, ix, iy);
+                    if (!sample_inside3(f, px, py)) continue;
+                    zq[nq] = sample_depth3(f, px, py);
+                    aq[nq] = depth + (long long)iy * W + ix;
+                    rq[nq] = r;
+                    tq[nq] = t;
+                    if (++nq == 4) {
+                        unsigned long long k0 = aq[0][0], k1 = aq[1][0], k2 = aq[2][0], k3 = aq[3][0];
+                        unsigned long long kk[4] = {k0, k1, k2, k3};
+#pragma unroll
+                        for (int q = 0; q < 4; q++) {
+                            if (depth_passes(zq[q], key_f64(kk[q]))) {
+                                flags[tq[q]] = 1;
+                                cw.done[rq[q]] = 1;
+                            }
+                        }
+                        nq = 0;
+                        skip = cw.done[r] != 0;
+                    }
+                }
+                for (int q = 0; q < nq; q++) {
+                    if (depth_passes(zq[q], key_f64(*aq[q]))) {
+                        flags[tq[q]] = 1;
+                        cw.done[rq[q]] = 1;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
 // ---- pass 2 small: one thread per covering triangle -----------------------
 __global__ void __launch_bounds__(256) k_raster_vis_small(const double4* __restrict__ clip, const int* __restrict__ tris,
                                                           const int* __restrict__ small_list,
@@ -229,8 +348,8 @@ __global__ void __launch_bounds__(256) k_raster_vis_small(const double4* __restr
     int n3 = st->n_small3;
     int n = st->n_small;
     int stride = gridDim.x * blockDim.x;
-    // stored records: gather up to 4 covered samples, then issue their depth
-    // loads together (independent loads instead of one round trip each)
+    // stored records, one thread each: stop at the first passing sample;
+    // gather up to 4 covered samples, then issue their depth loads together
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n3; i += stride) {
         Setup3 f;
         int t;
@@ -259,6 +378,7 @@ __global__ void __launch_bounds__(256) k_raster_vis_small(const double4* __restr
         for (int q = 0; q < nq && !vis; q++) vis = depth_passes(zq[q], key_f64(*aq[q]));
         if (vis) flags[t] = 1;
     }
+    // generic (clipped) small triangles: full setup again (rare)
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         int t = small_list[i];
         bool vis = false;
@@ -283,13 +403,23 @@ __global__ void __launch_bounds__(256) k_raster_vis_tiles(const TriSetup* __rest
                                                           const int2* __restrict__ tiles, int W,
                                                           const unsigned long long* __restrict__ depth,
                                                           unsigned char* __restrict__ flags,
-                                                          const fa_dstat* __restrict__ st, int max_tiles) {
+                                                          const fa_dstat* __restrict__ st, int max_tiles,
+                                                          int max_large, int phase) {
+    // phase 0: the tile at the centre of each large triangle's bbox (most
+    // visible triangles are decided there); phase 1: every other tile of the
+    // triangles that are still not visible.
     __shared__ TriSetup sm[8];
     int warp = threadIdx.x >> 5, lane = lane_id();
     int nwarps = gridDim.x * 8;
-    int n_tiles = min(st->n_tiles, max_tiles);
-    for (int w = blockIdx.x * 8 + warp; w < n_tiles; w += nwarps) {
-        int2 rec = tiles[w];
+    int n_items = phase == 0 ? min(st->n_large, max_large) : min(st->n_tiles, max_tiles);
+    for (int w = blockIdx.x * 8 + warp; w < n_items; w += nwarps) {
+        int2 rec;
+        if (phase == 0) {
+            rec.x = w;
+            rec.y = -1;
+        } else {
+            rec = tiles[w];
+        }
         int t = __ldg(&large[rec.x].tri);
         int seen = 0;
         if (lane == 0) seen = *(volatile unsigned char*)(flags + t);
@@ -299,6 +429,9 @@ __global__ void __launch_bounds__(256) k_raster_vis_tiles(const TriSetup* __rest
         const TriSetup& s = sm[warp];
         int bw = s.max_x - s.min_x + 1;
         int tx = (bw + TILE_W - 1) / TILE_W;
+        int centre = ((s.max_y - s.min_y + 1) / 2 / TILE_H) * tx + (bw / 2) / TILE_W;
+        if (phase == 0) rec.y = centre;
+        else if (rec.y == centre) continue;
         int x = s.min_x + (rec.y % tx) * TILE_W + (lane & 15);
         int y0 = s.min_y + (rec.y / tx) * TILE_H + (lane >> 4);
         bool vis = false;
@@ -340,6 +473,8 @@ void fa_launch_raster_setup(bool write_depth, const double4* clip, const int* tr
     else
         k_raster_setup<false><<<grid, 256, 0, s>>>(clip, tris, T, W, H, cull, depth, small_list, small_rec, large, max_large,
                                                    tiles, max_tiles, st);
+    // depth pass: sample the recorded small triangles (warp-cooperative)
+    if (write_depth) fa_launch_small_coop(false, small_rec, T, W, depth, nullptr, st, s);
 }
 
 void fa_launch_raster_depth_tiles(const TriSetup* large, const int2* tiles, int max_tiles, int W,
@@ -349,12 +484,22 @@ void fa_launch_raster_depth_tiles(const TriSetup* large, const int2* tiles, int 
 
 void fa_launch_raster_vis(const double4* clip, const int* tris, const int* small_list, const SmallRec* small_rec,
                           const TriSetup* large,
-                          const int2* tiles, int max_tiles, int T, int W, int H, int cull,
+                          const int2* tiles, int max_tiles, int max_large, int T, int W, int H, int cull,
                           const unsigned long long* depth, unsigned char* flags, const fa_dstat* st,
                           cudaStream_t s) {
     k_raster_vis_small<<<fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s>>>(clip, tris, small_list, small_rec, W, H, cull,
                                                                        depth, flags, st);
-    k_raster_vis_tiles<<<FA_NUM_SMS * 8, 256, 0, s>>>(large, tiles, W, depth, flags, st, max_tiles);
+    k_raster_vis_tiles<<<FA_NUM_SMS * 8, 256, 0, s>>>(large, tiles, W, depth, flags, st, max_tiles, max_large, 0);
+    k_raster_vis_tiles<<<FA_NUM_SMS * 8, 256, 0, s>>>(large, tiles, W, depth, flags, st, max_tiles, max_large, 1);
+}
+
+void fa_launch_small_coop(bool vis, const SmallRec* recs, int T, int W, unsigned long long* depth,
+                          unsigned char* flags, const fa_dstat* st, cudaStream_t s) {
+    int grid = fa_grid((long long)T, COOP_WARPS * 32 * 2, FA_NUM_SMS * 6);
+    if (vis)
+        k_small_coop<true><<<grid, COOP_WARPS * 32, 0, s>>>(recs, W, depth, flags, st);
+    else
+        k_small_coop<false><<<grid, COOP_WARPS * 32, 0, s>>>(recs, W, depth, flags, st);
 }
 
 void fa_launch_count_finite(const unsigned long long* depth, long long npx, fa_dstat* st, cudaStream_t s) {
