@@ -14,7 +14,9 @@
 #include "fa_internal.h"
 #include "fa_raster.cuh"
 
+#ifndef FA_SMALL_PX
 #define FA_SMALL_PX 48
+#endif
 #define TILE_W 16
 #define TILE_H 8
 
@@ -272,19 +274,29 @@ __global__ void __launch_bounds__(COOP_WARPS * 32) k_small_coop(const SmallRec* 
             int bw = f.max_x - f.min_x + 1;
             int pr = cw.prefix[r], pe = cw.prefix[r + 1];
             if (!VIS) {
+                // consecutive samples: step (ix, iy) instead of dividing per sample
+                double px, py;
+                int ix, iy;
+                coop_locate(f, s - pr, bw, px, py, ix, iy);
                 for (; s < s_end; s++) {
-                    while (s >= pe) {
-                        r++;
+                    if (s >= pe) {
+                        do {
+                            r++;
+                            pr = pe;
+                            pe = cw.prefix[r + 1];
+                        } while (s >= pe);
                         load_rec(&cw.rec[r], f, t);
-                        bw = f.max_x - f.min_x + 1;
-                        pr = pe;
-                        pe = cw.prefix[r + 1];
+                        ix = f.min_x;
+                        iy = f.min_y;
                     }
-                    double px, py;
-                    int ix, iy;
-                    coop_locate(f, s - pr, bw, px, py, ix, iy);
+                    px = (double)ix + 0.5;
+                    py = (double)iy + 0.5;
                     if (sample_inside3(f, px, py))
                         atomicMin(depth + (long long)iy * W + ix, f64_key(sample_depth3(f, px, py)));
+                    if (++ix > f.max_x) {
+                        ix = f.min_x;
+                        iy++;
+                    }
                 }
             } else {
                 // gather up to 4 covered samples (possibly of different
