@@ -169,15 +169,22 @@ __device__ __forceinline__ long long block_exclusive_scan_ll(long long v, long l
     return base + x - v;
 }
 
+// Block reductions: warp shuffles, then warp 0 reduces the per-warp partials
+// and broadcasts through slot 32.  smem32 must hold 33 entries.  Two barriers;
+// the broadcast slot is only rewritten after the next call's first barrier,
+// which every reader of the previous value has passed.
 __device__ __forceinline__ long long block_max_ll(long long v, long long* smem32) {
     int lane = lane_id(), wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     v = warp_max_ll(v);
     if (lane == 0) smem32[wid] = v;
     __syncthreads();
-    long long r = smem32[0];
-    for (int i = 1; i < nw; i++) r = r > smem32[i] ? r : smem32[i];
+    if (wid == 0) {
+        long long x = lane < nw ? smem32[lane] : (long long)0x8000000000000000ll;
+        x = warp_max_ll(x);
+        if (lane == 0) smem32[32] = x;
+    }
     __syncthreads();
-    return r;
+    return smem32[32];
 }
 
 __device__ __forceinline__ long long block_sum_ll(long long v, long long* smem32) {
@@ -185,10 +192,13 @@ __device__ __forceinline__ long long block_sum_ll(long long v, long long* smem32
     v = warp_sum(v);
     if (lane == 0) smem32[wid] = v;
     __syncthreads();
-    long long r = 0;
-    for (int i = 0; i < nw; i++) r += smem32[i];
+    if (wid == 0) {
+        long long x = lane < nw ? smem32[lane] : 0;
+        x = warp_sum(x);
+        if (lane == 0) smem32[32] = x;
+    }
     __syncthreads();
-    return r;
+    return smem32[32];
 }
 
 static inline int fa_grid(long long n, int block, int max_blocks) {

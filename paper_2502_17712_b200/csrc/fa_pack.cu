@@ -18,7 +18,9 @@
 // semantics; the snap uses 128-bit intermediates.
 #include "fa_internal.h"
 
-#define PK_THREADS 1024
+#ifndef PK_THREADS
+#define PK_THREADS 512  // measured on B200: 512 > 1024 > 256 threads per candidate CTA at C2
+#endif
 #define SORT_THREADS 1024
 
 // numpy int64 semantics of -((-num * t) // den) (packing.py:349)
@@ -131,7 +133,7 @@ struct SortSmem {
     int hist[256];
     int base[256];
     int wcnt[32][257];
-    long long red[32];
+    long long red[33];
     int flag;
 };
 
@@ -297,7 +299,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_orient_sort(const long long* _
 // packing candidates
 // ============================================================================
 struct PackSmem {
-    long long red[32];
+    long long red[33];
     int red_i[32];
     int flag;
 };
@@ -475,7 +477,7 @@ __global__ void __launch_bounds__(1024) k_select(const long long* __restrict__ o
                                                  const int* __restrict__ cand_w, const int* __restrict__ cand_h,
                                                  const int* __restrict__ cand_y, long long* __restrict__ placements,
                                                  unsigned char* __restrict__ accept_out, fa_dstat* __restrict__ st) {
-    __shared__ long long red[32];
+    __shared__ long long red[33];
     __shared__ long long s_best;
     int n = n_dev ? *n_dev : n_max;
     int tid = threadIdx.x;
@@ -546,7 +548,7 @@ __global__ void __launch_bounds__(1024) k_select(const long long* __restrict__ o
 __global__ void __launch_bounds__(1024) k_fold(const long long* __restrict__ w, int n, long long omega,
                                                long long* __restrict__ rows, long long* __restrict__ xs,
                                                long long* __restrict__ m_out) {
-    __shared__ long long red[32];
+    __shared__ long long red[33];
     int kbits = 63 - __clzll(omega);
     long long carry = 0, mloc = -(1ll << 62);
     for (int c0 = 0; c0 < n; c0 += blockDim.x) {
@@ -574,7 +576,7 @@ __global__ void __launch_bounds__(1024) k_push_up(const long long* __restrict__ 
                                                   long long* __restrict__ y, long long* __restrict__ used_out,
                                                   int* gfront) {
     extern __shared__ int dyn_front[];
-    __shared__ long long red[32];
+    __shared__ long long red[33];
     int* front = gfront ? gfront : dyn_front;
     int tid = threadIdx.x;
     for (int c = tid; c <= omega; c += blockDim.x) front[c] = 0;
