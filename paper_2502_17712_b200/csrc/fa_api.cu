@@ -644,10 +644,10 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     fa_launch_compact_visible(flags, T, P<int>(ctx->blocks), P<int>(ctx->vis_list), P<int>(ctx->label), st, s);
     nl += 2;
     mark();  // 4: visible compaction
-    fa_launch_uf_vertex(ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->vmin), P<int>(ctx->label), T, st, s);
+    nl += fa_launch_uf_vertex(ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->vmin), P<int>(ctx->label), T, st, s);
     fa_launch_uf_compress(P<int>(ctx->vis_list), P<int>(ctx->label), T, st, s);
     fa_launch_v2c(P<int>(ctx->vmin), P<int>(ctx->label), P<int>(ctx->v2c), V, s);
-    nl += 5;
+    nl += 2;
     mark();  // 5: union-find charts
     fa_launch_compact_roots(P<int>(ctx->vis_list), P<int>(ctx->label), T, P<int>(ctx->blocks), P<int>(ctx->roots),
                             P<int>(ctx->cidx), P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), st, s);

@@ -97,9 +97,19 @@ void fa_launch_compact_visible(const unsigned char* flags, int T, int* blocks, i
 
 // ---- union-find ---------------------------------------------------------------
 // parent[x] <= x always holds; find with pointer jumping (ECL-CC style)
-// (only while hooking: every jump keeps a node inside its own set)
+// (only while hooking: every jump keeps a node inside its own set).  Loads may
+// be L1-cached and stale: a stale chain still only climbs through ancestors
+// (parent <= node always holds), a stale root can only make two nodes look
+// unmerged (never wrongly merged), and every failed CAS returns a fresh value.
+#ifndef FA_UF_VOLATILE
+#define FA_UF_VOLATILE 0
+#endif
 __device__ __forceinline__ int uf_find(int* parent, int x) {
+#if FA_UF_VOLATILE
     volatile int* p = parent;
+#else
+    int* p = parent;
+#endif
     int cur = p[x];
     if (cur != x) {
         int next, prev = x;
@@ -201,6 +211,45 @@ __global__ void k_uf_init_vmin(const int* __restrict__ tris, const int* __restri
     }
 }
 
+// Min-label propagation round before hooking (fire-and-forget, no CAS):
+//   A: vmin[v] = min over incident visible t of label[t]   (RED.MIN)
+//   B: label[t] = min(label[t], vmin[v0..2], label[label[t]])
+// Every value written is a visible triangle of the same component with an
+// index <= the node's own, so label stays a valid min-rooted forest and
+// vmin[v] stays a member of v's component for the hooking pass.
+__global__ void k_uf_prop_a(const int* __restrict__ tris, const int* __restrict__ vis_list, int* __restrict__ vmin,
+                            const int* __restrict__ label, const fa_dstat* __restrict__ st) {
+    int n = st->n_vis;
+    int stride = gridDim.x * blockDim.x;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+        int t = vis_list[k];
+        int l = label[t];
+#pragma unroll
+        for (int j = 0; j < 3; j++) {
+            int v = __ldg(tris + 3 * t + j);
+            if (*(volatile int*)(vmin + v) > l) atomicMin(vmin + v, l);
+        }
+    }
+}
+
+__global__ void k_uf_prop_b(const int* __restrict__ tris, const int* __restrict__ vis_list,
+                            const int* __restrict__ vmin, int* label, const fa_dstat* __restrict__ st) {
+    int n = st->n_vis;
+    int stride = gridDim.x * blockDim.x;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+        int t = vis_list[k];
+        int m = label[t];
+#pragma unroll
+        for (int j = 0; j < 3; j++) m = min(m, vmin[__ldg(tris + 3 * t + j)]);
+        m = min(m, *(volatile int*)(label + m));
+        label[t] = m;
+    }
+}
+
+#ifndef FA_UF_PROP_ROUNDS
+#define FA_UF_PROP_ROUNDS 1
+#endif
+
 __global__ void k_hook_vertex(const int* __restrict__ tris, const int* __restrict__ vis_list,
                               const int* __restrict__ vmin, int* label, const fa_dstat* __restrict__ st) {
     int n = st->n_vis;
@@ -208,11 +257,11 @@ __global__ void k_hook_vertex(const int* __restrict__ tris, const int* __restric
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
         int t = vis_list[k];
         int u0 = vmin[__ldg(tris + 3 * t)], u1 = vmin[__ldg(tris + 3 * t + 1)], u2 = vmin[__ldg(tris + 3 * t + 2)];
-        // the init already linked t to min(t, u0, u1, u2)
-        int m = min(min(t, u0), min(u1, u2));
-        if (u0 != m && u0 != t) uf_union(label, t, u0);
-        if (u1 != m && u1 != t && u1 != u0) uf_union(label, t, u1);
-        if (u2 != m && u2 != t && u2 != u0 && u2 != u1) uf_union(label, t, u2);
+        // t's current parent is an ancestor forever: a union with it is implied
+        int p = *(volatile int*)(label + t);
+        if (u0 != p && u0 != t) uf_union(label, t, u0);
+        if (u1 != p && u1 != t && u1 != u0) uf_union(label, t, u1);
+        if (u2 != p && u2 != t && u2 != u0 && u2 != u1) uf_union(label, t, u2);
     }
 }
 
@@ -293,11 +342,16 @@ __global__ void k_flags_from_labels(const int* __restrict__ labels, unsigned cha
 
 static inline int uf_grid(int T) { return fa_grid(T, 256, FA_NUM_SMS * 8); }
 
-void fa_launch_uf_vertex(const int* tris, const int* vis_list, int* vmin, int* label, int T, const fa_dstat* st,
-                         cudaStream_t s) {
+int fa_launch_uf_vertex(const int* tris, const int* vis_list, int* vmin, int* label, int T, const fa_dstat* st,
+                        cudaStream_t s) {
     k_vmin<<<uf_grid(T), 256, 0, s>>>(tris, vis_list, vmin, st);
     k_uf_init_vmin<<<uf_grid(T), 256, 0, s>>>(tris, vis_list, vmin, label, st);
+    for (int r = 0; r < FA_UF_PROP_ROUNDS; r++) {
+        k_uf_prop_a<<<uf_grid(T), 256, 0, s>>>(tris, vis_list, vmin, label, st);
+        k_uf_prop_b<<<uf_grid(T), 256, 0, s>>>(tris, vis_list, vmin, label, st);
+    }
     k_hook_vertex<<<uf_grid(T), 256, 0, s>>>(tris, vis_list, vmin, label, st);
+    return 3 + 2 * FA_UF_PROP_ROUNDS;
 }
 
 void fa_launch_uf_edges(const int* adjacency, const unsigned char* flags, const int* vis_list, int* label, int T,

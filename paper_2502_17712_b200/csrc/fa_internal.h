@@ -91,7 +91,7 @@ size_t fa_trisetup_bytes();
 void fa_launch_compact_visible(const unsigned char* flags, int T, int* blocks, int* vis_list, int* label,
                                fa_dstat* st, cudaStream_t s);
 int fa_compact_blocks(long long n);
-void fa_launch_uf_vertex(const int* tris, const int* vis_list, int* vmin, int* label, int T, const fa_dstat* st,
+int fa_launch_uf_vertex(const int* tris, const int* vis_list, int* vmin, int* label, int T, const fa_dstat* st,
                          cudaStream_t s);
 void fa_launch_uf_edges(const int* adjacency, const unsigned char* flags, const int* vis_list, int* label, int T,
                         const fa_dstat* st, cudaStream_t s);
