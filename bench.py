@@ -132,6 +132,34 @@ def frame_bytes(T, V, W, H, n_vis, C) -> int:
     return 24 * V + 12 * T + 16 * W * H + 2 * T + 4 * T + 4 * V + 24 * n_vis + 64 * C
 
 
+STAGE_KERNELS = {
+    "project+clear": ["k_frame_init"],
+    "depth pass": ["k_raster_setup<1>", "k_small_coop<0>", "k_raster_depth_tiles", "k_count_finite"],
+    "visibility pass": ["k_raster_vis_small", "k_raster_vis_tiles"],
+    "union-find": ["k_vmin", "k_uf_init_vmin", "k_uf_prop_a", "k_uf_prop_b", "k_hook_vertex", "k_compress", "k_v2c"],
+    "pack+select": ["k_pack", "k_select"],
+}
+
+
+def stage_traffic(stage: str):
+    """DRAM bytes per launch of the stage's kernels from the committed ncu
+    --set full capture (profiles/*_ncu_kernels.json; cold cache, so an upper
+    bound on the warm in-frame traffic).  None when not captured."""
+    import glob
+    files = sorted(glob.glob(os.path.join(REPO, "profiles", "r*_ncu_kernels.json")))
+    if not files:
+        return None, None
+    try:
+        with open(files[-1]) as fh:
+            caps = json.load(fh)
+    except (OSError, ValueError):
+        return None, None
+    ks = [k for k in STAGE_KERNELS.get(stage, []) if k in caps]
+    if not ks:
+        return None, None
+    return int(sum(caps[k]["dram_bytes"] for k in ks)), {"source": os.path.relpath(files[-1], REPO), "kernels": ks}
+
+
 def _peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
@@ -333,8 +361,9 @@ def main():
         if top:
             b = stage_bytes(top, T, V, W, H, n_vis, C)
             gbs = b / (stage_ms[top] * 1e-3) / 1e9
+            traffic, tsrc = stage_traffic(top)
             roof = {"bound": "hbm", "kernel": top, "achieved": gbs, "peak": peak, "unit": "GB/s",
-                    "frac": gbs / peak, "peak_source": peak_kind, "traffic": None,
+                    "frac": gbs / peak, "peak_source": peak_kind, "traffic": traffic, "traffic_source": tsrc,
                     "algorithmic_bytes": b, "kernel_ms": stage_ms[top],
                     "frame_bytes": frame_bytes(T, V, W, H, n_vis, C),
                     "frame_frac": frame_bytes(T, V, W, H, n_vis, C) / (dev_ms / K * 1e-3) / 1e9 / peak}
