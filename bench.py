@@ -281,7 +281,8 @@ def main():
     eng = FrameEngine(mesh, device=local, settings=settings)
     views = _views()
     K = args.steps
-    vps = [_vp(views[(rank * K + s) % 64], spec.screen) for s in range(K)]
+    from paper_2502_17712_b200 import distributed as fdist
+    vps = [_vp(views[v], spec.screen) for v in fdist.step_views(K, rank)]
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -347,10 +348,7 @@ def main():
     stage_ms = {k: float(np.mean(v)) for k, v in acc.items()}
 
     # ---------------- reduce over ranks ----------------
-    t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dev_ms, e2e_ms = float(t[0]), float(t[1])
+    dev_ms, e2e_ms = fdist.max_over_ranks([dev_ms, e2e_ms], device=dev)
     frames_total = K * world
     if rank == 0:
         n_vis = int(np.mean([a for a, _ in stats]))
