@@ -154,6 +154,9 @@ typedef struct fa_frame_result {
     int64_t scale_num, scale_den; /* AtlasLayout.scale */
     int64_t screen_fragments;     /* cli.py:390 */
     int64_t texels_allocated;     /* cli.py:391-393 */
+    double stretch_l2;            /* scene_stretch L2 (metrics.py:84-111, via cli.py:409-454) */
+    double stretch_linf;          /* scene_stretch Linf */
+    int64_t stretch_count;        /* triangle pairs in the stretch sums; 0 -> stretch is None */
     /* device pointers owned by the context, valid until its next frame */
     const double *depth;            /* (H,W) float64 when want_depth */
     const uint8_t *flags;           /* (T,) visibility */

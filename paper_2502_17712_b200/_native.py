@@ -64,6 +64,7 @@ class FrameResult(ctypes.Structure):
         ("status", ctypes.c_int), ("n_visible", ctypes.c_int32), ("n_charts", ctypes.c_int32),
         ("scale_num", ctypes.c_int64), ("scale_den", ctypes.c_int64),
         ("screen_fragments", ctypes.c_int64), ("texels_allocated", ctypes.c_int64),
+        ("stretch_l2", ctypes.c_double), ("stretch_linf", ctypes.c_double), ("stretch_count", ctypes.c_int64),
         ("depth", ctypes.c_void_p), ("flags", ctypes.c_void_p), ("visible", ctypes.c_void_p),
         ("chart_of_triangle", ctypes.c_void_p), ("vertex_to_chart", ctypes.c_void_p),
         ("roots", ctypes.c_void_p), ("ndc", ctypes.c_void_p), ("px", ctypes.c_void_p),

@@ -20,7 +20,6 @@ import numpy as np
 from .charts import Mesh, load_obj
 from .frame import FrameEngine, FrameOutput, FrameSettings
 from .geometry import CameraFrame, W_EPSILON
-from .metrics import NoValidTriangles, scene_stretch_arrays
 from .packing import ChartBox, PackFailure, pack
 
 EXIT_OK = 0
@@ -190,23 +189,9 @@ class SceneResult:
 
     @property
     def stretch(self):
-        """cli.py:409-454: screen-vs-atlas stretch over fully projectable triangles."""
-        def compute():
-            uv = self.uv.astype(np.float64)
-            ok = ~np.isnan(uv[:, 0])
-            if not np.any(ok):
-                return None
-            tris = self.mesh.triangles[self.visible[ok]]
-            vp = self.camera.view_proj
-            clip = np.concatenate([self.mesh.positions[tris], np.ones((len(tris), 3, 1))], axis=2) @ vp.T
-            ndc = clip[..., :2] / clip[..., 3:4]
-            W, H = self.config.screen
-            screen = np.stack([(ndc[..., 0] + 1.0) * 0.5 * W, (ndc[..., 1] + 1.0) * 0.5 * H], axis=-1)
-            try:
-                return scene_stretch_arrays(screen, uv[ok].reshape(-1, 3, 2))
-            except NoValidTriangles:
-                return None
-        return self._get("stretch", compute)
+        """cli.py:409-454: screen-vs-atlas stretch over fully projectable
+        triangles, reduced on the GPU inside the UV kernel (csrc/fa_uv.cu)."""
+        return self._get("stretch", self.frame.stretch)
 
 
 def run_scene_pipeline(cfg: SceneConfig, packer: str = "fastatlas", mesh: Mesh | None = None,

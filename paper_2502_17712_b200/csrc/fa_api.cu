@@ -5,6 +5,7 @@
 // device status block (fa_dstat), so the whole frame needs no host round
 // trip and is captured once per shape into a CUDA graph; per frame only the
 // 128-byte camera matrix is uploaded before the graph launch.
+#include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
 #include <string.h>
@@ -779,6 +780,13 @@ int fa_frame_finish(fa_ctx* ctx, fa_frame_result* out, void* stream) {
     out->scale_den = h->scale_den;
     out->screen_fragments = h->screen_fragments;
     out->texels_allocated = h->texels_allocated;
+    out->stretch_count = h->stretch_valid;
+    {
+        double linf;
+        memcpy(&linf, &h->stretch_linf_bits, sizeof(linf));
+        out->stretch_linf = h->stretch_valid ? linf : 0.0;
+        out->stretch_l2 = (h->stretch_valid && h->stretch_area > 0) ? sqrt(h->stretch_wsum / h->stretch_area) : 0.0;
+    }
     out->depth = ctx->last_params.want_depth ? P<double>(ctx->depth_f64) : nullptr;
     out->flags = P<uint8_t>(ctx->flags);
     out->visible = P<int32_t>(ctx->vis_list);

@@ -161,7 +161,7 @@ void fa_launch_fold(const long long* w, int n, long long omega, long long* rows,
 // ---- uv (fa_uv.cu) -------------------------------------------------------
 void fa_launch_uv(const double4* clip, const int* tris, const int* vis_list, const int* label, const int* cidx,
                   const int* pinv, const double* ndc, const int* px, const long long* placements, int T, int W, int H,
-                  long long pad, bool f64, void* uv, const fa_dstat* st, cudaStream_t s);
+                  long long pad, bool f64, void* uv, fa_dstat* st, cudaStream_t s);
 
 // ---- standalone helpers (fa_bounds.cu / fa_pack.cu) -------------------------
 void fa_launch_blinn_points(const double* p4, int n, double* out, cudaStream_t s);

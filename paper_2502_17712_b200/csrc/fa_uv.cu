@@ -9,6 +9,29 @@
 
 #define UV_THREADS 256
 
+// Stretch of one (screen, atlas) triangle pair (metrics.py:58-111): the
+// atlas->screen affine map M = Es * Ea^-1; area-weighted L2 needs only
+// ||M||_F^2 = S1^2 + S2^2, Linf the larger singular value (closed form).
+// Returns false for a degenerate atlas triangle (det == 0, skipped).
+__device__ __forceinline__ bool tri_stretch(const double (&s)[6], const double (&a)[6], double& wterm, double& area,
+                                            double& big) {
+    double ea00 = a[2] - a[0], ea10 = a[3] - a[1], ea01 = a[4] - a[0], ea11 = a[5] - a[1];
+    double es00 = s[2] - s[0], es10 = s[3] - s[1], es01 = s[4] - s[0], es11 = s[5] - s[1];
+    double det = ea00 * ea11 - ea01 * ea10;
+    if (det == 0.0) return false;
+    double i00 = ea11 / det, i01 = -ea01 / det, i10 = -ea10 / det, i11 = ea00 / det;
+    double m00 = es00 * i00 + es01 * i10, m01 = es00 * i01 + es01 * i11;
+    double m10 = es10 * i00 + es11 * i10, m11 = es10 * i01 + es11 * i11;
+    double f2 = m00 * m00 + m01 * m01 + m10 * m10 + m11 * m11;
+    // stable 2x2 largest singular value: (|q| + |r|) / 2 with
+    // q = (a + d, c - b), r = (a - d, c + b); no cancellation when S1 ~ S2
+    double q = hypot(m00 + m11, m10 - m01), r = hypot(m00 - m11, m10 + m01);
+    big = 0.5 * (q + r);
+    area = fabs(es00 * es11 - es10 * es01) * 0.5;
+    wterm = area * f2 * 0.5;
+    return true;
+}
+
 template <typename OutT>
 __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ clip, const int* __restrict__ tris,
                                                    const int* __restrict__ vis_list, const int* __restrict__ label,
@@ -16,8 +39,12 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
                                                    const double* __restrict__ ndc, const int* __restrict__ px,
                                                    const long long* __restrict__ placements, int W, int H,
                                                    long long pad, OutT* __restrict__ uv,
-                                                   const fa_dstat* __restrict__ st) {
+                                                   fa_dstat* __restrict__ st) {
     __shared__ __align__(16) OutT stage[UV_THREADS * 6];
+    __shared__ double red_w[UV_THREADS / 32], red_a[UV_THREADS / 32], red_m[UV_THREADS / 32];
+    __shared__ int red_c[UV_THREADS / 32];
+    double acc_w = 0.0, acc_a = 0.0, acc_m = 0.0;
+    int acc_c = 0;
     int n = st->n_vis;
     bool failed = (st->flags & (FA_DFLAG_PACK_FAILURE | FA_DFLAG_HEIGHT_OVERFLOW | FA_DFLAG_QUEUE_OVERFLOW)) != 0;
     for (int k0 = blockIdx.x * UV_THREADS; k0 < n; k0 += gridDim.x * UV_THREADS) {
@@ -46,6 +73,7 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
                 bool rot = P[5] != 0;
                 double rx = rot ? __ddiv_rn((double)cw, h_px) : __ddiv_rn((double)cw, w_px);
                 double ry = rot ? __ddiv_rn((double)ch, w_px) : __ddiv_rn((double)ch, h_px);
+                double scr[6];
 #pragma unroll
                 for (int i = 0; i < 3; i++) {
                     double nx = __ddiv_rn(v[i].x, v[i].w), ny = __ddiv_rn(v[i].y, v[i].w);
@@ -53,6 +81,15 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
                     double vv = __dmul_rn(__dmul_rn(__dsub_rn(ny, mny), 0.5), (double)H);
                     out[2 * i] = __dadd_rn(bx, __dmul_rn(rot ? vv : u, rx));
                     out[2 * i + 1] = __dadd_rn(by, __dmul_rn(rot ? u : vv, ry));
+                    scr[2 * i] = __dmul_rn(__dmul_rn(__dadd_rn(nx, 1.0), 0.5), (double)W);      // cli.py:437-439
+                    scr[2 * i + 1] = __dmul_rn(__dmul_rn(__dadd_rn(ny, 1.0), 0.5), (double)H);
+                }
+                double wt, ar, big;
+                if (tri_stretch(scr, out, wt, ar, big)) {
+                    acc_w += wt;
+                    acc_a += ar;
+                    acc_m = big > acc_m ? big : acc_m;
+                    acc_c++;
                 }
             }
         }
@@ -69,11 +106,43 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
         for (int i = nvec * per16 + threadIdx.x; i < nelem; i += UV_THREADS) dst[i] = stage[i];
         __syncthreads();
     }
+    // stretch sums: warp shuffles, then one set of atomics per block
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        acc_w += __shfl_xor_sync(0xffffffffu, acc_w, o);
+        acc_a += __shfl_xor_sync(0xffffffffu, acc_a, o);
+        acc_m = fmax(acc_m, __shfl_xor_sync(0xffffffffu, acc_m, o));
+        acc_c += __shfl_xor_sync(0xffffffffu, acc_c, o);
+    }
+    int wid = threadIdx.x >> 5;
+    if (lane_id() == 0) {
+        red_w[wid] = acc_w;
+        red_a[wid] = acc_a;
+        red_m[wid] = acc_m;
+        red_c[wid] = acc_c;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double w = 0, a = 0, m = 0;
+        int c = 0;
+        for (int i = 0; i < UV_THREADS / 32; i++) {
+            w += red_w[i];
+            a += red_a[i];
+            m = fmax(m, red_m[i]);
+            c += red_c[i];
+        }
+        if (c) {
+            atomicAdd(&st->stretch_wsum, w);
+            atomicAdd(&st->stretch_area, a);
+            atomicMax(&st->stretch_linf_bits, (unsigned long long)__double_as_longlong(m));
+            atomicAdd(&st->stretch_valid, c);
+        }
+    }
 }
 
 void fa_launch_uv(const double4* clip, const int* tris, const int* vis_list, const int* label, const int* cidx,
                   const int* pinv, const double* ndc, const int* px, const long long* placements, int T, int W, int H,
-                  long long pad, bool f64, void* uv, const fa_dstat* st, cudaStream_t s) {
+                  long long pad, bool f64, void* uv, fa_dstat* st, cudaStream_t s) {
     int grid = fa_grid(T, UV_THREADS, FA_NUM_SMS * 8);
     if (f64)
         k_uv<double><<<grid, UV_THREADS, 0, s>>>(clip, tris, vis_list, label, cidx, pinv, ndc, px, placements, W, H,

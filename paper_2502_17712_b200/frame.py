@@ -63,6 +63,9 @@ class FrameOutput:
         self.scale = Fraction(int(res.scale_num), int(res.scale_den)) if res.scale_den else None
         self.screen_fragments = int(res.screen_fragments)
         self.texels_allocated = int(res.texels_allocated)
+        self.stretch_l2 = float(res.stretch_l2)
+        self.stretch_linf = float(res.stretch_linf)
+        self.stretch_count = int(res.stretch_count)
         self.settings = settings
         C, nv = self.n_charts, self.n_visible
         W, H = settings.screen
@@ -111,6 +114,13 @@ class FrameOutput:
     def layout(self) -> AtlasLayout:
         return AtlasLayout(omega=int(self.settings.omega), scale=self.scale,
                            placements=placements_from_array(self.placements.cpu().numpy()))
+
+    def stretch(self):
+        """StretchReport of the frame (computed on the GPU in the UV kernel), None if no valid pair."""
+        from .metrics import StretchReport
+        if self.stretch_count == 0:
+            return None
+        return StretchReport(l2=self.stretch_l2, linf=self.stretch_linf)
 
     def chart_ndc(self) -> dict:
         r = self.roots.cpu().numpy()

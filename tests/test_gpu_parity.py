@@ -249,6 +249,13 @@ class TestFrames:
         assert out.screen_fragments == m["screen_fragments"]
         assert out.texels_allocated == m["texels_allocated"]
         assert fa.layout_digest(out.layout()).digest == m["digest"]
+        # stretch (metrics.py:84-111): GPU closed form vs the reference's LAPACK SVD
+        if m.get("stretch") is None:
+            assert out.stretch() is None
+        else:
+            st = out.stretch()
+            assert st.l2 == pytest.approx(m["stretch"][0], rel=1e-9)
+            assert st.linf == pytest.approx(m["stretch"][1], rel=1e-9)
         vis = h["visible"]
         assert np.array_equal(vis, np.flatnonzero(g["flags"]))
         pos_of = {int(t): k for k, t in enumerate(vis)}
