@@ -69,6 +69,11 @@ int fa_depth_prepass(fa_ctx *ctx, const double *vp_host, int width, int height, 
 int fa_mark_visible(fa_ctx *ctx, const double *vp_host, const double *depth, int width, int height,
                     int backface_cull, uint8_t *flags_out, void *stream);
 
+/* build_adjacency (charts.py:64-77) of the bound mesh: adjacency_out (T,3)
+ * int32, the triangle sharing edge e of t, or -1 unless exactly two (t, e)
+ * slots use that edge.  Synchronises the stream (per mesh, not per frame). */
+int fa_build_adjacency(fa_ctx *ctx, int32_t *adjacency_out, void *stream);
+
 /* connected_charts (charts.py:343-359): labels_out (T,) int32, -1 invisible. */
 int fa_connected_charts(fa_ctx *ctx, const int32_t *adjacency, const uint8_t *flags,
                         int32_t *labels_out, void *stream);

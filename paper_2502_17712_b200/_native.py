@@ -36,7 +36,7 @@ FA_INTERNAL_ERROR = -2
 # every symbol declared by include/fastatlas.h
 EXPORTS = (
     "fa_abi_version", "fa_last_error", "fa_create", "fa_destroy", "fa_set_mesh", "fa_project",
-    "fa_depth_prepass", "fa_mark_visible", "fa_connected_charts", "fa_merge_shared_vertices",
+    "fa_depth_prepass", "fa_mark_visible", "fa_build_adjacency", "fa_connected_charts", "fa_merge_shared_vertices",
     "fa_chart_boxes", "fa_blinn_clamped_ndc", "fa_select_side_plane", "fa_chart_bbox",
     "fa_viewport_box", "fa_orient", "fa_orient_order", "fa_fold", "fa_push_up", "fa_pack_at_scale",
     "fa_pack", "fa_frame_launch", "fa_frame_finish", "fa_frame", "fa_last_launch_count",
@@ -106,6 +106,7 @@ def load_library():
             "fa_project": ([vp, vp, vp, vp], ci),
             "fa_depth_prepass": ([vp, vp, ci, ci, ci, vp, vp], ci),
             "fa_mark_visible": ([vp, vp, vp, ci, ci, ci, vp, vp], ci),
+            "fa_build_adjacency": ([vp, vp, vp], ci),
             "fa_connected_charts": ([vp, vp, vp, vp, vp], ci),
             "fa_merge_shared_vertices": ([vp, vp, vp, vp, vp], ci),
             "fa_chart_boxes": ([vp, vp, vp, ci, ci, cd, vp, vp, vp, vp, vp, vp], ci),

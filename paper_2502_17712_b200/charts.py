@@ -23,27 +23,23 @@ from .geometry import CameraFrame, W_EPSILON  # noqa: F401  (re-exported like th
 DEPTH_EPSILON = 1e-6  # charts.py:26
 
 
+def _device_adjacency(tris_dev, ctx):
+    """charts.py:64-77 on the GPU (fa_build_adjacency: edge hash table)."""
+    torch = nat._torch()
+    T = tris_dev.shape[0]
+    adj = torch.empty((max(T, 1), 3), dtype=torch.int32, device=ctx.torch_device)
+    if T:
+        nat.raise_for_status(ctx.L.fa_build_adjacency(ctx.h, nat.ptr(adj), ctx.stream_ptr()))
+    return adj[:T]
+
+
 def build_adjacency(triangles: np.ndarray) -> np.ndarray:
-    """charts.py:64-77: link edges used by exactly two (triangle, edge) slots."""
+    """charts.py:64-77: link edges used by exactly two (triangle, edge) slots (GPU)."""
     tris = np.asarray(triangles, dtype=np.int64).reshape(-1, 3)
-    T = len(tris)
-    adjacency = np.full((T, 3), -1, dtype=np.int64)
-    if T == 0:
-        return adjacency
-    e = np.stack([tris[:, [0, 1]], tris[:, [1, 2]], tris[:, [2, 0]]], axis=1).reshape(-1, 2)
-    lo, hi = e.min(axis=1), e.max(axis=1)
-    base = int(max(int(tris.max()) + 1, 1))
-    key = lo * base + hi
-    order = np.argsort(key, kind="stable")
-    ks = key[order]
-    starts = np.flatnonzero(np.concatenate([[True], ks[1:] != ks[:-1]]))
-    counts = np.diff(np.concatenate([starts, [len(ks)]]))
-    pair = starts[counts == 2]
-    a, b = order[pair], order[pair + 1]
-    flat = adjacency.reshape(-1)
-    flat[a] = b // 3
-    flat[b] = a // 3
-    return adjacency
+    if len(tris) == 0:
+        return np.full((0, 3), -1, dtype=np.int64)
+    n = int(tris.max()) + 1
+    return Mesh(np.zeros((n, 3)), tris).adjacency
 
 
 class Mesh:
@@ -59,8 +55,10 @@ class Mesh:
 
     @property
     def adjacency(self) -> np.ndarray:
+        """Edge adjacency (charts.py:64-77), built once per mesh on the GPU."""
         if self._adjacency is None:
-            self._adjacency = build_adjacency(self.triangles)
+            ctx = nat.default_context()
+            self._adjacency = self.device_adjacency(ctx.torch_device).cpu().numpy().astype(np.int64)
         return self._adjacency
 
     @adjacency.setter
@@ -95,7 +93,13 @@ class Mesh:
         key = ("adj", str(device))
         got = self._dev.get(key)
         if got is None:
-            got = torch.as_tensor(np.ascontiguousarray(self.adjacency, dtype=np.int32)).to(device)
+            if self._adjacency is not None:  # caller-supplied adjacency (Mesh(adjacency=...))
+                got = torch.as_tensor(np.ascontiguousarray(self._adjacency, dtype=np.int32)).to(device)
+            else:
+                ctx = nat.default_context(torch.device(device).index)
+                pos, tris = self.device_arrays(device)
+                ctx.set_mesh(pos, tris)
+                got = _device_adjacency(tris, ctx)
             self._dev[key] = got
         return got
 

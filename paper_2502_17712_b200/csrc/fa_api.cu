@@ -353,6 +353,33 @@ int fa_mark_visible(fa_ctx* ctx, const double* vp_host, const double* depth, int
     return set_err(FA_INTERNAL_ERROR, "raster queue kept overflowing");
 }
 
+int fa_build_adjacency(fa_ctx* ctx, int32_t* adjacency_out, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || (ctx->T && !adjacency_out)) return set_err(FA_VALUE_ERROR, "bad arguments");
+    if (ctx->T == 0) return FA_OK;
+    CK(cudaSetDevice(ctx->device));
+    unsigned long long n = 3ull * (unsigned long long)ctx->T, size = 1;
+    while (size < 2 * n) size <<= 1;  // load factor <= 1/2
+    fa_buf keys, cnt, c0, c1;
+    bool ok = fa_ensure(ctx, keys, size * 8) && fa_ensure(ctx, cnt, size * 4) && fa_ensure(ctx, c0, size * 4) &&
+              fa_ensure(ctx, c1, size * 4);
+    int r = FA_OK;
+    if (!ok) {
+        r = set_err(FA_CUDA_ERROR, "out of device memory for the edge table");
+    } else {
+        fa_launch_build_adjacency(ctx->tris, (int)ctx->T, P<unsigned long long>(keys), P<int>(cnt), P<int>(c0),
+                                  P<int>(c1), size, adjacency_out, s);
+        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) r = set_err(FA_CUDA_ERROR, "build_adjacency: %s", cudaGetErrorString(e));
+    }
+    free_buf(keys);
+    free_buf(cnt);
+    free_buf(c0);
+    free_buf(c1);
+    return r;
+}
+
 int fa_connected_charts(fa_ctx* ctx, const int32_t* adjacency, const uint8_t* flags, int32_t* labels_out,
                         void* stream) {
     cudaStream_t s = (cudaStream_t)stream;

@@ -342,6 +342,72 @@ __global__ void k_flags_from_labels(const int* __restrict__ labels, unsigned cha
 
 static inline int uf_grid(int T) { return fa_grid(T, 256, FA_NUM_SMS * 8); }
 
+// ---- mesh edge adjacency (charts.py:64-77) ------------------------------------
+// Open-addressing hash on the undirected edge key (min<<32 | max).  Insert
+// counts the (triangle, edge) slots per key and records the first two; resolve
+// links the two slots of keys used exactly twice (symmetric, so slot order
+// does not matter) and leaves every other edge at -1, like the reference.
+#define ADJ_EMPTY 0xffffffffffffffffull
+
+__device__ __forceinline__ unsigned long long edge_key(const int* __restrict__ tris, int code) {
+    int t = code / 3, e = code - 3 * t;
+    unsigned a = (unsigned)__ldg(tris + 3 * t + e), b = (unsigned)__ldg(tris + 3 * t + (e == 2 ? 0 : e + 1));
+    unsigned lo = a < b ? a : b, hi = a < b ? b : a;
+    return ((unsigned long long)lo << 32) | hi;
+}
+
+__device__ __forceinline__ unsigned long long edge_hash(unsigned long long k) {
+    k ^= k >> 33;
+    k *= 0xff51afd7ed558ccdull;
+    k ^= k >> 33;
+    k *= 0xc4ceb9fe1a85ec53ull;
+    k ^= k >> 33;
+    return k;
+}
+
+__global__ void k_adj_insert(const int* __restrict__ tris, int n_codes, unsigned long long* __restrict__ keys,
+                             int* __restrict__ cnt, int* __restrict__ c0, int* __restrict__ c1,
+                             unsigned long long mask) {
+    for (int code = blockIdx.x * blockDim.x + threadIdx.x; code < n_codes; code += gridDim.x * blockDim.x) {
+        unsigned long long key = edge_key(tris, code);
+        unsigned long long h = edge_hash(key) & mask;
+        while (true) {
+            unsigned long long old = atomicCAS(keys + h, ADJ_EMPTY, key);
+            if (old == ADJ_EMPTY || old == key) break;
+            h = (h + 1) & mask;
+        }
+        int k = atomicAdd(cnt + h, 1);
+        if (k == 0) c0[h] = code;
+        else if (k == 1) c1[h] = code;
+    }
+}
+
+__global__ void k_adj_resolve(const int* __restrict__ tris, int n_codes, const unsigned long long* __restrict__ keys,
+                              const int* __restrict__ cnt, const int* __restrict__ c0, const int* __restrict__ c1,
+                              unsigned long long mask, int* __restrict__ adj) {
+    for (int code = blockIdx.x * blockDim.x + threadIdx.x; code < n_codes; code += gridDim.x * blockDim.x) {
+        unsigned long long key = edge_key(tris, code);
+        unsigned long long h = edge_hash(key) & mask;
+        while (keys[h] != key) h = (h + 1) & mask;
+        int other = -1;
+        if (cnt[h] == 2) {
+            int a = c0[h], b = c1[h];
+            other = (a == code ? b : a) / 3;
+        }
+        adj[code] = other;
+    }
+}
+
+void fa_launch_build_adjacency(const int* tris, int T, unsigned long long* keys, int* cnt, int* c0, int* c1,
+                               unsigned long long table_size, int* adj, cudaStream_t s) {
+    int n = 3 * T;
+    cudaMemsetAsync(keys, 0xff, table_size * sizeof(unsigned long long), s);
+    cudaMemsetAsync(cnt, 0, table_size * sizeof(int), s);
+    int grid = fa_grid(n, 256, FA_NUM_SMS * 8);
+    k_adj_insert<<<grid, 256, 0, s>>>(tris, n, keys, cnt, c0, c1, table_size - 1);
+    k_adj_resolve<<<grid, 256, 0, s>>>(tris, n, keys, cnt, c0, c1, table_size - 1, adj);
+}
+
 int fa_launch_uf_vertex(const int* tris, const int* vis_list, int* vmin, int* label, int T, const fa_dstat* st,
                         cudaStream_t s) {
     k_vmin<<<uf_grid(T), 256, 0, s>>>(tris, vis_list, vmin, st);

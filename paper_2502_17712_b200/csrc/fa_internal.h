@@ -98,6 +98,8 @@ void fa_launch_uf_edges(const int* adjacency, const unsigned char* flags, const 
 void fa_launch_uf_labels(const int* labels_in, const int* vis_list, int* label, int T, const fa_dstat* st,
                          cudaStream_t s);
 void fa_launch_iota(int* label, int T, cudaStream_t s);
+void fa_launch_build_adjacency(const int* tris, int T, unsigned long long* keys, int* cnt, int* c0, int* c1,
+                               unsigned long long table_size, int* adj, cudaStream_t s);
 void fa_launch_uf_compress(const int* vis_list, int* label, int T, const fa_dstat* st, cudaStream_t s);
 void fa_launch_canonicalize(const int* vis_list, int* label, int* tmp, int T, const fa_dstat* st, cudaStream_t s);
 void fa_launch_v2c(const int* vmin, const int* label, int* v2c, int V, cudaStream_t s);

@@ -88,10 +88,24 @@ class TestCharts:
         assert np.array_equal(merged.vertex_chart_array, g["v2c"])
         assert list(merged.charts.keys()) == g["roots"].tolist()
 
-    def test_host_adjacency_matches_reference(self):
+    def test_gpu_adjacency_matches_reference(self):
+        """build_adjacency (charts.py:64-77) incl. non-manifold edges, on the GPU."""
         for case in meta()["charts"]:
             g = group(npz("charts.npz"), case)
             assert np.array_equal(fa.Mesh(g["pos"], g["tris"]).adjacency, g["adj"])
+        assert fa.Mesh(np.zeros((5, 3)), [(0, 1, 2), (0, 1, 3), (0, 1, 4)]).adjacency.tolist() == [[-1] * 3] * 3
+
+    def test_gpu_adjacency_full_size(self):
+        spec = scenes.build_scene("C2")
+        adj = fa.Mesh(spec.positions, spec.triangles).adjacency
+        assert np.array_equal(adj, oracle.build_adjacency(spec.triangles))
+
+    def test_connected_charts_with_gpu_adjacency(self):
+        for case in meta()["charts"][:12]:
+            g = group(npz("charts.npz"), case)
+            mesh = fa.Mesh(g["pos"], g["tris"])  # adjacency built on the GPU
+            pre = fa.connected_charts(mesh, fa.VisibilityBuffer(g["flags"], (8, 8)))
+            assert np.array_equal(pre.chart_of_triangle, g["pre"])
 
 
 # ---------------------------------------------------------------- bounds ----
