@@ -352,6 +352,55 @@ def test_full_size_vs_oracle(cfg):
     assert grid.max() <= 1
 
 
+def _check_vs_oracle(h, r, status_ok=True):
+    assert np.array_equal(h["flags"].astype(bool), r.flags)
+    assert np.array_equal(h["chart_of_triangle"].astype(np.int64), r.chart_of_triangle)
+    assert np.array_equal(h["vertex_to_chart"].astype(np.int64), r.vertex_to_chart)
+    if status_ok:
+        assert np.array_equal(h["placements"], r.pack.placements)
+        assert (h["scale"].numerator, h["scale"].denominator) == r.pack.scale
+        assert same_bits(h["uv"], r.uv)
+        assert h["screen_fragments"] == r.screen_fragments
+        assert h["texels_allocated"] == r.texels_allocated
+
+
+@pytest.mark.parametrize("cfg,idx", [("C4", 0), ("C4", 59), ("C4", 119), ("C5", 0), ("C5", 1), ("C5", 2),
+                                     ("C5", 37)])
+def test_camera_path_and_views_vs_oracle(cfg, idx):
+    """C4 (120-frame path) and C5 (64 streaming views) poses on the 1M-triangle scene."""
+    spec = scenes.build_scene(cfg)
+    vp = _scene_vp(spec, spec.poses[idx])
+    eng = FrameEngine(fa.Mesh(spec.positions, spec.triangles),
+                      settings=FrameSettings(screen=spec.screen, omega=spec.omega, uv_f64=True))
+    h = eng.run(vp).to_host()
+    r = oracle.run_frame(spec.positions, spec.triangles, vp, spec.screen, spec.omega)
+    assert r.status == oracle.OK
+    _check_vs_oracle(h, r)
+
+
+def test_no_cull_frame_vs_oracle():
+    """backface_cull=False (charts.py:216-219 flips clockwise polygons)."""
+    fpos, ftris, rng = scenes.sphere_field(1)
+    pos, tris = scenes._merge((fpos, ftris), scenes.ground_plane(20, 16, rng=rng))
+    spec = scenes.build_scene("C1")
+    vp = _scene_vp(spec, scenes.views_c5(8)[3])
+    eng = FrameEngine(fa.Mesh(pos, tris), settings=FrameSettings(screen=(300, 200), omega=256, uv_f64=True,
+                                                                 backface_cull=False, padding=1, min_dim=2))
+    out = eng.run(vp, check=False)
+    r = oracle.run_frame(pos, tris, vp, (300, 200), 256, min_dim=2, padding=1, cull=False)
+    assert out.status == r.status
+    _check_vs_oracle(out.to_host(), r, status_ok=r.status == oracle.OK)
+
+
+def test_height_overflow_frame():
+    """A prescale pushing a chart box past 2^23 raises HeightOverflow like order() (packing.py:127-129)."""
+    m, g, pos, tris = _frame_case("mini_v0")
+    eng = FrameEngine(fa.Mesh(pos, tris), settings=FrameSettings(screen=tuple(m["screen"]), omega=m["omega"],
+                                                                 prescale=1e6))
+    with pytest.raises(fa.HeightOverflow):
+        eng.run(g["vp"])
+
+
 @pytest.mark.parametrize("frac", [0.18, 0.5])
 def test_union_find_under_contention(frac):
     """Random visibility on the 4M-triangle mesh: many small components and
