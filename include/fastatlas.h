@@ -137,6 +137,28 @@ int fa_pack(fa_ctx *ctx, const int64_t *target_w, const int64_t *target_h, const
             int64_t padding, int64_t *placements_out, int64_t *scale_host, uint8_t *accept_out,
             void *stream);
 
+/* ---- comparison packers (atlaspack.baselines, used by `compare`) -------- */
+
+/* sequential_scale_search (baselines.py:110-141): placements_out (n,8) in
+ * packing order, scale_host[2]; FA_PACK_FAILURE when no candidate fits. */
+int fa_sequential_scale_search(fa_ctx *ctx, const int64_t *target_w, const int64_t *target_h,
+                               const int64_t *chart_id, const int64_t *min_tri, int64_t n, int64_t omega,
+                               int64_t n_scales, int64_t min_dim, int64_t padding, int64_t *placements_out,
+                               int64_t *scale_host, void *stream);
+
+/* sequential_fold + sequential_pack (baselines.py:53-107) on the caller's
+ * order at the stated dims (widths must be in [1, omega]): rows/x/y (n) int64
+ * and the used height; the layout is accepted iff *used_host <= omega. */
+int fa_sequential_pack(fa_ctx *ctx, const int64_t *widths, const int64_t *heights, int64_t n, int64_t omega,
+                       int64_t *rows_out, int64_t *x_out, int64_t *y_out, int64_t *used_host, void *stream);
+
+/* superblock_pack (baselines.py:187-261): placements_out (n,8), scale_host[2]
+ * = worst per-box downscale, *block_used_host = block size that succeeded;
+ * FA_PACK_FAILURE when even the halving floor fails (reference returns None). */
+int fa_superblock_pack(fa_ctx *ctx, const int64_t *target_w, const int64_t *target_h, const int64_t *chart_id,
+                       const int64_t *min_tri, int64_t n, int64_t omega, int64_t block_size, int halving_enabled,
+                       int64_t *placements_out, int64_t *scale_host, int64_t *block_used_host, void *stream);
+
 /* ---- whole frame: run_scene_pipeline (cli.py:360-406) -------------------- */
 typedef struct fa_frame_params {
     int width, height;       /* SceneConfig.screen */

@@ -131,13 +131,28 @@ def parse_scene_config(path) -> SceneConfig:
 
 
 def make_packer(name: str, n_scales: int, min_dim: int, padding: int, block_size: int | None = None):
-    """cli.py:318-339.  Only the FastAtlas packer is on the per-frame path; the
-    sequential / superblock comparison packers are SURVEY §8f-4 ("next")."""
+    """cli.py:318-339: the FastAtlas packer plus the comparison packers
+    (csrc/fa_baselines.cu), all on the GPU."""
+    from .baselines import SuperblockConfig, sequential_scale_search, superblock_pack
     if name == "fastatlas":
         return lambda boxes, omega: pack(boxes, omega, n_scales=n_scales, min_dim=min_dim, padding=padding)
-    if name in ("sequential", "superblock"):
-        raise NotImplementedError(f"packer '{name}' (comparison baseline) is not part of the B200 path yet")
+    if name == "sequential":
+        return lambda boxes, omega: sequential_scale_search(boxes, omega, n_scales=n_scales, min_dim=min_dim,
+                                                            padding=padding)
+    if name == "superblock":
+        def run(boxes, omega):
+            cfg = SuperblockConfig(block_size=block_size or default_block_size(omega))
+            layout = superblock_pack(boxes, omega, cfg)
+            if layout is None:
+                raise PackFailure("superblock allocation failed at the halving floor")
+            return layout
+        return run
     raise InputError(f"unknown packer '{name}' (choose from {', '.join(PACKER_NAMES)})")
+
+
+def default_block_size(omega: int) -> int:
+    """cli.py:314-315."""
+    return max(16, min(omega, omega // 8))
 
 
 class SceneResult:

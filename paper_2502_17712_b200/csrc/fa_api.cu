@@ -955,6 +955,153 @@ int fa_viewport_box(fa_ctx* ctx, const double* boxes4, int64_t n, int width, int
     return FA_OK;
 }
 
+int fa_sequential_scale_search(fa_ctx* ctx, const int64_t* target_w, const int64_t* target_h,
+                               const int64_t* chart_id, const int64_t* min_tri, int64_t n, int64_t omega,
+                               int64_t n_scales, int64_t min_dim, int64_t padding, int64_t* placements_out,
+                               int64_t* scale_host, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    int r = check_omega(omega);
+    if (r) return r;
+    if (!ctx || n < 0 || n >= (1ll << 30) || n_scales > (1 << 20)) return set_err(FA_VALUE_ERROR, "bad arguments");
+    if (n > 0 && n_scales < 1) return set_err(FA_PACK_FAILURE, "every candidate scale was rejected");
+    if (min_dim < 1 || padding < 0 || min_dim > (1 << 28) || padding > (1 << 28))
+        return set_err(FA_VALUE_ERROR, "min_dim must be >= 1 and padding >= 0");
+    if (n == 0) {
+        if (scale_host) { scale_host[0] = 1; scale_host[1] = 1; }
+        return FA_OK;
+    }
+    CK(cudaSetDevice(ctx->device));
+    int batch = (int)(n_scales < ctx->pack_batch ? n_scales : ctx->pack_batch);
+    r = ensure_pack(ctx, n, n_scales, omega, batch);
+    if (r) return r;
+    ENSURE(dstat, sizeof(fa_dstat));
+    ENSURE(aux, 64);
+    CK(cudaMemsetAsync(ctx->dstat.p, 0, sizeof(fa_dstat), s));
+    CK(cudaMemsetAsync(ctx->cand.p, 0, (size_t)n_scales * FA_CAND_REC * 8, s));
+    fa_dstat* st = P<fa_dstat>(ctx->dstat);
+    int nn = (int)n;
+    fa_launch_orient_sort_mt((const long long*)target_w, (const long long*)target_h, (const long long*)min_tri, nn,
+                             FA_MAX_BOX_DIM, P<long long>(ctx->ow), P<long long>(ctx->oh), P<unsigned char>(ctx->orot),
+                             P<int>(ctx->oidx), P<int>(ctx->pinv), P<unsigned long long>(ctx->sortk),
+                             P<int>(ctx->sortv), 0, st, s);
+    int stride = (int)ctx->pack_cap;
+    (void)stride;
+    fa_launch_seq_search(P<long long>(ctx->ow), P<long long>(ctx->oh), nn, omega, n_scales, min_dim, padding, batch,
+                         P<int>(ctx->cand_w), P<int>(ctx->cand_h), P<int>(ctx->cand_p), P<int>(ctx->cand_y),
+                         P<int>(ctx->rowstart), fa_front_in_smem(omega) ? nullptr : P<int>(ctx->okey),
+                         P<long long>(ctx->cand), &st->done, s);
+    fa_launch_seq_select((const long long*)target_w, (const long long*)target_h, (const long long*)chart_id,
+                         P<unsigned char>(ctx->orot), P<int>(ctx->oidx), nn, n_scales, P<long long>(ctx->cand),
+                         P<int>(ctx->cand_w), P<int>(ctx->cand_h), P<int>(ctx->cand_p), P<int>(ctx->cand_y),
+                         (long long*)placements_out, P<long long>(ctx->aux), s);
+    CKL();
+    r = read_stat(ctx, s);
+    if (r) return r;
+    r = status_from_flags(ctx->hstat);
+    if (r) return r;
+    long long best = 0;
+    CK(cudaMemcpy(&best, ctx->aux.p, 8, cudaMemcpyDeviceToHost));
+    if (best == 0) return set_err(FA_PACK_FAILURE, "every candidate scale was rejected");
+    if (scale_host) {
+        long long g = best, b = n_scales;
+        while (b) { long long t = g % b; g = b; b = t; }
+        scale_host[0] = best / g;
+        scale_host[1] = n_scales / g;
+    }
+    return FA_OK;
+}
+
+int fa_sequential_pack(fa_ctx* ctx, const int64_t* widths, const int64_t* heights, int64_t n, int64_t omega,
+                       int64_t* rows_out, int64_t* x_out, int64_t* y_out, int64_t* used_host, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    int r = check_omega(omega);
+    if (r) return r;
+    if (!ctx || n < 1 || n >= (1ll << 30)) return set_err(FA_VALUE_ERROR, "bad arguments");
+    CK(cudaSetDevice(ctx->device));
+    r = ensure_pack(ctx, n, 1, omega, 1);
+    if (r) return r;
+    ENSURE(dstat, sizeof(fa_dstat));
+    CK(cudaMemsetAsync(ctx->dstat.p, 0, sizeof(fa_dstat), s));
+    CK(cudaMemsetAsync(ctx->cand.p, 0, FA_CAND_REC * 8, s));
+    fa_launch_seq_single((const long long*)widths, (const long long*)heights, (int)n, omega, P<int>(ctx->cand_w),
+                         P<int>(ctx->cand_h), P<int>(ctx->cand_p), P<int>(ctx->cand_y), P<int>(ctx->rowstart),
+                         P<int>(ctx->oidx), fa_front_in_smem(omega) ? nullptr : P<int>(ctx->okey),
+                         P<long long>(ctx->cand), &P<fa_dstat>(ctx->dstat)->done, (long long*)rows_out,
+                         (long long*)x_out, (long long*)y_out, s);
+    CKL();
+    long long rec[3];
+    CK(cudaMemcpyAsync(rec, ctx->cand.p, sizeof(rec), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (used_host) *used_host = rec[1];
+    return FA_OK;
+}
+
+int fa_superblock_pack(fa_ctx* ctx, const int64_t* target_w, const int64_t* target_h, const int64_t* chart_id,
+                       const int64_t* min_tri, int64_t n, int64_t omega, int64_t block_size, int halving_enabled,
+                       int64_t* placements_out, int64_t* scale_host, int64_t* block_used_host, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    int r = check_omega(omega);
+    if (r) return r;
+    if (!ctx || n < 0 || n >= (1ll << 30)) return set_err(FA_VALUE_ERROR, "bad arguments");
+    if (block_size < 1 || (block_size & (block_size - 1)))
+        return set_err(FA_VALUE_ERROR, "block_size must be a power of two");
+    if (block_size > omega) return set_err(FA_VALUE_ERROR, "block_size must not exceed omega");
+    if (omega % block_size) return set_err(FA_VALUE_ERROR, "omega must be divisible by block_size");
+    int n_levels = 1;
+    if (halving_enabled)
+        while ((block_size >> n_levels) >= 16) n_levels++;
+    if (n == 0) {
+        if (scale_host) { scale_host[0] = 1; scale_host[1] = 1; }
+        if (block_used_host) *block_used_host = block_size;
+        return FA_OK;
+    }
+    CK(cudaSetDevice(ctx->device));
+    r = ensure_pack(ctx, n, 1, omega, 1);
+    if (r) return r;
+    ENSURE(dstat, sizeof(fa_dstat));
+    CK(cudaMemsetAsync(ctx->dstat.p, 0, sizeof(fa_dstat), s));
+    fa_dstat* st = P<fa_dstat>(ctx->dstat);
+    int nn = (int)n;
+    fa_launch_orient_sort_mt((const long long*)target_w, (const long long*)target_h, (const long long*)min_tri, nn,
+                             FA_MAX_BOX_DIM, P<long long>(ctx->ow), P<long long>(ctx->oh), P<unsigned char>(ctx->orot),
+                             P<int>(ctx->oidx), P<int>(ctx->pinv), P<unsigned long long>(ctx->sortk),
+                             P<int>(ctx->sortv), 0, st, s);
+    // per level: used_h[nb] + nsh[nb] + 3 * nb * block shelf arrays (largest at the smallest block)
+    long long smallest = block_size >> (n_levels - 1);
+    long long nb_max = (omega / smallest) * (omega / smallest);
+    size_t state_stride = (size_t)(2 * nb_max + 3 * nb_max * smallest);
+    size_t out_stride = (size_t)4 * nn;
+    fa_buf state, xywh, lvl, out;
+    bool ok = fa_ensure(ctx, state, state_stride * n_levels * 4) && fa_ensure(ctx, xywh, out_stride * n_levels * 4) &&
+              fa_ensure(ctx, lvl, 64 * 4) && fa_ensure(ctx, out, 64);
+    if (ok) {
+        fa_launch_superblock(P<long long>(ctx->ow), P<long long>(ctx->oh), (const long long*)target_w,
+                             (const long long*)target_h, (const long long*)chart_id, P<unsigned char>(ctx->orot),
+                             P<int>(ctx->oidx), nn, omega, (int)block_size, n_levels, P<int>(state), state_stride,
+                             P<int>(xywh), out_stride, P<int>(lvl), (long long*)placements_out, P<long long>(out), s);
+        r = FA_OK;
+        cudaError_t e = cudaGetLastError();
+        long long res[3] = {-1, 1, 1};
+        if (e == cudaSuccess) e = cudaMemcpyAsync(res, out.p, sizeof(res), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) {
+            r = set_err(FA_CUDA_ERROR, "superblock: %s", cudaGetErrorString(e));
+        } else if (res[0] < 0) {
+            r = set_err(FA_PACK_FAILURE, "superblock allocation failed at the halving floor");
+        } else {
+            if (scale_host) { scale_host[0] = res[1]; scale_host[1] = res[2]; }
+            if (block_used_host) *block_used_host = block_size >> res[0];
+        }
+    } else {
+        r = set_err(FA_CUDA_ERROR, "out of device memory for superblock state");
+    }
+    free_buf(state);
+    free_buf(xywh);
+    free_buf(lvl);
+    free_buf(out);
+    return r;
+}
+
 int fa_orient(fa_ctx* ctx, const int64_t* target_w, const int64_t* target_h, int64_t n, int64_t* ow_out,
               int64_t* oh_out, uint8_t* rot_out, void* stream) {
     if (!ctx || n < 0 || n >= (1ll << 31)) return set_err(FA_VALUE_ERROR, "bad arguments");

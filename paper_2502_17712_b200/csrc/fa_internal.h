@@ -165,6 +165,22 @@ void fa_launch_uv(const double4* clip, const int* tris, const int* vis_list, con
                   const int* pinv, const double* ndc, const int* px, const long long* placements, int T, int W, int H,
                   long long pad, bool f64, void* uv, fa_dstat* st, cudaStream_t s);
 
+// ---- comparison packers (fa_baselines.cu) -----------------------------------
+void fa_launch_seq_search(const long long* ow, const long long* oh, int n, long long omega, long long n_scales,
+                          long long min_dim, long long pad, int batch, int* cw, int* ch, int* cx, int* cy,
+                          int* rowstart, int* gfront, long long* cand, unsigned* done, cudaStream_t s);
+void fa_launch_seq_single(const long long* w, const long long* h, int n, long long omega, int* cw, int* ch, int* cx,
+                          int* cy, int* rowstart, int* rows, int* gfront, long long* cand, const unsigned* done_zero,
+                          long long* rows_out, long long* x_out, long long* y_out, cudaStream_t s);
+void fa_launch_seq_select(const long long* tw, const long long* th, const long long* cid, const unsigned char* rot,
+                          const int* perm, int n, long long n_scales, const long long* cand, const int* cw,
+                          const int* ch, const int* cx, const int* cy, long long* placements, long long* out,
+                          cudaStream_t s);
+void fa_launch_superblock(const long long* ow, const long long* oh, const long long* tw, const long long* th,
+                          const long long* cid, const unsigned char* rot, const int* perm, int n, long long omega,
+                          int block0, int n_levels, int* state, size_t state_stride, int* xywh, size_t out_stride,
+                          int* level_ok, long long* placements, long long* out, cudaStream_t s);
+
 // ---- standalone helpers (fa_bounds.cu / fa_pack.cu) -------------------------
 void fa_launch_blinn_points(const double* p4, int n, double* out, cudaStream_t s);
 void fa_launch_select_side_plane(const double* t12, int n, int* out, cudaStream_t s);

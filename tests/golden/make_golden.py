@@ -477,6 +477,54 @@ def gen_c2(out):
     print(f"  C2: {r['status']} {r['wall_s']:.1f}s charts={rec['n_charts']} vis={rec['n_visible']}")
 
 
+def gen_baselines(out):
+    """Comparison packers (baselines.py:53-261) on seeded box sets."""
+    from atlaspack import baselines as bl
+    rng = np.random.default_rng(77)
+    seq, sb, prim = [], [], []
+
+    def boxrecs(boxes):
+        return [[b.target_w, b.target_h, b.chart_id, b.min_tri] for b in boxes]
+
+    for k in range(36):
+        om = int(2 ** rng.integers(5, 12))
+        cnt = int(rng.integers(1, 400))
+        boxes = generate_boxes(cnt, om, np.random.default_rng(500 + k))
+        ns = int(rng.choice([8, 16, 64]))
+        md, pad = int(rng.integers(1, 3)), int(rng.integers(0, 2))
+        rec = dict(omega=om, n_scales=ns, min_dim=md, padding=pad, boxes=boxrecs(boxes))
+        try:
+            lay = bl.sequential_scale_search(boxes, om, n_scales=ns, min_dim=md, padding=pad)
+            rec.update(status="ok", **layout_rec(lay))
+        except ap.PackFailure:
+            rec["status"] = "PackFailure"
+        seq.append(rec)
+        blk = max(16, min(om, om // 8))
+        for halving, bsz in ((True, blk), (False, blk), (True, om)):
+            r2 = dict(omega=om, block_size=bsz, halving=halving, boxes=boxrecs(boxes))
+            lay = bl.superblock_pack(boxes, om, bl.SuperblockConfig(block_size=bsz, halving_enabled=halving))
+            if lay is None:
+                r2["status"] = "None"
+            else:
+                r2.update(status="ok", block_used=lay.block_size, **layout_rec(lay))
+            sb.append(r2)
+    for _ in range(100):
+        om = int(2 ** rng.integers(2, 10))
+        n = int(rng.integers(1, 60))
+        widths = np.clip((om * rng.random(n) ** 3).astype(int), 1, om)
+        f = bl.sequential_fold(widths.tolist(), om)
+        heights = rng.integers(1, om + 1, size=n)
+        ordered = ap.order([ap.OrientedBox(w=int(w), h=int(h), rotated=False,
+                                           source=ap.ChartBox(int(w), int(h), i, i))
+                            for i, (w, h) in enumerate(zip(widths, heights))])
+        lay = bl.sequential_pack(ordered, om)
+        prim.append(dict(omega=om, widths=widths.tolist(), rows=f.row_of_box.tolist(), x=f.x_of_box.tolist(),
+                         ordered=[[b.w, b.h, b.source.chart_id] for b in ordered],
+                         pack=None if lay is None else [[p.chart_id, p.x, p.y, p.w, p.h] for p in lay.placements]))
+    with open(os.path.join(out, "baselines.json"), "w") as fh:
+        json.dump(dict(sequential=seq, superblock=sb, prim=prim), fh)
+
+
 def main():
     ap_ = argparse.ArgumentParser()
     ap_.add_argument("--c2", action="store_true", help="also run the ~6 min C2 reference frame")
@@ -493,6 +541,8 @@ def main():
         gen_bounds(out)
     if only is None or "pack" in only:
         gen_pack(out)
+    if only is None or "baselines" in only:
+        gen_baselines(out)
     if only is None or "frames" in only:
         meta["frames"] = gen_frames(out)
     if meta:

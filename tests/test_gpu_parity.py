@@ -414,3 +414,70 @@ def test_union_find_under_contention(frac):
         cs = fa.merge_shared_vertices(fa.ChartSet(lab0), mesh)
         assert np.array_equal(cs.chart_of_triangle, ref)
         assert np.array_equal(cs.vertex_chart_array, ref_v2c)
+
+
+# ---------------------------------------------- comparison packers (§8f-4) ---
+def _bl_cases():
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "baselines.json")) as fh:
+        return json.load(fh)
+
+
+def _plc(lay):
+    return [[p.chart_id, p.x, p.y, p.w, p.h, int(p.rotated), p.target_w, p.target_h] for p in lay.placements]
+
+
+class TestBaselines:
+    def test_sequential_scale_search_vs_reference(self):
+        from paper_2502_17712_b200.baselines import sequential_scale_search
+        for c in _bl_cases()["sequential"]:
+            boxes = [fa.ChartBox(*b) for b in c["boxes"]]
+            if c["status"] != "ok":
+                with pytest.raises(fa.PackFailure):
+                    sequential_scale_search(boxes, c["omega"], c["n_scales"], c["min_dim"], c["padding"])
+                continue
+            lay = sequential_scale_search(boxes, c["omega"], c["n_scales"], c["min_dim"], c["padding"])
+            assert [lay.scale.numerator, lay.scale.denominator] == c["scale"]
+            assert _plc(lay) == c["placements"]
+
+    def test_superblock_vs_reference(self):
+        from paper_2502_17712_b200.baselines import SuperblockConfig, superblock_pack
+        for c in _bl_cases()["superblock"]:
+            boxes = [fa.ChartBox(*b) for b in c["boxes"]]
+            lay = superblock_pack(boxes, c["omega"], SuperblockConfig(c["block_size"], c["halving"]))
+            if c["status"] != "ok":
+                assert lay is None
+                continue
+            assert lay.block_size == c["block_used"]
+            assert [lay.scale.numerator, lay.scale.denominator] == c["scale"]
+            assert _plc(lay) == c["placements"]
+
+    def test_sequential_fold_and_pack_vs_reference(self):
+        from paper_2502_17712_b200.baselines import sequential_fold, sequential_pack
+        for c in _bl_cases()["prim"]:
+            f = sequential_fold(c["widths"], c["omega"])
+            assert f.row_of_box.tolist() == c["rows"] and f.x_of_box.tolist() == c["x"]
+            ordered = [fa.OrientedBox(w=o[0], h=o[1], rotated=False, source=fa.ChartBox(o[0], o[1], o[2], o[2]))
+                       for o in c["ordered"]]
+            lay = sequential_pack(ordered, c["omega"])
+            if c["pack"] is None:
+                assert lay is None
+            else:
+                assert [[p.chart_id, p.x, p.y, p.w, p.h] for p in lay.placements] == c["pack"]
+
+    def test_make_packer_registry(self):
+        from paper_2502_17712_b200.cli import make_packer
+        c = next(c for c in _bl_cases()["sequential"] if c["status"] == "ok")
+        boxes = [fa.ChartBox(*b) for b in c["boxes"]]
+        for name in ("fastatlas", "sequential"):
+            lay = make_packer(name, 64, 1, 0)(boxes, c["omega"])
+            assert len(lay.placements) == len(boxes)
+        sb = next(s for s in _bl_cases()["superblock"] if s["status"] == "ok")
+        lay = make_packer("superblock", 64, 1, 0, block_size=sb["block_size"])(
+            [fa.ChartBox(*b) for b in sb["boxes"]], sb["omega"])
+        assert _plc(lay) == sb["placements"]
+        bad = next(s for s in _bl_cases()["superblock"] if s["status"] != "ok" and s["halving"])
+        with pytest.raises(fa.PackFailure):
+            make_packer("superblock", 64, 1, 0, block_size=bad["block_size"])(
+                [fa.ChartBox(*b) for b in bad["boxes"]], bad["omega"])
