@@ -267,8 +267,8 @@ static int launch_depth(fa_ctx* ctx, int W, int H, int cull, unsigned char* flag
     fa_launch_raster_setup(true, P<double4>(ctx->clip), ctx->tris, T, W, H, cull,
                            P<unsigned long long>(ctx->depth_keys), P<int>(ctx->small_list), P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large),
                            ctx->max_large, P<int2>(ctx->tiles), ctx->max_tiles, P<fa_dstat>(ctx->dstat), s);
-    fa_launch_raster_depth_tiles(P<TriSetup>(ctx->large), P<int2>(ctx->tiles), ctx->max_tiles, W,
-                                 P<unsigned long long>(ctx->depth_keys), P<fa_dstat>(ctx->dstat), s);
+    fa_launch_raster_depth_tiles(P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large), P<int2>(ctx->tiles),
+                                 ctx->max_tiles, W, P<unsigned long long>(ctx->depth_keys), P<fa_dstat>(ctx->dstat), s);
     nl += 4;
     return FA_OK;
 }
@@ -659,8 +659,8 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     fa_launch_raster_setup(true, P<double4>(ctx->clip), ctx->tris, T, W, H, p->backface_cull,
                            P<unsigned long long>(ctx->depth_keys), P<int>(ctx->small_list), P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large),
                            ctx->max_large, P<int2>(ctx->tiles), ctx->max_tiles, st, s);
-    fa_launch_raster_depth_tiles(P<TriSetup>(ctx->large), P<int2>(ctx->tiles), ctx->max_tiles, W,
-                                 P<unsigned long long>(ctx->depth_keys), st, s);
+    fa_launch_raster_depth_tiles(P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large), P<int2>(ctx->tiles),
+                                 ctx->max_tiles, W, P<unsigned long long>(ctx->depth_keys), st, s);
     fa_launch_count_finite(P<unsigned long long>(ctx->depth_keys), (long long)W * H, st, s);
     nl += 4;
     mark();  // 2: depth pass

@@ -49,11 +49,12 @@ struct fa_dstat {
     int max_h;            // max oriented height (sort key range)
     unsigned int done;    // pack batch early-exit
     int n_small3;         // stored small-triangle records (pass 2 input)
+    int n_large3;         // compact large-triangle records (stored from the back of the record array)
     int stretch_valid;    // triangles that entered the stretch sums
     double stretch_wsum;  // sum area * (S1^2 + S2^2) / 2   (metrics.py:103)
     double stretch_area;  // sum area                       (metrics.py:104)
     unsigned long long stretch_linf_bits;  // max S1 (positive double bits)
-    int pad[37];
+    int pad[36];
 };
 
 // ---- float64 <-> order-preserving u64 key --------------------------------

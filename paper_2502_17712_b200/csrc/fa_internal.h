@@ -73,7 +73,7 @@ void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* c
 void fa_launch_raster_setup(bool write_depth, const double4* clip, const int* tris, int T, int W, int H, int cull,
                             unsigned long long* depth, int* small_list, SmallRec* small_rec, TriSetup* large,
                             int max_large, int2* tiles, int max_tiles, fa_dstat* st, cudaStream_t s);
-void fa_launch_raster_depth_tiles(const TriSetup* large, const int2* tiles, int max_tiles, int W,
+void fa_launch_raster_depth_tiles(const SmallRec* recs, const TriSetup* large, const int2* tiles, int max_tiles, int W,
                                   unsigned long long* depth, fa_dstat* st, cudaStream_t s);
 void fa_launch_raster_vis(const double4* clip, const int* tris, const int* small_list, const SmallRec* small_rec,
                           const TriSetup* large,

@@ -92,6 +92,19 @@ __global__ void __launch_bounds__(256, 3) k_raster_setup(const double4* __restri
                 store_rec(f, t, small_rec + slot);
                 continue;
             }
+            // unclipped large triangle: compact record from the back of the
+            // record array (small + large <= T, so the two ends never meet);
+            // tiles reference it by a non-negative index
+            int slot = active_append1(&st->n_large3);
+            int ri = T - slot;
+            store_rec(f, t, small_rec + ri);
+            int tx = (bw + TILE_W - 1) / TILE_W, ty = (bh + TILE_H - 1) / TILE_H;
+            int nt = tx * ty;
+            int base = atomicAdd(&st->n_tiles, nt);
+            int end = base + nt;
+            if (end > max_tiles) { atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW); end = max_tiles; }
+            for (int k = base; k < end; k++) tiles[k] = make_int2(ri, k - base);
+            continue;
         }
         TriSetup s;
         int r;
@@ -138,7 +151,8 @@ __global__ void __launch_bounds__(256, 3) k_raster_setup(const double4* __restri
             // capacity) and flag the frame; the host grows the queue and reruns
             int end = base + nt;
             if (end > max_tiles) { atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW); end = max_tiles; }
-            for (int k = base; k < end; k++) tiles[k] = make_int2(slot, k - base);
+            // generic (clipped) setups are referenced by negative ids
+            for (int k = base; k < end; k++) tiles[k] = make_int2(-slot - 1, k - base);
         }
     }
 }
@@ -170,8 +184,28 @@ __device__ __forceinline__ void load_setup_warp(const TriSetup* __restrict__ g, 
     __syncwarp();
 }
 
+// tile (ti) of a bbox -> this lane's pixel column x and first row y0
+// (16 columns x 2 rows per step; 4 steps cover the 16x8 tile)
+__device__ __forceinline__ void tile_lane_origin(int min_x, int max_x, int min_y, int ti, int& x, int& y0) {
+    int tx = (max_x - min_x + 1 + TILE_W - 1) / TILE_W;
+    int lane = lane_id();
+    x = min_x + (ti % tx) * TILE_W + (lane & 15);
+    y0 = min_y + (ti / tx) * TILE_H + (lane >> 4);
+}
+
+__device__ __forceinline__ int tile_centre(int min_x, int max_x, int min_y, int max_y) {
+    int bw = max_x - min_x + 1;
+    int tx = (bw + TILE_W - 1) / TILE_W;
+    return ((max_y - min_y + 1) / 2 / TILE_H) * tx + (bw / 2) / TILE_W;
+}
+
 // ---- pass 1 large: one warp per 16x8 tile --------------------------------
-__global__ void __launch_bounds__(256) k_raster_depth_tiles(const TriSetup* __restrict__ large,
+// Tile records: x >= 0 indexes a compact unclipped record (every lane loads
+// the same 96 bytes — one broadcast transaction per LDG — and rebuilds the
+// edge functions in registers); x < 0 is a generic clipped setup, staged in
+// warp-private shared memory.
+__global__ void __launch_bounds__(256) k_raster_depth_tiles(const SmallRec* __restrict__ recs,
+                                                            const TriSetup* __restrict__ large,
                                                             const int2* __restrict__ tiles, int W,
                                                             unsigned long long* __restrict__ depth,
                                                             fa_dstat* __restrict__ st, int max_tiles) {
@@ -181,6 +215,28 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const TriSetup* __re
     int n_tiles = min(st->n_tiles, max_tiles);
     for (int w = blockIdx.x * 8 + warp; w < n_tiles; w += nwarps) {
         int2 rec = tiles[w];
+        if (rec.x >= 0) {
+            Setup3 f;
+            int t;
+            load_rec(recs + rec.x, f, t);
+            int x, y0;
+            tile_lane_origin(f.min_x, f.max_x, f.min_y, rec.y, x, y0);
+            if (x <= f.max_x) {
+                double px = (double)x + 0.5;
+#pragma unroll
+                for (int k = 0; k < TILE_H / 2; k++) {
+                    int y = y0 + 2 * k;
+                    if (y > f.max_y) break;
+                    double py = (double)y + 0.5;
+                    if (!sample_inside3(f, px, py)) continue;
+                    unsigned long long key = f64_key(sample_depth3(f, px, py));
+                    unsigned long long* d = depth + (long long)y * W + x;
+                    if (key < *d) atomicMin(d, key);
+                }
+            }
+            continue;
+        }
+        rec.x = -rec.x - 1;
         __syncwarp();
         load_setup_warp(large + rec.x, &sm[warp]);
         const TriSetup& s = sm[warp];
@@ -411,7 +467,8 @@ __global__ void __launch_bounds__(256) k_raster_vis_small(const double4* __restr
 }
 
 // ---- pass 2 large: one warp per tile --------------------------------------
-__global__ void __launch_bounds__(256) k_raster_vis_tiles(const TriSetup* __restrict__ large,
+__global__ void __launch_bounds__(256) k_raster_vis_tiles(const SmallRec* __restrict__ recs, int T,
+                                                          const TriSetup* __restrict__ large,
                                                           const int2* __restrict__ tiles, int W,
                                                           const unsigned long long* __restrict__ depth,
                                                           unsigned char* __restrict__ flags,
@@ -419,19 +476,58 @@ __global__ void __launch_bounds__(256) k_raster_vis_tiles(const TriSetup* __rest
                                                           int max_large, int phase) {
     // phase 0: the tile at the centre of each large triangle's bbox (most
     // visible triangles are decided there); phase 1: every other tile of the
-    // triangles that are still not visible.
+    // triangles that are still not visible.  Phase-0 items are the compact
+    // records (stored downward from index T) followed by the generic setups.
     __shared__ TriSetup sm[8];
     int warp = threadIdx.x >> 5, lane = lane_id();
     int nwarps = gridDim.x * 8;
-    int n_items = phase == 0 ? min(st->n_large, max_large) : min(st->n_tiles, max_tiles);
+    int n3 = st->n_large3;
+    int n_items = phase == 0 ? n3 + min(st->n_large, max_large) : min(st->n_tiles, max_tiles);
     for (int w = blockIdx.x * 8 + warp; w < n_items; w += nwarps) {
         int2 rec;
         if (phase == 0) {
-            rec.x = w;
+            rec.x = w < n3 ? T - w : -(w - n3) - 1;
             rec.y = -1;
         } else {
             rec = tiles[w];
         }
+        if (rec.x >= 0) {
+            Setup3 f;
+            int t;
+            load_rec(recs + rec.x, f, t);
+            int seen = 0;
+            if (lane == 0) seen = *(volatile unsigned char*)(flags + t);
+            if (__shfl_sync(0xffffffffu, seen, 0)) continue;  // already visible (warp-uniform)
+            int centre = tile_centre(f.min_x, f.max_x, f.min_y, f.max_y);
+            if (phase == 0) rec.y = centre;
+            else if (rec.y == centre) continue;
+            int x, y0;
+            tile_lane_origin(f.min_x, f.max_x, f.min_y, rec.y, x, y0);
+            bool vis = false;
+            if (x <= f.max_x) {
+                // evaluate the lane's 4 samples, then issue their depth
+                // loads together (static indices keep the arrays in registers)
+                double px = (double)x + 0.5;
+                double zq[TILE_H / 2];
+                bool in[TILE_H / 2];
+                unsigned long long kq[TILE_H / 2];
+#pragma unroll
+                for (int k = 0; k < TILE_H / 2; k++) {
+                    int y = y0 + 2 * k;
+                    double py = (double)y + 0.5;
+                    in[k] = y <= f.max_y && sample_inside3(f, px, py);
+                    zq[k] = in[k] ? sample_depth3(f, px, py) : 0.0;
+                }
+#pragma unroll
+                for (int k = 0; k < TILE_H / 2; k++)
+                    kq[k] = in[k] ? depth[(long long)(y0 + 2 * k) * W + x] : 0ull;
+#pragma unroll
+                for (int k = 0; k < TILE_H / 2; k++) vis = vis || (in[k] && depth_passes(zq[k], key_f64(kq[k])));
+            }
+            if (__any_sync(0xffffffffu, vis) && lane == 0) flags[t] = 1;
+            continue;
+        }
+        rec.x = -rec.x - 1;
         int t = __ldg(&large[rec.x].tri);
         int seen = 0;
         if (lane == 0) seen = *(volatile unsigned char*)(flags + t);
@@ -489,9 +585,9 @@ void fa_launch_raster_setup(bool write_depth, const double4* clip, const int* tr
     if (write_depth) fa_launch_small_coop(false, small_rec, T, W, depth, nullptr, st, s);
 }
 
-void fa_launch_raster_depth_tiles(const TriSetup* large, const int2* tiles, int max_tiles, int W,
+void fa_launch_raster_depth_tiles(const SmallRec* recs, const TriSetup* large, const int2* tiles, int max_tiles, int W,
                                   unsigned long long* depth, fa_dstat* st, cudaStream_t s) {
-    k_raster_depth_tiles<<<FA_NUM_SMS * 8, 256, 0, s>>>(large, tiles, W, depth, st, max_tiles);
+    k_raster_depth_tiles<<<FA_NUM_SMS * 8, 256, 0, s>>>(recs, large, tiles, W, depth, st, max_tiles);
 }
 
 void fa_launch_raster_vis(const double4* clip, const int* tris, const int* small_list, const SmallRec* small_rec,
@@ -501,8 +597,10 @@ void fa_launch_raster_vis(const double4* clip, const int* tris, const int* small
                           cudaStream_t s) {
     k_raster_vis_small<<<fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s>>>(clip, tris, small_list, small_rec, W, H, cull,
                                                                        depth, flags, st);
-    k_raster_vis_tiles<<<FA_NUM_SMS * 8, 256, 0, s>>>(large, tiles, W, depth, flags, st, max_tiles, max_large, 0);
-    k_raster_vis_tiles<<<FA_NUM_SMS * 8, 256, 0, s>>>(large, tiles, W, depth, flags, st, max_tiles, max_large, 1);
+    k_raster_vis_tiles<<<FA_NUM_SMS * 8, 256, 0, s>>>(small_rec, T, large, tiles, W, depth, flags, st, max_tiles,
+                                                      max_large, 0);
+    k_raster_vis_tiles<<<FA_NUM_SMS * 8, 256, 0, s>>>(small_rec, T, large, tiles, W, depth, flags, st, max_tiles,
+                                                      max_large, 1);
 }
 
 void fa_launch_small_coop(bool vis, const SmallRec* recs, int T, int W, unsigned long long* depth,
