@@ -110,12 +110,12 @@ void fa_destroy(fa_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
-    fa_buf* bufs[] = {&c->small_rec, &c->clip, &c->depth_keys, &c->depth_f64, &c->flags, &c->vis_list, &c->small_list, &c->large,
+    fa_buf* bufs[] = {&c->small_rec, &c->clip, &c->depth_keys, &c->depth_f64, &c->flags, &c->vis_list, &c->large,
                       &c->tiles, &c->label, &c->vmin, &c->v2c, &c->cidx, &c->roots, &c->ndc_keys, &c->ndc, &c->px,
                       &c->target, &c->survived, &c->okey, &c->oidx, &c->ow, &c->oh, &c->orot, &c->sortk, &c->sortv,
                       &c->pinv, &c->cand, &c->cand_p, &c->cand_w, &c->cand_h, &c->cand_y, &c->rowstart,
                       &c->placements, &c->uv, &c->vp_dev, &c->blocks, &c->dstat, &c->aux, &c->in_tw, &c->in_th,
-                      &c->in_cid, &c->in_mt};
+                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list};
     for (fa_buf* b : bufs) free_buf(*b);
     if (c->hstat) cudaFreeHost(c->hstat);
     if (c->hvp) cudaFreeHost(c->hvp);
@@ -144,9 +144,10 @@ int fa_set_mesh(fa_ctx* ctx, const double* positions, int64_t n_vertices, const 
 static int ensure_raster(fa_ctx* ctx, int W, int H, bool depth) {
     int64_t T = ctx->T, V = ctx->V;
     ENSURE(clip, (V > 0 ? V : 1) * sizeof(double4));
+    ENSURE(scr, (V > 0 ? V : 1) * sizeof(double4));
     if (depth) ENSURE(depth_keys, (size_t)W * H * 8);
     ENSURE(flags, ((T + 15) / 16 + 1) * 16);
-    ENSURE(small_list, (T + 1) * 4);
+    ENSURE(clip_list, (T + 1) * 4);
     ENSURE(small_rec, (T + 1) * sizeof(SmallRec));
     long long want_tiles = (long long)W * H / 32;
     if (want_tiles > ctx->max_tiles) ctx->max_tiles = (int)(want_tiles < (1ll << 30) ? want_tiles : (1 << 30));
@@ -262,14 +263,15 @@ static int upload_vp(fa_ctx* ctx, const double* vp_host, cudaStream_t s) {
 // depth pass (shared by fa_depth_prepass and the frame)
 static int launch_depth(fa_ctx* ctx, int W, int H, int cull, unsigned char* flags_out, cudaStream_t s, int& nl) {
     int T = (int)ctx->T, V = (int)ctx->V;
-    fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), P<int>(ctx->vmin),
-                         P<unsigned long long>(ctx->depth_keys), (long long)W * H, flags_out, T, s);
-    fa_launch_raster_setup(true, P<double4>(ctx->clip), ctx->tris, T, W, H, cull,
-                           P<unsigned long long>(ctx->depth_keys), P<int>(ctx->small_list), P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large),
-                           ctx->max_large, P<int2>(ctx->tiles), ctx->max_tiles, P<fa_dstat>(ctx->dstat), s);
+    fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), P<double4>(ctx->scr), W, H,
+                         P<int>(ctx->vmin), P<unsigned long long>(ctx->depth_keys), (long long)W * H, flags_out, T, s);
+    fa_launch_raster_setup(true, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, W, H, cull,
+                           P<unsigned long long>(ctx->depth_keys), P<SmallRec>(ctx->small_rec),
+                           P<int>(ctx->clip_list), P<TriSetup>(ctx->large), ctx->max_large, P<int2>(ctx->tiles),
+                           ctx->max_tiles, P<fa_dstat>(ctx->dstat), s);
     fa_launch_raster_depth_tiles(P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large), P<int2>(ctx->tiles),
                                  ctx->max_tiles, W, P<unsigned long long>(ctx->depth_keys), P<fa_dstat>(ctx->dstat), s);
-    nl += 4;
+    nl += 5;
     return FA_OK;
 }
 
@@ -282,8 +284,8 @@ int fa_project(fa_ctx* ctx, const double* vp_host, double* clip_out, void* strea
     ENSURE(vp_dev, 16 * sizeof(double));
     int r = upload_vp(ctx, vp_host, s);
     if (r) return r;
-    fa_launch_frame_init(ctx->pos, (int)ctx->V, P<double>(ctx->vp_dev), (double4*)clip_out, nullptr, nullptr, 0,
-                         nullptr, 0, s);
+    fa_launch_frame_init(ctx->pos, (int)ctx->V, P<double>(ctx->vp_dev), (double4*)clip_out, nullptr, 0, 0, nullptr,
+                         nullptr, 0, nullptr, 0, s);
     CKL();
     return FA_OK;
 }
@@ -330,16 +332,16 @@ int fa_mark_visible(fa_ctx* ctx, const double* vp_host, const double* depth, int
         CK(cudaMemsetAsync(ctx->dstat.p, 0, sizeof(fa_dstat), s));
         r = upload_vp(ctx, vp_host, s);
         if (r) return r;
-        fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), nullptr, nullptr, 0,
-                             P<unsigned char>(ctx->flags), T, s);
+        fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), P<double4>(ctx->scr), width,
+                             height, nullptr, nullptr, 0, P<unsigned char>(ctx->flags), T, s);
         fa_launch_encode_depth(depth, P<unsigned long long>(ctx->depth_keys), (long long)width * height, s);
-        fa_launch_raster_setup(false, P<double4>(ctx->clip), ctx->tris, T, width, height, backface_cull, nullptr,
-                               P<int>(ctx->small_list), P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large), ctx->max_large, P<int2>(ctx->tiles),
+        fa_launch_raster_setup(false, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, width, height,
+                               backface_cull, nullptr, P<SmallRec>(ctx->small_rec),
+                               P<int>(ctx->clip_list), P<TriSetup>(ctx->large), ctx->max_large, P<int2>(ctx->tiles),
                                ctx->max_tiles, P<fa_dstat>(ctx->dstat), s);
-        fa_launch_raster_vis(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->small_list), P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large),
-                             P<int2>(ctx->tiles), ctx->max_tiles, ctx->max_large, T,width, height, backface_cull,
-                             P<unsigned long long>(ctx->depth_keys), P<unsigned char>(ctx->flags),
-                             P<fa_dstat>(ctx->dstat), s);
+        fa_launch_raster_vis(P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large), P<int2>(ctx->tiles),
+                             ctx->max_tiles, ctx->max_large, T, width, P<unsigned long long>(ctx->depth_keys),
+                             P<unsigned char>(ctx->flags), P<fa_dstat>(ctx->dstat), s);
         CKL();
         r = read_stat(ctx, s);
         if (r) return r;
@@ -447,8 +449,8 @@ int fa_chart_boxes(fa_ctx* ctx, const double* vp_host, const int32_t* labels, in
     if (r) return r;
     fa_dstat* st = P<fa_dstat>(ctx->dstat);
     unsigned char* fl = P<unsigned char>(ctx->flags);
-    fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), nullptr, nullptr, 0, nullptr, 0,
-                         s);
+    fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), nullptr, 0, 0, nullptr, nullptr, 0,
+                         nullptr, 0, s);
     fa_launch_flags_from_labels(labels, fl, T, s);
     fa_launch_compact_visible(fl, T, P<int>(ctx->blocks), P<int>(ctx->vis_list), P<int>(ctx->aux), st, s);
     fa_launch_compact_roots(P<int>(ctx->vis_list), labels, T, P<int>(ctx->blocks), P<int>(ctx->roots),
@@ -652,22 +654,22 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     (void)T_;
     int V_ = V;
     mark();  // 0: start
-    fa_launch_frame_init(ctx->pos, V_, P<double>(ctx->vp_dev), P<double4>(ctx->clip), P<int>(ctx->vmin),
-                         P<unsigned long long>(ctx->depth_keys), (long long)W * H, flags, T, s);
+    fa_launch_frame_init(ctx->pos, V_, P<double>(ctx->vp_dev), P<double4>(ctx->clip), P<double4>(ctx->scr), W, H,
+                         P<int>(ctx->vmin), P<unsigned long long>(ctx->depth_keys), (long long)W * H, flags, T, s);
     nl += 1;
     mark();  // 1: project + clears
-    fa_launch_raster_setup(true, P<double4>(ctx->clip), ctx->tris, T, W, H, p->backface_cull,
-                           P<unsigned long long>(ctx->depth_keys), P<int>(ctx->small_list), P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large),
-                           ctx->max_large, P<int2>(ctx->tiles), ctx->max_tiles, st, s);
+    fa_launch_raster_setup(true, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, W, H, p->backface_cull,
+                           P<unsigned long long>(ctx->depth_keys), P<SmallRec>(ctx->small_rec),
+                           P<int>(ctx->clip_list), P<TriSetup>(ctx->large), ctx->max_large, P<int2>(ctx->tiles),
+                           ctx->max_tiles, st, s);
     fa_launch_raster_depth_tiles(P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large), P<int2>(ctx->tiles),
                                  ctx->max_tiles, W, P<unsigned long long>(ctx->depth_keys), st, s);
     fa_launch_count_finite(P<unsigned long long>(ctx->depth_keys), (long long)W * H, st, s);
-    nl += 4;
+    nl += 5;
     mark();  // 2: depth pass
-    fa_launch_raster_vis(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->small_list), P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large),
-                         P<int2>(ctx->tiles), ctx->max_tiles, ctx->max_large, T,W, H, p->backface_cull,
-                         P<unsigned long long>(ctx->depth_keys), flags, st, s);
-    nl += 3;  // records + generic small, centre tiles, remaining tiles
+    fa_launch_raster_vis(P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large), P<int2>(ctx->tiles), ctx->max_tiles,
+                         ctx->max_large, T, W, P<unsigned long long>(ctx->depth_keys), flags, st, s);
+    nl += 3;  // small records, centre tiles (+ small clipped windows), remaining tiles
     mark();  // 3: visibility pass
     fa_launch_compact_visible(flags, T, P<int>(ctx->blocks), P<int>(ctx->vis_list), P<int>(ctx->label), st, s);
     nl += 2;

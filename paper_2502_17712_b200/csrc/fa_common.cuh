@@ -50,12 +50,14 @@ struct fa_dstat {
     unsigned int done;    // pack batch early-exit
     int n_small3;         // stored small-triangle records (pass 2 input)
     int n_large3;         // compact large-triangle records (stored from the back of the record array)
+    int n_clip;           // triangles routed to the generic (clipping) path
     int stretch_valid;    // triangles that entered the stretch sums
     double stretch_wsum;  // sum area * (S1^2 + S2^2) / 2   (metrics.py:103)
     double stretch_area;  // sum area                       (metrics.py:104)
     unsigned long long stretch_linf_bits;  // max S1 (positive double bits)
-    int pad[36];
+    int pad[34];
 };
+static_assert(sizeof(fa_dstat) == 256, "fa_dstat is one 256-byte block");
 
 // ---- float64 <-> order-preserving u64 key --------------------------------
 __device__ __forceinline__ unsigned long long f64_key(double x) {

@@ -39,10 +39,11 @@ struct fa_ctx {
     int64_t V = 0, T = 0;
 
     // scratch (grown on demand)
-    fa_buf small_rec, clip, depth_keys, depth_f64, flags, vis_list, small_list, large, tiles, label, vmin, v2c, cidx;
+    fa_buf small_rec, clip, depth_keys, depth_f64, flags, vis_list, large, tiles, label, vmin, v2c, cidx;
     fa_buf roots, ndc_keys, ndc, px, target, survived, okey, oidx, ow, oh, orot, sortk, sortv, pinv;
     fa_buf cand, cand_p, cand_w, cand_h, cand_y, rowstart, placements, uv, vp_dev, blocks, dstat, aux;
     fa_buf in_tw, in_th, in_cid, in_mt;
+    fa_buf scr, clip_list;  // per-vertex screen records; generic-path triangle list
     size_t gen = 0;
     int max_large = 0, max_tiles = 0;
     int pack_batch = 0;  // candidates per pack launch
@@ -68,17 +69,18 @@ struct fa_ctx {
 bool fa_ensure(fa_ctx* ctx, fa_buf& b, size_t bytes);
 
 // ---- raster (fa_raster.cu) ------------------------------------------------
-void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* clip, int* vmin,
+void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* clip, double4* scr, int W, int H,
+                          int* vmin,
                           unsigned long long* depth, long long npx, unsigned char* flags, int T, cudaStream_t s);
-void fa_launch_raster_setup(bool write_depth, const double4* clip, const int* tris, int T, int W, int H, int cull,
-                            unsigned long long* depth, int* small_list, SmallRec* small_rec, TriSetup* large,
-                            int max_large, int2* tiles, int max_tiles, fa_dstat* st, cudaStream_t s);
+void fa_launch_raster_setup(bool write_depth, const double4* clip, const double4* scr, const int* tris, int T, int W,
+                            int H, int cull, unsigned long long* depth, SmallRec* small_rec,
+                            int* clip_list, TriSetup* large, int max_large, int2* tiles, int max_tiles, fa_dstat* st,
+                            cudaStream_t s);
 void fa_launch_raster_depth_tiles(const SmallRec* recs, const TriSetup* large, const int2* tiles, int max_tiles, int W,
                                   unsigned long long* depth, fa_dstat* st, cudaStream_t s);
-void fa_launch_raster_vis(const double4* clip, const int* tris, const int* small_list, const SmallRec* small_rec,
-                          const TriSetup* large,
-                          const int2* tiles, int max_tiles, int max_large, int T, int W, int H, int cull,
-                          const unsigned long long* depth, unsigned char* flags, const fa_dstat* st, cudaStream_t s);
+void fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const int2* tiles, int max_tiles,
+                          int max_large, int T, int W, const unsigned long long* depth, unsigned char* flags,
+                          const fa_dstat* st, cudaStream_t s);
 void fa_launch_decode_depth(const unsigned long long* keys, double* out, long long n, cudaStream_t s);
 void fa_launch_count_finite(const unsigned long long* depth, long long npx, fa_dstat* st, cudaStream_t s);
 void fa_launch_small_coop(bool vis, const SmallRec* recs, int T, int W, unsigned long long* depth,

@@ -33,7 +33,7 @@ __device__ __forceinline__ int active_append1(int* counter) {
 
 // ---- frame init: projection + buffer clears ------------------------------
 __global__ void k_frame_init(const double* __restrict__ pos, int V, const double* __restrict__ vp_dev,
-                             double4* __restrict__ clip,
+                             double4* __restrict__ clip, double4* __restrict__ scr, int W, int H,
                              int* __restrict__ vmin, unsigned long long* __restrict__ depth, long long npx,
                              unsigned int* __restrict__ flags32, int nflag32) {
     long long stride = (long long)gridDim.x * blockDim.x;
@@ -43,7 +43,9 @@ __global__ void k_frame_init(const double* __restrict__ pos, int V, const double
     for (int i = 0; i < 16; i++) m[i] = __ldg(vp_dev + i);
     for (long long v = i0; v < V; v += stride) {
         double x = pos[3 * v], y = pos[3 * v + 1], z = pos[3 * v + 2];
-        clip[v] = project_point(x, y, z, m);
+        double4 c = project_point(x, y, z, m);
+        clip[v] = c;
+        if (scr) scr[v] = vertex_screen(c, W, H);
         if (vmin) vmin[v] = 0x7fffffff;
     }
     if (depth) {
@@ -68,91 +70,161 @@ __global__ void k_encode_depth(const double* __restrict__ in, unsigned long long
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) keys[i] = f64_key(in[i]);
 }
 
-// ---- pass 1: setup + small raster + large enqueue -------------------------
-// WRITE_DEPTH=false builds the work lists only (standalone mark_visible).
-template <bool WRITE_DEPTH>
-__global__ void __launch_bounds__(256, 3) k_raster_setup(const double4* __restrict__ clip, const int* __restrict__ tris,
+// ---- pass 1: setup + record / tile enqueue --------------------------------
+// One warp per 32 consecutive triangles (warp-uniform loop, so every append
+// is one warp-aggregated atomic).  Per triangle: 3 index loads, 3 gathers of
+// the per-vertex screen records, the exact cull / bbox / edge / plane setup
+// (tri_setup3s), then
+//   small unclipped  -> 96-byte record at the front of `recs` (k_small_coop),
+//   large unclipped  -> record at the back of `recs` + its 16x8 tiles, whose
+//                       descriptors the warp writes together,
+//   anything else    -> index into `clip_list` for k_raster_clipped.
+// Nothing is rasterized here, so no lane waits on another's pixels.
+__global__ void __launch_bounds__(256) k_raster_setup(const double4* __restrict__ scr, const int* __restrict__ tris,
                                                       int T, int W, int H, int cull,
-                                                      unsigned long long* __restrict__ depth,
-                                                      int* __restrict__ small_list, SmallRec* __restrict__ small_rec,
-                                                      TriSetup* __restrict__ large,
-                                                      int max_large, int2* __restrict__ tiles, int max_tiles,
+                                                      SmallRec* __restrict__ recs, int* __restrict__ clip_list,
+                                                      int2* __restrict__ tiles, int max_tiles,
                                                       fa_dstat* __restrict__ st) {
-    int stride = gridDim.x * blockDim.x;
+    const int lane = lane_id();
+    const int wpb = blockDim.x >> 5;
+    const int total_warps = gridDim.x * wpb;
     const bool rec_ok = W <= 32767 && H <= 32767;
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += stride) {
+    const unsigned lt_mask = (1u << lane) - 1u;
+    for (int base = (blockIdx.x * wpb + (threadIdx.x >> 5)) * 32; base < T; base += total_warps * 32) {
+        const int t = base + lane;
         Setup3 f;
-        int r3 = tri_setup3(clip, tris, t, W, H, cull != 0, f);
-        if (r3 == 0) continue;
-        if (r3 == 1 && rec_ok) {
-            int bw = f.max_x - f.min_x + 1, bh = f.max_y - f.min_y + 1;
-            if (bw * bh <= FA_SMALL_PX) {
-                // unclipped small triangle: record it; k_small_coop samples it
-                int slot = active_append1(&st->n_small3);
-                store_rec(f, t, small_rec + slot);
-                continue;
+        int kind = 0;  // 0 none, 1 small record, 2 large record, 3 generic path
+        int nt = 0;
+        if (t < T) {
+            int ia = __ldg(tris + 3 * t), ib = __ldg(tris + 3 * t + 1), ic = __ldg(tris + 3 * t + 2);
+            int r3 = tri_setup3s(scr, ia, ib, ic, W, H, cull != 0, f);
+            if (r3 == 2 || (r3 == 1 && !rec_ok)) {
+                kind = 3;
+            } else if (r3 == 1) {
+                int bw = f.max_x - f.min_x + 1, bh = f.max_y - f.min_y + 1;
+                if (bw * bh <= FA_SMALL_PX) {
+                    kind = 1;
+                } else {
+                    kind = 2;
+                    nt = ((bw + TILE_W - 1) / TILE_W) * ((bh + TILE_H - 1) / TILE_H);
+                }
             }
-            // unclipped large triangle: compact record from the back of the
-            // record array (small + large <= T, so the two ends never meet);
-            // tiles reference it by a non-negative index
-            int slot = active_append1(&st->n_large3);
-            int ri = T - slot;
-            store_rec(f, t, small_rec + ri);
-            int tx = (bw + TILE_W - 1) / TILE_W, ty = (bh + TILE_H - 1) / TILE_H;
-            int nt = tx * ty;
-            int base = atomicAdd(&st->n_tiles, nt);
-            int end = base + nt;
-            if (end > max_tiles) { atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW); end = max_tiles; }
-            for (int k = base; k < end; k++) tiles[k] = make_int2(ri, k - base);
+        }
+        const unsigned m1 = __ballot_sync(0xffffffffu, kind == 1);
+        const unsigned m2 = __ballot_sync(0xffffffffu, kind == 2);
+        const unsigned m3 = __ballot_sync(0xffffffffu, kind == 3);
+        if (m1) {
+            int b = 0;
+            if (lane == 0) b = atomicAdd(&st->n_small3, __popc(m1));
+            b = __shfl_sync(0xffffffffu, b, 0);
+            if (kind == 1) store_rec(f, t, recs + b + __popc(m1 & lt_mask));
+        }
+        if (m3) {
+            int b = 0;
+            if (lane == 0) b = atomicAdd(&st->n_clip, __popc(m3));
+            b = __shfl_sync(0xffffffffu, b, 0);
+            if (kind == 3) clip_list[b + __popc(m3 & lt_mask)] = t;
+        }
+        if (m2) {
+            // large records are stored downward from index T (small + large
+            // records <= T, so the two ends never meet)
+            int incl = nt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            int total = __shfl_sync(0xffffffffu, incl, 31);
+            int rb = 0, tb = 0;
+            if (lane == 0) {
+                rb = atomicAdd(&st->n_large3, __popc(m2));
+                tb = atomicAdd(&st->n_tiles, total);
+            }
+            rb = __shfl_sync(0xffffffffu, rb, 0);
+            tb = __shfl_sync(0xffffffffu, tb, 0);
+            int ri = T - (rb + __popc(m2 & lt_mask));
+            if (kind == 2) store_rec(f, t, recs + ri);
+            if (tb + total > max_tiles && lane == 0) atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW);
+            // the warp writes every large lane's tile descriptors, coalesced
+            unsigned m = m2;
+            while (m) {
+                int src = __ffs(m) - 1;
+                m &= m - 1;
+                int r_src = __shfl_sync(0xffffffffu, ri, src);
+                int n_src = __shfl_sync(0xffffffffu, nt, src);
+                int e_src = tb + __shfl_sync(0xffffffffu, incl, src) - n_src;
+                for (int k = lane; k < n_src; k += 32)
+                    if (e_src + k < max_tiles) tiles[e_src + k] = make_int2(r_src, k);
+            }
+        }
+    }
+}
+
+// ---- pass 1, generic path: clipped polygons (and oversize screens) --------
+// One warp per listed triangle: lane 0 clips and builds the TriSetup in
+// shared memory (the serial part), then the warp stores it to the `large`
+// queue and either samples the whole window (<= FA_SMALL_PX pixels, depth
+// pass only) or writes the descriptors of its 16x8 tiles (negative ids).
+// The visibility pass finds every stored setup through the queue.
+template <bool WRITE_DEPTH>
+__global__ void __launch_bounds__(256) k_raster_clipped(const double4* __restrict__ clip, const int* __restrict__ tris,
+                                                        int W, int H, int cull, const int* __restrict__ clip_list,
+                                                        unsigned long long* __restrict__ depth,
+                                                        TriSetup* __restrict__ large, int max_large,
+                                                        int2* __restrict__ tiles, int max_tiles,
+                                                        fa_dstat* __restrict__ st) {
+    __shared__ TriSetup sm[8];
+    const int warp = threadIdx.x >> 5, lane = lane_id();
+    const int nwarps = gridDim.x * 8;
+    const int n = st->n_clip;
+    for (int w = blockIdx.x * 8 + warp; w < n; w += nwarps) {
+        const int t = clip_list[w];
+        int r = 0;
+        __syncwarp();
+        if (lane == 0) r = tri_setup(clip, tris, t, W, H, cull != 0, sm[warp]);
+        r = __shfl_sync(0xffffffffu, r, 0);
+        __syncwarp();
+        if (r < 0) {
+            if (lane == 0) atomicOr(&st->flags, FA_DFLAG_POLY_OVERFLOW);
             continue;
         }
-        TriSetup s;
-        int r;
-        if (r3 == 1) {
-            setup3_to_generic(f, t, s);
-            r = 1;
-        } else {
-            r = tri_setup(clip, tris, t, W, H, cull != 0, s);
-        }
-        if (r < 0) { atomicOr(&st->flags, FA_DFLAG_POLY_OVERFLOW); continue; }
         if (r == 0) continue;
-        int bw = s.max_x - s.min_x + 1, bh = s.max_y - s.min_y + 1;
+        const TriSetup& s = sm[warp];
+        int slot = 0;
+        if (lane == 0) slot = atomicAdd(&st->n_large, 1);
+        slot = __shfl_sync(0xffffffffu, slot, 0);
+        if (slot >= max_large) {
+            if (lane == 0) atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW);
+            continue;
+        }
+        {
+            const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&s);
+            unsigned long long* dst = reinterpret_cast<unsigned long long*>(large + slot);
+            for (int i = lane; i < (int)(sizeof(TriSetup) / 8); i += 32) dst[i] = src[i];
+        }
+        const int bw = s.max_x - s.min_x + 1, bh = s.max_y - s.min_y + 1;
         if (bw * bh <= FA_SMALL_PX) {
-            // clipped small polygon (generic setup)
-            bool covered = false;
-            for (int iy = s.min_y; iy <= s.max_y; iy++) {
-                double py = (double)iy + 0.5;
-                for (int ix = s.min_x; ix <= s.max_x; ix++) {
-                    double px = (double)ix + 0.5;
+            if (WRITE_DEPTH) {
+                for (int k = lane; k < bw * bh; k += 32) {
+                    int dy = k / bw;
+                    int iy = s.min_y + dy, ix = s.min_x + (k - dy * bw);
+                    double px = (double)ix + 0.5, py = (double)iy + 0.5;
                     if (!sample_inside(s, px, py)) continue;
-                    covered = true;
-                    if (WRITE_DEPTH) {
-                        unsigned long long key = f64_key(sample_depth(s, px, py));
-                        unsigned long long* d = depth + (long long)iy * W + ix;
-                        if (key < *d) atomicMin(d, key);
-                    } else {
-                        break;
-                    }
+                    unsigned long long key = f64_key(sample_depth(s, px, py));
+                    unsigned long long* d = depth + (long long)iy * W + ix;
+                    if (key < *d) atomicMin(d, key);
                 }
-                if (!WRITE_DEPTH && covered) break;
-            }
-            if (covered) {
-                int slot = active_append1(&st->n_small);
-                small_list[slot] = t;
             }
         } else {
-            int slot = active_append1(&st->n_large);
-            if (slot >= max_large) { atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW); continue; }
-            large[slot] = s;
-            int tx = (bw + TILE_W - 1) / TILE_W, ty = (bh + TILE_H - 1) / TILE_H;
-            int nt = tx * ty;
-            int base = atomicAdd(&st->n_tiles, nt);
+            const int nt = ((bw + TILE_W - 1) / TILE_W) * ((bh + TILE_H - 1) / TILE_H);
+            int base = 0;
+            if (lane == 0) base = atomicAdd(&st->n_tiles, nt);
+            base = __shfl_sync(0xffffffffu, base, 0);
             // on overflow write the part that fits (no unwritten records below
             // capacity) and flag the frame; the host grows the queue and reruns
-            int end = base + nt;
-            if (end > max_tiles) { atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW); end = max_tiles; }
-            // generic (clipped) setups are referenced by negative ids
-            for (int k = base; k < end; k++) tiles[k] = make_int2(-slot - 1, k - base);
+            if (base + nt > max_tiles && lane == 0) atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW);
+            for (int k = lane; k < nt; k += 32)
+                if (base + k < max_tiles) tiles[base + k] = make_int2(-slot - 1, k);
         }
     }
 }
@@ -407,14 +479,11 @@ __global__ void __launch_bounds__(COOP_WARPS * 32) k_small_coop(const SmallRec* 
 }
 
 // ---- pass 2 small: one thread per covering triangle -----------------------
-__global__ void __launch_bounds__(256) k_raster_vis_small(const double4* __restrict__ clip, const int* __restrict__ tris,
-                                                          const int* __restrict__ small_list,
-                                                          const SmallRec* __restrict__ small_rec, int W, int H,
-                                                          int cull, const unsigned long long* __restrict__ depth,
+__global__ void __launch_bounds__(256) k_raster_vis_small(const SmallRec* __restrict__ small_rec, int W,
+                                                          const unsigned long long* __restrict__ depth,
                                                           unsigned char* __restrict__ flags,
                                                           const fa_dstat* __restrict__ st) {
     int n3 = st->n_small3;
-    int n = st->n_small;
     int stride = gridDim.x * blockDim.x;
     // stored records, one thread each: stop at the first passing sample;
     // gather up to 4 covered samples, then issue their depth loads together
@@ -444,24 +513,6 @@ __global__ void __launch_bounds__(256) k_raster_vis_small(const double4* __restr
             }
         }
         for (int q = 0; q < nq && !vis; q++) vis = depth_passes(zq[q], key_f64(*aq[q]));
-        if (vis) flags[t] = 1;
-    }
-    // generic (clipped) small triangles: full setup again (rare)
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        int t = small_list[i];
-        bool vis = false;
-        TriSetup s;
-        if (tri_setup(clip, tris, t, W, H, cull != 0, s) <= 0) continue;
-        for (int iy = s.min_y; iy <= s.max_y && !vis; iy++) {
-            double py = (double)iy + 0.5;
-            for (int ix = s.min_x; ix <= s.max_x; ix++) {
-                double px = (double)ix + 0.5;
-                if (!sample_inside(s, px, py)) continue;
-                double z = sample_depth(s, px, py);
-                double stored = key_f64(depth[(long long)iy * W + ix]);
-                if (depth_passes(z, stored)) { vis = true; break; }
-            }
-        }
         if (vis) flags[t] = 1;
     }
 }
@@ -535,14 +586,26 @@ __global__ void __launch_bounds__(256) k_raster_vis_tiles(const SmallRec* __rest
         __syncwarp();
         load_setup_warp(large + rec.x, &sm[warp]);
         const TriSetup& s = sm[warp];
-        int bw = s.max_x - s.min_x + 1;
+        int bw = s.max_x - s.min_x + 1, bh = s.max_y - s.min_y + 1;
+        bool vis = false;
+        if (bw * bh <= FA_SMALL_PX) {
+            // small clipped polygon (no tiles): the warp covers its window in phase 0
+            for (int k = lane; k < bw * bh && !vis; k += 32) {
+                int dy = k / bw;
+                int iy = s.min_y + dy, ix = s.min_x + (k - dy * bw);
+                double px = (double)ix + 0.5, py = (double)iy + 0.5;
+                if (!sample_inside(s, px, py)) continue;
+                vis = depth_passes(sample_depth(s, px, py), key_f64(depth[(long long)iy * W + ix]));
+            }
+            if (__any_sync(0xffffffffu, vis) && lane == 0) flags[t] = 1;
+            continue;
+        }
         int tx = (bw + TILE_W - 1) / TILE_W;
         int centre = ((s.max_y - s.min_y + 1) / 2 / TILE_H) * tx + (bw / 2) / TILE_W;
         if (phase == 0) rec.y = centre;
         else if (rec.y == centre) continue;
         int x = s.min_x + (rec.y % tx) * TILE_W + (lane & 15);
         int y0 = s.min_y + (rec.y / tx) * TILE_H + (lane >> 4);
-        bool vis = false;
         if (x <= s.max_x) {
             double px = (double)x + 0.5;
             for (int k = 0; k < TILE_H / 2; k++) {
@@ -560,27 +623,29 @@ __global__ void __launch_bounds__(256) k_raster_vis_tiles(const SmallRec* __rest
 }
 
 // ---- host launchers -------------------------------------------------------
-void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* clip, int* vmin,
-                          unsigned long long* depth, long long npx, unsigned char* flags, int T,
+void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* clip, double4* scr, int W, int H,
+                          int* vmin, unsigned long long* depth, long long npx, unsigned char* flags, int T,
                           cudaStream_t s) {
     long long work = V;
     if (depth && npx / 2 > work) work = npx / 2;
     int nflag32 = flags ? (T + 3) / 4 : 0;
     if (nflag32 > work) work = nflag32;
     k_frame_init<<<fa_grid(work, 256, FA_NUM_SMS * 8), 256, 0, s>>>(
-        pos, V, vp, clip, vmin, depth, npx, reinterpret_cast<unsigned int*>(flags), nflag32);
+        pos, V, vp, clip, scr, W, H, vmin, depth, npx, reinterpret_cast<unsigned int*>(flags), nflag32);
 }
 
-void fa_launch_raster_setup(bool write_depth, const double4* clip, const int* tris, int T, int W, int H, int cull,
-                            unsigned long long* depth, int* small_list, SmallRec* small_rec, TriSetup* large,
-                            int max_large, int2* tiles, int max_tiles, fa_dstat* st, cudaStream_t s) {
-    int grid = fa_grid(T, 256, FA_NUM_SMS * 16);
+void fa_launch_raster_setup(bool write_depth, const double4* clip, const double4* scr, const int* tris, int T, int W,
+                            int H, int cull, unsigned long long* depth, SmallRec* small_rec,
+                            int* clip_list, TriSetup* large, int max_large, int2* tiles, int max_tiles, fa_dstat* st,
+                            cudaStream_t s) {
+    k_raster_setup<<<fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s>>>(scr, tris, T, W, H, cull, small_rec, clip_list,
+                                                                    tiles, max_tiles, st);
     if (write_depth)
-        k_raster_setup<true><<<grid, 256, 0, s>>>(clip, tris, T, W, H, cull, depth, small_list, small_rec, large, max_large,
-                                                  tiles, max_tiles, st);
+        k_raster_clipped<true><<<FA_NUM_SMS * 2, 256, 0, s>>>(clip, tris, W, H, cull, clip_list, depth, large,
+                                                              max_large, tiles, max_tiles, st);
     else
-        k_raster_setup<false><<<grid, 256, 0, s>>>(clip, tris, T, W, H, cull, depth, small_list, small_rec, large, max_large,
-                                                   tiles, max_tiles, st);
+        k_raster_clipped<false><<<FA_NUM_SMS * 2, 256, 0, s>>>(clip, tris, W, H, cull, clip_list, depth, large,
+                                                               max_large, tiles, max_tiles, st);
     // depth pass: sample the recorded small triangles (warp-cooperative)
     if (write_depth) fa_launch_small_coop(false, small_rec, T, W, depth, nullptr, st, s);
 }
@@ -590,13 +655,10 @@ void fa_launch_raster_depth_tiles(const SmallRec* recs, const TriSetup* large, c
     k_raster_depth_tiles<<<FA_NUM_SMS * 8, 256, 0, s>>>(recs, large, tiles, W, depth, st, max_tiles);
 }
 
-void fa_launch_raster_vis(const double4* clip, const int* tris, const int* small_list, const SmallRec* small_rec,
-                          const TriSetup* large,
-                          const int2* tiles, int max_tiles, int max_large, int T, int W, int H, int cull,
-                          const unsigned long long* depth, unsigned char* flags, const fa_dstat* st,
-                          cudaStream_t s) {
-    k_raster_vis_small<<<fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s>>>(clip, tris, small_list, small_rec, W, H, cull,
-                                                                       depth, flags, st);
+void fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const int2* tiles, int max_tiles,
+                          int max_large, int T, int W, const unsigned long long* depth, unsigned char* flags,
+                          const fa_dstat* st, cudaStream_t s) {
+    k_raster_vis_small<<<fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s>>>(small_rec, W, depth, flags, st);
     k_raster_vis_tiles<<<FA_NUM_SMS * 8, 256, 0, s>>>(small_rec, T, large, tiles, W, depth, flags, st, max_tiles,
                                                       max_large, 0);
     k_raster_vis_tiles<<<FA_NUM_SMS * 8, 256, 0, s>>>(small_rec, T, large, tiles, W, depth, flags, st, max_tiles,

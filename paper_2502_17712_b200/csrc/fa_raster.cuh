@@ -249,6 +249,106 @@ struct Setup3 {
     int min_x, max_x, min_y, max_y;
 };
 
+// ---- per-vertex screen record (written once per vertex by k_frame_init) ----
+// {screen x, screen y, NDC z, outcode bits}: the divisions of the unclipped
+// fast path depend only on the vertex, so they are done V times instead of
+// 3T times (bit-identical: same operations on the same inputs).
+// Outcode: bit 0 = !(w - 1e-9 > 0); bits 1-6 = !(d_p >= 0) and bits 7-12 =
+// (d_p < 0) for the planes L,R,B,T,N,F (d = w+x, w-x, w+y, w-y, w+z, w-z),
+// both kept so NaN coordinates classify exactly as the float tests do.
+#define FA_OC_BEHIND 1u
+#define FA_OC_NOTGE(p) (2u << (p))
+#define FA_OC_LT(p) (0x80u << (p))
+
+__device__ __forceinline__ double4 vertex_screen(double4 c, int W, int H) {
+    unsigned code = __dsub_rn(c.w, FA_W_EPSILON) > 0 ? 0u : FA_OC_BEHIND;
+    double d[6] = {__dadd_rn(c.w, c.x), __dsub_rn(c.w, c.x), __dadd_rn(c.w, c.y),
+                   __dsub_rn(c.w, c.y), __dadd_rn(c.w, c.z), __dsub_rn(c.w, c.z)};
+#pragma unroll
+    for (int p = 0; p < 6; p++) {
+        if (!(d[p] >= 0)) code |= FA_OC_NOTGE(p);
+        if (d[p] < 0) code |= FA_OC_LT(p);
+    }
+    double4 o;
+    if (code == 0) {
+        o.x = __dmul_rn(__dmul_rn(__dadd_rn(__ddiv_rn(c.x, c.w), 1.0), 0.5), (double)W);
+        o.y = __dmul_rn(__dmul_rn(__dadd_rn(__ddiv_rn(c.y, c.w), 1.0), 0.5), (double)H);
+        o.z = __ddiv_rn(c.z, c.w);
+    } else {
+        o.x = o.y = o.z = 0.0;  // only read by the clipping path, which uses clip space
+    }
+    o.w = __longlong_as_double((long long)code);
+    return o;
+}
+
+// 1 = Setup3 filled, 0 = no samples, 2 = needs the generic (clipping) path.
+// Same decisions as tri_setup3 below, from the per-vertex screen records.
+__device__ __forceinline__ int tri_setup3s(const double4* __restrict__ scr, int ia, int ib, int ic, int W, int H,
+                                           bool cull, Setup3& s) {
+    double4 v0 = ldg4(scr + ia), v1 = ldg4(scr + ib), v2 = ldg4(scr + ic);
+    unsigned c0 = (unsigned)__double_as_longlong(v0.w), c1 = (unsigned)__double_as_longlong(v1.w),
+             c2 = (unsigned)__double_as_longlong(v2.w);
+    unsigned any = c0 | c1 | c2;
+    if (any) {
+        unsigned all = c0 & c1 & c2;
+        if (all & FA_OC_BEHIND) return 0;  // no vertex in front (charts.py:163-165)
+        if (!(any & FA_OC_BEHIND)) {
+            // exact trivial reject: first plane not passed by all vertices
+#pragma unroll
+            for (int p = 0; p < 6; p++) {
+                if (!(any & FA_OC_NOTGE(p))) continue;
+                if (all & FA_OC_LT(p)) return 0;
+                break;
+            }
+        }
+        return 2;
+    }
+    double x0 = v0.x, y0 = v0.y, z0 = v0.z;
+    double x1 = v1.x, y1 = v1.y, z1 = v1.z;
+    double x2 = v2.x, y2 = v2.y, z2 = v2.z;
+    double A = __dadd_rn(__fma_rn(y0, x2, __fma_rn(y2, x1, __fma_rn(y1, x0, 0.0))), 0.0);
+    double B = __dadd_rn(__fma_rn(x0, y2, __fma_rn(x2, y1, __fma_rn(x1, y0, 0.0))), 0.0);
+    double area2 = __dsub_rn(A, B);
+    if (area2 == 0.0) return 0;
+    if (area2 < 0.0) {
+        if (cull) return 0;
+        double t;
+        t = x0; x0 = x2; x2 = t;
+        t = y0; y0 = y2; y2 = t;
+        t = z0; z0 = z2; z2 = t;
+    }
+    double mnx = x0, mxx = x0, mny = y0, mxy = y0;
+    mnx = x1 < mnx ? x1 : mnx; mxx = x1 > mxx ? x1 : mxx; mny = y1 < mny ? y1 : mny; mxy = y1 > mxy ? y1 : mxy;
+    mnx = x2 < mnx ? x2 : mnx; mxx = x2 > mxx ? x2 : mxx; mny = y2 < mny ? y2 : mny; mxy = y2 > mxy ? y2 : mxy;
+    long long fx = (long long)floor(__dsub_rn(mnx, 0.5)), cx = (long long)ceil(mxx);
+    long long fy = (long long)floor(__dsub_rn(mny, 0.5)), cy = (long long)ceil(mxy);
+    s.min_x = fx > 0 ? (int)fx : 0;
+    s.max_x = cx < W - 1 ? (int)cx : W - 1;
+    s.min_y = fy > 0 ? (int)fy : 0;
+    s.max_y = cy < H - 1 ? (int)cy : H - 1;
+    if (s.min_x > s.max_x || s.min_y > s.max_y) return 0;
+    s.ax0 = x0; s.ay0 = y0; s.dx0 = __dsub_rn(x1, x0); s.dy0 = __dsub_rn(y1, y0);
+    s.ax1 = x1; s.ay1 = y1; s.dx1 = __dsub_rn(x2, x1); s.dy1 = __dsub_rn(y2, y1);
+    s.ax2 = x2; s.ay2 = y2; s.dx2 = __dsub_rn(x0, x2); s.dy2 = __dsub_rn(y0, y2);
+    s.incl = ((s.dy0 > 0 || (s.dy0 == 0 && s.dx0 < 0)) ? 1 : 0) | ((s.dy1 > 0 || (s.dy1 == 0 && s.dx1 < 0)) ? 2 : 0) |
+             ((s.dy2 > 0 || (s.dy2 == 0 && s.dx2 < 0)) ? 4 : 0);
+    double a1x = s.dx0, a1y = s.dy0, a1z = __dsub_rn(z1, z0);
+    double a2x = __dsub_rn(x2, x0), a2y = __dsub_rn(y2, y0), a2z = __dsub_rn(z2, z0);
+    double det = __dsub_rn(__dmul_rn(a1x, a2y), __dmul_rn(a2x, a1y));
+    s.p0x = x0; s.p0y = y0; s.p0z = z0;
+    if (fabs(det) > 1e-12) {
+        s.gx = __ddiv_rn(__dsub_rn(__dmul_rn(a1z, a2y), __dmul_rn(a2z, a1y)), det);
+        s.gy = __ddiv_rn(__dsub_rn(__dmul_rn(a2z, a1x), __dmul_rn(a1z, a2x)), det);
+        s.use_plane = 1;
+        s.zmean = 0.0;
+    } else {
+        s.use_plane = 0;
+        s.gx = s.gy = 0.0;
+        s.zmean = __ddiv_rn(__dadd_rn(__dadd_rn(__dadd_rn(-0.0, z0), z1), z2), 3.0);
+    }
+    return 1;
+}
+
 // 1 = Setup3 filled, 0 = no samples, 2 = needs the generic (clipping) path
 __device__ __forceinline__ int tri_setup3(const double4* __restrict__ clip, const int* __restrict__ tris, int t,
                                           int W, int H, bool cull, Setup3& s) {
