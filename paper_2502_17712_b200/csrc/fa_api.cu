@@ -117,6 +117,11 @@ void fa_destroy(fa_ctx* c) {
                       &c->placements, &c->uv, &c->vp_dev, &c->blocks, &c->dstat, &c->aux, &c->in_tw, &c->in_th,
                       &c->in_cid, &c->in_mt, &c->scr, &c->clip_list};
     for (fa_buf* b : bufs) free_buf(*b);
+    for (cudaEvent_t e : c->fj)
+        if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->ev)
+        if (e) cudaEventDestroy(e);
+    if (c->side) cudaStreamDestroy(c->side);
     if (c->hstat) cudaFreeHost(c->hstat);
     if (c->hvp) cudaFreeHost(c->hvp);
     delete c;
@@ -265,13 +270,19 @@ static int launch_depth(fa_ctx* ctx, int W, int H, int cull, unsigned char* flag
     int T = (int)ctx->T, V = (int)ctx->V;
     fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), P<double4>(ctx->scr), W, H,
                          P<int>(ctx->vmin), P<unsigned long long>(ctx->depth_keys), (long long)W * H, flags_out, T, s);
-    fa_launch_raster_setup(true, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, W, H, cull,
-                           P<unsigned long long>(ctx->depth_keys), P<SmallRec>(ctx->small_rec),
-                           P<int>(ctx->clip_list), P<TriSetup>(ctx->large), ctx->max_large, P<int2>(ctx->tiles),
-                           ctx->max_tiles, P<fa_dstat>(ctx->dstat), s);
-    fa_launch_raster_depth_tiles(P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large), P<int2>(ctx->tiles),
-                                 ctx->max_tiles, W, P<unsigned long long>(ctx->depth_keys), P<fa_dstat>(ctx->dstat), s);
-    nl += 5;
+    nl += 1 + fa_launch_depth_pass(true, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, W, H, cull,
+                                   P<unsigned long long>(ctx->depth_keys), P<SmallRec>(ctx->small_rec),
+                                   P<int>(ctx->clip_list), P<TriSetup>(ctx->large), ctx->max_large,
+                                   P<int2>(ctx->tiles), ctx->max_tiles, P<fa_dstat>(ctx->dstat), s, nullptr, nullptr,
+                                   nullptr);
+    return FA_OK;
+}
+
+// side stream and fork/join events (created on first use)
+static int ensure_side(fa_ctx* ctx) {
+    if (!ctx->side) CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : ctx->fj)
+        if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     return FA_OK;
 }
 
@@ -335,13 +346,13 @@ int fa_mark_visible(fa_ctx* ctx, const double* vp_host, const double* depth, int
         fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), P<double4>(ctx->scr), width,
                              height, nullptr, nullptr, 0, P<unsigned char>(ctx->flags), T, s);
         fa_launch_encode_depth(depth, P<unsigned long long>(ctx->depth_keys), (long long)width * height, s);
-        fa_launch_raster_setup(false, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, width, height,
-                               backface_cull, nullptr, P<SmallRec>(ctx->small_rec),
-                               P<int>(ctx->clip_list), P<TriSetup>(ctx->large), ctx->max_large, P<int2>(ctx->tiles),
-                               ctx->max_tiles, P<fa_dstat>(ctx->dstat), s);
+        fa_launch_depth_pass(false, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, width, height,
+                             backface_cull, nullptr, P<SmallRec>(ctx->small_rec), P<int>(ctx->clip_list),
+                             P<TriSetup>(ctx->large), ctx->max_large, P<int2>(ctx->tiles), ctx->max_tiles,
+                             P<fa_dstat>(ctx->dstat), s, nullptr, nullptr, nullptr);
         fa_launch_raster_vis(P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large), P<int2>(ctx->tiles),
                              ctx->max_tiles, ctx->max_large, T, width, P<unsigned long long>(ctx->depth_keys),
-                             P<unsigned char>(ctx->flags), P<fa_dstat>(ctx->dstat), s);
+                             P<unsigned char>(ctx->flags), P<fa_dstat>(ctx->dstat), s, nullptr, nullptr, nullptr);
         CKL();
         r = read_stat(ctx, s);
         if (r) return r;
@@ -658,18 +669,18 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
                          P<int>(ctx->vmin), P<unsigned long long>(ctx->depth_keys), (long long)W * H, flags, T, s);
     nl += 1;
     mark();  // 1: project + clears
-    fa_launch_raster_setup(true, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, W, H, p->backface_cull,
-                           P<unsigned long long>(ctx->depth_keys), P<SmallRec>(ctx->small_rec),
-                           P<int>(ctx->clip_list), P<TriSetup>(ctx->large), ctx->max_large, P<int2>(ctx->tiles),
-                           ctx->max_tiles, st, s);
-    fa_launch_raster_depth_tiles(P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large), P<int2>(ctx->tiles),
-                                 ctx->max_tiles, W, P<unsigned long long>(ctx->depth_keys), st, s);
+    int r = ensure_side(ctx);
+    if (r) return r;
+    nl += fa_launch_depth_pass(true, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, W, H,
+                               p->backface_cull, P<unsigned long long>(ctx->depth_keys), P<SmallRec>(ctx->small_rec),
+                               P<int>(ctx->clip_list), P<TriSetup>(ctx->large), ctx->max_large, P<int2>(ctx->tiles),
+                               ctx->max_tiles, st, s, ctx->side, ctx->fj[0], ctx->fj[1]);
     fa_launch_count_finite(P<unsigned long long>(ctx->depth_keys), (long long)W * H, st, s);
-    nl += 5;
+    nl += 1;
     mark();  // 2: depth pass
-    fa_launch_raster_vis(P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large), P<int2>(ctx->tiles), ctx->max_tiles,
-                         ctx->max_large, T, W, P<unsigned long long>(ctx->depth_keys), flags, st, s);
-    nl += 3;  // small records, centre tiles (+ small clipped windows), remaining tiles
+    nl += fa_launch_raster_vis(P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large), P<int2>(ctx->tiles),
+                               ctx->max_tiles, ctx->max_large, T, W, P<unsigned long long>(ctx->depth_keys), flags, st,
+                               s, ctx->side, ctx->fj[2], ctx->fj[3]);
     mark();  // 3: visibility pass
     fa_launch_compact_visible(flags, T, P<int>(ctx->blocks), P<int>(ctx->vis_list), P<int>(ctx->label), st, s);
     nl += 2;

@@ -63,6 +63,10 @@ struct fa_ctx {
     static const int kMaxStages = 12;
     cudaEvent_t ev[kMaxStages + 1] = {};
     int n_stage_marks = 0;
+
+    // side stream + fork/join events for the independent raster branches
+    cudaStream_t side = nullptr;
+    cudaEvent_t fj[4] = {};
 };
 
 // growth helper: ensures buf has >= bytes; returns false on allocation failure
@@ -72,15 +76,16 @@ bool fa_ensure(fa_ctx* ctx, fa_buf& b, size_t bytes);
 void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* clip, double4* scr, int W, int H,
                           int* vmin,
                           unsigned long long* depth, long long npx, unsigned char* flags, int T, cudaStream_t s);
-void fa_launch_raster_setup(bool write_depth, const double4* clip, const double4* scr, const int* tris, int T, int W,
-                            int H, int cull, unsigned long long* depth, SmallRec* small_rec,
-                            int* clip_list, TriSetup* large, int max_large, int2* tiles, int max_tiles, fa_dstat* st,
-                            cudaStream_t s);
-void fa_launch_raster_depth_tiles(const SmallRec* recs, const TriSetup* large, const int2* tiles, int max_tiles, int W,
-                                  unsigned long long* depth, fa_dstat* st, cudaStream_t s);
-void fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const int2* tiles, int max_tiles,
-                          int max_large, int T, int W, const unsigned long long* depth, unsigned char* flags,
-                          const fa_dstat* st, cudaStream_t s);
+// side == nullptr: everything on s; otherwise fork/join through the events.
+// Both return the number of kernels launched.
+int fa_launch_depth_pass(bool write_depth, const double4* clip, const double4* scr, const int* tris, int T, int W,
+                         int H, int cull, unsigned long long* depth, SmallRec* small_rec, int* clip_list,
+                         TriSetup* large, int max_large, int2* tiles, int max_tiles, fa_dstat* st, cudaStream_t s,
+                         cudaStream_t side, cudaEvent_t ev_fork, cudaEvent_t ev_join);
+int fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const int2* tiles, int max_tiles,
+                         int max_large, int T, int W, const unsigned long long* depth, unsigned char* flags,
+                         const fa_dstat* st, cudaStream_t s, cudaStream_t side, cudaEvent_t ev_fork,
+                         cudaEvent_t ev_join);
 void fa_launch_decode_depth(const unsigned long long* keys, double* out, long long n, cudaStream_t s);
 void fa_launch_count_finite(const unsigned long long* depth, long long npx, fa_dstat* st, cudaStream_t s);
 void fa_launch_small_coop(bool vis, const SmallRec* recs, int T, int W, unsigned long long* depth,

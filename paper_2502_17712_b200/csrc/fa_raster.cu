@@ -634,35 +634,53 @@ void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* c
         pos, V, vp, clip, scr, W, H, vmin, depth, npx, reinterpret_cast<unsigned int*>(flags), nflag32);
 }
 
-void fa_launch_raster_setup(bool write_depth, const double4* clip, const double4* scr, const int* tris, int T, int W,
-                            int H, int cull, unsigned long long* depth, SmallRec* small_rec,
-                            int* clip_list, TriSetup* large, int max_large, int2* tiles, int max_tiles, fa_dstat* st,
-                            cudaStream_t s) {
+// fork `side` off `s` (side waits for everything issued on s so far)
+static void fork_to(cudaStream_t s, cudaStream_t side, cudaEvent_t ev) {
+    cudaEventRecord(ev, s);
+    cudaStreamWaitEvent(side, ev, 0);
+}
+
+// Depth pass (write_depth) or work-list build (standalone mark_visible).
+// With a side stream: setup, then {small records on s} || {clipped polygons
+// -> large tiles on side}, joined back into s.  Both branches only lower
+// depth keys with atomicMin, so their order does not matter.
+int fa_launch_depth_pass(bool write_depth, const double4* clip, const double4* scr, const int* tris, int T, int W,
+                         int H, int cull, unsigned long long* depth, SmallRec* small_rec, int* clip_list,
+                         TriSetup* large, int max_large, int2* tiles, int max_tiles, fa_dstat* st, cudaStream_t s,
+                         cudaStream_t side, cudaEvent_t ev_fork, cudaEvent_t ev_join) {
     k_raster_setup<<<fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s>>>(scr, tris, T, W, H, cull, small_rec, clip_list,
                                                                     tiles, max_tiles, st);
-    if (write_depth)
-        k_raster_clipped<true><<<FA_NUM_SMS * 2, 256, 0, s>>>(clip, tris, W, H, cull, clip_list, depth, large,
+    cudaStream_t b = side ? side : s;
+    if (side) fork_to(s, side, ev_fork);
+    if (write_depth) {
+        k_raster_clipped<true><<<FA_NUM_SMS * 2, 256, 0, b>>>(clip, tris, W, H, cull, clip_list, depth, large,
                                                               max_large, tiles, max_tiles, st);
-    else
-        k_raster_clipped<false><<<FA_NUM_SMS * 2, 256, 0, s>>>(clip, tris, W, H, cull, clip_list, depth, large,
+        k_raster_depth_tiles<<<FA_NUM_SMS * 8, 256, 0, b>>>(small_rec, large, tiles, W, depth, st, max_tiles);
+        // small unclipped triangles (warp-cooperative)
+        fa_launch_small_coop(false, small_rec, T, W, depth, nullptr, st, s);
+    } else {
+        k_raster_clipped<false><<<FA_NUM_SMS * 2, 256, 0, b>>>(clip, tris, W, H, cull, clip_list, depth, large,
                                                                max_large, tiles, max_tiles, st);
-    // depth pass: sample the recorded small triangles (warp-cooperative)
-    if (write_depth) fa_launch_small_coop(false, small_rec, T, W, depth, nullptr, st, s);
+    }
+    if (side) fork_to(side, s, ev_join);
+    return write_depth ? 4 : 2;
 }
 
-void fa_launch_raster_depth_tiles(const SmallRec* recs, const TriSetup* large, const int2* tiles, int max_tiles, int W,
-                                  unsigned long long* depth, fa_dstat* st, cudaStream_t s) {
-    k_raster_depth_tiles<<<FA_NUM_SMS * 8, 256, 0, s>>>(recs, large, tiles, W, depth, st, max_tiles);
-}
-
-void fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const int2* tiles, int max_tiles,
-                          int max_large, int T, int W, const unsigned long long* depth, unsigned char* flags,
-                          const fa_dstat* st, cudaStream_t s) {
-    k_raster_vis_small<<<fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s>>>(small_rec, W, depth, flags, st);
-    k_raster_vis_tiles<<<FA_NUM_SMS * 8, 256, 0, s>>>(small_rec, T, large, tiles, W, depth, flags, st, max_tiles,
+// Visibility pass: small records on s || large tiles (centre tile first,
+// then the rest of the still-invisible ones) on side.
+int fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const int2* tiles, int max_tiles,
+                         int max_large, int T, int W, const unsigned long long* depth, unsigned char* flags,
+                         const fa_dstat* st, cudaStream_t s, cudaStream_t side, cudaEvent_t ev_fork,
+                         cudaEvent_t ev_join) {
+    cudaStream_t b = side ? side : s;
+    if (side) fork_to(s, side, ev_fork);
+    k_raster_vis_tiles<<<FA_NUM_SMS * 8, 256, 0, b>>>(small_rec, T, large, tiles, W, depth, flags, st, max_tiles,
                                                       max_large, 0);
-    k_raster_vis_tiles<<<FA_NUM_SMS * 8, 256, 0, s>>>(small_rec, T, large, tiles, W, depth, flags, st, max_tiles,
+    k_raster_vis_tiles<<<FA_NUM_SMS * 8, 256, 0, b>>>(small_rec, T, large, tiles, W, depth, flags, st, max_tiles,
                                                       max_large, 1);
+    k_raster_vis_small<<<fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s>>>(small_rec, W, depth, flags, st);
+    if (side) fork_to(side, s, ev_join);
+    return 3;
 }
 
 void fa_launch_small_coop(bool vis, const SmallRec* recs, int T, int W, unsigned long long* depth,
