@@ -206,6 +206,16 @@ int fa_frame_finish(fa_ctx *ctx, fa_frame_result *out, void *stream);
 int fa_frame(fa_ctx *ctx, const double *vp_host, const fa_frame_params *params, fa_frame_result *out,
              void *stream);
 
+/* Enqueue (asynchronously, on `stream`) the device->host copies of a
+ * finished frame's results into caller buffers (pinned for overlap); any
+ * pointer may be NULL to skip that output.  Sizes come from `res`:
+ * chart_of_triangle T int32, visible n_visible int32, uv n_visible x 6
+ * (float32, or float64 when the frame ran with uv_f64), placements n_charts
+ * x 8 int64.  The caller synchronises `stream` before reading.  Replaces the
+ * per-array `.cpu()` reads of SceneResult (reference cli.py:404-406). */
+int fa_frame_download(fa_ctx *ctx, const fa_frame_result *res, int32_t *chart_of_triangle, int32_t *visible,
+                      void *uv, int64_t *placements, void *stream);
+
 /* Number of kernels the last fa_frame_launch enqueued (benchmark accounting). */
 int fa_last_launch_count(fa_ctx *ctx);
 

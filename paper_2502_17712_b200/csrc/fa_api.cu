@@ -883,6 +883,22 @@ int fa_frame(fa_ctx* ctx, const double* vp_host, const fa_frame_params* p, fa_fr
     return set_err(FA_INTERNAL_ERROR, "frame kept overflowing its work queues");
 }
 
+int fa_frame_download(fa_ctx* ctx, const fa_frame_result* res, int32_t* chart_of_triangle, int32_t* visible,
+                      void* uv, int64_t* placements, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || !res) return set_err(FA_VALUE_ERROR, "bad arguments");
+    if (res->status != FA_OK) return set_err(FA_VALUE_ERROR, "frame result has no outputs (status %d)", res->status);
+    CK(cudaSetDevice(ctx->device));
+    size_t nv = (size_t)res->n_visible, C = (size_t)res->n_charts;
+    size_t uv_elem = ctx->last_params.uv_f64 ? 8 : 4;
+    if (chart_of_triangle && ctx->T)
+        CK(cudaMemcpyAsync(chart_of_triangle, res->chart_of_triangle, (size_t)ctx->T * 4, cudaMemcpyDeviceToHost, s));
+    if (visible && nv) CK(cudaMemcpyAsync(visible, res->visible, nv * 4, cudaMemcpyDeviceToHost, s));
+    if (uv && nv) CK(cudaMemcpyAsync(uv, res->uv, nv * 6 * uv_elem, cudaMemcpyDeviceToHost, s));
+    if (placements && C) CK(cudaMemcpyAsync(placements, res->placements, C * 64, cudaMemcpyDeviceToHost, s));
+    return FA_OK;
+}
+
 int fa_last_launch_count(fa_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
 
 static const char* kStageNames[] = {"project+clear", "depth pass",   "visibility pass", "visible compaction",

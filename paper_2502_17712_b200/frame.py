@@ -182,6 +182,10 @@ class FrameEngine:
                                self.ctx.torch_device, owner=self)
         raise RuntimeError("frame work queues kept overflowing")
 
+    def run_views(self, views, settings: FrameSettings | None = None, stream=None) -> list:
+        """Sequential convenience: one cloned FrameOutput per view."""
+        return [self.run(v, settings, stream).clone() for v in views]
+
     def launch_count(self) -> int:
         return int(self.ctx.L.fa_last_launch_count(self.ctx.h))
 
@@ -190,3 +194,160 @@ class FrameEngine:
         buf = (ctypes.c_float * 16)()
         n = self.ctx.L.fa_stage_times(self.ctx.h, buf, 16, self._stream)
         return {self.ctx.L.fa_stage_name(i).decode(): float(buf[i]) for i in range(n)}
+
+
+class HostFrame:
+    """One pipelined view's results in pinned host memory.
+
+    The arrays are views into a pipeline slot and are overwritten once the
+    slot is reused (`depth` views later): `on_frame` consumers that keep them
+    must copy.  `error` holds the reference exception (NothingVisible,
+    PackFailure, ...) when the frame failed; the arrays are then None."""
+
+    __slots__ = ("index", "status", "error", "n_visible", "n_charts", "scale", "screen_fragments",
+                 "texels_allocated", "chart_of_triangle", "visible", "uv", "placements")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.status = 0
+        self.error = None
+        self.n_visible = self.n_charts = 0
+        self.scale = None
+        self.screen_fragments = self.texels_allocated = 0
+        self.chart_of_triangle = self.visible = self.uv = self.placements = None
+
+    def d2h_bytes(self) -> int:
+        return sum(a.nbytes for a in (self.chart_of_triangle, self.visible, self.uv, self.placements) if a is not None)
+
+
+class FramePipeline:
+    """Independent views (streaming clients, camera paths) through `depth`
+    resident FrameEngines, each replaying its frame graph on its own CUDA
+    stream.  While one slot's frame computes, the others' kernels fill the
+    SMs its latency-bound stages leave idle and the copy engines return the
+    finished frames' chart ids, visible list, UVs and placements to pinned
+    host memory.  Results are delivered in view order through
+    `on_frame(HostFrame)`."""
+
+    def __init__(self, mesh: Mesh, device: int | None = None, settings: FrameSettings | None = None,
+                 depth: int = 4, outputs: tuple = ("chart_of_triangle", "visible", "uv", "placements")):
+        torch = nat.require_device()
+        if depth < 1:
+            raise ValueError("depth must be >= 1")
+        self.settings = settings or FrameSettings()
+        self.engines = [FrameEngine(mesh, device, self.settings) for _ in range(depth)]
+        self.device = self.engines[0].device
+        self.streams = [torch.cuda.Stream(device=self.device) for _ in range(depth)]
+        self.outputs = tuple(outputs)
+        T = mesh.n_triangles
+        uv_dt = torch.float64 if self.settings.uv_f64 else torch.float32
+        self._host = []
+        for _ in range(depth):
+            h = {}
+            if "chart_of_triangle" in outputs:
+                h["chart_of_triangle"] = torch.empty(T, dtype=torch.int32).pin_memory()
+            if "visible" in outputs:
+                h["visible"] = torch.empty(T, dtype=torch.int32).pin_memory()
+            if "uv" in outputs:
+                h["uv"] = torch.empty((T, 6), dtype=uv_dt).pin_memory()
+            if "placements" in outputs:
+                h["placements"] = torch.empty((T + 1, 8), dtype=torch.int64).pin_memory()
+            self._host.append(h)
+        self._np = [{k: t.numpy() for k, t in h.items()} for h in self._host]
+
+    @property
+    def depth(self) -> int:
+        return len(self.engines)
+
+    def _finish(self, slot: int, index: int, view) -> HostFrame:
+        """Wait for the slot's frame, then queue its D2H copies on the slot
+        stream (fa_frame_download; no device tensors are built per frame)."""
+        eng, st = self.engines[slot], self.streams[slot]
+        L, h_ctx, res = eng.ctx.L, eng.ctx.h, eng._res
+        sp = ctypes.c_void_p(st.cuda_stream)
+        hf = HostFrame(index)
+        for _ in range(4):
+            code = L.fa_frame_finish(h_ctx, ctypes.byref(res), sp)
+            if code == nat.FA_INTERNAL_ERROR and "rerun" in nat.last_error():
+                eng.launch(view, stream=st)  # work queues grown: replay the same view
+                continue
+            break
+        else:
+            hf.status, hf.error = -2, RuntimeError("frame work queues kept overflowing")
+            return hf
+        if code != nat.FA_OK:
+            hf.status = int(code)
+            try:
+                nat.raise_for_status(code)
+            except Exception as exc:  # the reference exception (NothingVisible, PackFailure, ...)
+                hf.error = exc
+            return hf
+        nv, C = int(res.n_visible), int(res.n_charts)
+        hf.n_visible, hf.n_charts = nv, C
+        hf.scale = Fraction(int(res.scale_num), int(res.scale_den)) if res.scale_den else None
+        hf.screen_fragments, hf.texels_allocated = int(res.screen_fragments), int(res.texels_allocated)
+        h = self._host[slot]
+        ptr = {k: ctypes.c_void_p(t.data_ptr()) if k in h else None
+               for k, t in ((k, h.get(k)) for k in ("chart_of_triangle", "visible", "uv", "placements"))}
+        if any(p is not None for p in ptr.values()):
+            nat.raise_for_status(L.fa_frame_download(h_ctx, ctypes.byref(res), ptr["chart_of_triangle"],
+                                                     ptr["visible"], ptr["uv"], ptr["placements"], sp))
+        if "chart_of_triangle" in h:
+            hf.chart_of_triangle = self._np[slot]["chart_of_triangle"]
+        if "visible" in h:
+            hf.visible = self._np[slot]["visible"][:nv]
+        if "uv" in h:
+            hf.uv = self._np[slot]["uv"][:nv]
+        if "placements" in h:
+            hf.placements = self._np[slot]["placements"][:C]
+        return hf
+
+    def run(self, views, on_frame=None, before_launch=None) -> int:
+        """Process `views` (4x4 view-projection matrices) in order.
+
+        on_frame(HostFrame) is called once per view, in view order, after its
+        host copies completed.  before_launch(stream) (optional) runs just
+        before each frame is enqueued on its slot stream.  Returns the number
+        of views processed."""
+        P = self.depth
+        inflight = [None] * P   # (index, view) launched, not finished
+        copied = [None] * P     # HostFrame whose copies are queued
+        done_ev = [None] * P
+        torch = nat._torch()
+        n = 0
+
+        def deliver(slot):
+            if copied[slot] is not None:
+                done_ev[slot].synchronize()
+                if on_frame is not None:
+                    on_frame(copied[slot])
+                copied[slot] = None
+
+        def retire(slot):
+            if inflight[slot] is not None:
+                idx, v = inflight[slot]
+                copied[slot] = self._finish(slot, idx, v)
+                ev = torch.cuda.Event()
+                ev.record(self.streams[slot])
+                done_ev[slot] = ev
+                inflight[slot] = None
+
+        for i, view in enumerate(views):
+            slot = i % P
+            deliver(slot)
+            retire(slot)
+            st = self.streams[slot]
+            if before_launch is not None:
+                before_launch(st)
+            self.engines[slot].launch(view, stream=st)
+            inflight[slot] = (i, view)
+            n += 1
+        # drain in view order
+        order = sorted((inflight[s][0], s) for s in range(P) if inflight[s] is not None)
+        pend = sorted((copied[s].index, s) for s in range(P) if copied[s] is not None)
+        for _, s in pend:
+            deliver(s)
+        for _, s in order:
+            retire(s)
+            deliver(s)
+        return n
