@@ -115,7 +115,7 @@ void fa_destroy(fa_ctx* c) {
                       &c->target, &c->survived, &c->okey, &c->oidx, &c->ow, &c->oh, &c->orot, &c->sortk, &c->sortv,
                       &c->pinv, &c->cand, &c->cand_p, &c->cand_w, &c->cand_h, &c->cand_y, &c->rowstart,
                       &c->placements, &c->uv, &c->vp_dev, &c->blocks, &c->dstat, &c->aux, &c->in_tw, &c->in_th,
-                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list};
+                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list, &c->hiz, &c->wid};
     for (fa_buf* b : bufs) free_buf(*b);
     for (cudaEvent_t e : c->fj)
         if (e) cudaEventDestroy(e);
@@ -151,6 +151,8 @@ static int ensure_raster(fa_ctx* ctx, int W, int H, bool depth) {
     ENSURE(clip, (V > 0 ? V : 1) * sizeof(double4));
     ENSURE(scr, (V > 0 ? V : 1) * sizeof(double4));
     if (depth) ENSURE(depth_keys, (size_t)W * H * 8);
+    if (depth && T < (1 << 24)) ENSURE(wid, (size_t)W * H * 8);
+    ENSURE(hiz, (size_t)fa_hiz_dim(W) * fa_hiz_dim(H) * 8);
     ENSURE(flags, ((T + 15) / 16 + 1) * 16);
     ENSURE(clip_list, (T + 1) * 4);
     ENSURE(small_rec, (T + 1) * sizeof(SmallRec));
@@ -269,9 +271,10 @@ static int upload_vp(fa_ctx* ctx, const double* vp_host, cudaStream_t s) {
 static int launch_depth(fa_ctx* ctx, int W, int H, int cull, unsigned char* flags_out, cudaStream_t s, int& nl) {
     int T = (int)ctx->T, V = (int)ctx->V;
     fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), P<double4>(ctx->scr), W, H,
-                         P<int>(ctx->vmin), P<unsigned long long>(ctx->depth_keys), (long long)W * H, flags_out, T, s);
+                         P<int>(ctx->vmin), P<unsigned long long>(ctx->depth_keys), nullptr, (long long)W * H,
+                         flags_out, T, s);
     nl += 1 + fa_launch_depth_pass(true, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, W, H, cull,
-                                   P<unsigned long long>(ctx->depth_keys), P<SmallRec>(ctx->small_rec),
+                                   P<unsigned long long>(ctx->depth_keys), nullptr, P<SmallRec>(ctx->small_rec),
                                    P<int>(ctx->clip_list), P<TriSetup>(ctx->large), ctx->max_large,
                                    P<int2>(ctx->tiles), ctx->max_tiles, P<fa_dstat>(ctx->dstat), s, nullptr, nullptr,
                                    nullptr);
@@ -296,7 +299,7 @@ int fa_project(fa_ctx* ctx, const double* vp_host, double* clip_out, void* strea
     int r = upload_vp(ctx, vp_host, s);
     if (r) return r;
     fa_launch_frame_init(ctx->pos, (int)ctx->V, P<double>(ctx->vp_dev), (double4*)clip_out, nullptr, 0, 0, nullptr,
-                         nullptr, 0, nullptr, 0, s);
+                         nullptr, nullptr, 0, nullptr, 0, s);
     CKL();
     return FA_OK;
 }
@@ -344,15 +347,18 @@ int fa_mark_visible(fa_ctx* ctx, const double* vp_host, const double* depth, int
         r = upload_vp(ctx, vp_host, s);
         if (r) return r;
         fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), P<double4>(ctx->scr), width,
-                             height, nullptr, nullptr, 0, P<unsigned char>(ctx->flags), T, s);
+                             height, nullptr, nullptr, nullptr, 0, P<unsigned char>(ctx->flags), T, s);
         fa_launch_encode_depth(depth, P<unsigned long long>(ctx->depth_keys), (long long)width * height, s);
         fa_launch_depth_pass(false, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, width, height,
-                             backface_cull, nullptr, P<SmallRec>(ctx->small_rec), P<int>(ctx->clip_list),
+                             backface_cull, nullptr, nullptr, P<SmallRec>(ctx->small_rec), P<int>(ctx->clip_list),
                              P<TriSetup>(ctx->large), ctx->max_large, P<int2>(ctx->tiles), ctx->max_tiles,
                              P<fa_dstat>(ctx->dstat), s, nullptr, nullptr, nullptr);
+        fa_launch_depth_hiz(P<unsigned long long>(ctx->depth_keys), nullptr, width, height,
+                            P<unsigned long long>(ctx->hiz), nullptr, nullptr, s);
         fa_launch_raster_vis(P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large), P<int2>(ctx->tiles),
                              ctx->max_tiles, ctx->max_large, T, width, P<unsigned long long>(ctx->depth_keys),
-                             P<unsigned char>(ctx->flags), P<fa_dstat>(ctx->dstat), s, nullptr, nullptr, nullptr);
+                             P<unsigned long long>(ctx->hiz), P<unsigned char>(ctx->flags), P<fa_dstat>(ctx->dstat),
+                             s, nullptr, nullptr, nullptr);
         CKL();
         r = read_stat(ctx, s);
         if (r) return r;
@@ -460,8 +466,8 @@ int fa_chart_boxes(fa_ctx* ctx, const double* vp_host, const int32_t* labels, in
     if (r) return r;
     fa_dstat* st = P<fa_dstat>(ctx->dstat);
     unsigned char* fl = P<unsigned char>(ctx->flags);
-    fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), nullptr, 0, 0, nullptr, nullptr, 0,
-                         nullptr, 0, s);
+    fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), nullptr, 0, 0, nullptr, nullptr,
+                         nullptr, 0, nullptr, 0, s);
     fa_launch_flags_from_labels(labels, fl, T, s);
     fa_launch_compact_visible(fl, T, P<int>(ctx->blocks), P<int>(ctx->vis_list), P<int>(ctx->aux), st, s);
     fa_launch_compact_roots(P<int>(ctx->vis_list), labels, T, P<int>(ctx->blocks), P<int>(ctx->roots),
@@ -661,26 +667,28 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
         return FA_OK;
     };
     unsigned char* flags = P<unsigned char>(ctx->flags);
-    int T_ = T;
-    (void)T_;
-    int V_ = V;
+    // pixel-winner buffer: triangle ids must fit the low FA_WID_BITS (24) bits
+    unsigned long long* wid = T < (1 << 24) ? P<unsigned long long>(ctx->wid) : nullptr;
     mark();  // 0: start
-    fa_launch_frame_init(ctx->pos, V_, P<double>(ctx->vp_dev), P<double4>(ctx->clip), P<double4>(ctx->scr), W, H,
-                         P<int>(ctx->vmin), P<unsigned long long>(ctx->depth_keys), (long long)W * H, flags, T, s);
+    fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), P<double4>(ctx->scr), W, H,
+                         P<int>(ctx->vmin), P<unsigned long long>(ctx->depth_keys), wid, (long long)W * H, flags, T,
+                         s);
     nl += 1;
     mark();  // 1: project + clears
     int r = ensure_side(ctx);
     if (r) return r;
     nl += fa_launch_depth_pass(true, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, W, H,
-                               p->backface_cull, P<unsigned long long>(ctx->depth_keys), P<SmallRec>(ctx->small_rec),
-                               P<int>(ctx->clip_list), P<TriSetup>(ctx->large), ctx->max_large, P<int2>(ctx->tiles),
-                               ctx->max_tiles, st, s, ctx->side, ctx->fj[0], ctx->fj[1]);
-    fa_launch_count_finite(P<unsigned long long>(ctx->depth_keys), (long long)W * H, st, s);
+                               p->backface_cull, P<unsigned long long>(ctx->depth_keys), wid,
+                               P<SmallRec>(ctx->small_rec), P<int>(ctx->clip_list), P<TriSetup>(ctx->large),
+                               ctx->max_large, P<int2>(ctx->tiles), ctx->max_tiles, st, s, ctx->side, ctx->fj[0],
+                               ctx->fj[1]);
+    fa_launch_depth_hiz(P<unsigned long long>(ctx->depth_keys), wid, W, H, P<unsigned long long>(ctx->hiz), flags, st,
+                        s);
     nl += 1;
     mark();  // 2: depth pass
     nl += fa_launch_raster_vis(P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large), P<int2>(ctx->tiles),
-                               ctx->max_tiles, ctx->max_large, T, W, P<unsigned long long>(ctx->depth_keys), flags, st,
-                               s, ctx->side, ctx->fj[2], ctx->fj[3]);
+                               ctx->max_tiles, ctx->max_large, T, W, P<unsigned long long>(ctx->depth_keys),
+                               P<unsigned long long>(ctx->hiz), flags, st, s, ctx->side, ctx->fj[2], ctx->fj[3]);
     mark();  // 3: visibility pass
     fa_launch_compact_visible(flags, T, P<int>(ctx->blocks), P<int>(ctx->vis_list), P<int>(ctx->label), st, s);
     nl += 2;

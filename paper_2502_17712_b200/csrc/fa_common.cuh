@@ -20,6 +20,7 @@
 #define FA_MAXV 16              // clipped polygon capacity (real max is 10)
 
 #define FA_NUM_SMS 148
+#define FA_HIZ 8                // hierarchical-Z tile edge (pixels)
 
 // device status bits (fa_ctx::dstat->flags)
 #define FA_DFLAG_POLY_OVERFLOW 1u

@@ -44,6 +44,8 @@ struct fa_ctx {
     fa_buf cand, cand_p, cand_w, cand_h, cand_y, rowstart, placements, uv, vp_dev, blocks, dstat, aux;
     fa_buf in_tw, in_th, in_cid, in_mt;
     fa_buf scr, clip_list;  // per-vertex screen records; generic-path triangle list
+    fa_buf hiz;             // 8x8 hierarchical-Z max keys of the final depth
+    fa_buf wid;             // pass-1 pixel winners (truncated key | triangle id)
     size_t gen = 0;
     int max_large = 0, max_tiles = 0;
     int pack_batch = 0;  // candidates per pack launch
@@ -73,23 +75,26 @@ struct fa_ctx {
 bool fa_ensure(fa_ctx* ctx, fa_buf& b, size_t bytes);
 
 // ---- raster (fa_raster.cu) ------------------------------------------------
+// wid (may be null): pass-1 winner buffer, cleared to all ones with depth
 void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* clip, double4* scr, int W, int H,
-                          int* vmin,
-                          unsigned long long* depth, long long npx, unsigned char* flags, int T, cudaStream_t s);
+                          int* vmin, unsigned long long* depth, unsigned long long* wid, long long npx,
+                          unsigned char* flags, int T, cudaStream_t s);
 // side == nullptr: everything on s; otherwise fork/join through the events.
-// Both return the number of kernels launched.
+// Both return the number of kernels launched.  wid: see depth_min (may be null).
 int fa_launch_depth_pass(bool write_depth, const double4* clip, const double4* scr, const int* tris, int T, int W,
-                         int H, int cull, unsigned long long* depth, SmallRec* small_rec, int* clip_list,
-                         TriSetup* large, int max_large, int2* tiles, int max_tiles, fa_dstat* st, cudaStream_t s,
-                         cudaStream_t side, cudaEvent_t ev_fork, cudaEvent_t ev_join);
+                         int H, int cull, unsigned long long* depth, unsigned long long* wid, SmallRec* small_rec,
+                         int* clip_list, TriSetup* large, int max_large, int2* tiles, int max_tiles, fa_dstat* st,
+                         cudaStream_t s, cudaStream_t side, cudaEvent_t ev_fork, cudaEvent_t ev_join);
 int fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const int2* tiles, int max_tiles,
-                         int max_large, int T, int W, const unsigned long long* depth, unsigned char* flags,
-                         const fa_dstat* st, cudaStream_t s, cudaStream_t side, cudaEvent_t ev_fork,
-                         cudaEvent_t ev_join);
+                         int max_large, int T, int W, const unsigned long long* depth, const unsigned long long* hiz,
+                         unsigned char* flags, const fa_dstat* st, cudaStream_t s, cudaStream_t side,
+                         cudaEvent_t ev_fork, cudaEvent_t ev_join);
 void fa_launch_decode_depth(const unsigned long long* keys, double* out, long long n, cudaStream_t s);
-void fa_launch_count_finite(const unsigned long long* depth, long long npx, fa_dstat* st, cudaStream_t s);
-void fa_launch_small_coop(bool vis, const SmallRec* recs, int T, int W, unsigned long long* depth,
-                          unsigned char* flags, const fa_dstat* st, cudaStream_t s);
+// screen_fragments (st may be null) + 8x8 hierarchical-Z max keys + flags of
+// the pass-1 pixel winners (wid may be null)
+void fa_launch_depth_hiz(const unsigned long long* depth, const unsigned long long* wid, int W, int H,
+                         unsigned long long* hiz, unsigned char* flags, fa_dstat* st, cudaStream_t s);
+static inline int fa_hiz_dim(int n) { return (n + FA_HIZ - 1) / FA_HIZ; }
 void fa_launch_encode_depth(const double* in, unsigned long long* keys, long long n, cudaStream_t s);
 size_t fa_trisetup_bytes();
 

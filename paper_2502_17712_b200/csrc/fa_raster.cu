@@ -20,6 +20,34 @@
 #define TILE_W 16
 #define TILE_H 8
 
+#ifdef FA_HIZ_STATS
+// debug build only: [small records rejected by the hierarchical Z, small
+// records sampled, tiles tested, tiles rejected, tiles skipped (visible)]
+__device__ unsigned long long g_hiz_stats[6];
+extern "C" void fa_debug_hiz_stats(unsigned long long* out) {
+    cudaMemcpyFromSymbol(out, g_hiz_stats, sizeof(g_hiz_stats));
+    unsigned long long z[6] = {0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_hiz_stats, z, sizeof(z));
+}
+#endif
+
+// Pass-1 depth write.  Besides the exact order-preserving key minimum, when a
+// winner buffer is bound it keeps min((key & ~0xFFFFFF) | t): the triangle it
+// names at a pixel has a key equal to the final minimum in its top 40 bits
+// (sign, exponent, 28 mantissa bits), i.e. a depth within 2^-27 relative of
+// it — far inside the visibility slack of 1e-6 (charts.py:309-311), so that
+// triangle is visible and k_depth_hiz can flag it without a second raster.
+// `check` skips both atomics when the stored key is already <= key: the
+// triangle that first lowers a pixel to its final key always executes them.
+#define FA_WID_BITS 24
+__device__ __forceinline__ void depth_min(unsigned long long* __restrict__ depth, unsigned long long* __restrict__ wid,
+                                          long long off, unsigned long long key, int t, bool check) {
+    unsigned long long* d = depth + off;
+    if (check && !(key < *d)) return;
+    atomicMin(d, key);
+    if (wid) atomicMin(wid + off, (key & ~((1ull << FA_WID_BITS) - 1)) | (unsigned long long)t);
+}
+
 // warp-aggregated single-slot append among the currently active lanes
 __device__ __forceinline__ int active_append1(int* counter) {
     unsigned mask = __activemask();
@@ -34,7 +62,8 @@ __device__ __forceinline__ int active_append1(int* counter) {
 // ---- frame init: projection + buffer clears ------------------------------
 __global__ void k_frame_init(const double* __restrict__ pos, int V, const double* __restrict__ vp_dev,
                              double4* __restrict__ clip, double4* __restrict__ scr, int W, int H,
-                             int* __restrict__ vmin, unsigned long long* __restrict__ depth, long long npx,
+                             int* __restrict__ vmin, unsigned long long* __restrict__ depth,
+                             unsigned long long* __restrict__ wid, long long npx,
                              unsigned int* __restrict__ flags32, int nflag32) {
     long long stride = (long long)gridDim.x * blockDim.x;
     long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -53,6 +82,12 @@ __global__ void k_frame_init(const double* __restrict__ pos, int V, const double
         long long n2 = npx >> 1;
         for (long long i = i0; i < n2; i += stride) d2[i] = make_ulonglong2(FA_KEY_POS_INF, FA_KEY_POS_INF);
         if ((npx & 1) && i0 == 0) depth[npx - 1] = FA_KEY_POS_INF;
+    }
+    if (wid) {
+        ulonglong2* w2 = reinterpret_cast<ulonglong2*>(wid);
+        long long n2 = npx >> 1;
+        for (long long i = i0; i < n2; i += stride) w2[i] = make_ulonglong2(~0ull, ~0ull);
+        if ((npx & 1) && i0 == 0) wid[npx - 1] = ~0ull;
     }
     if (flags32)
         for (long long i = i0; i < nflag32; i += stride) flags32[i] = 0u;
@@ -170,6 +205,7 @@ template <bool WRITE_DEPTH>
 __global__ void __launch_bounds__(256) k_raster_clipped(const double4* __restrict__ clip, const int* __restrict__ tris,
                                                         int W, int H, int cull, const int* __restrict__ clip_list,
                                                         unsigned long long* __restrict__ depth,
+                                                        unsigned long long* __restrict__ wid,
                                                         TriSetup* __restrict__ large, int max_large,
                                                         int2* __restrict__ tiles, int max_tiles,
                                                         fa_dstat* __restrict__ st) {
@@ -210,9 +246,7 @@ __global__ void __launch_bounds__(256) k_raster_clipped(const double4* __restric
                     int iy = s.min_y + dy, ix = s.min_x + (k - dy * bw);
                     double px = (double)ix + 0.5, py = (double)iy + 0.5;
                     if (!sample_inside(s, px, py)) continue;
-                    unsigned long long key = f64_key(sample_depth(s, px, py));
-                    unsigned long long* d = depth + (long long)iy * W + ix;
-                    if (key < *d) atomicMin(d, key);
+                    depth_min(depth, wid, (long long)iy * W + ix, f64_key(sample_depth(s, px, py)), t, true);
                 }
             }
         } else {
@@ -229,22 +263,54 @@ __global__ void __launch_bounds__(256) k_raster_clipped(const double4* __restric
     }
 }
 
-// screen_fragments = #finite depth samples (cli.py:390), one pass over the keys
-__global__ void k_count_finite(const unsigned long long* __restrict__ depth, long long npx, fa_dstat* __restrict__ st) {
+// One pass over the final depth keys, one thread per 8x8 pixel tile:
+//  * screen_fragments = #finite depth samples (cli.py:390), and
+//  * the hierarchical-Z buffer for the visibility pass: per tile the largest
+//    key in [key(-inf), key(+inf)) — +inf (empty) and NaN pixels can never make
+//    a sample pass (charts.py:309-311), so they are left out — or 0 when the
+//    tile has none (nothing can be covered there).
+//  * with a winner buffer (depth_min), the flag of every pixel's winner at a
+//    finite final depth — those triangles are visible (see depth_min), so the
+//    visibility pass skips them.  (At -inf the slack test is NaN: no flag.)
+__global__ void __launch_bounds__(256) k_depth_hiz(const unsigned long long* __restrict__ depth,
+                                                   const unsigned long long* __restrict__ wid, int W, int H,
+                                                   unsigned long long* __restrict__ hiz, int htx, int hty,
+                                                   unsigned char* __restrict__ flags, fa_dstat* __restrict__ st) {
+    // one thread per pixel column of a tile row (8 pixels tall): the loads of
+    // a warp are 32 consecutive pixels of one image row; 8 consecutive lanes
+    // form one tile and reduce its maximum with shuffles
     long long c = 0;
-    long long stride = (long long)gridDim.x * blockDim.x;
-    const ulonglong2* d2 = reinterpret_cast<const ulonglong2*>(depth);
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < npx / 2; i += stride) {
-        ulonglong2 v = d2[i];
-        // finite <=> key strictly between key(-inf) and key(+inf)
-        c += (v.x > FA_KEY_NEG_INF && v.x < FA_KEY_POS_INF) + (v.y > FA_KEY_NEG_INF && v.y < FA_KEY_POS_INF);
-    }
-    if ((npx & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
-        unsigned long long v = depth[npx - 1];
-        c += (v > FA_KEY_NEG_INF && v < FA_KEY_POS_INF);
+    const int rowlen = htx * FA_HIZ;
+    const int n = rowlen * hty;
+    const int n_pad = (n + 31) & ~31;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += gridDim.x * blockDim.x) {
+        const int ty = i / rowlen, x = i - ty * rowlen;
+        const int y0 = ty * FA_HIZ, y1 = min(y0 + FA_HIZ, H);
+        unsigned long long mx = 0;
+        if (i < n && x < W) {
+            int last = -1;
+            for (int y = y0; y < y1; y++) {
+                const long long p = (long long)y * W + x;
+                unsigned long long v = depth[p];
+                bool fin = v > FA_KEY_NEG_INF && v < FA_KEY_POS_INF;
+                c += fin;
+                if (v >= FA_KEY_NEG_INF && v < FA_KEY_POS_INF && v > mx) mx = v;
+                if (wid && fin) {
+                    int id = (int)(wid[p] & ((1ull << FA_WID_BITS) - 1));
+                    if (id != last) flags[id] = 1;
+                    last = id;
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 1; o < FA_HIZ; o <<= 1) {
+            unsigned long long m = __shfl_xor_sync(0xffffffffu, mx, o);
+            mx = m > mx ? m : mx;
+        }
+        if (i < n && (x & (FA_HIZ - 1)) == 0) hiz[ty * htx + x / FA_HIZ] = mx;
     }
     c = warp_sum(c);
-    if (lane_id() == 0 && c) atomicAdd((unsigned long long*)&st->screen_fragments, (unsigned long long)c);
+    if (st && lane_id() == 0 && c) atomicAdd((unsigned long long*)&st->screen_fragments, (unsigned long long)c);
 }
 
 // copy one TriSetup into warp-private shared memory
@@ -280,6 +346,7 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const SmallRec* __re
                                                             const TriSetup* __restrict__ large,
                                                             const int2* __restrict__ tiles, int W,
                                                             unsigned long long* __restrict__ depth,
+                                                            unsigned long long* __restrict__ wid,
                                                             fa_dstat* __restrict__ st, int max_tiles) {
     __shared__ TriSetup sm[8];
     int warp = threadIdx.x >> 5, lane = lane_id();
@@ -294,16 +361,14 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const SmallRec* __re
             int x, y0;
             tile_lane_origin(f.min_x, f.max_x, f.min_y, rec.y, x, y0);
             if (x <= f.max_x) {
-                double px = (double)x + 0.5;
+                const ColTerms ct = col_terms(f, (double)x + 0.5);
 #pragma unroll
                 for (int k = 0; k < TILE_H / 2; k++) {
                     int y = y0 + 2 * k;
                     if (y > f.max_y) break;
                     double py = (double)y + 0.5;
-                    if (!sample_inside3(f, px, py)) continue;
-                    unsigned long long key = f64_key(sample_depth3(f, px, py));
-                    unsigned long long* d = depth + (long long)y * W + x;
-                    if (key < *d) atomicMin(d, key);
+                    if (!inside_col(f, ct, py)) continue;
+                    depth_min(depth, wid, (long long)y * W + x, f64_key(depth_col(f, ct, py)), t, true);
                 }
             }
             continue;
@@ -323,9 +388,7 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const SmallRec* __re
                 if (y > s.max_y) break;
                 double py = (double)y + 0.5;
                 if (!sample_inside(s, px, py)) continue;
-                unsigned long long key = f64_key(sample_depth(s, px, py));
-                unsigned long long* d = depth + (long long)y * W + x;
-                if (key < *d) atomicMin(d, key);
+                depth_min(depth, wid, (long long)y * W + x, f64_key(sample_depth(s, px, py)), s.tri, true);
             }
         }
     }
@@ -335,14 +398,12 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const SmallRec* __re
 // A warp stages 32 records in shared memory, prefix-sums their bbox sample
 // counts, and gives every lane one contiguous, equal chunk of the combined
 // sample space, so per-triangle size differences no longer diverge the warp.
-// VIS = false: depth pass (RED.MIN.64 per covered sample).
-// VIS = true: visibility pass (any covered sample passing the slack test sets
-// the flag; a per-record shared "done" bit lets other lanes skip the rest).
+// Depth pass only (RED.MIN.64 per covered sample): the visibility pass stops
+// at a record's first passing sample, which an even split cannot exploit.
 #define COOP_WARPS 8
 struct CoopWarp {
     SmallRec rec[32];
     int prefix[33];
-    int done[32];
 };
 
 __device__ __forceinline__ void coop_locate(const Setup3& f, int li, int bw, double& px, double& py, int& ix, int& iy) {
@@ -353,10 +414,9 @@ __device__ __forceinline__ void coop_locate(const Setup3& f, int li, int bw, dou
     py = (double)iy + 0.5;
 }
 
-template <bool VIS>
 __global__ void __launch_bounds__(COOP_WARPS * 32) k_small_coop(const SmallRec* __restrict__ recs, int W,
                                                                 unsigned long long* __restrict__ depth,
-                                                                unsigned char* __restrict__ flags,
+                                                                unsigned long long* __restrict__ wid,
                                                                 const fa_dstat* __restrict__ st) {
     __shared__ CoopWarp sh[COOP_WARPS];
     const int warp = threadIdx.x >> 5, lane = lane_id();
@@ -382,7 +442,6 @@ __global__ void __launch_bounds__(COOP_WARPS * 32) k_small_coop(const SmallRec* 
         }
         cw.prefix[lane + 1] = incl;
         if (lane == 0) cw.prefix[0] = 0;
-        cw.done[lane] = 0;
         __syncwarp();
         const int S = __shfl_sync(0xffffffffu, incl, 31);
         const int chunk = (S + 31) >> 5;
@@ -401,76 +460,30 @@ __global__ void __launch_bounds__(COOP_WARPS * 32) k_small_coop(const SmallRec* 
             load_rec(&cw.rec[r], f, t);
             int bw = f.max_x - f.min_x + 1;
             int pr = cw.prefix[r], pe = cw.prefix[r + 1];
-            if (!VIS) {
-                // consecutive samples: step (ix, iy) instead of dividing per sample
-                double px, py;
-                int ix, iy;
-                coop_locate(f, s - pr, bw, px, py, ix, iy);
-                for (; s < s_end; s++) {
-                    if (s >= pe) {
-                        do {
-                            r++;
-                            pr = pe;
-                            pe = cw.prefix[r + 1];
-                        } while (s >= pe);
-                        load_rec(&cw.rec[r], f, t);
-                        ix = f.min_x;
-                        iy = f.min_y;
-                    }
-                    px = (double)ix + 0.5;
-                    py = (double)iy + 0.5;
-                    if (sample_inside3(f, px, py))
-                        atomicMin(depth + (long long)iy * W + ix, f64_key(sample_depth3(f, px, py)));
-                    if (++ix > f.max_x) {
-                        ix = f.min_x;
-                        iy++;
-                    }
-                }
-            } else {
-                // gather up to 4 covered samples (possibly of different
-                // records), then issue their depth loads together
-                double zq[4];
-                const unsigned long long* aq[4];
-                int rq[4], tq[4];
-                int nq = 0;
-                bool skip = cw.done[r] != 0;
-                for (; s < s_end; s++) {
-                    while (s >= pe) {
+            // consecutive samples: step (ix, iy) instead of dividing per sample
+            double px, py;
+            int ix, iy;
+            coop_locate(f, s - pr, bw, px, py, ix, iy);
+            RowTerms rt = row_terms(f, py);
+            for (; s < s_end; s++) {
+                if (s >= pe) {
+                    do {
                         r++;
-                        load_rec(&cw.rec[r], f, t);
-                        bw = f.max_x - f.min_x + 1;
                         pr = pe;
                         pe = cw.prefix[r + 1];
-                        skip = cw.done[r] != 0;
-                    }
-                    if (skip) { s = pe - 1; continue; }
-                    double px, py;
-                    int ix, iy;
-                    coop_locate(f, s - pr, bw, px, py, ix, iy);
-                    if (!sample_inside3(f, px, py)) continue;
-                    zq[nq] = sample_depth3(f, px, py);
-                    aq[nq] = depth + (long long)iy * W + ix;
-                    rq[nq] = r;
-                    tq[nq] = t;
-                    if (++nq == 4) {
-                        unsigned long long k0 = aq[0][0], k1 = aq[1][0], k2 = aq[2][0], k3 = aq[3][0];
-                        unsigned long long kk[4] = {k0, k1, k2, k3};
-#pragma unroll
-                        for (int q = 0; q < 4; q++) {
-                            if (depth_passes(zq[q], key_f64(kk[q]))) {
-                                flags[tq[q]] = 1;
-                                cw.done[rq[q]] = 1;
-                            }
-                        }
-                        nq = 0;
-                        skip = cw.done[r] != 0;
-                    }
+                    } while (s >= pe);
+                    load_rec(&cw.rec[r], f, t);
+                    ix = f.min_x;
+                    iy = f.min_y;
+                    rt = row_terms(f, (double)iy + 0.5);
                 }
-                for (int q = 0; q < nq; q++) {
-                    if (depth_passes(zq[q], key_f64(*aq[q]))) {
-                        flags[tq[q]] = 1;
-                        cw.done[rq[q]] = 1;
-                    }
+                px = (double)ix + 0.5;
+                if (inside_row(f, rt, px))
+                    depth_min(depth, wid, (long long)iy * W + ix, f64_key(depth_row(f, rt, px)), t, false);
+                if (++ix > f.max_x) {
+                    ix = f.min_x;
+                    iy++;
+                    rt = row_terms(f, (double)iy + 0.5);
                 }
             }
         }
@@ -481,38 +494,73 @@ __global__ void __launch_bounds__(COOP_WARPS * 32) k_small_coop(const SmallRec* 
 // ---- pass 2 small: one thread per covering triangle -----------------------
 __global__ void __launch_bounds__(256) k_raster_vis_small(const SmallRec* __restrict__ small_rec, int W,
                                                           const unsigned long long* __restrict__ depth,
+                                                          const unsigned long long* __restrict__ hiz, int htx,
                                                           unsigned char* __restrict__ flags,
                                                           const fa_dstat* __restrict__ st) {
     int n3 = st->n_small3;
     int stride = gridDim.x * blockDim.x;
-    // stored records, one thread each: stop at the first passing sample;
-    // gather up to 4 covered samples, then issue their depth loads together
+    // Stored records, one thread each.  One round trip first decides most
+    // records without sampling: the flag (set by k_depth_hiz for the pixel
+    // winners of pass 1) and the record's 8x8 hierarchical-Z tiles (when its
+    // window spans at most 2x2 of them).  The rest stop at the first passing
+    // sample, gathering up to 4 covered samples per batch of depth loads.
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n3; i += stride) {
         Setup3 f;
         int t;
         load_rec(small_rec + i, f, t);
+        const int tx0 = f.min_x / FA_HIZ, tx1 = f.max_x / FA_HIZ, ty0 = f.min_y / FA_HIZ, ty1 = f.max_y / FA_HIZ;
+        const bool hz = tx1 - tx0 <= 1 && ty1 - ty0 <= 1;
+        unsigned long long h00 = 1, h01 = 1, h10 = 1, h11 = 1;
+        const unsigned char seen = flags[t];
+        if (hz) {
+            h00 = __ldg(hiz + ty0 * htx + tx0);
+            h01 = __ldg(hiz + ty0 * htx + tx1);
+            h10 = __ldg(hiz + ty1 * htx + tx0);
+            h11 = __ldg(hiz + ty1 * htx + tx1);
+        }
+        const double zlb = depth_lower_bound(f, f.min_x, f.max_x, f.min_y, f.max_y);
+        if (seen) continue;
+        if (hz && hiz_tile_rejects(h00, zlb) && hiz_tile_rejects(h01, zlb) && hiz_tile_rejects(h10, zlb) &&
+            hiz_tile_rejects(h11, zlb)) {
+#ifdef FA_HIZ_STATS
+            atomicAdd(&g_hiz_stats[0], 1ull);
+#endif
+            continue;
+        }
+#ifdef FA_HIZ_STATS
+        atomicAdd(&g_hiz_stats[1], 1ull);
+#endif
         bool vis = false;
-        double zq[4];
-        const unsigned long long* aq[4];
+        // queue of up to 4 covered samples in named registers (no local memory)
+        double z0 = 0, z1 = 0, z2 = 0, z3 = 0;
+        const unsigned long long *a0 = depth, *a1 = depth, *a2 = depth, *a3 = depth;
         int nq = 0;
         for (int iy = f.min_y; iy <= f.max_y && !vis; iy++) {
-            double py = (double)iy + 0.5;
+            const RowTerms rt = row_terms(f, (double)iy + 0.5);
             const unsigned long long* row = depth + (long long)iy * W;
             for (int ix = f.min_x; ix <= f.max_x; ix++) {
                 double px = (double)ix + 0.5;
-                if (!sample_inside3(f, px, py)) continue;
-                zq[nq] = sample_depth3(f, px, py);
-                aq[nq] = row + ix;
+                if (!inside_row(f, rt, px)) continue;
+                double z = depth_row(f, rt, px);
+                const unsigned long long* a = row + ix;
+                if (nq == 0) { z0 = z; a0 = a; }
+                else if (nq == 1) { z1 = z; a1 = a; }
+                else if (nq == 2) { z2 = z; a2 = a; }
+                else { z3 = z; a3 = a; }
                 if (++nq == 4) {
-                    unsigned long long k0 = aq[0][0], k1 = aq[1][0], k2 = aq[2][0], k3 = aq[3][0];
-                    vis = depth_passes(zq[0], key_f64(k0)) || depth_passes(zq[1], key_f64(k1)) ||
-                          depth_passes(zq[2], key_f64(k2)) || depth_passes(zq[3], key_f64(k3));
+                    unsigned long long k0 = *a0, k1 = *a1, k2 = *a2, k3 = *a3;
+                    vis = depth_passes(z0, key_f64(k0)) | depth_passes(z1, key_f64(k1)) |
+                          depth_passes(z2, key_f64(k2)) | depth_passes(z3, key_f64(k3));
                     nq = 0;
                     if (vis) break;
                 }
             }
         }
-        for (int q = 0; q < nq && !vis; q++) vis = depth_passes(zq[q], key_f64(*aq[q]));
+        if (!vis && nq > 0) {
+            unsigned long long k0 = *a0, k1 = nq > 1 ? *a1 : 0ull, k2 = nq > 2 ? *a2 : 0ull;
+            vis = depth_passes(z0, key_f64(k0)) | (nq > 1 && depth_passes(z1, key_f64(k1))) |
+                  (nq > 2 && depth_passes(z2, key_f64(k2)));
+        }
         if (vis) flags[t] = 1;
     }
 }
@@ -522,6 +570,7 @@ __global__ void __launch_bounds__(256) k_raster_vis_tiles(const SmallRec* __rest
                                                           const TriSetup* __restrict__ large,
                                                           const int2* __restrict__ tiles, int W,
                                                           const unsigned long long* __restrict__ depth,
+                                                          const unsigned long long* __restrict__ hiz, int htx,
                                                           unsigned char* __restrict__ flags,
                                                           const fa_dstat* __restrict__ st, int max_tiles,
                                                           int max_large, int phase) {
@@ -548,17 +597,37 @@ __global__ void __launch_bounds__(256) k_raster_vis_tiles(const SmallRec* __rest
             load_rec(recs + rec.x, f, t);
             int seen = 0;
             if (lane == 0) seen = *(volatile unsigned char*)(flags + t);
-            if (__shfl_sync(0xffffffffu, seen, 0)) continue;  // already visible (warp-uniform)
+            if (__shfl_sync(0xffffffffu, seen, 0)) {
+#ifdef FA_HIZ_STATS
+                if (lane == 0) atomicAdd(&g_hiz_stats[4], 1ull);
+#endif
+                continue;  // already visible (warp-uniform)
+            }
             int centre = tile_centre(f.min_x, f.max_x, f.min_y, f.max_y);
             if (phase == 0) rec.y = centre;
             else if (rec.y == centre) continue;
+            {
+                // hierarchical-Z test of the tile's rectangle (warp-uniform)
+                int ntx = (f.max_x - f.min_x + 1 + TILE_W - 1) / TILE_W;
+                int xa = f.min_x + (rec.y % ntx) * TILE_W, ya = f.min_y + (rec.y / ntx) * TILE_H;
+                int xb = min(xa + TILE_W - 1, f.max_x), yb = min(ya + TILE_H - 1, f.max_y);
+#ifdef FA_HIZ_STATS
+                if (lane == 0) atomicAdd(&g_hiz_stats[2], 1ull);
+#endif
+                if (hiz_rejects(hiz, htx, xa, xb, ya, yb, depth_lower_bound(f, xa, xb, ya, yb))) {
+#ifdef FA_HIZ_STATS
+                    if (lane == 0) atomicAdd(&g_hiz_stats[3], 1ull);
+#endif
+                    continue;
+                }
+            }
             int x, y0;
             tile_lane_origin(f.min_x, f.max_x, f.min_y, rec.y, x, y0);
             bool vis = false;
             if (x <= f.max_x) {
                 // evaluate the lane's 4 samples, then issue their depth
                 // loads together (static indices keep the arrays in registers)
-                double px = (double)x + 0.5;
+                const ColTerms ct = col_terms(f, (double)x + 0.5);
                 double zq[TILE_H / 2];
                 bool in[TILE_H / 2];
                 unsigned long long kq[TILE_H / 2];
@@ -566,8 +635,8 @@ __global__ void __launch_bounds__(256) k_raster_vis_tiles(const SmallRec* __rest
                 for (int k = 0; k < TILE_H / 2; k++) {
                     int y = y0 + 2 * k;
                     double py = (double)y + 0.5;
-                    in[k] = y <= f.max_y && sample_inside3(f, px, py);
-                    zq[k] = in[k] ? sample_depth3(f, px, py) : 0.0;
+                    in[k] = y <= f.max_y && inside_col(f, ct, py);
+                    zq[k] = in[k] ? depth_col(f, ct, py) : 0.0;
                 }
 #pragma unroll
                 for (int k = 0; k < TILE_H / 2; k++)
@@ -624,14 +693,14 @@ __global__ void __launch_bounds__(256) k_raster_vis_tiles(const SmallRec* __rest
 
 // ---- host launchers -------------------------------------------------------
 void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* clip, double4* scr, int W, int H,
-                          int* vmin, unsigned long long* depth, long long npx, unsigned char* flags, int T,
-                          cudaStream_t s) {
+                          int* vmin, unsigned long long* depth, unsigned long long* wid, long long npx,
+                          unsigned char* flags, int T, cudaStream_t s) {
     long long work = V;
     if (depth && npx / 2 > work) work = npx / 2;
     int nflag32 = flags ? (T + 3) / 4 : 0;
     if (nflag32 > work) work = nflag32;
     k_frame_init<<<fa_grid(work, 256, FA_NUM_SMS * 8), 256, 0, s>>>(
-        pos, V, vp, clip, scr, W, H, vmin, depth, npx, reinterpret_cast<unsigned int*>(flags), nflag32);
+        pos, V, vp, clip, scr, W, H, vmin, depth, wid, npx, reinterpret_cast<unsigned int*>(flags), nflag32);
 }
 
 // fork `side` off `s` (side waits for everything issued on s so far)
@@ -645,22 +714,23 @@ static void fork_to(cudaStream_t s, cudaStream_t side, cudaEvent_t ev) {
 // -> large tiles on side}, joined back into s.  Both branches only lower
 // depth keys with atomicMin, so their order does not matter.
 int fa_launch_depth_pass(bool write_depth, const double4* clip, const double4* scr, const int* tris, int T, int W,
-                         int H, int cull, unsigned long long* depth, SmallRec* small_rec, int* clip_list,
-                         TriSetup* large, int max_large, int2* tiles, int max_tiles, fa_dstat* st, cudaStream_t s,
-                         cudaStream_t side, cudaEvent_t ev_fork, cudaEvent_t ev_join) {
+                         int H, int cull, unsigned long long* depth, unsigned long long* wid, SmallRec* small_rec,
+                         int* clip_list, TriSetup* large, int max_large, int2* tiles, int max_tiles, fa_dstat* st,
+                         cudaStream_t s, cudaStream_t side, cudaEvent_t ev_fork, cudaEvent_t ev_join) {
     k_raster_setup<<<fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s>>>(scr, tris, T, W, H, cull, small_rec, clip_list,
                                                                     tiles, max_tiles, st);
     cudaStream_t b = side ? side : s;
     if (side) fork_to(s, side, ev_fork);
     if (write_depth) {
-        k_raster_clipped<true><<<FA_NUM_SMS * 2, 256, 0, b>>>(clip, tris, W, H, cull, clip_list, depth, large,
+        k_raster_clipped<true><<<FA_NUM_SMS * 2, 256, 0, b>>>(clip, tris, W, H, cull, clip_list, depth, wid, large,
                                                               max_large, tiles, max_tiles, st);
-        k_raster_depth_tiles<<<FA_NUM_SMS * 8, 256, 0, b>>>(small_rec, large, tiles, W, depth, st, max_tiles);
+        k_raster_depth_tiles<<<FA_NUM_SMS * 8, 256, 0, b>>>(small_rec, large, tiles, W, depth, wid, st, max_tiles);
         // small unclipped triangles (warp-cooperative)
-        fa_launch_small_coop(false, small_rec, T, W, depth, nullptr, st, s);
+        k_small_coop<<<fa_grid((long long)T, COOP_WARPS * 32 * 2, FA_NUM_SMS * 6), COOP_WARPS * 32, 0, s>>>(
+            small_rec, W, depth, wid, st);
     } else {
-        k_raster_clipped<false><<<FA_NUM_SMS * 2, 256, 0, b>>>(clip, tris, W, H, cull, clip_list, depth, large,
-                                                               max_large, tiles, max_tiles, st);
+        k_raster_clipped<false><<<FA_NUM_SMS * 2, 256, 0, b>>>(clip, tris, W, H, cull, clip_list, depth, nullptr,
+                                                               large, max_large, tiles, max_tiles, st);
     }
     if (side) fork_to(side, s, ev_join);
     return write_depth ? 4 : 2;
@@ -669,31 +739,26 @@ int fa_launch_depth_pass(bool write_depth, const double4* clip, const double4* s
 // Visibility pass: small records on s || large tiles (centre tile first,
 // then the rest of the still-invisible ones) on side.
 int fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const int2* tiles, int max_tiles,
-                         int max_large, int T, int W, const unsigned long long* depth, unsigned char* flags,
-                         const fa_dstat* st, cudaStream_t s, cudaStream_t side, cudaEvent_t ev_fork,
-                         cudaEvent_t ev_join) {
+                         int max_large, int T, int W, const unsigned long long* depth, const unsigned long long* hiz,
+                         unsigned char* flags, const fa_dstat* st, cudaStream_t s, cudaStream_t side,
+                         cudaEvent_t ev_fork, cudaEvent_t ev_join) {
     cudaStream_t b = side ? side : s;
+    const int htx = fa_hiz_dim(W);
     if (side) fork_to(s, side, ev_fork);
-    k_raster_vis_tiles<<<FA_NUM_SMS * 8, 256, 0, b>>>(small_rec, T, large, tiles, W, depth, flags, st, max_tiles,
-                                                      max_large, 0);
-    k_raster_vis_tiles<<<FA_NUM_SMS * 8, 256, 0, b>>>(small_rec, T, large, tiles, W, depth, flags, st, max_tiles,
-                                                      max_large, 1);
-    k_raster_vis_small<<<fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s>>>(small_rec, W, depth, flags, st);
+    k_raster_vis_tiles<<<FA_NUM_SMS * 8, 256, 0, b>>>(small_rec, T, large, tiles, W, depth, hiz, htx, flags, st,
+                                                      max_tiles, max_large, 0);
+    k_raster_vis_tiles<<<FA_NUM_SMS * 8, 256, 0, b>>>(small_rec, T, large, tiles, W, depth, hiz, htx, flags, st,
+                                                      max_tiles, max_large, 1);
+    k_raster_vis_small<<<fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s>>>(small_rec, W, depth, hiz, htx, flags, st);
     if (side) fork_to(side, s, ev_join);
     return 3;
 }
 
-void fa_launch_small_coop(bool vis, const SmallRec* recs, int T, int W, unsigned long long* depth,
-                          unsigned char* flags, const fa_dstat* st, cudaStream_t s) {
-    int grid = fa_grid((long long)T, COOP_WARPS * 32 * 2, FA_NUM_SMS * 6);
-    if (vis)
-        k_small_coop<true><<<grid, COOP_WARPS * 32, 0, s>>>(recs, W, depth, flags, st);
-    else
-        k_small_coop<false><<<grid, COOP_WARPS * 32, 0, s>>>(recs, W, depth, flags, st);
-}
-
-void fa_launch_count_finite(const unsigned long long* depth, long long npx, fa_dstat* st, cudaStream_t s) {
-    k_count_finite<<<fa_grid(npx / 2 + 1, 256, FA_NUM_SMS * 4), 256, 0, s>>>(depth, npx, st);
+void fa_launch_depth_hiz(const unsigned long long* depth, const unsigned long long* wid, int W, int H,
+                         unsigned long long* hiz, unsigned char* flags, fa_dstat* st, cudaStream_t s) {
+    int htx = fa_hiz_dim(W), hty = fa_hiz_dim(H);
+    k_depth_hiz<<<fa_grid((long long)htx * FA_HIZ * hty, 256, FA_NUM_SMS * 8), 256, 0, s>>>(depth, wid, W, H, hiz, htx,
+                                                                                           hty, flags, st);
 }
 
 void fa_launch_decode_depth(const unsigned long long* keys, double* out, long long n, cudaStream_t s) {

@@ -504,6 +504,104 @@ __device__ __forceinline__ double sample_depth3(const Setup3& s, double px, doub
     return s.zmean;
 }
 
+// ---- hoisted sample evaluation -------------------------------------------
+// e_i = dx_i*(py - ay_i) - dy_i*(px - ax_i) and z = (p0z + gx*(px - p0x)) +
+// gy*(py - p0y) are evaluated with exactly the operations above; only the
+// terms that depend on one coordinate are computed once per row (or per
+// column) instead of once per sample, and the three edges are combined
+// without short-circuiting so their DP chains overlap.
+struct RowTerms {
+    double r0, r1, r2;  // dx_i * (py - ay_i)
+    double zr;          // gy * (py - p0y)
+};
+
+__device__ __forceinline__ RowTerms row_terms(const Setup3& s, double py) {
+    RowTerms r;
+    r.r0 = __dmul_rn(s.dx0, __dsub_rn(py, s.ay0));
+    r.r1 = __dmul_rn(s.dx1, __dsub_rn(py, s.ay1));
+    r.r2 = __dmul_rn(s.dx2, __dsub_rn(py, s.ay2));
+    r.zr = __dmul_rn(s.gy, __dsub_rn(py, s.p0y));
+    return r;
+}
+
+__device__ __forceinline__ bool inside_row(const Setup3& s, const RowTerms& r, double px) {
+    double e0 = __dsub_rn(r.r0, __dmul_rn(s.dy0, __dsub_rn(px, s.ax0)));
+    double e1 = __dsub_rn(r.r1, __dmul_rn(s.dy1, __dsub_rn(px, s.ax1)));
+    double e2 = __dsub_rn(r.r2, __dmul_rn(s.dy2, __dsub_rn(px, s.ax2)));
+    bool k0 = (s.incl & 1) ? (e0 >= 0) : (e0 > 0);
+    bool k1 = (s.incl & 2) ? (e1 >= 0) : (e1 > 0);
+    bool k2 = (s.incl & 4) ? (e2 >= 0) : (e2 > 0);
+    return k0 & k1 & k2;
+}
+
+__device__ __forceinline__ double depth_row(const Setup3& s, const RowTerms& r, double px) {
+    if (s.use_plane) return __dadd_rn(__dadd_rn(s.p0z, __dmul_rn(s.gx, __dsub_rn(px, s.p0x))), r.zr);
+    return s.zmean;
+}
+
+struct ColTerms {
+    double c0, c1, c2;  // dy_i * (px - ax_i)
+    double zc;          // p0z + gx * (px - p0x)
+};
+
+__device__ __forceinline__ ColTerms col_terms(const Setup3& s, double px) {
+    ColTerms c;
+    c.c0 = __dmul_rn(s.dy0, __dsub_rn(px, s.ax0));
+    c.c1 = __dmul_rn(s.dy1, __dsub_rn(px, s.ax1));
+    c.c2 = __dmul_rn(s.dy2, __dsub_rn(px, s.ax2));
+    c.zc = __dadd_rn(s.p0z, __dmul_rn(s.gx, __dsub_rn(px, s.p0x)));
+    return c;
+}
+
+__device__ __forceinline__ bool inside_col(const Setup3& s, const ColTerms& c, double py) {
+    double e0 = __dsub_rn(__dmul_rn(s.dx0, __dsub_rn(py, s.ay0)), c.c0);
+    double e1 = __dsub_rn(__dmul_rn(s.dx1, __dsub_rn(py, s.ay1)), c.c1);
+    double e2 = __dsub_rn(__dmul_rn(s.dx2, __dsub_rn(py, s.ay2)), c.c2);
+    bool k0 = (s.incl & 1) ? (e0 >= 0) : (e0 > 0);
+    bool k1 = (s.incl & 2) ? (e1 >= 0) : (e1 > 0);
+    bool k2 = (s.incl & 4) ? (e2 >= 0) : (e2 > 0);
+    return k0 & k1 & k2;
+}
+
+__device__ __forceinline__ double depth_col(const Setup3& s, const ColTerms& c, double py) {
+    if (s.use_plane) return __dadd_rn(c.zc, __dmul_rn(s.gy, __dsub_rn(py, s.p0y)));
+    return s.zmean;
+}
+
+// ---- hierarchical-Z rejection for the visibility pass ----------------------
+// Lower bound of the sampled depth over the pixel rectangle [xa,xb]x[ya,yb]:
+// the plane is linear, so its minimum over the rectangle's sample positions is
+// at a corner; the computed z (three roundings, charts.py:266 order) differs
+// from the exact plane value by < 8 ulp of |p0z| + |gx dx| + |gy dy|, far below
+// the 1e-12 relative margin subtracted here.
+__device__ __forceinline__ double depth_lower_bound(const Setup3& f, int xa, int xb, int ya, int yb) {
+    if (!f.use_plane) return f.zmean;
+    double ta = f.gx * (((double)xa + 0.5) - f.p0x), tb = f.gx * (((double)xb + 0.5) - f.p0x);
+    double ua = f.gy * (((double)ya + 0.5) - f.p0y), ub = f.gy * (((double)yb + 0.5) - f.p0y);
+    double lo = f.p0z + fmin(ta, tb) + fmin(ua, ub);
+    double mag = fabs(f.p0z) + fmax(fabs(ta), fabs(tb)) + fmax(fabs(ua), fabs(ub));
+    return lo - 1e-12 * mag;
+}
+
+// True when no sample in the rectangle can pass z <= stored + 1e-6 max(1,|stored|)
+// against the final depth: for every 8x8 tile it touches, zlb exceeds the
+// threshold of the tile's largest stored depth (the threshold is monotone in
+// the stored depth, so that bounds every pixel of the tile).  NaN never rejects.
+__device__ __forceinline__ bool hiz_tile_rejects(unsigned long long k, double zlb) {
+    if (k == 0) return true;  // no coverable pixel in this tile
+    double stored = key_f64(k), a = fabs(stored);
+    double thr = __dadd_rn(stored, __dmul_rn(FA_DEPTH_EPSILON, 1.0 > a ? 1.0 : a));  // as depth_passes
+    return zlb > thr;
+}
+
+__device__ __forceinline__ bool hiz_rejects(const unsigned long long* __restrict__ hiz, int htx, int xa, int xb,
+                                            int ya, int yb, double zlb) {
+    for (int ty = ya / FA_HIZ; ty <= yb / FA_HIZ; ty++)
+        for (int tx = xa / FA_HIZ; tx <= xb / FA_HIZ; tx++)
+            if (!hiz_tile_rejects(__ldg(hiz + ty * htx + tx), zlb)) return false;
+    return true;
+}
+
 __device__ __forceinline__ void setup3_to_generic(const Setup3& a, int t, TriSetup& s) {
     s.tri = t;
     s.n = 3;
