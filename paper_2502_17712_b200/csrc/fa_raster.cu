@@ -331,11 +331,6 @@ __device__ __forceinline__ void tile_lane_origin(int min_x, int max_x, int min_y
     y0 = min_y + (ti / tx) * TILE_H + (lane >> 4);
 }
 
-__device__ __forceinline__ int tile_centre(int min_x, int max_x, int min_y, int max_y) {
-    int bw = max_x - min_x + 1;
-    int tx = (bw + TILE_W - 1) / TILE_W;
-    return ((max_y - min_y + 1) / 2 / TILE_H) * tx + (bw / 2) / TILE_W;
-}
 
 // ---- pass 1 large: one warp per 16x8 tile --------------------------------
 // Tile records: x >= 0 indexes a compact unclipped record (every lane loads
@@ -573,23 +568,23 @@ __global__ void __launch_bounds__(256) k_raster_vis_tiles(const SmallRec* __rest
                                                           const unsigned long long* __restrict__ hiz, int htx,
                                                           unsigned char* __restrict__ flags,
                                                           const fa_dstat* __restrict__ st, int max_tiles,
-                                                          int max_large, int phase) {
-    // phase 0: the tile at the centre of each large triangle's bbox (most
-    // visible triangles are decided there); phase 1: every other tile of the
-    // triangles that are still not visible.  Phase-0 items are the compact
-    // records (stored downward from index T) followed by the generic setups.
+                                                          int max_large) {
+    // Items: every 16x8 tile of the large triangles, then the generic setups
+    // (only the small clipped windows, which have no tiles, are sampled
+    // there).  Triangles already flagged — pass-1 pixel winners, or decided by
+    // an earlier tile — are skipped; tiles the hierarchical Z rejects too.
     __shared__ TriSetup sm[8];
     int warp = threadIdx.x >> 5, lane = lane_id();
     int nwarps = gridDim.x * 8;
-    int n3 = st->n_large3;
-    int n_items = phase == 0 ? n3 + min(st->n_large, max_large) : min(st->n_tiles, max_tiles);
+    const int n_tiles = min(st->n_tiles, max_tiles);
+    const int n_items = n_tiles + min(st->n_large, max_large);
     for (int w = blockIdx.x * 8 + warp; w < n_items; w += nwarps) {
         int2 rec;
-        if (phase == 0) {
-            rec.x = w < n3 ? T - w : -(w - n3) - 1;
-            rec.y = -1;
-        } else {
+        if (w < n_tiles) {
             rec = tiles[w];
+        } else {
+            rec.x = -(w - n_tiles) - 1;
+            rec.y = -1;
         }
         if (rec.x >= 0) {
             Setup3 f;
@@ -603,9 +598,6 @@ __global__ void __launch_bounds__(256) k_raster_vis_tiles(const SmallRec* __rest
 #endif
                 continue;  // already visible (warp-uniform)
             }
-            int centre = tile_centre(f.min_x, f.max_x, f.min_y, f.max_y);
-            if (phase == 0) rec.y = centre;
-            else if (rec.y == centre) continue;
             {
                 // hierarchical-Z test of the tile's rectangle (warp-uniform)
                 int ntx = (f.max_x - f.min_x + 1 + TILE_W - 1) / TILE_W;
@@ -657,8 +649,9 @@ __global__ void __launch_bounds__(256) k_raster_vis_tiles(const SmallRec* __rest
         const TriSetup& s = sm[warp];
         int bw = s.max_x - s.min_x + 1, bh = s.max_y - s.min_y + 1;
         bool vis = false;
-        if (bw * bh <= FA_SMALL_PX) {
-            // small clipped polygon (no tiles): the warp covers its window in phase 0
+        if (rec.y < 0) {
+            // generic setup item: only small clipped windows (no tiles) are sampled here
+            if (bw * bh > FA_SMALL_PX) continue;
             for (int k = lane; k < bw * bh && !vis; k += 32) {
                 int dy = k / bw;
                 int iy = s.min_y + dy, ix = s.min_x + (k - dy * bw);
@@ -670,9 +663,6 @@ __global__ void __launch_bounds__(256) k_raster_vis_tiles(const SmallRec* __rest
             continue;
         }
         int tx = (bw + TILE_W - 1) / TILE_W;
-        int centre = ((s.max_y - s.min_y + 1) / 2 / TILE_H) * tx + (bw / 2) / TILE_W;
-        if (phase == 0) rec.y = centre;
-        else if (rec.y == centre) continue;
         int x = s.min_x + (rec.y % tx) * TILE_W + (lane & 15);
         int y0 = s.min_y + (rec.y / tx) * TILE_H + (lane >> 4);
         if (x <= s.max_x) {
@@ -736,8 +726,8 @@ int fa_launch_depth_pass(bool write_depth, const double4* clip, const double4* s
     return write_depth ? 4 : 2;
 }
 
-// Visibility pass: small records on s || large tiles (centre tile first,
-// then the rest of the still-invisible ones) on side.
+// Visibility pass: small records on s || large tiles + small clipped windows
+// on side.  Both only set flags, which k_depth_hiz seeded with the winners.
 int fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const int2* tiles, int max_tiles,
                          int max_large, int T, int W, const unsigned long long* depth, const unsigned long long* hiz,
                          unsigned char* flags, const fa_dstat* st, cudaStream_t s, cudaStream_t side,
@@ -746,12 +736,10 @@ int fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const
     const int htx = fa_hiz_dim(W);
     if (side) fork_to(s, side, ev_fork);
     k_raster_vis_tiles<<<FA_NUM_SMS * 8, 256, 0, b>>>(small_rec, T, large, tiles, W, depth, hiz, htx, flags, st,
-                                                      max_tiles, max_large, 0);
-    k_raster_vis_tiles<<<FA_NUM_SMS * 8, 256, 0, b>>>(small_rec, T, large, tiles, W, depth, hiz, htx, flags, st,
-                                                      max_tiles, max_large, 1);
+                                                      max_tiles, max_large);
     k_raster_vis_small<<<fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s>>>(small_rec, W, depth, hiz, htx, flags, st);
     if (side) fork_to(side, s, ev_join);
-    return 3;
+    return 2;
 }
 
 void fa_launch_depth_hiz(const unsigned long long* depth, const unsigned long long* wid, int W, int H,
