@@ -115,23 +115,37 @@ __global__ void k_encode_depth(const double* __restrict__ in, unsigned long long
 //                       descriptors the warp writes together,
 //   anything else    -> index into `clip_list` for k_raster_clipped.
 // Nothing is rasterized here, so no lane waits on another's pixels.
-__global__ void __launch_bounds__(256) k_raster_setup(const double4* __restrict__ scr, const int* __restrict__ tris,
+#define SETUP_WARPS 8
+__global__ void __launch_bounds__(SETUP_WARPS * 32) k_raster_setup(const double4* __restrict__ scr,
+                                                      const int* __restrict__ tris,
                                                       int T, int W, int H, int cull,
                                                       SmallRec* __restrict__ recs, int* __restrict__ clip_list,
                                                       int2* __restrict__ tiles, int max_tiles,
                                                       fa_dstat* __restrict__ st) {
-    const int lane = lane_id();
-    const int wpb = blockDim.x >> 5;
-    const int total_warps = gridDim.x * wpb;
+    // per-warp counts -> per-warp bases; one atomic per counter per block step
+    // (a same-address atomic per warp serialises ~30K times in the L2)
+    __shared__ int s_cnt[4][SETUP_WARPS];
+    __shared__ int s_base[4][SETUP_WARPS];
+    const int lane = lane_id(), warp = threadIdx.x >> 5;
     const bool rec_ok = W <= 32767 && H <= 32767;
     const unsigned lt_mask = (1u << lane) - 1u;
-    for (int base = (blockIdx.x * wpb + (threadIdx.x >> 5)) * 32; base < T; base += total_warps * 32) {
-        const int t = base + lane;
+    const int step = gridDim.x * SETUP_WARPS * 32;
+    // the next step's vertex indices are loaded one step ahead, so each step
+    // waits for one round trip (the screen-record gathers), not two
+    int na = 0, nb = 0, nc = 0;
+    {
+        const int t0 = blockIdx.x * SETUP_WARPS * 32 + warp * 32 + lane;
+        if (t0 < T) na = __ldg(tris + 3 * t0), nb = __ldg(tris + 3 * t0 + 1), nc = __ldg(tris + 3 * t0 + 2);
+    }
+    for (int bbase = blockIdx.x * SETUP_WARPS * 32; bbase < T; bbase += step) {
+        const int t = bbase + warp * 32 + lane;
+        const int ia = na, ib = nb, ic = nc;
+        if (t + step < T)
+            na = __ldg(tris + 3 * (t + step)), nb = __ldg(tris + 3 * (t + step) + 1), nc = __ldg(tris + 3 * (t + step) + 2);
         Setup3 f;
         int kind = 0;  // 0 none, 1 small record, 2 large record, 3 generic path
         int nt = 0;
         if (t < T) {
-            int ia = __ldg(tris + 3 * t), ib = __ldg(tris + 3 * t + 1), ic = __ldg(tris + 3 * t + 2);
             int r3 = tri_setup3s(scr, ia, ib, ic, W, H, cull != 0, f);
             if (r3 == 2 || (r3 == 1 && !rec_ok)) {
                 kind = 3;
@@ -148,35 +162,38 @@ __global__ void __launch_bounds__(256) k_raster_setup(const double4* __restrict_
         const unsigned m1 = __ballot_sync(0xffffffffu, kind == 1);
         const unsigned m2 = __ballot_sync(0xffffffffu, kind == 2);
         const unsigned m3 = __ballot_sync(0xffffffffu, kind == 3);
-        if (m1) {
-            int b = 0;
-            if (lane == 0) b = atomicAdd(&st->n_small3, __popc(m1));
-            b = __shfl_sync(0xffffffffu, b, 0);
-            if (kind == 1) store_rec(f, t, recs + b + __popc(m1 & lt_mask));
+        int incl = nt;  // inclusive scan of the warp's tile counts
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
         }
-        if (m3) {
-            int b = 0;
-            if (lane == 0) b = atomicAdd(&st->n_clip, __popc(m3));
-            b = __shfl_sync(0xffffffffu, b, 0);
-            if (kind == 3) clip_list[b + __popc(m3 & lt_mask)] = t;
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        if (lane == 0) {
+            s_cnt[0][warp] = __popc(m1);
+            s_cnt[1][warp] = __popc(m2);
+            s_cnt[2][warp] = __popc(m3);
+            s_cnt[3][warp] = total;
         }
+        __syncthreads();
+        if (threadIdx.x < 4) {
+            const int c = threadIdx.x;
+            int sum = 0;
+            for (int w = 0; w < SETUP_WARPS; w++) sum += s_cnt[c][w];
+            int* ctr = c == 0 ? &st->n_small3 : c == 1 ? &st->n_large3 : c == 2 ? &st->n_clip : &st->n_tiles;
+            int b = sum ? atomicAdd(ctr, sum) : 0;
+            for (int w = 0; w < SETUP_WARPS; w++) {
+                s_base[c][w] = b;
+                b += s_cnt[c][w];
+            }
+        }
+        __syncthreads();
+        if (m1 && kind == 1) store_rec(f, t, recs + s_base[0][warp] + __popc(m1 & lt_mask));
+        if (m3 && kind == 3) clip_list[s_base[2][warp] + __popc(m3 & lt_mask)] = t;
         if (m2) {
             // large records are stored downward from index T (small + large
             // records <= T, so the two ends never meet)
-            int incl = nt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                int y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            int total = __shfl_sync(0xffffffffu, incl, 31);
-            int rb = 0, tb = 0;
-            if (lane == 0) {
-                rb = atomicAdd(&st->n_large3, __popc(m2));
-                tb = atomicAdd(&st->n_tiles, total);
-            }
-            rb = __shfl_sync(0xffffffffu, rb, 0);
-            tb = __shfl_sync(0xffffffffu, tb, 0);
+            const int rb = s_base[1][warp], tb = s_base[3][warp];
             int ri = T - (rb + __popc(m2 & lt_mask));
             if (kind == 2) store_rec(f, t, recs + ri);
             if (tb + total > max_tiles && lane == 0) atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW);
@@ -707,7 +724,7 @@ int fa_launch_depth_pass(bool write_depth, const double4* clip, const double4* s
                          int H, int cull, unsigned long long* depth, unsigned long long* wid, SmallRec* small_rec,
                          int* clip_list, TriSetup* large, int max_large, int2* tiles, int max_tiles, fa_dstat* st,
                          cudaStream_t s, cudaStream_t side, cudaEvent_t ev_fork, cudaEvent_t ev_join) {
-    k_raster_setup<<<fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s>>>(scr, tris, T, W, H, cull, small_rec, clip_list,
+    k_raster_setup<<<fa_grid(T, 256, FA_NUM_SMS * 4), 256, 0, s>>>(scr, tris, T, W, H, cull, small_rec, clip_list,
                                                                     tiles, max_tiles, st);
     cudaStream_t b = side ? side : s;
     if (side) fork_to(s, side, ev_fork);
