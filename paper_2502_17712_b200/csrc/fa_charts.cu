@@ -211,57 +211,50 @@ __global__ void k_uf_init_vmin(const int* __restrict__ tris, const int* __restri
     }
 }
 
-// Min-label propagation round before hooking (fire-and-forget, no CAS):
-//   A: vmin[v] = min over incident visible t of label[t]   (RED.MIN)
-//   B: label[t] = min(label[t], vmin[v0..2], label[label[t]])
-// Every value written is a visible triangle of the same component with an
-// index <= the node's own, so label stays a valid min-rooted forest and
-// vmin[v] stays a member of v's component for the hooking pass.
-__global__ void k_uf_prop_a(const int* __restrict__ tris, const int* __restrict__ vis_list, int* __restrict__ vmin,
-                            const int* __restrict__ label, const fa_dstat* __restrict__ st) {
+
+// Multi-way hooking: t joins the sets of vmin[v0..2] in one step.  The four
+// finds (from t's parent and from the three vertex minima) advance together,
+// one parent load each per round, so the dependent chain is as long as the
+// deepest path rather than the sum of three unions; every root other than
+// the smallest is then hooked to it with independent CASes.  A CAS that
+// loses a race (the root got a new parent) sends that node up again.
+// Hooking to a node m that has meanwhile stopped being a root is still a
+// valid union (parent[r] = m < r keeps the min-rooted forest).
+__global__ void k_hook_multi(const int* __restrict__ tris, const int* __restrict__ vis_list,
+                             const int* __restrict__ vmin, int* label, const fa_dstat* __restrict__ st) {
     int n = st->n_vis;
     int stride = gridDim.x * blockDim.x;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
         int t = vis_list[k];
-        int l = label[t];
-#pragma unroll
-        for (int j = 0; j < 3; j++) {
-            int v = __ldg(tris + 3 * t + j);
-            if (*(volatile int*)(vmin + v) > l) atomicMin(vmin + v, l);
+        int r1 = vmin[__ldg(tris + 3 * t)], r2 = vmin[__ldg(tris + 3 * t + 1)], r3 = vmin[__ldg(tris + 3 * t + 2)];
+        int r0 = label[t];
+        // lock-free: every lost CAS moves a node strictly down, so this ends
+        while (true) {
+            // joint find: one parent load per node per round
+            while (true) {
+                int p0 = label[r0], p1 = label[r1], p2 = label[r2], p3 = label[r3];
+                bool roots = (p0 == r0) & (p1 == r1) & (p2 == r2) & (p3 == r3);
+                r0 = p0;
+                r1 = p1;
+                r2 = p2;
+                r3 = p3;
+                if (roots) break;
+            }
+            int m = min(min(r0, r1), min(r2, r3));
+            if (r0 == m && r1 == m && r2 == m && r3 == m) break;
+            int o0 = r0 != m ? atomicCAS(label + r0, r0, m) : m;
+            int o1 = r1 != m && r1 != r0 ? atomicCAS(label + r1, r1, m) : m;
+            int o2 = r2 != m && r2 != r0 && r2 != r1 ? atomicCAS(label + r2, r2, m) : m;
+            int o3 = r3 != m && r3 != r0 && r3 != r1 && r3 != r2 ? atomicCAS(label + r3, r3, m) : m;
+            bool ok = (o0 == r0 || o0 == m) && (o1 == r1 || o1 == m) && (o2 == r2 || o2 == m) &&
+                      (o3 == r3 || o3 == m);
+            if (ok) break;
+            // lost races: continue from the fresh parents (all still ancestors)
+            if (o0 != r0 && o0 != m) r0 = o0;
+            if (o1 != r1 && o1 != m) r1 = o1;
+            if (o2 != r2 && o2 != m) r2 = o2;
+            if (o3 != r3 && o3 != m) r3 = o3;
         }
-    }
-}
-
-__global__ void k_uf_prop_b(const int* __restrict__ tris, const int* __restrict__ vis_list,
-                            const int* __restrict__ vmin, int* label, const fa_dstat* __restrict__ st) {
-    int n = st->n_vis;
-    int stride = gridDim.x * blockDim.x;
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
-        int t = vis_list[k];
-        int m = label[t];
-#pragma unroll
-        for (int j = 0; j < 3; j++) m = min(m, vmin[__ldg(tris + 3 * t + j)]);
-        m = min(m, *(volatile int*)(label + m));
-        label[t] = m;
-    }
-}
-
-#ifndef FA_UF_PROP_ROUNDS
-#define FA_UF_PROP_ROUNDS 1
-#endif
-
-__global__ void k_hook_vertex(const int* __restrict__ tris, const int* __restrict__ vis_list,
-                              const int* __restrict__ vmin, int* label, const fa_dstat* __restrict__ st) {
-    int n = st->n_vis;
-    int stride = gridDim.x * blockDim.x;
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
-        int t = vis_list[k];
-        int u0 = vmin[__ldg(tris + 3 * t)], u1 = vmin[__ldg(tris + 3 * t + 1)], u2 = vmin[__ldg(tris + 3 * t + 2)];
-        // t's current parent is an ancestor forever: a union with it is implied
-        int p = *(volatile int*)(label + t);
-        if (u0 != p && u0 != t) uf_union(label, t, u0);
-        if (u1 != p && u1 != t && u1 != u0) uf_union(label, t, u1);
-        if (u2 != p && u2 != t && u2 != u0 && u2 != u1) uf_union(label, t, u2);
     }
 }
 
@@ -412,12 +405,8 @@ int fa_launch_uf_vertex(const int* tris, const int* vis_list, int* vmin, int* la
                         cudaStream_t s) {
     k_vmin<<<uf_grid(T), 256, 0, s>>>(tris, vis_list, vmin, st);
     k_uf_init_vmin<<<uf_grid(T), 256, 0, s>>>(tris, vis_list, vmin, label, st);
-    for (int r = 0; r < FA_UF_PROP_ROUNDS; r++) {
-        k_uf_prop_a<<<uf_grid(T), 256, 0, s>>>(tris, vis_list, vmin, label, st);
-        k_uf_prop_b<<<uf_grid(T), 256, 0, s>>>(tris, vis_list, vmin, label, st);
-    }
-    k_hook_vertex<<<uf_grid(T), 256, 0, s>>>(tris, vis_list, vmin, label, st);
-    return 3 + 2 * FA_UF_PROP_ROUNDS;
+    k_hook_multi<<<uf_grid(T), 256, 0, s>>>(tris, vis_list, vmin, label, st);
+    return 3;
 }
 
 void fa_launch_uf_edges(const int* adjacency, const unsigned char* flags, const int* vis_list, int* label, int T,
