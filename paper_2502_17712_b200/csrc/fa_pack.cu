@@ -71,8 +71,9 @@ __device__ __forceinline__ void snap_scale(long long& num, long long& den, long 
     unsigned long long dd = (unsigned long long)den * (unsigned long long)(omega + m);
     if (num >= 0 && num < (1ll << 31) && omega < (1ll << 31) && (nw >> 40) == 0 && den > 0 &&
         den < (1ll << 31) && (omega + m) < (1ll << 32)) {
-        // common case: numerator fits in 64 bits, one u64 division
-        fn = (long long)((nw << FA_SCALE_GRID_BITS) / dd);
+        // common case: numerator fits in 64 bits, quotient < 2^25
+        const unsigned long long nn = nw << FA_SCALE_GRID_BITS;
+        fn = dd < (1ull << 60) ? (long long)floor_div_u64_small_q(nn, dd) : (long long)(nn / dd);
     } else {
         u128 n = mul64((unsigned long long)num, (unsigned long long)omega);  // < 2^116 overall after shift
         n = shl128(n, FA_SCALE_GRID_BITS);
@@ -261,9 +262,48 @@ __global__ void __launch_bounds__(SORT_THREADS) k_orient_sort(const long long* _
 // ============================================================================
 struct PackSmem {
     long long red[33];
+    long long red2[33];
     int red_i[32];
     int flag;
 };
+
+// block max of two values at once (one pair of barriers); red/red2 hold 33
+__device__ __forceinline__ void block_max2_ll(long long& a, long long& b, long long* red, long long* red2) {
+    int lane = lane_id(), wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    a = warp_max_ll(a);
+    b = warp_max_ll(b);
+    if (lane == 0) {
+        red[wid] = a;
+        red2[wid] = b;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        long long x = lane < nw ? red[lane] : (long long)0x8000000000000000ll;
+        long long y = lane < nw ? red2[lane] : (long long)0x8000000000000000ll;
+        x = warp_max_ll(x);
+        y = warp_max_ll(y);
+        if (lane == 0) {
+            red[32] = x;
+            red2[32] = y;
+        }
+    }
+    __syncthreads();
+    a = red[32];
+    b = red2[32];
+}
+
+// boxes per thread kept in registers by the fold rounds (n <= PK_KREG * PK_THREADS)
+#define PK_KREG 4
+
+#ifdef FA_PACK_PROF
+// debug build only: per candidate CTA [t_fold_done, t_heights, t_rowstart, t_rows_done, iterations, rows]
+__device__ long long g_pack_prof[256][8];
+extern "C" void fa_debug_pack_prof(long long* out) { cudaMemcpyFromSymbol(out, g_pack_prof, sizeof(g_pack_prof)); }
+#define PACK_MARK(k, v) \
+    if (threadIdx.x == 0 && blockIdx.x < 256) g_pack_prof[blockIdx.x][k] = (v)
+#else
+#define PACK_MARK(k, v)
+#endif
 
 // One candidate: returns accept; fills cand_w/h/p/y/rowstart for the CTA.
 __device__ bool pack_candidate(const long long* __restrict__ ow, const long long* __restrict__ oh, int n,
@@ -273,7 +313,88 @@ __device__ bool pack_candidate(const long long* __restrict__ ow, const long long
     int tid = threadIdx.x;
     bool have_fold = false;
     long long m = 0;
+#ifdef FA_PACK_PROF
+    long long t0 = clock64();
+    PACK_MARK(0, 0);
+    PACK_MARK(1, 0);
+    PACK_MARK(2, 0);
+    PACK_MARK(3, 0);
+    PACK_MARK(4, 0);
+    PACK_MARK(5, 0);
+#endif
+    const int K = (n + blockDim.x - 1) / blockDim.x;
+    if (K <= PK_KREG) {
+        // Register-resident rounds: thread tid owns boxes [tid*K, tid*K + K);
+        // widths, the running fold offset and the overflow stay in registers,
+        // so a round is the divisions + one block scan + one paired max.
+        const int b0 = tid * K;
+        long long owr[PK_KREG], wr[PK_KREG];
+#pragma unroll
+        for (int k = 0; k < PK_KREG; k++) owr[k] = (k < K && b0 + k < n) ? ow[b0 + k] : 0;
+        long long base = 0;
+        for (int it = 0; it < FA_MAX_OVERFLOW_ITERS + 1; it++) {
+            PACK_MARK(4, it + 1);
+#ifdef FA_PACK_PROF
+            long long ti = clock64();
+#endif
+            long long wmax = 0, local = 0;
+            const double rdn = 1.0 / (double)den;
+#pragma unroll
+            for (int k = 0; k < PK_KREG; k++) {
+                long long w = 0;
+                if (k < K && b0 + k < n) w = scaled_dim_rcp(owr[k], num, den, rdn, min_dim, pad);
+                wr[k] = w;
+                wmax = w > wmax ? w : wmax;
+                local += w;
+            }
+#ifdef FA_PACK_PROF
+            if (it == 1) PACK_MARK(6, clock64() - ti);
+#endif
+            long long tot;
+            base = block_exclusive_scan_ll(local, sm.red, &tot);
+#ifdef FA_PACK_PROF
+            if (it == 1) PACK_MARK(7, clock64() - ti);
+#endif
+            long long p = base, mloc = -(1ll << 62);
+#pragma unroll
+            for (int k = 0; k < PK_KREG; k++) {
+                if (k < K && b0 + k < n) {
+                    long long q = p & (omega - 1);
+                    long long over = q + wr[k] - omega;
+                    mloc = over > mloc ? over : mloc;
+                    p += wr[k];
+                }
+            }
+            block_max2_ll(wmax, mloc, sm.red, sm.red2);
+#ifdef FA_PACK_PROF
+            if (it == 1) PACK_MARK(1, clock64() - ti);
+#endif
+            if (wmax > omega) {
+                m = wmax - omega;  // no fold: the widest box alone overflows
+            } else {
+                m = mloc > 0 ? mloc : 0;
+                have_fold = true;
+            }
+            if (m == 0) break;
+            have_fold = false;
+            snap_scale(num, den, omega, m);
+#ifdef FA_PACK_PROF
+            if (it == 1) PACK_MARK(2, clock64() - ti);
+#endif
+        }
+        long long p = base;
+#pragma unroll
+        for (int k = 0; k < PK_KREG; k++) {
+            if (k < K && b0 + k < n) {
+                cw[b0 + k] = (int)wr[k];
+                cp[b0 + k] = p;
+                p += wr[k];
+            }
+        }
+        __syncthreads();
+    } else
     for (int it = 0; it < FA_MAX_OVERFLOW_ITERS + 1; it++) {
+        PACK_MARK(4, it + 1);
         long long wmax = 0;
         for (int b = tid; b < n; b += blockDim.x) {
             long long w = scaled_dim(ow[b], num, den, min_dim, pad);
@@ -308,15 +429,17 @@ __device__ bool pack_candidate(const long long* __restrict__ ow, const long long
         have_fold = false;
         snap_scale(num, den, omega, m);
     }
+    PACK_MARK(0, clock64() - t0);
     if (!have_fold || m != 0) return false;
     // heights + pigeonhole (packing.py:271-274), int64 wrapping sum
     unsigned long long area = 0;
     for (int b = tid; b < n; b += blockDim.x) {
-        long long h = scaled_dim(oh[b], num, den, min_dim, pad);
+        long long h = scaled_dim_rcp(oh[b], num, den, 1.0 / (double)den, min_dim, pad);
         ch[b] = (int)h;
         area += (unsigned long long)cw[b] * (unsigned long long)h;
     }
     area = (unsigned long long)block_sum_ll((long long)area, sm.red);
+    PACK_MARK(1, clock64() - t0);
     if ((long long)area > omega * omega) return false;
     // row starts
     for (int b = tid; b < n; b += blockDim.x) {
@@ -327,6 +450,8 @@ __device__ bool pack_candidate(const long long* __restrict__ ow, const long long
     if (tid == 0) sm.flag = 0;
     __syncthreads();
     int n_rows = (int)(cp[n - 1] >> kbits) + 1;
+    PACK_MARK(2, clock64() - t0);
+    PACK_MARK(5, n_rows);
     long long used = 0;
     for (int r = 0; r < n_rows; r++) {
         int b0 = rowstart[r];
@@ -362,6 +487,7 @@ __device__ bool pack_candidate(const long long* __restrict__ ow, const long long
         __syncthreads();
     }
     used = block_max_ll(used, sm.red);
+    PACK_MARK(3, clock64() - t0);
     out_used = used;
     if (used > omega) return false;
     long long g2 = gcd_ll(num, den);
