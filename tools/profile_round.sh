@@ -1,0 +1,20 @@
+#!/bin/bash
+# Round artefacts for profiles/: bench lines (both arms), the ncu launch list
+# of the bench command, and one ncu --set full capture of the frame kernels.
+# usage (on the GPU box): bash tools/profile_round.sh r1
+tag=${1:-r1}
+mkdir -p gpurun_out
+python bench.py > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err || exit 1
+python bench.py --impl reference > gpurun_out/${tag}_bench_reference.json 2> gpurun_out/${tag}_bench_reference.err
+# launch list (cold-cache, serialised per-launch times; compare shares)
+ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
+    --log-file gpurun_out/${tag}_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
+    --profile-frames 0 > gpurun_out/${tag}_ncu_launch.log 2>&1
+python tools/launch_table.py gpurun_out/${tag}_launches.csv > gpurun_out/${tag}_launches.txt
+# full capture of the frame kernels (non-graph path, a few frames)
+ncu --set full --import-source on --clock-control none -s 30 -c 40 -o gpurun_out/${tag}_full \
+    python tools/profile_frame.py C2 3 > gpurun_out/${tag}_ncu_full.log 2>&1
+python tools/ncu_traffic.py gpurun_out/${tag}_full.ncu-rep > gpurun_out/${tag}_ncu_kernels.out
+python tools/ncu_summary.py gpurun_out/${tag}_full.ncu-rep > gpurun_out/${tag}_ncu_summary.txt
+tail -3 gpurun_out/${tag}_launches.txt
+cat gpurun_out/${tag}_ncu_summary.txt | head -40
