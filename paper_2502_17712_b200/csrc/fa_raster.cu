@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const SmallRec* __re
                                                             const int2* __restrict__ tiles, int W,
                                                             unsigned long long* __restrict__ depth,
                                                             unsigned long long* __restrict__ wid,
-                                                            fa_dstat* __restrict__ st, int max_tiles) {
+                                                            fa_dstat* __restrict__ st, int max_tiles, int check) {
     __shared__ TriSetup sm[8];
     int warp = threadIdx.x >> 5, lane = lane_id();
     int nwarps = gridDim.x * 8;
@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const SmallRec* __re
                     if (y > f.max_y) break;
                     double py = (double)y + 0.5;
                     if (!inside_col(f, ct, py)) continue;
-                    depth_min(depth, wid, (long long)y * W + x, f64_key(depth_col(f, ct, py)), t, true);
+                    depth_min(depth, wid, (long long)y * W + x, f64_key(depth_col(f, ct, py)), t, check != 0);
                 }
             }
             continue;
@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const SmallRec* __re
                 if (y > s.max_y) break;
                 double py = (double)y + 0.5;
                 if (!sample_inside(s, px, py)) continue;
-                depth_min(depth, wid, (long long)y * W + x, f64_key(sample_depth(s, px, py)), s.tri, true);
+                depth_min(depth, wid, (long long)y * W + x, f64_key(sample_depth(s, px, py)), s.tri, check != 0);
             }
         }
     }
@@ -490,8 +490,9 @@ __global__ void __launch_bounds__(COOP_WARPS * 32) k_small_coop(const SmallRec* 
                     rt = row_terms(f, (double)iy + 0.5);
                 }
                 px = (double)ix + 0.5;
-                if (inside_row(f, rt, px))
-                    depth_min(depth, wid, (long long)iy * W + ix, f64_key(depth_row(f, rt, px)), t, false);
+                // depth evaluated alongside the edges (independent DP chains)
+                const double z = depth_row(f, rt, px);
+                if (inside_row(f, rt, px)) depth_min(depth, wid, (long long)iy * W + ix, f64_key(z), t, false);
                 if (++ix > f.max_x) {
                     ix = f.min_x;
                     iy++;
@@ -731,7 +732,8 @@ int fa_launch_depth_pass(bool write_depth, const double4* clip, const double4* s
     if (write_depth) {
         k_raster_clipped<true><<<FA_NUM_SMS * 2, 256, 0, b>>>(clip, tris, W, H, cull, clip_list, depth, wid, large,
                                                               max_large, tiles, max_tiles, st);
-        k_raster_depth_tiles<<<FA_NUM_SMS * 8, 256, 0, b>>>(small_rec, large, tiles, W, depth, wid, st, max_tiles);
+        // fire-and-forget REDs measured faster than a load-then-atomic check here
+        k_raster_depth_tiles<<<FA_NUM_SMS * 8, 256, 0, b>>>(small_rec, large, tiles, W, depth, wid, st, max_tiles, 0);
         // small unclipped triangles (warp-cooperative)
         k_small_coop<<<fa_grid((long long)T, COOP_WARPS * 32 * 2, FA_NUM_SMS * 6), COOP_WARPS * 32, 0, s>>>(
             small_rec, W, depth, wid, st);
