@@ -3,14 +3,16 @@
 // Reference: charts.py:269-313 (depth_prepass / mark_visible) over the
 // per-triangle clip + raster of charts.py:160-266.
 //
-// Work split (load balance): one thread per triangle computes the clip /
-// screen setup; triangles whose sample window is at most FA_SMALL_PX pixels
-// are rasterized in that thread, larger ones store their setup in a queue
-// and reserve 16x8-pixel tiles that a warp each rasterizes (4 px per lane).
-// The depth buffer holds order-preserving u64 keys of the float64 NDC depth
-// so the per-pixel minimum is a single 64-bit atomicMin in L2 (checked with
-// a plain load first).  Pass 2 revisits only triangles that covered a sample
-// in pass 1 (small list) and the stored large setups.
+// Work split (load balance): k_raster_setup builds one exact setup per
+// triangle from the per-vertex screen records and emits 96-byte records —
+// small windows (<= FA_SMALL_PX pixels) for the warp-cooperative sampler,
+// large ones with their 16x8 tiles for a warp per tile — and lists the
+// clipped triangles for a warp each (k_raster_clipped).  The depth buffer
+// holds order-preserving u64 keys of the float64 NDC depth, so the per-pixel
+// minimum is one fire-and-forget 64-bit RED.MIN in L2; a second RED keeps the
+// pixel winner.  Pass 2 (visibility) skips the winners, rejects occluded
+// records with an 8x8 hierarchical Z, and replays the stored records.
+// DESIGN.md §2.1 has the full picture.
 #include "fa_internal.h"
 #include "fa_raster.cuh"
 
