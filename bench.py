@@ -243,7 +243,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-frames", type=int, default=5)
-    ap.add_argument("--depth", type=int, default=4, help="concurrent views per GPU (FramePipeline slots)")
+    ap.add_argument("--depth", type=int, default=6, help="concurrent views per GPU (FramePipeline slots)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
 

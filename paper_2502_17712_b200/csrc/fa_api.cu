@@ -159,7 +159,7 @@ static int ensure_raster(fa_ctx* ctx, int W, int H, bool depth) {
     long long want_tiles = (long long)W * H / 32;
     if (want_tiles > ctx->max_tiles) ctx->max_tiles = (int)(want_tiles < (1ll << 30) ? want_tiles : (1 << 30));
     ENSURE(large, (size_t)ctx->max_large * sizeof(TriSetup));
-    ENSURE(tiles, (size_t)ctx->max_tiles * sizeof(int2));
+    ENSURE(tiles, (size_t)ctx->max_tiles * sizeof(int4));
     ENSURE(dstat, sizeof(fa_dstat));
     ENSURE(vp_dev, 16 * sizeof(double));
     return FA_OK;
@@ -276,7 +276,7 @@ static int launch_depth(fa_ctx* ctx, int W, int H, int cull, unsigned char* flag
     nl += 1 + fa_launch_depth_pass(true, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, W, H, cull,
                                    P<unsigned long long>(ctx->depth_keys), nullptr, P<SmallRec>(ctx->small_rec),
                                    P<int>(ctx->clip_list), P<TriSetup>(ctx->large), ctx->max_large,
-                                   P<int2>(ctx->tiles), ctx->max_tiles, P<fa_dstat>(ctx->dstat), s, nullptr, nullptr,
+                                   P<int4>(ctx->tiles), ctx->max_tiles, P<fa_dstat>(ctx->dstat), s, nullptr, nullptr,
                                    nullptr);
     return FA_OK;
 }
@@ -351,11 +351,11 @@ int fa_mark_visible(fa_ctx* ctx, const double* vp_host, const double* depth, int
         fa_launch_encode_depth(depth, P<unsigned long long>(ctx->depth_keys), (long long)width * height, s);
         fa_launch_depth_pass(false, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, width, height,
                              backface_cull, nullptr, nullptr, P<SmallRec>(ctx->small_rec), P<int>(ctx->clip_list),
-                             P<TriSetup>(ctx->large), ctx->max_large, P<int2>(ctx->tiles), ctx->max_tiles,
+                             P<TriSetup>(ctx->large), ctx->max_large, P<int4>(ctx->tiles), ctx->max_tiles,
                              P<fa_dstat>(ctx->dstat), s, nullptr, nullptr, nullptr);
         fa_launch_depth_hiz(P<unsigned long long>(ctx->depth_keys), nullptr, width, height,
                             P<unsigned long long>(ctx->hiz), nullptr, nullptr, s);
-        fa_launch_raster_vis(P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large), P<int2>(ctx->tiles),
+        fa_launch_raster_vis(P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large), P<int4>(ctx->tiles),
                              ctx->max_tiles, ctx->max_large, T, width, P<unsigned long long>(ctx->depth_keys),
                              P<unsigned long long>(ctx->hiz), P<unsigned char>(ctx->flags), P<fa_dstat>(ctx->dstat),
                              s, nullptr, nullptr, nullptr);
@@ -680,13 +680,13 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     nl += fa_launch_depth_pass(true, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, W, H,
                                p->backface_cull, P<unsigned long long>(ctx->depth_keys), wid,
                                P<SmallRec>(ctx->small_rec), P<int>(ctx->clip_list), P<TriSetup>(ctx->large),
-                               ctx->max_large, P<int2>(ctx->tiles), ctx->max_tiles, st, s, ctx->side, ctx->fj[0],
+                               ctx->max_large, P<int4>(ctx->tiles), ctx->max_tiles, st, s, ctx->side, ctx->fj[0],
                                ctx->fj[1]);
     fa_launch_depth_hiz(P<unsigned long long>(ctx->depth_keys), wid, W, H, P<unsigned long long>(ctx->hiz), flags, st,
                         s);
     nl += 1;
     mark();  // 2: depth pass
-    nl += fa_launch_raster_vis(P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large), P<int2>(ctx->tiles),
+    nl += fa_launch_raster_vis(P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large), P<int4>(ctx->tiles),
                                ctx->max_tiles, ctx->max_large, T, W, P<unsigned long long>(ctx->depth_keys),
                                P<unsigned long long>(ctx->hiz), flags, st, s, ctx->side, ctx->fj[2], ctx->fj[3]);
     mark();  // 3: visibility pass

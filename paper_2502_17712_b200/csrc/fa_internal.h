@@ -83,9 +83,9 @@ void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* c
 // Both return the number of kernels launched.  wid: see depth_min (may be null).
 int fa_launch_depth_pass(bool write_depth, const double4* clip, const double4* scr, const int* tris, int T, int W,
                          int H, int cull, unsigned long long* depth, unsigned long long* wid, SmallRec* small_rec,
-                         int* clip_list, TriSetup* large, int max_large, int2* tiles, int max_tiles, fa_dstat* st,
+                         int* clip_list, TriSetup* large, int max_large, int4* tiles, int max_tiles, fa_dstat* st,
                          cudaStream_t s, cudaStream_t side, cudaEvent_t ev_fork, cudaEvent_t ev_join);
-int fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const int2* tiles, int max_tiles,
+int fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const int4* tiles, int max_tiles,
                          int max_large, int T, int W, const unsigned long long* depth, const unsigned long long* hiz,
                          unsigned char* flags, const fa_dstat* st, cudaStream_t s, cudaStream_t side,
                          cudaEvent_t ev_fork, cudaEvent_t ev_join);

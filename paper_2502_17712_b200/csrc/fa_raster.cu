@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(SETUP_WARPS * 32) k_raster_setup(const double4
                                                       const int* __restrict__ tris,
                                                       int T, int W, int H, int cull,
                                                       SmallRec* __restrict__ recs, int* __restrict__ clip_list,
-                                                      int2* __restrict__ tiles, int max_tiles,
+                                                      int4* __restrict__ tiles, int max_tiles,
                                                       fa_dstat* __restrict__ st) {
     // per-warp counts -> per-warp bases; one atomic per counter per block step
     // (a same-address atomic per warp serialises ~30K times in the L2)
@@ -206,9 +206,10 @@ __global__ void __launch_bounds__(SETUP_WARPS * 32) k_raster_setup(const double4
                 m &= m - 1;
                 int r_src = __shfl_sync(0xffffffffu, ri, src);
                 int n_src = __shfl_sync(0xffffffffu, nt, src);
+                int t_src = __shfl_sync(0xffffffffu, t, src);
                 int e_src = tb + __shfl_sync(0xffffffffu, incl, src) - n_src;
                 for (int k = lane; k < n_src; k += 32)
-                    if (e_src + k < max_tiles) tiles[e_src + k] = make_int2(r_src, k);
+                    if (e_src + k < max_tiles) tiles[e_src + k] = make_int4(r_src, k, t_src, 0);
             }
         }
     }
@@ -226,7 +227,7 @@ __global__ void __launch_bounds__(256) k_raster_clipped(const double4* __restric
                                                         unsigned long long* __restrict__ depth,
                                                         unsigned long long* __restrict__ wid,
                                                         TriSetup* __restrict__ large, int max_large,
-                                                        int2* __restrict__ tiles, int max_tiles,
+                                                        int4* __restrict__ tiles, int max_tiles,
                                                         fa_dstat* __restrict__ st) {
     __shared__ TriSetup sm[8];
     const int warp = threadIdx.x >> 5, lane = lane_id();
@@ -277,7 +278,7 @@ __global__ void __launch_bounds__(256) k_raster_clipped(const double4* __restric
             // capacity) and flag the frame; the host grows the queue and reruns
             if (base + nt > max_tiles && lane == 0) atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW);
             for (int k = lane; k < nt; k += 32)
-                if (base + k < max_tiles) tiles[base + k] = make_int2(-slot - 1, k);
+                if (base + k < max_tiles) tiles[base + k] = make_int4(-slot - 1, k, t, 0);
         }
     }
 }
@@ -358,7 +359,7 @@ __device__ __forceinline__ void tile_lane_origin(int min_x, int max_x, int min_y
 // warp-private shared memory.
 __global__ void __launch_bounds__(256) k_raster_depth_tiles(const SmallRec* __restrict__ recs,
                                                             const TriSetup* __restrict__ large,
-                                                            const int2* __restrict__ tiles, int W,
+                                                            const int4* __restrict__ tiles, int W,
                                                             unsigned long long* __restrict__ depth,
                                                             unsigned long long* __restrict__ wid,
                                                             fa_dstat* __restrict__ st, int max_tiles, int check) {
@@ -367,7 +368,7 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const SmallRec* __re
     int nwarps = gridDim.x * 8;
     int n_tiles = min(st->n_tiles, max_tiles);
     for (int w = blockIdx.x * 8 + warp; w < n_tiles; w += nwarps) {
-        int2 rec = tiles[w];
+        int4 rec = tiles[w];
         if (rec.x >= 0) {
             Setup3 f;
             int t;
@@ -583,7 +584,7 @@ __global__ void __launch_bounds__(256) k_raster_vis_small(const SmallRec* __rest
 // ---- pass 2 large: one warp per tile --------------------------------------
 __global__ void __launch_bounds__(256) k_raster_vis_tiles(const SmallRec* __restrict__ recs, int T,
                                                           const TriSetup* __restrict__ large,
-                                                          const int2* __restrict__ tiles, int W,
+                                                          const int4* __restrict__ tiles, int W,
                                                           const unsigned long long* __restrict__ depth,
                                                           const unsigned long long* __restrict__ hiz, int htx,
                                                           unsigned char* __restrict__ flags,
@@ -599,19 +600,20 @@ __global__ void __launch_bounds__(256) k_raster_vis_tiles(const SmallRec* __rest
     const int n_tiles = min(st->n_tiles, max_tiles);
     const int n_items = n_tiles + min(st->n_large, max_large);
     for (int w = blockIdx.x * 8 + warp; w < n_items; w += nwarps) {
-        int2 rec;
+        int4 rec;
         if (w < n_tiles) {
             rec = tiles[w];
         } else {
-            rec.x = -(w - n_tiles) - 1;
-            rec.y = -1;
+            rec = make_int4(-(w - n_tiles) - 1, -1, -1, 0);
         }
         if (rec.x >= 0) {
+            // the descriptor names the triangle: its flag (already visible?)
+            // is read in the same round trip as the record
+            int seen = 0;
+            if (lane == 0) seen = flags[rec.z];
             Setup3 f;
             int t;
             load_rec(recs + rec.x, f, t);
-            int seen = 0;
-            if (lane == 0) seen = *(volatile unsigned char*)(flags + t);
             if (__shfl_sync(0xffffffffu, seen, 0)) {
 #ifdef FA_HIZ_STATS
                 if (lane == 0) atomicAdd(&g_hiz_stats[4], 1ull);
@@ -619,14 +621,21 @@ __global__ void __launch_bounds__(256) k_raster_vis_tiles(const SmallRec* __rest
                 continue;  // already visible (warp-uniform)
             }
             {
-                // hierarchical-Z test of the tile's rectangle (warp-uniform)
+                // lanes 0..5 read the hierarchical-Z tiles under the 16x8
+                // rectangle (at most 3 x 2 of them) in one round trip
                 int ntx = (f.max_x - f.min_x + 1 + TILE_W - 1) / TILE_W;
                 int xa = f.min_x + (rec.y % ntx) * TILE_W, ya = f.min_y + (rec.y / ntx) * TILE_H;
                 int xb = min(xa + TILE_W - 1, f.max_x), yb = min(ya + TILE_H - 1, f.max_y);
+                const int hx0 = xa / FA_HIZ, hy0 = ya / FA_HIZ, hnx = xb / FA_HIZ - hx0 + 1;
+                const int hn = hnx * (yb / FA_HIZ - hy0 + 1);
+                const bool hv = lane < hn;
+                unsigned long long hk = 0;
+                if (hv) hk = __ldg(hiz + (hy0 + lane / hnx) * htx + hx0 + lane % hnx);
+                const double zlb = depth_lower_bound(f, xa, xb, ya, yb);
 #ifdef FA_HIZ_STATS
                 if (lane == 0) atomicAdd(&g_hiz_stats[2], 1ull);
 #endif
-                if (hiz_rejects(hiz, htx, xa, xb, ya, yb, depth_lower_bound(f, xa, xb, ya, yb))) {
+                if (!__any_sync(0xffffffffu, hv && !hiz_tile_rejects(hk, zlb))) {
 #ifdef FA_HIZ_STATS
                     if (lane == 0) atomicAdd(&g_hiz_stats[3], 1ull);
 #endif
@@ -725,7 +734,7 @@ static void fork_to(cudaStream_t s, cudaStream_t side, cudaEvent_t ev) {
 // depth keys with atomicMin, so their order does not matter.
 int fa_launch_depth_pass(bool write_depth, const double4* clip, const double4* scr, const int* tris, int T, int W,
                          int H, int cull, unsigned long long* depth, unsigned long long* wid, SmallRec* small_rec,
-                         int* clip_list, TriSetup* large, int max_large, int2* tiles, int max_tiles, fa_dstat* st,
+                         int* clip_list, TriSetup* large, int max_large, int4* tiles, int max_tiles, fa_dstat* st,
                          cudaStream_t s, cudaStream_t side, cudaEvent_t ev_fork, cudaEvent_t ev_join) {
     k_raster_setup<<<fa_grid(T, 256, FA_NUM_SMS * 4), 256, 0, s>>>(scr, tris, T, W, H, cull, small_rec, clip_list,
                                                                     tiles, max_tiles, st);
@@ -749,7 +758,7 @@ int fa_launch_depth_pass(bool write_depth, const double4* clip, const double4* s
 
 // Visibility pass: small records on s || large tiles + small clipped windows
 // on side.  Both only set flags, which k_depth_hiz seeded with the winners.
-int fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const int2* tiles, int max_tiles,
+int fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const int4* tiles, int max_tiles,
                          int max_large, int T, int W, const unsigned long long* depth, const unsigned long long* hiz,
                          unsigned char* flags, const fa_dstat* st, cudaStream_t s, cudaStream_t side,
                          cudaEvent_t ev_fork, cudaEvent_t ev_join) {
