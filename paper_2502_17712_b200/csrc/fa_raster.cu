@@ -316,9 +316,15 @@ __global__ void __launch_bounds__(256) k_depth_hiz(const unsigned long long* __r
                 c += fin;
                 if (v >= FA_KEY_NEG_INF && v < FA_KEY_POS_INF && v > mx) mx = v;
                 if (wid && fin) {
-                    int id = (int)(wid[p] & ((1ull << FA_WID_BITS) - 1));
-                    if (id != last) flags[id] = 1;
-                    last = id;
+                    // the winner is only trusted when its truncated key is the
+                    // final key's (so any subset of writers may skip the RED)
+                    const unsigned long long wv = wid[p];
+                    const unsigned long long hi = ~((1ull << FA_WID_BITS) - 1);
+                    if ((wv & hi) == (v & hi)) {
+                        int id = (int)(wv & ~hi);
+                        if (id != last) flags[id] = 1;
+                        last = id;
+                    }
                 }
             }
         }
@@ -362,13 +368,18 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const SmallRec* __re
                                                             const int4* __restrict__ tiles, int W,
                                                             unsigned long long* __restrict__ depth,
                                                             unsigned long long* __restrict__ wid,
-                                                            fa_dstat* __restrict__ st, int max_tiles, int check) {
+                                                            fa_dstat* __restrict__ st, int max_tiles, int check,
+                                                            int tile_wid) {
     __shared__ TriSetup sm[8];
     int warp = threadIdx.x >> 5, lane = lane_id();
     int nwarps = gridDim.x * 8;
     int n_tiles = min(st->n_tiles, max_tiles);
+    // descriptors are read one step ahead: a step waits for the record only
+    int4 nxt = make_int4(0, 0, 0, 0);
+    if (blockIdx.x * 8 + warp < n_tiles) nxt = tiles[blockIdx.x * 8 + warp];
     for (int w = blockIdx.x * 8 + warp; w < n_tiles; w += nwarps) {
-        int4 rec = tiles[w];
+        int4 rec = nxt;
+        if (w + nwarps < n_tiles) nxt = tiles[w + nwarps];
         if (rec.x >= 0) {
             Setup3 f;
             int t;
@@ -383,7 +394,8 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const SmallRec* __re
                     if (y > f.max_y) break;
                     double py = (double)y + 0.5;
                     if (!inside_col(f, ct, py)) continue;
-                    depth_min(depth, wid, (long long)y * W + x, f64_key(depth_col(f, ct, py)), t, check != 0);
+                    depth_min(depth, tile_wid ? wid : nullptr, (long long)y * W + x, f64_key(depth_col(f, ct, py)), t,
+                              check != 0);
                 }
             }
             continue;
@@ -744,7 +756,8 @@ int fa_launch_depth_pass(bool write_depth, const double4* clip, const double4* s
         k_raster_clipped<true><<<FA_NUM_SMS * 2, 256, 0, b>>>(clip, tris, W, H, cull, clip_list, depth, wid, large,
                                                               max_large, tiles, max_tiles, st);
         // fire-and-forget REDs measured faster than a load-then-atomic check here
-        k_raster_depth_tiles<<<FA_NUM_SMS * 8, 256, 0, b>>>(small_rec, large, tiles, W, depth, wid, st, max_tiles, 0);
+        k_raster_depth_tiles<<<FA_NUM_SMS * 8, 256, 0, b>>>(small_rec, large, tiles, W, depth, wid, st, max_tiles, 0,
+                                                            1);
         // small unclipped triangles (warp-cooperative)
         k_small_coop<<<fa_grid((long long)T, COOP_WARPS * 32 * 2, FA_NUM_SMS * 6), COOP_WARPS * 32, 0, s>>>(
             small_rec, W, depth, wid, st);

@@ -510,9 +510,15 @@ __device__ __forceinline__ double sample_depth3(const Setup3& s, double px, doub
 // terms that depend on one coordinate are computed once per row (or per
 // column) instead of once per sample, and the three edges are combined
 // without short-circuiting so their DP chains overlap.
+// Edge acceptance as one compare: incl ? e >= 0 : e > 0  ==  e >= thr with
+// thr = 0 or the smallest positive subnormal (FP64 keeps subnormals; NaN
+// fails both forms).
+__device__ __forceinline__ double edge_thr(int incl_bit) { return incl_bit ? 0.0 : __longlong_as_double(1ll); }
+
 struct RowTerms {
     double r0, r1, r2;  // dx_i * (py - ay_i)
     double zr;          // gy * (py - p0y)
+    double t0, t1, t2;  // edge thresholds (edge_thr)
 };
 
 __device__ __forceinline__ RowTerms row_terms(const Setup3& s, double py) {
@@ -521,6 +527,9 @@ __device__ __forceinline__ RowTerms row_terms(const Setup3& s, double py) {
     r.r1 = __dmul_rn(s.dx1, __dsub_rn(py, s.ay1));
     r.r2 = __dmul_rn(s.dx2, __dsub_rn(py, s.ay2));
     r.zr = __dmul_rn(s.gy, __dsub_rn(py, s.p0y));
+    r.t0 = edge_thr(s.incl & 1);
+    r.t1 = edge_thr(s.incl & 2);
+    r.t2 = edge_thr(s.incl & 4);
     return r;
 }
 
@@ -528,10 +537,7 @@ __device__ __forceinline__ bool inside_row(const Setup3& s, const RowTerms& r, d
     double e0 = __dsub_rn(r.r0, __dmul_rn(s.dy0, __dsub_rn(px, s.ax0)));
     double e1 = __dsub_rn(r.r1, __dmul_rn(s.dy1, __dsub_rn(px, s.ax1)));
     double e2 = __dsub_rn(r.r2, __dmul_rn(s.dy2, __dsub_rn(px, s.ax2)));
-    bool k0 = (s.incl & 1) ? (e0 >= 0) : (e0 > 0);
-    bool k1 = (s.incl & 2) ? (e1 >= 0) : (e1 > 0);
-    bool k2 = (s.incl & 4) ? (e2 >= 0) : (e2 > 0);
-    return k0 & k1 & k2;
+    return (e0 >= r.t0) & (e1 >= r.t1) & (e2 >= r.t2);
 }
 
 __device__ __forceinline__ double depth_row(const Setup3& s, const RowTerms& r, double px) {
@@ -542,6 +548,7 @@ __device__ __forceinline__ double depth_row(const Setup3& s, const RowTerms& r, 
 struct ColTerms {
     double c0, c1, c2;  // dy_i * (px - ax_i)
     double zc;          // p0z + gx * (px - p0x)
+    double t0, t1, t2;  // edge thresholds (edge_thr)
 };
 
 __device__ __forceinline__ ColTerms col_terms(const Setup3& s, double px) {
@@ -550,6 +557,9 @@ __device__ __forceinline__ ColTerms col_terms(const Setup3& s, double px) {
     c.c1 = __dmul_rn(s.dy1, __dsub_rn(px, s.ax1));
     c.c2 = __dmul_rn(s.dy2, __dsub_rn(px, s.ax2));
     c.zc = __dadd_rn(s.p0z, __dmul_rn(s.gx, __dsub_rn(px, s.p0x)));
+    c.t0 = edge_thr(s.incl & 1);
+    c.t1 = edge_thr(s.incl & 2);
+    c.t2 = edge_thr(s.incl & 4);
     return c;
 }
 
@@ -557,10 +567,7 @@ __device__ __forceinline__ bool inside_col(const Setup3& s, const ColTerms& c, d
     double e0 = __dsub_rn(__dmul_rn(s.dx0, __dsub_rn(py, s.ay0)), c.c0);
     double e1 = __dsub_rn(__dmul_rn(s.dx1, __dsub_rn(py, s.ay1)), c.c1);
     double e2 = __dsub_rn(__dmul_rn(s.dx2, __dsub_rn(py, s.ay2)), c.c2);
-    bool k0 = (s.incl & 1) ? (e0 >= 0) : (e0 > 0);
-    bool k1 = (s.incl & 2) ? (e1 >= 0) : (e1 > 0);
-    bool k2 = (s.incl & 4) ? (e2 >= 0) : (e2 > 0);
-    return k0 & k1 & k2;
+    return (e0 >= c.t0) & (e1 >= c.t1) & (e2 >= c.t2);
 }
 
 __device__ __forceinline__ double depth_col(const Setup3& s, const ColTerms& c, double py) {
