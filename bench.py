@@ -143,7 +143,7 @@ STAGE_KERNELS = {
     "project+clear": ["k_frame_init"],
     "depth pass": ["k_raster_setup", "k_small_coop", "k_raster_clipped<1>", "k_raster_depth_tiles", "k_depth_hiz"],
     "visibility pass": ["k_raster_vis_small", "k_raster_vis_tiles"],
-    "union-find": ["k_vmin", "k_uf_init_vmin", "k_hook_multi", "k_compress", "k_v2c"],
+    "union-find": ["k_hook_multi", "k_compress", "k_v2c"],
     "pack+select": ["k_pack", "k_select"],
 }
 

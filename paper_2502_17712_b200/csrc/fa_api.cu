@@ -690,10 +690,13 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
                                ctx->max_tiles, ctx->max_large, T, W, P<unsigned long long>(ctx->depth_keys),
                                P<unsigned long long>(ctx->hiz), flags, st, s, ctx->side, ctx->fj[2], ctx->fj[3]);
     mark();  // 3: visibility pass
-    fa_launch_compact_visible(flags, T, P<int>(ctx->blocks), P<int>(ctx->vis_list), P<int>(ctx->label), st, s);
+    // the compaction also lowers vmin (frame_init filled it with INT_MAX)
+    fa_launch_compact_visible(flags, T, P<int>(ctx->blocks), P<int>(ctx->vis_list), P<int>(ctx->label), st, s,
+                              ctx->tris, P<int>(ctx->vmin));
     nl += 2;
     mark();  // 4: visible compaction
-    nl += fa_launch_uf_vertex(ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->vmin), P<int>(ctx->label), T, st, s);
+    nl += fa_launch_uf_vertex(ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->vmin), P<int>(ctx->label), T, st, s,
+                              true);
     fa_launch_uf_compress(P<int>(ctx->vis_list), P<int>(ctx->label), T, st, s);
     fa_launch_v2c(P<int>(ctx->vmin), P<int>(ctx->label), P<int>(ctx->v2c), V, s);
     nl += 2;

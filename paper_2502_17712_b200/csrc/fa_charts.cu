@@ -55,9 +55,12 @@ __global__ void __launch_bounds__(CMP_THREADS) k_count_flags(const unsigned char
     }
 }
 
+// With `vmin` bound it also lowers vmin[v] to the smallest visible triangle
+// of each vertex (the union-find's first_chart, charts.py:330-336).
 __global__ void __launch_bounds__(CMP_THREADS) k_scatter_visible(const unsigned char* __restrict__ flags, int T,
                                                                  const int* __restrict__ blocks, int nblocks,
                                                                  int* __restrict__ vis_list, int* __restrict__ label,
+                                                                 const int* __restrict__ tris, int* __restrict__ vmin,
                                                                  fa_dstat* __restrict__ st) {
     __shared__ int sm[32];
     int offset = block_prefix_of(blocks, blockIdx.x, sm);
@@ -77,22 +80,39 @@ __global__ void __launch_bounds__(CMP_THREADS) k_scatter_visible(const unsigned 
     for (int i = 0; i < CMP_ITEMS; i++) c += f[i] != 0;
     int total;
     int pos = offset + block_exclusive_scan(c, sm, &total);
+    if (base + CMP_ITEMS <= T) {
+        // 16 consecutive labels: four 128-bit stores
+        int4* l4 = reinterpret_cast<int4*>(label + base);
+#pragma unroll
+        for (int q = 0; q < CMP_ITEMS / 4; q++)
+            l4[q] = make_int4(f[4 * q] ? base + 4 * q : -1, f[4 * q + 1] ? base + 4 * q + 1 : -1,
+                              f[4 * q + 2] ? base + 4 * q + 2 : -1, f[4 * q + 3] ? base + 4 * q + 3 : -1);
+    } else {
+#pragma unroll
+        for (int i = 0; i < CMP_ITEMS; i++)
+            if (base + i < T) label[base + i] = f[i] ? base + i : -1;
+    }
 #pragma unroll
     for (int i = 0; i < CMP_ITEMS; i++) {
         int t = base + i;
-        if (t < T) {
-            if (f[i]) vis_list[pos++] = t;
-            label[t] = f[i] ? t : -1;
+        if (t < T && f[i]) {
+            vis_list[pos++] = t;
+            if (vmin) {
+                // fire-and-forget REDs: a load-first check would put a round
+                // trip per vertex into this thread's sequential item loop
+#pragma unroll
+                for (int j = 0; j < 3; j++) atomicMin(vmin + __ldg(tris + 3 * t + j), t);
+            }
         }
     }
     if (blockIdx.x == nblocks - 1 && threadIdx.x == 0) st->n_vis = offset + total;
 }
 
 void fa_launch_compact_visible(const unsigned char* flags, int T, int* blocks, int* vis_list, int* label,
-                               fa_dstat* st, cudaStream_t s) {
+                               fa_dstat* st, cudaStream_t s, const int* tris, int* vmin) {
     int nb = fa_compact_blocks(T);
     k_count_flags<<<nb, CMP_THREADS, 0, s>>>(flags, T, blocks);
-    k_scatter_visible<<<nb, CMP_THREADS, 0, s>>>(flags, T, blocks, nb, vis_list, label, st);
+    k_scatter_visible<<<nb, CMP_THREADS, 0, s>>>(flags, T, blocks, nb, vis_list, label, tris, vmin, st);
 }
 
 // ---- union-find ---------------------------------------------------------------
@@ -194,25 +214,10 @@ __global__ void k_vmin(const int* __restrict__ tris, const int* __restrict__ vis
     }
 }
 
-// ECL-CC style initialisation: parent[t] = smallest triangle sharing a vertex
-// with t (<= t, same component), so hooking starts from shallow trees.
-// Must run as its own kernel: a plain store racing a hooking CAS could lose it.
-__global__ void k_uf_init_vmin(const int* __restrict__ tris, const int* __restrict__ vis_list,
-                               const int* __restrict__ vmin, int* __restrict__ label,
-                               const fa_dstat* __restrict__ st) {
-    int n = st->n_vis;
-    int stride = gridDim.x * blockDim.x;
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
-        int t = vis_list[k];
-        int m = t;
-#pragma unroll
-        for (int j = 0; j < 3; j++) m = min(m, vmin[__ldg(tris + 3 * t + j)]);
-        label[t] = m;
-    }
-}
-
-
-// Multi-way hooking: t joins the sets of vmin[v0..2] in one step.  The four
+// Multi-way hooking: t joins the sets of vmin[v0..2] in one step.  First the
+// ECL-CC initialisation, fused: t, if still its own root, points at the
+// smallest of its vertex minima (a CAS, never a plain store, so a hook that
+// already gave t a parent is never lost).  Then the four
 // finds (from t's parent and from the three vertex minima) advance together,
 // one parent load each per round, so the dependent chain is as long as the
 // deepest path rather than the sum of three unions; every root other than
@@ -227,7 +232,9 @@ __global__ void k_hook_multi(const int* __restrict__ tris, const int* __restrict
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
         int t = vis_list[k];
         int r1 = vmin[__ldg(tris + 3 * t)], r2 = vmin[__ldg(tris + 3 * t + 1)], r3 = vmin[__ldg(tris + 3 * t + 2)];
-        int r0 = label[t];
+        const int m0 = min(min(t, r1), min(r2, r3));
+        int r0 = m0 < t ? atomicCAS(label + t, t, m0) : label[t];
+        if (r0 == t) r0 = m0;
         // lock-free: every lost CAS moves a node strictly down, so this ends
         while (true) {
             // joint find: one parent load per node per round
@@ -402,11 +409,10 @@ void fa_launch_build_adjacency(const int* tris, int T, unsigned long long* keys,
 }
 
 int fa_launch_uf_vertex(const int* tris, const int* vis_list, int* vmin, int* label, int T, const fa_dstat* st,
-                        cudaStream_t s) {
-    k_vmin<<<uf_grid(T), 256, 0, s>>>(tris, vis_list, vmin, st);
-    k_uf_init_vmin<<<uf_grid(T), 256, 0, s>>>(tris, vis_list, vmin, label, st);
+                        cudaStream_t s, bool vmin_ready) {
+    if (!vmin_ready) k_vmin<<<uf_grid(T), 256, 0, s>>>(tris, vis_list, vmin, st);
     k_hook_multi<<<uf_grid(T), 256, 0, s>>>(tris, vis_list, vmin, label, st);
-    return 3;
+    return vmin_ready ? 1 : 2;
 }
 
 void fa_launch_uf_edges(const int* adjacency, const unsigned char* flags, const int* vis_list, int* label, int T,

@@ -100,11 +100,14 @@ size_t fa_trisetup_bytes();
 
 // ---- charts (fa_charts.cu) -----------------------------------------------
 // ordered compaction of flags -> vis list; label[t] = flag ? t : -1
+// with tris + vmin (vmin pre-filled with INT_MAX) it also computes vmin
 void fa_launch_compact_visible(const unsigned char* flags, int T, int* blocks, int* vis_list, int* label,
-                               fa_dstat* st, cudaStream_t s);
+                               fa_dstat* st, cudaStream_t s, const int* tris = nullptr, int* vmin = nullptr);
 int fa_compact_blocks(long long n);
+// vmin_ready: vmin already holds the per-vertex minima (computed by the
+// visible compaction); otherwise it must hold INT_MAX and is computed here
 int fa_launch_uf_vertex(const int* tris, const int* vis_list, int* vmin, int* label, int T, const fa_dstat* st,
-                         cudaStream_t s);
+                         cudaStream_t s, bool vmin_ready = false);
 void fa_launch_uf_edges(const int* adjacency, const unsigned char* flags, const int* vis_list, int* label, int T,
                         const fa_dstat* st, cudaStream_t s);
 void fa_launch_uf_labels(const int* labels_in, const int* vis_list, int* label, int T, const fa_dstat* st,
