@@ -697,14 +697,22 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     mark();  // 4: visible compaction
     nl += fa_launch_uf_vertex(ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->vmin), P<int>(ctx->label), T, st, s,
                               true);
-    fa_launch_uf_compress(P<int>(ctx->vis_list), P<int>(ctx->label), T, st, s);
-    fa_launch_v2c(P<int>(ctx->vmin), P<int>(ctx->label), P<int>(ctx->v2c), V, s);
+    mark();  // 5: union-find charts (hooking)
+    // Roots are the nodes with label[t] == t after hooking, which flattening
+    // never changes (it only rewrites non-roots to their root, also != t), so
+    // the roots compaction (s) and the flatten + vertex map (side) overlap.
+    CK(cudaEventRecord(ctx->fj[4], s));
+    CK(cudaStreamWaitEvent(ctx->side, ctx->fj[4], 0));
+    fa_launch_uf_compress(P<int>(ctx->vis_list), P<int>(ctx->label), T, st, ctx->side);
+    CK(cudaEventRecord(ctx->fj[5], ctx->side));
+    fa_launch_v2c(P<int>(ctx->vmin), P<int>(ctx->label), P<int>(ctx->v2c), V, ctx->side);
+    CK(cudaEventRecord(ctx->fj[6], ctx->side));
     nl += 2;
-    mark();  // 5: union-find charts
     fa_launch_compact_roots(P<int>(ctx->vis_list), P<int>(ctx->label), T, P<int>(ctx->blocks), P<int>(ctx->roots),
                             P<int>(ctx->cidx), P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), st, s);
     nl += 2;
-    mark();  // 6: chart roots
+    CK(cudaStreamWaitEvent(s, ctx->fj[5], 0));  // bounds read the flattened labels
+    mark();  // 6: chart roots (+ flatten)
     fa_launch_chart_bounds(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->label),
                            P<int>(ctx->cidx), T, P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), st, s);
     fa_launch_box_dims(P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), P<int>(ctx->roots), T, W, H,
@@ -729,6 +737,7 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
         fa_launch_decode_depth(P<unsigned long long>(ctx->depth_keys), P<double>(ctx->depth_f64), (long long)W * H, s);
         nl += 1;
     }
+    CK(cudaStreamWaitEvent(s, ctx->fj[6], 0));  // vertex -> chart map
     CK(cudaMemcpyAsync(ctx->hstat, ctx->dstat.p, sizeof(fa_dstat), cudaMemcpyDeviceToHost, s));
     CKL();
     return FA_OK;

@@ -68,7 +68,7 @@ struct fa_ctx {
 
     // side stream + fork/join events for the independent raster branches
     cudaStream_t side = nullptr;
-    cudaEvent_t fj[4] = {};
+    cudaEvent_t fj[8] = {};
 };
 
 // growth helper: ensures buf has >= bytes; returns false on allocation failure
