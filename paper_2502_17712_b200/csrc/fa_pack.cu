@@ -577,8 +577,9 @@ __global__ void __launch_bounds__(1024) k_select(const long long* __restrict__ o
     }
     // floor-scale width check (packing.py:327-332)
     long long fmax = 0;
+    const double rdn = 1.0 / (double)n_scales;
     for (int b = tid; b < n; b += blockDim.x) {
-        long long f = scaled_dim(ow[b], 1, n_scales, min_dim, pad);
+        long long f = scaled_dim_rcp(ow[b], 1, n_scales, rdn, min_dim, pad);
         fmax = f > fmax ? f : fmax;
     }
     fmax = block_max_ll(fmax, red);
@@ -607,7 +608,7 @@ __global__ void __launch_bounds__(1024) k_select(const long long* __restrict__ o
     long long tex = 0;
     for (int j = tid; j < n; j += blockDim.x) {
         long long q = p[j] & (omega - 1);
-        long long r = p[j] >> kbits;
+        int r = (int)(p[j] >> kbits);  // row index < n <= 2^31
         long long x = (r % FA_DIRECTION_PERIOD == 0) ? q : omega - q - w[j];
         int src = perm[j];
         long long* P = placements + 8 * (long long)j;
