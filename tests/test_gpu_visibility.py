@@ -1,0 +1,128 @@
+"""Visibility stress cases for the pass-2 shortcuts (pixel winners, 8x8
+hierarchical Z, single-compare edges): stacked layers whose NDC depths sit
+just inside and just outside the visibility slack 1e-6*max(1,|d|)
+(charts.py:309-311), mixed small / tiled / near-clipped triangles.  Every
+flag, chart id and placement must equal the C oracle's.  Run with -m gpu."""
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+fa = pytest.importorskip("paper_2502_17712_b200")
+from paper_2502_17712_b200 import FrameEngine, FrameSettings  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    oracle.build()
+
+
+SCREEN = (320, 240)
+
+
+def _camera():
+    return fa.CameraFrame.from_params(math.radians(60.0), SCREEN[0] / SCREEN[1], 0.1, 100.0,
+                                      position=(0.0, 0.0, 0.0), look_at=(0.0, 0.0, -1.0))
+
+
+def _ndc_z(vp, d):
+    c = np.asarray(vp) @ np.array([0.0, 0.0, -d, 1.0])
+    return c[2] / c[3]
+
+
+def _depth_for(vp, z_target):
+    """distance d on the view axis whose NDC depth is z_target (bisection)."""
+    lo, hi = 0.1, 100.0
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        if _ndc_z(vp, mid) < z_target:
+            lo = mid
+        else:
+            hi = mid
+    return 0.5 * (lo + hi)
+
+
+def _layer(d, n, half, rng, jitter):
+    """n x n quad grid facing the camera at distance d (2 tris / cell, ccw)."""
+    xs = np.linspace(-half, half, n + 1)
+    gx, gy = np.meshgrid(xs, xs, indexing="xy")
+    pos = np.stack([gx.ravel(), gy.ravel(), np.full(gx.size, -d)], 1)
+    pos[:, :2] += rng.uniform(-jitter, jitter, size=(len(pos), 2)) * (2 * half / n)
+    tris = []
+    for j in range(n):
+        for i in range(n):
+            a = j * (n + 1) + i
+            b, c, e = a + 1, a + n + 1, a + n + 2
+            tris += [(a, b, e), (a, e, c)]
+    return pos, np.asarray(tris, np.int64)
+
+
+def _merge(parts):
+    pos, tris, base = [], [], 0
+    for p, t in parts:
+        pos.append(p)
+        tris.append(t + base)
+        base += len(p)
+    return np.vstack(pos), np.vstack(tris).astype(np.int32)
+
+
+def _check(pos, tris, vp, omega=512):
+    eng = FrameEngine(fa.Mesh(pos, tris), settings=FrameSettings(screen=SCREEN, omega=omega, uv_f64=True))
+    out = eng.run(vp, check=False)
+    r = oracle.run_frame(pos, tris, vp, SCREEN, omega)
+    assert out.status == r.status
+    h = out.to_host()
+    assert np.array_equal(h["flags"].astype(bool), r.flags)
+    assert np.array_equal(h["chart_of_triangle"].astype(np.int64), r.chart_of_triangle)
+    if r.status == oracle.OK:
+        assert np.array_equal(h["placements"], r.pack.placements)
+        assert h["screen_fragments"] == r.screen_fragments
+    # standalone passes (hierarchical Z without pixel winners)
+    mesh = fa.Mesh(pos, tris)
+    depth = fa.depth_prepass(mesh, _camera(), SCREEN)
+    assert np.array_equal(depth, r.depth)  # +-0 compare equal
+    vis = fa.mark_visible(mesh, _camera(), depth)
+    assert np.array_equal(vis.flags, r.flags)
+    return r
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_layers_around_the_slack(seed):
+    rng = np.random.default_rng(seed)
+    vp = _camera().view_proj
+    z0 = _ndc_z(vp, 6.0)
+    parts = []
+    # relative NDC offsets: inside the slack (visible), at its edge, outside (hidden)
+    for k, dz in enumerate([0.0, 0.2e-6, 0.9e-6, 1.1e-6, 3e-6, 1e-4]):
+        d = _depth_for(vp, z0 + dz)
+        n = [8, 13, 40, 21, 64, 5][k]  # big (tiled) and small (record) triangles
+        parts.append(_layer(d, n, 3.0 + 0.1 * k, rng, 0.2))
+    # a layer crossing the near plane (clipping path) and one far behind
+    near = _layer(0.5, 6, 1.0, rng, 0.1)
+    near[0][:, 2] += rng.uniform(-0.45, 0.2, size=len(near[0]))
+    parts.append(near)
+    parts.append(_layer(50.0, 30, 40.0, rng, 0.3))
+    pos, tris = _merge(parts)
+    r = _check(pos, tris, vp)
+    assert r.status == oracle.OK
+    assert r.flags.sum() > 0
+
+
+def test_coplanar_duplicates():
+    """Exact duplicates at equal depth: both copies pass the slack test."""
+    rng = np.random.default_rng(7)
+    vp = _camera().view_proj
+    a = _layer(5.0, 30, 2.5, rng, 0.3)
+    b = (a[0].copy(), a[1][:, ::-1].copy())  # same geometry, reversed winding (culled)
+    c = (a[0].copy(), a[1].copy())           # same geometry, same winding
+    pos, tris = _merge([a, b, c, _layer(9.0, 50, 6.0, rng, 0.4)])
+    r = _check(pos, tris, vp)
+    assert r.status == oracle.OK
