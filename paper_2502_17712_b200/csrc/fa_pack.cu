@@ -339,10 +339,21 @@ __device__ bool pack_candidate(const long long* __restrict__ ow, const long long
 #endif
             long long wmax = 0, local = 0;
             const double rdn = 1.0 / (double)den;
+            // after a snap the denominator is a power of two: the ceiling is
+            // a shift (non-negative num*t < 2^62, the numpy value exactly)
+            const bool pow2 = den > 0 && (den & (den - 1)) == 0 && num >= 0 && num < (1ll << 31);
+            const int dsh = pow2 ? __ffsll(den) - 1 : 0;
 #pragma unroll
             for (int k = 0; k < PK_KREG; k++) {
                 long long w = 0;
-                if (k < K && b0 + k < n) w = scaled_dim_rcp(owr[k], num, den, rdn, min_dim, pad);
+                if (k < K && b0 + k < n) {
+                    if (pow2 && owr[k] >= 0 && owr[k] < (1ll << 31)) {
+                        w = (num * owr[k] + (den - 1)) >> dsh;
+                        w = (w < min_dim ? min_dim : w) + 2 * pad;
+                    } else {
+                        w = scaled_dim_rcp(owr[k], num, den, rdn, min_dim, pad);
+                    }
+                }
                 wr[k] = w;
                 wmax = w > wmax ? w : wmax;
                 local += w;
