@@ -293,7 +293,9 @@ __device__ __forceinline__ void block_max2_ll(long long& a, long long& b, long l
 }
 
 // boxes per thread kept in registers by the fold rounds (n <= PK_KREG * PK_THREADS)
+#ifndef PK_KREG
 #define PK_KREG 4
+#endif
 
 #ifdef FA_PACK_PROF
 // debug build only: per candidate CTA [t_fold_done, t_heights, t_rowstart, t_rows_done, iterations, rows]
