@@ -108,8 +108,8 @@ __global__ void k_encode_depth(const double* __restrict__ in, unsigned long long
 }
 
 // ---- pass 1: setup + record / tile enqueue --------------------------------
-// One warp per 32 consecutive triangles (warp-uniform loop, so every append
-// is one warp-aggregated atomic).  Per triangle: 3 index loads, 3 gathers of
+// One warp per 32 consecutive triangles (block-uniform loop; appends are
+// aggregated per block step).  Per triangle: 3 index loads, 3 gathers of
 // the per-vertex screen records, the exact cull / bbox / edge / plane setup
 // (tri_setup3s), then
 //   small unclipped  -> 96-byte record at the front of `recs` (k_small_coop),
