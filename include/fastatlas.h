@@ -225,6 +225,12 @@ int fa_last_launch_count(fa_ctx *ctx);
 int fa_stage_times(fa_ctx *ctx, float *ms_out, int max, void *stream);
 const char *fa_stage_name(int i);
 
+/* Work-queue counters of the last finished frame (diagnostics; valid after
+ * fa_frame_finish): [small records, large records, clipped triangles,
+ * generic setups, large-raster tiles, visible, charts, screen fragments].
+ * Returns the number written (<= max). */
+int fa_frame_counters(fa_ctx *ctx, int64_t *out, int max);
+
 #ifdef __cplusplus
 }
 #endif

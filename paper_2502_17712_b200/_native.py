@@ -40,7 +40,7 @@ EXPORTS = (
     "fa_chart_boxes", "fa_blinn_clamped_ndc", "fa_select_side_plane", "fa_chart_bbox",
     "fa_viewport_box", "fa_orient", "fa_orient_order", "fa_fold", "fa_push_up", "fa_pack_at_scale",
     "fa_pack", "fa_frame_launch", "fa_frame_finish", "fa_frame", "fa_frame_download", "fa_last_launch_count",
-    "fa_stage_times", "fa_stage_name", "fa_sequential_scale_search", "fa_sequential_pack", "fa_superblock_pack",
+    "fa_stage_times", "fa_stage_name", "fa_frame_counters", "fa_sequential_scale_search", "fa_sequential_pack", "fa_superblock_pack",
 )
 
 
@@ -127,6 +127,7 @@ def load_library():
             "fa_last_launch_count": ([vp], ci),
             "fa_stage_times": ([vp, ctypes.POINTER(ctypes.c_float), ci, vp], ci),
             "fa_stage_name": ([ci], ctypes.c_char_p),
+            "fa_frame_counters": ([vp, vp, ci], ci),
             "fa_sequential_scale_search": ([vp, vp, vp, vp, vp, i64, i64, i64, i64, i64, vp, vp, vp], ci),
             "fa_superblock_pack": ([vp, vp, vp, vp, vp, i64, i64, i64, ci, vp, vp, vp, vp], ci),
             "fa_sequential_pack": ([vp, vp, vp, i64, i64, vp, vp, vp, vp, vp], ci),

@@ -7,6 +7,7 @@
 // 128-byte camera matrix is uploaded before the graph launch.
 #include <math.h>
 #include <stdarg.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -122,6 +123,7 @@ void fa_destroy(fa_ctx* c) {
     for (cudaEvent_t e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->side) cudaStreamDestroy(c->side);
+    if (c->side2) cudaStreamDestroy(c->side2);
     if (c->hstat) cudaFreeHost(c->hstat);
     if (c->hvp) cudaFreeHost(c->hvp);
     delete c;
@@ -142,6 +144,25 @@ int fa_set_mesh(fa_ctx* ctx, const double* positions, int64_t n_vertices, const 
 }
 
 }  // extern "C"
+
+float fa_grid_cap_scale() {
+    static float f = -1.f;
+    if (f < 0.f) {
+        const char* e = getenv("FASTATLAS_GRID_CAP");
+        f = e ? (float)atof(e) : 1.f;
+        if (!(f > 0.f)) f = 1.f;
+    }
+    return f;
+}
+
+bool fa_pdl_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("FASTATLAS_PDL");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on != 0;
+}
 
 // ---------------------------------------------------------------------------
 // internal helpers
@@ -251,7 +272,8 @@ static int status_from_flags(const fa_dstat* h) {
 
 static void grow_queues(fa_ctx* ctx, const fa_dstat* h) {
     if (h->n_large > ctx->max_large) ctx->max_large = h->n_large + h->n_large / 2;
-    if (h->n_tiles > ctx->max_tiles) ctx->max_tiles = h->n_tiles + h->n_tiles / 2;
+    long long nt = (long long)h->n_tiles + h->n_tiles_clip;
+    if (nt > ctx->max_tiles) ctx->max_tiles = (int)(nt + nt / 2 < (1ll << 30) ? nt + nt / 2 : (1 << 30));
 }
 
 static int read_stat(fa_ctx* ctx, cudaStream_t s) {
@@ -277,13 +299,14 @@ static int launch_depth(fa_ctx* ctx, int W, int H, int cull, unsigned char* flag
                                    P<unsigned long long>(ctx->depth_keys), nullptr, P<SmallRec>(ctx->small_rec),
                                    P<int>(ctx->clip_list), P<TriSetup>(ctx->large), ctx->max_large,
                                    P<int4>(ctx->tiles), ctx->max_tiles, P<fa_dstat>(ctx->dstat), s, nullptr, nullptr,
-                                   nullptr);
+                                   nullptr, nullptr, nullptr);
     return FA_OK;
 }
 
 // side stream and fork/join events (created on first use)
 static int ensure_side(fa_ctx* ctx) {
     if (!ctx->side) CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    if (!ctx->side2) CK(cudaStreamCreateWithFlags(&ctx->side2, cudaStreamNonBlocking));
     for (cudaEvent_t& e : ctx->fj)
         if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     return FA_OK;
@@ -352,7 +375,7 @@ int fa_mark_visible(fa_ctx* ctx, const double* vp_host, const double* depth, int
         fa_launch_depth_pass(false, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, width, height,
                              backface_cull, nullptr, nullptr, P<SmallRec>(ctx->small_rec), P<int>(ctx->clip_list),
                              P<TriSetup>(ctx->large), ctx->max_large, P<int4>(ctx->tiles), ctx->max_tiles,
-                             P<fa_dstat>(ctx->dstat), s, nullptr, nullptr, nullptr);
+                             P<fa_dstat>(ctx->dstat), s, nullptr, nullptr, nullptr, nullptr, nullptr);
         fa_launch_depth_hiz(P<unsigned long long>(ctx->depth_keys), nullptr, width, height,
                             P<unsigned long long>(ctx->hiz), nullptr, nullptr, s);
         fa_launch_raster_vis(P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large), P<int4>(ctx->tiles),
@@ -680,8 +703,8 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     nl += fa_launch_depth_pass(true, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, W, H,
                                p->backface_cull, P<unsigned long long>(ctx->depth_keys), wid,
                                P<SmallRec>(ctx->small_rec), P<int>(ctx->clip_list), P<TriSetup>(ctx->large),
-                               ctx->max_large, P<int4>(ctx->tiles), ctx->max_tiles, st, s, ctx->side, ctx->fj[0],
-                               ctx->fj[1]);
+                               ctx->max_large, P<int4>(ctx->tiles), ctx->max_tiles, st, s, ctx->side, ctx->side2,
+                               ctx->fj[0], ctx->fj[1], ctx->fj[7]);
     fa_launch_depth_hiz(P<unsigned long long>(ctx->depth_keys), wid, W, H, P<unsigned long long>(ctx->hiz), flags, st,
                         s);
     nl += 1;
@@ -920,6 +943,16 @@ int fa_frame_download(fa_ctx* ctx, const fa_frame_result* res, int32_t* chart_of
 }
 
 int fa_last_launch_count(fa_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
+
+int fa_frame_counters(fa_ctx* ctx, int64_t* out, int max) {
+    if (!ctx || !out || !ctx->hstat) return 0;
+    const fa_dstat* h = ctx->hstat;
+    const int64_t v[8] = {h->n_small3, h->n_large3, h->n_clip, h->n_large, h->n_tiles, h->n_vis, h->n_charts,
+                          h->screen_fragments};
+    int n = max < 8 ? max : 8;
+    for (int i = 0; i < n; i++) out[i] = v[i];
+    return n;
+}
 
 static const char* kStageNames[] = {"project+clear", "depth pass",   "visibility pass", "visible compaction",
                                     "union-find",    "chart roots",  "bounds+dims",     "order",

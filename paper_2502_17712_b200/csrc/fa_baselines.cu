@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(BL_THREADS) k_seq_candidates(const long long* 
                                                                long long* __restrict__ cand,
                                                                const unsigned* __restrict__ done,
                                                                int* __restrict__ rows_out) {
+    FA_PDL_PROLOGUE();
     extern __shared__ int dyn_front[];
     __shared__ long long red[33];
     __shared__ int s_rows;
@@ -123,6 +124,7 @@ __global__ void __launch_bounds__(BL_THREADS) k_seq_candidates(const long long* 
 }
 
 __global__ void k_seq_batch_done(const long long* __restrict__ cand, long long lo, long long hi, unsigned* done) {
+    FA_PDL_PROLOGUE();
     bool any = false;
     for (long long i = lo + threadIdx.x; i <= hi; i += blockDim.x) any |= cand[SEQ_REC * (i - 1)] != 0;
     if (__syncthreads_or(any) && threadIdx.x == 0) *done = 1;
@@ -135,6 +137,7 @@ __global__ void __launch_bounds__(1024) k_seq_select(const long long* __restrict
                                                      const int* __restrict__ cw, const int* __restrict__ ch,
                                                      const int* __restrict__ cx, const int* __restrict__ cy,
                                                      long long* __restrict__ placements, long long* __restrict__ out) {
+    FA_PDL_PROLOGUE();
     __shared__ long long red[33];
     long long best = 0;
     for (long long i = threadIdx.x + 1; i <= n_scales; i += blockDim.x)
@@ -176,6 +179,7 @@ __device__ __forceinline__ int sb_probe(const int* sh_h, const int* sh_cur, int 
 __global__ void k_superblock(const long long* __restrict__ ow, const long long* __restrict__ oh, int n,
                              long long omega, int block0, int* __restrict__ state, size_t state_stride,
                              int* __restrict__ out_xywh, size_t out_stride, int* __restrict__ level_ok) {
+    FA_PDL_PROLOGUE();
     int L = blockIdx.x;
     int block = block0 >> L;
     int lane = threadIdx.x;
@@ -260,6 +264,7 @@ __global__ void k_superblock_select(const long long* __restrict__ tw, const long
                                     const int* __restrict__ perm, int n, int n_levels, const int* __restrict__ xywh,
                                     size_t out_stride, const int* __restrict__ level_ok,
                                     long long* __restrict__ placements, long long* __restrict__ out) {
+    FA_PDL_PROLOGUE();
     __shared__ int s_level;
     __shared__ unsigned long long s_best;
     if (threadIdx.x == 0) {
@@ -315,14 +320,15 @@ void fa_launch_seq_search(const long long* ow, const long long* oh, int n, long 
     for (long long hi = n_scales; hi >= 1; hi -= batch) {
         long long lo = hi - batch + 1;
         if (lo < 1) lo = 1;
-        k_seq_candidates<<<(int)(hi - lo + 1), BL_THREADS, dyn, s>>>(ow, oh, n, omega, n_scales, hi, min_dim, pad, cw,
+        fa_launch(k_seq_candidates, (int)(hi - lo + 1), BL_THREADS, dyn, s, ow, oh, n, omega, n_scales, hi, min_dim, pad, cw,
                                                                    ch, cx, cy, rowstart, gfront, cand, done, nullptr);
-        if (lo > 1) k_seq_batch_done<<<1, 256, 0, s>>>(cand, lo, hi, done);
+        if (lo > 1) fa_launch(k_seq_batch_done, 1, 256, 0, s, cand, lo, hi, done);
     }
 }
 
 __global__ void k_widen3(const int* __restrict__ a, const int* __restrict__ b, const int* __restrict__ c, int n,
                          long long* __restrict__ oa, long long* __restrict__ ob, long long* __restrict__ oc) {
+    FA_PDL_PROLOGUE();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         oa[i] = a[i];
         ob[i] = b[i];
@@ -341,23 +347,23 @@ void fa_launch_seq_single(const long long* w, const long long* h, int n, long lo
         cudaFuncSetAttribute(k_seq_candidates, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
-    k_seq_candidates<<<1, BL_THREADS, dyn, s>>>(w, h, n, omega, 1, 1, 1, 0, cw, ch, cx, cy, rowstart, gfront, cand,
+    fa_launch(k_seq_candidates, 1, BL_THREADS, dyn, s, w, h, n, omega, 1, 1, 1, 0, cw, ch, cx, cy, rowstart, gfront, cand,
                                                done_zero, rows);
-    k_widen3<<<fa_grid(n, 256, FA_NUM_SMS), 256, 0, s>>>(rows, cx, cy, n, rows_out, x_out, y_out);
+    fa_launch(k_widen3, fa_grid(n, 256, FA_NUM_SMS), 256, 0, s, rows, cx, cy, n, rows_out, x_out, y_out);
 }
 
 void fa_launch_seq_select(const long long* tw, const long long* th, const long long* cid, const unsigned char* rot,
                           const int* perm, int n, long long n_scales, const long long* cand, const int* cw,
                           const int* ch, const int* cx, const int* cy, long long* placements, long long* out,
                           cudaStream_t s) {
-    k_seq_select<<<1, 1024, 0, s>>>(tw, th, cid, rot, perm, n, n_scales, cand, cw, ch, cx, cy, placements, out);
+    fa_launch(k_seq_select, 1, 1024, 0, s, tw, th, cid, rot, perm, n, n_scales, cand, cw, ch, cx, cy, placements, out);
 }
 
 void fa_launch_superblock(const long long* ow, const long long* oh, const long long* tw, const long long* th,
                           const long long* cid, const unsigned char* rot, const int* perm, int n, long long omega,
                           int block0, int n_levels, int* state, size_t state_stride, int* xywh, size_t out_stride,
                           int* level_ok, long long* placements, long long* out, cudaStream_t s) {
-    k_superblock<<<n_levels, 32, 0, s>>>(ow, oh, n, omega, block0, state, state_stride, xywh, out_stride, level_ok);
-    k_superblock_select<<<1, 256, 0, s>>>(tw, th, cid, rot, perm, n, n_levels, xywh, out_stride, level_ok, placements,
+    fa_launch(k_superblock, n_levels, 32, 0, s, ow, oh, n, omega, block0, state, state_stride, xywh, out_stride, level_ok);
+    fa_launch(k_superblock_select, 1, 256, 0, s, tw, th, cid, rot, perm, n, n_levels, xywh, out_stride, level_ok, placements,
                                           out);
 }

@@ -127,6 +127,7 @@ __global__ void __launch_bounds__(256) k_chart_bounds(const double4* __restrict_
                                                       const int* __restrict__ cidx,
                                                       unsigned long long* __restrict__ keys,
                                                       int* __restrict__ survived, const fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
     int n = st->n_vis;
     int lane = lane_id();
     int stride = gridDim.x * blockDim.x;
@@ -190,6 +191,7 @@ __global__ void k_box_dims(const unsigned long long* __restrict__ keys, const in
                            int* __restrict__ px, long long* __restrict__ target, long long* __restrict__ otw,
                            long long* __restrict__ oth, long long* __restrict__ cid, int cap,
                            fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
     int n = st->n_charts;
     int stride = gridDim.x * blockDim.x;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
@@ -224,20 +226,21 @@ __global__ void k_box_dims(const unsigned long long* __restrict__ keys, const in
 void fa_launch_chart_bounds(const double4* clip, const int* tris, const int* vis_list, const int* label,
                             const int* cidx, int T, unsigned long long* ndc_keys, int* survived, const fa_dstat* st,
                             cudaStream_t s) {
-    k_chart_bounds<<<fa_grid(T, 256, FA_NUM_SMS * 8), 256, 0, s>>>(clip, tris, vis_list, label, cidx, ndc_keys,
+    fa_launch(k_chart_bounds, fa_grid(T, 256, FA_NUM_SMS * 8), 256, 0, s, clip, tris, vis_list, label, cidx, ndc_keys,
                                                                    survived, st);
 }
 
 void fa_launch_box_dims(const unsigned long long* ndc_keys, const int* survived, const int* roots, int T, int W, int H,
                         double prescale, double* ndc, int* px, long long* target, long long* tw, long long* th,
                         long long* cid, int cap, fa_dstat* st, cudaStream_t s) {
-    k_box_dims<<<fa_grid(T, 256, FA_NUM_SMS * 4), 256, 0, s>>>(ndc_keys, survived, roots, W, H, prescale, ndc, px,
+    fa_launch(k_box_dims, fa_grid(T, 256, FA_NUM_SMS * 4), 256, 0, s, ndc_keys, survived, roots, W, H, prescale, ndc, px,
                                                                target, tw, th, cid, cap, st);
 }
 
 // ---- batched standalone API kernels -------------------------------------------
 // blinn_clamped_ndc (geometry.py:185-200) over n homogeneous points
 __global__ void k_blinn_points(const double* __restrict__ p4, int n, double* __restrict__ out) {
+    FA_PDL_PROLOGUE();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         NBox b = empty_box();
         blinn_add(p4[4 * i], p4[4 * i + 1], p4[4 * i + 3], b);
@@ -248,6 +251,7 @@ __global__ void k_blinn_points(const double* __restrict__ p4, int n, double* __r
 
 // select_side_plane over n homogeneous triangles (n,3,4)
 __global__ void k_select_side_plane(const double* __restrict__ t12, int n, int* __restrict__ out) {
+    FA_PDL_PROLOGUE();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         double4 c[3];
 #pragma unroll
@@ -261,6 +265,7 @@ __global__ void k_select_side_plane(const double* __restrict__ t12, int n, int* 
 // chart_bbox (geometry.py:281-322) over n world triangles (n,3,3)
 __global__ void k_chart_bbox_world(const double* __restrict__ xyz, int n, const double* __restrict__ vp,
                                    unsigned long long* __restrict__ keys, int* __restrict__ surv) {
+    FA_PDL_PROLOGUE();
     double m[16];
 #pragma unroll
     for (int i = 0; i < 16; i++) m[i] = vp[i];
@@ -280,17 +285,20 @@ __global__ void k_chart_bbox_world(const double* __restrict__ xyz, int n, const 
 }
 
 __global__ void k_init_box_keys(unsigned long long* keys, int* surv) {
+    FA_PDL_PROLOGUE();
     keys[0] = keys[1] = FA_KEY_POS_INF;
     keys[2] = keys[3] = FA_KEY_NEG_INF;
     *surv = 0;
 }
 
 __global__ void k_decode_box(const unsigned long long* keys, double* out) {
+    FA_PDL_PROLOGUE();
     if (threadIdx.x < 4) out[threadIdx.x] = key_f64(keys[threadIdx.x]);
 }
 
 // viewport_box (geometry.py:352-362) over n boxes
 __global__ void k_viewport_box(const double* __restrict__ box, int n, int W, int H, long long* __restrict__ out) {
+    FA_PDL_PROLOGUE();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         double fw = ceil(__dmul_rn(__ddiv_rn(__dsub_rn(box[4 * i + 2], box[4 * i]), 2.0), (double)W));
         double fh = ceil(__dmul_rn(__ddiv_rn(__dsub_rn(box[4 * i + 3], box[4 * i + 1]), 2.0), (double)H));
@@ -300,17 +308,17 @@ __global__ void k_viewport_box(const double* __restrict__ box, int n, int W, int
 }
 
 void fa_launch_blinn_points(const double* p4, int n, double* out, cudaStream_t s) {
-    k_blinn_points<<<fa_grid(n, 256, FA_NUM_SMS * 4), 256, 0, s>>>(p4, n, out);
+    fa_launch(k_blinn_points, fa_grid(n, 256, FA_NUM_SMS * 4), 256, 0, s, p4, n, out);
 }
 void fa_launch_select_side_plane(const double* t12, int n, int* out, cudaStream_t s) {
-    k_select_side_plane<<<fa_grid(n, 256, FA_NUM_SMS * 4), 256, 0, s>>>(t12, n, out);
+    fa_launch(k_select_side_plane, fa_grid(n, 256, FA_NUM_SMS * 4), 256, 0, s, t12, n, out);
 }
 void fa_launch_chart_bbox_world(const double* xyz, int n, const double* vp, unsigned long long* keys, int* surv,
                                 double* box_out, cudaStream_t s) {
-    k_init_box_keys<<<1, 1, 0, s>>>(keys, surv);
-    k_chart_bbox_world<<<fa_grid(n, 256, FA_NUM_SMS * 4), 256, 0, s>>>(xyz, n, vp, keys, surv);
-    k_decode_box<<<1, 32, 0, s>>>(keys, box_out);
+    fa_launch(k_init_box_keys, 1, 1, 0, s, keys, surv);
+    fa_launch(k_chart_bbox_world, fa_grid(n, 256, FA_NUM_SMS * 4), 256, 0, s, xyz, n, vp, keys, surv);
+    fa_launch(k_decode_box, 1, 32, 0, s, keys, box_out);
 }
 void fa_launch_viewport_box(const double* box, int n, int W, int H, long long* out, cudaStream_t s) {
-    k_viewport_box<<<fa_grid(n, 256, FA_NUM_SMS * 4), 256, 0, s>>>(box, n, W, H, out);
+    fa_launch(k_viewport_box, fa_grid(n, 256, FA_NUM_SMS * 4), 256, 0, s, box, n, W, H, out);
 }

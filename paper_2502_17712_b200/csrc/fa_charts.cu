@@ -36,6 +36,7 @@ __device__ __forceinline__ int block_prefix_of(const int* blocks, int b, int* sm
 // ---- visible compaction ----------------------------------------------------
 __global__ void __launch_bounds__(CMP_THREADS) k_count_flags(const unsigned char* __restrict__ flags, int T,
                                                              int* __restrict__ blocks) {
+    FA_PDL_PROLOGUE();
     __shared__ int sm[32];
     int base = blockIdx.x * CMP_TILE + threadIdx.x * CMP_ITEMS;
     int c = 0;
@@ -62,6 +63,7 @@ __global__ void __launch_bounds__(CMP_THREADS) k_scatter_visible(const unsigned 
                                                                  int* __restrict__ vis_list, int* __restrict__ label,
                                                                  const int* __restrict__ tris, int* __restrict__ vmin,
                                                                  fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
     __shared__ int sm[32];
     int offset = block_prefix_of(blocks, blockIdx.x, sm);
     int base = blockIdx.x * CMP_TILE + threadIdx.x * CMP_ITEMS;
@@ -111,8 +113,8 @@ __global__ void __launch_bounds__(CMP_THREADS) k_scatter_visible(const unsigned 
 void fa_launch_compact_visible(const unsigned char* flags, int T, int* blocks, int* vis_list, int* label,
                                fa_dstat* st, cudaStream_t s, const int* tris, int* vmin) {
     int nb = fa_compact_blocks(T);
-    k_count_flags<<<nb, CMP_THREADS, 0, s>>>(flags, T, blocks);
-    k_scatter_visible<<<nb, CMP_THREADS, 0, s>>>(flags, T, blocks, nb, vis_list, label, tris, vmin, st);
+    fa_launch(k_count_flags, nb, CMP_THREADS, 0, s, flags, T, blocks);
+    fa_launch(k_scatter_visible, nb, CMP_THREADS, 0, s, flags, T, blocks, nb, vis_list, label, tris, vmin, st);
 }
 
 // ---- union-find ---------------------------------------------------------------
@@ -202,6 +204,7 @@ __device__ __forceinline__ void uf_union(int* parent, int a, int b) {
 
 __global__ void k_vmin(const int* __restrict__ tris, const int* __restrict__ vis_list, int* __restrict__ vmin,
                        const fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
     int n = st->n_vis;
     int stride = gridDim.x * blockDim.x;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
@@ -227,6 +230,7 @@ __global__ void k_vmin(const int* __restrict__ tris, const int* __restrict__ vis
 // valid union (parent[r] = m < r keeps the min-rooted forest).
 __global__ void k_hook_multi(const int* __restrict__ tris, const int* __restrict__ vis_list,
                              const int* __restrict__ vmin, int* label, const fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
     int n = st->n_vis;
     int stride = gridDim.x * blockDim.x;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
@@ -267,6 +271,7 @@ __global__ void k_hook_multi(const int* __restrict__ tris, const int* __restrict
 
 __global__ void k_hook_edges(const int* __restrict__ adj, const unsigned char* __restrict__ flags,
                              const int* __restrict__ vis_list, int* label, const fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
     int n = st->n_vis;
     int stride = gridDim.x * blockDim.x;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
@@ -281,6 +286,7 @@ __global__ void k_hook_edges(const int* __restrict__ adj, const unsigned char* _
 
 __global__ void k_hook_labels(const int* __restrict__ labels_in, const int* __restrict__ vis_list, int* label,
                               const fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
     int n = st->n_vis;
     int stride = gridDim.x * blockDim.x;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
@@ -291,6 +297,7 @@ __global__ void k_hook_labels(const int* __restrict__ labels_in, const int* __re
 }
 
 __global__ void k_compress(const int* __restrict__ vis_list, int* label, const fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
     int n = st->n_vis;
     int stride = gridDim.x * blockDim.x;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
@@ -300,11 +307,13 @@ __global__ void k_compress(const int* __restrict__ vis_list, int* label, const f
 }
 
 __global__ void k_iota(int* a, int n) {
+    FA_PDL_PROLOGUE();
     int stride = gridDim.x * blockDim.x;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) a[i] = i;
 }
 
 __global__ void k_fill(int* a, int n, int v) {
+    FA_PDL_PROLOGUE();
     int stride = gridDim.x * blockDim.x;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) a[i] = v;
 }
@@ -313,6 +322,7 @@ __global__ void k_fill(int* a, int n, int v) {
 // (charts.py:396-402).  tmp must be pre-filled with INT_MAX.
 __global__ void k_canon_min(const int* __restrict__ vis_list, const int* __restrict__ label, int* tmp,
                             const fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
     int n = st->n_vis;
     int stride = gridDim.x * blockDim.x;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
@@ -322,12 +332,14 @@ __global__ void k_canon_min(const int* __restrict__ vis_list, const int* __restr
 }
 
 __global__ void k_canon_apply(const unsigned char* __restrict__ flags, int* label, const int* __restrict__ tmp, int T) {
+    FA_PDL_PROLOGUE();
     int stride = gridDim.x * blockDim.x;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += stride)
         label[t] = flags[t] ? tmp[label[t]] : -1;
 }
 
 __global__ void k_v2c(const int* __restrict__ vmin, const int* __restrict__ label, int* __restrict__ v2c, int V) {
+    FA_PDL_PROLOGUE();
     int stride = gridDim.x * blockDim.x;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += stride) {
         int m = vmin[v];
@@ -336,6 +348,7 @@ __global__ void k_v2c(const int* __restrict__ vmin, const int* __restrict__ labe
 }
 
 __global__ void k_flags_from_labels(const int* __restrict__ labels, unsigned char* __restrict__ flags, int T) {
+    FA_PDL_PROLOGUE();
     int stride = gridDim.x * blockDim.x;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += stride) flags[t] = labels[t] >= 0;
 }
@@ -368,6 +381,7 @@ __device__ __forceinline__ unsigned long long edge_hash(unsigned long long k) {
 __global__ void k_adj_insert(const int* __restrict__ tris, int n_codes, unsigned long long* __restrict__ keys,
                              int* __restrict__ cnt, int* __restrict__ c0, int* __restrict__ c1,
                              unsigned long long mask) {
+    FA_PDL_PROLOGUE();
     for (int code = blockIdx.x * blockDim.x + threadIdx.x; code < n_codes; code += gridDim.x * blockDim.x) {
         unsigned long long key = edge_key(tris, code);
         unsigned long long h = edge_hash(key) & mask;
@@ -385,6 +399,7 @@ __global__ void k_adj_insert(const int* __restrict__ tris, int n_codes, unsigned
 __global__ void k_adj_resolve(const int* __restrict__ tris, int n_codes, const unsigned long long* __restrict__ keys,
                               const int* __restrict__ cnt, const int* __restrict__ c0, const int* __restrict__ c1,
                               unsigned long long mask, int* __restrict__ adj) {
+    FA_PDL_PROLOGUE();
     for (int code = blockIdx.x * blockDim.x + threadIdx.x; code < n_codes; code += gridDim.x * blockDim.x) {
         unsigned long long key = edge_key(tris, code);
         unsigned long long h = edge_hash(key) & mask;
@@ -404,59 +419,60 @@ void fa_launch_build_adjacency(const int* tris, int T, unsigned long long* keys,
     cudaMemsetAsync(keys, 0xff, table_size * sizeof(unsigned long long), s);
     cudaMemsetAsync(cnt, 0, table_size * sizeof(int), s);
     int grid = fa_grid(n, 256, FA_NUM_SMS * 8);
-    k_adj_insert<<<grid, 256, 0, s>>>(tris, n, keys, cnt, c0, c1, table_size - 1);
-    k_adj_resolve<<<grid, 256, 0, s>>>(tris, n, keys, cnt, c0, c1, table_size - 1, adj);
+    fa_launch(k_adj_insert, grid, 256, 0, s, tris, n, keys, cnt, c0, c1, table_size - 1);
+    fa_launch(k_adj_resolve, grid, 256, 0, s, tris, n, keys, cnt, c0, c1, table_size - 1, adj);
 }
 
 int fa_launch_uf_vertex(const int* tris, const int* vis_list, int* vmin, int* label, int T, const fa_dstat* st,
                         cudaStream_t s, bool vmin_ready) {
-    if (!vmin_ready) k_vmin<<<uf_grid(T), 256, 0, s>>>(tris, vis_list, vmin, st);
-    k_hook_multi<<<uf_grid(T), 256, 0, s>>>(tris, vis_list, vmin, label, st);
+    if (!vmin_ready) fa_launch(k_vmin, uf_grid(T), 256, 0, s, tris, vis_list, vmin, st);
+    fa_launch(k_hook_multi, uf_grid(T), 256, 0, s, tris, vis_list, vmin, label, st);
     return vmin_ready ? 1 : 2;
 }
 
 void fa_launch_uf_edges(const int* adjacency, const unsigned char* flags, const int* vis_list, int* label, int T,
                         const fa_dstat* st, cudaStream_t s) {
-    k_hook_edges<<<uf_grid(T), 256, 0, s>>>(adjacency, flags, vis_list, label, st);
+    fa_launch(k_hook_edges, uf_grid(T), 256, 0, s, adjacency, flags, vis_list, label, st);
 }
 
-void fa_launch_iota(int* label, int T, cudaStream_t s) { k_iota<<<uf_grid(T), 256, 0, s>>>(label, T); }
+void fa_launch_iota(int* label, int T, cudaStream_t s) { fa_launch(k_iota, uf_grid(T), 256, 0, s, label, T); }
 
 // union(t, labels_in[t]) for every visible t (charts.py:372-374); run after
 // fa_launch_uf_vertex, whose initialisation overwrites parent pointers
 void fa_launch_uf_labels(const int* labels_in, const int* vis_list, int* label, int T, const fa_dstat* st,
                          cudaStream_t s) {
-    k_hook_labels<<<uf_grid(T), 256, 0, s>>>(labels_in, vis_list, label, st);
+    fa_launch(k_hook_labels, uf_grid(T), 256, 0, s, labels_in, vis_list, label, st);
 }
 
 void fa_launch_uf_compress(const int* vis_list, int* label, int T, const fa_dstat* st, cudaStream_t s) {
-    k_compress<<<uf_grid(T), 256, 0, s>>>(vis_list, label, st);
+    fa_launch(k_compress, uf_grid(T), 256, 0, s, vis_list, label, st);
 }
 
 void fa_launch_canonicalize(const int* vis_list, int* label, int* tmp, int T, const fa_dstat* st, cudaStream_t s) {
     // label holds roots for visible triangles; flags are recovered from the vis list
-    k_fill<<<uf_grid(T), 256, 0, s>>>(tmp, T, 0x7fffffff);
-    k_canon_min<<<uf_grid(T), 256, 0, s>>>(vis_list, label, tmp, st);
+    fa_launch(k_fill, uf_grid(T), 256, 0, s, tmp, T, 0x7fffffff);
+    fa_launch(k_canon_min, uf_grid(T), 256, 0, s, vis_list, label, tmp, st);
 }
 
 void fa_launch_canon_apply(const unsigned char* flags, int* label, const int* tmp, int T, cudaStream_t s) {
-    k_canon_apply<<<uf_grid(T), 256, 0, s>>>(flags, label, tmp, T);
+    fa_launch(k_canon_apply, uf_grid(T), 256, 0, s, flags, label, tmp, T);
 }
 
 void fa_launch_v2c(const int* vmin, const int* label, int* v2c, int V, cudaStream_t s) {
-    k_v2c<<<fa_grid(V, 256, FA_NUM_SMS * 8), 256, 0, s>>>(vmin, label, v2c, V);
+    fa_launch(k_v2c, fa_grid(V, 256, FA_NUM_SMS * 8), 256, 0, s, vmin, label, v2c, V);
 }
 
 void fa_launch_flags_from_labels(const int* labels, unsigned char* flags, int T, cudaStream_t s) {
-    k_flags_from_labels<<<uf_grid(T), 256, 0, s>>>(labels, flags, T);
+    fa_launch(k_flags_from_labels, uf_grid(T), 256, 0, s, labels, flags, T);
 }
 
-void fa_launch_fill(int* a, int n, int v, cudaStream_t s) { k_fill<<<uf_grid(n), 256, 0, s>>>(a, n, v); }
+void fa_launch_fill(int* a, int n, int v, cudaStream_t s) { fa_launch(k_fill, uf_grid(n), 256, 0, s, a, n, v); }
 
 // ---- chart roots: ordered compaction of label[t] == t over the vis list -------
 __global__ void __launch_bounds__(CMP_THREADS) k_count_roots(const int* __restrict__ vis_list,
                                                              const int* __restrict__ label, int* __restrict__ blocks,
                                                              const fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
     __shared__ int sm[32];
     int n = st->n_vis;
     int base = blockIdx.x * CMP_TILE + threadIdx.x * CMP_ITEMS;
@@ -485,6 +501,7 @@ __global__ void __launch_bounds__(CMP_THREADS) k_scatter_roots(const int* __rest
                                                                int* __restrict__ roots, int* __restrict__ cidx,
                                                                unsigned long long* __restrict__ ndc_keys,
                                                                int* __restrict__ survived, fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
     __shared__ int sm[32];
     int n = st->n_vis;
     int last = (n + CMP_TILE - 1) / CMP_TILE - 1;
@@ -524,6 +541,6 @@ __global__ void __launch_bounds__(CMP_THREADS) k_scatter_roots(const int* __rest
 void fa_launch_compact_roots(const int* vis_list, const int* label, int T, int* blocks, int* roots, int* cidx,
                              unsigned long long* ndc_keys, int* survived, fa_dstat* st, cudaStream_t s) {
     int nb = fa_compact_blocks(T);
-    k_count_roots<<<nb, CMP_THREADS, 0, s>>>(vis_list, label, blocks, st);
-    k_scatter_roots<<<nb, CMP_THREADS, 0, s>>>(vis_list, label, blocks, nb, roots, cidx, ndc_keys, survived, st);
+    fa_launch(k_count_roots, nb, CMP_THREADS, 0, s, vis_list, label, blocks, st);
+    fa_launch(k_scatter_roots, nb, CMP_THREADS, 0, s, vis_list, label, blocks, nb, roots, cidx, ndc_keys, survived, st);
 }

@@ -56,7 +56,8 @@ struct fa_dstat {
     double stretch_wsum;  // sum area * (S1^2 + S2^2) / 2   (metrics.py:103)
     double stretch_area;  // sum area                       (metrics.py:104)
     unsigned long long stretch_linf_bits;  // max S1 (positive double bits)
-    int pad[34];
+    int n_tiles_clip;     // tiles of clipped (generic) setups, stored downward from max_tiles - 1
+    int pad[33];
 };
 static_assert(sizeof(fa_dstat) == 256, "fa_dstat is one 256-byte block");
 
@@ -209,7 +210,50 @@ __device__ __forceinline__ long long block_sum_ll(long long v, long long* smem32
     return smem32[32];
 }
 
+// ---- programmatic dependent launch (PDL) ---------------------------------
+// Frame kernels are launched with programmatic stream serialization, so a
+// kernel's CTAs are scheduled while its predecessor drains instead of after
+// it.  Every such kernel starts with FA_PDL_PROLOGUE(): wait until the
+// predecessor grid has completed and its writes are visible (before ANY
+// global read or write), then let the successor be scheduled.  Both are
+// no-ops when the kernel was launched without the attribute.
+__device__ __forceinline__ void fa_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void fa_pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#define FA_PDL_PROLOGUE() \
+    do {                  \
+        fa_pdl_wait();    \
+        fa_pdl_trigger(); \
+    } while (0)
+
+bool fa_pdl_enabled();  // FASTATLAS_PDL=0 disables (fa_api.cu)
+
+template <typename... KArgs, typename... Args>
+static inline void fa_launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                             Args... args) {
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    a[0].val.programmaticStreamSerializationAllowed = fa_pdl_enabled() ? 1 : 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = a;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
+// Grid-stride kernels cap their grid at a multiple of the SM count; the cap
+// scale (FASTATLAS_GRID_CAP, default 1) trades single-frame latency for room
+// that concurrent frames' kernels can share.
+float fa_grid_cap_scale();
+static inline int fa_cap(int max_blocks) {
+    int c = (int)(max_blocks * fa_grid_cap_scale());
+    return c > 0 ? c : 1;
+}
+
 static inline int fa_grid(long long n, int block, int max_blocks) {
+    max_blocks = fa_cap(max_blocks);
     long long g = (n + block - 1) / block;
     if (g < 1) g = 1;
     if (g > max_blocks) g = max_blocks;

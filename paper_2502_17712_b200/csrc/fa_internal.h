@@ -67,8 +67,8 @@ struct fa_ctx {
     int n_stage_marks = 0;
 
     // side stream + fork/join events for the independent raster branches
-    cudaStream_t side = nullptr;
-    cudaEvent_t fj[8] = {};
+    cudaStream_t side = nullptr, side2 = nullptr;
+    cudaEvent_t fj[12] = {};
 };
 
 // growth helper: ensures buf has >= bytes; returns false on allocation failure
@@ -84,7 +84,8 @@ void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* c
 int fa_launch_depth_pass(bool write_depth, const double4* clip, const double4* scr, const int* tris, int T, int W,
                          int H, int cull, unsigned long long* depth, unsigned long long* wid, SmallRec* small_rec,
                          int* clip_list, TriSetup* large, int max_large, int4* tiles, int max_tiles, fa_dstat* st,
-                         cudaStream_t s, cudaStream_t side, cudaEvent_t ev_fork, cudaEvent_t ev_join);
+                         cudaStream_t s, cudaStream_t side, cudaStream_t side2, cudaEvent_t ev_fork,
+                         cudaEvent_t ev_join, cudaEvent_t ev_join2);
 int fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const int4* tiles, int max_tiles,
                          int max_large, int T, int W, const unsigned long long* depth, const unsigned long long* hiz,
                          unsigned char* flags, const fa_dstat* st, cudaStream_t s, cudaStream_t side,

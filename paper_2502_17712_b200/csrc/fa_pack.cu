@@ -158,6 +158,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_orient_sort(const long long* _
                                                               unsigned char* __restrict__ rot, int* __restrict__ perm,
                                                               int* __restrict__ pinv, unsigned long long* sk,
                                                               int* sv, int reject_dups, fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
     __shared__ SortSmem sm;
     int n = n_dev ? *n_dev : n_max;
     if (n > n_max) {
@@ -522,6 +523,7 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack(const long long* __restrict
                                                      int* __restrict__ cand_h, int* __restrict__ cand_y,
                                                      int* __restrict__ rowstart, int* __restrict__ gfront,
                                                      fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
     extern __shared__ int dyn_front[];
     __shared__ PackSmem sm;
     int n = n_dev ? *n_dev : n_max;
@@ -562,6 +564,7 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack(const long long* __restrict
 
 // after a batch: done |= any accepted in [lo, hi]
 __global__ void k_batch_done(const long long* __restrict__ cand, long long lo, long long hi, fa_dstat* st) {
+    FA_PDL_PROLOGUE();
     bool any = false;
     for (long long i = lo + threadIdx.x; i <= hi; i += blockDim.x) any |= cand[CAND_REC * (i - 1)] != 0;
     if (__syncthreads_or(any) && threadIdx.x == 0) st->done = 1;
@@ -577,6 +580,7 @@ __global__ void __launch_bounds__(1024) k_select(const long long* __restrict__ o
                                                  const int* __restrict__ cand_w, const int* __restrict__ cand_h,
                                                  const int* __restrict__ cand_y, long long* __restrict__ placements,
                                                  unsigned char* __restrict__ accept_out, fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
     __shared__ long long red[33];
     __shared__ long long s_best;
     int n = n_dev ? *n_dev : n_max;
@@ -649,6 +653,7 @@ __global__ void __launch_bounds__(1024) k_select(const long long* __restrict__ o
 __global__ void __launch_bounds__(1024) k_fold(const long long* __restrict__ w, int n, long long omega,
                                                long long* __restrict__ rows, long long* __restrict__ xs,
                                                long long* __restrict__ m_out) {
+    FA_PDL_PROLOGUE();
     __shared__ long long red[33];
     int kbits = 63 - __clzll(omega);
     long long carry = 0, mloc = -(1ll << 62);
@@ -676,6 +681,7 @@ __global__ void __launch_bounds__(1024) k_push_up(const long long* __restrict__ 
                                                   int n, long long omega, int* __restrict__ rowstart,
                                                   long long* __restrict__ y, long long* __restrict__ used_out,
                                                   int* gfront) {
+    FA_PDL_PROLOGUE();
     extern __shared__ int dyn_front[];
     __shared__ long long red[33];
     int* front = gfront ? gfront : dyn_front;
@@ -732,6 +738,7 @@ __global__ void __launch_bounds__(1024) k_push_up(const long long* __restrict__ 
 __global__ void k_xywh(const long long* __restrict__ cand, const long long* __restrict__ cand_p,
                        const int* __restrict__ cand_w, const int* __restrict__ cand_h, const int* __restrict__ cand_y,
                        int n, long long omega, long long* __restrict__ out) {
+    FA_PDL_PROLOGUE();
     if (cand[0] == 0) return;
     int kbits = 63 - __clzll(omega);
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
@@ -759,14 +766,14 @@ static void ensure_smem_attr() {
 
 void fa_launch_orient_sort(const fa_pack_bufs& b, int n_max, const int* n_dev, long long max_h, fa_dstat* st,
                            cudaStream_t s) {
-    k_orient_sort<<<1, SORT_THREADS, 0, s>>>(b.tw, b.th, nullptr, n_max, n_dev, max_h, b.ow, b.oh, b.rot, b.perm,
+    fa_launch(k_orient_sort, 1, SORT_THREADS, 0, s, b.tw, b.th, nullptr, n_max, n_dev, max_h, b.ow, b.oh, b.rot, b.perm,
                                               b.pinv, b.sortk, b.sortv, 0, st);
 }
 
 void fa_launch_orient_sort_mt(const long long* tw, const long long* th, const long long* mt, int n, long long max_h,
                               long long* ow, long long* oh, unsigned char* rot, int* perm, int* pinv,
                               unsigned long long* sk, int* sv, int reject_dups, fa_dstat* st, cudaStream_t s) {
-    k_orient_sort<<<1, SORT_THREADS, 0, s>>>(tw, th, mt, n, nullptr, max_h, ow, oh, rot, perm, pinv, sk, sv,
+    fa_launch(k_orient_sort, 1, SORT_THREADS, 0, s, tw, th, mt, n, nullptr, max_h, ow, oh, rot, perm, pinv, sk, sv,
                                               reject_dups, st);
 }
 
@@ -782,16 +789,16 @@ int fa_launch_pack(const fa_pack_bufs& b, int n_max, const int* n_dev, long long
         long long lo = hi - batch + 1;
         if (lo < 1) lo = 1;
         int grid = (int)(hi - lo + 1);
-        k_pack<<<grid, PK_THREADS, dyn, s>>>(b.ow, b.oh, n_max, n_dev, omega, kbits, n_scales, hi, 0, 0, min_dim, pad,
+        fa_launch(k_pack, grid, PK_THREADS, dyn, s, b.ow, b.oh, n_max, n_dev, omega, kbits, n_scales, hi, 0, 0, min_dim, pad,
                                              b.cand, b.cand_p, b.cand_w, b.cand_h, b.cand_y, b.rowstart,
                                              smem_front ? nullptr : b.gfront, st);
         launches++;
         if (lo > 1) {
-            k_batch_done<<<1, 256, 0, s>>>(b.cand, lo, hi, st);
+            fa_launch(k_batch_done, 1, 256, 0, s, b.cand, lo, hi, st);
             launches++;
         }
     }
-    k_select<<<1, 1024, 0, s>>>(b.ow, b.tw, b.th, b.chart_id, b.rot, b.perm, n_max, n_dev, omega, n_scales, min_dim,
+    fa_launch(k_select, 1, 1024, 0, s, b.ow, b.tw, b.th, b.chart_id, b.rot, b.perm, n_max, n_dev, omega, n_scales, min_dim,
                                 pad, b.cand, b.cand_p, b.cand_w, b.cand_h, b.cand_y, b.placements, b.accept_out, st);
     return launches + 1;
 }
@@ -802,19 +809,19 @@ void fa_launch_pack_at_scale(const long long* ow, const long long* oh, int n, lo
     ensure_smem_attr();
     int kbits = 63 - __builtin_clzll((unsigned long long)omega);
     bool smem_front = front_smem(omega) <= kMaxFrontSmem;
-    k_pack<<<1, PK_THREADS, smem_front ? front_smem(omega) : 0, s>>>(ow, oh, n, nullptr, omega, kbits, 1, 1, num, den,
+    fa_launch(k_pack, 1, PK_THREADS, smem_front ? front_smem(omega) : 0, s, ow, oh, n, nullptr, omega, kbits, 1, 1, num, den,
                                                                      min_dim, pad, cand, cand_p, cand_w, cand_h, cand_y,
                                                                      rowstart, smem_front ? nullptr : gfront, nullptr);
 }
 
 void fa_launch_xywh(const long long* cand, const long long* cand_p, const int* cand_w, const int* cand_h,
                     const int* cand_y, int n, long long omega, long long* out, cudaStream_t s) {
-    k_xywh<<<fa_grid(n, 256, FA_NUM_SMS), 256, 0, s>>>(cand, cand_p, cand_w, cand_h, cand_y, n, omega, out);
+    fa_launch(k_xywh, fa_grid(n, 256, FA_NUM_SMS), 256, 0, s, cand, cand_p, cand_w, cand_h, cand_y, n, omega, out);
 }
 
 void fa_launch_fold(const long long* w, int n, long long omega, long long* rows, long long* x, long long* m,
                     cudaStream_t s) {
-    k_fold<<<1, 1024, 0, s>>>(w, n, omega, rows, x, m);
+    fa_launch(k_fold, 1, 1024, 0, s, w, n, omega, rows, x, m);
 }
 
 void fa_launch_push_up_impl(const long long* rows, const long long* x, const long long* w, const long long* h, int n,
@@ -822,7 +829,7 @@ void fa_launch_push_up_impl(const long long* rows, const long long* x, const lon
                             cudaStream_t s) {
     ensure_smem_attr();
     size_t dyn = gfront ? 0 : front_smem(omega);
-    k_push_up<<<1, 1024, dyn, s>>>(rows, x, w, h, n, omega, rowstart, y, used, gfront);
+    fa_launch(k_push_up, 1, 1024, dyn, s, rows, x, w, h, n, omega, rowstart, y, used, gfront);
 }
 
 bool fa_front_in_smem(long long omega) { return front_smem(omega) <= kMaxFrontSmem; }
@@ -830,6 +837,7 @@ bool fa_front_in_smem(long long omega) { return front_smem(omega) <= kMaxFrontSm
 // orient (packing.py:109-117): rotate boxes wider than tall
 __global__ void k_orient(const long long* __restrict__ tw, const long long* __restrict__ th, int n,
                          long long* __restrict__ ow, long long* __restrict__ oh, unsigned char* __restrict__ rot) {
+    FA_PDL_PROLOGUE();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         long long w = tw[i], h = th[i];
         bool r = w > h;
@@ -841,5 +849,5 @@ __global__ void k_orient(const long long* __restrict__ tw, const long long* __re
 
 void fa_launch_orient(const long long* tw, const long long* th, int n, long long* ow, long long* oh,
                       unsigned char* rot, cudaStream_t s) {
-    k_orient<<<fa_grid(n, 256, FA_NUM_SMS * 4), 256, 0, s>>>(tw, th, n, ow, oh, rot);
+    fa_launch(k_orient, fa_grid(n, 256, FA_NUM_SMS * 4), 256, 0, s, tw, th, n, ow, oh, rot);
 }

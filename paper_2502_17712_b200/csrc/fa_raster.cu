@@ -67,6 +67,7 @@ __global__ void k_frame_init(const double* __restrict__ pos, int V, const double
                              int* __restrict__ vmin, unsigned long long* __restrict__ depth,
                              unsigned long long* __restrict__ wid, long long npx,
                              unsigned int* __restrict__ flags32, int nflag32) {
+    FA_PDL_PROLOGUE();
     long long stride = (long long)gridDim.x * blockDim.x;
     long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     double m[16];
@@ -97,12 +98,14 @@ __global__ void k_frame_init(const double* __restrict__ pos, int V, const double
 
 // keys -> float64 depth (debug / standalone depth_prepass output)
 __global__ void k_decode_depth(const unsigned long long* __restrict__ keys, double* __restrict__ out, long long n) {
+    FA_PDL_PROLOGUE();
     long long stride = (long long)gridDim.x * blockDim.x;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = key_f64(keys[i]);
 }
 
 // float64 depth -> keys (standalone mark_visible input)
 __global__ void k_encode_depth(const double* __restrict__ in, unsigned long long* __restrict__ keys, long long n) {
+    FA_PDL_PROLOGUE();
     long long stride = (long long)gridDim.x * blockDim.x;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) keys[i] = f64_key(in[i]);
 }
@@ -124,6 +127,7 @@ __global__ void __launch_bounds__(SETUP_WARPS * 32) k_raster_setup(const double4
                                                       SmallRec* __restrict__ recs, int* __restrict__ clip_list,
                                                       int4* __restrict__ tiles, int max_tiles,
                                                       fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
     // per-warp counts -> per-warp bases; one atomic per counter per block step
     // (a same-address atomic per warp serialises ~30K times in the L2)
     __shared__ int s_cnt[4][SETUP_WARPS];
@@ -229,6 +233,7 @@ __global__ void __launch_bounds__(256) k_raster_clipped(const double4* __restric
                                                         TriSetup* __restrict__ large, int max_large,
                                                         int4* __restrict__ tiles, int max_tiles,
                                                         fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
     __shared__ TriSetup sm[8];
     const int warp = threadIdx.x >> 5, lane = lane_id();
     const int nwarps = gridDim.x * 8;
@@ -270,15 +275,19 @@ __global__ void __launch_bounds__(256) k_raster_clipped(const double4* __restric
                 }
             }
         } else {
+            // tiles of generic setups are stored downward from max_tiles - 1
+            // (k_raster_setup's unclipped tiles fill the front, and were all
+            // counted before this kernel started)
             const int nt = ((bw + TILE_W - 1) / TILE_W) * ((bh + TILE_H - 1) / TILE_H);
+            const int room = max_tiles - min(st->n_tiles, max_tiles);
             int base = 0;
-            if (lane == 0) base = atomicAdd(&st->n_tiles, nt);
+            if (lane == 0) base = atomicAdd(&st->n_tiles_clip, nt);
             base = __shfl_sync(0xffffffffu, base, 0);
-            // on overflow write the part that fits (no unwritten records below
-            // capacity) and flag the frame; the host grows the queue and reruns
-            if (base + nt > max_tiles && lane == 0) atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW);
+            // on overflow write the part that fits and flag the frame; the
+            // host grows the queue and reruns
+            if (base + nt > room && lane == 0) atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW);
             for (int k = lane; k < nt; k += 32)
-                if (base + k < max_tiles) tiles[base + k] = make_int4(-slot - 1, k, t, 0);
+                if (base + k < room) tiles[max_tiles - 1 - (base + k)] = make_int4(-slot - 1, k, t, 0);
         }
     }
 }
@@ -296,6 +305,7 @@ __global__ void __launch_bounds__(256) k_depth_hiz(const unsigned long long* __r
                                                    const unsigned long long* __restrict__ wid, int W, int H,
                                                    unsigned long long* __restrict__ hiz, int htx, int hty,
                                                    unsigned char* __restrict__ flags, fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
     // one thread per pixel column of a tile row (8 pixels tall): the loads of
     // a warp are 32 consecutive pixels of one image row; 8 consecutive lanes
     // form one tile and reduce its maximum with shuffles
@@ -369,17 +379,24 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const SmallRec* __re
                                                             unsigned long long* __restrict__ depth,
                                                             unsigned long long* __restrict__ wid,
                                                             fa_dstat* __restrict__ st, int max_tiles, int check,
-                                                            int tile_wid) {
+                                                            int tile_wid, int from_back) {
+    FA_PDL_PROLOGUE();
     __shared__ TriSetup sm[8];
     int warp = threadIdx.x >> 5, lane = lane_id();
     int nwarps = gridDim.x * 8;
-    int n_tiles = min(st->n_tiles, max_tiles);
+    // front: the unclipped tiles of k_raster_setup; back: the clipped
+    // (generic) setups' tiles of k_raster_clipped, stored downward
+    const int n_front = min(st->n_tiles, max_tiles);
+    const int n_tiles = from_back ? min(st->n_tiles_clip, max_tiles - n_front) : n_front;
+    const int4* tl = from_back ? tiles + (max_tiles - 1) : tiles;
+    const int dir = from_back ? -1 : 1;
     // descriptors are read one step ahead: a step waits for the record only
     int4 nxt = make_int4(0, 0, 0, 0);
-    if (blockIdx.x * 8 + warp < n_tiles) nxt = tiles[blockIdx.x * 8 + warp];
-    for (int w = blockIdx.x * 8 + warp; w < n_tiles; w += nwarps) {
+    const int w0 = (int)blockIdx.x * 8 + warp;
+    if (w0 < n_tiles) nxt = tl[dir * w0];
+    for (int w = w0; w < n_tiles; w += nwarps) {
         int4 rec = nxt;
-        if (w + nwarps < n_tiles) nxt = tiles[w + nwarps];
+        if (w + nwarps < n_tiles) nxt = tl[dir * (w + nwarps)];
         if (rec.x >= 0) {
             Setup3 f;
             int t;
@@ -422,45 +439,58 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const SmallRec* __re
 }
 
 // ---- small unclipped triangles: warp-cooperative sampling ------------------
-// A warp stages 32 records in shared memory, prefix-sums their bbox sample
+// A warp stages 32 records in shared memory, prefix-sums their window ROW
 // counts, and gives every lane one contiguous, equal chunk of the combined
-// sample space, so per-triangle size differences no longer diverge the warp.
-// Depth pass only (RED.MIN.64 per covered sample): the visibility pass stops
-// at a record's first passing sample, which an even split cannot exploit.
-#define COOP_WARPS 8
+// rows, so per-triangle size differences no longer diverge the warp.  Per row
+// only the conservative span (row_span) is tested exactly: a small record's
+// window averages ~20 samples for ~1.5 covered ones.  Depth pass only
+// (RED.MIN.64 per covered sample).
+#define COOP_WARPS 4
 struct CoopWarp {
-    SmallRec rec[32];
+    SmallRec rec[2][32];  // double buffer: the next 32 records stream in (cp.async) during the current ones
     int prefix[33];
 };
 
-__device__ __forceinline__ void coop_locate(const Setup3& f, int li, int bw, double& px, double& py, int& ix, int& iy) {
-    int dy = li / bw;
-    iy = f.min_y + dy;
-    ix = f.min_x + (li - dy * bw);
-    px = (double)ix + 0.5;
-    py = (double)iy + 0.5;
+__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+__device__ __forceinline__ void coop_issue(const SmallRec* __restrict__ recs, int base, int n, SmallRec* dst) {
+    const int lane = lane_id();
+    if (base + lane < n) {
+        const char* src = reinterpret_cast<const char*>(recs + base + lane);
+        char* d = reinterpret_cast<char*>(dst + lane);
+#pragma unroll
+        for (int q = 0; q < (int)(sizeof(SmallRec) / 16); q++) cp_async16(d + 16 * q, src + 16 * q);
+    }
 }
 
-__global__ void __launch_bounds__(COOP_WARPS * 32) k_small_coop(const SmallRec* __restrict__ recs, int W,
-                                                                unsigned long long* __restrict__ depth,
-                                                                unsigned long long* __restrict__ wid,
-                                                                const fa_dstat* __restrict__ st) {
+__global__ void __launch_bounds__(COOP_WARPS * 32, 6) k_small_coop(const SmallRec* __restrict__ recs, int W,
+                                                                   unsigned long long* __restrict__ depth,
+                                                                   unsigned long long* __restrict__ wid,
+                                                                   const fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
     __shared__ CoopWarp sh[COOP_WARPS];
     const int warp = threadIdx.x >> 5, lane = lane_id();
     CoopWarp& cw = sh[warp];
     const int n = st->n_small3;
-    const int total_warps = gridDim.x * COOP_WARPS;
-    for (int base = (blockIdx.x * COOP_WARPS + warp) * 32; base < n; base += total_warps * 32) {
+    const int stride = gridDim.x * COOP_WARPS * 32;
+    int base = ((int)blockIdx.x * COOP_WARPS + warp) * 32;
+    int buf = 0;
+    coop_issue(recs, base, n, cw.rec[0]);
+    cp_async_commit();
+    for (; base < n; base += stride, buf ^= 1) {
+        coop_issue(recs, base + stride, n, cw.rec[buf ^ 1]);
+        cp_async_commit();
+        cp_async_wait1();
+        __syncwarp();
+        const SmallRec* rb = cw.rec[buf];
         const int cnt = min(32, n - base);
         int np = 0;
-        if (lane < cnt) {
-            const uint4* src = reinterpret_cast<const uint4*>(recs + base + lane);
-            uint4* dst = reinterpret_cast<uint4*>(&cw.rec[lane]);
-#pragma unroll
-            for (int q = 0; q < (int)(sizeof(SmallRec) / 16); q++) dst[q] = __ldg(src + q);
-            const SmallRec& r = cw.rec[lane];
-            np = (r.max_x - r.min_x + 1) * (r.max_y - r.min_y + 1);
-        }
+        if (lane < cnt) np = rb[lane].max_y - rb[lane].min_y + 1;
         int incl = np;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -475,7 +505,7 @@ __global__ void __launch_bounds__(COOP_WARPS * 32) k_small_coop(const SmallRec* 
         int s = lane * chunk;
         const int s_end = min(S, s + chunk);
         if (s < s_end) {
-            // record holding sample s: largest r with prefix[r] <= s
+            // record holding row s: largest r with prefix[r] <= s
             int lo = 0, hi = cnt - 1;
             while (lo < hi) {
                 int mid = (lo + hi + 1) >> 1;
@@ -484,34 +514,28 @@ __global__ void __launch_bounds__(COOP_WARPS * 32) k_small_coop(const SmallRec* 
             int r = lo;
             Setup3 f;
             int t;
-            load_rec(&cw.rec[r], f, t);
-            int bw = f.max_x - f.min_x + 1;
-            int pr = cw.prefix[r], pe = cw.prefix[r + 1];
-            // consecutive samples: step (ix, iy) instead of dividing per sample
-            double px, py;
-            int ix, iy;
-            coop_locate(f, s - pr, bw, px, py, ix, iy);
-            RowTerms rt = row_terms(f, py);
-            for (; s < s_end; s++) {
+            load_rec(&rb[r], f, t);
+            SpanEdges se = span_edges(f);
+            int pe = cw.prefix[r + 1];
+            int iy = f.min_y + (s - cw.prefix[r]);
+            for (; s < s_end; s++, iy++) {
                 if (s >= pe) {
                     do {
                         r++;
-                        pr = pe;
                         pe = cw.prefix[r + 1];
                     } while (s >= pe);
-                    load_rec(&cw.rec[r], f, t);
-                    ix = f.min_x;
+                    load_rec(&rb[r], f, t);
+                    se = span_edges(f);
                     iy = f.min_y;
-                    rt = row_terms(f, (double)iy + 0.5);
                 }
-                px = (double)ix + 0.5;
-                // depth evaluated alongside the edges (independent DP chains)
-                const double z = depth_row(f, rt, px);
-                if (inside_row(f, rt, px)) depth_min(depth, wid, (long long)iy * W + ix, f64_key(z), t, false);
-                if (++ix > f.max_x) {
-                    ix = f.min_x;
-                    iy++;
-                    rt = row_terms(f, (double)iy + 0.5);
+                const RowTerms rt = row_terms(f, (double)iy + 0.5);
+                int xa, xb;
+                row_span(f, rt, se, xa, xb);
+                for (int ix = xa; ix <= xb; ix++) {
+                    const double px = (double)ix + 0.5;
+                    // depth evaluated alongside the edges (independent DP chains)
+                    const double z = depth_row(f, rt, px);
+                    if (inside_row(f, rt, px)) depth_min(depth, wid, (long long)iy * W + ix, f64_key(z), t, false);
                 }
             }
         }
@@ -525,6 +549,7 @@ __global__ void __launch_bounds__(256) k_raster_vis_small(const SmallRec* __rest
                                                           const unsigned long long* __restrict__ hiz, int htx,
                                                           unsigned char* __restrict__ flags,
                                                           const fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
     int n3 = st->n_small3;
     int stride = gridDim.x * blockDim.x;
     // Stored records, one thread each.  One round trip first decides most
@@ -602,6 +627,7 @@ __global__ void __launch_bounds__(256) k_raster_vis_tiles(const SmallRec* __rest
                                                           unsigned char* __restrict__ flags,
                                                           const fa_dstat* __restrict__ st, int max_tiles,
                                                           int max_large) {
+    FA_PDL_PROLOGUE();
     // Items: every 16x8 tile of the large triangles, then the generic setups
     // (only the small clipped windows, which have no tiles, are sampled
     // there).  Triangles already flagged — pass-1 pixel winners, or decided by
@@ -609,12 +635,15 @@ __global__ void __launch_bounds__(256) k_raster_vis_tiles(const SmallRec* __rest
     __shared__ TriSetup sm[8];
     int warp = threadIdx.x >> 5, lane = lane_id();
     int nwarps = gridDim.x * 8;
-    const int n_tiles = min(st->n_tiles, max_tiles);
+    const int n_front = min(st->n_tiles, max_tiles);
+    const int n_tiles = n_front + min(st->n_tiles_clip, max_tiles - n_front);
     const int n_items = n_tiles + min(st->n_large, max_large);
     for (int w = blockIdx.x * 8 + warp; w < n_items; w += nwarps) {
         int4 rec;
-        if (w < n_tiles) {
+        if (w < n_front) {
             rec = tiles[w];
+        } else if (w < n_tiles) {
+            rec = tiles[max_tiles - 1 - (w - n_front)];
         } else {
             rec = make_int4(-(w - n_tiles) - 1, -1, -1, 0);
         }
@@ -730,7 +759,7 @@ void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* c
     if (depth && npx / 2 > work) work = npx / 2;
     int nflag32 = flags ? (T + 3) / 4 : 0;
     if (nflag32 > work) work = nflag32;
-    k_frame_init<<<fa_grid(work, 256, FA_NUM_SMS * 8), 256, 0, s>>>(
+    fa_launch(k_frame_init, fa_grid(work, 256, FA_NUM_SMS * 8), 256, 0, s, 
         pos, V, vp, clip, scr, W, H, vmin, depth, wid, npx, reinterpret_cast<unsigned int*>(flags), nflag32);
 }
 
@@ -741,32 +770,44 @@ static void fork_to(cudaStream_t s, cudaStream_t side, cudaEvent_t ev) {
 }
 
 // Depth pass (write_depth) or work-list build (standalone mark_visible).
-// With a side stream: setup, then {small records on s} || {clipped polygons
-// -> large tiles on side}, joined back into s.  Both branches only lower
-// depth keys with atomicMin, so their order does not matter.
+// With side streams: setup, then {small records on s} || {unclipped large
+// tiles on side} || {clipped polygons -> their tiles on side2}, joined back
+// into s.  Every branch only lowers depth keys with atomicMin, so their order
+// does not matter.
 int fa_launch_depth_pass(bool write_depth, const double4* clip, const double4* scr, const int* tris, int T, int W,
                          int H, int cull, unsigned long long* depth, unsigned long long* wid, SmallRec* small_rec,
                          int* clip_list, TriSetup* large, int max_large, int4* tiles, int max_tiles, fa_dstat* st,
-                         cudaStream_t s, cudaStream_t side, cudaEvent_t ev_fork, cudaEvent_t ev_join) {
-    k_raster_setup<<<fa_grid(T, 256, FA_NUM_SMS * 4), 256, 0, s>>>(scr, tris, T, W, H, cull, small_rec, clip_list,
-                                                                    tiles, max_tiles, st);
+                         cudaStream_t s, cudaStream_t side, cudaStream_t side2, cudaEvent_t ev_fork,
+                         cudaEvent_t ev_join, cudaEvent_t ev_join2) {
+    fa_launch(k_raster_setup, fa_grid(T, 256, FA_NUM_SMS * 4), 256, 0, s, scr, tris, T, W, H, cull, small_rec,
+              clip_list, tiles, max_tiles, st);
     cudaStream_t b = side ? side : s;
+    cudaStream_t b2 = side2 ? side2 : b;
     if (side) fork_to(s, side, ev_fork);
+    if (side2) cudaStreamWaitEvent(side2, ev_fork, 0);
+    int n = 0;
     if (write_depth) {
-        k_raster_clipped<true><<<FA_NUM_SMS * 2, 256, 0, b>>>(clip, tris, W, H, cull, clip_list, depth, wid, large,
-                                                              max_large, tiles, max_tiles, st);
-        // fire-and-forget REDs measured faster than a load-then-atomic check here
-        k_raster_depth_tiles<<<FA_NUM_SMS * 8, 256, 0, b>>>(small_rec, large, tiles, W, depth, wid, st, max_tiles, 0,
-                                                            1);
-        // small unclipped triangles (warp-cooperative)
-        k_small_coop<<<fa_grid((long long)T, COOP_WARPS * 32 * 2, FA_NUM_SMS * 6), COOP_WARPS * 32, 0, s>>>(
-            small_rec, W, depth, wid, st);
+        // three independent branches, all lowering depth keys with RED.MIN:
+        //   s:     small unclipped records (warp-cooperative)
+        //   side:  the unclipped large records' tiles
+        //   side2: clipped polygons -> their tiles
+        fa_launch(k_raster_depth_tiles, fa_cap(FA_NUM_SMS * 8), 256, 0, b, small_rec, large, tiles, W, depth, wid, st,
+                  max_tiles, 0, 1, 0);
+        fa_launch(k_raster_clipped<true>, fa_cap(FA_NUM_SMS * 2), 256, 0, b2, clip, tris, W, H, cull, clip_list, depth, wid,
+                  large, max_large, tiles, max_tiles, st);
+        fa_launch(k_raster_depth_tiles, fa_cap(FA_NUM_SMS * 4), 256, 0, b2, small_rec, large, tiles, W, depth, wid, st,
+                  max_tiles, 0, 1, 1);
+        fa_launch(k_small_coop, fa_grid((long long)T, COOP_WARPS * 32 * 2, FA_NUM_SMS * 12), COOP_WARPS * 32, 0, s,
+                  small_rec, W, depth, wid, st);
+        n = 5;
     } else {
-        k_raster_clipped<false><<<FA_NUM_SMS * 2, 256, 0, b>>>(clip, tris, W, H, cull, clip_list, depth, nullptr,
-                                                               large, max_large, tiles, max_tiles, st);
+        fa_launch(k_raster_clipped<false>, fa_cap(FA_NUM_SMS * 2), 256, 0, b, clip, tris, W, H, cull, clip_list, depth,
+                  nullptr, large, max_large, tiles, max_tiles, st);
+        n = 2;
     }
     if (side) fork_to(side, s, ev_join);
-    return write_depth ? 4 : 2;
+    if (side2 && write_depth) fork_to(side2, s, ev_join2);
+    return n;
 }
 
 // Visibility pass: small records on s || large tiles + small clipped windows
@@ -778,9 +819,9 @@ int fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const
     cudaStream_t b = side ? side : s;
     const int htx = fa_hiz_dim(W);
     if (side) fork_to(s, side, ev_fork);
-    k_raster_vis_tiles<<<FA_NUM_SMS * 8, 256, 0, b>>>(small_rec, T, large, tiles, W, depth, hiz, htx, flags, st,
+    fa_launch(k_raster_vis_tiles, fa_cap(FA_NUM_SMS * 8), 256, 0, b, small_rec, T, large, tiles, W, depth, hiz, htx, flags, st,
                                                       max_tiles, max_large);
-    k_raster_vis_small<<<fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s>>>(small_rec, W, depth, hiz, htx, flags, st);
+    fa_launch(k_raster_vis_small, fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s, small_rec, W, depth, hiz, htx, flags, st);
     if (side) fork_to(side, s, ev_join);
     return 2;
 }
@@ -788,14 +829,14 @@ int fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const
 void fa_launch_depth_hiz(const unsigned long long* depth, const unsigned long long* wid, int W, int H,
                          unsigned long long* hiz, unsigned char* flags, fa_dstat* st, cudaStream_t s) {
     int htx = fa_hiz_dim(W), hty = fa_hiz_dim(H);
-    k_depth_hiz<<<fa_grid((long long)htx * FA_HIZ * hty, 256, FA_NUM_SMS * 8), 256, 0, s>>>(depth, wid, W, H, hiz, htx,
+    fa_launch(k_depth_hiz, fa_grid((long long)htx * FA_HIZ * hty, 256, FA_NUM_SMS * 8), 256, 0, s, depth, wid, W, H, hiz, htx,
                                                                                            hty, flags, st);
 }
 
 void fa_launch_decode_depth(const unsigned long long* keys, double* out, long long n, cudaStream_t s) {
-    k_decode_depth<<<fa_grid(n, 256, FA_NUM_SMS * 8), 256, 0, s>>>(keys, out, n);
+    fa_launch(k_decode_depth, fa_grid(n, 256, FA_NUM_SMS * 8), 256, 0, s, keys, out, n);
 }
 
 void fa_launch_encode_depth(const double* in, unsigned long long* keys, long long n, cudaStream_t s) {
-    k_encode_depth<<<fa_grid(n, 256, FA_NUM_SMS * 8), 256, 0, s>>>(in, keys, n);
+    fa_launch(k_encode_depth, fa_grid(n, 256, FA_NUM_SMS * 8), 256, 0, s, in, keys, n);
 }

@@ -545,6 +545,70 @@ __device__ __forceinline__ double depth_row(const Setup3& s, const RowTerms& r, 
     return s.zmean;
 }
 
+// ---- conservative row spans (sample pruning) -------------------------------
+// Along a row, edge i's value is e_i(px) = r_i - dy_i*(px - ax_i), whose sign
+// changes at x_i = ax_i + r_i/dy_i: dy_i > 0 bounds the covered samples from
+// the right, dy_i < 0 from the left.  row_span() returns the pixel range
+// whose samples lie within FA_SPAN_MARGIN of [max left, min right]; every
+// sample outside it fails the reference's exact test (charts.py:237-249), so
+// only the range is tested — exactly, with the operations above.
+// Why skipping is exact (window of B+1 <= 300 pixels on a side, so
+// |dx_i|, |dy_i|, |py - ay_i|, |px - ax_i| <= B+1): 1/dy_i comes from an FP32
+// MUFU reciprocal (relative error < 2^-22) plus one FP64 Newton step
+// (relative error < 1e-13) and is only used when |dy_i| >= 1e-3, so the
+// computed x_i is within 1e-10 (B+1)^2 <= 1e-5 px of the exact crossing of
+// the reference's r_i.  A sample FA_SPAN_MARGIN (1e-4 px) beyond the
+// computed x_i then has |dy_i (px - x_i)| >= 1e-3 * 9e-5 ~ 1e-7, while the
+// reference's rounded dy_i*(px - ax_i) is within 4.5e-16 (B+1)^2 < 1e-10 of
+// exact, so its e_i (whose sign is that of r_i minus that product) has the
+// excluded sign.  Edges with |dy_i| < 1e-3 give no bound (their samples are
+// all tested exactly).
+#define FA_SPAN_MARGIN 1e-4
+#define FA_SPAN_MIN_DY 1e-3
+
+struct SpanEdges {
+    double inv0, inv1, inv2;  // ~1/dy_i
+    int kind;                 // 2 bits per edge: 1 right bound (dy > 0), 2 left bound (dy < 0), 0 none
+};
+
+__device__ __forceinline__ double approx_inv(double d) {
+    float rf;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rf) : "f"((float)d));  // MUFU.RCP, rel. error < 2^-22
+    double r = (double)rf;
+    return __dmul_rn(r, __dsub_rn(2.0, __dmul_rn(d, r)));
+}
+
+__device__ __forceinline__ SpanEdges span_edges(const Setup3& f) {
+    SpanEdges se;
+    se.kind = 0;
+    se.inv0 = se.inv1 = se.inv2 = 0.0;
+    if (fabs(f.dy0) >= FA_SPAN_MIN_DY) { se.inv0 = approx_inv(f.dy0); se.kind |= f.dy0 > 0 ? 1 : 2; }
+    if (fabs(f.dy1) >= FA_SPAN_MIN_DY) { se.inv1 = approx_inv(f.dy1); se.kind |= (f.dy1 > 0 ? 1 : 2) << 2; }
+    if (fabs(f.dy2) >= FA_SPAN_MIN_DY) { se.inv2 = approx_inv(f.dy2); se.kind |= (f.dy2 > 0 ? 1 : 2) << 4; }
+    return se;
+}
+
+__device__ __forceinline__ void span_edge(int k, double ax, double r, double inv, double& xl, double& xr) {
+    if (k == 0) return;
+    double x = ax + r * inv;
+    if (k == 1) xr = fmin(xr, x);
+    else xl = fmax(xl, x);
+}
+
+// pixel columns [lo, hi] of row terms rt that can hold covered samples
+__device__ __forceinline__ void row_span(const Setup3& f, const RowTerms& rt, const SpanEdges& se, int& lo, int& hi) {
+    double xl = (double)f.min_x, xr = (double)f.max_x + 1.0;
+    span_edge(se.kind & 3, f.ax0, rt.r0, se.inv0, xl, xr);
+    span_edge((se.kind >> 2) & 3, f.ax1, rt.r1, se.inv1, xl, xr);
+    span_edge((se.kind >> 4) & 3, f.ax2, rt.r2, se.inv2, xl, xr);
+    // sample px = ix + 0.5 is a candidate iff xl - m <= px <= xr + m
+    // (clamped to the window so the conversions below stay in range)
+    xl = fmin(xl, (double)f.max_x + 2.0);
+    xr = fmax(xr, (double)f.min_x - 1.0);
+    lo = max(f.min_x, (int)ceil(xl - 0.5 - FA_SPAN_MARGIN));
+    hi = min(f.max_x, (int)floor(xr - 0.5 + FA_SPAN_MARGIN));
+}
+
 struct ColTerms {
     double c0, c1, c2;  // dy_i * (px - ax_i)
     double zc;          // p0z + gx * (px - p0x)

@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
                                                    const long long* __restrict__ placements, int W, int H,
                                                    long long pad, OutT* __restrict__ uv,
                                                    fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
     __shared__ __align__(16) OutT stage[UV_THREADS * 6];
     __shared__ double red_w[UV_THREADS / 32], red_a[UV_THREADS / 32], red_m[UV_THREADS / 32];
     __shared__ int red_c[UV_THREADS / 32];
@@ -145,9 +146,9 @@ void fa_launch_uv(const double4* clip, const int* tris, const int* vis_list, con
                   long long pad, bool f64, void* uv, fa_dstat* st, cudaStream_t s) {
     int grid = fa_grid(T, UV_THREADS, FA_NUM_SMS * 8);
     if (f64)
-        k_uv<double><<<grid, UV_THREADS, 0, s>>>(clip, tris, vis_list, label, cidx, pinv, ndc, px, placements, W, H,
+        fa_launch(k_uv<double>, grid, UV_THREADS, 0, s, clip, tris, vis_list, label, cidx, pinv, ndc, px, placements, W, H,
                                                  pad, (double*)uv, st);
     else
-        k_uv<float><<<grid, UV_THREADS, 0, s>>>(clip, tris, vis_list, label, cidx, pinv, ndc, px, placements, W, H,
+        fa_launch(k_uv<float>, grid, UV_THREADS, 0, s, clip, tris, vis_list, label, cidx, pinv, ndc, px, placements, W, H,
                                                 pad, (float*)uv, st);
 }

@@ -136,12 +136,15 @@ class FrameOutput:
 class FrameEngine:
     """One mesh resident on one GPU; `run(camera)` produces one atlas."""
 
-    def __init__(self, mesh: Mesh, device: int | None = None, settings: FrameSettings | None = None):
+    def __init__(self, mesh: Mesh, device: int | None = None, settings: FrameSettings | None = None,
+                 private_mesh: bool = False):
         torch = nat.require_device()
         self.device = torch.cuda.current_device() if device is None else int(device)
         self.ctx = nat.Context(self.device)  # private context: outputs survive other API calls
         self.mesh = mesh
         self.pos, self.tris = mesh.device_arrays(self.ctx.torch_device)
+        if private_mesh:  # own device copy (e.g. one replica per pipeline slot)
+            self.pos, self.tris = self.pos.clone(), self.tris.clone()
         self.ctx.set_mesh(self.pos, self.tris)
         self.settings = settings or FrameSettings()
         self._res = nat.FrameResult()
@@ -189,6 +192,15 @@ class FrameEngine:
     def launch_count(self) -> int:
         return int(self.ctx.L.fa_last_launch_count(self.ctx.h))
 
+    COUNTERS = ("small_records", "large_records", "clipped", "generic_setups", "tiles", "visible", "charts",
+                "screen_fragments")
+
+    def counters(self) -> dict:
+        """Work-queue counters of the last finished frame (fa_frame_counters)."""
+        buf = (ctypes.c_int64 * 8)()
+        n = self.ctx.L.fa_frame_counters(self.ctx.h, buf, 8)
+        return {self.COUNTERS[i]: int(buf[i]) for i in range(n)}
+
     def stage_times(self) -> dict:
         """{stage name: ms} of the last frame run with settings.profile=True."""
         buf = (ctypes.c_float * 16)()
@@ -230,12 +242,13 @@ class FramePipeline:
     `on_frame(HostFrame)`."""
 
     def __init__(self, mesh: Mesh, device: int | None = None, settings: FrameSettings | None = None,
-                 depth: int = 4, outputs: tuple = ("chart_of_triangle", "visible", "uv", "placements")):
+                 depth: int = 4, outputs: tuple = ("chart_of_triangle", "visible", "uv", "placements"),
+                 mesh_replicas: bool = False):
         torch = nat.require_device()
         if depth < 1:
             raise ValueError("depth must be >= 1")
         self.settings = settings or FrameSettings()
-        self.engines = [FrameEngine(mesh, device, self.settings) for _ in range(depth)]
+        self.engines = [FrameEngine(mesh, device, self.settings, private_mesh=mesh_replicas) for _ in range(depth)]
         self.device = self.engines[0].device
         self.streams = [torch.cuda.Stream(device=self.device) for _ in range(depth)]
         self.outputs = tuple(outputs)
