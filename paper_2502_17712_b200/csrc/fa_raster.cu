@@ -588,10 +588,13 @@ __global__ void __launch_bounds__(256) k_raster_vis_small(const SmallRec* __rest
         double z0 = 0, z1 = 0, z2 = 0, z3 = 0;
         const unsigned long long *a0 = depth, *a1 = depth, *a2 = depth, *a3 = depth;
         int nq = 0;
+        const SpanEdges se = span_edges(f);
         for (int iy = f.min_y; iy <= f.max_y && !vis; iy++) {
             const RowTerms rt = row_terms(f, (double)iy + 0.5);
             const unsigned long long* row = depth + (long long)iy * W;
-            for (int ix = f.min_x; ix <= f.max_x; ix++) {
+            int xa, xb;
+            row_span(f, rt, se, xa, xb);  // only samples that can be covered
+            for (int ix = xa; ix <= xb; ix++) {
                 double px = (double)ix + 0.5;
                 if (!inside_row(f, rt, px)) continue;
                 double z = depth_row(f, rt, px);
