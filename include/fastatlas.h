@@ -196,6 +196,7 @@ typedef struct fa_frame_result {
     const int64_t *target;          /* (n_charts,2) target_w target_h */
     const int64_t *placements;      /* (n_charts,8) packing order */
     const void *uv;                 /* (n_visible,6) float32 or float64, NaN = no UV */
+    const int32_t *visible_chart;   /* (n_visible,) chart id of each visible triangle (sparse chart_of_triangle) */
 } fa_frame_result;
 
 /* Enqueue a whole frame on `stream` (no host synchronisation). */
@@ -215,6 +216,14 @@ int fa_frame(fa_ctx *ctx, const double *vp_host, const fa_frame_params *params, 
  * per-array `.cpu()` reads of SceneResult (reference cli.py:404-406). */
 int fa_frame_download(fa_ctx *ctx, const fa_frame_result *res, int32_t *chart_of_triangle, int32_t *visible,
                       void *uv, int64_t *placements, void *stream);
+
+/* Sparse form of fa_frame_download for streaming clients: the chart ids of
+ * the visible triangles only (visible_chart, n_visible int32; every other
+ * triangle's chart id is -1), so chart_of_triangle[visible[i]] =
+ * visible_chart[i] is rebuilt on the host without copying the (T,) array.
+ * Same conventions as fa_frame_download. */
+int fa_frame_download_visible(fa_ctx *ctx, const fa_frame_result *res, int32_t *visible, int32_t *visible_chart,
+                              void *uv, int64_t *placements, void *stream);
 
 /* Number of kernels the last fa_frame_launch enqueued (benchmark accounting). */
 int fa_last_launch_count(fa_ctx *ctx);

@@ -116,7 +116,7 @@ void fa_destroy(fa_ctx* c) {
                       &c->target, &c->survived, &c->okey, &c->oidx, &c->ow, &c->oh, &c->orot, &c->sortk, &c->sortv,
                       &c->pinv, &c->cand, &c->cand_p, &c->cand_w, &c->cand_h, &c->cand_y, &c->rowstart,
                       &c->placements, &c->uv, &c->vp_dev, &c->blocks, &c->dstat, &c->aux, &c->in_tw, &c->in_th,
-                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list, &c->hiz, &c->wid};
+                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list, &c->hiz, &c->wid, &c->vis_chart};
     for (fa_buf* b : bufs) free_buf(*b);
     for (cudaEvent_t e : c->fj)
         if (e) cudaEventDestroy(e);
@@ -753,7 +753,7 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     mark();  // 9: candidate pack + select
     fa_launch_uv(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->label), P<int>(ctx->cidx),
                  P<int>(ctx->pinv), P<double>(ctx->ndc), P<int>(ctx->px), P<long long>(ctx->placements), T, W, H,
-                 p->padding, p->uv_f64 != 0, ctx->uv.p, st, s);
+                 p->padding, p->uv_f64 != 0, ctx->uv.p, P<int>(ctx->vis_chart), st, s);
     nl += 1;
     mark();  // 10: uv
     if (p->want_depth) {
@@ -785,6 +785,7 @@ static int frame_prepare(fa_ctx* ctx, const fa_frame_params* p) {
     r = ensure_pack(ctx, cap, p->n_scales, p->omega, batch);
     if (r) return r;
     ENSURE(uv, (size_t)(ctx->T + 1) * 6 * (p->uv_f64 ? 8 : 4));
+    ENSURE(vis_chart, (size_t)(ctx->T + 1) * 4);
     if (p->want_depth) ENSURE(depth_f64, (size_t)p->width * p->height * 8);
     return FA_OK;
 }
@@ -881,6 +882,7 @@ int fa_frame_finish(fa_ctx* ctx, fa_frame_result* out, void* stream) {
     out->target = P<int64_t>(ctx->target);
     out->placements = P<int64_t>(ctx->placements);
     out->uv = ctx->uv.p;
+    out->visible_chart = P<int32_t>(ctx->vis_chart);
     int64_t n_cap = ctx->pack_cap;
     ctx->needs_rerun = false;
     if (h->flags & FA_DFLAG_QUEUE_OVERFLOW || h->n_charts > n_cap) {
@@ -937,6 +939,22 @@ int fa_frame_download(fa_ctx* ctx, const fa_frame_result* res, int32_t* chart_of
     if (chart_of_triangle && ctx->T)
         CK(cudaMemcpyAsync(chart_of_triangle, res->chart_of_triangle, (size_t)ctx->T * 4, cudaMemcpyDeviceToHost, s));
     if (visible && nv) CK(cudaMemcpyAsync(visible, res->visible, nv * 4, cudaMemcpyDeviceToHost, s));
+    if (uv && nv) CK(cudaMemcpyAsync(uv, res->uv, nv * 6 * uv_elem, cudaMemcpyDeviceToHost, s));
+    if (placements && C) CK(cudaMemcpyAsync(placements, res->placements, C * 64, cudaMemcpyDeviceToHost, s));
+    return FA_OK;
+}
+
+int fa_frame_download_visible(fa_ctx* ctx, const fa_frame_result* res, int32_t* visible, int32_t* visible_chart,
+                              void* uv, int64_t* placements, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || !res) return set_err(FA_VALUE_ERROR, "bad arguments");
+    if (res->status != FA_OK) return set_err(FA_VALUE_ERROR, "frame result has no outputs (status %d)", res->status);
+    CK(cudaSetDevice(ctx->device));
+    size_t nv = (size_t)res->n_visible, C = (size_t)res->n_charts;
+    size_t uv_elem = ctx->last_params.uv_f64 ? 8 : 4;
+    if (visible && nv) CK(cudaMemcpyAsync(visible, res->visible, nv * 4, cudaMemcpyDeviceToHost, s));
+    if (visible_chart && nv)
+        CK(cudaMemcpyAsync(visible_chart, res->visible_chart, nv * 4, cudaMemcpyDeviceToHost, s));
     if (uv && nv) CK(cudaMemcpyAsync(uv, res->uv, nv * 6 * uv_elem, cudaMemcpyDeviceToHost, s));
     if (placements && C) CK(cudaMemcpyAsync(placements, res->placements, C * 64, cudaMemcpyDeviceToHost, s));
     return FA_OK;

@@ -46,6 +46,7 @@ struct fa_ctx {
     fa_buf scr, clip_list;  // per-vertex screen records; generic-path triangle list
     fa_buf hiz;             // 8x8 hierarchical-Z max keys of the final depth
     fa_buf wid;             // pass-1 pixel winners (truncated key | triangle id)
+    fa_buf vis_chart;       // chart id of each visible triangle (written by k_uv)
     size_t gen = 0;
     int max_large = 0, max_tiles = 0;
     int pack_batch = 0;  // candidates per pack launch
@@ -179,7 +180,7 @@ void fa_launch_fold(const long long* w, int n, long long omega, long long* rows,
 // ---- uv (fa_uv.cu) -------------------------------------------------------
 void fa_launch_uv(const double4* clip, const int* tris, const int* vis_list, const int* label, const int* cidx,
                   const int* pinv, const double* ndc, const int* px, const long long* placements, int T, int W, int H,
-                  long long pad, bool f64, void* uv, fa_dstat* st, cudaStream_t s);
+                  long long pad, bool f64, void* uv, int* vis_chart, fa_dstat* st, cudaStream_t s);
 
 // ---- comparison packers (fa_baselines.cu) -----------------------------------
 void fa_launch_seq_search(const long long* ow, const long long* oh, int n, long long omega, long long n_scales,

@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
                                                    const double* __restrict__ ndc, const int* __restrict__ px,
                                                    const long long* __restrict__ placements, int W, int H,
                                                    long long pad, OutT* __restrict__ uv,
-                                                   fa_dstat* __restrict__ st) {
+                                                   int* __restrict__ vis_chart, fa_dstat* __restrict__ st) {
     FA_PDL_PROLOGUE();
     __shared__ __align__(16) OutT stage[UV_THREADS * 6];
     __shared__ double red_w[UV_THREADS / 32], red_a[UV_THREADS / 32], red_m[UV_THREADS / 32];
@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
         const double qnan = __longlong_as_double(0x7ff8000000000000ll);
 #pragma unroll
         for (int i = 0; i < 6; i++) out[i] = qnan;
+        if (k < n && vis_chart) vis_chart[k] = label[vis_list[k]];  // sparse chart_of_triangle
         if (k < n && !failed) {
             int t = vis_list[k];
             int c = cidx[label[t]];
@@ -143,12 +144,12 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
 
 void fa_launch_uv(const double4* clip, const int* tris, const int* vis_list, const int* label, const int* cidx,
                   const int* pinv, const double* ndc, const int* px, const long long* placements, int T, int W, int H,
-                  long long pad, bool f64, void* uv, fa_dstat* st, cudaStream_t s) {
+                  long long pad, bool f64, void* uv, int* vis_chart, fa_dstat* st, cudaStream_t s) {
     int grid = fa_grid(T, UV_THREADS, FA_NUM_SMS * 8);
     if (f64)
         fa_launch(k_uv<double>, grid, UV_THREADS, 0, s, clip, tris, vis_list, label, cidx, pinv, ndc, px, placements, W, H,
-                                                 pad, (double*)uv, st);
+                                                 pad, (double*)uv, vis_chart, st);
     else
         fa_launch(k_uv<float>, grid, UV_THREADS, 0, s, clip, tris, vis_list, label, cidx, pinv, ndc, px, placements, W, H,
-                                                pad, (float*)uv, st);
+                                                pad, (float*)uv, vis_chart, st);
 }

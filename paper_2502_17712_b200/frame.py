@@ -214,22 +214,42 @@ class HostFrame:
     The arrays are views into a pipeline slot and are overwritten once the
     slot is reused (`depth` views later): `on_frame` consumers that keep them
     must copy.  `error` holds the reference exception (NothingVisible,
-    PackFailure, ...) when the frame failed; the arrays are then None."""
+    PackFailure, ...) when the frame failed; the arrays are then None.
+
+    Chart ids arrive sparse by default (`visible_chart`: the chart of each
+    visible triangle; every other triangle's chart is -1, charts.py:136-141);
+    `chart_of_triangle` rebuilds the dense (T,) int32 array on first access
+    (or is the downloaded dense array when the pipeline asked for it)."""
 
     __slots__ = ("index", "status", "error", "n_visible", "n_charts", "scale", "screen_fragments",
-                 "texels_allocated", "chart_of_triangle", "visible", "uv", "placements")
+                 "texels_allocated", "_cot", "_T", "visible", "visible_chart", "uv", "placements")
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, n_triangles: int = 0):
         self.index = index
         self.status = 0
         self.error = None
         self.n_visible = self.n_charts = 0
         self.scale = None
         self.screen_fragments = self.texels_allocated = 0
-        self.chart_of_triangle = self.visible = self.uv = self.placements = None
+        self._cot = self.visible = self.visible_chart = self.uv = self.placements = None
+        self._T = n_triangles
+
+    @property
+    def chart_of_triangle(self):
+        if self._cot is None and self.visible is not None and self.visible_chart is not None:
+            cot = np.full(self._T, -1, dtype=np.int32)
+            cot[self.visible] = self.visible_chart
+            self._cot = cot
+        return self._cot
 
     def d2h_bytes(self) -> int:
-        return sum(a.nbytes for a in (self.chart_of_triangle, self.visible, self.uv, self.placements) if a is not None)
+        """Bytes copied device -> host for this view (a rebuilt dense chart
+        array is host work, not a copy)."""
+        arrs = (self.visible, self.visible_chart, self.uv, self.placements)
+        n = sum(a.nbytes for a in arrs if a is not None)
+        if self._cot is not None and self.visible_chart is None:
+            n += self._cot.nbytes
+        return n
 
 
 class FramePipeline:
@@ -242,7 +262,7 @@ class FramePipeline:
     `on_frame(HostFrame)`."""
 
     def __init__(self, mesh: Mesh, device: int | None = None, settings: FrameSettings | None = None,
-                 depth: int = 4, outputs: tuple = ("chart_of_triangle", "visible", "uv", "placements"),
+                 depth: int = 4, outputs: tuple = ("visible", "visible_chart", "uv", "placements"),
                  mesh_replicas: bool = False):
         torch = nat.require_device()
         if depth < 1:
@@ -259,8 +279,10 @@ class FramePipeline:
             h = {}
             if "chart_of_triangle" in outputs:
                 h["chart_of_triangle"] = torch.empty(T, dtype=torch.int32).pin_memory()
-            if "visible" in outputs:
+            if "visible" in outputs or "visible_chart" in outputs:
                 h["visible"] = torch.empty(T, dtype=torch.int32).pin_memory()
+            if "visible_chart" in outputs:
+                h["visible_chart"] = torch.empty(T, dtype=torch.int32).pin_memory()
             if "uv" in outputs:
                 h["uv"] = torch.empty((T, 6), dtype=uv_dt).pin_memory()
             if "placements" in outputs:
@@ -278,7 +300,7 @@ class FramePipeline:
         eng, st = self.engines[slot], self.streams[slot]
         L, h_ctx, res = eng.ctx.L, eng.ctx.h, eng._res
         sp = ctypes.c_void_p(st.cuda_stream)
-        hf = HostFrame(index)
+        hf = HostFrame(index, self.engines[slot].n_triangles)
         for _ in range(4):
             code = L.fa_frame_finish(h_ctx, ctypes.byref(res), sp)
             if code == nat.FA_INTERNAL_ERROR and "rerun" in nat.last_error():
@@ -301,12 +323,19 @@ class FramePipeline:
         hf.screen_fragments, hf.texels_allocated = int(res.screen_fragments), int(res.texels_allocated)
         h = self._host[slot]
         ptr = {k: ctypes.c_void_p(t.data_ptr()) if k in h else None
-               for k, t in ((k, h.get(k)) for k in ("chart_of_triangle", "visible", "uv", "placements"))}
-        if any(p is not None for p in ptr.values()):
+               for k, t in ((k, h.get(k)) for k in ("chart_of_triangle", "visible", "visible_chart", "uv",
+                                                     "placements"))}
+        if ptr["chart_of_triangle"] is not None:
             nat.raise_for_status(L.fa_frame_download(h_ctx, ctypes.byref(res), ptr["chart_of_triangle"],
                                                      ptr["visible"], ptr["uv"], ptr["placements"], sp))
+        elif any(p is not None for p in ptr.values()):
+            nat.raise_for_status(L.fa_frame_download_visible(h_ctx, ctypes.byref(res), ptr["visible"],
+                                                             ptr["visible_chart"], ptr["uv"], ptr["placements"],
+                                                             sp))
         if "chart_of_triangle" in h:
-            hf.chart_of_triangle = self._np[slot]["chart_of_triangle"]
+            hf._cot = self._np[slot]["chart_of_triangle"]
+        if "visible_chart" in h:
+            hf.visible_chart = self._np[slot]["visible_chart"][:nv]
         if "visible" in h:
             hf.visible = self._np[slot]["visible"][:nv]
         if "uv" in h:

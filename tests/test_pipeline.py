@@ -29,8 +29,11 @@ def _vps(spec, poses):
     return out
 
 
-@pytest.mark.parametrize("depth", [1, 3])
-def test_pipeline_matches_sequential(depth):
+@pytest.mark.parametrize("depth,outputs", [(1, None), (3, None),
+                                           (2, ("chart_of_triangle", "visible", "uv", "placements"))])
+def test_pipeline_matches_sequential(depth, outputs):
+    """Sparse chart ids (default: visible_chart, dense array rebuilt on the
+    host) and the dense download give the sequential engine's outputs."""
     spec = scenes.build_scene("C5")
     mesh = fa.Mesh(spec.positions, spec.triangles)
     settings = FrameSettings(screen=spec.screen, omega=spec.omega)
@@ -49,7 +52,8 @@ def test_pipeline_matches_sequential(depth):
         got.append((hf.index, {"chart": hf.chart_of_triangle.copy(), "vis": hf.visible.copy(), "uv": hf.uv.copy(),
                                "plc": hf.placements.copy(), "scale": hf.scale, "frag": hf.screen_fragments}))
 
-    pipe = FramePipeline(mesh, settings=settings, depth=depth)
+    kw = {} if outputs is None else {"outputs": outputs}
+    pipe = FramePipeline(mesh, settings=settings, depth=depth, **kw)
     assert pipe.run(vps, on_frame) == len(vps)
     assert [i for i, _ in got] == list(range(len(vps)))
     for (_, g), w in zip(got, want):
