@@ -126,3 +126,58 @@ def test_coplanar_duplicates():
     pos, tris = _merge([a, b, c, _layer(9.0, 50, 6.0, rng, 0.4)])
     r = _check(pos, tris, vp)
     assert r.status == oracle.OK
+
+
+def _screen_tris(vp_cam, pts_px, depths):
+    """World triangles whose corners project to the given screen points
+    (pixels, row 0 at NDC y = -1) at view distance `depths` (one per tri)."""
+    W, H = SCREEN
+    t = math.tan(math.radians(60.0) / 2)
+    aspect = W / H
+    pos = []
+    for tri, d in zip(pts_px, depths):
+        for sx, sy in tri:
+            nx, ny = 2.0 * sx / W - 1.0, 2.0 * sy / H - 1.0
+            pos.append((nx * d * t * aspect, ny * d * t, -d))
+    pos = np.asarray(pos, np.float64)
+    tris = np.arange(len(pos)).reshape(-1, 3)
+    return pos, tris
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_edges_through_sample_centres(seed):
+    """Small triangles whose corners sit on pixel centres +- 1e-12..5e-3 px,
+    so their edges graze sample centres at every distance around the span
+    margin (and edges are near-horizontal with |dy| around the 1e-3 / 1e-2
+    span thresholds): the pruned row spans of the small-record path must
+    drop no sample the reference covers (charts.py:237-249)."""
+    rng = np.random.default_rng(100 + seed)
+    offs = np.array([0.0, 1e-12, -1e-12, 1e-9, -1e-9, 1e-6, -1e-6, 1e-4, -1e-4, 1e-3, -1e-3, 5e-3, -5e-3])
+    pts, depths = [], []
+    W, H = SCREEN
+    for _ in range(3000):
+        cx, cy = rng.integers(8, W - 56), rng.integers(8, H - 16)
+        kind = rng.integers(0, 3)
+        if kind == 0:    # compact triangle, corners on centres + tiny offsets
+            c = np.array([[0, 0], [rng.integers(1, 6), rng.integers(0, 3)], [rng.integers(0, 3), rng.integers(1, 6)]],
+                         np.float64)
+        elif kind == 1:  # long, nearly horizontal edge (dy ~ 1e-3 .. 1e-2 over up to 40 px)
+            L = rng.integers(10, 40)
+            c = np.array([[0, 0], [L, rng.choice([1e-3, -1e-3, 1e-2, -1e-2, 2e-2, 0.0])], [rng.integers(0, L), 1]],
+                         np.float64)
+        else:            # thin sliver crossing a column of centres
+            c = np.array([[0, 0], [rng.choice([1e-3, 1e-2, 0.5]), rng.integers(4, 9)], [1, rng.integers(1, 5)]],
+                         np.float64)
+        c = c + 0.5 + rng.choice(offs, size=(3, 2))
+        c[:, 0] += cx
+        c[:, 1] += cy
+        tri = [tuple(p) for p in c]
+        # counter-clockwise in screen space (front-facing with culling on)
+        a2 = (c[1, 0] - c[0, 0]) * (c[2, 1] - c[0, 1]) - (c[2, 0] - c[0, 0]) * (c[1, 1] - c[0, 1])
+        if a2 < 0:
+            tri = [tri[0], tri[2], tri[1]]
+        pts.append(tri)
+        depths.append(rng.uniform(3.0, 9.0))
+    pos, tris = _screen_tris(None, pts, depths)
+    r = _check(pos, tris, _camera().view_proj)
+    assert r.flags.sum() > 100
