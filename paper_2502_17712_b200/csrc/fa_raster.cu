@@ -641,51 +641,71 @@ __global__ void __launch_bounds__(256) k_raster_vis_tiles(const SmallRec* __rest
     const int n_front = min(st->n_tiles, max_tiles);
     const int n_tiles = n_front + min(st->n_tiles_clip, max_tiles - n_front);
     const int n_items = n_tiles + min(st->n_large, max_large);
-    for (int w = blockIdx.x * 8 + warp; w < n_items; w += nwarps) {
-        int4 rec;
-        if (w < n_front) {
-            rec = tiles[w];
-        } else if (w < n_tiles) {
-            rec = tiles[max_tiles - 1 - (w - n_front)];
-        } else {
-            rec = make_int4(-(w - n_tiles) - 1, -1, -1, 0);
+    // Two phases per 32 items.  Filter (one lane per item, so a warp has 32
+    // descriptor -> flag/record -> hierarchical-Z round trips in flight):
+    // most tiles belong to triangles already flagged or lie behind the final
+    // depth.  Sample (whole warp per surviving item, ~2% of the tiles).
+    // lane l of warp g takes item g + nwarps * (l + 32 k): consecutive tiles
+    // (mostly of one triangle) land in different warps, so survivors spread
+    const int wg = (int)blockIdx.x * 8 + warp;
+    for (int base = 0; wg + nwarps * base < n_items; base += 32) {
+        const int wi = wg + nwarps * (base + lane);
+        int4 rec0 = make_int4(0, 0, -1, 0);
+        bool need = false;
+        if (wi < n_items) {
+            if (wi < n_front) rec0 = tiles[wi];
+            else if (wi < n_tiles) rec0 = tiles[max_tiles - 1 - (wi - n_front)];
+            else rec0 = make_int4(-(wi - n_tiles) - 1, -1, -1, 0);
+            if (rec0.x < 0) {
+                need = true;  // generic setup: decided by the sampling phase
+            } else if (!flags[rec0.z]) {
+                const SmallRec* q = recs + rec0.x;
+                Setup3 f;
+                f.min_x = q->min_x; f.max_x = q->max_x; f.min_y = q->min_y; f.max_y = q->max_y;
+                f.use_plane = (q->flags >> 3) & 1;
+                f.p0x = q->x0; f.p0y = q->y0; f.p0z = q->z0;
+                f.gx = q->g0; f.gy = q->g1; f.zmean = q->g0;
+                const int ntx = (f.max_x - f.min_x + 1 + TILE_W - 1) / TILE_W;
+                const int xa = f.min_x + (rec0.y % ntx) * TILE_W, ya = f.min_y + (rec0.y / ntx) * TILE_H;
+                const int xb = min(xa + TILE_W - 1, f.max_x), yb = min(ya + TILE_H - 1, f.max_y);
+                const double zlb = depth_lower_bound(f, xa, xb, ya, yb);
+                // the hierarchical-Z tiles under the rectangle (at most 3 x 2)
+                const int hx0 = xa / FA_HIZ, hx1 = xb / FA_HIZ, hy0 = ya / FA_HIZ, hy1 = yb / FA_HIZ;
+                unsigned long long hk[6];
+#pragma unroll
+                for (int q2 = 0; q2 < 6; q2++) {
+                    const int hx = hx0 + q2 % 3, hy = hy0 + q2 / 3;
+                    hk[q2] = (hx <= hx1 && hy <= hy1) ? __ldg(hiz + hy * htx + hx) : FA_KEY_POS_INF;
+                }
+#pragma unroll
+                for (int q2 = 0; q2 < 6; q2++) {
+                    const int hx = hx0 + q2 % 3, hy = hy0 + q2 / 3;
+                    if (hx <= hx1 && hy <= hy1 && !hiz_tile_rejects(hk[q2], zlb)) need = true;
+                }
+#ifdef FA_HIZ_STATS
+                atomicAdd(&g_hiz_stats[2], 1ull);
+                if (!need) atomicAdd(&g_hiz_stats[3], 1ull);
+            } else {
+                atomicAdd(&g_hiz_stats[4], 1ull);
+#endif
+            }
         }
+        unsigned todo = __ballot_sync(0xffffffffu, need);
+        while (todo) {
+        const int src = __ffs(todo) - 1;
+        todo &= todo - 1;
+        int4 rec;
+        rec.x = __shfl_sync(0xffffffffu, rec0.x, src);
+        rec.y = __shfl_sync(0xffffffffu, rec0.y, src);
+        rec.z = __shfl_sync(0xffffffffu, rec0.z, src);
+        rec.w = 0;
         if (rec.x >= 0) {
-            // the descriptor names the triangle: its flag (already visible?)
-            // is read in the same round trip as the record
             int seen = 0;
-            if (lane == 0) seen = flags[rec.z];
+            if (lane == 0) seen = *(volatile unsigned char*)(flags + rec.z);
             Setup3 f;
             int t;
             load_rec(recs + rec.x, f, t);
-            if (__shfl_sync(0xffffffffu, seen, 0)) {
-#ifdef FA_HIZ_STATS
-                if (lane == 0) atomicAdd(&g_hiz_stats[4], 1ull);
-#endif
-                continue;  // already visible (warp-uniform)
-            }
-            {
-                // lanes 0..5 read the hierarchical-Z tiles under the 16x8
-                // rectangle (at most 3 x 2 of them) in one round trip
-                int ntx = (f.max_x - f.min_x + 1 + TILE_W - 1) / TILE_W;
-                int xa = f.min_x + (rec.y % ntx) * TILE_W, ya = f.min_y + (rec.y / ntx) * TILE_H;
-                int xb = min(xa + TILE_W - 1, f.max_x), yb = min(ya + TILE_H - 1, f.max_y);
-                const int hx0 = xa / FA_HIZ, hy0 = ya / FA_HIZ, hnx = xb / FA_HIZ - hx0 + 1;
-                const int hn = hnx * (yb / FA_HIZ - hy0 + 1);
-                const bool hv = lane < hn;
-                unsigned long long hk = 0;
-                if (hv) hk = __ldg(hiz + (hy0 + lane / hnx) * htx + hx0 + lane % hnx);
-                const double zlb = depth_lower_bound(f, xa, xb, ya, yb);
-#ifdef FA_HIZ_STATS
-                if (lane == 0) atomicAdd(&g_hiz_stats[2], 1ull);
-#endif
-                if (!__any_sync(0xffffffffu, hv && !hiz_tile_rejects(hk, zlb))) {
-#ifdef FA_HIZ_STATS
-                    if (lane == 0) atomicAdd(&g_hiz_stats[3], 1ull);
-#endif
-                    continue;
-                }
-            }
+            if (__shfl_sync(0xffffffffu, seen, 0)) continue;  // flagged meanwhile (warp-uniform)
             int x, y0;
             tile_lane_origin(f.min_x, f.max_x, f.min_y, rec.y, x, y0);
             bool vis = false;
@@ -751,6 +771,7 @@ __global__ void __launch_bounds__(256) k_raster_vis_tiles(const SmallRec* __rest
             }
         }
         if (__any_sync(0xffffffffu, vis) && lane == 0) flags[t] = 1;
+        }
     }
 }
 
