@@ -266,6 +266,7 @@ struct PackSmem {
     long long red2[33];
     int red_i[32];
     int flag;
+    int part_sum[2][32], part_max[2][32], part_m[2][32];  // narrow rounds: per-warp partials (double-buffered)
 };
 
 // block max of two values at once (one pair of barriers); red/red2 hold 33
@@ -300,7 +301,7 @@ __device__ __forceinline__ void block_max2_ll(long long& a, long long& b, long l
 
 #ifdef FA_PACK_PROF
 // debug build only: per candidate CTA [t_fold_done, t_heights, t_rowstart, t_rows_done, iterations, rows]
-__device__ long long g_pack_prof[256][8];
+__device__ long long g_pack_prof[256][12];
 extern "C" void fa_debug_pack_prof(long long* out) { cudaMemcpyFromSymbol(out, g_pack_prof, sizeof(g_pack_prof)); }
 #define PACK_MARK(k, v) \
     if (threadIdx.x == 0 && blockIdx.x < 256) g_pack_prof[blockIdx.x][k] = (v)
@@ -332,8 +333,23 @@ __device__ bool pack_candidate(const long long* __restrict__ ow, const long long
         // so a round is the divisions + one block scan + one paired max.
         const int b0 = tid * K;
         long long owr[PK_KREG], wr[PK_KREG];
+        long long owmax = -1, negmin = 0;
 #pragma unroll
-        for (int k = 0; k < PK_KREG; k++) owr[k] = (k < K && b0 + k < n) ? ow[b0 + k] : 0;
+        for (int k = 0; k < PK_KREG; k++) {
+            owr[k] = (k < K && b0 + k < n) ? ow[b0 + k] : 0;
+            owmax = owr[k] > owmax ? owr[k] : owmax;
+            negmin = -owr[k] > negmin ? -owr[k] : negmin;
+        }
+        // Narrow rounds: with scale <= 1 every width is <= wb, so when n*wb
+        // < 2^31 all prefix sums and overflows fit int32: warp scans on
+        // 32-bit values, REDUX max, and one barrier per block reduction
+        // (every thread combines the per-warp partials itself).
+        block_max2_ll(owmax, negmin, sm.red, sm.red2);
+        const long long wb = (owmax > min_dim ? owmax : min_dim) + 2 * pad;
+        const bool narrow = negmin <= 0 && owmax >= 0 && owmax < (1ll << 31) && wb < (1ll << 31) &&
+                            (long long)n * wb < (1ll << 31);
+        const int lane = lane_id(), wid = tid >> 5, nw = blockDim.x >> 5;
+        int pb = 0;
         long long base = 0;
         for (int it = 0; it < FA_MAX_OVERFLOW_ITERS + 1; it++) {
             PACK_MARK(4, it + 1);
@@ -341,10 +357,10 @@ __device__ bool pack_candidate(const long long* __restrict__ ow, const long long
             long long ti = clock64();
 #endif
             long long wmax = 0, local = 0;
-            const double rdn = 1.0 / (double)den;
             // after a snap the denominator is a power of two: the ceiling is
             // a shift (non-negative num*t < 2^62, the numpy value exactly)
             const bool pow2 = den > 0 && (den & (den - 1)) == 0 && num >= 0 && num < (1ll << 31);
+            const double rdn = pow2 ? 0.0 : 1.0 / (double)den;
             const int dsh = pow2 ? __ffsll(den) - 1 : 0;
 #pragma unroll
             for (int k = 0; k < PK_KREG; k++) {
@@ -364,24 +380,66 @@ __device__ bool pack_candidate(const long long* __restrict__ ow, const long long
 #ifdef FA_PACK_PROF
             if (it == 1) PACK_MARK(6, clock64() - ti);
 #endif
-            long long tot;
-            base = block_exclusive_scan_ll(local, sm.red, &tot);
-#ifdef FA_PACK_PROF
-            if (it == 1) PACK_MARK(7, clock64() - ti);
-#endif
-            long long p = base, mloc = -(1ll << 62);
+            long long mloc = -(1ll << 62);
+            if (narrow) {
+                int x = (int)local;
 #pragma unroll
-            for (int k = 0; k < PK_KREG; k++) {
-                if (k < K && b0 + k < n) {
-                    long long q = p & (omega - 1);
-                    long long over = q + wr[k] - omega;
-                    mloc = over > mloc ? over : mloc;
-                    p += wr[k];
+                for (int o = 1; o < 32; o <<= 1) {
+                    int y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
                 }
-            }
-            block_max2_ll(wmax, mloc, sm.red, sm.red2);
+                const int wm = __reduce_max_sync(0xffffffffu, (int)wmax);
+                if (lane == 31) sm.part_sum[pb][wid] = x;
+                if (lane == 0) sm.part_max[pb][wid] = wm;
+                __syncthreads();
+                int pre = 0, bw = 0;
+                for (int w = 0; w < nw; w++) {
+                    const int ps = sm.part_sum[pb][w];
+                    pre += w < wid ? ps : 0;
+                    bw = max(bw, sm.part_max[pb][w]);
+                }
+                base = (long long)(pre + x - (int)local);
+                wmax = bw;
 #ifdef FA_PACK_PROF
-            if (it == 1) PACK_MARK(1, clock64() - ti);
+                if (it == 1) PACK_MARK(7, clock64() - ti);
+#endif
+                int p = (int)base, ml = -(1 << 30) - 1;
+                const int om = (int)omega;
+#pragma unroll
+                for (int k = 0; k < PK_KREG; k++) {
+                    if (k < K && b0 + k < n) {
+                        const int over = (p & (om - 1)) + (int)wr[k] - om;
+                        ml = over > ml ? over : ml;
+                        p += (int)wr[k];
+                    }
+                }
+                ml = __reduce_max_sync(0xffffffffu, ml);
+                if (lane == 0) sm.part_m[pb][wid] = ml;
+                __syncthreads();
+                int bm = -(1 << 30) - 1;
+                for (int w = 0; w < nw; w++) bm = max(bm, sm.part_m[pb][w]);
+                mloc = bm;
+                pb ^= 1;
+            } else {
+                long long tot;
+                base = block_exclusive_scan_ll(local, sm.red, &tot);
+#ifdef FA_PACK_PROF
+                if (it == 1) PACK_MARK(7, clock64() - ti);
+#endif
+                long long p = base;
+#pragma unroll
+                for (int k = 0; k < PK_KREG; k++) {
+                    if (k < K && b0 + k < n) {
+                        long long q = p & (omega - 1);
+                        long long over = q + wr[k] - omega;
+                        mloc = over > mloc ? over : mloc;
+                        p += wr[k];
+                    }
+                }
+                block_max2_ll(wmax, mloc, sm.red, sm.red2);
+            }
+#ifdef FA_PACK_PROF
+            if (it == 1) PACK_MARK(8, clock64() - ti);
 #endif
             if (wmax > omega) {
                 m = wmax - omega;  // no fold: the widest box alone overflows
@@ -393,7 +451,7 @@ __device__ bool pack_candidate(const long long* __restrict__ ow, const long long
             have_fold = false;
             snap_scale(num, den, omega, m);
 #ifdef FA_PACK_PROF
-            if (it == 1) PACK_MARK(2, clock64() - ti);
+            if (it == 1) PACK_MARK(9, clock64() - ti);
 #endif
         }
         long long p = base;
@@ -506,8 +564,8 @@ __device__ bool pack_candidate(const long long* __restrict__ ow, const long long
     if (used > omega) return false;
     long long g2 = gcd_ll(num, den);
     if (g2 == 0) g2 = 1;
-    out_num = num / g2;
-    out_den = den / g2;
+    out_num = div_by_gcd(num, g2);
+    out_den = div_by_gcd(den, g2);
     return true;
 }
 
@@ -539,12 +597,12 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack(const long long* __restrict
     long long num, den;
     if (explicit_den > 0) {
         long long g = gcd_ll(explicit_num, explicit_den);
-        num = explicit_num / g;
-        den = explicit_den / g;
+        num = div_by_gcd(explicit_num, g);
+        den = div_by_gcd(explicit_den, g);
     } else {
         long long g = gcd_ll(i, n_scales);
-        num = i / g;
-        den = n_scales / g;
+        num = div_by_gcd(i, g);
+        den = div_by_gcd(n_scales, g);
     }
     size_t slot = blockIdx.x;
     int* front = gfront ? gfront + slot * (size_t)(omega + 1) : dyn_front;

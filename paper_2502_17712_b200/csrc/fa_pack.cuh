@@ -66,13 +66,29 @@ __device__ __forceinline__ long long scaled_dim_rcp(long long t, long long num, 
     return s + 2 * pad;
 }
 
+// binary (Stein) gcd: shifts and subtractions, no 64-bit division loop
 __device__ __forceinline__ long long gcd_ll(long long a, long long b) {
-    if (a < 0) a = -a;
-    if (b < 0) b = -b;
-    while (b) {
-        long long t = a % b;
-        a = b;
-        b = t;
-    }
-    return a;
+    unsigned long long u = a < 0 ? 0ull - (unsigned long long)a : (unsigned long long)a;
+    unsigned long long v = b < 0 ? 0ull - (unsigned long long)b : (unsigned long long)b;
+    if (u == 0) return (long long)v;
+    if (v == 0) return (long long)u;
+    const int sh = __ffsll((long long)(u | v)) - 1;
+    u >>= __ffsll((long long)u) - 1;
+    do {
+        v >>= __ffsll((long long)v) - 1;
+        if (u > v) {
+            unsigned long long t = u;
+            u = v;
+            v = t;
+        }
+        v -= u;
+    } while (v);
+    return (long long)(u << sh);
+}
+
+// x / g for g = gcd(...) > 0: a shift when g is a power of two (always after
+// a dyadic snap), else a 64-bit division
+__device__ __forceinline__ long long div_by_gcd(long long x, long long g) {
+    if ((g & (g - 1)) == 0) return x >> (__ffsll(g) - 1);
+    return x / g;
 }

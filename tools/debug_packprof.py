@@ -15,7 +15,7 @@ eng = FrameEngine(fa.Mesh(spec.positions, spec.triangles),
                   settings=FrameSettings(screen=spec.screen, omega=spec.omega, use_graph=False))
 L = _native.load_library()
 L.fa_debug_pack_prof.argtypes = [ctypes.c_void_p]
-buf = np.zeros((256, 8), np.int64)
+buf = np.zeros((256, 12), np.int64)
 p = spec.poses[0]
 cam = fa.CameraFrame.from_params(math.radians(p.fov_y_deg), spec.screen[0] / spec.screen[1], p.near, p.far,
                                  position=p.position, look_at=p.look_at, up=p.up)
@@ -26,4 +26,5 @@ print("charts", out.n_charts, "scale", out.scale)
 for i in range(64):
     r = buf[i]
     print(i, "fold %.1f us  heights %.1f  rowstart %.1f  rows %.1f  iters %d  n_rows %d | round 2: widths %d cyc, "
-          "+scan %d cyc" % (r[0] / 1920, r[1] / 1920, r[2] / 1920, r[3] / 1920, r[4], r[5], r[6], r[7]))
+          "+scan %d cyc +max2 %d +snap %d" % (r[0] / 1920, r[1] / 1920, r[2] / 1920, r[3] / 1920, r[4], r[5], r[6], r[7],
+                                    r[8], r[9]))
