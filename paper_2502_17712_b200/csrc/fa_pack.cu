@@ -64,6 +64,23 @@ __device__ u128 div128(u128 n, u128 d) {
     return q;
 }
 
+// exact floor(n / d) for 0 < d < 2^60 when the quotient is <= 2^25 (the
+// snap: num <= den bounds it by 2^24): an FP32 MUFU reciprocal refined by one
+// FP64 Newton step (relative error < 2^-40) puts the estimate within one of
+// the quotient; the remainder checks make it exact.
+__device__ __forceinline__ unsigned long long floor_div_snap(unsigned long long n, unsigned long long d) {
+    float rf;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rf) : "f"((float)d));
+    const double dd = (double)d;
+    double r = (double)rf;
+    r = __dmul_rn(r, __dsub_rn(2.0, __dmul_rn(dd, r)));
+    unsigned long long q = (unsigned long long)__dmul_rn((double)n, r);
+    long long rem = (long long)(n - q * d);  // |rem| < 3d: exact as a wrapped difference
+    while (rem < 0) { q -= 1; rem += (long long)d; }
+    while (rem >= (long long)d) { q += 1; rem -= (long long)d; }
+    return q;
+}
+
 // (num, den) <- reduce(floor(num*omega*2^24 / (den*(omega+m))), 2^24)
 __device__ __forceinline__ void snap_scale(long long& num, long long& den, long long omega, long long m) {
     long long fn;
@@ -73,7 +90,7 @@ __device__ __forceinline__ void snap_scale(long long& num, long long& den, long 
         den < (1ll << 31) && (omega + m) < (1ll << 32)) {
         // common case: numerator fits in 64 bits, quotient < 2^25
         const unsigned long long nn = nw << FA_SCALE_GRID_BITS;
-        fn = dd < (1ull << 60) ? (long long)floor_div_u64_small_q(nn, dd) : (long long)(nn / dd);
+        fn = dd < (1ull << 60) ? (long long)floor_div_snap(nn, dd) : (long long)(nn / dd);
     } else {
         u128 n = mul64((unsigned long long)num, (unsigned long long)omega);  // < 2^116 overall after shift
         n = shl128(n, FA_SCALE_GRID_BITS);
@@ -392,12 +409,11 @@ __device__ bool pack_candidate(const long long* __restrict__ ow, const long long
                 if (lane == 31) sm.part_sum[pb][wid] = x;
                 if (lane == 0) sm.part_max[pb][wid] = wm;
                 __syncthreads();
-                int pre = 0, bw = 0;
-                for (int w = 0; w < nw; w++) {
-                    const int ps = sm.part_sum[pb][w];
-                    pre += w < wid ? ps : 0;
-                    bw = max(bw, sm.part_max[pb][w]);
-                }
+                // every warp combines the partials itself: one load per lane + REDUX
+                const int ps = lane < nw ? sm.part_sum[pb][lane] : 0;
+                const int pm = lane < nw ? sm.part_max[pb][lane] : 0;
+                const int pre = __reduce_add_sync(0xffffffffu, lane < wid ? ps : 0);
+                const int bw = __reduce_max_sync(0xffffffffu, pm);
                 base = (long long)(pre + x - (int)local);
                 wmax = bw;
 #ifdef FA_PACK_PROF
@@ -416,9 +432,7 @@ __device__ bool pack_candidate(const long long* __restrict__ ow, const long long
                 ml = __reduce_max_sync(0xffffffffu, ml);
                 if (lane == 0) sm.part_m[pb][wid] = ml;
                 __syncthreads();
-                int bm = -(1 << 30) - 1;
-                for (int w = 0; w < nw; w++) bm = max(bm, sm.part_m[pb][w]);
-                mloc = bm;
+                mloc = __reduce_max_sync(0xffffffffu, lane < nw ? sm.part_m[pb][lane] : -(1 << 30) - 1);
                 pb ^= 1;
             } else {
                 long long tot;
