@@ -13,10 +13,23 @@
 #include "fa_internal.h"
 
 #define CMP_THREADS 256
-#define CMP_ITEMS 16
+// flags per thread of the visible compaction (one 32-bit load) and visible
+// triangles per thread of the roots compaction: few items per thread, so the
+// latency-bound gathers have many threads in flight
+#define CMP_ITEMS 4
 #define CMP_TILE (CMP_THREADS * CMP_ITEMS)
+#define ROOT_ITEMS 2
+#define ROOT_TILE (CMP_THREADS * ROOT_ITEMS)
 
-int fa_compact_blocks(long long n) { return (int)((n + CMP_TILE - 1) / CMP_TILE) > 0 ? (int)((n + CMP_TILE - 1) / CMP_TILE) : 1; }
+// per-block count slots for n items (sized for the smaller tile)
+int fa_compact_blocks(long long n) {
+    long long b = (n + ROOT_TILE - 1) / ROOT_TILE;
+    return b > 0 ? (int)b : 1;
+}
+static int blocks_for(long long n, int tile) {
+    long long b = (n + tile - 1) / tile;
+    return b > 0 ? (int)b : 1;
+}
 
 __device__ __forceinline__ int byte_sum4(unsigned int v) { return (int)((v * 0x01010101u) >> 24); }
 
@@ -41,8 +54,7 @@ __global__ void __launch_bounds__(CMP_THREADS) k_count_flags(const unsigned char
     int base = blockIdx.x * CMP_TILE + threadIdx.x * CMP_ITEMS;
     int c = 0;
     if (base + CMP_ITEMS <= T) {
-        uint4 v = *reinterpret_cast<const uint4*>(flags + base);
-        c = byte_sum4(v.x) + byte_sum4(v.y) + byte_sum4(v.z) + byte_sum4(v.w);
+        c = byte_sum4(*reinterpret_cast<const unsigned int*>(flags + base));
     } else {
         for (int i = base; i < T; i++) c += flags[i] != 0;
     }
@@ -69,10 +81,9 @@ __global__ void __launch_bounds__(CMP_THREADS) k_scatter_visible(const unsigned 
     int base = blockIdx.x * CMP_TILE + threadIdx.x * CMP_ITEMS;
     unsigned char f[CMP_ITEMS];
     if (base + CMP_ITEMS <= T) {
-        uint4 v = *reinterpret_cast<const uint4*>(flags + base);
-        unsigned int w[4] = {v.x, v.y, v.z, v.w};
+        const unsigned int w = *reinterpret_cast<const unsigned int*>(flags + base);
 #pragma unroll
-        for (int i = 0; i < CMP_ITEMS; i++) f[i] = (w[i >> 2] >> (8 * (i & 3))) & 0xffu;
+        for (int i = 0; i < CMP_ITEMS; i++) f[i] = (w >> (8 * i)) & 0xffu;
     } else {
 #pragma unroll
         for (int i = 0; i < CMP_ITEMS; i++) f[i] = (base + i < T) ? flags[base + i] : 0;
@@ -83,7 +94,7 @@ __global__ void __launch_bounds__(CMP_THREADS) k_scatter_visible(const unsigned 
     int total;
     int pos = offset + block_exclusive_scan(c, sm, &total);
     if (base + CMP_ITEMS <= T) {
-        // 16 consecutive labels: four 128-bit stores
+        // CMP_ITEMS consecutive labels: 128-bit stores
         int4* l4 = reinterpret_cast<int4*>(label + base);
 #pragma unroll
         for (int q = 0; q < CMP_ITEMS / 4; q++)
@@ -112,7 +123,7 @@ __global__ void __launch_bounds__(CMP_THREADS) k_scatter_visible(const unsigned 
 
 void fa_launch_compact_visible(const unsigned char* flags, int T, int* blocks, int* vis_list, int* label,
                                fa_dstat* st, cudaStream_t s, const int* tris, int* vmin) {
-    int nb = fa_compact_blocks(T);
+    int nb = blocks_for(T, CMP_TILE);
     fa_launch(k_count_flags, nb, CMP_THREADS, 0, s, flags, T, blocks);
     fa_launch(k_scatter_visible, nb, CMP_THREADS, 0, s, flags, T, blocks, nb, vis_list, label, tris, vmin, st);
 }
@@ -475,10 +486,10 @@ __global__ void __launch_bounds__(CMP_THREADS) k_count_roots(const int* __restri
     FA_PDL_PROLOGUE();
     __shared__ int sm[32];
     int n = st->n_vis;
-    int base = blockIdx.x * CMP_TILE + threadIdx.x * CMP_ITEMS;
+    int base = blockIdx.x * ROOT_TILE + threadIdx.x * ROOT_ITEMS;
     int c = 0;
-#pragma unroll 4
-    for (int i = 0; i < CMP_ITEMS; i++) {
+#pragma unroll
+    for (int i = 0; i < ROOT_ITEMS; i++) {
         int k = base + i;
         if (k < n) {
             int t = vis_list[k];
@@ -504,15 +515,15 @@ __global__ void __launch_bounds__(CMP_THREADS) k_scatter_roots(const int* __rest
     FA_PDL_PROLOGUE();
     __shared__ int sm[32];
     int n = st->n_vis;
-    int last = (n + CMP_TILE - 1) / CMP_TILE - 1;
+    int last = (n + ROOT_TILE - 1) / ROOT_TILE - 1;
     if (last < 0) last = 0;
     if ((int)blockIdx.x > last) return;
     int offset = block_prefix_of(blocks, blockIdx.x, sm);
-    int base = blockIdx.x * CMP_TILE + threadIdx.x * CMP_ITEMS;
-    int tv[CMP_ITEMS];
+    int base = blockIdx.x * ROOT_TILE + threadIdx.x * ROOT_ITEMS;
+    int tv[ROOT_ITEMS];
     int c = 0;
 #pragma unroll
-    for (int i = 0; i < CMP_ITEMS; i++) {
+    for (int i = 0; i < ROOT_ITEMS; i++) {
         int k = base + i;
         tv[i] = -1;
         if (k < n) {
@@ -523,7 +534,7 @@ __global__ void __launch_bounds__(CMP_THREADS) k_scatter_roots(const int* __rest
     int total;
     int pos = offset + block_exclusive_scan(c, sm, &total);
 #pragma unroll
-    for (int i = 0; i < CMP_ITEMS; i++) {
+    for (int i = 0; i < ROOT_ITEMS; i++) {
         if (tv[i] >= 0) {
             roots[pos] = tv[i];
             cidx[tv[i]] = pos;
@@ -540,7 +551,7 @@ __global__ void __launch_bounds__(CMP_THREADS) k_scatter_roots(const int* __rest
 
 void fa_launch_compact_roots(const int* vis_list, const int* label, int T, int* blocks, int* roots, int* cidx,
                              unsigned long long* ndc_keys, int* survived, fa_dstat* st, cudaStream_t s) {
-    int nb = fa_compact_blocks(T);
+    int nb = blocks_for(T, ROOT_TILE);
     fa_launch(k_count_roots, nb, CMP_THREADS, 0, s, vis_list, label, blocks, st);
     fa_launch(k_scatter_roots, nb, CMP_THREADS, 0, s, vis_list, label, blocks, nb, roots, cidx, ndc_keys, survived, st);
 }
