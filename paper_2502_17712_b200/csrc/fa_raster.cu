@@ -318,20 +318,28 @@ __global__ void __launch_bounds__(256) k_depth_hiz(const unsigned long long* __r
         const int y0 = ty * FA_HIZ, y1 = min(y0 + FA_HIZ, H);
         unsigned long long mx = 0;
         if (i < n && x < W) {
+            // all loads of the strip first (one round trip), then the tests
+            unsigned long long dv[FA_HIZ], wv[FA_HIZ];
+#pragma unroll
+            for (int k = 0; k < FA_HIZ; k++) {
+                const long long p = (long long)(y0 + k) * W + x;
+                const bool in = y0 + k < y1;
+                dv[k] = in ? depth[p] : FA_KEY_POS_INF;
+                wv[k] = (in && wid) ? wid[p] : ~0ull;
+            }
             int last = -1;
-            for (int y = y0; y < y1; y++) {
-                const long long p = (long long)y * W + x;
-                unsigned long long v = depth[p];
+#pragma unroll
+            for (int k = 0; k < FA_HIZ; k++) {
+                const unsigned long long v = dv[k];
                 bool fin = v > FA_KEY_NEG_INF && v < FA_KEY_POS_INF;
                 c += fin;
                 if (v >= FA_KEY_NEG_INF && v < FA_KEY_POS_INF && v > mx) mx = v;
                 if (wid && fin) {
                     // the winner is only trusted when its truncated key is the
                     // final key's (so any subset of writers may skip the RED)
-                    const unsigned long long wv = wid[p];
                     const unsigned long long hi = ~((1ull << FA_WID_BITS) - 1);
-                    if ((wv & hi) == (v & hi)) {
-                        int id = (int)(wv & ~hi);
+                    if ((wv[k] & hi) == (v & hi)) {
+                        int id = (int)(wv[k] & ~hi);
                         if (id != last) flags[id] = 1;
                         last = id;
                     }
