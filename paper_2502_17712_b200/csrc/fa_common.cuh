@@ -32,34 +32,41 @@
 #define FA_DFLAG_KEY_RANGE 64u
 #define FA_DFLAG_BAD_ARGS 128u
 
-// Per-frame device counters and status (one 256-byte struct, zeroed per frame).
+// Per-frame device counters and status (zeroed per frame).  The four append
+// counters of k_raster_setup take one atomic per block step each (~4K per
+// frame at C2); they sit 256 bytes apart so their atomics are served by
+// different L2 slices instead of queueing on one.
 struct fa_dstat {
     unsigned int flags;
     int n_vis;            // visible triangles
     int n_charts;         // chart roots (ascending)
     int n_small;          // small-raster triangle list length (pass 2 input)
     int n_large;          // large-raster triangle setups
-    int n_tiles;          // large-raster tile work items
     int best;             // selected candidate (1-based), 0 = none
     int floor_fail;       // pack floor-width failure
+    int n_rows_max;
     long long screen_fragments;
     long long texels_allocated;
     long long scale_num;
     long long scale_den;
-    int n_rows_max;
     int max_h;            // max oriented height (sort key range)
     unsigned int done;    // pack batch early-exit
-    int n_small3;         // stored small-triangle records (pass 2 input)
-    int n_large3;         // compact large-triangle records (stored from the back of the record array)
-    int n_clip;           // triangles routed to the generic (clipping) path
     int stretch_valid;    // triangles that entered the stretch sums
+    int n_tiles_clip;     // tiles of clipped (generic) setups, stored downward from max_tiles - 1
     double stretch_wsum;  // sum area * (S1^2 + S2^2) / 2   (metrics.py:103)
     double stretch_area;  // sum area                       (metrics.py:104)
     unsigned long long stretch_linf_bits;  // max S1 (positive double bits)
-    int n_tiles_clip;     // tiles of clipped (generic) setups, stored downward from max_tiles - 1
-    int pad[33];
+    int pad0[38];
+    int n_small3;         // stored small-triangle records (pass 2 input)
+    int pad1[63];
+    int n_large3;         // compact large-triangle records (stored from the back of the record array)
+    int pad2[63];
+    int n_clip;           // triangles routed to the generic (clipping) path
+    int pad3[63];
+    int n_tiles;          // large-raster tile work items
+    int pad4[63];
 };
-static_assert(sizeof(fa_dstat) == 256, "fa_dstat is one 256-byte block");
+static_assert(sizeof(fa_dstat) == 1280, "fa_dstat: a 256-byte status block + four 256-byte counter slots");
 
 // ---- float64 <-> order-preserving u64 key --------------------------------
 __device__ __forceinline__ unsigned long long f64_key(double x) {
