@@ -380,8 +380,8 @@ int fa_mark_visible(fa_ctx* ctx, const double* vp_host, const double* depth, int
                             P<unsigned long long>(ctx->hiz), nullptr, nullptr, s);
         fa_launch_raster_vis(P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large), P<int4>(ctx->tiles),
                              ctx->max_tiles, ctx->max_large, T, width, P<unsigned long long>(ctx->depth_keys),
-                             P<unsigned long long>(ctx->hiz), P<unsigned char>(ctx->flags), P<fa_dstat>(ctx->dstat),
-                             s, nullptr, nullptr, nullptr);
+                             P<unsigned long long>(ctx->hiz), P<unsigned char>(ctx->flags), P<int>(ctx->clip_list),
+                             P<fa_dstat>(ctx->dstat), s, nullptr, nullptr, nullptr);
         CKL();
         r = read_stat(ctx, s);
         if (r) return r;
@@ -711,7 +711,8 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     mark();  // 2: depth pass
     nl += fa_launch_raster_vis(P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large), P<int4>(ctx->tiles),
                                ctx->max_tiles, ctx->max_large, T, W, P<unsigned long long>(ctx->depth_keys),
-                               P<unsigned long long>(ctx->hiz), flags, st, s, ctx->side, ctx->fj[2], ctx->fj[3]);
+                               P<unsigned long long>(ctx->hiz), flags, P<int>(ctx->clip_list), st, s, ctx->side,
+                               ctx->fj[2], ctx->fj[3]);
     mark();  // 3: visibility pass
     // the compaction also lowers vmin (frame_init filled it with INT_MAX)
     fa_launch_compact_visible(flags, T, P<int>(ctx->blocks), P<int>(ctx->vis_list), P<int>(ctx->label), st, s,

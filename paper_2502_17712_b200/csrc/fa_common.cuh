@@ -40,7 +40,7 @@ struct fa_dstat {
     unsigned int flags;
     int n_vis;            // visible triangles
     int n_charts;         // chart roots (ascending)
-    int n_small;          // small-raster triangle list length (pass 2 input)
+    int n_vis_q;          // small records the visibility filter left for sampling
     int n_large;          // large-raster triangle setups
     int best;             // selected candidate (1-based), 0 = none
     int floor_fail;       // pack floor-width failure

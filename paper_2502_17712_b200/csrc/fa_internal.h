@@ -89,7 +89,7 @@ int fa_launch_depth_pass(bool write_depth, const double4* clip, const double4* s
                          cudaEvent_t ev_join, cudaEvent_t ev_join2);
 int fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const int4* tiles, int max_tiles,
                          int max_large, int T, int W, const unsigned long long* depth, const unsigned long long* hiz,
-                         unsigned char* flags, const fa_dstat* st, cudaStream_t s, cudaStream_t side,
+                         unsigned char* flags, int* vis_queue, fa_dstat* st, cudaStream_t s, cudaStream_t side,
                          cudaEvent_t ev_fork, cudaEvent_t ev_join);
 void fa_launch_decode_depth(const unsigned long long* keys, double* out, long long n, cudaStream_t s);
 // screen_fragments (st may be null) + 8x8 hierarchical-Z max keys + flags of

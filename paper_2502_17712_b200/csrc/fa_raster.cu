@@ -551,46 +551,76 @@ __global__ void __launch_bounds__(COOP_WARPS * 32, 6) k_small_coop(const SmallRe
     }
 }
 
-// ---- pass 2 small: one thread per covering triangle -----------------------
-__global__ void __launch_bounds__(256) k_raster_vis_small(const SmallRec* __restrict__ small_rec, int W,
-                                                          const unsigned long long* __restrict__ depth,
+// ---- pass 2 small: filter, then sample the survivors densely ---------------
+// One thread per stored record.  One round trip decides most records without
+// sampling: the flag (set by k_depth_hiz for the pixel winners of pass 1) and
+// the record's 8x8 hierarchical-Z tiles (when its window spans at most 2x2 of
+// them).  The ~20% that survive are appended (one atomic per block step) to a
+// queue that k_vis_small_sample walks one thread per survivor, so sampling
+// lanes are not spread thinly over warps that are mostly done.
+__global__ void __launch_bounds__(256) k_vis_small_filter(const SmallRec* __restrict__ small_rec,
                                                           const unsigned long long* __restrict__ hiz, int htx,
+                                                          const unsigned char* __restrict__ flags,
+                                                          int* __restrict__ queue, fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
+    __shared__ int s_cnt[8], s_base;
+    const int n3 = st->n_small3;
+    const int lane = lane_id(), warp = threadIdx.x >> 5;
+    for (int b0 = (int)blockIdx.x * blockDim.x; b0 < n3; b0 += gridDim.x * blockDim.x) {
+        const int i = b0 + threadIdx.x;
+        bool need = false;
+        if (i < n3) {
+            Setup3 f;
+            int t;
+            load_rec(small_rec + i, f, t);
+            const int tx0 = f.min_x / FA_HIZ, tx1 = f.max_x / FA_HIZ, ty0 = f.min_y / FA_HIZ, ty1 = f.max_y / FA_HIZ;
+            const bool hz = tx1 - tx0 <= 1 && ty1 - ty0 <= 1;
+            unsigned long long h00 = 1, h01 = 1, h10 = 1, h11 = 1;
+            const unsigned char seen = flags[t];
+            if (hz) {
+                h00 = __ldg(hiz + ty0 * htx + tx0);
+                h01 = __ldg(hiz + ty0 * htx + tx1);
+                h10 = __ldg(hiz + ty1 * htx + tx0);
+                h11 = __ldg(hiz + ty1 * htx + tx1);
+            }
+            const double zlb = depth_lower_bound(f, f.min_x, f.max_x, f.min_y, f.max_y);
+            need = !seen && !(hz && hiz_tile_rejects(h00, zlb) && hiz_tile_rejects(h01, zlb) &&
+                              hiz_tile_rejects(h10, zlb) && hiz_tile_rejects(h11, zlb));
+#ifdef FA_HIZ_STATS
+            if (!seen) atomicAdd(&g_hiz_stats[need ? 1 : 0], 1ull);
+#endif
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, need);
+        if (lane == 0) s_cnt[warp] = __popc(m);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int tot = 0;
+            for (int w = 0; w < 8; w++) tot += s_cnt[w];
+            s_base = tot ? atomicAdd(&st->n_vis_q, tot) : 0;
+        }
+        __syncthreads();
+        if (need) {
+            int off = s_base + __popc(m & ((1u << lane) - 1u));
+            for (int w = 0; w < warp; w++) off += s_cnt[w];
+            queue[off] = i;
+        }
+        __syncthreads();
+    }
+}
+
+// Survivors of the filter, one thread each: sample the row spans, stopping
+// at the first passing sample; up to 4 covered samples per batch of depth loads.
+__global__ void __launch_bounds__(256) k_vis_small_sample(const SmallRec* __restrict__ small_rec, int W,
+                                                          const unsigned long long* __restrict__ depth,
+                                                          const int* __restrict__ queue,
                                                           unsigned char* __restrict__ flags,
                                                           const fa_dstat* __restrict__ st) {
     FA_PDL_PROLOGUE();
-    int n3 = st->n_small3;
-    int stride = gridDim.x * blockDim.x;
-    // Stored records, one thread each.  One round trip first decides most
-    // records without sampling: the flag (set by k_depth_hiz for the pixel
-    // winners of pass 1) and the record's 8x8 hierarchical-Z tiles (when its
-    // window spans at most 2x2 of them).  The rest stop at the first passing
-    // sample, gathering up to 4 covered samples per batch of depth loads.
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n3; i += stride) {
+    const int nq_total = st->n_vis_q;
+    for (int qi = (int)blockIdx.x * blockDim.x + threadIdx.x; qi < nq_total; qi += gridDim.x * blockDim.x) {
         Setup3 f;
         int t;
-        load_rec(small_rec + i, f, t);
-        const int tx0 = f.min_x / FA_HIZ, tx1 = f.max_x / FA_HIZ, ty0 = f.min_y / FA_HIZ, ty1 = f.max_y / FA_HIZ;
-        const bool hz = tx1 - tx0 <= 1 && ty1 - ty0 <= 1;
-        unsigned long long h00 = 1, h01 = 1, h10 = 1, h11 = 1;
-        const unsigned char seen = flags[t];
-        if (hz) {
-            h00 = __ldg(hiz + ty0 * htx + tx0);
-            h01 = __ldg(hiz + ty0 * htx + tx1);
-            h10 = __ldg(hiz + ty1 * htx + tx0);
-            h11 = __ldg(hiz + ty1 * htx + tx1);
-        }
-        const double zlb = depth_lower_bound(f, f.min_x, f.max_x, f.min_y, f.max_y);
-        if (seen) continue;
-        if (hz && hiz_tile_rejects(h00, zlb) && hiz_tile_rejects(h01, zlb) && hiz_tile_rejects(h10, zlb) &&
-            hiz_tile_rejects(h11, zlb)) {
-#ifdef FA_HIZ_STATS
-            atomicAdd(&g_hiz_stats[0], 1ull);
-#endif
-            continue;
-        }
-#ifdef FA_HIZ_STATS
-        atomicAdd(&g_hiz_stats[1], 1ull);
-#endif
+        load_rec(small_rec + queue[qi], f, t);
         bool vis = false;
         // queue of up to 4 covered samples in named registers (no local memory)
         double z0 = 0, z1 = 0, z2 = 0, z3 = 0;
@@ -846,16 +876,19 @@ int fa_launch_depth_pass(bool write_depth, const double4* clip, const double4* s
 // on side.  Both only set flags, which k_depth_hiz seeded with the winners.
 int fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const int4* tiles, int max_tiles,
                          int max_large, int T, int W, const unsigned long long* depth, const unsigned long long* hiz,
-                         unsigned char* flags, const fa_dstat* st, cudaStream_t s, cudaStream_t side,
+                         unsigned char* flags, int* vis_queue, fa_dstat* st, cudaStream_t s, cudaStream_t side,
                          cudaEvent_t ev_fork, cudaEvent_t ev_join) {
     cudaStream_t b = side ? side : s;
     const int htx = fa_hiz_dim(W);
     if (side) fork_to(s, side, ev_fork);
     fa_launch(k_raster_vis_tiles, fa_cap(FA_NUM_SMS * 8), 256, 0, b, small_rec, T, large, tiles, W, depth, hiz, htx, flags, st,
                                                       max_tiles, max_large);
-    fa_launch(k_raster_vis_small, fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s, small_rec, W, depth, hiz, htx, flags, st);
+    fa_launch(k_vis_small_filter, fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s, small_rec, hiz, htx, flags, vis_queue,
+              st);
+    fa_launch(k_vis_small_sample, fa_grid(T / 4, 256, FA_NUM_SMS * 8), 256, 0, s, small_rec, W, depth, vis_queue, flags,
+              st);
     if (side) fork_to(side, s, ev_join);
-    return 2;
+    return 3;
 }
 
 void fa_launch_depth_hiz(const unsigned long long* depth, const unsigned long long* wid, int W, int H,
