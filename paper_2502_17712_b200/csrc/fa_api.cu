@@ -116,7 +116,7 @@ void fa_destroy(fa_ctx* c) {
                       &c->target, &c->survived, &c->okey, &c->oidx, &c->ow, &c->oh, &c->orot, &c->sortk, &c->sortv,
                       &c->pinv, &c->cand, &c->cand_p, &c->cand_w, &c->cand_h, &c->cand_y, &c->rowstart,
                       &c->placements, &c->uv, &c->vp_dev, &c->blocks, &c->dstat, &c->aux, &c->in_tw, &c->in_th,
-                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list, &c->hiz, &c->wid, &c->vis_chart};
+                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list, &c->hiz, &c->wid, &c->vis_chart, &c->vis_cidx, &c->plc_c};
     for (fa_buf* b : bufs) free_buf(*b);
     for (cudaEvent_t e : c->fj)
         if (e) cudaEventDestroy(e);
@@ -226,6 +226,7 @@ static int ensure_pack(fa_ctx* ctx, int64_t n_cap, int64_t n_scales, int64_t ome
     ENSURE(cand_y, (size_t)batch * n * 4);
     ENSURE(rowstart, (size_t)batch * n * 4);
     ENSURE(placements, n * 64);
+    ENSURE(plc_c, n * 32);
     if (!fa_front_in_smem(omega)) ENSURE(okey, (size_t)batch * (omega + 1) * 4);
     return FA_OK;
 }
@@ -250,6 +251,7 @@ static fa_pack_bufs pack_bufs(fa_ctx* ctx, const long long* tw, const long long*
     b.cand_y = P<int>(ctx->cand_y);
     b.rowstart = P<int>(ctx->rowstart);
     b.placements = placements;
+    b.plc_by_src = nullptr;
     b.accept_out = accept_out;
     b.gfront = P<int>(ctx->okey);
     return b;
@@ -738,7 +740,8 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     CK(cudaStreamWaitEvent(s, ctx->fj[5], 0));  // bounds read the flattened labels
     mark();  // 6: chart roots (+ flatten)
     fa_launch_chart_bounds(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->label),
-                           P<int>(ctx->cidx), T, P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), st, s);
+                           P<int>(ctx->cidx), T, P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), st, s,
+                           P<int>(ctx->vis_cidx));
     fa_launch_box_dims(P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), P<int>(ctx->roots), T, W, H,
                        p->prescale, P<double>(ctx->ndc), P<int>(ctx->px), P<long long>(ctx->target),
                        P<long long>(ctx->in_tw), P<long long>(ctx->in_th), P<long long>(ctx->in_cid), (int)n_cap,
@@ -747,6 +750,7 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     mark();  // 7: chart bounds + box dims
     fa_pack_bufs b = pack_bufs(ctx, P<long long>(ctx->in_tw), P<long long>(ctx->in_th), P<long long>(ctx->in_cid),
                                P<long long>(ctx->placements), nullptr);
+    b.plc_by_src = P<int4>(ctx->plc_c);
     fa_launch_orient_sort(b, (int)n_cap, &st->n_charts, FA_MAX_BOX_DIM, st, s);
     nl += 1;
     mark();  // 8: orient + radix order
@@ -754,7 +758,8 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     mark();  // 9: candidate pack + select
     fa_launch_uv(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->label), P<int>(ctx->cidx),
                  P<int>(ctx->pinv), P<double>(ctx->ndc), P<int>(ctx->px), P<long long>(ctx->placements), T, W, H,
-                 p->padding, p->uv_f64 != 0, ctx->uv.p, P<int>(ctx->vis_chart), st, s);
+                 p->padding, p->uv_f64 != 0, ctx->uv.p, P<int>(ctx->vis_chart), P<int>(ctx->vis_cidx),
+                 P<int4>(ctx->plc_c), st, s);
     nl += 1;
     mark();  // 10: uv
     if (p->want_depth) {
@@ -787,6 +792,7 @@ static int frame_prepare(fa_ctx* ctx, const fa_frame_params* p) {
     if (r) return r;
     ENSURE(uv, (size_t)(ctx->T + 1) * 6 * (p->uv_f64 ? 8 : 4));
     ENSURE(vis_chart, (size_t)(ctx->T + 1) * 4);
+    ENSURE(vis_cidx, (size_t)(ctx->T + 1) * 4);
     if (p->want_depth) ENSURE(depth_f64, (size_t)p->width * p->height * 8);
     return FA_OK;
 }

@@ -126,7 +126,8 @@ __global__ void __launch_bounds__(256) k_chart_bounds(const double4* __restrict_
                                                       const int* __restrict__ vis_list, const int* __restrict__ label,
                                                       const int* __restrict__ cidx,
                                                       unsigned long long* __restrict__ keys,
-                                                      int* __restrict__ survived, const fa_dstat* __restrict__ st) {
+                                                      int* __restrict__ survived, const fa_dstat* __restrict__ st,
+                                                      int* __restrict__ vis_cidx) {
     FA_PDL_PROLOGUE();
     int n = st->n_vis;
     int lane = lane_id();
@@ -140,6 +141,7 @@ __global__ void __launch_bounds__(256) k_chart_bounds(const double4* __restrict_
         if (k < n) {
             int t = vis_list[k];
             c = cidx[label[t]];
+            if (vis_cidx) vis_cidx[k] = c;  // k_uv's chart index (saves it two dependent loads)
             double4 cc[3];
 #pragma unroll
             for (int j = 0; j < 3; j++) cc[j] = ldg4(clip + __ldg(tris + 3 * t + j));
@@ -225,9 +227,9 @@ __global__ void k_box_dims(const unsigned long long* __restrict__ keys, const in
 
 void fa_launch_chart_bounds(const double4* clip, const int* tris, const int* vis_list, const int* label,
                             const int* cidx, int T, unsigned long long* ndc_keys, int* survived, const fa_dstat* st,
-                            cudaStream_t s) {
+                            cudaStream_t s, int* vis_cidx) {
     fa_launch(k_chart_bounds, fa_grid(T, 256, FA_NUM_SMS * 8), 256, 0, s, clip, tris, vis_list, label, cidx, ndc_keys,
-                                                                   survived, st);
+              survived, st, vis_cidx);
 }
 
 void fa_launch_box_dims(const unsigned long long* ndc_keys, const int* survived, const int* roots, int T, int W, int H,

@@ -47,6 +47,8 @@ struct fa_ctx {
     fa_buf hiz;             // 8x8 hierarchical-Z max keys of the final depth
     fa_buf wid;             // pass-1 pixel winners (truncated key | triangle id)
     fa_buf vis_chart;       // chart id of each visible triangle (written by k_uv)
+    fa_buf vis_cidx;        // chart index of each visible triangle (written by k_chart_bounds, read by k_uv)
+    fa_buf plc_c;           // placements by chart index (2 x int4 each; written by k_select, read by k_uv)
     size_t gen = 0;
     int max_large = 0, max_tiles = 0;
     int pack_batch = 0;  // candidates per pack launch
@@ -130,7 +132,7 @@ void fa_launch_fill(int* a, int n, int v, cudaStream_t s);
 // ---- bounds (fa_bounds.cu) -----------------------------------------------
 void fa_launch_chart_bounds(const double4* clip, const int* tris, const int* vis_list, const int* label,
                             const int* cidx, int T, unsigned long long* ndc_keys, int* survived, const fa_dstat* st,
-                            cudaStream_t s);
+                            cudaStream_t s, int* vis_cidx = nullptr);
 void fa_launch_box_dims(const unsigned long long* ndc_keys, const int* survived, const int* roots, int T, int W, int H,
                         double prescale, double* ndc, int* px, long long* target, long long* tw, long long* th,
                         long long* cid, int cap, fa_dstat* st, cudaStream_t s);
@@ -154,6 +156,7 @@ struct fa_pack_bufs {
     int* cand_y;
     int* rowstart;             // per-candidate row starts (n each)
     long long* placements;     // (n,8) packing order
+    int4* plc_by_src;          // optional (n,2) int4 per input box: {x, y, w, h}, {rot, 0, 0, 0}
     unsigned char* accept_out; // optional
     int* gfront;               // global frontline (batch x (omega+1)) when omega is too big for smem
 };
@@ -180,7 +183,8 @@ void fa_launch_fold(const long long* w, int n, long long omega, long long* rows,
 // ---- uv (fa_uv.cu) -------------------------------------------------------
 void fa_launch_uv(const double4* clip, const int* tris, const int* vis_list, const int* label, const int* cidx,
                   const int* pinv, const double* ndc, const int* px, const long long* placements, int T, int W, int H,
-                  long long pad, bool f64, void* uv, int* vis_chart, fa_dstat* st, cudaStream_t s);
+                  long long pad, bool f64, void* uv, int* vis_chart, const int* vis_cidx, const int4* plc_c,
+                  fa_dstat* st, cudaStream_t s);
 
 // ---- comparison packers (fa_baselines.cu) -----------------------------------
 void fa_launch_seq_search(const long long* ow, const long long* oh, int n, long long omega, long long n_scales,

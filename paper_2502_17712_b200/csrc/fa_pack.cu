@@ -651,7 +651,8 @@ __global__ void __launch_bounds__(1024) k_select(const long long* __restrict__ o
                                                  const long long* __restrict__ cand, const long long* __restrict__ cand_p,
                                                  const int* __restrict__ cand_w, const int* __restrict__ cand_h,
                                                  const int* __restrict__ cand_y, long long* __restrict__ placements,
-                                                 unsigned char* __restrict__ accept_out, fa_dstat* __restrict__ st) {
+                                                 int4* __restrict__ plc_by_src, unsigned char* __restrict__ accept_out,
+                                                 fa_dstat* __restrict__ st) {
     FA_PDL_PROLOGUE();
     __shared__ long long red[33];
     __shared__ long long s_best;
@@ -709,6 +710,10 @@ __global__ void __launch_bounds__(1024) k_select(const long long* __restrict__ o
         P[5] = rot[j];
         P[6] = tw[src];
         P[7] = th[src];
+        if (plc_by_src) {  // k_uv reads its chart's placement directly (x, y, w, h < 2^31)
+            plc_by_src[2 * src] = make_int4((int)x, y[j], w[j], h[j]);
+            plc_by_src[2 * src + 1] = make_int4(rot[j], 0, 0, 0);
+        }
         long long cw = w[j] - 2 * pad, chh = h[j] - 2 * pad;
         tex += (cw > 0 ? cw : 0) * (chh > 0 ? chh : 0);
     }
@@ -871,7 +876,7 @@ int fa_launch_pack(const fa_pack_bufs& b, int n_max, const int* n_dev, long long
         }
     }
     fa_launch(k_select, 1, 1024, 0, s, b.ow, b.tw, b.th, b.chart_id, b.rot, b.perm, n_max, n_dev, omega, n_scales, min_dim,
-                                pad, b.cand, b.cand_p, b.cand_w, b.cand_h, b.cand_y, b.placements, b.accept_out, st);
+                                pad, b.cand, b.cand_p, b.cand_w, b.cand_h, b.cand_y, b.placements, b.plc_by_src, b.accept_out, st);
     return launches + 1;
 }
 

@@ -39,7 +39,8 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
                                                    const double* __restrict__ ndc, const int* __restrict__ px,
                                                    const long long* __restrict__ placements, int W, int H,
                                                    long long pad, OutT* __restrict__ uv,
-                                                   int* __restrict__ vis_chart, fa_dstat* __restrict__ st) {
+                                                   int* __restrict__ vis_chart, const int* __restrict__ vis_cidx,
+                                                   const int4* __restrict__ plc_c, fa_dstat* __restrict__ st) {
     FA_PDL_PROLOGUE();
     __shared__ __align__(16) OutT stage[UV_THREADS * 6];
     __shared__ double red_w[UV_THREADS / 32], red_a[UV_THREADS / 32], red_m[UV_THREADS / 32];
@@ -57,7 +58,9 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
         if (k < n && vis_chart) vis_chart[k] = label[vis_list[k]];  // sparse chart_of_triangle
         if (k < n && !failed) {
             int t = vis_list[k];
-            int c = cidx[label[t]];
+            // chart index and placement straight from the bounds / select
+            // side outputs when present (two dependent loads instead of four)
+            int c = vis_cidx ? vis_cidx[k] : cidx[label[t]];
             double4 v[3];
             bool behind = false;
 #pragma unroll
@@ -66,13 +69,21 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
                 if (v[i].w <= FA_W_EPSILON) behind = true;
             }
             if (!behind) {
-                int j = pinv[c];
-                const long long* P = placements + 8 * (long long)j;
-                long long cw = P[3] - 2 * pad, ch = P[4] - 2 * pad;
+                long long px_, py_, pw_, ph_;
+                bool rot;
+                if (plc_c) {
+                    const int4 a = plc_c[2 * c], b = plc_c[2 * c + 1];
+                    px_ = a.x; py_ = a.y; pw_ = a.z; ph_ = a.w;
+                    rot = b.x != 0;
+                } else {
+                    const long long* P = placements + 8 * (long long)pinv[c];
+                    px_ = P[1]; py_ = P[2]; pw_ = P[3]; ph_ = P[4];
+                    rot = P[5] != 0;
+                }
+                long long cw = pw_ - 2 * pad, ch = ph_ - 2 * pad;
                 double w_px = (double)px[2 * c], h_px = (double)px[2 * c + 1];
-                double bx = (double)(P[1] + pad), by = (double)(P[2] + pad);
+                double bx = (double)(px_ + pad), by = (double)(py_ + pad);
                 double mnx = ndc[4 * c], mny = ndc[4 * c + 1];
-                bool rot = P[5] != 0;
                 double rx = rot ? __ddiv_rn((double)cw, h_px) : __ddiv_rn((double)cw, w_px);
                 double ry = rot ? __ddiv_rn((double)ch, w_px) : __ddiv_rn((double)ch, h_px);
                 double scr[6];
@@ -144,12 +155,13 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
 
 void fa_launch_uv(const double4* clip, const int* tris, const int* vis_list, const int* label, const int* cidx,
                   const int* pinv, const double* ndc, const int* px, const long long* placements, int T, int W, int H,
-                  long long pad, bool f64, void* uv, int* vis_chart, fa_dstat* st, cudaStream_t s) {
+                  long long pad, bool f64, void* uv, int* vis_chart, const int* vis_cidx, const int4* plc_c,
+                  fa_dstat* st, cudaStream_t s) {
     int grid = fa_grid(T, UV_THREADS, FA_NUM_SMS * 8);
     if (f64)
         fa_launch(k_uv<double>, grid, UV_THREADS, 0, s, clip, tris, vis_list, label, cidx, pinv, ndc, px, placements, W, H,
-                                                 pad, (double*)uv, vis_chart, st);
+                                                 pad, (double*)uv, vis_chart, vis_cidx, plc_c, st);
     else
         fa_launch(k_uv<float>, grid, UV_THREADS, 0, s, clip, tris, vis_list, label, cidx, pinv, ndc, px, placements, W, H,
-                                                pad, (float*)uv, vis_chart, st);
+                                                pad, (float*)uv, vis_chart, vis_cidx, plc_c, st);
 }
