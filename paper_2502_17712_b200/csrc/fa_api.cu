@@ -145,6 +145,12 @@ int fa_set_mesh(fa_ctx* ctx, const double* positions, int64_t n_vertices, const 
 
 }  // extern "C"
 
+// integer tuning knob from the environment (read once per name)
+int fa_env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
 float fa_grid_cap_scale() {
     static float f = -1.f;
     if (f < 0.f) {
@@ -705,7 +711,9 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     nl += fa_launch_depth_pass(true, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, W, H,
                                p->backface_cull, P<unsigned long long>(ctx->depth_keys), wid,
                                P<SmallRec>(ctx->small_rec), P<int>(ctx->clip_list), P<TriSetup>(ctx->large),
-                               ctx->max_large, P<int4>(ctx->tiles), ctx->max_tiles, st, s, ctx->side, ctx->side2,
+                               ctx->max_large, P<int4>(ctx->tiles), ctx->max_tiles, st, s,
+                               fa_env_int("FASTATLAS_DEPTH_BRANCHES", 3) >= 2 ? ctx->side : nullptr,
+                               fa_env_int("FASTATLAS_DEPTH_BRANCHES", 3) >= 3 ? ctx->side2 : nullptr,
                                ctx->fj[0], ctx->fj[1], ctx->fj[7]);
     fa_launch_depth_hiz(P<unsigned long long>(ctx->depth_keys), wid, W, H, P<unsigned long long>(ctx->hiz), flags, st,
                         s);
