@@ -454,6 +454,9 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const SmallRec* __re
 // window averages ~20 samples for ~1.5 covered ones.  Depth pass only
 // (RED.MIN.64 per covered sample).
 #define COOP_WARPS 4
+#ifndef COOP_MIN_BLOCKS
+#define COOP_MIN_BLOCKS 5
+#endif
 struct CoopWarp {
     SmallRec rec[2][32];  // double buffer: the next 32 records stream in (cp.async) during the current ones
     int prefix[33];
@@ -476,7 +479,7 @@ __device__ __forceinline__ void coop_issue(const SmallRec* __restrict__ recs, in
     }
 }
 
-__global__ void __launch_bounds__(COOP_WARPS * 32, 6) k_small_coop(const SmallRec* __restrict__ recs, int W,
+__global__ void __launch_bounds__(COOP_WARPS * 32, COOP_MIN_BLOCKS) k_small_coop(const SmallRec* __restrict__ recs, int W,
                                                                    unsigned long long* __restrict__ depth,
                                                                    unsigned long long* __restrict__ wid,
                                                                    const fa_dstat* __restrict__ st) {
@@ -539,11 +542,12 @@ __global__ void __launch_bounds__(COOP_WARPS * 32, 6) k_small_coop(const SmallRe
                 const RowTerms rt = row_terms(f, (double)iy + 0.5);
                 int xa, xb;
                 row_span(f, rt, se, xa, xb);
-                for (int ix = xa; ix <= xb; ix++) {
-                    const double px = (double)ix + 0.5;
+                const long long rowoff = (long long)iy * W;
+                double px = (double)xa + 0.5;  // px += 1 below is exact (half-integers < 2^52)
+                for (int ix = xa; ix <= xb; ix++, px += 1.0) {
                     // depth evaluated alongside the edges (independent DP chains)
                     const double z = depth_row(f, rt, px);
-                    if (inside_row(f, rt, px)) depth_min(depth, wid, (long long)iy * W + ix, f64_key(z), t, false);
+                    if (inside_row(f, rt, px)) depth_min(depth, wid, rowoff + ix, f64_key(z), t, false);
                 }
             }
         }
