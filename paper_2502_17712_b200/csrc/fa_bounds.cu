@@ -177,12 +177,14 @@ __global__ void __launch_bounds__(256) k_chart_bounds(const double4* __restrict_
         int next_c = __shfl_down_sync(0xffffffffu, c, 1);
         bool tail = (lane == 31) || (next_c != c);
         if (tail && c >= 0 && surv) {
+            // fire-and-forget REDs (one set per chart run per warp); a
+            // load-first check would add a round trip to every run
             unsigned long long* kk = keys + 4 * (long long)c;
-            if (k0 < kk[0]) atomicMin(kk + 0, k0);
-            if (k1 < kk[1]) atomicMin(kk + 1, k1);
-            if (k2 > kk[2]) atomicMax(kk + 2, k2);
-            if (k3 > kk[3]) atomicMax(kk + 3, k3);
-            if (!survived[c]) survived[c] = 1;
+            atomicMin(kk + 0, k0);
+            atomicMin(kk + 1, k1);
+            atomicMax(kk + 2, k2);
+            atomicMax(kk + 3, k3);
+            survived[c] = 1;
         }
     }
 }
@@ -235,8 +237,9 @@ void fa_launch_chart_bounds(const double4* clip, const int* tris, const int* vis
 void fa_launch_box_dims(const unsigned long long* ndc_keys, const int* survived, const int* roots, int T, int W, int H,
                         double prescale, double* ndc, int* px, long long* target, long long* tw, long long* th,
                         long long* cid, int cap, fa_dstat* st, cudaStream_t s) {
-    fa_launch(k_box_dims, fa_grid(T, 256, FA_NUM_SMS * 4), 256, 0, s, ndc_keys, survived, roots, W, H, prescale, ndc, px,
-                                                               target, tw, th, cid, cap, st);
+    // grid-stride over the chart count; sized by the chart capacity, not T
+    fa_launch(k_box_dims, fa_grid(cap < T ? cap : T, 256, FA_NUM_SMS * 4), 256, 0, s, ndc_keys, survived, roots, W, H,
+              prescale, ndc, px, target, tw, th, cid, cap, st);
 }
 
 // ---- batched standalone API kernels -------------------------------------------
