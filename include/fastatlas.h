@@ -208,8 +208,9 @@ int fa_frame(fa_ctx *ctx, const double *vp_host, const fa_frame_params *params, 
              void *stream);
 
 /* Enqueue (asynchronously, on `stream`) the device->host copies of a
- * finished frame's results into caller buffers (pinned for overlap); any
- * pointer may be NULL to skip that output.  Sizes come from `res`:
+ * finished frame's results into caller buffers (pinned host memory for
+ * overlap, or device memory: the copies use cudaMemcpyDefault); any pointer
+ * may be NULL to skip that output.  Sizes come from `res`:
  * chart_of_triangle T int32, visible n_visible int32, uv n_visible x 6
  * (float32, or float64 when the frame ran with uv_f64), placements n_charts
  * x 8 int64.  The caller synchronises `stream` before reading.  Replaces the

@@ -952,10 +952,10 @@ int fa_frame_download(fa_ctx* ctx, const fa_frame_result* res, int32_t* chart_of
     size_t nv = (size_t)res->n_visible, C = (size_t)res->n_charts;
     size_t uv_elem = ctx->last_params.uv_f64 ? 8 : 4;
     if (chart_of_triangle && ctx->T)
-        CK(cudaMemcpyAsync(chart_of_triangle, res->chart_of_triangle, (size_t)ctx->T * 4, cudaMemcpyDeviceToHost, s));
-    if (visible && nv) CK(cudaMemcpyAsync(visible, res->visible, nv * 4, cudaMemcpyDeviceToHost, s));
-    if (uv && nv) CK(cudaMemcpyAsync(uv, res->uv, nv * 6 * uv_elem, cudaMemcpyDeviceToHost, s));
-    if (placements && C) CK(cudaMemcpyAsync(placements, res->placements, C * 64, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(chart_of_triangle, res->chart_of_triangle, (size_t)ctx->T * 4, cudaMemcpyDefault, s));
+    if (visible && nv) CK(cudaMemcpyAsync(visible, res->visible, nv * 4, cudaMemcpyDefault, s));
+    if (uv && nv) CK(cudaMemcpyAsync(uv, res->uv, nv * 6 * uv_elem, cudaMemcpyDefault, s));
+    if (placements && C) CK(cudaMemcpyAsync(placements, res->placements, C * 64, cudaMemcpyDefault, s));
     return FA_OK;
 }
 
@@ -967,11 +967,11 @@ int fa_frame_download_visible(fa_ctx* ctx, const fa_frame_result* res, int32_t* 
     CK(cudaSetDevice(ctx->device));
     size_t nv = (size_t)res->n_visible, C = (size_t)res->n_charts;
     size_t uv_elem = ctx->last_params.uv_f64 ? 8 : 4;
-    if (visible && nv) CK(cudaMemcpyAsync(visible, res->visible, nv * 4, cudaMemcpyDeviceToHost, s));
+    if (visible && nv) CK(cudaMemcpyAsync(visible, res->visible, nv * 4, cudaMemcpyDefault, s));
     if (visible_chart && nv)
-        CK(cudaMemcpyAsync(visible_chart, res->visible_chart, nv * 4, cudaMemcpyDeviceToHost, s));
-    if (uv && nv) CK(cudaMemcpyAsync(uv, res->uv, nv * 6 * uv_elem, cudaMemcpyDeviceToHost, s));
-    if (placements && C) CK(cudaMemcpyAsync(placements, res->placements, C * 64, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(visible_chart, res->visible_chart, nv * 4, cudaMemcpyDefault, s));
+    if (uv && nv) CK(cudaMemcpyAsync(uv, res->uv, nv * 6 * uv_elem, cudaMemcpyDefault, s));
+    if (placements && C) CK(cudaMemcpyAsync(placements, res->placements, C * 64, cudaMemcpyDefault, s));
     return FA_OK;
 }
 
