@@ -51,8 +51,13 @@ const char *fa_last_error(void);
 int fa_create(fa_ctx **out, int device);
 void fa_destroy(fa_ctx *ctx);
 
-/* Bind a resident mesh (Mesh, charts.py:29-61).  The caller keeps both
- * buffers alive while the context uses them. */
+/* Bind a resident mesh (Mesh, charts.py:29-61): device pointers, positions
+ * (V,3) float64 and triangles (T,3) int32.  The context keeps its own copy
+ * with the vertices renumbered in order of first use (better locality for
+ * the per-vertex gathers; triangle order and every output are unchanged,
+ * per-vertex outputs come back in the caller's numbering), so call it again
+ * after modifying the caller's arrays.  ValueError on an index outside
+ * [0, V).  `positions` must stay valid for fa_project, which reads it. */
 int fa_set_mesh(fa_ctx *ctx, const double *positions, int64_t n_vertices,
                 const int32_t *triangles, int64_t n_triangles);
 

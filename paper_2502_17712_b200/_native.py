@@ -17,6 +17,7 @@ import ctypes
 import os
 import subprocess
 import threading
+import weakref
 
 import numpy as np
 
@@ -244,11 +245,15 @@ class Context:
         return ctypes.c_void_p(_torch().cuda.current_stream(self.device).cuda_stream)
 
     def set_mesh(self, pos_t, tris_t):
+        """Bind a mesh (fa_set_mesh keeps a renumbered device copy).  Re-binding
+        the same live tensors is free; a different or freed-and-reallocated
+        mesh (same pointers, new contents) is bound again."""
         key = (pos_t.data_ptr(), tris_t.data_ptr(), pos_t.shape[0], tris_t.shape[0])
-        if key != self._mesh_key:
+        prev = self._mesh_key
+        if prev is None or prev[0] != key or prev[1]() is not pos_t or prev[2]() is not tris_t:
             raise_for_status(self.L.fa_set_mesh(self.h, ctypes.c_void_p(pos_t.data_ptr()), pos_t.shape[0],
                                                 ctypes.c_void_p(tris_t.data_ptr()), tris_t.shape[0]))
-            self._mesh_key = key
+            self._mesh_key = (key, weakref.ref(pos_t), weakref.ref(tris_t))
 
 
 _contexts: dict = {}

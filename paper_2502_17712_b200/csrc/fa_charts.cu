@@ -349,13 +349,31 @@ __global__ void k_canon_apply(const unsigned char* __restrict__ flags, int* labe
         label[t] = flags[t] ? tmp[label[t]] : -1;
 }
 
-__global__ void k_v2c(const int* __restrict__ vmin, const int* __restrict__ label, int* __restrict__ v2c, int V) {
+// vertex -> chart in the caller's vertex numbering (vperm: internal -> caller index)
+__global__ void k_v2c(const int* __restrict__ vmin, const int* __restrict__ label, int* __restrict__ v2c, int V,
+                      const int* __restrict__ vperm) {
     FA_PDL_PROLOGUE();
     int stride = gridDim.x * blockDim.x;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += stride) {
         int m = vmin[v];
-        v2c[v] = m == 0x7fffffff ? -1 : label[m];
+        v2c[vperm ? vperm[v] : v] = m == 0x7fffffff ? -1 : label[m];
     }
+}
+
+__global__ void k_permute_pos(const double* __restrict__ pos, const int* __restrict__ vperm,
+                              double* __restrict__ out, int V) {
+    FA_PDL_PROLOGUE();
+    int stride = gridDim.x * blockDim.x;
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += stride) {
+        const long long o = 3ll * vperm[v];
+        out[3ll * v] = pos[o];
+        out[3ll * v + 1] = pos[o + 1];
+        out[3ll * v + 2] = pos[o + 2];
+    }
+}
+
+void fa_launch_permute_pos(const double* pos, const int* vperm, double* out, int V, cudaStream_t s) {
+    fa_launch(k_permute_pos, fa_grid(V, 256, FA_NUM_SMS * 8), 256, 0, s, pos, vperm, out, V);
 }
 
 __global__ void k_flags_from_labels(const int* __restrict__ labels, unsigned char* __restrict__ flags, int T) {
@@ -469,8 +487,8 @@ void fa_launch_canon_apply(const unsigned char* flags, int* label, const int* tm
     fa_launch(k_canon_apply, uf_grid(T), 256, 0, s, flags, label, tmp, T);
 }
 
-void fa_launch_v2c(const int* vmin, const int* label, int* v2c, int V, cudaStream_t s) {
-    fa_launch(k_v2c, fa_grid(V, 256, FA_NUM_SMS * 8), 256, 0, s, vmin, label, v2c, V);
+void fa_launch_v2c(const int* vmin, const int* label, int* v2c, int V, cudaStream_t s, const int* vperm) {
+    fa_launch(k_v2c, fa_grid(V, 256, FA_NUM_SMS * 8), 256, 0, s, vmin, label, v2c, V, vperm);
 }
 
 void fa_launch_flags_from_labels(const int* labels, unsigned char* flags, int T, cudaStream_t s) {

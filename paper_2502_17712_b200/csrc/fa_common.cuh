@@ -233,6 +233,7 @@ __device__ __forceinline__ void fa_pdl_trigger() { asm volatile("griddepcontrol.
     } while (0)
 
 bool fa_pdl_enabled();  // FASTATLAS_PDL=0 disables (fa_api.cu)
+int fa_env_int(const char* name, int dflt);  // integer knob from the environment (fa_api.cu)
 
 template <typename... KArgs, typename... Args>
 static inline void fa_launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,

@@ -33,10 +33,17 @@ struct fa_graph_key {
 
 struct fa_ctx {
     int device = 0;
-    // resident mesh (caller-owned)
+    // resident mesh.  pos/tris are what the kernels read: the context's own
+    // copy with vertices renumbered in order of first use (fa_set_mesh), so
+    // the three vertices of consecutive triangles share cache lines; the
+    // caller's arrays stay untouched (pos_user feeds per-vertex outputs in
+    // the caller's numbering, vperm maps new -> caller vertex index).
     const double* pos = nullptr;
     const int* tris = nullptr;
+    const double* pos_user = nullptr;
+    const int* vperm = nullptr;
     int64_t V = 0, T = 0;
+    fa_buf pos_perm, tris_perm, vperm_buf;
 
     // scratch (grown on demand)
     fa_buf small_rec, clip, depth_keys, depth_f64, flags, vis_list, large, tiles, label, vmin, v2c, cidx;
@@ -121,7 +128,9 @@ void fa_launch_build_adjacency(const int* tris, int T, unsigned long long* keys,
                                unsigned long long table_size, int* adj, cudaStream_t s);
 void fa_launch_uf_compress(const int* vis_list, int* label, int T, const fa_dstat* st, cudaStream_t s);
 void fa_launch_canonicalize(const int* vis_list, int* label, int* tmp, int T, const fa_dstat* st, cudaStream_t s);
-void fa_launch_v2c(const int* vmin, const int* label, int* v2c, int V, cudaStream_t s);
+void fa_launch_v2c(const int* vmin, const int* label, int* v2c, int V, cudaStream_t s, const int* vperm = nullptr);
+// out[v] = pos[vperm[v]] (3 doubles each)
+void fa_launch_permute_pos(const double* pos, const int* vperm, double* out, int V, cudaStream_t s);
 void fa_launch_flags_from_labels(const int* labels, unsigned char* flags, int T, cudaStream_t s);
 // ordered compaction of roots (label[t]==t over the vis list) -> roots, cidx, chart init
 void fa_launch_compact_roots(const int* vis_list, const int* label, int T, int* blocks, int* roots, int* cidx,
