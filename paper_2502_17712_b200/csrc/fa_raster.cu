@@ -460,6 +460,7 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const SmallRec* __re
 struct CoopWarp {
     SmallRec rec[2][32];  // double buffer: the next 32 records stream in (cp.async) during the current ones
     int prefix[33];
+    SpanEdges se[32];     // each record's span reciprocals, computed once by the lane that owns it
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* g) {
@@ -501,7 +502,13 @@ __global__ void __launch_bounds__(COOP_WARPS * 32, COOP_MIN_BLOCKS) k_small_coop
         const SmallRec* rb = cw.rec[buf];
         const int cnt = min(32, n - base);
         int np = 0;
-        if (lane < cnt) np = rb[lane].max_y - rb[lane].min_y + 1;
+        if (lane < cnt) {
+            np = rb[lane].max_y - rb[lane].min_y + 1;
+            Setup3 fo;
+            int to;
+            load_rec(&rb[lane], fo, to);
+            cw.se[lane] = span_edges(fo);
+        }
         int incl = np;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -526,7 +533,7 @@ __global__ void __launch_bounds__(COOP_WARPS * 32, COOP_MIN_BLOCKS) k_small_coop
             Setup3 f;
             int t;
             load_rec(&rb[r], f, t);
-            SpanEdges se = span_edges(f);
+            SpanEdges se = cw.se[r];
             int pe = cw.prefix[r + 1];
             int iy = f.min_y + (s - cw.prefix[r]);
             for (; s < s_end; s++, iy++) {
@@ -536,7 +543,7 @@ __global__ void __launch_bounds__(COOP_WARPS * 32, COOP_MIN_BLOCKS) k_small_coop
                         pe = cw.prefix[r + 1];
                     } while (s >= pe);
                     load_rec(&rb[r], f, t);
-                    se = span_edges(f);
+                    se = cw.se[r];
                     iy = f.min_y;
                 }
                 const RowTerms rt = row_terms(f, (double)iy + 0.5);
