@@ -217,6 +217,14 @@ __device__ __forceinline__ long long block_sum_ll(long long v, long long* smem32
     return smem32[32];
 }
 
+// ---- cp.async (LDGSTS): global -> shared copies that complete in the background
+__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
 // ---- programmatic dependent launch (PDL) ---------------------------------
 // Frame kernels are launched with programmatic stream serialization, so a
 // kernel's CTAs are scheduled while its predecessor drains instead of after

@@ -398,17 +398,34 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const SmallRec* __re
     const int n_tiles = from_back ? min(st->n_tiles_clip, max_tiles - n_front) : n_front;
     const int4* tl = from_back ? tiles + (max_tiles - 1) : tiles;
     const int dir = from_back ? -1 : 1;
-    // descriptors are read one step ahead: a step waits for the record only
-    int4 nxt = make_int4(0, 0, 0, 0);
+    // Pipeline: the next tile's 96-byte record streams into shared memory
+    // (cp.async, lanes 0-5) while this tile samples, and descriptors are read
+    // two steps ahead, so a step waits for neither.
+    __shared__ __align__(16) SmallRec srec[8][2];
     const int w0 = (int)blockIdx.x * 8 + warp;
-    if (w0 < n_tiles) nxt = tl[dir * w0];
-    for (int w = w0; w < n_tiles; w += nwarps) {
-        int4 rec = nxt;
-        if (w + nwarps < n_tiles) nxt = tl[dir * (w + nwarps)];
+    int4 cur = make_int4(-1, 0, 0, 0), nxt = make_int4(-1, 0, 0, 0);
+    if (w0 < n_tiles) cur = tl[dir * w0];
+    if (w0 + nwarps < n_tiles) nxt = tl[dir * (w0 + nwarps)];
+    auto fetch = [&](const int4& d, int b) {
+        if (d.x >= 0 && lane < (int)(sizeof(SmallRec) / 16))
+            cp_async16(reinterpret_cast<char*>(&srec[warp][b]) + 16 * lane,
+                       reinterpret_cast<const char*>(recs + d.x) + 16 * lane);
+    };
+    if (w0 < n_tiles) fetch(cur, 0);
+    cp_async_commit();
+    int buf = 0;
+    for (int w = w0; w < n_tiles; w += nwarps, buf ^= 1) {
+        int4 rec = cur;
+        cur = nxt;
+        if (w + 2 * nwarps < n_tiles) nxt = tl[dir * (w + 2 * nwarps)];
+        if (w + nwarps < n_tiles) fetch(cur, buf ^ 1);
+        cp_async_commit();
+        cp_async_wait1();
+        __syncwarp();
         if (rec.x >= 0) {
             Setup3 f;
             int t;
-            load_rec(recs + rec.x, f, t);
+            load_rec(&srec[warp][buf], f, t);
             int x, y0;
             tile_lane_origin(f.min_x, f.max_x, f.min_y, rec.y, x, y0);
             if (x <= f.max_x) {
@@ -423,6 +440,7 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const SmallRec* __re
                               check != 0);
                 }
             }
+            __syncwarp();  // this buffer is refilled by the next step's prefetch
             continue;
         }
         rec.x = -rec.x - 1;
@@ -443,6 +461,7 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const SmallRec* __re
                 depth_min(depth, wid, (long long)y * W + x, f64_key(sample_depth(s, px, py)), s.tri, check != 0);
             }
         }
+        __syncwarp();
     }
 }
 
@@ -463,12 +482,6 @@ struct CoopWarp {
     SpanEdges se[32];     // each record's span reciprocals, computed once by the lane that owns it
 };
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 __device__ __forceinline__ void coop_issue(const SmallRec* __restrict__ recs, int base, int n, SmallRec* dst) {
     const int lane = lane_id();
