@@ -117,7 +117,7 @@ void fa_destroy(fa_ctx* c) {
                       &c->target, &c->survived, &c->okey, &c->oidx, &c->ow, &c->oh, &c->orot, &c->sortk, &c->sortv,
                       &c->pinv, &c->cand, &c->cand_p, &c->cand_w, &c->cand_h, &c->cand_y, &c->rowstart,
                       &c->placements, &c->uv, &c->vp_dev, &c->blocks, &c->dstat, &c->aux, &c->in_tw, &c->in_th,
-                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list, &c->hiz, &c->wid, &c->vis_chart, &c->vis_cidx, &c->plc_c, &c->pos_perm, &c->tris_perm, &c->vperm_buf};
+                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list, &c->hiz, &c->wid, &c->vis_chart, &c->vis_cidx, &c->plc_c, &c->pos_perm, &c->tris_perm, &c->vperm_buf, &c->vis_tris};
     for (fa_buf* b : bufs) free_buf(*b);
     for (cudaEvent_t e : c->fj)
         if (e) cudaEventDestroy(e);
@@ -234,6 +234,7 @@ static int ensure_raster(fa_ctx* ctx, int W, int H, bool depth) {
 static int ensure_charts(fa_ctx* ctx) {
     int64_t T = ctx->T, V = ctx->V;
     ENSURE(vis_list, (T + 1) * 4);
+    ENSURE(vis_tris, (T + 1) * 16);
     ENSURE(label, (T + 1) * 4);
     ENSURE(vmin, (V + 1) * 4);
     ENSURE(v2c, (V + 1) * 4);
@@ -765,11 +766,11 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     mark();  // 3: visibility pass
     // the compaction also lowers vmin (frame_init filled it with INT_MAX)
     fa_launch_compact_visible(flags, T, P<int>(ctx->blocks), P<int>(ctx->vis_list), P<int>(ctx->label), st, s,
-                              ctx->tris, P<int>(ctx->vmin));
+                              ctx->tris, P<int>(ctx->vmin), P<int4>(ctx->vis_tris));
     nl += 2;
     mark();  // 4: visible compaction
     nl += fa_launch_uf_vertex(ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->vmin), P<int>(ctx->label), T, st, s,
-                              true);
+                              true, P<int4>(ctx->vis_tris));
     mark();  // 5: union-find charts (hooking)
     // Roots are the nodes with label[t] == t after hooking, which flattening
     // never changes (it only rewrites non-roots to their root, also != t), so
@@ -788,7 +789,7 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     mark();  // 6: chart roots (+ flatten)
     fa_launch_chart_bounds(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->label),
                            P<int>(ctx->cidx), T, P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), st, s,
-                           P<int>(ctx->vis_cidx));
+                           P<int>(ctx->vis_cidx), P<int4>(ctx->vis_tris));
     fa_launch_box_dims(P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), P<int>(ctx->roots), T, W, H,
                        p->prescale, P<double>(ctx->ndc), P<int>(ctx->px), P<long long>(ctx->target),
                        P<long long>(ctx->in_tw), P<long long>(ctx->in_th), P<long long>(ctx->in_cid), (int)n_cap,
@@ -806,7 +807,7 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     fa_launch_uv(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->label), P<int>(ctx->cidx),
                  P<int>(ctx->pinv), P<double>(ctx->ndc), P<int>(ctx->px), P<long long>(ctx->placements), T, W, H,
                  p->padding, p->uv_f64 != 0, ctx->uv.p, P<int>(ctx->vis_chart), P<int>(ctx->vis_cidx),
-                 P<int4>(ctx->plc_c), st, s);
+                 P<int4>(ctx->plc_c), st, s, P<int4>(ctx->vis_tris));
     nl += 1;
     mark();  // 10: uv
     if (p->want_depth) {

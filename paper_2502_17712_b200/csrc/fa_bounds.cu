@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(256) k_chart_bounds(const double4* __restrict_
                                                       const int* __restrict__ cidx,
                                                       unsigned long long* __restrict__ keys,
                                                       int* __restrict__ survived, const fa_dstat* __restrict__ st,
-                                                      int* __restrict__ vis_cidx) {
+                                                      int* __restrict__ vis_cidx, const int4* __restrict__ vis_tris) {
     FA_PDL_PROLOGUE();
     int n = st->n_vis;
     int lane = lane_id();
@@ -139,12 +139,21 @@ __global__ void __launch_bounds__(256) k_chart_bounds(const double4* __restrict_
         unsigned long long k0 = FA_KEY_POS_INF, k1 = FA_KEY_POS_INF, k2 = FA_KEY_NEG_INF, k3 = FA_KEY_NEG_INF;
         int surv = 0;
         if (k < n) {
-            int t = vis_list[k];
+            double4 cc[3];
+            int t;
+            if (vis_tris) {  // vertex indices next to the id: one dependent load fewer
+                const int4 q = vis_tris[k];
+                t = q.w;
+                cc[0] = ldg4(clip + q.x);
+                cc[1] = ldg4(clip + q.y);
+                cc[2] = ldg4(clip + q.z);
+            } else {
+                t = vis_list[k];
+#pragma unroll
+                for (int j = 0; j < 3; j++) cc[j] = ldg4(clip + __ldg(tris + 3 * t + j));
+            }
             c = cidx[label[t]];
             if (vis_cidx) vis_cidx[k] = c;  // k_uv's chart index (saves it two dependent loads)
-            double4 cc[3];
-#pragma unroll
-            for (int j = 0; j < 3; j++) cc[j] = ldg4(clip + __ldg(tris + 3 * t + j));
             NBox b = empty_box();
             if (tri_box(cc, b)) {
                 surv = 1;
@@ -229,9 +238,9 @@ __global__ void k_box_dims(const unsigned long long* __restrict__ keys, const in
 
 void fa_launch_chart_bounds(const double4* clip, const int* tris, const int* vis_list, const int* label,
                             const int* cidx, int T, unsigned long long* ndc_keys, int* survived, const fa_dstat* st,
-                            cudaStream_t s, int* vis_cidx) {
+                            cudaStream_t s, int* vis_cidx, const int4* vis_tris) {
     fa_launch(k_chart_bounds, fa_grid(T, 256, FA_NUM_SMS * 8), 256, 0, s, clip, tris, vis_list, label, cidx, ndc_keys,
-              survived, st, vis_cidx);
+              survived, st, vis_cidx, vis_tris);
 }
 
 void fa_launch_box_dims(const unsigned long long* ndc_keys, const int* survived, const int* roots, int T, int W, int H,

@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(CMP_THREADS) k_scatter_visible(const unsigned 
                                                                  const int* __restrict__ blocks, int nblocks,
                                                                  int* __restrict__ vis_list, int* __restrict__ label,
                                                                  const int* __restrict__ tris, int* __restrict__ vmin,
+                                                                 int4* __restrict__ vis_tris,
                                                                  fa_dstat* __restrict__ st) {
     FA_PDL_PROLOGUE();
     __shared__ int sm[32];
@@ -109,23 +110,34 @@ __global__ void __launch_bounds__(CMP_THREADS) k_scatter_visible(const unsigned 
     for (int i = 0; i < CMP_ITEMS; i++) {
         int t = base + i;
         if (t < T && f[i]) {
-            vis_list[pos++] = t;
-            if (vmin) {
+            if (vis_tris) {
+                // the visible triangle's vertex indices next to its id: the
+                // later per-visible-triangle kernels skip one dependent load
+                const int a = __ldg(tris + 3 * t), b = __ldg(tris + 3 * t + 1), c = __ldg(tris + 3 * t + 2);
+                vis_tris[pos] = make_int4(a, b, c, t);
+                if (vmin) {
+                    atomicMin(vmin + a, t);
+                    atomicMin(vmin + b, t);
+                    atomicMin(vmin + c, t);
+                }
+            } else if (vmin) {
                 // fire-and-forget REDs: a load-first check would put a round
                 // trip per vertex into this thread's sequential item loop
 #pragma unroll
                 for (int j = 0; j < 3; j++) atomicMin(vmin + __ldg(tris + 3 * t + j), t);
             }
+            vis_list[pos++] = t;
         }
     }
     if (blockIdx.x == nblocks - 1 && threadIdx.x == 0) st->n_vis = offset + total;
 }
 
 void fa_launch_compact_visible(const unsigned char* flags, int T, int* blocks, int* vis_list, int* label,
-                               fa_dstat* st, cudaStream_t s, const int* tris, int* vmin) {
+                               fa_dstat* st, cudaStream_t s, const int* tris, int* vmin, int4* vis_tris) {
     int nb = blocks_for(T, CMP_TILE);
     fa_launch(k_count_flags, nb, CMP_THREADS, 0, s, flags, T, blocks);
-    fa_launch(k_scatter_visible, nb, CMP_THREADS, 0, s, flags, T, blocks, nb, vis_list, label, tris, vmin, st);
+    fa_launch(k_scatter_visible, nb, CMP_THREADS, 0, s, flags, T, blocks, nb, vis_list, label, tris, vmin,
+              tris ? vis_tris : nullptr, st);
 }
 
 // ---- union-find ---------------------------------------------------------------
@@ -240,13 +252,21 @@ __global__ void k_vmin(const int* __restrict__ tris, const int* __restrict__ vis
 // Hooking to a node m that has meanwhile stopped being a root is still a
 // valid union (parent[r] = m < r keeps the min-rooted forest).
 __global__ void k_hook_multi(const int* __restrict__ tris, const int* __restrict__ vis_list,
-                             const int* __restrict__ vmin, int* label, const fa_dstat* __restrict__ st) {
+                             const int* __restrict__ vmin, int* label, const fa_dstat* __restrict__ st,
+                             const int4* __restrict__ vis_tris) {
     FA_PDL_PROLOGUE();
     int n = st->n_vis;
     int stride = gridDim.x * blockDim.x;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
-        int t = vis_list[k];
-        int r1 = vmin[__ldg(tris + 3 * t)], r2 = vmin[__ldg(tris + 3 * t + 1)], r3 = vmin[__ldg(tris + 3 * t + 2)];
+        int t, r1, r2, r3;
+        if (vis_tris) {
+            const int4 q = vis_tris[k];
+            t = q.w;
+            r1 = vmin[q.x], r2 = vmin[q.y], r3 = vmin[q.z];
+        } else {
+            t = vis_list[k];
+            r1 = vmin[__ldg(tris + 3 * t)], r2 = vmin[__ldg(tris + 3 * t + 1)], r3 = vmin[__ldg(tris + 3 * t + 2)];
+        }
         const int m0 = min(min(t, r1), min(r2, r3));
         int r0 = m0 < t ? atomicCAS(label + t, t, m0) : label[t];
         if (r0 == t) r0 = m0;
@@ -453,9 +473,9 @@ void fa_launch_build_adjacency(const int* tris, int T, unsigned long long* keys,
 }
 
 int fa_launch_uf_vertex(const int* tris, const int* vis_list, int* vmin, int* label, int T, const fa_dstat* st,
-                        cudaStream_t s, bool vmin_ready) {
+                        cudaStream_t s, bool vmin_ready, const int4* vis_tris) {
     if (!vmin_ready) fa_launch(k_vmin, uf_grid(T), 256, 0, s, tris, vis_list, vmin, st);
-    fa_launch(k_hook_multi, uf_grid(T), 256, 0, s, tris, vis_list, vmin, label, st);
+    fa_launch(k_hook_multi, uf_grid(T), 256, 0, s, tris, vis_list, vmin, label, st, vis_tris);
     return vmin_ready ? 1 : 2;
 }
 

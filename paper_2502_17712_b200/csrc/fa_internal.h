@@ -56,6 +56,7 @@ struct fa_ctx {
     fa_buf vis_chart;       // chart id of each visible triangle (written by k_uv)
     fa_buf vis_cidx;        // chart index of each visible triangle (written by k_chart_bounds, read by k_uv)
     fa_buf plc_c;           // placements by chart index (2 x int4 each; written by k_select, read by k_uv)
+    fa_buf vis_tris;        // (a, b, c, t) of each visible triangle (written by the compaction)
     size_t gen = 0;
     int max_large = 0, max_tiles = 0;
     int pack_batch = 0;  // candidates per pack launch
@@ -112,13 +113,16 @@ size_t fa_trisetup_bytes();
 // ---- charts (fa_charts.cu) -----------------------------------------------
 // ordered compaction of flags -> vis list; label[t] = flag ? t : -1
 // with tris + vmin (vmin pre-filled with INT_MAX) it also computes vmin
+// with tris: also vis_tris[k] = (a, b, c, t) of each visible triangle (when
+// non-null) and vmin lowering (when non-null)
 void fa_launch_compact_visible(const unsigned char* flags, int T, int* blocks, int* vis_list, int* label,
-                               fa_dstat* st, cudaStream_t s, const int* tris = nullptr, int* vmin = nullptr);
+                               fa_dstat* st, cudaStream_t s, const int* tris = nullptr, int* vmin = nullptr,
+                               int4* vis_tris = nullptr);
 int fa_compact_blocks(long long n);
 // vmin_ready: vmin already holds the per-vertex minima (computed by the
 // visible compaction); otherwise it must hold INT_MAX and is computed here
 int fa_launch_uf_vertex(const int* tris, const int* vis_list, int* vmin, int* label, int T, const fa_dstat* st,
-                         cudaStream_t s, bool vmin_ready = false);
+                         cudaStream_t s, bool vmin_ready = false, const int4* vis_tris = nullptr);
 void fa_launch_uf_edges(const int* adjacency, const unsigned char* flags, const int* vis_list, int* label, int T,
                         const fa_dstat* st, cudaStream_t s);
 void fa_launch_uf_labels(const int* labels_in, const int* vis_list, int* label, int T, const fa_dstat* st,
@@ -141,7 +145,7 @@ void fa_launch_fill(int* a, int n, int v, cudaStream_t s);
 // ---- bounds (fa_bounds.cu) -----------------------------------------------
 void fa_launch_chart_bounds(const double4* clip, const int* tris, const int* vis_list, const int* label,
                             const int* cidx, int T, unsigned long long* ndc_keys, int* survived, const fa_dstat* st,
-                            cudaStream_t s, int* vis_cidx = nullptr);
+                            cudaStream_t s, int* vis_cidx = nullptr, const int4* vis_tris = nullptr);
 void fa_launch_box_dims(const unsigned long long* ndc_keys, const int* survived, const int* roots, int T, int W, int H,
                         double prescale, double* ndc, int* px, long long* target, long long* tw, long long* th,
                         long long* cid, int cap, fa_dstat* st, cudaStream_t s);
@@ -193,7 +197,7 @@ void fa_launch_fold(const long long* w, int n, long long omega, long long* rows,
 void fa_launch_uv(const double4* clip, const int* tris, const int* vis_list, const int* label, const int* cidx,
                   const int* pinv, const double* ndc, const int* px, const long long* placements, int T, int W, int H,
                   long long pad, bool f64, void* uv, int* vis_chart, const int* vis_cidx, const int4* plc_c,
-                  fa_dstat* st, cudaStream_t s);
+                  fa_dstat* st, cudaStream_t s, const int4* vis_tris = nullptr);
 
 // ---- comparison packers (fa_baselines.cu) -----------------------------------
 void fa_launch_seq_search(const long long* ow, const long long* oh, int n, long long omega, long long n_scales,

@@ -40,7 +40,8 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
                                                    const long long* __restrict__ placements, int W, int H,
                                                    long long pad, OutT* __restrict__ uv,
                                                    int* __restrict__ vis_chart, const int* __restrict__ vis_cidx,
-                                                   const int4* __restrict__ plc_c, fa_dstat* __restrict__ st) {
+                                                   const int4* __restrict__ plc_c, const int4* __restrict__ vis_tris,
+                                                   fa_dstat* __restrict__ st) {
     FA_PDL_PROLOGUE();
     __shared__ __align__(16) OutT stage[UV_THREADS * 6];
     __shared__ double red_w[UV_THREADS / 32], red_a[UV_THREADS / 32], red_m[UV_THREADS / 32];
@@ -55,9 +56,11 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
         const double qnan = __longlong_as_double(0x7ff8000000000000ll);
 #pragma unroll
         for (int i = 0; i < 6; i++) out[i] = qnan;
-        if (k < n && vis_chart) vis_chart[k] = label[vis_list[k]];  // sparse chart_of_triangle
+        int4 vq = make_int4(0, 0, 0, -1);
+        if (k < n && vis_tris) vq = vis_tris[k];
+        if (k < n && vis_chart) vis_chart[k] = label[vis_tris ? vq.w : vis_list[k]];  // sparse chart_of_triangle
         if (k < n && !failed) {
-            int t = vis_list[k];
+            int t = vis_tris ? vq.w : vis_list[k];
             // chart index and placement straight from the bounds / select
             // side outputs when present (two dependent loads instead of four)
             int c = vis_cidx ? vis_cidx[k] : cidx[label[t]];
@@ -65,7 +68,7 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
             bool behind = false;
 #pragma unroll
             for (int i = 0; i < 3; i++) {
-                v[i] = ldg4(clip + __ldg(tris + 3 * t + i));
+                v[i] = ldg4(clip + (vis_tris ? (i == 0 ? vq.x : (i == 1 ? vq.y : vq.z)) : __ldg(tris + 3 * t + i)));
                 if (v[i].w <= FA_W_EPSILON) behind = true;
             }
             if (!behind) {
@@ -156,12 +159,12 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
 void fa_launch_uv(const double4* clip, const int* tris, const int* vis_list, const int* label, const int* cidx,
                   const int* pinv, const double* ndc, const int* px, const long long* placements, int T, int W, int H,
                   long long pad, bool f64, void* uv, int* vis_chart, const int* vis_cidx, const int4* plc_c,
-                  fa_dstat* st, cudaStream_t s) {
+                  fa_dstat* st, cudaStream_t s, const int4* vis_tris) {
     int grid = fa_grid(T, UV_THREADS, FA_NUM_SMS * 8);
     if (f64)
         fa_launch(k_uv<double>, grid, UV_THREADS, 0, s, clip, tris, vis_list, label, cidx, pinv, ndc, px, placements, W, H,
-                                                 pad, (double*)uv, vis_chart, vis_cidx, plc_c, st);
+                                                 pad, (double*)uv, vis_chart, vis_cidx, plc_c, vis_tris, st);
     else
         fa_launch(k_uv<float>, grid, UV_THREADS, 0, s, clip, tris, vis_list, label, cidx, pinv, ndc, px, placements, W, H,
-                                                pad, (float*)uv, vis_chart, vis_cidx, plc_c, st);
+                                                pad, (float*)uv, vis_chart, vis_cidx, plc_c, vis_tris, st);
 }
