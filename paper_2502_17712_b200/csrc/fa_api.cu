@@ -790,16 +790,16 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     fa_launch_chart_bounds(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->label),
                            P<int>(ctx->cidx), T, P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), st, s,
                            P<int>(ctx->vis_cidx), P<int4>(ctx->vis_tris));
-    fa_launch_box_dims(P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), P<int>(ctx->roots), T, W, H,
-                       p->prescale, P<double>(ctx->ndc), P<int>(ctx->px), P<long long>(ctx->target),
-                       P<long long>(ctx->in_tw), P<long long>(ctx->in_th), P<long long>(ctx->in_cid), (int)n_cap,
-                       st, s);
-    nl += 2;
-    mark();  // 7: chart bounds + box dims
+    nl += 1;
+    mark();  // 7: chart bounds (the box dims run at the head of the order kernel)
     fa_pack_bufs b = pack_bufs(ctx, P<long long>(ctx->in_tw), P<long long>(ctx->in_th), P<long long>(ctx->in_cid),
                                P<long long>(ctx->placements), nullptr);
     b.plc_by_src = P<int4>(ctx->plc_c);
-    fa_launch_orient_sort(b, (int)n_cap, &st->n_charts, FA_MAX_BOX_DIM, st, s);
+    const fa_box_dims_args bd{P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), P<int>(ctx->roots), W, H,
+                              p->prescale, P<double>(ctx->ndc), P<int>(ctx->px), P<long long>(ctx->target),
+                              P<long long>(ctx->in_tw), P<long long>(ctx->in_th), P<long long>(ctx->in_cid),
+                              (int)n_cap};
+    fa_launch_orient_sort(b, (int)n_cap, &st->n_charts, FA_MAX_BOX_DIM, st, s, &bd);
     nl += 1;
     mark();  // 8: orient + radix order
     nl += fa_launch_pack(b, (int)n_cap, &st->n_charts, p->omega, p->n_scales, p->min_dim, p->padding, batch, st, s);

@@ -207,33 +207,8 @@ __global__ void k_box_dims(const unsigned long long* __restrict__ keys, const in
     FA_PDL_PROLOGUE();
     int n = st->n_charts;
     int stride = gridDim.x * blockDim.x;
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
-        if (!survived[j]) atomicOr(&st->flags, FA_DFLAG_DEGENERATE_CHART);
-        double mnx = key_f64(keys[4 * j]), mny = key_f64(keys[4 * j + 1]);
-        double mxx = key_f64(keys[4 * j + 2]), mxy = key_f64(keys[4 * j + 3]);
-        ndc[4 * j] = mnx;
-        ndc[4 * j + 1] = mny;
-        ndc[4 * j + 2] = mxx;
-        ndc[4 * j + 3] = mxy;
-        double fw = ceil(__dmul_rn(__ddiv_rn(__dsub_rn(mxx, mnx), 2.0), (double)W));
-        double fh = ceil(__dmul_rn(__ddiv_rn(__dsub_rn(mxy, mny), 2.0), (double)H));
-        long long w = fw < 1.0 ? 1 : (long long)fw;
-        long long h = fh < 1.0 ? 1 : (long long)fh;
-        px[2 * j] = (int)w;
-        px[2 * j + 1] = (int)h;
-        double tw = ceil(__dmul_rn(prescale, (double)w));
-        double th = ceil(__dmul_rn(prescale, (double)h));
-        long long itw = tw < 1.0 ? 1 : (long long)tw, ith = th < 1.0 ? 1 : (long long)th;
-        target[2 * j] = itw;
-        target[2 * j + 1] = ith;
-        if (j >= cap) {
-            atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW);
-            continue;
-        }
-        otw[j] = itw;
-        oth[j] = ith;
-        cid[j] = roots[j];
-    }
+    fa_box_dims_args a{keys, survived, roots, W, H, prescale, ndc, px, target, otw, oth, cid, cap};
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) fa_box_dims_one(a, j, st);
 }
 
 void fa_launch_chart_bounds(const double4* clip, const int* tris, const int* vis_list, const int* label,

@@ -282,3 +282,50 @@ __device__ __forceinline__ double4 ldg4(const double4* p) {
     double2 a = __ldg(q), b = __ldg(q + 1);
     return make_double4(a.x, a.y, b.x, b.y);
 }
+
+// ---- per-chart box dims (geometry.py:352-362 viewport_box + cli.py:379-384) --
+// NDC box -> (w_px, h_px) = max(1, ceil(extent/2 * W)) -> target dims
+// max(1, ceil(prescale * dim)); the packer's inputs for j < cap.  Shared by
+// k_box_dims and the frame's fused order kernel.
+struct fa_box_dims_args {
+    const unsigned long long* keys;  // 4 order-preserving keys per chart (min x, min y, max x, max y)
+    const int* survived;
+    const int* roots;
+    int W, H;
+    double prescale;
+    double* ndc;
+    int* px;
+    long long* target;
+    long long* otw;
+    long long* oth;
+    long long* cid;
+    int cap;
+};
+
+__device__ __forceinline__ void fa_box_dims_one(const fa_box_dims_args& a, int j, fa_dstat* st) {
+    if (!a.survived[j]) atomicOr(&st->flags, FA_DFLAG_DEGENERATE_CHART);
+    double mnx = key_f64(a.keys[4 * j]), mny = key_f64(a.keys[4 * j + 1]);
+    double mxx = key_f64(a.keys[4 * j + 2]), mxy = key_f64(a.keys[4 * j + 3]);
+    a.ndc[4 * j] = mnx;
+    a.ndc[4 * j + 1] = mny;
+    a.ndc[4 * j + 2] = mxx;
+    a.ndc[4 * j + 3] = mxy;
+    double fw = ceil(__dmul_rn(__ddiv_rn(__dsub_rn(mxx, mnx), 2.0), (double)a.W));
+    double fh = ceil(__dmul_rn(__ddiv_rn(__dsub_rn(mxy, mny), 2.0), (double)a.H));
+    long long w = fw < 1.0 ? 1 : (long long)fw;
+    long long h = fh < 1.0 ? 1 : (long long)fh;
+    a.px[2 * j] = (int)w;
+    a.px[2 * j + 1] = (int)h;
+    double tw = ceil(__dmul_rn(a.prescale, (double)w));
+    double th = ceil(__dmul_rn(a.prescale, (double)h));
+    long long itw = tw < 1.0 ? 1 : (long long)tw, ith = th < 1.0 ? 1 : (long long)th;
+    a.target[2 * j] = itw;
+    a.target[2 * j + 1] = ith;
+    if (j >= a.cap) {
+        atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW);
+        return;
+    }
+    a.otw[j] = itw;
+    a.oth[j] = ith;
+    a.cid[j] = a.roots[j];
+}

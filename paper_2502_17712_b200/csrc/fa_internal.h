@@ -173,8 +173,9 @@ struct fa_pack_bufs {
     unsigned char* accept_out; // optional
     int* gfront;               // global frontline (batch x (omega+1)) when omega is too big for smem
 };
+// bd (optional): compute the per-chart box dims (k_box_dims' work) first, in the same launch
 void fa_launch_orient_sort(const fa_pack_bufs& b, int n_max, const int* n_dev, long long max_h, fa_dstat* st,
-                           cudaStream_t s);
+                           cudaStream_t s, const fa_box_dims_args* bd = nullptr);
 int fa_launch_pack(const fa_pack_bufs& b, int n_max, const int* n_dev, long long omega, long long n_scales,
                    long long min_dim, long long pad, int batch, fa_dstat* st, cudaStream_t s);
 void fa_launch_orient_sort_mt(const long long* tw, const long long* th, const long long* mt, int n, long long max_h,

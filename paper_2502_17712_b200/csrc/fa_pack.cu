@@ -167,15 +167,24 @@ __device__ void radix_pass(const unsigned long long* ki, const int* vi, unsigned
 }
 
 // Frame mode (mt == nullptr): input order already ascending min_tri.
-__global__ void __launch_bounds__(SORT_THREADS) k_orient_sort(const long long* __restrict__ tw,
-                                                              const long long* __restrict__ th,
+// With bd.keys set (frame mode) the per-chart box dims are computed first
+// (fa_box_dims_one, formerly its own launch); tw/th are then the dims this
+// block just wrote, so they are read without __restrict__ (no .nc loads).
+__global__ void __launch_bounds__(SORT_THREADS) k_orient_sort(const long long* tw,
+                                                              const long long* th,
                                                               const long long* __restrict__ mt, int n_max,
                                                               const int* __restrict__ n_dev, long long max_h,
                                                               long long* __restrict__ ow, long long* __restrict__ oh,
                                                               unsigned char* __restrict__ rot, int* __restrict__ perm,
                                                               int* __restrict__ pinv, unsigned long long* sk,
-                                                              int* sv, int reject_dups, fa_dstat* __restrict__ st) {
+                                                              int* sv, int reject_dups, fa_dstat* __restrict__ st,
+                                                              fa_box_dims_args bd) {
     FA_PDL_PROLOGUE();
+    if (bd.keys) {
+        const int nc = n_dev ? *n_dev : n_max;
+        for (int j = threadIdx.x; j < nc; j += blockDim.x) fa_box_dims_one(bd, j, st);
+        __syncthreads();
+    }
     __shared__ SortSmem sm;
     int n = n_dev ? *n_dev : n_max;
     if (n > n_max) {
@@ -842,16 +851,18 @@ static void ensure_smem_attr() {
 }
 
 void fa_launch_orient_sort(const fa_pack_bufs& b, int n_max, const int* n_dev, long long max_h, fa_dstat* st,
-                           cudaStream_t s) {
+                           cudaStream_t s, const fa_box_dims_args* bd) {
+    fa_box_dims_args none{};
     fa_launch(k_orient_sort, 1, SORT_THREADS, 0, s, b.tw, b.th, nullptr, n_max, n_dev, max_h, b.ow, b.oh, b.rot, b.perm,
-                                              b.pinv, b.sortk, b.sortv, 0, st);
+              b.pinv, b.sortk, b.sortv, 0, st, bd ? *bd : none);
 }
 
 void fa_launch_orient_sort_mt(const long long* tw, const long long* th, const long long* mt, int n, long long max_h,
                               long long* ow, long long* oh, unsigned char* rot, int* perm, int* pinv,
                               unsigned long long* sk, int* sv, int reject_dups, fa_dstat* st, cudaStream_t s) {
+    fa_box_dims_args none{};
     fa_launch(k_orient_sort, 1, SORT_THREADS, 0, s, tw, th, mt, n, nullptr, max_h, ow, oh, rot, perm, pinv, sk, sv,
-                                              reject_dups, st);
+              reject_dups, st, none);
 }
 
 // returns number of kernel launches
