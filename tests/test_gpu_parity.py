@@ -481,3 +481,28 @@ class TestBaselines:
         with pytest.raises(fa.PackFailure):
             make_packer("superblock", 64, 1, 0, block_size=bad["block_size"])(
                 [fa.ChartBox(*b) for b in bad["boxes"]], bad["omega"])
+
+
+@pytest.mark.parametrize("order", ["1", "0"])
+def test_shuffled_vertices_and_unused_vertices(order, monkeypatch):
+    """fa_set_mesh renumbers vertices in order of first use (FASTATLAS_VERTEX_ORDER=1,
+    the default) or keeps the caller's numbering (=0); with shuffled vertex ids
+    and vertices no triangle uses, every output -- the per-vertex map in the
+    caller's numbering included (unused vertices -1) -- equals the oracle's."""
+    monkeypatch.setenv("FASTATLAS_VERTEX_ORDER", order)
+    spec = scenes.build_scene("C1")
+    rng = np.random.default_rng(5)
+    V = len(spec.positions)
+    extra = rng.normal(size=(300, 3))                      # never referenced
+    pos = np.vstack([spec.positions, extra])
+    perm = rng.permutation(len(pos))                       # new id of each old vertex
+    pos_s = np.empty_like(pos)
+    pos_s[perm] = pos
+    tris_s = perm[spec.triangles.astype(np.int64)].astype(np.int32)
+    vp = _scene_vp(spec, spec.poses[0])
+    eng = FrameEngine(fa.Mesh(pos_s, tris_s), settings=FrameSettings(screen=spec.screen, omega=spec.omega,
+                                                                      uv_f64=True))
+    h = eng.run(vp).to_host()
+    r = oracle.run_frame(pos_s, tris_s, vp, spec.screen, spec.omega)
+    _check_vs_oracle(h, r)
+    assert np.all(h["vertex_to_chart"][perm[V:]] == -1)
