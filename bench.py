@@ -421,8 +421,9 @@ def main():
             "e2e": {"value": frames_total / (e2e_ms * 1e-3), "unit": "atlases/s", "h2d_bytes_per_step": 128,
                     "d2h_bytes_per_step": int(d2h[0] / K),
                     "what": "FramePipeline.run over pinned camera matrices (H2D per view) with the visible list, "
-                            "the chart id of each visible triangle (sparse chart_of_triangle), f32 UVs and "
-                            "placements copied into pinned host buffers (D2H per view)"},
+                            "the chart id of each visible triangle (sparse chart_of_triangle), the f32 UV of each "
+                            "visible vertex (compact form of the per-triangle f32 UV rows, rebuilt bit-identically "
+                            "on access) and the placements copied into pinned host buffers (D2H per view)"},
             "gpu_launches": launches_per_frame * K,
             "launches_per_frame": launches_per_frame,
             "stage_ms": stage_ms,

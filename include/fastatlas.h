@@ -202,6 +202,9 @@ typedef struct fa_frame_result {
     const int64_t *placements;      /* (n_charts,8) packing order */
     const void *uv;                 /* (n_visible,6) float32 or float64, NaN = no UV */
     const int32_t *visible_chart;   /* (n_visible,) chart id of each visible triangle (sparse chart_of_triangle) */
+    int64_t n_visible_vertices;     /* vertices touched by a visible triangle */
+    const int32_t *visible_vertices; /* (n_visible_vertices,) their ids, ascending, caller's numbering */
+    const float *vertex_uv;         /* (n_visible_vertices,2) float32 UV of each (NaN: at/behind the camera plane) */
 } fa_frame_result;
 
 /* Enqueue a whole frame on `stream` (no host synchronisation). */
@@ -230,6 +233,16 @@ int fa_frame_download(fa_ctx *ctx, const fa_frame_result *res, int32_t *chart_of
  * Same conventions as fa_frame_download. */
 int fa_frame_download_visible(fa_ctx *ctx, const fa_frame_result *res, int32_t *visible, int32_t *visible_chart,
                               void *uv, int64_t *placements, void *stream);
+
+/* Compact wire format for streaming clients: fa_frame_download_visible
+ * without the (n_visible,6) UV rows, plus the UV of each visible vertex
+ * (visible_vertices n_visible_vertices int32, vertex_uv n_visible_vertices x 2
+ * float32).  Every triangle of a vertex's chart computes the same UV for it
+ * (cli.py:436-449 depends on the vertex and its chart only), so a visible
+ * triangle's float32 row is (vertex_uv of its 3 vertices), NaN when any of
+ * them is NaN -- bit-identical to the frame's float32 `uv` rows. */
+int fa_frame_download_compact(fa_ctx *ctx, const fa_frame_result *res, int32_t *visible, int32_t *visible_chart,
+                              int32_t *visible_vertices, float *vertex_uv, int64_t *placements, void *stream);
 
 /* Number of kernels the last fa_frame_launch enqueued (benchmark accounting). */
 int fa_last_launch_count(fa_ctx *ctx);

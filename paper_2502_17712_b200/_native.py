@@ -40,7 +40,7 @@ EXPORTS = (
     "fa_depth_prepass", "fa_mark_visible", "fa_build_adjacency", "fa_connected_charts", "fa_merge_shared_vertices",
     "fa_chart_boxes", "fa_blinn_clamped_ndc", "fa_select_side_plane", "fa_chart_bbox",
     "fa_viewport_box", "fa_orient", "fa_orient_order", "fa_fold", "fa_push_up", "fa_pack_at_scale",
-    "fa_pack", "fa_frame_launch", "fa_frame_finish", "fa_frame", "fa_frame_download", "fa_frame_download_visible", "fa_last_launch_count",
+    "fa_pack", "fa_frame_launch", "fa_frame_finish", "fa_frame", "fa_frame_download", "fa_frame_download_visible", "fa_frame_download_compact", "fa_last_launch_count",
     "fa_stage_times", "fa_stage_name", "fa_frame_counters", "fa_sequential_scale_search", "fa_sequential_pack", "fa_superblock_pack",
 )
 
@@ -71,6 +71,7 @@ class FrameResult(ctypes.Structure):
         ("roots", ctypes.c_void_p), ("ndc", ctypes.c_void_p), ("px", ctypes.c_void_p),
         ("target", ctypes.c_void_p), ("placements", ctypes.c_void_p), ("uv", ctypes.c_void_p),
         ("visible_chart", ctypes.c_void_p),
+        ("n_visible_vertices", ctypes.c_int64), ("visible_vertices", ctypes.c_void_p), ("vertex_uv", ctypes.c_void_p),
     ]
 
 
@@ -127,6 +128,7 @@ def load_library():
             "fa_frame": ([vp, vp, ctypes.POINTER(FrameParams), ctypes.POINTER(FrameResult), vp], ci),
             "fa_frame_download": ([vp, ctypes.POINTER(FrameResult), vp, vp, vp, vp, vp], ci),
             "fa_frame_download_visible": ([vp, ctypes.POINTER(FrameResult), vp, vp, vp, vp, vp], ci),
+            "fa_frame_download_compact": ([vp, ctypes.POINTER(FrameResult), vp, vp, vp, vp, vp, vp], ci),
             "fa_last_launch_count": ([vp], ci),
             "fa_stage_times": ([vp, ctypes.POINTER(ctypes.c_float), ci, vp], ci),
             "fa_stage_name": ([ci], ctypes.c_char_p),

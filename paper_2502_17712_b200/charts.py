@@ -70,6 +70,10 @@ class Mesh:
     def n_triangles(self) -> int:
         return len(self.triangles)
 
+    @property
+    def n_vertices(self) -> int:
+        return len(self.positions)
+
     def triangle_corners(self, indices=None) -> np.ndarray:
         tris = self.triangles if indices is None else self.triangles[indices]
         return self.positions[tris]

@@ -117,7 +117,7 @@ void fa_destroy(fa_ctx* c) {
                       &c->target, &c->survived, &c->okey, &c->oidx, &c->ow, &c->oh, &c->orot, &c->sortk, &c->sortv,
                       &c->pinv, &c->cand, &c->cand_p, &c->cand_w, &c->cand_h, &c->cand_y, &c->rowstart,
                       &c->placements, &c->uv, &c->vp_dev, &c->blocks, &c->dstat, &c->aux, &c->in_tw, &c->in_th,
-                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list, &c->hiz, &c->wid, &c->vis_chart, &c->vis_cidx, &c->plc_c, &c->pos_perm, &c->tris_perm, &c->vperm_buf, &c->vis_tris};
+                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list, &c->hiz, &c->wid, &c->vis_chart, &c->vis_cidx, &c->plc_c, &c->pos_perm, &c->tris_perm, &c->vperm_buf, &c->vis_tris, &c->vslot, &c->vlist, &c->vuv, &c->vblocks};
     for (fa_buf* b : bufs) free_buf(*b);
     for (cudaEvent_t e : c->fj)
         if (e) cudaEventDestroy(e);
@@ -780,8 +780,10 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     fa_launch_uf_compress(P<int>(ctx->vis_list), P<int>(ctx->label), T, st, ctx->side);
     CK(cudaEventRecord(ctx->fj[5], ctx->side));
     fa_launch_v2c(P<int>(ctx->vmin), P<int>(ctx->label), P<int>(ctx->v2c), V, ctx->side, ctx->vperm);
+    fa_launch_visible_vertices(P<int>(ctx->vmin), V, ctx->vperm, P<int>(ctx->vblocks), P<int>(ctx->vslot),
+                               P<int>(ctx->vlist), st, ctx->side);
     CK(cudaEventRecord(ctx->fj[6], ctx->side));
-    nl += 2;
+    nl += 4;
     fa_launch_compact_roots(P<int>(ctx->vis_list), P<int>(ctx->label), T, P<int>(ctx->blocks), P<int>(ctx->roots),
                             P<int>(ctx->cidx), P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), st, s);
     nl += 2;
@@ -804,17 +806,18 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     mark();  // 8: orient + radix order
     nl += fa_launch_pack(b, (int)n_cap, &st->n_charts, p->omega, p->n_scales, p->min_dim, p->padding, batch, st, s);
     mark();  // 9: candidate pack + select
+    CK(cudaStreamWaitEvent(s, ctx->fj[6], 0));  // vertex -> chart map and the visible-vertex slots
     fa_launch_uv(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->label), P<int>(ctx->cidx),
                  P<int>(ctx->pinv), P<double>(ctx->ndc), P<int>(ctx->px), P<long long>(ctx->placements), T, W, H,
                  p->padding, p->uv_f64 != 0, ctx->uv.p, P<int>(ctx->vis_chart), P<int>(ctx->vis_cidx),
-                 P<int4>(ctx->plc_c), st, s, P<int4>(ctx->vis_tris));
+                 P<int4>(ctx->plc_c), st, s, P<int4>(ctx->vis_tris), P<int>(ctx->vslot), P<float2>(ctx->vuv));
     nl += 1;
     mark();  // 10: uv
     if (p->want_depth) {
         fa_launch_decode_depth(P<unsigned long long>(ctx->depth_keys), P<double>(ctx->depth_f64), (long long)W * H, s);
         nl += 1;
     }
-    CK(cudaStreamWaitEvent(s, ctx->fj[6], 0));  // vertex -> chart map
+
     CK(cudaMemcpyAsync(ctx->hstat, ctx->dstat.p, sizeof(fa_dstat), cudaMemcpyDeviceToHost, s));
     CKL();
     return FA_OK;
@@ -841,6 +844,10 @@ static int frame_prepare(fa_ctx* ctx, const fa_frame_params* p) {
     ENSURE(uv, (size_t)(ctx->T + 1) * 6 * (p->uv_f64 ? 8 : 4));
     ENSURE(vis_chart, (size_t)(ctx->T + 1) * 4);
     ENSURE(vis_cidx, (size_t)(ctx->T + 1) * 4);
+    ENSURE(vslot, (size_t)(ctx->V + 1) * 4);
+    ENSURE(vlist, (size_t)(ctx->V + 1) * 4);
+    ENSURE(vuv, (size_t)(ctx->V + 1) * 8);
+    ENSURE(vblocks, (size_t)fa_vertex_blocks(ctx->V + 1) * 4 + 64);
     if (p->want_depth) ENSURE(depth_f64, (size_t)p->width * p->height * 8);
     return FA_OK;
 }
@@ -938,6 +945,9 @@ int fa_frame_finish(fa_ctx* ctx, fa_frame_result* out, void* stream) {
     out->placements = P<int64_t>(ctx->placements);
     out->uv = ctx->uv.p;
     out->visible_chart = P<int32_t>(ctx->vis_chart);
+    out->n_visible_vertices = h->n_vis_vertices;
+    out->visible_vertices = P<int32_t>(ctx->vlist);
+    out->vertex_uv = P<float>(ctx->vuv);
     int64_t n_cap = ctx->pack_cap;
     ctx->needs_rerun = false;
     if (h->flags & FA_DFLAG_QUEUE_OVERFLOW || h->n_charts > n_cap) {
@@ -995,6 +1005,22 @@ int fa_frame_download(fa_ctx* ctx, const fa_frame_result* res, int32_t* chart_of
         CK(cudaMemcpyAsync(chart_of_triangle, res->chart_of_triangle, (size_t)ctx->T * 4, cudaMemcpyDefault, s));
     if (visible && nv) CK(cudaMemcpyAsync(visible, res->visible, nv * 4, cudaMemcpyDefault, s));
     if (uv && nv) CK(cudaMemcpyAsync(uv, res->uv, nv * 6 * uv_elem, cudaMemcpyDefault, s));
+    if (placements && C) CK(cudaMemcpyAsync(placements, res->placements, C * 64, cudaMemcpyDefault, s));
+    return FA_OK;
+}
+
+int fa_frame_download_compact(fa_ctx* ctx, const fa_frame_result* res, int32_t* visible, int32_t* visible_chart,
+                              int32_t* visible_vertices, float* vertex_uv, int64_t* placements, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || !res) return set_err(FA_VALUE_ERROR, "bad arguments");
+    if (res->status != FA_OK) return set_err(FA_VALUE_ERROR, "frame result has no outputs (status %d)", res->status);
+    CK(cudaSetDevice(ctx->device));
+    size_t nv = (size_t)res->n_visible, C = (size_t)res->n_charts, nvv = (size_t)res->n_visible_vertices;
+    if (visible && nv) CK(cudaMemcpyAsync(visible, res->visible, nv * 4, cudaMemcpyDefault, s));
+    if (visible_chart && nv) CK(cudaMemcpyAsync(visible_chart, res->visible_chart, nv * 4, cudaMemcpyDefault, s));
+    if (visible_vertices && nvv)
+        CK(cudaMemcpyAsync(visible_vertices, res->visible_vertices, nvv * 4, cudaMemcpyDefault, s));
+    if (vertex_uv && nvv) CK(cudaMemcpyAsync(vertex_uv, res->vertex_uv, nvv * 8, cudaMemcpyDefault, s));
     if (placements && C) CK(cudaMemcpyAsync(placements, res->placements, C * 64, cudaMemcpyDefault, s));
     return FA_OK;
 }

@@ -507,6 +507,71 @@ void fa_launch_canon_apply(const unsigned char* flags, int* label, const int* tm
     fa_launch(k_canon_apply, uf_grid(T), 256, 0, s, flags, label, tmp, T);
 }
 
+// ---- visible vertices (the compact UV wire format) --------------------------
+// A vertex is visible when a visible triangle touches it (vmin[v] != INT_MAX).
+// Ordered compaction: vslot[v] = its index in the list, vlist[slot] = its id
+// in the caller's numbering.  k_uv then writes one UV pair per visible vertex
+// (every triangle of the vertex's chart computes the same value).
+#define VTX_ITEMS 4
+#define VTX_TILE (CMP_THREADS * VTX_ITEMS)
+__global__ void __launch_bounds__(CMP_THREADS) k_vert_count(const int* __restrict__ vmin, int V,
+                                                            int* __restrict__ blocks) {
+    FA_PDL_PROLOGUE();
+    __shared__ int sm[32];
+    const int base = blockIdx.x * VTX_TILE + threadIdx.x * VTX_ITEMS;
+    int c = 0;
+#pragma unroll
+    for (int i = 0; i < VTX_ITEMS; i++) c += (base + i < V && vmin[base + i] != 0x7fffffff);
+    c = warp_sum(c);
+    if (lane_id() == 0) sm[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int s = 0;
+        for (int i = 0; i < CMP_THREADS / 32; i++) s += sm[i];
+        blocks[blockIdx.x] = s;
+    }
+}
+
+__global__ void __launch_bounds__(CMP_THREADS) k_vert_scatter(const int* __restrict__ vmin, int V,
+                                                              const int* __restrict__ blocks, int nblocks,
+                                                              const int* __restrict__ vperm, int* __restrict__ vslot,
+                                                              int* __restrict__ vlist, fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
+    __shared__ int sm[32];
+    const int offset = block_prefix_of(blocks, blockIdx.x, sm);
+    const int base = blockIdx.x * VTX_TILE + threadIdx.x * VTX_ITEMS;
+    bool vis[VTX_ITEMS];
+    int c = 0;
+#pragma unroll
+    for (int i = 0; i < VTX_ITEMS; i++) {
+        vis[i] = base + i < V && vmin[base + i] != 0x7fffffff;
+        c += vis[i];
+    }
+    int total;
+    int pos = offset + block_exclusive_scan(c, sm, &total);
+#pragma unroll
+    for (int i = 0; i < VTX_ITEMS; i++) {
+        if (base + i < V) vslot[base + i] = vis[i] ? pos : -1;
+        if (vis[i]) {
+            vlist[pos] = vperm ? vperm[base + i] : base + i;
+            pos++;
+        }
+    }
+    if (blockIdx.x == nblocks - 1 && threadIdx.x == 0) st->n_vis_vertices = offset + total;
+}
+
+int fa_vertex_blocks(long long V) {
+    long long b = (V + VTX_TILE - 1) / VTX_TILE;
+    return b > 0 ? (int)b : 1;
+}
+
+void fa_launch_visible_vertices(const int* vmin, int V, const int* vperm, int* blocks, int* vslot, int* vlist,
+                                fa_dstat* st, cudaStream_t s) {
+    const int nb = fa_vertex_blocks(V);
+    fa_launch(k_vert_count, nb, CMP_THREADS, 0, s, vmin, V, blocks);
+    fa_launch(k_vert_scatter, nb, CMP_THREADS, 0, s, vmin, V, blocks, nb, vperm, vslot, vlist, st);
+}
+
 void fa_launch_v2c(const int* vmin, const int* label, int* v2c, int V, cudaStream_t s, const int* vperm) {
     fa_launch(k_v2c, fa_grid(V, 256, FA_NUM_SMS * 8), 256, 0, s, vmin, label, v2c, V, vperm);
 }

@@ -53,10 +53,12 @@ struct fa_dstat {
     unsigned int done;    // pack batch early-exit
     int stretch_valid;    // triangles that entered the stretch sums
     int n_tiles_clip;     // tiles of clipped (generic) setups, stored downward from max_tiles - 1
+    int n_vis_vertices;   // vertices touched by a visible triangle (compact UV format)
+    int pad_v;
     double stretch_wsum;  // sum area * (S1^2 + S2^2) / 2   (metrics.py:103)
     double stretch_area;  // sum area                       (metrics.py:104)
     unsigned long long stretch_linf_bits;  // max S1 (positive double bits)
-    int pad0[38];
+    int pad0[36];
     int n_small3;         // stored small-triangle records (pass 2 input)
     int pad1[63];
     int n_large3;         // compact large-triangle records (stored from the back of the record array)

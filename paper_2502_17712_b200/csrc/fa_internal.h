@@ -57,6 +57,7 @@ struct fa_ctx {
     fa_buf vis_cidx;        // chart index of each visible triangle (written by k_chart_bounds, read by k_uv)
     fa_buf plc_c;           // placements by chart index (2 x int4 each; written by k_select, read by k_uv)
     fa_buf vis_tris;        // (a, b, c, t) of each visible triangle (written by the compaction)
+    fa_buf vslot, vlist, vuv, vblocks;  // visible vertices: slot per vertex, caller ids, f32 UV pairs, block counts
     size_t gen = 0;
     int max_large = 0, max_tiles = 0;
     int pack_batch = 0;  // candidates per pack launch
@@ -133,6 +134,11 @@ void fa_launch_build_adjacency(const int* tris, int T, unsigned long long* keys,
 void fa_launch_uf_compress(const int* vis_list, int* label, int T, const fa_dstat* st, cudaStream_t s);
 void fa_launch_canonicalize(const int* vis_list, int* label, int* tmp, int T, const fa_dstat* st, cudaStream_t s);
 void fa_launch_v2c(const int* vmin, const int* label, int* v2c, int V, cudaStream_t s, const int* vperm = nullptr);
+// visible vertices: vslot (V,) slot or -1, vlist (n,) caller ids, st->n_vis_vertices;
+// blocks holds fa_vertex_blocks(V) ints
+int fa_vertex_blocks(long long V);
+void fa_launch_visible_vertices(const int* vmin, int V, const int* vperm, int* blocks, int* vslot, int* vlist,
+                                fa_dstat* st, cudaStream_t s);
 // out[v] = pos[vperm[v]] (3 doubles each)
 void fa_launch_permute_pos(const double* pos, const int* vperm, double* out, int V, cudaStream_t s);
 void fa_launch_flags_from_labels(const int* labels, unsigned char* flags, int T, cudaStream_t s);
@@ -198,7 +204,8 @@ void fa_launch_fold(const long long* w, int n, long long omega, long long* rows,
 void fa_launch_uv(const double4* clip, const int* tris, const int* vis_list, const int* label, const int* cidx,
                   const int* pinv, const double* ndc, const int* px, const long long* placements, int T, int W, int H,
                   long long pad, bool f64, void* uv, int* vis_chart, const int* vis_cidx, const int4* plc_c,
-                  fa_dstat* st, cudaStream_t s, const int4* vis_tris = nullptr);
+                  fa_dstat* st, cudaStream_t s, const int4* vis_tris = nullptr, const int* vslot = nullptr,
+                  float2* vuv = nullptr);
 
 // ---- comparison packers (fa_baselines.cu) -----------------------------------
 void fa_launch_seq_search(const long long* ow, const long long* oh, int n, long long omega, long long n_scales,

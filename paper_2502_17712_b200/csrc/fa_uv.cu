@@ -41,6 +41,7 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
                                                    long long pad, OutT* __restrict__ uv,
                                                    int* __restrict__ vis_chart, const int* __restrict__ vis_cidx,
                                                    const int4* __restrict__ plc_c, const int4* __restrict__ vis_tris,
+                                                   const int* __restrict__ vslot, float2* __restrict__ vuv,
                                                    fa_dstat* __restrict__ st) {
     FA_PDL_PROLOGUE();
     __shared__ __align__(16) OutT stage[UV_THREADS * 6];
@@ -71,6 +72,15 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
                 v[i] = ldg4(clip + (vis_tris ? (i == 0 ? vq.x : (i == 1 ? vq.y : vq.z)) : __ldg(tris + 3 * t + i)));
                 if (v[i].w <= FA_W_EPSILON) behind = true;
             }
+            if (behind && vuv) {
+                // a vertex at or behind the camera plane makes every row it is
+                // in NaN (cli.py:433-435): its compact UV is NaN
+                const float qn = __int_as_float(0x7fc00000);
+#pragma unroll
+                for (int i = 0; i < 3; i++)
+                    if (v[i].w <= FA_W_EPSILON)
+                        vuv[vslot[i == 0 ? vq.x : (i == 1 ? vq.y : vq.z)]] = make_float2(qn, qn);
+            }
             if (!behind) {
                 long long px_, py_, pw_, ph_;
                 bool rot;
@@ -99,6 +109,15 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
                     out[2 * i + 1] = __dadd_rn(by, __dmul_rn(rot ? u : vv, ry));
                     scr[2 * i] = __dmul_rn(__dmul_rn(__dadd_rn(nx, 1.0), 0.5), (double)W);      // cli.py:437-439
                     scr[2 * i + 1] = __dmul_rn(__dmul_rn(__dadd_rn(ny, 1.0), 0.5), (double)H);
+                }
+                if (vuv) {
+                    // compact format: one f32 pair per visible vertex (all of a
+                    // vertex's triangles are in its chart and compute this value)
+#pragma unroll
+                    for (int i = 0; i < 3; i++) {
+                        const int vtx = i == 0 ? vq.x : (i == 1 ? vq.y : vq.z);
+                        vuv[vslot[vtx]] = make_float2((float)out[2 * i], (float)out[2 * i + 1]);
+                    }
                 }
                 double wt, ar, big;
                 if (tri_stretch(scr, out, wt, ar, big)) {
@@ -159,12 +178,13 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
 void fa_launch_uv(const double4* clip, const int* tris, const int* vis_list, const int* label, const int* cidx,
                   const int* pinv, const double* ndc, const int* px, const long long* placements, int T, int W, int H,
                   long long pad, bool f64, void* uv, int* vis_chart, const int* vis_cidx, const int4* plc_c,
-                  fa_dstat* st, cudaStream_t s, const int4* vis_tris) {
+                  fa_dstat* st, cudaStream_t s, const int4* vis_tris, const int* vslot, float2* vuv) {
+    if (!vis_tris) vuv = nullptr;  // the compact UVs index vertices through vis_tris
     int grid = fa_grid(T, UV_THREADS, FA_NUM_SMS * 8);
     if (f64)
         fa_launch(k_uv<double>, grid, UV_THREADS, 0, s, clip, tris, vis_list, label, cidx, pinv, ndc, px, placements, W, H,
-                                                 pad, (double*)uv, vis_chart, vis_cidx, plc_c, vis_tris, st);
+                                                 pad, (double*)uv, vis_chart, vis_cidx, plc_c, vis_tris, vslot, vuv, st);
     else
         fa_launch(k_uv<float>, grid, UV_THREADS, 0, s, clip, tris, vis_list, label, cidx, pinv, ndc, px, placements, W, H,
-                                                pad, (float*)uv, vis_chart, vis_cidx, plc_c, vis_tris, st);
+                                                pad, (float*)uv, vis_chart, vis_cidx, plc_c, vis_tris, vslot, vuv, st);
 }

@@ -219,20 +219,42 @@ class HostFrame:
     Chart ids arrive sparse by default (`visible_chart`: the chart of each
     visible triangle; every other triangle's chart is -1, charts.py:136-141);
     `chart_of_triangle` rebuilds the dense (T,) int32 array on first access
-    (or is the downloaded dense array when the pipeline asked for it)."""
+    (or is the downloaded dense array when the pipeline asked for it).
+
+    UVs arrive per visible vertex by default (`visible_vertices`,
+    `vertex_uv`: float32 pairs, NaN at/behind the camera plane): a vertex's
+    UV depends on the vertex and its chart only (cli.py:436-449), so `uv`
+    rebuilds the (n_visible, 6) float32 rows on first access -- NaN rows
+    where any corner is NaN -- bit-identical to the frame's float32 rows (or
+    is the downloaded rows when the pipeline asked for "uv")."""
 
     __slots__ = ("index", "status", "error", "n_visible", "n_charts", "scale", "screen_fragments",
-                 "texels_allocated", "_cot", "_T", "visible", "visible_chart", "uv", "placements")
+                 "texels_allocated", "_cot", "_T", "visible", "visible_chart", "_uv", "_uv_copied", "placements",
+                 "visible_vertices", "vertex_uv", "_tris", "_V")
 
-    def __init__(self, index: int, n_triangles: int = 0):
+    def __init__(self, index: int, n_triangles: int = 0, triangles=None, n_vertices: int = 0):
         self.index = index
         self.status = 0
         self.error = None
         self.n_visible = self.n_charts = 0
         self.scale = None
         self.screen_fragments = self.texels_allocated = 0
-        self._cot = self.visible = self.visible_chart = self.uv = self.placements = None
+        self._cot = self.visible = self.visible_chart = self._uv = self.placements = None
+        self.visible_vertices = self.vertex_uv = None
+        self._uv_copied = False
         self._T = n_triangles
+        self._tris = triangles
+        self._V = n_vertices
+
+    @property
+    def uv(self):
+        if self._uv is None and self.vertex_uv is not None and self.visible is not None:
+            full = np.full((self._V, 2), np.nan, dtype=np.float32)
+            full[self.visible_vertices] = self.vertex_uv
+            rows = full[self._tris[self.visible]].reshape(-1, 6)
+            rows[np.isnan(rows).any(axis=1)] = np.nan
+            self._uv = rows
+        return self._uv
 
     @property
     def chart_of_triangle(self):
@@ -245,7 +267,8 @@ class HostFrame:
     def d2h_bytes(self) -> int:
         """Bytes copied device -> host for this view (a rebuilt dense chart
         array is host work, not a copy)."""
-        arrs = (self.visible, self.visible_chart, self.uv, self.placements)
+        arrs = (self.visible, self.visible_chart, self._uv if self._uv_copied else None, self.placements,
+                self.visible_vertices, self.vertex_uv)
         n = sum(a.nbytes for a in arrs if a is not None)
         if self._cot is not None and self.visible_chart is None:
             n += self._cot.nbytes
@@ -262,7 +285,7 @@ class FramePipeline:
     `on_frame(HostFrame)`."""
 
     def __init__(self, mesh: Mesh, device: int | None = None, settings: FrameSettings | None = None,
-                 depth: int = 4, outputs: tuple = ("visible", "visible_chart", "uv", "placements"),
+                 depth: int = 4, outputs: tuple = ("visible", "visible_chart", "vertex_uv", "placements"),
                  mesh_replicas: bool = False):
         torch = nat.require_device()
         if depth < 1:
@@ -283,12 +306,18 @@ class FramePipeline:
                 h["visible"] = torch.empty(T, dtype=torch.int32).pin_memory()
             if "visible_chart" in outputs:
                 h["visible_chart"] = torch.empty(T, dtype=torch.int32).pin_memory()
-            if "uv" in outputs:
+            if "uv" in outputs or ("vertex_uv" in outputs and self.settings.uv_f64):
+                # (float64 UVs have no compact form: the rows are downloaded)
                 h["uv"] = torch.empty((T, 6), dtype=uv_dt).pin_memory()
+            elif "vertex_uv" in outputs:
+                h["visible_vertices"] = torch.empty(mesh.n_vertices, dtype=torch.int32).pin_memory()
+                h["vertex_uv"] = torch.empty((mesh.n_vertices, 2), dtype=torch.float32).pin_memory()
             if "placements" in outputs:
                 h["placements"] = torch.empty((T + 1, 8), dtype=torch.int64).pin_memory()
             self._host.append(h)
         self._np = [{k: t.numpy() for k, t in h.items()} for h in self._host]
+        self._tris = np.asarray(mesh.triangles)
+        self._V = mesh.n_vertices
 
     @property
     def depth(self) -> int:
@@ -300,7 +329,7 @@ class FramePipeline:
         eng, st = self.engines[slot], self.streams[slot]
         L, h_ctx, res = eng.ctx.L, eng.ctx.h, eng._res
         sp = ctypes.c_void_p(st.cuda_stream)
-        hf = HostFrame(index, self.engines[slot].n_triangles)
+        hf = HostFrame(index, self.engines[slot].n_triangles, self._tris, self._V)
         for _ in range(4):
             code = L.fa_frame_finish(h_ctx, ctypes.byref(res), sp)
             if code == nat.FA_INTERNAL_ERROR and "rerun" in nat.last_error():
@@ -324,8 +353,15 @@ class FramePipeline:
         h = self._host[slot]
         ptr = {k: ctypes.c_void_p(t.data_ptr()) if k in h else None
                for k, t in ((k, h.get(k)) for k in ("chart_of_triangle", "visible", "visible_chart", "uv",
-                                                     "placements"))}
-        if ptr["chart_of_triangle"] is not None:
+                                                     "placements", "visible_vertices", "vertex_uv"))}
+        if ptr["vertex_uv"] is not None:
+            nat.raise_for_status(L.fa_frame_download_compact(h_ctx, ctypes.byref(res), ptr["visible"],
+                                                             ptr["visible_chart"], ptr["visible_vertices"],
+                                                             ptr["vertex_uv"], ptr["placements"], sp))
+            if ptr["chart_of_triangle"] is not None:
+                nat.raise_for_status(L.fa_frame_download(h_ctx, ctypes.byref(res), ptr["chart_of_triangle"],
+                                                         None, None, None, sp))
+        elif ptr["chart_of_triangle"] is not None:
             nat.raise_for_status(L.fa_frame_download(h_ctx, ctypes.byref(res), ptr["chart_of_triangle"],
                                                      ptr["visible"], ptr["uv"], ptr["placements"], sp))
         elif any(p is not None for p in ptr.values()):
@@ -339,7 +375,12 @@ class FramePipeline:
         if "visible" in h:
             hf.visible = self._np[slot]["visible"][:nv]
         if "uv" in h:
-            hf.uv = self._np[slot]["uv"][:nv]
+            hf._uv = self._np[slot]["uv"][:nv]
+            hf._uv_copied = True
+        if "vertex_uv" in h:
+            nvv = int(res.n_visible_vertices)
+            hf.visible_vertices = self._np[slot]["visible_vertices"][:nvv]
+            hf.vertex_uv = self._np[slot]["vertex_uv"][:nvv]
         if "placements" in h:
             hf.placements = self._np[slot]["placements"][:C]
         return hf

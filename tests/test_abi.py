@@ -45,7 +45,7 @@ def test_struct_layouts_match_header():
     # fa_frame_params: 2 int, 4 int64, double, 5 int (+4 pad) -> 8 + 32 + 8 + 20 + 4 = 72
     assert ctypes.sizeof(_native.FrameParams) == 72
     # fa_frame_result: int + 2 int32 (+pad to 8) + 4 int64 + 2 double + int64 + 11 pointers
-    assert ctypes.sizeof(_native.FrameResult) == 16 + 4 * 8 + 3 * 8 + 12 * 8
+    assert ctypes.sizeof(_native.FrameResult) == 16 + 5 * 8 + 3 * 8 + 14 * 8
 
 
 def test_create_without_gpu_fails_loudly(lib):
