@@ -84,3 +84,43 @@ def test_pipeline_reports_failures_in_order():
     assert isinstance(got[1][1], fa.NothingVisible)
     assert got[1][2] is None
     assert np.array_equal(got[0][2], got[2][2])
+
+
+def test_compact_uv_rows_match_engine_rows():
+    """The compact download (f32 UV per visible vertex) rebuilds the engine's
+    f32 rows bit for bit, NaN rows of triangles with a corner at/behind the
+    camera plane (cli.py:433-435) included: a grid through the camera plane."""
+    rng = np.random.default_rng(3)
+    # a background grid plus long triangles reaching from in front of the
+    # camera to behind it (third corner at z = +1: w < 0)
+    nx = 20
+    gx, gz = np.meshgrid(np.linspace(-4.0, 4.0, nx + 1), np.linspace(-9.0, -5.0, 5))
+    grid = np.stack([gx.ravel(), gz.ravel() * 0.0 - 1.0 + 0.05 * gz.ravel(), gz.ravel()], 1)
+    tris = []
+    for j in range(4):
+        for i in range(nx):
+            a = j * (nx + 1) + i
+            tris += [(a, a + nx + 2, a + 1), (a, a + nx + 1, a + nx + 2)]
+    pos = [grid]
+    base = len(grid)
+    for k in range(6):
+        x0 = -1.5 + 0.6 * k + rng.uniform(-0.05, 0.05)
+        pos.append(np.array([[x0, -0.4, -3.0], [x0 + 0.5, -0.4, -3.0], [x0 + 0.25, -0.6, 1.0]]))
+        tris.append((base, base + 1, base + 2))
+        base += 3
+    pos = np.vstack(pos)
+    tris = np.asarray(tris, np.int32)
+    mesh = fa.Mesh(pos, tris)
+    cam = fa.CameraFrame.from_params(math.radians(70.0), 1.5, 0.1, 50.0, position=(0.0, 0.0, 0.0),
+                                     look_at=(0.0, -0.2, -1.0))
+    settings = FrameSettings(screen=(240, 160), omega=512, backface_cull=False)
+    o = FrameEngine(mesh, settings=settings).run(cam.view_proj)
+    want = o.uv.cpu().numpy()
+    assert np.isnan(want).any(), "the scene must have rows with a corner behind the camera"
+    got = []
+    FramePipeline(mesh, settings=settings, depth=2).run([cam.view_proj] * 3,
+                                                        lambda hf: got.append(hf.uv.copy()))
+    assert len(got) == 3
+    for g in got:
+        assert g.dtype == np.float32 and g.shape == want.shape
+        assert np.array_equal(g.view(np.uint32), want.view(np.uint32))
