@@ -741,20 +741,27 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     // pixel-winner buffer: triangle ids must fit the low FA_WID_BITS (24) bits
     unsigned long long* wid = T < (1 << 24) ? P<unsigned long long>(ctx->wid) : nullptr;
     mark();  // 0: start
-    fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), P<double4>(ctx->scr), W, H,
-                         P<int>(ctx->vmin), P<unsigned long long>(ctx->depth_keys), wid, (long long)W * H, flags, T,
-                         s);
-    nl += 1;
-    mark();  // 1: project + clears
+    // The depth/winner clears (33 MB at C2, HBM-bound) run on the side
+    // stream beside the projection and the setup, which never touch them.
     int r = ensure_side(ctx);
     if (r) return r;
+    CK(cudaEventRecord(ctx->fj[9], s));
+    CK(cudaStreamWaitEvent(ctx->side, ctx->fj[9], 0));
+    fa_launch_frame_init(nullptr, 0, nullptr, nullptr, nullptr, W, H, nullptr, P<unsigned long long>(ctx->depth_keys), wid,
+                         (long long)W * H, nullptr, T, ctx->side,
+                         fa_env_int("FASTATLAS_CLEAR_BLOCKS", FA_NUM_SMS));  // a slice of the GPU: the setup keeps the rest
+    CK(cudaEventRecord(ctx->fj[10], ctx->side));
+    fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), P<double4>(ctx->scr), W, H,
+                         P<int>(ctx->vmin), nullptr, nullptr, 0, flags, T, s);
+    nl += 2;
+    mark();  // 1: project + clears
     nl += fa_launch_depth_pass(true, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, W, H,
                                p->backface_cull, P<unsigned long long>(ctx->depth_keys), wid,
                                P<SmallRec>(ctx->small_rec), P<int>(ctx->clip_list), P<TriSetup>(ctx->large),
                                ctx->max_large, P<int4>(ctx->tiles), ctx->max_tiles, st, s,
                                fa_env_int("FASTATLAS_DEPTH_BRANCHES", 3) >= 2 ? ctx->side : nullptr,
                                fa_env_int("FASTATLAS_DEPTH_BRANCHES", 3) >= 3 ? ctx->side2 : nullptr,
-                               ctx->fj[0], ctx->fj[1], ctx->fj[7]);
+                               ctx->fj[0], ctx->fj[1], ctx->fj[7], ctx->fj[10]);
     fa_launch_depth_hiz(P<unsigned long long>(ctx->depth_keys), wid, W, H, P<unsigned long long>(ctx->hiz), flags, st,
                         s);
     nl += 1;

@@ -90,14 +90,14 @@ bool fa_ensure(fa_ctx* ctx, fa_buf& b, size_t bytes);
 // wid (may be null): pass-1 winner buffer, cleared to all ones with depth
 void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* clip, double4* scr, int W, int H,
                           int* vmin, unsigned long long* depth, unsigned long long* wid, long long npx,
-                          unsigned char* flags, int T, cudaStream_t s);
+                          unsigned char* flags, int T, cudaStream_t s, int max_blocks = 0);
 // side == nullptr: everything on s; otherwise fork/join through the events.
 // Both return the number of kernels launched.  wid: see depth_min (may be null).
 int fa_launch_depth_pass(bool write_depth, const double4* clip, const double4* scr, const int* tris, int T, int W,
                          int H, int cull, unsigned long long* depth, unsigned long long* wid, SmallRec* small_rec,
                          int* clip_list, TriSetup* large, int max_large, int4* tiles, int max_tiles, fa_dstat* st,
                          cudaStream_t s, cudaStream_t side, cudaStream_t side2, cudaEvent_t ev_fork,
-                         cudaEvent_t ev_join, cudaEvent_t ev_join2);
+                         cudaEvent_t ev_join, cudaEvent_t ev_join2, cudaEvent_t ev_clear = nullptr);
 int fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const int4* tiles, int max_tiles,
                          int max_large, int T, int W, const unsigned long long* depth, const unsigned long long* hiz,
                          unsigned char* flags, int* vis_queue, fa_dstat* st, cudaStream_t s, cudaStream_t side,

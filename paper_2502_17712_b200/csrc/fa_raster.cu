@@ -72,7 +72,7 @@ __global__ void k_frame_init(const double* __restrict__ pos, int V, const double
     long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     double m[16];
 #pragma unroll
-    for (int i = 0; i < 16; i++) m[i] = __ldg(vp_dev + i);
+    for (int i = 0; i < 16; i++) m[i] = V > 0 ? __ldg(vp_dev + i) : 0.0;  // (clear-only launches pass no matrix)
     for (long long v = i0; v < V; v += stride) {
         double x = pos[3 * v], y = pos[3 * v + 1], z = pos[3 * v + 2];
         double4 c = project_point(x, y, z, m);
@@ -840,12 +840,12 @@ __global__ void __launch_bounds__(256) k_raster_vis_tiles(const SmallRec* __rest
 // ---- host launchers -------------------------------------------------------
 void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* clip, double4* scr, int W, int H,
                           int* vmin, unsigned long long* depth, unsigned long long* wid, long long npx,
-                          unsigned char* flags, int T, cudaStream_t s) {
+                          unsigned char* flags, int T, cudaStream_t s, int max_blocks) {
     long long work = V;
     if (depth && npx / 2 > work) work = npx / 2;
     int nflag32 = flags ? (T + 3) / 4 : 0;
     if (nflag32 > work) work = nflag32;
-    fa_launch(k_frame_init, fa_grid(work, 256, FA_NUM_SMS * 8), 256, 0, s, 
+    fa_launch(k_frame_init, fa_grid(work, 256, max_blocks > 0 ? max_blocks : FA_NUM_SMS * 8), 256, 0, s, 
         pos, V, vp, clip, scr, W, H, vmin, depth, wid, npx, reinterpret_cast<unsigned int*>(flags), nflag32);
 }
 
@@ -864,9 +864,12 @@ int fa_launch_depth_pass(bool write_depth, const double4* clip, const double4* s
                          int H, int cull, unsigned long long* depth, unsigned long long* wid, SmallRec* small_rec,
                          int* clip_list, TriSetup* large, int max_large, int4* tiles, int max_tiles, fa_dstat* st,
                          cudaStream_t s, cudaStream_t side, cudaStream_t side2, cudaEvent_t ev_fork,
-                         cudaEvent_t ev_join, cudaEvent_t ev_join2) {
+                         cudaEvent_t ev_join, cudaEvent_t ev_join2, cudaEvent_t ev_clear) {
     fa_launch(k_raster_setup, fa_grid(T, 256, FA_NUM_SMS * 4), 256, 0, s, scr, tris, T, W, H, cull, small_rec,
               clip_list, tiles, max_tiles, st);
+    // the depth/winner clears ran beside the setup: every raster branch
+    // (forked from here) needs them
+    if (ev_clear) cudaStreamWaitEvent(s, ev_clear, 0);
     cudaStream_t b = side ? side : s;
     cudaStream_t b2 = side2 ? side2 : b;
     if (side) fork_to(s, side, ev_fork);
