@@ -1172,8 +1172,6 @@ int fa_sequential_scale_search(fa_ctx* ctx, const int64_t* target_w, const int64
                              FA_MAX_BOX_DIM, P<long long>(ctx->ow), P<long long>(ctx->oh), P<unsigned char>(ctx->orot),
                              P<int>(ctx->oidx), P<int>(ctx->pinv), P<unsigned long long>(ctx->sortk),
                              P<int>(ctx->sortv), 0, st, s);
-    int stride = (int)ctx->pack_cap;
-    (void)stride;
     fa_launch_seq_search(P<long long>(ctx->ow), P<long long>(ctx->oh), nn, omega, n_scales, min_dim, padding, batch,
                          P<int>(ctx->cand_w), P<int>(ctx->cand_h), P<int>(ctx->cand_p), P<int>(ctx->cand_y),
                          P<int>(ctx->rowstart), fa_front_in_smem(omega) ? nullptr : P<int>(ctx->okey),

@@ -266,12 +266,10 @@ __global__ void k_superblock_select(const long long* __restrict__ tw, const long
                                     long long* __restrict__ placements, long long* __restrict__ out) {
     FA_PDL_PROLOGUE();
     __shared__ int s_level;
-    __shared__ unsigned long long s_best;
     if (threadIdx.x == 0) {
         s_level = -1;
         for (int L = 0; L < n_levels; L++)
             if (level_ok[L]) { s_level = L; break; }
-        s_best = ~0ull;
         out[0] = s_level;
     }
     __syncthreads();
