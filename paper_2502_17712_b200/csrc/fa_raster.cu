@@ -120,7 +120,9 @@ __global__ void k_encode_depth(const double* __restrict__ in, unsigned long long
 //                       descriptors the warp writes together,
 //   anything else    -> index into `clip_list` for k_raster_clipped.
 // Nothing is rasterized here, so no lane waits on another's pixels.
+#ifndef SETUP_WARPS
 #define SETUP_WARPS 8
+#endif
 __global__ void __launch_bounds__(SETUP_WARPS * 32) k_raster_setup(const double4* __restrict__ scr,
                                                       const int* __restrict__ tris,
                                                       int T, int W, int H, int cull,
@@ -865,7 +867,7 @@ int fa_launch_depth_pass(bool write_depth, const double4* clip, const double4* s
                          int* clip_list, TriSetup* large, int max_large, int4* tiles, int max_tiles, fa_dstat* st,
                          cudaStream_t s, cudaStream_t side, cudaStream_t side2, cudaEvent_t ev_fork,
                          cudaEvent_t ev_join, cudaEvent_t ev_join2, cudaEvent_t ev_clear) {
-    fa_launch(k_raster_setup, fa_grid(T, 256, FA_NUM_SMS * 4), 256, 0, s, scr, tris, T, W, H, cull, small_rec,
+    fa_launch(k_raster_setup, fa_grid(T, SETUP_WARPS * 32, FA_NUM_SMS * (32 / SETUP_WARPS)), SETUP_WARPS * 32, 0, s, scr, tris, T, W, H, cull, small_rec,
               clip_list, tiles, max_tiles, st);
     // the depth/winner clears ran beside the setup: every raster branch
     // (forked from here) needs them
