@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define FA_ABI_VERSION 1
+#define FA_ABI_VERSION 2
 
 enum fa_status {
     FA_OK = 0,
@@ -165,6 +165,17 @@ int fa_superblock_pack(fa_ctx *ctx, const int64_t *target_w, const int64_t *targ
                        int64_t *placements_out, int64_t *scale_host, int64_t *block_used_host, void *stream);
 
 /* ---- whole frame: run_scene_pipeline (cli.py:360-406) -------------------- */
+
+/* fa_frame_params.packer: the packer registry of cli.py:318-339 (make_packer).
+ * FASTATLAS runs inside the frame's CUDA graph; the comparison packers run
+ * the frame without a graph, with one host synchronisation after the chart
+ * boxes (their box count sizes the launches).  Any other value fails with
+ * FA_VALUE_ERROR after the NothingVisible check, where the reference's
+ * make_packer raises InputError (cli.py:339, called at :386). */
+#define FA_PACKER_FASTATLAS 0   /* pack (packing.py:295-345) */
+#define FA_PACKER_SEQUENTIAL 1  /* sequential_scale_search (baselines.py:110-141) */
+#define FA_PACKER_SUPERBLOCK 2  /* superblock_pack (baselines.py:187-261); None -> FA_PACK_FAILURE (cli.py:333-335) */
+
 typedef struct fa_frame_params {
     int width, height;       /* SceneConfig.screen */
     int64_t omega;           /* SceneConfig.omega (power of two) */
@@ -177,6 +188,8 @@ typedef struct fa_frame_params {
     int want_depth;          /* 1: decode the depth buffer into float64 */
     int use_graph;           /* 1: replay a captured CUDA graph per shape */
     int profile;             /* 1: record CUDA events between stages (implies use_graph = 0) */
+    int packer;              /* FA_PACKER_* (run_scene_pipeline's `packer`, cli.py:360) */
+    int64_t block_size;      /* superblock block size; 0 = default_block_size(omega) (cli.py:313-314) */
 } fa_frame_params;
 
 typedef struct fa_frame_result {
@@ -204,7 +217,7 @@ typedef struct fa_frame_result {
     const int32_t *visible_chart;   /* (n_visible,) chart id of each visible triangle (sparse chart_of_triangle) */
     int64_t n_visible_vertices;     /* vertices touched by a visible triangle */
     const int32_t *visible_vertices; /* (n_visible_vertices,) their ids, ascending, caller's numbering */
-    const float *vertex_uv;         /* (n_visible_vertices,2) float32 UV of each (NaN: at/behind the camera plane) */
+    const float *vertex_uv;         /* (n_visible_vertices,2) float32 UV of each (NaN: at/behind the camera plane, or in no UV row) */
 } fa_frame_result;
 
 /* Enqueue a whole frame on `stream` (no host synchronisation). */

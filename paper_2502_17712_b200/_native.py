@@ -57,7 +57,12 @@ class FrameParams(ctypes.Structure):
         ("prescale", ctypes.c_double),
         ("backface_cull", ctypes.c_int), ("uv_f64", ctypes.c_int),
         ("want_depth", ctypes.c_int), ("use_graph", ctypes.c_int), ("profile", ctypes.c_int),
+        ("packer", ctypes.c_int), ("block_size", ctypes.c_int64),
     ]
+
+
+# fa_frame_params.packer (include/fastatlas.h): the make_packer registry, cli.py:318-339
+PACKER_CODES = {"fastatlas": 0, "sequential": 1, "superblock": 2}
 
 
 class FrameResult(ctypes.Structure):
@@ -248,9 +253,12 @@ class Context:
 
     def set_mesh(self, pos_t, tris_t):
         """Bind a mesh (fa_set_mesh keeps a renumbered device copy).  Re-binding
-        the same live tensors is free; a different or freed-and-reallocated
-        mesh (same pointers, new contents) is bound again."""
-        key = (pos_t.data_ptr(), tris_t.data_ptr(), pos_t.shape[0], tris_t.shape[0])
+        the same unmodified live tensors is free; a different mesh, a
+        freed-and-reallocated one (same pointers, new contents) or an in-place
+        update of the bound tensors (their torch version counter moved, e.g. a
+        deforming mesh) is bound again."""
+        key = (pos_t.data_ptr(), tris_t.data_ptr(), pos_t.shape[0], tris_t.shape[0], pos_t._version,
+               tris_t._version)
         prev = self._mesh_key
         if prev is None or prev[0] != key or prev[1]() is not pos_t or prev[2]() is not tris_t:
             raise_for_status(self.L.fa_set_mesh(self.h, ctypes.c_void_p(pos_t.data_ptr()), pos_t.shape[0],

@@ -213,14 +213,21 @@ def run_scene_pipeline(cfg: SceneConfig, packer: str = "fastatlas", mesh: Mesh |
                        engine: FrameEngine | None = None) -> SceneResult:
     """cli.py:360-406 on the GPU.  `mesh` skips OBJ parsing; `engine` reuses a
     resident FrameEngine (and its CUDA graph) across frames."""
-    if packer != "fastatlas":
-        make_packer(packer, cfg.n_scales, cfg.min_dim, cfg.padding)
     if mesh is None:
         mesh = engine.mesh if engine is not None else load_obj(cfg.mesh_path)
     cam = cfg.camera()
     if engine is None:
         engine = FrameEngine(mesh)
-    out = engine.run(cam.view_proj, cfg.frame_settings())
+    # the packer runs on the GPU inside the frame (fa_frame_params.packer):
+    # fastatlas in the frame's CUDA graph, sequential / superblock
+    # (baselines.py) after one synchronisation on the box count.  As in the
+    # reference, an unknown name fails only after the NothingVisible check.
+    try:
+        out = engine.run(cam.view_proj, cfg.frame_settings(packer=packer))
+    except ValueError:
+        if packer not in PACKER_NAMES:
+            raise InputError(f"unknown packer '{packer}' (choose from {', '.join(PACKER_NAMES)})") from None
+        raise
     return SceneResult(cfg, mesh, out, cam)
 
 

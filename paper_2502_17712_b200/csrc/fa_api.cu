@@ -11,6 +11,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -99,7 +100,7 @@ int fa_create(fa_ctx** out, int device) {
     c->max_tiles = 1 << 18;
     c->pack_batch = 148;
     if (cudaMallocHost(&c->hstat, sizeof(fa_dstat)) != cudaSuccess ||
-        cudaMallocHost(&c->hvp, 16 * sizeof(double)) != cudaSuccess) {
+        cudaMallocHost(&c->hvp, fa_ctx::kVpSlots * 16 * sizeof(double)) != cudaSuccess) {
         delete c;
         return set_err(FA_CUDA_ERROR, "cudaMallocHost failed");
     }
@@ -117,11 +118,13 @@ void fa_destroy(fa_ctx* c) {
                       &c->target, &c->survived, &c->okey, &c->oidx, &c->ow, &c->oh, &c->orot, &c->sortk, &c->sortv,
                       &c->pinv, &c->cand, &c->cand_p, &c->cand_w, &c->cand_h, &c->cand_y, &c->rowstart,
                       &c->placements, &c->uv, &c->vp_dev, &c->blocks, &c->dstat, &c->aux, &c->in_tw, &c->in_th,
-                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list, &c->hiz, &c->wid, &c->vis_chart, &c->vis_cidx, &c->plc_c, &c->pos_perm, &c->tris_perm, &c->vperm_buf, &c->vis_tris, &c->vslot, &c->vlist, &c->vuv, &c->vblocks};
+                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list, &c->hiz, &c->wid, &c->vis_chart, &c->vis_cidx, &c->plc_c, &c->pos_perm, &c->tris_perm, &c->vperm_buf, &c->vis_tris, &c->vslot, &c->vlist, &c->vuv, &c->vblocks, &c->pstat};
     for (fa_buf* b : bufs) free_buf(*b);
     for (cudaEvent_t e : c->fj)
         if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : c->ev)
+        if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->vp_ev)
         if (e) cudaEventDestroy(e);
     if (c->side) cudaStreamDestroy(c->side);
     if (c->side2) cudaStreamDestroy(c->side2);
@@ -137,48 +140,59 @@ int fa_set_mesh(fa_ctx* ctx, const double* positions, int64_t n_vertices, const 
         return set_err(FA_VALUE_ERROR, "mesh too large for 32-bit indices");
     if ((n_vertices > 0 && !positions) || (n_triangles > 0 && !triangles))
         return set_err(FA_VALUE_ERROR, "null mesh buffer");
-    ctx->pos = ctx->pos_user = positions;
-    ctx->tris = triangles;
+    // The context is rebound only once the new mesh is known to be valid: a
+    // failed call leaves no mesh bound (T = V = 0), never an invalid one.
+    ctx->pos = ctx->pos_user = nullptr;
+    ctx->tris = nullptr;
     ctx->vperm = nullptr;
+    ctx->V = ctx->T = 0;
+    ctx->gen++;  // any captured frame graph refers to the previous mesh
+    if (n_triangles > 0) {
+        // index range check (Mesh.__post_init__, charts.py:45-48) and the
+        // first use of every vertex, on the device; renumbering in order of
+        // first use (fa_mesh.cu) unless FASTATLAS_VERTEX_ORDER=0
+        CK(cudaSetDevice(ctx->device));
+        const bool renumber = fa_env_int("FASTATLAS_VERTEX_ORDER", 1) != 0;
+        fa_buf first, scratch;
+        const size_t vb = (size_t)(n_vertices > 0 ? n_vertices : 1) * 4;
+        bool ok = fa_ensure(ctx, first, vb) &&
+                  fa_ensure(ctx, scratch, (size_t)fa_mesh_scratch_ints(n_vertices, n_triangles) * 4 + vb + 16);
+        if (renumber && ok) {
+            ok = fa_ensure(ctx, ctx->tris_perm, (size_t)n_triangles * 12) &&
+                 fa_ensure(ctx, ctx->vperm_buf, vb) && fa_ensure(ctx, ctx->pos_perm, (size_t)n_vertices * 24 + 8);
+        }
+        if (!ok) {
+            free_buf(first);
+            free_buf(scratch);
+            return set_err(FA_CUDA_ERROR, "out of device memory binding the mesh");
+        }
+        cudaStream_t s = nullptr;
+        int* bad = P<int>(scratch);
+        fa_launch_mesh_validate(triangles, n_triangles, (int)n_vertices, P<int>(first), bad, s);
+        if (renumber)
+            fa_launch_mesh_renumber(positions, triangles, n_triangles, (int)n_vertices, P<int>(first), bad + 1,
+                                    P<int>(scratch) + 1 + fa_mesh_scratch_ints(n_vertices, n_triangles),
+                                    P<int>(ctx->tris_perm), P<int>(ctx->vperm_buf), P<double>(ctx->pos_perm), s);
+        int hbad = 0;
+        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaMemcpy(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost);
+        free_buf(first);
+        free_buf(scratch);
+        if (e != cudaSuccess) return set_err(FA_CUDA_ERROR, "fa_set_mesh: %s", cudaGetErrorString(e));
+        if (hbad) return set_err(FA_VALUE_ERROR, "triangle index out of range");
+        if (renumber) {
+            ctx->pos = P<double>(ctx->pos_perm);
+            ctx->tris = P<int>(ctx->tris_perm);
+            ctx->vperm = P<int>(ctx->vperm_buf);
+        }
+    }
+    if (!ctx->tris) {
+        ctx->pos = positions;
+        ctx->tris = triangles;
+    }
+    ctx->pos_user = positions;
     ctx->V = n_vertices;
     ctx->T = n_triangles;
-    if (n_vertices == 0 || n_triangles == 0 || fa_env_int("FASTATLAS_VERTEX_ORDER", 1) == 0) return FA_OK;
-    // Renumber vertices in order of first use by the triangle list (one-time,
-    // on the host): every per-vertex gather of the frame (screen records,
-    // clip coordinates, vertex minima) then touches ~45% fewer cache lines
-    // per warp at C2.  Triangle order -- and so every per-triangle result --
-    // is unchanged; per-vertex outputs are mapped back through vperm.
-    CK(cudaSetDevice(ctx->device));
-    const size_t nc = (size_t)n_triangles * 3;
-    std::vector<int32_t> th(nc);
-    CK(cudaMemcpy(th.data(), triangles, nc * 4, cudaMemcpyDeviceToHost));
-    std::vector<int32_t> newidx((size_t)n_vertices, -1), perm((size_t)n_vertices);
-    int32_t next = 0;
-    for (size_t c = 0; c < nc; c++) {
-        const int32_t v = th[c];
-        if (v < 0 || v >= n_vertices) return set_err(FA_VALUE_ERROR, "triangle index out of range");
-        if (newidx[v] < 0) {
-            newidx[v] = next;
-            perm[next++] = v;
-        }
-        th[c] = newidx[v];
-    }
-    for (int64_t v = 0; v < n_vertices; v++)
-        if (newidx[v] < 0) {
-            newidx[v] = next;
-            perm[next++] = (int32_t)v;
-        }
-    ENSURE(tris_perm, nc * 4);
-    ENSURE(vperm_buf, (size_t)n_vertices * 4);
-    ENSURE(pos_perm, (size_t)n_vertices * 24);
-    CK(cudaMemcpy(ctx->tris_perm.p, th.data(), nc * 4, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->vperm_buf.p, perm.data(), (size_t)n_vertices * 4, cudaMemcpyHostToDevice));
-    fa_launch_permute_pos(positions, P<int>(ctx->vperm_buf), P<double>(ctx->pos_perm), (int)n_vertices, 0);
-    CK(cudaStreamSynchronize(0));
-    CKL();
-    ctx->pos = P<double>(ctx->pos_perm);
-    ctx->tris = P<int>(ctx->tris_perm);
-    ctx->vperm = P<int>(ctx->vperm_buf);
     return FA_OK;
 }
 
@@ -331,9 +345,18 @@ static int read_stat(fa_ctx* ctx, cudaStream_t s) {
 }
 
 static int upload_vp(fa_ctx* ctx, const double* vp_host, cudaStream_t s) {
-    // pageable source: the copy is staged before the call returns, so the
-    // caller may reuse its matrix immediately
-    CK(cudaMemcpyAsync(ctx->vp_dev.p, vp_host, 16 * sizeof(double), cudaMemcpyHostToDevice, s));
+    // The 16 doubles are copied into a context-owned pinned slot before the
+    // call returns, so the caller may reuse or refill its matrix at once (a
+    // pinned caller buffer would otherwise be read asynchronously).  A slot
+    // is reused only after the copy that read it has executed.
+    const int k = ctx->vp_next;
+    ctx->vp_next = (k + 1) % fa_ctx::kVpSlots;
+    if (!ctx->vp_ev[k]) CK(cudaEventCreateWithFlags(&ctx->vp_ev[k], cudaEventDisableTiming));
+    else CK(cudaEventSynchronize(ctx->vp_ev[k]));
+    double* slot = ctx->hvp + 16 * k;
+    memcpy(slot, vp_host, 16 * sizeof(double));
+    CK(cudaMemcpyAsync(ctx->vp_dev.p, slot, 16 * sizeof(double), cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(ctx->vp_ev[k], s));
     return FA_OK;
 }
 
@@ -358,6 +381,120 @@ static int ensure_side(fa_ctx* ctx) {
     for (cudaEvent_t& e : ctx->fj)
         if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     return FA_OK;
+}
+
+// ---------------------------------------------------------------------------
+// comparison packers (shared by their entry points and the frame's packer
+// dispatch).  Boxes are device arrays, n >= 1; `stat` is the status block the
+// packer may clobber (the frame passes its own scratch, not the frame status).
+// ---------------------------------------------------------------------------
+static int seq_search_core(fa_ctx* ctx, const int64_t* target_w, const int64_t* target_h, const int64_t* chart_id,
+                           const int64_t* min_tri, int64_t n, int64_t omega, int64_t n_scales, int64_t min_dim,
+                           int64_t padding, int64_t* placements_out, int64_t* scale_host, fa_buf& stat,
+                           cudaStream_t s) {
+    int batch = (int)(n_scales < ctx->pack_batch ? n_scales : ctx->pack_batch);
+    int r = ensure_pack(ctx, n, n_scales, omega, batch);
+    if (r) return r;
+    ENSURE(aux, 64);
+    CK(cudaMemsetAsync(stat.p, 0, sizeof(fa_dstat), s));
+    CK(cudaMemsetAsync(ctx->cand.p, 0, (size_t)n_scales * FA_CAND_REC * 8, s));
+    fa_dstat* st = P<fa_dstat>(stat);
+    int nn = (int)n;
+    fa_launch_orient_sort_mt((const long long*)target_w, (const long long*)target_h, (const long long*)min_tri, nn,
+                             FA_MAX_BOX_DIM, P<long long>(ctx->ow), P<long long>(ctx->oh), P<unsigned char>(ctx->orot),
+                             P<int>(ctx->oidx), P<int>(ctx->pinv), P<unsigned long long>(ctx->sortk),
+                             P<int>(ctx->sortv), 0, st, s);
+    fa_launch_seq_search(P<long long>(ctx->ow), P<long long>(ctx->oh), nn, omega, n_scales, min_dim, padding, batch,
+                         P<int>(ctx->cand_w), P<int>(ctx->cand_h), P<int>(ctx->cand_p), P<int>(ctx->cand_y),
+                         P<int>(ctx->rowstart), fa_front_in_smem(omega) ? nullptr : P<int>(ctx->okey),
+                         P<long long>(ctx->cand), &st->done, s);
+    fa_launch_seq_select((const long long*)target_w, (const long long*)target_h, (const long long*)chart_id,
+                         P<unsigned char>(ctx->orot), P<int>(ctx->oidx), nn, n_scales, P<long long>(ctx->cand),
+                         P<int>(ctx->cand_w), P<int>(ctx->cand_h), P<int>(ctx->cand_p), P<int>(ctx->cand_y),
+                         (long long*)placements_out, P<long long>(ctx->aux), s);
+    CKL();
+    fa_dstat hs;
+    long long best = 0;
+    CK(cudaMemcpyAsync(&hs, stat.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&best, ctx->aux.p, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    r = status_from_flags(&hs);
+    if (r) return r;
+    if (best == 0) return set_err(FA_PACK_FAILURE, "every candidate scale was rejected");
+    if (scale_host) {
+        long long g = best, b = n_scales;
+        while (b) { long long t = g % b; g = b; b = t; }
+        scale_host[0] = best / g;
+        scale_host[1] = n_scales / g;
+    }
+    return FA_OK;
+}
+
+static int check_superblock(int64_t omega, int64_t block_size) {
+    int r = check_omega(omega);
+    if (r) return r;
+    if (block_size < 1 || (block_size & (block_size - 1)))
+        return set_err(FA_VALUE_ERROR, "block_size must be a power of two");
+    if (block_size > omega) return set_err(FA_VALUE_ERROR, "block_size must not exceed omega");
+    if (omega % block_size) return set_err(FA_VALUE_ERROR, "omega must be divisible by block_size");
+    return FA_OK;
+}
+
+static int superblock_core(fa_ctx* ctx, const int64_t* target_w, const int64_t* target_h, const int64_t* chart_id,
+                           const int64_t* min_tri, int64_t n, int64_t omega, int64_t block_size, int halving_enabled,
+                           int64_t* placements_out, int64_t* scale_host, int64_t* block_used_host, fa_buf& stat,
+                           cudaStream_t s) {
+    int n_levels = 1;
+    if (halving_enabled)
+        while ((block_size >> n_levels) >= 16) n_levels++;
+    int r = ensure_pack(ctx, n, 1, omega, 1);
+    if (r) return r;
+    CK(cudaMemsetAsync(stat.p, 0, sizeof(fa_dstat), s));
+    fa_dstat* st = P<fa_dstat>(stat);
+    int nn = (int)n;
+    fa_launch_orient_sort_mt((const long long*)target_w, (const long long*)target_h, (const long long*)min_tri, nn,
+                             FA_MAX_BOX_DIM, P<long long>(ctx->ow), P<long long>(ctx->oh), P<unsigned char>(ctx->orot),
+                             P<int>(ctx->oidx), P<int>(ctx->pinv), P<unsigned long long>(ctx->sortk),
+                             P<int>(ctx->sortv), 0, st, s);
+    // per level: used_h[nb] + nsh[nb] + 3 * nb * block shelf arrays (largest at the smallest block)
+    long long smallest = block_size >> (n_levels - 1);
+    long long nb_max = (omega / smallest) * (omega / smallest);
+    size_t state_stride = (size_t)(2 * nb_max + 3 * nb_max * smallest);
+    size_t out_stride = (size_t)4 * nn;
+    fa_buf state, xywh, lvl, out;
+    bool ok = fa_ensure(ctx, state, state_stride * n_levels * 4) && fa_ensure(ctx, xywh, out_stride * n_levels * 4) &&
+              fa_ensure(ctx, lvl, 64 * 4) && fa_ensure(ctx, out, 64);
+    if (ok) {
+        fa_launch_superblock(P<long long>(ctx->ow), P<long long>(ctx->oh), (const long long*)target_w,
+                             (const long long*)target_h, (const long long*)chart_id, P<unsigned char>(ctx->orot),
+                             P<int>(ctx->oidx), nn, omega, (int)block_size, n_levels, P<int>(state), state_stride,
+                             P<int>(xywh), out_stride, P<int>(lvl), (long long*)placements_out, P<long long>(out), s);
+        r = FA_OK;
+        cudaError_t e = cudaGetLastError();
+        long long res[3] = {-1, 1, 1};
+        fa_dstat hs;
+        if (e == cudaSuccess) e = cudaMemcpyAsync(res, out.p, sizeof(res), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&hs, stat.p, sizeof(hs), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) {
+            r = set_err(FA_CUDA_ERROR, "superblock: %s", cudaGetErrorString(e));
+        } else if ((r = status_from_flags(&hs)) != FA_OK) {
+        } else if (res[0] < 0) {
+            r = set_err(FA_PACK_FAILURE, "superblock allocation failed at the halving floor");
+        } else {
+            long long g = res[1], b = res[2];
+            while (b) { long long t = g % b; g = b; b = t; }
+            if (scale_host) { scale_host[0] = res[1] / g; scale_host[1] = res[2] / g; }
+            if (block_used_host) *block_used_host = block_size >> res[0];
+        }
+    } else {
+        r = set_err(FA_CUDA_ERROR, "out of device memory for superblock state");
+    }
+    free_buf(state);
+    free_buf(xywh);
+    free_buf(lvl);
+    free_buf(out);
+    return r;
 }
 
 extern "C" {
@@ -720,6 +857,73 @@ int fa_pack(fa_ctx* ctx, const int64_t* target_w, const int64_t* target_h, const
 // ---------------------------------------------------------------------------
 // whole frame
 // ---------------------------------------------------------------------------
+// The comparison packers of make_packer (cli.py:318-339) inside the frame.
+// Runs outside graph capture: the frame so far (boxes in in_tw / in_th /
+// in_cid, ascending roots) is synchronised once, the packer runs on the box
+// count it reads, and the frame status receives the layout's scale and
+// texel count.  k_uv then reads the placements in packing order through
+// pinv (written by the packer's own orient + order, packing.py:109-130).
+static int frame_external_pack(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s, int& nl) {
+    int r = read_stat(ctx, s);
+    if (r) return r;
+    fa_dstat* h = ctx->hstat;
+    int64_t n = h->n_charts;
+    // any earlier failure (or a box count beyond the scratch, which
+    // fa_frame_finish grows and reruns) is reported by fa_frame_finish; the
+    // pack-failure flag keeps k_uv from reading placements
+    if (h->flags || h->n_vis == 0 || n > ctx->pack_cap) {
+        h->flags |= FA_DFLAG_PACK_FAILURE;
+        CK(cudaMemcpyAsync(ctx->dstat.p, h, sizeof(fa_dstat), cudaMemcpyHostToDevice, s));
+        return FA_OK;
+    }
+    ENSURE(pstat, sizeof(fa_dstat));
+    const int64_t* tw = P<int64_t>(ctx->in_tw);
+    const int64_t* th = P<int64_t>(ctx->in_th);
+    const int64_t* cid = P<int64_t>(ctx->in_cid);
+    int64_t* plc = P<int64_t>(ctx->placements);
+    int64_t scale[2] = {1, 1};
+    if (p->packer == FA_PACKER_SEQUENTIAL) {
+        if (n > 0) {
+            if (p->n_scales < 1) r = set_err(FA_PACK_FAILURE, "every candidate scale was rejected");
+            else r = seq_search_core(ctx, tw, th, cid, cid, n, p->omega, p->n_scales, p->min_dim, p->padding, plc,
+                                     scale, ctx->pstat, s);
+            nl += 3;
+        }
+    } else if (p->packer == FA_PACKER_SUPERBLOCK) {
+        // SuperblockConfig(block_size or default_block_size(omega)), halving on (cli.py:331-333)
+        int64_t bs = p->block_size;
+        if (bs == 0) bs = std::max<int64_t>(16, std::min<int64_t>(p->omega, p->omega / 8));
+        r = check_superblock(p->omega, bs);
+        if (!r && n > 0) {
+            r = superblock_core(ctx, tw, th, cid, cid, n, p->omega, bs, 1, plc, scale, nullptr, ctx->pstat, s);
+            nl += 3;
+        }
+    } else {
+        return set_err(FA_VALUE_ERROR, "unknown packer '%d' (choose from fastatlas, sequential, superblock)",
+                       p->packer);
+    }
+    if (r == FA_PACK_FAILURE) {
+        h->flags |= FA_DFLAG_PACK_FAILURE;
+    } else if (r) {
+        return r;
+    } else {
+        // texels_allocated (cli.py:391-393) over the placements
+        std::vector<long long> hp((size_t)n * 8);
+        if (n) CK(cudaMemcpy(hp.data(), plc, (size_t)n * 64, cudaMemcpyDeviceToHost));
+        long long tex = 0;
+        for (int64_t j = 0; j < n; j++) {
+            long long cw = hp[8 * j + 3] - 2 * p->padding, ch = hp[8 * j + 4] - 2 * p->padding;
+            tex += (cw > 0 ? cw : 0) * (ch > 0 ? ch : 0);
+        }
+        h->scale_num = scale[0];
+        h->scale_den = scale[1];
+        h->texels_allocated = tex;
+        h->best = 1;
+    }
+    CK(cudaMemcpyAsync(ctx->dstat.p, h, sizeof(fa_dstat), cudaMemcpyHostToDevice, s));
+    return FA_OK;
+}
+
 static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s, int& nl) {
     int T = (int)ctx->T, V = (int)ctx->V, W = p->width, H = p->height;
     fa_dstat* st = P<fa_dstat>(ctx->dstat);
@@ -788,7 +992,7 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     CK(cudaEventRecord(ctx->fj[5], ctx->side));
     fa_launch_v2c(P<int>(ctx->vmin), P<int>(ctx->label), P<int>(ctx->v2c), V, ctx->side, ctx->vperm);
     fa_launch_visible_vertices(P<int>(ctx->vmin), V, ctx->vperm, P<int>(ctx->vblocks), P<int>(ctx->vslot),
-                               P<int>(ctx->vlist), st, ctx->side);
+                               P<int>(ctx->vlist), st, ctx->side, P<float2>(ctx->vuv));
     CK(cudaEventRecord(ctx->fj[6], ctx->side));
     nl += 4;
     fa_launch_compact_roots(P<int>(ctx->vis_list), P<int>(ctx->label), T, P<int>(ctx->blocks), P<int>(ctx->roots),
@@ -811,13 +1015,19 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     fa_launch_orient_sort(b, (int)n_cap, &st->n_charts, FA_MAX_BOX_DIM, st, s, &bd);
     nl += 1;
     mark();  // 8: orient + radix order
-    nl += fa_launch_pack(b, (int)n_cap, &st->n_charts, p->omega, p->n_scales, p->min_dim, p->padding, batch, st, s);
+    if (p->packer == FA_PACKER_FASTATLAS) {
+        nl += fa_launch_pack(b, (int)n_cap, &st->n_charts, p->omega, p->n_scales, p->min_dim, p->padding, batch, st, s);
+    } else {
+        r = frame_external_pack(ctx, p, s, nl);
+        if (r) return r;
+    }
     mark();  // 9: candidate pack + select
     CK(cudaStreamWaitEvent(s, ctx->fj[6], 0));  // vertex -> chart map and the visible-vertex slots
     fa_launch_uv(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->label), P<int>(ctx->cidx),
                  P<int>(ctx->pinv), P<double>(ctx->ndc), P<int>(ctx->px), P<long long>(ctx->placements), T, W, H,
                  p->padding, p->uv_f64 != 0, ctx->uv.p, P<int>(ctx->vis_chart), P<int>(ctx->vis_cidx),
-                 P<int4>(ctx->plc_c), st, s, P<int4>(ctx->vis_tris), P<int>(ctx->vslot), P<float2>(ctx->vuv));
+                 p->packer == FA_PACKER_FASTATLAS ? P<int4>(ctx->plc_c) : nullptr, st, s, P<int4>(ctx->vis_tris),
+                 P<int>(ctx->vslot), P<float2>(ctx->vuv));
     nl += 1;
     mark();  // 10: uv
     if (p->want_depth) {
@@ -870,7 +1080,7 @@ int fa_frame_launch(fa_ctx* ctx, const double* vp_host, const fa_frame_params* p
     ctx->last_params = *p;
     r = upload_vp(ctx, vp_host, s);
     if (r) return r;
-    if (!p->use_graph || p->profile) {
+    if (!p->use_graph || p->profile || p->packer != FA_PACKER_FASTATLAS) {
         fa_frame_params q = *p;
         q.use_graph = 0;
         p = &q;
@@ -1159,42 +1369,9 @@ int fa_sequential_scale_search(fa_ctx* ctx, const int64_t* target_w, const int64
         return FA_OK;
     }
     CK(cudaSetDevice(ctx->device));
-    int batch = (int)(n_scales < ctx->pack_batch ? n_scales : ctx->pack_batch);
-    r = ensure_pack(ctx, n, n_scales, omega, batch);
-    if (r) return r;
     ENSURE(dstat, sizeof(fa_dstat));
-    ENSURE(aux, 64);
-    CK(cudaMemsetAsync(ctx->dstat.p, 0, sizeof(fa_dstat), s));
-    CK(cudaMemsetAsync(ctx->cand.p, 0, (size_t)n_scales * FA_CAND_REC * 8, s));
-    fa_dstat* st = P<fa_dstat>(ctx->dstat);
-    int nn = (int)n;
-    fa_launch_orient_sort_mt((const long long*)target_w, (const long long*)target_h, (const long long*)min_tri, nn,
-                             FA_MAX_BOX_DIM, P<long long>(ctx->ow), P<long long>(ctx->oh), P<unsigned char>(ctx->orot),
-                             P<int>(ctx->oidx), P<int>(ctx->pinv), P<unsigned long long>(ctx->sortk),
-                             P<int>(ctx->sortv), 0, st, s);
-    fa_launch_seq_search(P<long long>(ctx->ow), P<long long>(ctx->oh), nn, omega, n_scales, min_dim, padding, batch,
-                         P<int>(ctx->cand_w), P<int>(ctx->cand_h), P<int>(ctx->cand_p), P<int>(ctx->cand_y),
-                         P<int>(ctx->rowstart), fa_front_in_smem(omega) ? nullptr : P<int>(ctx->okey),
-                         P<long long>(ctx->cand), &st->done, s);
-    fa_launch_seq_select((const long long*)target_w, (const long long*)target_h, (const long long*)chart_id,
-                         P<unsigned char>(ctx->orot), P<int>(ctx->oidx), nn, n_scales, P<long long>(ctx->cand),
-                         P<int>(ctx->cand_w), P<int>(ctx->cand_h), P<int>(ctx->cand_p), P<int>(ctx->cand_y),
-                         (long long*)placements_out, P<long long>(ctx->aux), s);
-    CKL();
-    r = read_stat(ctx, s);
-    if (r) return r;
-    r = status_from_flags(ctx->hstat);
-    if (r) return r;
-    long long best = 0;
-    CK(cudaMemcpy(&best, ctx->aux.p, 8, cudaMemcpyDeviceToHost));
-    if (best == 0) return set_err(FA_PACK_FAILURE, "every candidate scale was rejected");
-    if (scale_host) {
-        long long g = best, b = n_scales;
-        while (b) { long long t = g % b; g = b; b = t; }
-        scale_host[0] = best / g;
-        scale_host[1] = n_scales / g;
-    }
-    return FA_OK;
+    return seq_search_core(ctx, target_w, target_h, chart_id, min_tri, n, omega, n_scales, min_dim, padding,
+                           placements_out, scale_host, ctx->dstat, s);
 }
 
 int fa_sequential_pack(fa_ctx* ctx, const int64_t* widths, const int64_t* heights, int64_t n, int64_t omega,
@@ -1226,66 +1403,18 @@ int fa_superblock_pack(fa_ctx* ctx, const int64_t* target_w, const int64_t* targ
                        const int64_t* min_tri, int64_t n, int64_t omega, int64_t block_size, int halving_enabled,
                        int64_t* placements_out, int64_t* scale_host, int64_t* block_used_host, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    int r = check_omega(omega);
-    if (r) return r;
     if (!ctx || n < 0 || n >= (1ll << 30)) return set_err(FA_VALUE_ERROR, "bad arguments");
-    if (block_size < 1 || (block_size & (block_size - 1)))
-        return set_err(FA_VALUE_ERROR, "block_size must be a power of two");
-    if (block_size > omega) return set_err(FA_VALUE_ERROR, "block_size must not exceed omega");
-    if (omega % block_size) return set_err(FA_VALUE_ERROR, "omega must be divisible by block_size");
-    int n_levels = 1;
-    if (halving_enabled)
-        while ((block_size >> n_levels) >= 16) n_levels++;
+    int r = check_superblock(omega, block_size);
+    if (r) return r;
     if (n == 0) {
         if (scale_host) { scale_host[0] = 1; scale_host[1] = 1; }
         if (block_used_host) *block_used_host = block_size;
         return FA_OK;
     }
     CK(cudaSetDevice(ctx->device));
-    r = ensure_pack(ctx, n, 1, omega, 1);
-    if (r) return r;
     ENSURE(dstat, sizeof(fa_dstat));
-    CK(cudaMemsetAsync(ctx->dstat.p, 0, sizeof(fa_dstat), s));
-    fa_dstat* st = P<fa_dstat>(ctx->dstat);
-    int nn = (int)n;
-    fa_launch_orient_sort_mt((const long long*)target_w, (const long long*)target_h, (const long long*)min_tri, nn,
-                             FA_MAX_BOX_DIM, P<long long>(ctx->ow), P<long long>(ctx->oh), P<unsigned char>(ctx->orot),
-                             P<int>(ctx->oidx), P<int>(ctx->pinv), P<unsigned long long>(ctx->sortk),
-                             P<int>(ctx->sortv), 0, st, s);
-    // per level: used_h[nb] + nsh[nb] + 3 * nb * block shelf arrays (largest at the smallest block)
-    long long smallest = block_size >> (n_levels - 1);
-    long long nb_max = (omega / smallest) * (omega / smallest);
-    size_t state_stride = (size_t)(2 * nb_max + 3 * nb_max * smallest);
-    size_t out_stride = (size_t)4 * nn;
-    fa_buf state, xywh, lvl, out;
-    bool ok = fa_ensure(ctx, state, state_stride * n_levels * 4) && fa_ensure(ctx, xywh, out_stride * n_levels * 4) &&
-              fa_ensure(ctx, lvl, 64 * 4) && fa_ensure(ctx, out, 64);
-    if (ok) {
-        fa_launch_superblock(P<long long>(ctx->ow), P<long long>(ctx->oh), (const long long*)target_w,
-                             (const long long*)target_h, (const long long*)chart_id, P<unsigned char>(ctx->orot),
-                             P<int>(ctx->oidx), nn, omega, (int)block_size, n_levels, P<int>(state), state_stride,
-                             P<int>(xywh), out_stride, P<int>(lvl), (long long*)placements_out, P<long long>(out), s);
-        r = FA_OK;
-        cudaError_t e = cudaGetLastError();
-        long long res[3] = {-1, 1, 1};
-        if (e == cudaSuccess) e = cudaMemcpyAsync(res, out.p, sizeof(res), cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-        if (e != cudaSuccess) {
-            r = set_err(FA_CUDA_ERROR, "superblock: %s", cudaGetErrorString(e));
-        } else if (res[0] < 0) {
-            r = set_err(FA_PACK_FAILURE, "superblock allocation failed at the halving floor");
-        } else {
-            if (scale_host) { scale_host[0] = res[1]; scale_host[1] = res[2]; }
-            if (block_used_host) *block_used_host = block_size >> res[0];
-        }
-    } else {
-        r = set_err(FA_CUDA_ERROR, "out of device memory for superblock state");
-    }
-    free_buf(state);
-    free_buf(xywh);
-    free_buf(lvl);
-    free_buf(out);
-    return r;
+    return superblock_core(ctx, target_w, target_h, chart_id, min_tri, n, omega, block_size, halving_enabled,
+                           placements_out, scale_host, block_used_host, ctx->dstat, s);
 }
 
 int fa_orient(fa_ctx* ctx, const int64_t* target_w, const int64_t* target_h, int64_t n, int64_t* ow_out,

@@ -535,7 +535,8 @@ __global__ void __launch_bounds__(CMP_THREADS) k_vert_count(const int* __restric
 __global__ void __launch_bounds__(CMP_THREADS) k_vert_scatter(const int* __restrict__ vmin, int V,
                                                               const int* __restrict__ blocks, int nblocks,
                                                               const int* __restrict__ vperm, int* __restrict__ vslot,
-                                                              int* __restrict__ vlist, fa_dstat* __restrict__ st) {
+                                                              int* __restrict__ vlist, float2* __restrict__ vuv,
+                                                              fa_dstat* __restrict__ st) {
     FA_PDL_PROLOGUE();
     __shared__ int sm[32];
     const int offset = block_prefix_of(blocks, blockIdx.x, sm);
@@ -554,6 +555,10 @@ __global__ void __launch_bounds__(CMP_THREADS) k_vert_scatter(const int* __restr
         if (base + i < V) vslot[base + i] = vis[i] ? pos : -1;
         if (vis[i]) {
             vlist[pos] = vperm ? vperm[base + i] : base + i;
+            // NaN until k_uv writes it: a vertex in front of the camera whose
+            // visible triangles all reach behind it keeps NaN (its UV rows are
+            // NaN, cli.py:433-435), never stale data
+            if (vuv) vuv[pos] = make_float2(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
             pos++;
         }
     }
@@ -566,10 +571,10 @@ int fa_vertex_blocks(long long V) {
 }
 
 void fa_launch_visible_vertices(const int* vmin, int V, const int* vperm, int* blocks, int* vslot, int* vlist,
-                                fa_dstat* st, cudaStream_t s) {
+                                fa_dstat* st, cudaStream_t s, float2* vuv) {
     const int nb = fa_vertex_blocks(V);
     fa_launch(k_vert_count, nb, CMP_THREADS, 0, s, vmin, V, blocks);
-    fa_launch(k_vert_scatter, nb, CMP_THREADS, 0, s, vmin, V, blocks, nb, vperm, vslot, vlist, st);
+    fa_launch(k_vert_scatter, nb, CMP_THREADS, 0, s, vmin, V, blocks, nb, vperm, vslot, vlist, vuv, st);
 }
 
 void fa_launch_v2c(const int* vmin, const int* label, int* v2c, int V, cudaStream_t s, const int* vperm) {

@@ -50,6 +50,7 @@ struct fa_ctx {
     fa_buf roots, ndc_keys, ndc, px, target, survived, okey, oidx, ow, oh, orot, sortk, sortv, pinv;
     fa_buf cand, cand_p, cand_w, cand_h, cand_y, rowstart, placements, uv, vp_dev, blocks, dstat, aux;
     fa_buf in_tw, in_th, in_cid, in_mt;
+    fa_buf pstat;           // comparison packers' status block inside a frame (the frame keeps dstat)
     fa_buf scr, clip_list;  // per-vertex screen records; generic-path triangle list
     fa_buf hiz;             // 8x8 hierarchical-Z max keys of the final depth
     fa_buf wid;             // pass-1 pixel winners (truncated key | triangle id)
@@ -65,7 +66,12 @@ struct fa_ctx {
     bool needs_rerun = false;
 
     fa_dstat* hstat = nullptr;  // pinned mirror of the device status
-    double* hvp = nullptr;      // pinned camera staging
+    // pinned camera staging: a ring of 16-double slots, each reused only
+    // after the event recorded behind its upload has completed
+    static const int kVpSlots = 8;
+    double* hvp = nullptr;      // kVpSlots x 16 doubles
+    cudaEvent_t vp_ev[kVpSlots] = {};
+    int vp_next = 0;
     fa_frame_params last_params{};
     int last_launches = 0;
 
@@ -138,7 +144,7 @@ void fa_launch_v2c(const int* vmin, const int* label, int* v2c, int V, cudaStrea
 // blocks holds fa_vertex_blocks(V) ints
 int fa_vertex_blocks(long long V);
 void fa_launch_visible_vertices(const int* vmin, int V, const int* vperm, int* blocks, int* vslot, int* vlist,
-                                fa_dstat* st, cudaStream_t s);
+                                fa_dstat* st, cudaStream_t s, float2* vuv = nullptr);
 // out[v] = pos[vperm[v]] (3 doubles each)
 void fa_launch_permute_pos(const double* pos, const int* vperm, double* out, int V, cudaStream_t s);
 void fa_launch_flags_from_labels(const int* labels, unsigned char* flags, int T, cudaStream_t s);
@@ -147,6 +153,12 @@ void fa_launch_compact_roots(const int* vis_list, const int* label, int T, int* 
                              unsigned long long* ndc_keys, int* survived, fa_dstat* st, cudaStream_t s);
 void fa_launch_canon_apply(const unsigned char* flags, int* label, const int* tmp, int T, cudaStream_t s);
 void fa_launch_fill(int* a, int n, int v, cudaStream_t s);
+
+// ---- mesh binding (fa_mesh.cu) ----------------------------------------------
+int fa_mesh_scratch_ints(long long V, long long T);
+void fa_launch_mesh_validate(const int* tris, long long T, int V, int* first, int* bad, cudaStream_t s);
+void fa_launch_mesh_renumber(const double* pos, const int* tris, long long T, int V, const int* first, int* scratch,
+                             int* newidx, int* tris_out, int* perm, double* pos_out, cudaStream_t s);
 
 // ---- bounds (fa_bounds.cu) -----------------------------------------------
 void fa_launch_chart_bounds(const double4* clip, const int* tris, const int* vis_list, const int* label,

@@ -37,6 +37,8 @@ class FrameSettings:
     want_depth: bool = False
     use_graph: bool = True
     profile: bool = False
+    packer: str = "fastatlas"   # make_packer name (cli.py:318-339); the comparison packers run ungraphed
+    block_size: int = 0         # superblock block size, 0 = default_block_size(omega)
 
     def params(self) -> nat.FrameParams:
         p = nat.FrameParams()
@@ -49,6 +51,8 @@ class FrameSettings:
         p.want_depth = int(bool(self.want_depth))
         p.use_graph = int(bool(self.use_graph))
         p.profile = int(bool(self.profile))
+        p.packer = nat.PACKER_CODES.get(self.packer, -1)  # unknown: ValueError after the NothingVisible check
+        p.block_size = int(self.block_size)
         return p
 
 

@@ -313,7 +313,7 @@ def write_obj(path, pos, tris):
 
 
 def run_reference_frame(pos, tris, pose, screen, omega, prescale=1.0, n_scales=64, min_dim=1,
-                        padding=0, cull=True):
+                        padding=0, cull=True, packer="fastatlas"):
     """Run the reference run_scene_pipeline (cli.py:360-406) and capture its
     intermediate arrays and the UV pairs it hands to scene_stretch."""
     captured = {}
@@ -357,12 +357,14 @@ def run_reference_frame(pos, tris, pose, screen, omega, prescale=1.0, n_scales=6
                                     backface_cull=cull, prescale=prescale)
             t0 = time.perf_counter()
             try:
-                res = apcli.run_scene_pipeline(cfg)
+                res = apcli.run_scene_pipeline(cfg, packer=packer)
                 status = "ok"
             except ap.PackFailure:
                 res, status = None, "PackFailure"
             except apcli.NothingVisible:
                 res, status = None, "NothingVisible"
+            except ValueError:  # e.g. superblock's block_size > omega (baselines.py:211-214)
+                res, status = None, "ValueError"
             wall = time.perf_counter() - t0
             vp = cfg.camera().view_proj
     finally:
@@ -458,10 +460,53 @@ def gen_frames(out, with_c1=True):
     return meta
 
 
+def gen_frames_packers(out):
+    """run_scene_pipeline(cfg, packer=p) for the comparison packers
+    (cli.py:318-339,386-387): layouts, UV rows and stretch of mini frames and
+    C1, including a superblock PackFailure (omega 16) and a ValueError
+    (omega 8 < the default 16-texel block)."""
+    arrays, meta = {}, []
+    pos, tris = mini_scene()
+    poses = scenes.views_c5(8)
+    path = scenes.camera_path_c4(120)
+    frames = [(f"mini_v{k}", pos, tris, poses[k], (320, 180), 256, 1.0, 1, 0) for k in range(2)]
+    frames += [("mini_p59", pos, tris, path[59], (240, 160), 128, 1.0, 1, 0),
+               ("mini_pad", pos, tris, poses[4], (200, 150), 256, 1.5, 2, 1),
+               ("mini_tiny", pos, tris, poses[5], (320, 180), 16, 1.0, 1, 0),
+               ("mini_fail", pos, tris, poses[5], (320, 180), 8, 1.0, 1, 0)]
+    s = scenes.scene_c1()
+    frames.append(("C1", s.positions, s.triangles, s.poses[0], s.screen, s.omega, 1.0, 1, 0))
+    for packer in ("sequential", "superblock"):
+        for name, p, t, pose, screen, omega, prescale, md, pad in frames:
+            r = run_reference_frame(p, t, pose, screen, omega, prescale=prescale, min_dim=md, padding=pad,
+                                    packer=packer)
+            key = f"{packer}/{name}"
+            print(f"  frame {key}: {r['status']} {r['wall_s']:.2f}s", flush=True)
+            m = dict(name=name, packer=packer, screen=list(screen), omega=omega, prescale=prescale, min_dim=md,
+                     padding=pad, status=r["status"])
+            arrays[f"{key}/vp"] = r["vp"]
+            for k in ("placements", "scale", "uv_tris", "uv", "box_roots", "target"):
+                if k in r:
+                    arrays[f"{key}/{k}"] = r[k]
+            for k in ("digest", "screen_fragments", "texels_allocated", "n_visible", "stretch"):
+                if k in r:
+                    m[k] = r[k]
+            meta.append(m)
+    np.savez_compressed(os.path.join(out, "frames_packers.npz"), **arrays)
+    return meta
+
+
 def gen_c2(out):
-    s = scenes.scene_c2()
-    r = run_reference_frame(s.positions, s.triangles, s.poses[0], s.screen, s.omega)
-    rec = dict(status=r["status"], wall_s=r["wall_s"], vp=r["vp"].tolist(),
+    gen_digest(out, "c2_reference.json", scenes.scene_c2(), 0)
+
+
+def gen_digest(out, fname, s, pose_idx, packer="fastatlas"):
+    """One full-size reference frame reduced to SHA-256 digests of its arrays
+    (depth, flags, chart ids, vertex map, NDC boxes, UV rows) plus the layout."""
+    r = run_reference_frame(s.positions, s.triangles, s.poses[pose_idx], s.screen, s.omega,
+                            prescale=s.prescale, packer=packer)
+    rec = dict(scene=s.name, pose=pose_idx, packer=packer, prescale=s.prescale,
+               screen=list(s.screen), omega=s.omega, status=r["status"], wall_s=r["wall_s"], vp=r["vp"].tolist(),
                depth_sha=sha(r["depth"]), flags_sha=sha(r["flags"].astype(np.uint8)),
                n_visible=int(r["flags"].sum()),
                chart_sha=sha(r["chart_of_triangle"].astype(np.int64)),
@@ -472,9 +517,9 @@ def gen_c2(out):
                uv_sha=sha(r["uv"]), uv_tris_sha=sha(r["uv_tris"]),
                screen_fragments=r["screen_fragments"], texels_allocated=r["texels_allocated"],
                stretch=r["stretch"])
-    with open(os.path.join(out, "c2_reference.json"), "w") as fh:
+    with open(os.path.join(out, fname), "w") as fh:
         json.dump(rec, fh)
-    print(f"  C2: {r['status']} {r['wall_s']:.1f}s charts={rec['n_charts']} vis={rec['n_visible']}")
+    print(f"  {fname}: {r['status']} {r['wall_s']:.1f}s charts={rec['n_charts']} vis={rec['n_visible']}")
 
 
 def gen_baselines(out):
@@ -529,10 +574,12 @@ def main():
     ap_ = argparse.ArgumentParser()
     ap_.add_argument("--c2", action="store_true", help="also run the ~6 min C2 reference frame")
     ap_.add_argument("--only", default=None)
+    ap_.add_argument("--digest", default=None,
+                     help="SCENE:POSE[:PACKER] full-size reference digest, e.g. C3:0, C4:59, C5:37")
     args = ap_.parse_args()
     out = HERE
     meta = {}
-    only = set(args.only.split(",")) if args.only else None
+    only = set(args.only.split(",")) if args.only else (set() if (args.c2 or args.digest) else None)
     if only is None or "raster" in only:
         meta["raster"] = gen_raster(out)
     if only is None or "charts" in only:
@@ -545,6 +592,8 @@ def main():
         gen_baselines(out)
     if only is None or "frames" in only:
         meta["frames"] = gen_frames(out)
+    if only is None or "frames_packers" in only:
+        meta["frames_packers"] = gen_frames_packers(out)
     if meta:
         mp = os.path.join(out, "meta.json")
         old = json.load(open(mp)) if os.path.exists(mp) else {}
@@ -553,6 +602,13 @@ def main():
             json.dump(old, fh, indent=1)
     if args.c2:
         gen_c2(out)
+    if args.digest:
+        parts = args.digest.split(":")
+        name, pose = parts[0], int(parts[1])
+        packer = parts[2] if len(parts) > 2 else "fastatlas"
+        suffix = "" if packer == "fastatlas" else f"_{packer}"
+        gen_digest(out, f"{name.lower()}_p{pose}{suffix}_reference.json", scenes.build_scene(name), pose,
+                   packer=packer)
 
 
 if __name__ == "__main__":

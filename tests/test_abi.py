@@ -37,13 +37,14 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.fa_abi_version() == 1
+    assert lib.fa_abi_version() == 2
 
 
 def test_struct_layouts_match_header():
     from paper_2502_17712_b200 import _native
-    # fa_frame_params: 2 int, 4 int64, double, 5 int (+4 pad) -> 8 + 32 + 8 + 20 + 4 = 72
-    assert ctypes.sizeof(_native.FrameParams) == 72
+    # fa_frame_params: 2 int, 4 int64, double, 6 int, int64 -> 8 + 32 + 8 + 24 + 8 = 80
+    assert ctypes.sizeof(_native.FrameParams) == 80
+    assert _native.FrameParams.block_size.offset == 72
     # fa_frame_result: int + 2 int32 (+pad to 8) + 4 int64 + 2 double + int64 + 11 pointers
     assert ctypes.sizeof(_native.FrameResult) == 16 + 5 * 8 + 3 * 8 + 14 * 8
 

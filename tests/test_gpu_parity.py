@@ -318,6 +318,88 @@ class TestFrames:
             fa.run_scene_pipeline(cfg)
 
 
+# ------------------------------------------- frames with comparison packers ---
+def _packer_case(key):
+    m = next(x for x in meta()["frames_packers"] if f"{x['packer']}/{x['name']}" == key)
+    g = group(npz("frames_packers.npz"), key)
+    if m["name"].startswith("C"):
+        s = scenes.build_scene(m["name"])
+        pos, tris = s.positions, s.triangles
+    else:  # every mini frame renders the same mini scene
+        mini = group(npz("frames.npz"), "mini_v0")
+        pos, tris = mini["pos"], mini["tris"]
+    return m, g, pos, tris
+
+
+class TestFramePackers:
+    """run_scene_pipeline(cfg, packer=...) with the comparison packers of
+    make_packer (cli.py:318-339,386-387) vs the reference frame."""
+
+    @pytest.mark.parametrize("key", [f"{m['packer']}/{m['name']}" for m in meta()["frames_packers"]])
+    def test_frame_vs_reference(self, key):
+        m, g, pos, tris = _packer_case(key)
+        settings = FrameSettings(screen=tuple(m["screen"]), omega=m["omega"], min_dim=m["min_dim"],
+                                 padding=m["padding"], prescale=m["prescale"], uv_f64=True, packer=m["packer"])
+        eng = FrameEngine(fa.Mesh(pos, tris), settings=settings)
+        if m["status"] == "ValueError":
+            with pytest.raises(ValueError):
+                eng.run(g["vp"])
+            return
+        out = eng.run(g["vp"], check=False)
+        if m["status"] == "PackFailure":
+            assert out.status == 2
+            return
+        assert out.status == 0
+        h = out.to_host()
+        assert np.array_equal(h["roots"].astype(np.int64), g["box_roots"])
+        assert np.array_equal(h["target"], g["target"])
+        assert np.array_equal(h["placements"], g["placements"])
+        assert [out.scale.numerator, out.scale.denominator] == g["scale"].tolist()
+        assert out.texels_allocated == m["texels_allocated"]
+        assert out.screen_fragments == m["screen_fragments"]
+        assert fa.layout_digest(out.layout()).digest == m["digest"]
+        if m.get("stretch") is None:
+            assert out.stretch() is None
+        else:
+            st = out.stretch()
+            assert st.l2 == pytest.approx(m["stretch"][0], rel=1e-9)
+            assert st.linf == pytest.approx(m["stretch"][1], rel=1e-9)
+        pos_of = {int(t): k for k, t in enumerate(h["visible"])}
+        rows = np.array([pos_of[int(t)] for t in g["uv_tris"]], dtype=np.int64)
+        assert same_bits(h["uv"][rows], g["uv"])
+        mask = np.ones(len(h["visible"]), bool)
+        mask[rows] = False
+        assert np.all(np.isnan(h["uv"][mask]))
+
+    def test_engine_switches_packers(self):
+        """One engine alternating the graphed FastAtlas frame and an ungraphed
+        comparison frame: each result equals a fresh engine's."""
+        m, g, pos, tris = _packer_case("sequential/mini_v0")
+        base = dict(screen=tuple(m["screen"]), omega=m["omega"], uv_f64=True)
+        eng = FrameEngine(fa.Mesh(pos, tris))
+        a = eng.run(g["vp"], FrameSettings(**base)).clone()
+        b = eng.run(g["vp"], FrameSettings(packer="sequential", **base)).clone()
+        c = eng.run(g["vp"], FrameSettings(**base))
+        assert np.array_equal(b.placements.cpu().numpy(), g["placements"])
+        for k in ("placements", "uv"):
+            assert np.array_equal(getattr(a, k).cpu().numpy().view(np.uint8), getattr(c, k).cpu().numpy().view(np.uint8))
+
+    def test_run_scene_pipeline_packer_argument(self, tmp_path):
+        """The packer argument reaches the frame; an unknown name is InputError
+        only after the NothingVisible check (cli.py:366-368 before :386)."""
+        obj = tmp_path / "quad.obj"
+        obj.write_text("v -2 -2 -2\nv 2 -2 -2\nv 2 2 -2\nv -2 2 -2\nf 1 2 3 4\n")
+        cfg = fa.SceneConfig(mesh_path=obj, fov_y_deg=90, near=0.1, far=100, screen=(128, 128), omega=256)
+        ref = {p: fa.run_scene_pipeline(cfg, packer=p).layout for p in ("fastatlas", "sequential", "superblock")}
+        assert ref["sequential"].scale == 1 and len(ref["superblock"].placements) == 1
+        from paper_2502_17712_b200.cli import InputError
+        with pytest.raises(InputError):
+            fa.run_scene_pipeline(cfg, packer="nope")
+        cfg.look_at = (0, 0, 1)
+        with pytest.raises(fa.NothingVisible):
+            fa.run_scene_pipeline(cfg, packer="nope")
+
+
 # ------------------------------------------------- full-size configurations ---
 def _scene_vp(spec, pose):
     cam = fa.CameraFrame.from_params(math.radians(pose.fov_y_deg), spec.screen[0] / spec.screen[1], pose.near,
@@ -506,3 +588,40 @@ def test_shuffled_vertices_and_unused_vertices(order, monkeypatch):
     r = oracle.run_frame(pos_s, tris_s, vp, spec.screen, spec.omega)
     _check_vs_oracle(h, r)
     assert np.all(h["vertex_to_chart"][perm[V:]] == -1)
+
+
+# ------------------------------------------------------------ mesh binding ---
+def test_in_place_mesh_update_is_rebound():
+    """A deforming mesh: updating the engine's device positions in place
+    rebinds the mesh (torch version counter), and the frame equals a fresh
+    engine's frame of the moved mesh."""
+    m, g, pos, tris = _frame_case("mini_v0")
+    st = FrameSettings(screen=tuple(m["screen"]), omega=m["omega"], uv_f64=True)
+    eng = FrameEngine(fa.Mesh(pos, tris), settings=st)
+    eng.run(g["vp"])
+    moved = pos + np.array([0.05, -0.02, 0.03])
+    eng.pos.copy_(eng.pos.new_tensor(moved))
+    a = eng.run(g["vp"]).clone()
+    b = FrameEngine(fa.Mesh(moved, tris), settings=st).run(g["vp"])
+    for k in ("flags", "chart_of_triangle", "placements", "uv"):
+        assert np.array_equal(getattr(a, k).cpu().numpy().view(np.uint8), getattr(b, k).cpu().numpy().view(np.uint8)), k
+
+
+def test_invalid_mesh_leaves_no_mesh_bound():
+    """fa_set_mesh validates indices on the device before binding; a failed
+    bind leaves an empty mesh (frames see nothing), never the invalid one."""
+    import ctypes
+    import torch
+    from paper_2502_17712_b200 import _native as nat
+    ctx = nat.Context(0)
+    pos = torch.zeros((4, 3), dtype=torch.float64, device="cuda")
+    for bad in ([[0, 1, 4]], [[0, -1, 2]]):
+        tri = torch.tensor(bad, dtype=torch.int32, device="cuda")
+        code = ctx.L.fa_set_mesh(ctx.h, ctypes.c_void_p(pos.data_ptr()), 4, ctypes.c_void_p(tri.data_ptr()), 1)
+        assert code == nat.FA_VALUE_ERROR and b"out of range" in ctx.L.fa_last_error()
+        p = FrameSettings(screen=(8, 8), omega=16).params()
+        res = nat.FrameResult()
+        vp = np.eye(4)
+        code = ctx.L.fa_frame(ctx.h, vp.ctypes.data_as(ctypes.c_void_p), ctypes.byref(p), ctypes.byref(res),
+                              ctx.stream_ptr())
+        assert code == nat.FA_NOTHING_VISIBLE
