@@ -184,22 +184,3 @@ class TestFrames:
         assert np.all(np.isnan(r.uv[mask]))
 
 
-@pytest.mark.slow
-def test_c2_reference_digests():
-    path = os.path.join(GOLDEN, "c2_reference.json")
-    if not os.path.exists(path):
-        pytest.skip("C2 reference digest not generated")
-    import hashlib
-
-    from paper_2502_17712_b200 import scenes
-    ref = json.load(open(path))
-    s = scenes.scene_c2()
-    vp = np.array(ref["vp"])
-    r = oracle.run_frame(s.positions, s.triangles, vp, s.screen, s.omega)
-    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
-    assert sha(canon(r.depth)) == ref["depth_sha"]
-    assert sha(r.flags.astype(np.uint8)) == ref["flags_sha"]
-    assert sha(r.chart_of_triangle.astype(np.int64)) == ref["chart_sha"]
-    assert sha(r.vertex_to_chart.astype(np.int64)) == ref["v2c_sha"]
-    assert r.pack.placements.tolist() == ref["placements"]
-    assert list(r.pack.scale) == ref["scale"]
