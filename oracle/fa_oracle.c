@@ -165,6 +165,17 @@ static double signed_area2(const spoly *s)
     return ddot_strided(s->x, ry, n) - ddot_strided(s->y, rx, n);
 }
 
+/* exported for the host-arithmetic probe (tests/test_host_arithmetic.py):
+ * _signed_area2 of an n-gon given as x[n], y[n] (charts.py:251-253) */
+double orc_signed_area2(const double *x, const double *y, int n)
+{
+    spoly s;
+    if (n < 1 || n > MAX_POLY) return 0.0;
+    s.n = n;
+    for (int i = 0; i < n; i++) { s.x[i] = x[i]; s.y[i] = y[i]; s.z[i] = 0.0; }
+    return signed_area2(&s);
+}
+
 /* numpy pairwise sum used by poly[:,2].mean() (charts.py:266) */
 static double np_mean(const double *a, int n)
 {

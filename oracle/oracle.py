@@ -61,6 +61,8 @@ def lib():
         L.orc_orient_order.argtypes = [vp, vp, vp, i64, i64, vp, vp, vp, vp]
         L.orc_pack.argtypes = [vp, vp, vp, vp, i64, i64, i64, i64, i64, vp, vp, vp, vp]
         L.orc_uv.argtypes = [vp, i64, vp, vp, vp, i64, vp, vp, vp, vp, ci, ci, i64, vp]
+        L.orc_signed_area2.argtypes = [vp, vp, ci]
+        L.orc_signed_area2.restype = ctypes.c_double
         _lib = L
     return _lib
 
@@ -85,6 +87,12 @@ def project(positions, vp):
     out = np.empty((len(pos), 4))
     lib().orc_project(_p(pos), len(pos), _p(_f64(vp, (4, 4))), _p(out))
     return out
+
+
+def signed_area2(xs, ys) -> float:
+    """charts.py:251-253 through the OpenBLAS ddot restatement."""
+    x, y = _f64(xs), _f64(ys)
+    return lib().orc_signed_area2(_p(x), _p(y), len(x))
 
 
 def depth_prepass(positions, triangles, vp, res, cull=True):
