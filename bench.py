@@ -123,18 +123,19 @@ class ClockSampler:
 
 # ------------------------------------------------------------------- roofline --
 def stage_bytes(stage: str, T: int, V: int, W: int, H: int, n_vis: int, C: int) -> int:
-    """Algorithmic (compulsory) bytes per launch of each stage."""
+    """SURVEY §8(d) compulsory bytes of one frame, split over the stages that
+    move them (each datum counted once; intermediates the design adds, like
+    screen records, winner keys or depth clears, are not counted).  The
+    stages sum to frame_bytes()."""
     table = {
-        "project+clear": 24 * V + 32 * V + 4 * V + 8 * W * H + T,
-        "depth pass": 12 * T + 32 * V + 16 * W * H,
-        "visibility pass": 12 * T + 32 * V + 8 * W * H + T,
-        "visible compaction": 2 * T + 4 * T + 4 * n_vis,
-        "union-find": 4 * n_vis + 12 * n_vis + 4 * V + 4 * n_vis + 4 * V,
-        "chart roots": 8 * n_vis + 4 * C,
-        "bounds+dims": 4 * n_vis + 12 * n_vis + 32 * V + 64 * C,
-        "order": 32 * C,
-        "pack+select": 64 * C,
-        "uv": 4 * n_vis + 12 * n_vis + 32 * V + 24 * n_vis,
+        "project+clear": 24 * V,                   # positions in
+        "depth pass": 12 * T + 8 * W * H,          # triangle indices in, depth out
+        "visibility pass": 8 * W * H + T,          # depth in, visibility flags out
+        "visible compaction": T + 4 * T,           # flags in, chart_of_triangle out
+        "union-find": 4 * V,                       # vertex -> chart out
+        "order": 32 * C,                           # boxes in
+        "pack+select": 32 * C,                     # placements out
+        "uv": 24 * n_vis,                          # f32 UV rows out
     }
     return int(table.get(stage, 0))
 
@@ -234,60 +235,109 @@ def cpu_baseline_sample(n_frames: int = 6):
     for k in range(n_frames):
         oracle.run_frame(s.positions, s.triangles, _vp(views[k], s.screen), s.screen, s.omega)
     wall = time.perf_counter() - t0
-    return {"value": n_frames / wall, "unit": "atlases/s", "cores": 1, "kind": "port",
+    return {"value": n_frames / wall, "unit": "atlases/s", "cores": 1, "kind": "port", "cpu_model": cpu_model(),
             "sample": f"{n_frames} C2 frames (views 0..{n_frames - 1}), single-threaded C oracle "
                       f"(oracle/fa_oracle.c), {1000 * wall / n_frames:.0f} ms/frame"}
 
 
 # ------------------------------------------------------------------------ main --
-def main():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=64)  # the C5 batch: 64 streaming views per GPU
     ap.add_argument("--warmup", type=int, default=6)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--split", default="weak", choices=["weak", "strong"],
+                    help="weak: --steps views per GPU; strong: the C5 batch of 64 views split 64/G per GPU "
+                         "(SURVEY §8e, distributed.view_shard)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-frames", type=int, default=5)
     ap.add_argument("--depth", type=int, default=6, help="concurrent views per GPU (FramePipeline slots)")
     ap.add_argument("--l2", default="replicas", choices=["replicas", "flush"],
                     help="pipelined L2 policy: per-slot mesh replicas (inputs > L2) or a 256 MiB flush per view")
-    args = ap.parse_args()
+    args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    return args
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
 
-    if args.impl == "reference":
-        if rank != 0:
-            return
-        workers = len(os.sched_getaffinity(0))
-        frames, wall = cpu_reference_run(args.steps, args.warmup, workers)
-        v = frames / wall
-        line = {"metric": METRIC, "value": v, "unit": "atlases/s", "n_gpus": args.gpus, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": 1000 * wall / args.steps, "ms_per_frame": 1000 * wall / frames,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic", "impl": "reference",
-                "config": {"workload": WORKLOAD, "host": f"{workers} processes, one frame each per step"},
-                "cpu_baseline": {"value": v, "unit": "atlases/s", "cores": workers, "kind": "port",
-                                 "sample": f"{frames} C2 frames, {workers} concurrent single-threaded oracle "
-                                           f"frames per step"},
-                "e2e": {"value": v, "unit": "atlases/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
+def torchrun_cmd(args_argv, n_gpus: int, port: int) -> list:
+    """The single-node launch the driver uses for N > 1, built for a bare
+    `bench.py --gpus N` (one process per GPU, rendezvous on 127.0.0.1)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n_gpus}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *args_argv]
+
+
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def rank_views(args, rank: int, world: int) -> list:
+    """Pool indices of the C5 views this rank renders."""
+    from paper_2502_17712_b200 import distributed as fdist
+    if args.split == "strong":
+        return list(fdist.view_shard(64, rank, world))
+    return fdist.step_views(args.steps, rank)
+
+
+def bench_config(args, world: int) -> dict:
+    """The workload description both arms print (identical dicts)."""
+    per_gpu = f"{args.steps} views per GPU" if args.split == "weak" else "64 views split contiguously 64/G per GPU"
+    return {"workload": WORKLOAD, "views": per_gpu, "split": args.split,
+            "parallelism": f"{world} independent view streams, one process per GPU (no collective)",
+            "l2": ("inputs larger than L2 between timed views: per-slot device mesh replicas and frame buffers "
+                   "(~0.9 GB cycled through the 126 MB L2); single-view latency flushes 256 MiB before each view"
+                   if args.l2 == "replicas" else
+                   "a 256 MiB L2 flush enqueued before every timed view")}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def reference_arm(args, rank: int, world: int) -> None:
+    if rank != 0:
         return
+    workers = len(os.sched_getaffinity(0))
+    frames, wall = cpu_reference_run(args.steps, args.warmup, workers)
+    v = frames / wall
+    line = {"metric": METRIC, "value": v, "unit": "atlases/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000 * wall / args.steps, "ms_per_frame": 1000 * wall / frames,
+            "higher_is_better": True, "scaling": "weak" if args.split == "weak" else "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": bench_config(args, args.gpus),
+            "host": f"{workers} processes, one C2 frame each per step, on {cpu_model()}",
+            "cpu_baseline": {"value": v, "unit": "atlases/s", "cores": workers, "kind": "port",
+                             "cpu_model": cpu_model(),
+                             "sample": f"{frames} C2 frames, {workers} concurrent single-threaded oracle frames "
+                                       f"per step",
+                             "note": "the C restatement of the reference (oracle/fa_oracle.c), ~470x faster than "
+                                     "the reference's own Python (~6 min per C2 frame in the build container), "
+                                     "which cannot run on the GPU box; the ratio against it is conservative"},
+            "e2e": {"value": v, "unit": "atlases/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
 
+
+def measure_gpu(args, rank: int, world: int, local: int, view_ids: list) -> dict:
+    """All GPU timing of one rank (device events; barriers between phases)."""
     import torch
-    import torch.distributed as dist
-
-    if world > 1:
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
 
     import paper_2502_17712_b200 as fa
     from paper_2502_17712_b200 import FrameEngine, FrameSettings, scenes
+    from paper_2502_17712_b200 import distributed as fdist
 
+    dev = torch.device("cuda", local)
     spec = scenes.scene_c2()
     W, H = spec.screen
     T, V = len(spec.triangles), len(spec.positions)
@@ -295,9 +345,8 @@ def main():
     settings = FrameSettings(screen=spec.screen, omega=spec.omega, n_scales=64, prescale=1.0)
     eng = FrameEngine(mesh, device=local, settings=settings)
     views = _views()
-    K = args.steps
-    from paper_2502_17712_b200 import distributed as fdist
-    vps = [_vp(views[v], spec.screen) for v in fdist.step_views(K, rank)]
+    vps = [_vp(views[v], spec.screen) for v in view_ids]
+    K = len(vps)
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -307,9 +356,7 @@ def main():
     torch.cuda.synchronize()
 
     def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
+        fdist.barrier(dev)
 
     # ---------------- single-frame latency (one engine, inputs resident) -------
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
@@ -328,10 +375,8 @@ def main():
     # ---------------- pipelined views: the throughput `value` and `e2e` ---------
     # FramePipeline keeps `depth` engines on their own streams (independent
     # views, the streaming-clients setting).  The timed region is one device
-    # event pair around all K views; each view's L2 flush (256 MiB write) is
-    # enqueued on its slot stream inside the region, so it is paid for.
+    # event pair around all K views.
     replicas = args.l2 == "replicas"
-    pipe = fa.FramePipeline(mesh, device=local, settings=settings, depth=args.depth, mesh_replicas=replicas)
     dev_pipe = fa.FramePipeline(mesh, device=local, settings=settings, depth=args.depth, outputs=(),
                                 mesh_replicas=replicas)
 
@@ -356,21 +401,32 @@ def main():
     with ClockSampler(local) as clocks:
         dev_ms = timed_run(dev_pipe, vps)
     clock = clocks.summary()
+    del dev_pipe
 
     # end to end through the public API, host buffers: camera matrices from
-    # pinned memory (H2D per view) and chart ids, visible list, f32 UVs and
-    # placements back into pinned memory (D2H per view), all inside the region
+    # pinned memory (H2D per view) and results back into pinned memory (D2H
+    # per view), all inside the region.  `compact`: visible list, chart id
+    # per visible triangle, f32 UV per visible vertex, placements.  `dense`:
+    # the reference's own output shapes -- the (T,) chart_of_triangle, the
+    # (n_visible, 6) f32 UV rows, visible list and placements.
     pin_cam = torch.empty((K, 16), dtype=torch.float64).pin_memory()
     pin_cam.copy_(torch.as_tensor(np.stack([v.reshape(-1) for v in vps])))
     cams = [pin_cam[s].numpy().reshape(4, 4) for s in range(K)]
-    d2h = [0]
+    e2e = {}
+    for kind, outputs in (("compact", ("visible", "visible_chart", "vertex_uv", "placements")),
+                          ("dense", ("chart_of_triangle", "visible", "uv", "placements"))):
+        pipe = fa.FramePipeline(mesh, device=local, settings=settings, depth=args.depth, outputs=outputs,
+                                mesh_replicas=replicas)
+        d2h = [0]
 
-    def count(hf):
-        if hf.error is not None:
-            raise hf.error
-        d2h[0] += hf.d2h_bytes()
+        def count(hf):
+            if hf.error is not None:
+                raise hf.error
+            d2h[0] += hf.d2h_bytes()
 
-    e2e_ms = timed_run(pipe, cams, count)
+        ms = timed_run(pipe, cams, count)
+        e2e[kind] = (ms, d2h[0] / K)
+        del pipe
 
     # ---------------- per-stage timing (same stream, CUDA events) ------------
     prof = FrameSettings(screen=spec.screen, omega=spec.omega, n_scales=64, profile=True, use_graph=False)
@@ -381,11 +437,58 @@ def main():
         for k, v in eng.stage_times().items():
             acc.setdefault(k, []).append(v)
     stage_ms = {k: float(np.mean(v)) for k, v in acc.items()}
+    return dict(views=K, dev_ms=dev_ms, lat_ms=lat_ms, e2e=e2e, stats=stats, stage_ms=stage_ms, clocks=clock,
+                launches_per_frame=launches_per_frame, T=T, V=V, W=W, H=H)
+
+
+def main(argv=None, measure=None):
+    args = parse_args(argv)
+    from paper_2502_17712_b200 import distributed as fdist
+    rank, world, local = fdist.world()
+
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # a bare `bench.py --gpus N`: start the N ranks (one process per GPU)
+        cmd = torchrun_cmd(sys.argv[1:] if argv is None else list(argv), args.gpus, _free_port())
+        raise SystemExit(subprocess.call(cmd))
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        backend = os.environ.get("FA_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            # NCCL communicator init is logged (the barrier / max-time comm);
+            # there is no collective on the data path
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend, rank=rank, world_size=world)
+    dev = None
+    if measure is None:
+        measure = measure_gpu
+        torch.cuda.set_device(local)
+        dev = torch.device("cuda", local)
+    view_ids = rank_views(args, rank, world)
+    r = measure(args, rank, world, local, view_ids)
+    fdist.barrier(dev)
 
     # ---------------- reduce over ranks ----------------
-    dev_ms, e2e_ms, lat_ms = fdist.max_over_ranks([dev_ms, e2e_ms, lat_ms], device=dev)
-    frames_total = K * world
+    dev_ms, e2e_c, e2e_d, lat_ms = fdist.max_over_ranks(
+        [r["dev_ms"], r["e2e"]["compact"][0], r["e2e"]["dense"][0], r["lat_ms"] / max(1, r["views"])], device=dev)
+    views_total = int(fdist.sum_over_ranks([r["views"]], device=dev)[0])
+    ranks_ran = int(fdist.sum_over_ranks([1], device=dev)[0])
     if rank == 0:
+        T, V, W, H = r["T"], r["V"], r["W"], r["H"]
+        K = r["views"]
+        stats = r["stats"]
+        stage_ms = r["stage_ms"]
         n_vis = int(np.mean([a for a, _ in stats]))
         C = int(np.mean([b for _, b in stats]))
         top = max(stage_ms, key=stage_ms.get) if stage_ms else None
@@ -395,44 +498,45 @@ def main():
             b = stage_bytes(top, T, V, W, H, n_vis, C)
             gbs = b / (stage_ms[top] * 1e-3) / 1e9
             traffic, tsrc = stage_traffic(top)
+            fb = frame_bytes(T, V, W, H, n_vis, C)
             roof = {"bound": "hbm", "kernel": top, "achieved": gbs, "peak": peak, "unit": "GB/s",
                     "frac": gbs / peak, "peak_source": peak_kind, "traffic": traffic, "traffic_source": tsrc,
                     "algorithmic_bytes": b, "kernel_ms": stage_ms[top],
-                    "frame_bytes": frame_bytes(T, V, W, H, n_vis, C),
-                    "frame_frac": frame_bytes(T, V, W, H, n_vis, C) / (dev_ms / K * 1e-3) / 1e9 / peak}
+                    "bytes_basis": "SURVEY §8(d) compulsory bytes of the stage (DESIGN §4)",
+                    "frame_bytes": fb, "frame_frac": fb / (dev_ms / K * 1e-3) / 1e9 / peak,
+                    "frame_frac_latency": fb / (lat_ms * 1e-3) / 1e9 / peak}
+        scaling = "weak" if args.split == "weak" else "strong"
         line = {
-            "metric": METRIC, "value": frames_total / (dev_ms * 1e-3), "unit": "atlases/s", "n_gpus": world,
+            "metric": METRIC, "value": views_total / (dev_ms * 1e-3), "unit": "atlases/s", "n_gpus": ranks_ran,
             "steps": K, "warmup": args.warmup, "ms_per_step": dev_ms / K,
-            "ms_per_frame": lat_ms / K,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "ms_per_frame": lat_ms,
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": WORKLOAD,
-                       "l2": (f"value/e2e: inputs larger than L2 -- each of the {args.depth} pipeline slots holds "
-                              "its own device mesh replica (24 MB) and frame buffers (~130 MB touched per view), "
-                              "so the slots cycle ~0.9 GB through the 126 MB L2; ms_per_frame: a 256 MiB L2 "
-                              "flush before every view, outside its event pair" if replicas else
-                              "flushed: a 256 MiB write enqueued before every view (inside the timed region for "
-                              "value/e2e, outside the event pair for ms_per_frame)"),
-                       "views_per_gpu": K, "mean_visible": n_vis, "mean_charts": C,
+            "config": bench_config(args, world),
+            "detail": {"views_total": views_total, "views_rank0": K, "mean_visible": n_vis, "mean_charts": C,
                        "concurrent_views_per_gpu": args.depth,
-                       "value_is": "views/s of FramePipeline (depth concurrent slot streams, device outputs)",
-                       "ms_per_frame_is": "single-view latency, one engine, mean of K event pairs",
-                       "parallelism": f"{world} independent view streams (no collective)"},
-            "e2e": {"value": frames_total / (e2e_ms * 1e-3), "unit": "atlases/s", "h2d_bytes_per_step": 128,
-                    "d2h_bytes_per_step": int(d2h[0] / K),
+                       "value_is": "views/s of FramePipeline (depth concurrent slot streams, device outputs), "
+                                   "all ranks' views / max-over-ranks device time",
+                       "ms_per_frame_is": "single-view latency, one engine, mean of K event pairs"},
+            "e2e": {"value": views_total / (e2e_c * 1e-3), "unit": "atlases/s", "h2d_bytes_per_step": 128,
+                    "d2h_bytes_per_step": int(r["e2e"]["compact"][1]),
                     "what": "FramePipeline.run over pinned camera matrices (H2D per view) with the visible list, "
                             "the chart id of each visible triangle (sparse chart_of_triangle), the f32 UV of each "
                             "visible vertex (compact form of the per-triangle f32 UV rows, rebuilt bit-identically "
-                            "on access) and the placements copied into pinned host buffers (D2H per view)"},
-            "gpu_launches": launches_per_frame * K,
-            "launches_per_frame": launches_per_frame,
+                            "on access) and the placements copied into pinned host buffers (D2H per view)",
+                    "dense": {"value": views_total / (e2e_d * 1e-3), "unit": "atlases/s",
+                              "h2d_bytes_per_step": 128, "d2h_bytes_per_step": int(r["e2e"]["dense"][1]),
+                              "what": "the reference's output shapes: dense (T,) chart_of_triangle, (n_visible, 6) "
+                                      "f32 UV rows, visible list and placements copied per view"}},
+            "gpu_launches": r["launches_per_frame"] * K,
+            "launches_per_frame": r["launches_per_frame"],
             "stage_ms": stage_ms,
             "roofline": roof,
-            "clocks": clock,
+            "clocks": r["clocks"],
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_sample()
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

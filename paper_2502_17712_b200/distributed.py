@@ -45,6 +45,16 @@ def max_over_ranks(values, device=None):
     return [float(v) for v in t.cpu()]
 
 
+def sum_over_ranks(values, device=None):
+    """Element-wise SUM all-reduce of a list of floats (identity when not distributed)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(v) for v in values], dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return [float(v) for v in t.cpu()]
+
+
 def barrier(device=None):
     import torch
     import torch.distributed as dist

@@ -69,3 +69,95 @@ def test_two_rank_gloo():
     for r, t, gathered in out:
         assert t == [2.0, 10.0]  # element-wise max over ranks
         assert [v for shard in gathered for v in shard] == list(range(64))
+
+
+# --------------------------------------------- bench.main's rank path (gloo) ---
+def _stand_in_measure(args, rank, world, local, view_ids):
+    """Stands in for bench.measure_gpu (no GPU here): rank r's device time is
+    10 + r ms for its views."""
+    n = len(view_ids)
+    return dict(views=n, dev_ms=10.0 + rank, lat_ms=0.3 * n, e2e={"compact": (12.0 + rank, 1000.0),
+                                                                    "dense": (14.0, 2000.0)},
+                stats=[(170000, 960)] * n, stage_ms={"depth pass": 0.1, "uv": 0.01}, clocks={"sm_mhz": None},
+                launches_per_frame=25, T=1000040, V=500302, W=1920, H=1080, view_ids=list(view_ids))
+
+
+def _bench_worker(rank, world, port, argv, q):
+    import contextlib
+    import io
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, repo)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank), FA_BENCH_BACKEND="gloo")
+    import bench
+    seen = []
+
+    def measure(args, r, w, local, view_ids):
+        seen.extend(view_ids)
+        return _stand_in_measure(args, r, w, local, view_ids)
+
+    buf = io.StringIO()
+    with contextlib.redirect_stdout(buf):
+        bench.main(argv, measure=measure)
+    q.put((rank, buf.getvalue(), seen))
+
+
+def _run_bench_ranks(argv, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_worker, args=(r, world, port, argv, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=180) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return out
+
+
+def test_bench_main_two_ranks_weak():
+    import json
+    out = _run_bench_ranks(["--gpus", "2", "--steps", "8", "--no-cpu-baseline"])
+    (r0, text0, v0), (r1, text1, v1) = out
+    assert text1 == ""  # only rank 0 prints
+    lines = [ln for ln in text0.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["scaling"] == "weak"
+    assert v0 == list(range(8)) and v1 == list(range(8, 16))
+    # all ranks' views over the max-over-ranks device time (rank 1: 11 ms)
+    assert line["value"] == pytest.approx(16 / 11e-3)
+    assert line["e2e"]["value"] == pytest.approx(16 / 13e-3)
+    assert line["config"]["parallelism"].startswith("2 independent view streams")
+
+
+def test_bench_main_two_ranks_strong_split():
+    import json
+    out = _run_bench_ranks(["--gpus", "2", "--split", "strong", "--no-cpu-baseline"])
+    (_, text0, v0), (_, _, v1) = out
+    line = json.loads(text0.strip())
+    assert v0 == list(range(32)) and v1 == list(range(32, 64))
+    assert line["scaling"] == "strong" and line["detail"]["views_total"] == 64
+    assert line["value"] == pytest.approx(64 / 11e-3)
+
+
+def test_bench_torchrun_command():
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, repo)
+    import bench
+    cmd = bench.torchrun_cmd(["--gpus", "4", "--steps", "8"], 4, 29511)
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "127.0.0.1" in cmd and cmd[-3:] == ["--gpus", "4", "--steps", "8"][-3:]
+
+
+def test_bench_reference_config_matches_b200_arm():
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, repo)
+    import bench
+    a = bench.parse_args(["--gpus", "1", "--steps", "20"])
+    b = bench.parse_args(["--gpus", "1", "--steps", "20", "--impl", "reference"])
+    assert bench.bench_config(a, 1) == bench.bench_config(b, 1)
