@@ -222,8 +222,8 @@ __global__ void __launch_bounds__(SETUP_WARPS * 32) k_raster_setup(const double4
 }
 
 // ---- pass 1, generic path: clipped polygons (and oversize screens) --------
-// One warp per listed triangle: lane 0 clips and builds the TriSetup in
-// shared memory (the serial part), then the warp stores it to the `large`
+// One warp per listed triangle: the warp clips (tri_setup_warp, a vertex per
+// lane) and builds the TriSetup in shared memory, then stores it to the `large`
 // queue and either samples the whole window (<= FA_SMALL_PX pixels, depth
 // pass only) or writes the descriptors of its 16x8 tiles (negative ids).
 // The visibility pass finds every stored setup through the queue.
@@ -237,16 +237,14 @@ __global__ void __launch_bounds__(256) k_raster_clipped(const double4* __restric
                                                         fa_dstat* __restrict__ st) {
     FA_PDL_PROLOGUE();
     __shared__ TriSetup sm[8];
+    __shared__ ClipScratch cs[8];
     const int warp = threadIdx.x >> 5, lane = lane_id();
     const int nwarps = gridDim.x * 8;
     const int n = st->n_clip;
     for (int w = blockIdx.x * 8 + warp; w < n; w += nwarps) {
         const int t = clip_list[w];
-        int r = 0;
         __syncwarp();
-        if (lane == 0) r = tri_setup(clip, tris, t, W, H, cull != 0, sm[warp]);
-        r = __shfl_sync(0xffffffffu, r, 0);
-        __syncwarp();
+        const int r = tri_setup_warp(clip, tris, t, W, H, cull != 0, sm[warp], cs[warp]);
         if (r < 0) {
             if (lane == 0) atomicOr(&st->flags, FA_DFLAG_POLY_OVERFLOW);
             continue;
@@ -562,14 +560,15 @@ __global__ void __launch_bounds__(COOP_WARPS * 32, COOP_MIN_BLOCKS) k_small_coop
                     iy = f.min_y;
                 }
                 const RowTerms rt = row_terms(f, (double)iy + 0.5);
-                int xa, xb;
-                row_span(f, rt, se, xa, xb);
+                int xa, xb, ca, cb;
+                row_span_cert(f, rt, se, xa, xb, ca, cb);
                 const long long rowoff = (long long)iy * W;
                 double px = (double)xa + 0.5;  // px += 1 below is exact (half-integers < 2^52)
                 for (int ix = xa; ix <= xb; ix++, px += 1.0) {
-                    // depth evaluated alongside the edges (independent DP chains)
+                    // the edge test only near a crossing (row_span_cert)
                     const double z = depth_row(f, rt, px);
-                    if (inside_row(f, rt, px)) depth_min(depth, wid, rowoff + ix, f64_key(z), t, false);
+                    if ((ix >= ca && ix <= cb) || inside_row(f, rt, px))
+                        depth_min(depth, wid, rowoff + ix, f64_key(z), t, false);
                 }
             }
         }
@@ -656,11 +655,11 @@ __global__ void __launch_bounds__(256) k_vis_small_sample(const SmallRec* __rest
         for (int iy = f.min_y; iy <= f.max_y && !vis; iy++) {
             const RowTerms rt = row_terms(f, (double)iy + 0.5);
             const unsigned long long* row = depth + (long long)iy * W;
-            int xa, xb;
-            row_span(f, rt, se, xa, xb);  // only samples that can be covered
+            int xa, xb, ca, cb;
+            row_span_cert(f, rt, se, xa, xb, ca, cb);  // only samples that can be covered
             for (int ix = xa; ix <= xb; ix++) {
                 double px = (double)ix + 0.5;
-                if (!inside_row(f, rt, px)) continue;
+                if (!(ix >= ca && ix <= cb) && !inside_row(f, rt, px)) continue;
                 double z = depth_row(f, rt, px);
                 const unsigned long long* a = row + ix;
                 if (nq == 0) { z0 = z; a0 = a; }

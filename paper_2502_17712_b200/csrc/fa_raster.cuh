@@ -239,6 +239,96 @@ __device__ __forceinline__ int tri_setup(const double4* __restrict__ clip, const
     return 1;
 }
 
+// ---- warp-parallel tri_setup (the clipping path) ---------------------------
+// Same operations on the same values as tri_setup (so the same bits), with
+// polygon vertex i on lane i: each Sutherland-Hodgman step (charts.py:
+// 178-189) computes every output vertex -- kept vertex and/or edge crossing
+// t = da / (da - db), a + t * (b - a) -- on the lane of its input vertex and
+// places it by a warp prefix sum; the screen divides run one vertex per lane;
+// lane 0 then finishes the setup (finish_setup: the OpenBLAS-order shoelace,
+// cull / flip, bbox, edges, depth plane).  scratch: per-warp shared memory.
+struct ClipScratch {
+    double4 v[FA_MAXV];
+    double sx[FA_MAXV], sy[FA_MAXV], sz[FA_MAXV];
+};
+
+// one clip step on the lanes' polygon (n vertices, vertex per lane, signed
+// distances d): keeps d >= 0.  Returns false on capacity overflow.
+__device__ __forceinline__ bool clip_step_warp(double4& v, int& n, double d, ClipScratch& cs) {
+    const int lane = lane_id();
+    const bool act = lane < n;
+    const int j = (lane + 1 == n) ? 0 : lane + 1;
+    const double db = __shfl_sync(0xffffffffu, d, j & 31);
+    const double bx = __shfl_sync(0xffffffffu, v.x, j & 31), by = __shfl_sync(0xffffffffu, v.y, j & 31);
+    const double bz = __shfl_sync(0xffffffffu, v.z, j & 31), bw = __shfl_sync(0xffffffffu, v.w, j & 31);
+    const bool keep = act && d >= 0;
+    const bool cross = act && ((d >= 0) != (db >= 0));
+    const int cnt = (int)keep + (int)cross;
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int m = __shfl_sync(0xffffffffu, incl, 31);
+    if (m > FA_MAXV) return false;  // tri_setup fails adding the (FA_MAXV+1)-th vertex
+    int pos = incl - cnt;
+    __syncwarp();
+    if (keep) cs.v[pos++] = v;
+    if (cross) {
+        const double t = __ddiv_rn(d, __dsub_rn(d, db));
+        double4 o;
+        o.x = __dadd_rn(v.x, __dmul_rn(t, __dsub_rn(bx, v.x)));
+        o.y = __dadd_rn(v.y, __dmul_rn(t, __dsub_rn(by, v.y)));
+        o.z = __dadd_rn(v.z, __dmul_rn(t, __dsub_rn(bz, v.z)));
+        o.w = __dadd_rn(v.w, __dmul_rn(t, __dsub_rn(bw, v.w)));
+        cs.v[pos] = o;
+    }
+    __syncwarp();
+    n = m;
+    if (lane < n) v = cs.v[lane];
+    return true;
+}
+
+// 1 = setup filled (on every lane's return; `s` in shared memory), 0 = no
+// samples, -1 = polygon capacity overflow.  Call with the whole warp.
+static __device__ __noinline__ int tri_setup_warp(const double4* __restrict__ clip, const int* __restrict__ tris, int t,
+                                           int W, int H, bool cull, TriSetup& s, ClipScratch& cs) {
+    const int lane = lane_id();
+    int n = 3;
+    double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
+    if (lane < 3) v = ldg4(clip + __ldg(tris + 3 * t + lane));
+    // charts.py:163-167: the w >= eps plane
+    double d = __dsub_rn(v.w, FA_W_EPSILON);
+    if (!__any_sync(0xffffffffu, lane < n && d > 0)) return 0;
+    if (__any_sync(0xffffffffu, lane < n && d <= 0))
+        if (!clip_step_warp(v, n, d, cs)) return -1;
+    // charts.py:168-174: L, R, B, T, N, F, each skipped when every d >= 0
+    for (int p = 0; p < 6; p++) {
+        if (n == 0) break;
+        const int axis = p >> 1;
+        const double c = axis == 0 ? v.x : (axis == 1 ? v.y : v.z);
+        d = (p & 1) ? __dsub_rn(v.w, c) : __dadd_rn(v.w, c);
+        if (__all_sync(0xffffffffu, !(lane < n) || d >= 0)) continue;
+        if (!clip_step_warp(v, n, d, cs)) return -1;
+    }
+    if (n < 3) return 0;
+    if (lane < n) {
+        cs.sx[lane] = screen_x(v.x, v.w, W);
+        cs.sy[lane] = screen_x(v.y, v.w, H);
+        cs.sz[lane] = __ddiv_rn(v.z, v.w);
+    }
+    __syncwarp();
+    int r = 0;
+    if (lane == 0) {
+        r = finish_setup(cs.sx, cs.sy, cs.sz, n, W, H, cull, s);
+        if (r > 0) s.tri = t;
+    }
+    r = __shfl_sync(0xffffffffu, r, 0);
+    __syncwarp();
+    return r;
+}
+
 // ---- register-resident setup for unclipped triangles (the common case) ----
 // Same arithmetic as tri_setup + finish_setup for n == 3, with every array
 // indexed by compile-time constants so nothing lands in local memory.
@@ -549,25 +639,32 @@ __device__ __forceinline__ double depth_row(const Setup3& s, const RowTerms& r, 
 // Along a row, edge i's value is e_i(px) = r_i - dy_i*(px - ax_i), whose sign
 // changes at x_i = ax_i + r_i/dy_i: dy_i > 0 bounds the covered samples from
 // the right, dy_i < 0 from the left.  row_span() returns the pixel range
-// whose samples lie within FA_SPAN_MARGIN of [max left, min right]; every
-// sample outside it fails the reference's exact test (charts.py:237-249), so
-// only the range is tested — exactly, with the operations above.
-// Why skipping is exact (window of B+1 <= 300 pixels on a side, so
-// |dx_i|, |dy_i|, |py - ay_i|, |px - ax_i| <= B+1): 1/dy_i comes from an FP32
-// MUFU reciprocal (relative error < 2^-22) plus one FP64 Newton step
-// (relative error < 1e-13) and is only used when |dy_i| >= 1e-3, so the
-// computed x_i is within 1e-10 (B+1)^2 <= 1e-5 px of the exact crossing of
-// the reference's r_i.  A sample FA_SPAN_MARGIN (1e-4 px) beyond the
-// computed x_i then has |dy_i (px - x_i)| >= 1e-3 * 9e-5 ~ 1e-7, while the
-// reference's rounded dy_i*(px - ax_i) is within 4.5e-16 (B+1)^2 < 1e-10 of
-// exact, so its e_i (whose sign is that of r_i minus that product) has the
-// excluded sign.  Edges with |dy_i| < 1e-3 give no bound (their samples are
-// all tested exactly).
+// whose samples lie within a margin M of [max left, min right]; every sample
+// outside it fails the reference's exact test (charts.py:237-249), so only
+// the range is tested -- exactly, with the operations above.
+// Why skipping is exact, for any window: 1/dy_i comes from an FP32 MUFU
+// reciprocal (relative error < 2^-22 after the FP32 rounding of dy_i) plus
+// one FP64 Newton step (relative error < 2.5e-13 including its roundings),
+// and is only used when |dy_i| >= 1e-3.  With |py - ay_i| <= rows + 3 (the
+// unclipped vertices lie inside the screen and the window is their rounded
+// bbox), the computed x_i is within
+//     delta_i = 3e-13 * |dx_i| * |1/dy_i| * (rows + 3) + 1e-9
+// px of the exact crossing of the reference's rounded r_i (the 1e-9 covers
+// the final multiply-add's rounding for coordinates < 2^20).  The margin is
+// M = FA_SPAN_MARGIN + max_i delta_i.  A sample more than M beyond the
+// computed x_i is at least FA_SPAN_MARGIN = 1e-4 px beyond the exact one,
+// so |r_i - dy_i (px - ax_i)| >= 1e-3 * 1e-4 = 1e-7 in the excluded
+// direction, while the reference's rounded dy_i*(px - ax_i) is within
+// 2.3e-16 |dy_i| (cols + 3) of exact -- below 1e-7 for windows < 10^8 px wide
+// -- so its e_i has the excluded sign.  Edges with |dy_i| < 1e-3 give no
+// bound (their samples are all tested exactly).  At C2 the margin stays
+// below 1e-3 px.
 #define FA_SPAN_MARGIN 1e-4
 #define FA_SPAN_MIN_DY 1e-3
 
 struct SpanEdges {
     double inv0, inv1, inv2;  // ~1/dy_i
+    double margin;            // M above
     int kind;                 // 2 bits per edge: 1 right bound (dy > 0), 2 left bound (dy < 0), 0 none
 };
 
@@ -582,9 +679,24 @@ __device__ __forceinline__ SpanEdges span_edges(const Setup3& f) {
     SpanEdges se;
     se.kind = 0;
     se.inv0 = se.inv1 = se.inv2 = 0.0;
-    if (fabs(f.dy0) >= FA_SPAN_MIN_DY) { se.inv0 = approx_inv(f.dy0); se.kind |= f.dy0 > 0 ? 1 : 2; }
-    if (fabs(f.dy1) >= FA_SPAN_MIN_DY) { se.inv1 = approx_inv(f.dy1); se.kind |= (f.dy1 > 0 ? 1 : 2) << 2; }
-    if (fabs(f.dy2) >= FA_SPAN_MIN_DY) { se.inv2 = approx_inv(f.dy2); se.kind |= (f.dy2 > 0 ? 1 : 2) << 4; }
+    double q = 0.0;  // max |dx_i / dy_i| over the bounding edges
+    if (fabs(f.dy0) >= FA_SPAN_MIN_DY) {
+        se.inv0 = approx_inv(f.dy0);
+        se.kind |= f.dy0 > 0 ? 1 : 2;
+        q = fmax(q, fabs(f.dx0 * se.inv0));
+    }
+    if (fabs(f.dy1) >= FA_SPAN_MIN_DY) {
+        se.inv1 = approx_inv(f.dy1);
+        se.kind |= (f.dy1 > 0 ? 1 : 2) << 2;
+        q = fmax(q, fabs(f.dx1 * se.inv1));
+    }
+    if (fabs(f.dy2) >= FA_SPAN_MIN_DY) {
+        se.inv2 = approx_inv(f.dy2);
+        se.kind |= (f.dy2 > 0 ? 1 : 2) << 4;
+        q = fmax(q, fabs(f.dx2 * se.inv2));
+    }
+    // (1 + 1e-9) covers the rounding of q itself
+    se.margin = FA_SPAN_MARGIN + 1e-9 + 3.0001e-13 * q * (double)(f.max_y - f.min_y + 4);
     return se;
 }
 
@@ -601,12 +713,36 @@ __device__ __forceinline__ void row_span(const Setup3& f, const RowTerms& rt, co
     span_edge(se.kind & 3, f.ax0, rt.r0, se.inv0, xl, xr);
     span_edge((se.kind >> 2) & 3, f.ax1, rt.r1, se.inv1, xl, xr);
     span_edge((se.kind >> 4) & 3, f.ax2, rt.r2, se.inv2, xl, xr);
-    // sample px = ix + 0.5 is a candidate iff xl - m <= px <= xr + m
+    // sample px = ix + 0.5 is a candidate iff xl - M <= px <= xr + M
     // (clamped to the window so the conversions below stay in range)
     xl = fmin(xl, (double)f.max_x + 2.0);
     xr = fmax(xr, (double)f.min_x - 1.0);
-    lo = max(f.min_x, (int)ceil(xl - 0.5 - FA_SPAN_MARGIN));
-    hi = min(f.max_x, (int)floor(xr - 0.5 + FA_SPAN_MARGIN));
+    lo = max(f.min_x, (int)ceil(xl - 0.5 - se.margin));
+    hi = min(f.max_x, (int)floor(xr - 0.5 + se.margin));
+}
+
+// Like row_span, plus the columns [clo, chi] whose samples certainly PASS the
+// reference's edge test: the mirror of the exclusion argument above -- a
+// sample more than M inside every edge's computed crossing has
+// |r_i - dy_i (px - ax_i)| >= 1e-7 on the inside, far above the reference's
+// rounding of e_i, so e_i > 0 (accepted with or without the top-left rule).
+// Only when all three edges bound the row (|dy_i| >= 1e-3); otherwise the
+// certified range is empty and every candidate is tested exactly.  Samples
+// in [lo, hi] outside [clo, chi] (a crossing within M of a sample centre:
+// rare) are tested exactly.
+__device__ __forceinline__ void row_span_cert(const Setup3& f, const RowTerms& rt, const SpanEdges& se, int& lo,
+                                              int& hi, int& clo, int& chi) {
+    double xl = (double)f.min_x, xr = (double)f.max_x + 1.0;
+    span_edge(se.kind & 3, f.ax0, rt.r0, se.inv0, xl, xr);
+    span_edge((se.kind >> 2) & 3, f.ax1, rt.r1, se.inv1, xl, xr);
+    span_edge((se.kind >> 4) & 3, f.ax2, rt.r2, se.inv2, xl, xr);
+    xl = fmin(xl, (double)f.max_x + 2.0);
+    xr = fmax(xr, (double)f.min_x - 1.0);
+    lo = max(f.min_x, (int)ceil(xl - 0.5 - se.margin));
+    hi = min(f.max_x, (int)floor(xr - 0.5 + se.margin));
+    const bool all3 = (se.kind & 3) && ((se.kind >> 2) & 3) && ((se.kind >> 4) & 3);
+    clo = all3 ? (int)ceil(xl - 0.5 + se.margin) : 1;
+    chi = all3 ? (int)floor(xr - 0.5 - se.margin) : 0;
 }
 
 struct ColTerms {
