@@ -335,8 +335,28 @@ extern "C" void fa_debug_pack_prof(long long* out) { cudaMemcpyFromSymbol(out, g
 #define PACK_MARK(k, v)
 #endif
 
+// max of f[a, b) (>= 0: the frontline starts at 0 and only rises) and fill of
+// f[a, b), 16-byte vector accesses in the aligned middle
+__device__ __forceinline__ int span_max(const int* f, int a, int b) {
+    int m = 0, c = a;
+    for (; c < b && (reinterpret_cast<uintptr_t>(f + c) & 15); c++) m = max(m, f[c]);
+    for (; c + 4 <= b; c += 4) {
+        const int4 v = *reinterpret_cast<const int4*>(f + c);
+        m = max(m, max(max(v.x, v.y), max(v.z, v.w)));
+    }
+    for (; c < b; c++) m = max(m, f[c]);
+    return m;
+}
+__device__ __forceinline__ void span_fill(int* f, int a, int b, int v) {
+    int c = a;
+    for (; c < b && (reinterpret_cast<uintptr_t>(f + c) & 15); c++) f[c] = v;
+    for (; c + 4 <= b; c += 4) *reinterpret_cast<int4*>(f + c) = make_int4(v, v, v, v);
+    for (; c < b; c++) f[c] = v;
+}
+
 // One candidate: returns accept; fills cand_w/h/p/y/rowstart for the CTA.
-__device__ bool pack_candidate(const long long* __restrict__ ow, const long long* __restrict__ oh, int n,
+template <typename DimT>
+__device__ bool pack_candidate(const DimT* __restrict__ ow, const DimT* __restrict__ oh, int n,
                                long long num, long long den, long long omega, int kbits, long long min_dim,
                                long long pad, int* cw, int* ch, long long* cp, int* cy, int* rowstart, int* front,
                                long long& out_num, long long& out_den, long long& out_used, PackSmem& sm) {
@@ -566,13 +586,17 @@ __device__ bool pack_candidate(const long long* __restrict__ ow, const long long
             int w = act ? cw[b] : 0;
             int x = left ? (int)q : (int)(omega - q - w);
             int rest = 0;
-            for (int c = x + gl; c < x + w; c += G) rest = max(rest, front[c]);
+            if (G == 1) rest = span_max(front, x, x + w);  // one thread per box: 4 columns per load
+            else
+                for (int c = x + gl; c < x + w; c += G) rest = max(rest, front[c]);
             for (int o = G >> 1; o > 0; o >>= 1) rest = max(rest, __shfl_xor_sync(0xffffffffu, rest, o, G));
             // saturate above omega: any such top already rejects the candidate
             long long top64 = (long long)rest + ch[b];
             int top = top64 > omega ? (int)(omega + 1) : (int)top64;
             if (act) {
-                for (int c = x + gl; c < x + w; c += G) front[c] = top;
+                if (G == 1) span_fill(front, x, x + w, top);
+                else
+                    for (int c = x + gl; c < x + w; c += G) front[c] = top;
                 if (gl == 0) cy[b] = rest;
                 used = top > used ? top : used;
             }
@@ -651,25 +675,19 @@ __global__ void k_batch_done(const long long* __restrict__ cand, long long lo, l
     if (__syncthreads_or(any) && threadIdx.x == 0) st->done = 1;
 }
 
-// selection (packing.py:327-345) + placements in packing order
-__global__ void __launch_bounds__(1024) k_select(const long long* __restrict__ ow, const long long* __restrict__ tw,
-                                                 const long long* __restrict__ th, const long long* __restrict__ chart_id,
-                                                 const unsigned char* __restrict__ rot, const int* __restrict__ perm,
-                                                 int n_max, const int* __restrict__ n_dev, long long omega,
-                                                 long long n_scales, long long min_dim, long long pad,
-                                                 const long long* __restrict__ cand, const long long* __restrict__ cand_p,
-                                                 const int* __restrict__ cand_w, const int* __restrict__ cand_h,
-                                                 const int* __restrict__ cand_y, long long* __restrict__ placements,
-                                                 int4* __restrict__ plc_by_src, unsigned char* __restrict__ accept_out,
-                                                 fa_dstat* __restrict__ st) {
-    FA_PDL_PROLOGUE();
-    __shared__ long long red[33];
-    __shared__ long long s_best;
-    int n = n_dev ? *n_dev : n_max;
-    int tid = threadIdx.x;
-    if (st->flags & (FA_DFLAG_HEIGHT_OVERFLOW | FA_DFLAG_KEY_RANGE | FA_DFLAG_DUPLICATE_MIN_TRI |
-                     FA_DFLAG_QUEUE_OVERFLOW))
-        return;
+// selection (packing.py:327-345) + placements in packing order, by one CTA;
+// red: 33 long longs of shared memory.  Array types are templated so the
+// frame's fused pack (k_pack_frame) can pass its shared-memory copies.
+template <typename OwT, typename TwT, typename RotT>
+__device__ void select_body(const OwT* ow, const TwT* tw, const TwT* th, const int* __restrict__ chart_id_i,
+                            const long long* __restrict__ chart_id, const RotT* rot, const int* perm, int n,
+                            long long omega, long long n_scales, long long min_dim, long long pad,
+                            const long long* __restrict__ cand, const long long* __restrict__ cand_p,
+                            const int* __restrict__ cand_w, const int* __restrict__ cand_h,
+                            const int* __restrict__ cand_y, int n_max, long long* __restrict__ placements,
+                            int4* __restrict__ plc_by_src, unsigned char* __restrict__ accept_out,
+                            fa_dstat* __restrict__ st, long long* red, long long* s_best) {
+    const int tid = threadIdx.x;
     if (n <= 0) {
         if (tid == 0) { st->scale_num = 1; st->scale_den = 1; st->best = -1; }
         return;
@@ -678,7 +696,7 @@ __global__ void __launch_bounds__(1024) k_select(const long long* __restrict__ o
     long long fmax = 0;
     const double rdn = 1.0 / (double)n_scales;
     for (int b = tid; b < n; b += blockDim.x) {
-        long long f = scaled_dim_rcp(ow[b], 1, n_scales, rdn, min_dim, pad);
+        long long f = scaled_dim_rcp((long long)ow[b], 1, n_scales, rdn, min_dim, pad);
         fmax = f > fmax ? f : fmax;
     }
     fmax = block_max_ll(fmax, red);
@@ -690,9 +708,9 @@ __global__ void __launch_bounds__(1024) k_select(const long long* __restrict__ o
     }
     best = block_max_ll(best, red);
     if (fmax > omega) best = 0;
-    if (tid == 0) s_best = best;
+    if (tid == 0) *s_best = best;
     __syncthreads();
-    best = s_best;
+    best = *s_best;
     if (best == 0) {
         if (tid == 0) { atomicOr(&st->flags, FA_DFLAG_PACK_FAILURE); st->best = 0; }
         return;
@@ -711,7 +729,7 @@ __global__ void __launch_bounds__(1024) k_select(const long long* __restrict__ o
         long long x = (r % FA_DIRECTION_PERIOD == 0) ? q : omega - q - w[j];
         int src = perm[j];
         long long* P = placements + 8 * (long long)j;
-        P[0] = chart_id ? chart_id[src] : src;
+        P[0] = chart_id_i ? (long long)chart_id_i[src] : (chart_id ? chart_id[src] : src);
         P[1] = x;
         P[2] = y[j];
         P[3] = w[j];
@@ -733,6 +751,27 @@ __global__ void __launch_bounds__(1024) k_select(const long long* __restrict__ o
         st->scale_den = rec[2];
         st->texels_allocated = tex;
     }
+}
+
+__global__ void __launch_bounds__(1024) k_select(const long long* __restrict__ ow, const long long* __restrict__ tw,
+                                                 const long long* __restrict__ th, const long long* __restrict__ chart_id,
+                                                 const unsigned char* __restrict__ rot, const int* __restrict__ perm,
+                                                 int n_max, const int* __restrict__ n_dev, long long omega,
+                                                 long long n_scales, long long min_dim, long long pad,
+                                                 const long long* __restrict__ cand, const long long* __restrict__ cand_p,
+                                                 const int* __restrict__ cand_w, const int* __restrict__ cand_h,
+                                                 const int* __restrict__ cand_y, long long* __restrict__ placements,
+                                                 int4* __restrict__ plc_by_src, unsigned char* __restrict__ accept_out,
+                                                 fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
+    __shared__ long long red[33];
+    __shared__ long long s_best;
+    int n = n_dev ? *n_dev : n_max;
+    if (st->flags & (FA_DFLAG_HEIGHT_OVERFLOW | FA_DFLAG_KEY_RANGE | FA_DFLAG_DUPLICATE_MIN_TRI |
+                     FA_DFLAG_QUEUE_OVERFLOW))
+        return;
+    select_body(ow, tw, th, (const int*)nullptr, chart_id, rot, perm, n, omega, n_scales, min_dim, pad, cand, cand_p,
+                cand_w, cand_h, cand_y, n_max, placements, plc_by_src, accept_out, st, red, &s_best);
 }
 
 // ---- standalone fold (packing.py:133-158) --------------------------------
@@ -921,6 +960,7 @@ void fa_launch_push_up_impl(const long long* rows, const long long* x, const lon
 }
 
 bool fa_front_in_smem(long long omega) { return front_smem(omega) <= kMaxFrontSmem; }
+
 
 // orient (packing.py:109-117): rotate boxes wider than tall
 __global__ void k_orient(const long long* __restrict__ tw, const long long* __restrict__ th, int n,
