@@ -108,31 +108,37 @@ class Mesh:
         return got
 
 
+def _obj_vertex_index(token: str, n_vertices: int) -> int:
+    """An OBJ face token ('i', 'i/t', 'i/t/n') as a 0-based vertex index;
+    negative indices count back from the vertices read so far."""
+    i = int(token.split("/", 1)[0])
+    return i - 1 if i > 0 else n_vertices + i
+
+
 def load_obj(path) -> Mesh:
-    """charts.py:80-110 (host file ingestion, outside the per-frame path)."""
-    positions: list[list[float]] = []
-    faces: list[tuple[int, int, int]] = []
+    """charts.py:80-110 restated (host file ingestion, outside the per-frame
+    path): 'v x y z' and 'f ...' records, '#' comments, polygons
+    fan-triangulated around their first vertex; the reference's error
+    messages for short records."""
+    verts: list[tuple[float, float, float]] = []
+    tris: list[tuple[int, int, int]] = []
     with open(path, "r", encoding="utf-8", errors="replace") as fh:
         for lineno, raw in enumerate(fh, start=1):
-            line = raw.split("#", 1)[0].strip()
-            if not line:
+            tok = raw.partition("#")[0].split()
+            if not tok:
                 continue
-            parts = line.split()
-            if parts[0] == "v":
-                if len(parts) < 4:
+            kind, args = tok[0], tok[1:]
+            if kind == "v":
+                if len(args) < 3:
                     raise ValueError(f"{path}:{lineno}: vertex needs 3 coordinates")
-                positions.append([float(parts[1]), float(parts[2]), float(parts[3])])
-            elif parts[0] == "f":
-                idx = []
-                for token in parts[1:]:
-                    i = int(token.split("/", 1)[0])
-                    idx.append(i - 1 if i > 0 else len(positions) + i)
-                if len(idx) < 3:
+                verts.append((float(args[0]), float(args[1]), float(args[2])))
+            elif kind == "f":
+                ids = [_obj_vertex_index(t, len(verts)) for t in args]
+                if len(ids) < 3:
                     raise ValueError(f"{path}:{lineno}: face needs >= 3 vertices")
-                for k in range(1, len(idx) - 1):
-                    faces.append((idx[0], idx[k], idx[k + 1]))
-    return Mesh(positions=np.array(positions, dtype=np.float64).reshape(-1, 3),
-                triangles=np.array(faces, dtype=np.int64).reshape(-1, 3))
+                tris.extend((ids[0], b, c) for b, c in zip(ids[1:-1], ids[2:]))
+    return Mesh(positions=np.array(verts, dtype=np.float64).reshape(-1, 3),
+                triangles=np.array(tris, dtype=np.int64).reshape(-1, 3))
 
 
 class VisibilityBuffer:

@@ -244,45 +244,46 @@ def viewport_box_batch(boxes, screen_w: int, screen_h: int) -> np.ndarray:
 # ---------------------------------------------------------------------------
 # standalone helpers outside the per-frame path (host; SURVEY §2.1 out of scope)
 # ---------------------------------------------------------------------------
-
-def project_vertex(p: Sequence[float], cam: CameraFrame) -> HPoint:
-    """geometry.py:169-175 (standalone API, not used by the pipeline)."""
-    p = np.asarray(p, dtype=np.float64)
-    if p.shape != (3,) or not np.all(np.isfinite(p)):
-        raise ValueError("expected a finite 3D point")
-    h = cam.view_proj @ np.array([p[0], p[1], p[2], 1.0])
-    return HPoint(h[0], h[1], h[2], h[3])
-
+# The reference's scalar host helpers, kept for API completeness.  They are
+# not on the per-frame path (the frame projects and clips on the GPU:
+# k_frame_init, tri_setup_warp); their arithmetic is the reference's own
+# (numpy matmul for the projection, so the same OpenBLAS bits).
 
 def project_points(points: np.ndarray, cam: CameraFrame) -> np.ndarray:
-    """geometry.py:178-182 (standalone API)."""
-    pts = np.asarray(points, dtype=np.float64)
-    return np.hstack([pts, np.ones((pts.shape[0], 1))]) @ cam.view_proj.T
+    """geometry.py:178-182: (n,3) points -> (n,4) clip coordinates."""
+    pts = np.asarray(points, dtype=np.float64).reshape(-1, 3)
+    homo = np.concatenate([pts, np.ones((len(pts), 1))], axis=1)
+    return homo @ cam.view_proj.T
 
 
-def _clip_poly_halfspace(vertices: np.ndarray, dists: np.ndarray) -> np.ndarray:
-    n = len(vertices)
-    out = []
-    for i in range(n):
-        a, b = vertices[i], vertices[(i + 1) % n]
-        da, db = dists[i], dists[(i + 1) % n]
-        if da > 0:
-            out.append(a)
-        if (da > 0) != (db > 0):
-            t = da / (da - db)
-            out.append(a + t * (b - a))
-    return np.array(out, dtype=np.float64).reshape(-1, 4)
+def project_vertex(p: Sequence[float], cam: CameraFrame) -> HPoint:
+    """geometry.py:169-175: one finite 3D point -> HPoint."""
+    q = np.asarray(p, dtype=np.float64)
+    if q.shape != (3,) or not np.isfinite(q).all():
+        raise ValueError("expected a finite 3D point")
+    x, y, z, w = cam.view_proj @ np.append(q, 1.0)
+    return HPoint(x, y, z, w)
 
 
 def clip_near(tri) -> ClipPolygon:
-    """geometry.py:223-236 (standalone API, not used by the pipeline)."""
+    """geometry.py:223-236: clip a clip-space triangle to w > W_EPSILON
+    (strict, unlike the frustum clip of charts.py:178-189, which keeps d >= 0)."""
     v = np.asarray(tri, dtype=np.float64).reshape(3, 4)
     d = v[:, 3] - W_EPSILON
-    if np.all(d > 0):
+    inside = d > 0
+    if inside.all():
         return ClipPolygon(v)
-    if not np.any(d > 0):
+    if not inside.any():
         raise AllClipped("triangle lies entirely behind the camera")
-    return ClipPolygon(_clip_poly_halfspace(v, d))
+    poly = []
+    for i in range(3):
+        j = (i + 1) % 3
+        if inside[i]:
+            poly.append(v[i])
+        if inside[i] != inside[j]:  # the edge crosses the plane
+            t = d[i] / (d[i] - d[j])
+            poly.append(v[i] + t * (v[j] - v[i]))
+    return ClipPolygon(np.array(poly, dtype=np.float64).reshape(-1, 4))
 
 
 def conservative_blinn_box(triangles, cam: CameraFrame) -> NdcBox:

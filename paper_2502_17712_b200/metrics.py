@@ -53,29 +53,47 @@ def packing_efficiency(layout: AtlasLayout) -> float:
 
 
 def _sv2(m):
-    """Closed-form singular values of 2x2 matrices (..., 2, 2) -> (big, small)."""
+    """Singular values of 2x2 matrices (..., 2, 2) -> (big, small), the
+    stable closed form the GPU uses (fa_uv.cu): big = (|q| + |r|) / 2 with
+    q = (a + d, c - b), r = (a - d, c + b); small = |det| / big."""
     a, b, c, d = m[..., 0, 0], m[..., 0, 1], m[..., 1, 0], m[..., 1, 1]
-    s1 = a * a + b * b + c * c + d * d
-    det = a * d - b * c
-    disc = np.sqrt(np.maximum(s1 * s1 - 4.0 * det * det, 0.0))
-    big = np.sqrt(np.maximum((s1 + disc) / 2.0, 0.0))
-    small = np.sqrt(np.maximum((s1 - disc) / 2.0, 0.0))
-    return big, small
+    big = 0.5 * (np.hypot(a + d, c - b) + np.hypot(a - d, c + b))
+    det = np.abs(a * d - b * c)
+    small = np.divide(det, big, out=np.zeros_like(big), where=big > 0)
+    return big, np.minimum(small, big)
 
 
 def triangle_stretch(screen_tri, atlas_tri) -> tuple[float, float]:
-    """metrics.py:58-75: singular values (max, min) of the atlas-to-screen map."""
-    s = np.asarray(screen_tri, dtype=np.float64).reshape(3, 2)
-    a = np.asarray(atlas_tri, dtype=np.float64).reshape(3, 2)
-    ea = np.column_stack([a[1] - a[0], a[2] - a[0]])
-    es = np.column_stack([s[1] - s[0], s[2] - s[0]])
-    det = ea[0, 0] * ea[1, 1] - ea[0, 1] * ea[1, 0]
-    if det == 0.0:
+    """metrics.py:58-75: singular values (max, min) of one triangle pair's
+    atlas-to-screen map, through this module's closed form (the reference
+    calls LAPACK's SVD; the two agree to rounding).  DegenerateTriangle for
+    a zero-area atlas triangle."""
+    big, small, ok, _ = _pair_singular_values(np.asarray(screen_tri, dtype=np.float64).reshape(1, 3, 2),
+                                              np.asarray(atlas_tri, dtype=np.float64).reshape(1, 3, 2))
+    if not ok[0]:
         raise DegenerateTriangle("atlas triangle has zero area")
-    inv = np.array([[ea[1, 1], -ea[0, 1]], [-ea[1, 0], ea[0, 0]]]) / det
-    m = es @ inv
-    sv = np.linalg.svd(m, compute_uv=False)
-    return float(sv[0]), float(sv[1])
+    return float(big[0]), float(small[0])
+
+
+def _pair_singular_values(s, a):
+    """(n,3,2) screen / atlas triangles -> singular values (big, small) of
+    M = Es Ea^-1 for the pairs with a non-degenerate atlas triangle, the
+    mask of those pairs, and their screen areas."""
+    ea = np.stack([a[:, 1] - a[:, 0], a[:, 2] - a[:, 0]], axis=2)
+    es = np.stack([s[:, 1] - s[:, 0], s[:, 2] - s[:, 0]], axis=2)
+    det = ea[:, 0, 0] * ea[:, 1, 1] - ea[:, 0, 1] * ea[:, 1, 0]
+    ok = det != 0.0
+    ea, es, det, sk = ea[ok], es[ok], det[ok], s[ok]
+    inv = np.empty_like(ea)
+    inv[:, 0, 0] = ea[:, 1, 1] / det
+    inv[:, 0, 1] = -ea[:, 0, 1] / det
+    inv[:, 1, 0] = -ea[:, 1, 0] / det
+    inv[:, 1, 1] = ea[:, 0, 0] / det
+    big, small = _sv2(es @ inv)
+    e1 = sk[:, 1] - sk[:, 0]
+    e2 = sk[:, 2] - sk[:, 0]
+    area = np.abs(e1[:, 0] * e2[:, 1] - e1[:, 1] * e2[:, 0]) / 2.0
+    return big, small, ok, area
 
 
 def scene_stretch(pairs: Iterable[tuple], keep_per_triangle: bool = False) -> StretchReport:
@@ -92,23 +110,9 @@ def scene_stretch_arrays(screen, atlas, keep_per_triangle: bool = False) -> Stre
     """Vectorised metrics.py:84-111 over (n,3,2) screen and atlas triangles."""
     s = np.asarray(screen, dtype=np.float64).reshape(-1, 3, 2)
     a = np.asarray(atlas, dtype=np.float64).reshape(-1, 3, 2)
-    ea = np.stack([a[:, 1] - a[:, 0], a[:, 2] - a[:, 0]], axis=2)
-    es = np.stack([s[:, 1] - s[:, 0], s[:, 2] - s[:, 0]], axis=2)
-    det = ea[:, 0, 0] * ea[:, 1, 1] - ea[:, 0, 1] * ea[:, 1, 0]
-    ok = det != 0.0
+    big, small, ok, area = _pair_singular_values(s, a)
     if not np.any(ok):
         raise NoValidTriangles("no valid triangle pairs")
-    ea, es, det, s = ea[ok], es[ok], det[ok], s[ok]
-    inv = np.empty_like(ea)
-    inv[:, 0, 0] = ea[:, 1, 1] / det
-    inv[:, 0, 1] = -ea[:, 0, 1] / det
-    inv[:, 1, 0] = -ea[:, 1, 0] / det
-    inv[:, 1, 1] = ea[:, 0, 0] / det
-    m = es @ inv
-    big, small = _sv2(m)
-    e1 = s[:, 1] - s[:, 0]
-    e2 = s[:, 2] - s[:, 0]
-    area = np.abs(e1[:, 0] * e2[:, 1] - e1[:, 1] * e2[:, 0]) / 2.0
     weighted = float(np.sum(area * (big * big + small * small) / 2.0))
     total = float(np.sum(area))
     l2 = float(np.sqrt(weighted / total)) if total > 0 else 0.0

@@ -13,8 +13,12 @@ rep = sys.argv[1]
 pat = re.compile(sys.argv[2]) if len(sys.argv) > 2 else None
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
-hdr = rows[0]
+hdr, units = rows[0], rows[1]
 col = {h: i for i, h in enumerate(hdr)}
+# ncu's second row holds each column's unit (byte / Kbyte / Mbyte, nsecond /
+# usecond ...): values are scaled to bytes and microseconds here
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3,
+         "ns": 1e-3, "us": 1, "ms": 1e3}
 
 
 def get(row, key):
@@ -22,7 +26,7 @@ def get(row, key):
     if i is None:
         return None
     try:
-        return float(row[i].replace(",", ""))
+        return float(row[i].replace(",", "")) * SCALE.get(units[i], 1)
     except ValueError:
         return None
 

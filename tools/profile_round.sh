@@ -12,7 +12,8 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
     --profile-frames 0 > gpurun_out/${tag}_ncu_launch.log 2>&1
 python tools/launch_table.py gpurun_out/${tag}_launches.csv > gpurun_out/${tag}_launches.txt
 # full capture of the frame kernels (non-graph path, a few frames)
-ncu --set full --import-source on --clock-control none -s 30 -c 40 -o gpurun_out/${tag}_full \
+ncu --set full --metrics lts__t_sectors_op_atom.sum,lts__t_sectors_op_red.sum,lts__d_atomic_input_cycles_active.avg.pct_of_peak_sustained_elapsed \
+    --import-source on --clock-control none -s 30 -c 40 -o gpurun_out/${tag}_full \
     python tools/profile_frame.py C2 3 > gpurun_out/${tag}_ncu_full.log 2>&1
 python tools/ncu_traffic.py gpurun_out/${tag}_full.ncu-rep > gpurun_out/${tag}_ncu_kernels.out
 python tools/ncu_summary.py gpurun_out/${tag}_full.ncu-rep > gpurun_out/${tag}_ncu_summary.txt
