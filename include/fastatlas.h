@@ -268,7 +268,8 @@ const char *fa_stage_name(int i);
 
 /* Work-queue counters of the last finished frame (diagnostics; valid after
  * fa_frame_finish): [small records, large records, clipped triangles,
- * generic setups, large-raster tiles, visible, charts, screen fragments].
+ * generic setups, large-raster tiles, visible, charts, screen fragments,
+ * 32-triangle clusters the setup processed (the rest culled as a whole)].
  * Returns the number written (<= max). */
 int fa_frame_counters(fa_ctx *ctx, int64_t *out, int max);
 

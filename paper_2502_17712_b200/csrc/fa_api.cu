@@ -118,7 +118,7 @@ void fa_destroy(fa_ctx* c) {
                       &c->target, &c->survived, &c->okey, &c->oidx, &c->ow, &c->oh, &c->orot, &c->sortk, &c->sortv,
                       &c->pinv, &c->cand, &c->cand_p, &c->cand_w, &c->cand_h, &c->cand_y, &c->rowstart,
                       &c->placements, &c->uv, &c->vp_dev, &c->blocks, &c->dstat, &c->aux, &c->in_tw, &c->in_th,
-                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list, &c->hiz, &c->wid, &c->vis_chart, &c->vis_cidx, &c->plc_c, &c->pos_perm, &c->tris_perm, &c->vperm_buf, &c->vis_tris, &c->vslot, &c->vlist, &c->vuv, &c->vblocks, &c->pstat};
+                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list, &c->hiz, &c->wid, &c->vis_chart, &c->vis_cidx, &c->plc_c, &c->pos_perm, &c->tris_perm, &c->vperm_buf, &c->vis_tris, &c->vslot, &c->vlist, &c->vuv, &c->vblocks, &c->pstat, &c->tperm_buf, &c->tris_sorted_buf, &c->clusters_buf, &c->live_buf};
     for (fa_buf* b : bufs) free_buf(*b);
     for (cudaEvent_t e : c->fj)
         if (e) cudaEventDestroy(e);
@@ -145,39 +145,75 @@ int fa_set_mesh(fa_ctx* ctx, const double* positions, int64_t n_vertices, const 
     ctx->pos = ctx->pos_user = nullptr;
     ctx->tris = nullptr;
     ctx->vperm = nullptr;
+    ctx->tperm = nullptr;
+    ctx->tris_sorted = nullptr;
+    ctx->clusters = nullptr;
     ctx->V = ctx->T = 0;
     ctx->gen++;  // any captured frame graph refers to the previous mesh
     if (n_triangles > 0) {
-        // index range check (Mesh.__post_init__, charts.py:45-48) and the
-        // first use of every vertex, on the device; renumbering in order of
-        // first use (fa_mesh.cu) unless FASTATLAS_VERTEX_ORDER=0
+        // On the device (fa_mesh.cu): the index range check (Mesh.__post_init__,
+        // charts.py:45-48); the raster setup's triangle order (Morton order of
+        // the centroids, FASTATLAS_TRI_ORDER=0: the given order); the vertices
+        // renumbered in order of first use along that order
+        // (FASTATLAS_VERTEX_ORDER=0: kept); the per-cluster culling data.
         CK(cudaSetDevice(ctx->device));
         const bool renumber = fa_env_int("FASTATLAS_VERTEX_ORDER", 1) != 0;
-        fa_buf first, scratch;
+        const bool order = fa_env_int("FASTATLAS_TRI_ORDER", 1) != 0;
+        const long long T = n_triangles;
+        const int V = (int)n_vertices;
+        fa_buf first, scratch, sort_scratch, tris_s;
         const size_t vb = (size_t)(n_vertices > 0 ? n_vertices : 1) * 4;
         bool ok = fa_ensure(ctx, first, vb) &&
-                  fa_ensure(ctx, scratch, (size_t)fa_mesh_scratch_ints(n_vertices, n_triangles) * 4 + vb + 16);
-        if (renumber && ok) {
-            ok = fa_ensure(ctx, ctx->tris_perm, (size_t)n_triangles * 12) &&
-                 fa_ensure(ctx, ctx->vperm_buf, vb) && fa_ensure(ctx, ctx->pos_perm, (size_t)n_vertices * 24 + 8);
+                  fa_ensure(ctx, scratch, (size_t)fa_mesh_scratch_ints(n_vertices, T) * 4 + vb + 16) &&
+                  fa_ensure(ctx, ctx->clusters_buf, (size_t)((T + 31) / 32) * sizeof(fa_cluster)) &&
+                  fa_ensure(ctx, ctx->tris_sorted_buf, (size_t)T * 12) && fa_ensure(ctx, ctx->tperm_buf, (size_t)T * 4);
+        if (ok && order) ok = fa_ensure(ctx, sort_scratch, fa_mesh_sort_scratch_bytes(T)) && fa_ensure(ctx, tris_s, (size_t)T * 12);
+        if (ok && renumber) {
+            ok = fa_ensure(ctx, ctx->tris_perm, (size_t)T * 12) && fa_ensure(ctx, ctx->vperm_buf, vb) &&
+                 fa_ensure(ctx, ctx->pos_perm, (size_t)n_vertices * 24 + 8);
         }
         if (!ok) {
             free_buf(first);
             free_buf(scratch);
+            free_buf(sort_scratch);
+            free_buf(tris_s);
             return set_err(FA_CUDA_ERROR, "out of device memory binding the mesh");
         }
         cudaStream_t s = nullptr;
         int* bad = P<int>(scratch);
-        fa_launch_mesh_validate(triangles, n_triangles, (int)n_vertices, P<int>(first), bad, s);
-        if (renumber)
-            fa_launch_mesh_renumber(positions, triangles, n_triangles, (int)n_vertices, P<int>(first), bad + 1,
-                                    P<int>(scratch) + 1 + fa_mesh_scratch_ints(n_vertices, n_triangles),
-                                    P<int>(ctx->tris_perm), P<int>(ctx->vperm_buf), P<double>(ctx->pos_perm), s);
+        int* newidx = P<int>(scratch) + 1 + fa_mesh_scratch_ints(n_vertices, T);
+        fa_launch_mesh_validate(triangles, T, V, P<int>(first), bad, s);
         int hbad = 0;
         cudaError_t e = cudaGetLastError();
         if (e == cudaSuccess) e = cudaMemcpy(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess && !hbad) {
+            // setup order: sorted slot -> triangle (user vertex ids)
+            const int* tri_src = triangles;  // triangles in setup order
+            if (order) {
+                fa_launch_mesh_order(positions, triangles, (int)T, V, sort_scratch.p, P<int>(ctx->tperm_buf),
+                                     P<int>(tris_s), s);
+                tri_src = P<int>(tris_s);
+            }
+            const double* pos_k = positions;
+            if (renumber) {
+                // first use along the setup order, then both triangle arrays remapped
+                fa_launch_mesh_validate(tri_src, T, V, P<int>(first), bad, s);
+                fa_launch_mesh_renumber(positions, tri_src, T, V, P<int>(first), bad + 1, newidx,
+                                        P<int>(ctx->tris_sorted_buf), P<int>(ctx->vperm_buf), P<double>(ctx->pos_perm),
+                                        s);
+                fa_launch_mesh_remap(triangles, T, newidx, P<int>(ctx->tris_perm), s);
+                pos_k = P<double>(ctx->pos_perm);
+            } else {
+                cudaMemcpyAsync(ctx->tris_sorted_buf.p, tri_src, (size_t)T * 12, cudaMemcpyDeviceToDevice, s);
+            }
+            fa_launch_cluster_build(pos_k, P<int>(ctx->tris_sorted_buf), (int)T, P<fa_cluster>(ctx->clusters_buf), s);
+            e = cudaGetLastError();
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        }
         free_buf(first);
         free_buf(scratch);
+        free_buf(sort_scratch);
+        free_buf(tris_s);
         if (e != cudaSuccess) return set_err(FA_CUDA_ERROR, "fa_set_mesh: %s", cudaGetErrorString(e));
         if (hbad) return set_err(FA_VALUE_ERROR, "triangle index out of range");
         if (renumber) {
@@ -185,6 +221,9 @@ int fa_set_mesh(fa_ctx* ctx, const double* positions, int64_t n_vertices, const 
             ctx->tris = P<int>(ctx->tris_perm);
             ctx->vperm = P<int>(ctx->vperm_buf);
         }
+        ctx->tperm = order ? P<int>(ctx->tperm_buf) : nullptr;
+        ctx->tris_sorted = P<int>(ctx->tris_sorted_buf);
+        ctx->clusters = P<fa_cluster>(ctx->clusters_buf);
     }
     if (!ctx->tris) {
         ctx->pos = positions;
@@ -242,6 +281,7 @@ static int ensure_raster(fa_ctx* ctx, int W, int H, bool depth) {
     ENSURE(tiles, (size_t)ctx->max_tiles * sizeof(int4));
     ENSURE(dstat, sizeof(fa_dstat));
     ENSURE(vp_dev, 16 * sizeof(double));
+    ENSURE(live_buf, (size_t)((T + 31) / 32 + 1) * 4);
     return FA_OK;
 }
 
@@ -360,17 +400,46 @@ static int upload_vp(fa_ctx* ctx, const double* vp_host, cudaStream_t s) {
     return FA_OK;
 }
 
+// the setup order + cluster culling of the bound mesh (vc: the view
+// constants k_frame_init writes each frame)
+static fa_setup_order setup_order(fa_ctx* ctx) {
+    fa_setup_order o{};
+    o.tperm = ctx->tperm;
+    o.tris_sorted = ctx->tris_sorted;
+    if (ctx->clusters && ctx->live_buf.p && fa_env_int("FASTATLAS_CLUSTER_CULL", 1)) {
+        o.live = P<int>(ctx->live_buf);
+        o.n_live = &P<fa_dstat>(ctx->dstat)->n_live;
+    }
+    return o;
+}
+
+// k_frame_init's cluster culling for setup_order's live list
+static fa_cull_args cull_args(fa_ctx* ctx, int cull) {
+    fa_cull_args c{};
+    if (ctx->clusters && ctx->live_buf.p && fa_env_int("FASTATLAS_CLUSTER_CULL", 1)) {
+        c.clusters = ctx->clusters;
+        c.n_clusters = (int)((ctx->T + 31) / 32);
+        c.cull = cull;
+        c.live = P<int>(ctx->live_buf);
+        c.st = P<fa_dstat>(ctx->dstat);
+    }
+    return c;
+}
+
 // depth pass (shared by fa_depth_prepass and the frame)
 static int launch_depth(fa_ctx* ctx, int W, int H, int cull, unsigned char* flags_out, cudaStream_t s, int& nl) {
     int T = (int)ctx->T, V = (int)ctx->V;
+    const fa_setup_order ord = setup_order(ctx);
+    fa_launch_cluster_cull(P<double>(ctx->vp_dev), W, H, cull_args(ctx, cull), s);
     fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), P<double4>(ctx->scr), W, H,
                          P<int>(ctx->vmin), P<unsigned long long>(ctx->depth_keys), nullptr, (long long)W * H,
                          flags_out, T, s);
+    if (ord.live) nl += 1;
     nl += 1 + fa_launch_depth_pass(true, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, W, H, cull,
                                    P<unsigned long long>(ctx->depth_keys), nullptr, P<SmallRec>(ctx->small_rec),
                                    P<int>(ctx->clip_list), P<TriSetup>(ctx->large), ctx->max_large,
                                    P<int4>(ctx->tiles), ctx->max_tiles, P<fa_dstat>(ctx->dstat), s, nullptr, nullptr,
-                                   nullptr, nullptr, nullptr);
+                                   nullptr, nullptr, nullptr, nullptr, ord);
     return FA_OK;
 }
 
@@ -554,13 +623,15 @@ int fa_mark_visible(fa_ctx* ctx, const double* vp_host, const double* depth, int
         CK(cudaMemsetAsync(ctx->dstat.p, 0, sizeof(fa_dstat), s));
         r = upload_vp(ctx, vp_host, s);
         if (r) return r;
+        const fa_setup_order ord = setup_order(ctx);
+        fa_launch_cluster_cull(P<double>(ctx->vp_dev), width, height, cull_args(ctx, backface_cull), s);
         fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), P<double4>(ctx->scr), width,
                              height, nullptr, nullptr, nullptr, 0, P<unsigned char>(ctx->flags), T, s);
         fa_launch_encode_depth(depth, P<unsigned long long>(ctx->depth_keys), (long long)width * height, s);
         fa_launch_depth_pass(false, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, width, height,
                              backface_cull, nullptr, nullptr, P<SmallRec>(ctx->small_rec), P<int>(ctx->clip_list),
                              P<TriSetup>(ctx->large), ctx->max_large, P<int4>(ctx->tiles), ctx->max_tiles,
-                             P<fa_dstat>(ctx->dstat), s, nullptr, nullptr, nullptr, nullptr, nullptr);
+                             P<fa_dstat>(ctx->dstat), s, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, ord);
         fa_launch_depth_hiz(P<unsigned long long>(ctx->depth_keys), nullptr, width, height,
                             P<unsigned long long>(ctx->hiz), nullptr, nullptr, s);
         fa_launch_raster_vis(P<SmallRec>(ctx->small_rec), P<TriSetup>(ctx->large), P<int4>(ctx->tiles),
@@ -955,9 +1026,11 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
                          (long long)W * H, nullptr, T, ctx->side,
                          fa_env_int("FASTATLAS_CLEAR_BLOCKS", FA_NUM_SMS));  // a slice of the GPU: the setup keeps the rest
     CK(cudaEventRecord(ctx->fj[10], ctx->side));
+    const fa_setup_order ord = setup_order(ctx);
+    fa_launch_cluster_cull(P<double>(ctx->vp_dev), W, H, cull_args(ctx, p->backface_cull), s);
     fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), P<double4>(ctx->scr), W, H,
                          P<int>(ctx->vmin), nullptr, nullptr, 0, flags, T, s);
-    nl += 2;
+    nl += ord.live ? 3 : 2;
     mark();  // 1: project + clears
     nl += fa_launch_depth_pass(true, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, W, H,
                                p->backface_cull, P<unsigned long long>(ctx->depth_keys), wid,
@@ -965,7 +1038,7 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
                                ctx->max_large, P<int4>(ctx->tiles), ctx->max_tiles, st, s,
                                fa_env_int("FASTATLAS_DEPTH_BRANCHES", 3) >= 2 ? ctx->side : nullptr,
                                fa_env_int("FASTATLAS_DEPTH_BRANCHES", 3) >= 3 ? ctx->side2 : nullptr,
-                               ctx->fj[0], ctx->fj[1], ctx->fj[7], ctx->fj[10]);
+                               ctx->fj[0], ctx->fj[1], ctx->fj[7], ctx->fj[10], ord);
     fa_launch_depth_hiz(P<unsigned long long>(ctx->depth_keys), wid, W, H, P<unsigned long long>(ctx->hiz), flags, st,
                         s);
     nl += 1;
@@ -1263,9 +1336,9 @@ int fa_last_launch_count(fa_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
 int fa_frame_counters(fa_ctx* ctx, int64_t* out, int max) {
     if (!ctx || !out || !ctx->hstat) return 0;
     const fa_dstat* h = ctx->hstat;
-    const int64_t v[8] = {h->n_small3, h->n_large3, h->n_clip, h->n_large, h->n_tiles, h->n_vis, h->n_charts,
-                          h->screen_fragments};
-    int n = max < 8 ? max : 8;
+    const int64_t v[9] = {h->n_small3, h->n_large3, h->n_clip, h->n_large, h->n_tiles, h->n_vis, h->n_charts,
+                          h->screen_fragments, h->n_live};
+    int n = max < 9 ? max : 9;
     for (int i = 0; i < n; i++) out[i] = v[i];
     return n;
 }

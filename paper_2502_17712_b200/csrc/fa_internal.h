@@ -9,6 +9,42 @@
 struct TriSetup;
 struct SmallRec;
 
+// Culling data of 32 consecutive triangles of the setup order (fa_mesh.cu)
+struct fa_cluster {
+    double c[3], r;        // bounding sphere
+    double a[3];           // normal cone axis (unit)
+    double cos_t, sin_t;   // cone half angle (widened for rounding)
+    double amin;           // smallest triangle area (0: never back-face culled)
+};
+
+// The raster setup's triangle order and cluster culling data (fa_set_mesh);
+// all null: the given order, no culling
+struct fa_setup_order {
+    const int* tperm;
+    const int* tris_sorted;
+    const int* live;    // live clusters (k_frame_init), or null: every slot
+    const int* n_live;
+};
+
+// k_frame_init's cluster culling (clusters null: none)
+struct fa_cull_args {
+    const fa_cluster* clusters;
+    int n_clusters;
+    int cull;
+    int* live;
+    fa_dstat* st;
+};
+
+// Per-frame view constants derived from the camera matrix (k_frame_init)
+struct fa_view_consts {
+    double plane[7][4];    // L, R, B, T, N, F (w +- x, y, z) and w - W_EPSILON, as rows over (x, y, z, 1)
+    double pn[7];          // |plane normal|
+    double cam[3];         // projection centre (x = y = w = 0)
+    double sigma;          // sign of det([VP_x; VP_y; VP_w] 3x3); 0 disables back-face culling
+    double area_k;         // W * H / 4 * |det3|
+    double tau;            // screen area (px^2) above any rounding of the reference's shoelace
+};
+
 // growable device buffer
 struct fa_buf {
     void* p = nullptr;
@@ -44,6 +80,13 @@ struct fa_ctx {
     const int* vperm = nullptr;
     int64_t V = 0, T = 0;
     fa_buf pos_perm, tris_perm, vperm_buf;
+    // the raster setup's order: Morton order of the triangle centroids
+    // (tperm[slot] = triangle id, tris_sorted = its renumbered vertex
+    // indices) and the culling data of each 32-slot cluster
+    const int* tperm = nullptr;
+    const int* tris_sorted = nullptr;
+    const fa_cluster* clusters = nullptr;
+    fa_buf tperm_buf, tris_sorted_buf, clusters_buf, live_buf;
 
     // scratch (grown on demand)
     fa_buf small_rec, clip, depth_keys, depth_f64, flags, vis_list, large, tiles, label, vmin, v2c, cidx;
@@ -97,13 +140,16 @@ bool fa_ensure(fa_ctx* ctx, fa_buf& b, size_t bytes);
 void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* clip, double4* scr, int W, int H,
                           int* vmin, unsigned long long* depth, unsigned long long* wid, long long npx,
                           unsigned char* flags, int T, cudaStream_t s, int max_blocks = 0);
+// the setup's live-cluster list (no-op when cu.clusters is null)
+void fa_launch_cluster_cull(const double* vp, int W, int H, const fa_cull_args& cu, cudaStream_t s);
 // side == nullptr: everything on s; otherwise fork/join through the events.
 // Both return the number of kernels launched.  wid: see depth_min (may be null).
 int fa_launch_depth_pass(bool write_depth, const double4* clip, const double4* scr, const int* tris, int T, int W,
                          int H, int cull, unsigned long long* depth, unsigned long long* wid, SmallRec* small_rec,
                          int* clip_list, TriSetup* large, int max_large, int4* tiles, int max_tiles, fa_dstat* st,
                          cudaStream_t s, cudaStream_t side, cudaStream_t side2, cudaEvent_t ev_fork,
-                         cudaEvent_t ev_join, cudaEvent_t ev_join2, cudaEvent_t ev_clear = nullptr);
+                         cudaEvent_t ev_join, cudaEvent_t ev_join2, cudaEvent_t ev_clear = nullptr,
+                         fa_setup_order ord = fa_setup_order{});
 int fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const int4* tiles, int max_tiles,
                          int max_large, int T, int W, const unsigned long long* depth, const unsigned long long* hiz,
                          unsigned char* flags, int* vis_queue, fa_dstat* st, cudaStream_t s, cudaStream_t side,
@@ -159,6 +205,12 @@ int fa_mesh_scratch_ints(long long V, long long T);
 void fa_launch_mesh_validate(const int* tris, long long T, int V, int* first, int* bad, cudaStream_t s);
 void fa_launch_mesh_renumber(const double* pos, const int* tris, long long T, int V, const int* first, int* scratch,
                              int* newidx, int* tris_out, int* perm, double* pos_out, cudaStream_t s);
+
+size_t fa_mesh_sort_scratch_bytes(long long T);
+void fa_launch_mesh_order(const double* pos, const int* tris, int T, int V, void* scratch, int* order,
+                          int* tris_sorted, cudaStream_t s);
+void fa_launch_mesh_remap(const int* tris, long long T, const int* newidx, int* out, cudaStream_t s);
+void fa_launch_cluster_build(const double* pos, const int* tris_sorted, int T, fa_cluster* out, cudaStream_t s);
 
 // ---- bounds (fa_bounds.cu) -----------------------------------------------
 void fa_launch_chart_bounds(const double4* clip, const int* tris, const int* vis_list, const int* label,

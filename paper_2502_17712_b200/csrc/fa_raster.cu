@@ -96,6 +96,35 @@ __global__ void k_frame_init(const double* __restrict__ pos, int V, const double
         for (long long i = i0; i < nflag32; i += stride) flags32[i] = 0u;
 }
 
+// The setup's live clusters: those not culled as a whole (cluster_culled:
+// outside the frustum or facing away -> no samples).  Their order does not
+// matter (every output is keyed by triangle id).  Independent of the
+// projection, so it runs beside it.
+__global__ void __launch_bounds__(256) k_cluster_cull(const double* __restrict__ vp_dev, int W, int H, fa_cull_args cu) {
+    FA_PDL_PROLOGUE();
+    __shared__ fa_view_consts s_vc;
+    if (threadIdx.x == 0) {
+        double m[16];
+        for (int i = 0; i < 16; i++) m[i] = vp_dev[i];
+        compute_view_consts(m, W, H, &s_vc);
+    }
+    __syncthreads();
+    const long long n_pad = ((long long)cu.n_clusters + 31) & ~31ll;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n_pad; c += (long long)gridDim.x * blockDim.x) {
+        const bool live = c < cu.n_clusters && !cluster_culled(cu.clusters[c], s_vc, cu.cull != 0);
+        const unsigned mk = __ballot_sync(0xffffffffu, live);
+        int base = 0;
+        if (lane_id() == 0 && mk) base = atomicAdd(&cu.st->n_live, __popc(mk));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (live) cu.live[base + __popc(mk & ((1u << lane_id()) - 1u))] = (int)c;
+    }
+}
+
+void fa_launch_cluster_cull(const double* vp, int W, int H, const fa_cull_args& cu, cudaStream_t s) {
+    if (!cu.clusters) return;
+    fa_launch(k_cluster_cull, fa_grid(cu.n_clusters, 256, FA_NUM_SMS), 256, 0, s, vp, W, H, cu);
+}
+
 // keys -> float64 depth (debug / standalone depth_prepass output)
 __global__ void k_decode_depth(const unsigned long long* __restrict__ keys, double* __restrict__ out, long long n) {
     FA_PDL_PROLOGUE();
@@ -128,7 +157,7 @@ __global__ void __launch_bounds__(SETUP_WARPS * 32) k_raster_setup(const double4
                                                       int T, int W, int H, int cull,
                                                       SmallRec* __restrict__ recs, int* __restrict__ clip_list,
                                                       int4* __restrict__ tiles, int max_tiles,
-                                                      fa_dstat* __restrict__ st) {
+                                                      fa_dstat* __restrict__ st, fa_setup_order ord) {
     FA_PDL_PROLOGUE();
     // per-warp counts -> per-warp bases; one atomic per counter per block step
     // (a same-address atomic per warp serialises ~30K times in the L2)
@@ -137,23 +166,39 @@ __global__ void __launch_bounds__(SETUP_WARPS * 32) k_raster_setup(const double4
     const int lane = lane_id(), warp = threadIdx.x >> 5;
     const bool rec_ok = W <= 32767 && H <= 32767;
     const unsigned lt_mask = (1u << lane) - 1u;
-    const int step = gridDim.x * SETUP_WARPS * 32;
     // the next step's vertex indices are loaded one step ahead, so each step
     // waits for one round trip (the screen-record gathers), not two
-    int na = 0, nb = 0, nc = 0;
-    {
-        const int t0 = blockIdx.x * SETUP_WARPS * 32 + warp * 32 + lane;
-        if (t0 < T) na = __ldg(tris + 3 * t0), nb = __ldg(tris + 3 * t0 + 1), nc = __ldg(tris + 3 * t0 + 2);
+    // slots walk the setup order (fa_mesh.cu: Morton order of the centroids,
+    // 32-slot clusters); t is the slot's triangle id
+    // With a live-cluster list (k_frame_init: clusters outside the frustum
+    // or facing away dropped) a warp step is one live cluster; otherwise 32
+    // consecutive slots.  t is the slot's triangle id.
+    const int* ts = ord.tris_sorted ? ord.tris_sorted : tris;
+    const int* live = ord.live;
+    const int n_items = live ? *ord.n_live : (T + 31) >> 5;  // warp items (32 slots each)
+    const int istep = gridDim.x * SETUP_WARPS;
+    auto slot_of = [&](int item) -> int {
+        if (item >= n_items) return T;
+        return (live ? __ldg(live + item) : item) * 32 + lane;
+    };
+    int nslot = slot_of(blockIdx.x * SETUP_WARPS + warp);
+    int na = 0, nb = 0, nc = 0, nt_id = T;
+    if (nslot < T) {
+        na = __ldg(ts + 3 * nslot), nb = __ldg(ts + 3 * nslot + 1), nc = __ldg(ts + 3 * nslot + 2);
+        nt_id = ord.tperm ? __ldg(ord.tperm + nslot) : nslot;
     }
-    for (int bbase = blockIdx.x * SETUP_WARPS * 32; bbase < T; bbase += step) {
-        const int t = bbase + warp * 32 + lane;
-        const int ia = na, ib = nb, ic = nc;
-        if (t + step < T)
-            na = __ldg(tris + 3 * (t + step)), nb = __ldg(tris + 3 * (t + step) + 1), nc = __ldg(tris + 3 * (t + step) + 2);
+    for (int ibase = blockIdx.x * SETUP_WARPS; ibase < n_items; ibase += istep) {
+        const int slot = nslot;
+        const int ia = na, ib = nb, ic = nc, t = nt_id;
+        nslot = slot_of(ibase + istep + warp);
+        if (nslot < T) {
+            na = __ldg(ts + 3 * nslot), nb = __ldg(ts + 3 * nslot + 1), nc = __ldg(ts + 3 * nslot + 2);
+            nt_id = ord.tperm ? __ldg(ord.tperm + nslot) : nslot;
+        }
         Setup3 f;
         int kind = 0;  // 0 none, 1 small record, 2 large record, 3 generic path
         int nt = 0;
-        if (t < T) {
+        if (slot < T) {
             int r3 = tri_setup3s(scr, ia, ib, ic, W, H, cull != 0, f);
             if (r3 == 2 || (r3 == 1 && !rec_ok)) {
                 kind = 3;
@@ -474,7 +519,7 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const SmallRec* __re
 // (RED.MIN.64 per covered sample).
 #define COOP_WARPS 4
 #ifndef COOP_MIN_BLOCKS
-#define COOP_MIN_BLOCKS 5
+#define COOP_MIN_BLOCKS 6
 #endif
 struct CoopWarp {
     SmallRec rec[2][32];  // double buffer: the next 32 records stream in (cp.async) during the current ones
@@ -865,9 +910,9 @@ int fa_launch_depth_pass(bool write_depth, const double4* clip, const double4* s
                          int H, int cull, unsigned long long* depth, unsigned long long* wid, SmallRec* small_rec,
                          int* clip_list, TriSetup* large, int max_large, int4* tiles, int max_tiles, fa_dstat* st,
                          cudaStream_t s, cudaStream_t side, cudaStream_t side2, cudaEvent_t ev_fork,
-                         cudaEvent_t ev_join, cudaEvent_t ev_join2, cudaEvent_t ev_clear) {
+                         cudaEvent_t ev_join, cudaEvent_t ev_join2, cudaEvent_t ev_clear, fa_setup_order ord) {
     fa_launch(k_raster_setup, fa_grid(T, SETUP_WARPS * 32, FA_NUM_SMS * (32 / SETUP_WARPS)), SETUP_WARPS * 32, 0, s, scr, tris, T, W, H, cull, small_rec,
-              clip_list, tiles, max_tiles, st);
+              clip_list, tiles, max_tiles, st, ord);
     // the depth/winner clears ran beside the setup: every raster branch
     // (forked from here) needs them
     if (ev_clear) cudaStreamWaitEvent(s, ev_clear, 0);

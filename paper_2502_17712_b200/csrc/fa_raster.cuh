@@ -239,6 +239,87 @@ __device__ __forceinline__ int tri_setup(const double4* __restrict__ clip, const
     return 1;
 }
 
+// ---- cluster culling (k_raster_setup) -------------------------------------
+// Whole 32-triangle clusters of the setup order (fa_mesh.cu) whose triangles
+// would all yield no samples are skipped before any vertex is gathered:
+//  * outside: the bounding sphere lies beyond a frustum plane (or behind
+//    w = W_EPSILON) by a margin far above the rounding of the reference's
+//    clip coordinates, so every vertex fails that plane and clipping
+//    (charts.py:160-189) leaves nothing -- clipped vertices are convex
+//    combinations, still outside;
+//  * back-facing (cull on, sphere strictly inside every plane, so no triangle
+//    is clipped): for w_i > 0 the reference's shoelace is
+//        area2 = W*H/4 * (-det3 * V) / (w0 w1 w2),  V = ((p1-p0) x (p2-p0)) . (C - p0),
+//    C the projection centre, det3 = det of the x, y, w rows' 3x3 block.  The
+//    normal cone and sphere bound sigma*V below by 2 * amin * g, g > 0, so
+//    area2 < -area_k * 2 amin g / wmax^3; the cluster is culled only when that
+//    bound exceeds tau (1e-6 px^2 + 1e-13 W H), far above the rounding of the
+//    reference's area (charts.py:213-218 culls area2 < 0).
+__device__ __forceinline__ bool cluster_culled(const fa_cluster& cl, const fa_view_consts& vc, bool cull) {
+    const double cx = cl.c[0], cy = cl.c[1], cz = cl.c[2], r = cl.r;
+    bool inside = true;
+#pragma unroll
+    for (int k = 0; k < 7; k++) {
+        const double* P = vc.plane[k];
+        const double dc = P[0] * cx + P[1] * cy + P[2] * cz + P[3];
+        const double nr = vc.pn[k] * r;
+        const double m = 1e-9 * (vc.pn[k] * (fabs(cx) + fabs(cy) + fabs(cz) + r) + fabs(P[3]));
+        if (dc + nr < -m) return true;  // (NaN compares false: never culled)
+        if (!(dc - nr > m)) inside = false;
+    }
+    if (!cull || !inside || !(cl.amin > 0) || vc.sigma == 0) return false;
+    const double vx = vc.sigma * (vc.cam[0] - cx), vy = vc.sigma * (vc.cam[1] - cy), vz = vc.sigma * (vc.cam[2] - cz);
+    const double vl = sqrt(vx * vx + vy * vy + vz * vz);
+    if (!(vl > 0)) return false;
+    const double cphi = (cl.a[0] * vx + cl.a[1] * vy + cl.a[2] * vz) / vl;
+    const double sphi = sqrt(fmax(0.0, 1.0 - cphi * cphi));
+    const double g = vl * (cphi * cl.cos_t - sphi * cl.sin_t) - r - 1e-9 * (vl + r);
+    if (!(g > 0)) return false;
+    const double* Pw = vc.plane[6];  // w - W_EPSILON
+    const double wmax = Pw[0] * cx + Pw[1] * cy + Pw[2] * cz + Pw[3] + FA_W_EPSILON + vc.pn[6] * r;
+    const double bound = vc.area_k * 2.0 * cl.amin * g / (wmax * wmax * wmax);
+    return bound > vc.tau;
+}
+
+// view constants of the camera matrix m (row-major VP), screen W x H
+__device__ __forceinline__ void compute_view_consts(const double* m, int W, int H, fa_view_consts* vc) {
+    const double* X = m;
+    const double* Y = m + 4;
+    const double* Z = m + 8;
+    const double* Wr = m + 12;
+    for (int k = 0; k < 4; k++) {
+        vc->plane[0][k] = Wr[k] + X[k];
+        vc->plane[1][k] = Wr[k] - X[k];
+        vc->plane[2][k] = Wr[k] + Y[k];
+        vc->plane[3][k] = Wr[k] - Y[k];
+        vc->plane[4][k] = Wr[k] + Z[k];
+        vc->plane[5][k] = Wr[k] - Z[k];
+        vc->plane[6][k] = Wr[k];
+    }
+    vc->plane[6][3] = Wr[3] - FA_W_EPSILON;
+    for (int q = 0; q < 7; q++)
+        vc->pn[q] = sqrt(vc->plane[q][0] * vc->plane[q][0] + vc->plane[q][1] * vc->plane[q][1] +
+                         vc->plane[q][2] * vc->plane[q][2]);
+    // projection centre: X.C + X3 = Y.C + Y3 = W.C + W3 = 0 (Cramer)
+    const double a00 = X[0], a01 = X[1], a02 = X[2], a10 = Y[0], a11 = Y[1], a12 = Y[2], a20 = Wr[0], a21 = Wr[1],
+                 a22 = Wr[2];
+    const double det3 = a00 * (a11 * a22 - a12 * a21) - a01 * (a10 * a22 - a12 * a20) + a02 * (a10 * a21 - a11 * a20);
+    const double b0 = -X[3], b1 = -Y[3], b2 = -Wr[3];
+    const double s = sqrt(a00 * a00 + a01 * a01 + a02 * a02) * sqrt(a10 * a10 + a11 * a11 + a12 * a12) *
+                     sqrt(a20 * a20 + a21 * a21 + a22 * a22);
+    if (!(fabs(det3) > 1e-9 * s)) {
+        vc->sigma = 0.0;  // degenerate projection: no back-face culling
+        vc->cam[0] = vc->cam[1] = vc->cam[2] = 0.0;
+    } else {
+        vc->sigma = det3 > 0 ? 1.0 : -1.0;
+        vc->cam[0] = (b0 * (a11 * a22 - a12 * a21) - a01 * (b1 * a22 - a12 * b2) + a02 * (b1 * a21 - a11 * b2)) / det3;
+        vc->cam[1] = (a00 * (b1 * a22 - a12 * b2) - b0 * (a10 * a22 - a12 * a20) + a02 * (a10 * b2 - b1 * a20)) / det3;
+        vc->cam[2] = (a00 * (a11 * b2 - b1 * a21) - a01 * (a10 * b2 - b1 * a20) + b0 * (a10 * a21 - a11 * a20)) / det3;
+    }
+    vc->area_k = (double)W * (double)H * 0.25 * fabs(det3);
+    vc->tau = 1e-6 + 1e-13 * (double)W * (double)H;
+}
+
 // ---- warp-parallel tri_setup (the clipping path) ---------------------------
 // Same operations on the same values as tri_setup (so the same bits), with
 // polygon vertex i on lane i: each Sutherland-Hodgman step (charts.py:

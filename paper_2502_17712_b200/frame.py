@@ -197,12 +197,12 @@ class FrameEngine:
         return int(self.ctx.L.fa_last_launch_count(self.ctx.h))
 
     COUNTERS = ("small_records", "large_records", "clipped", "generic_setups", "tiles", "visible", "charts",
-                "screen_fragments")
+                "screen_fragments", "live_clusters")
 
     def counters(self) -> dict:
         """Work-queue counters of the last finished frame (fa_frame_counters)."""
-        buf = (ctypes.c_int64 * 8)()
-        n = self.ctx.L.fa_frame_counters(self.ctx.h, buf, 8)
+        buf = (ctypes.c_int64 * 9)()
+        n = self.ctx.L.fa_frame_counters(self.ctx.h, buf, 9)
         return {self.COUNTERS[i]: int(buf[i]) for i in range(n)}
 
     def stage_times(self) -> dict:
