@@ -17,5 +17,8 @@ ncu --set full --metrics lts__t_sectors_op_atom.sum,lts__t_sectors_op_red.sum,lt
     python tools/profile_frame.py C2 3 > gpurun_out/${tag}_ncu_full.log 2>&1
 python tools/ncu_traffic.py gpurun_out/${tag}_full.ncu-rep > gpurun_out/${tag}_ncu_kernels.out
 python tools/ncu_summary.py gpurun_out/${tag}_full.ncu-rep > gpurun_out/${tag}_ncu_summary.txt
+python tools/bench_configs.py gpurun_out/${tag}_configs.json > gpurun_out/${tag}_configs.log 2>&1
+python tools/set_mesh_time.py C3 5 > gpurun_out/${tag}_set_mesh.txt 2>&1
+python tools/frame_counters.py C2 4 > gpurun_out/${tag}_counters.txt 2>&1
 tail -3 gpurun_out/${tag}_launches.txt
 cat gpurun_out/${tag}_ncu_summary.txt | head -40
