@@ -58,9 +58,8 @@ struct fa_dstat {
     double stretch_wsum;  // sum area * (S1^2 + S2^2) / 2   (metrics.py:103)
     double stretch_area;  // sum area                       (metrics.py:104)
     unsigned long long stretch_linf_bits;  // max S1 (positive double bits)
-    int n_live;           // 32-triangle clusters the setup processes (k_cluster_cull)
-    unsigned int pack_done;  // candidate CTAs finished (k_pack's fused selection)
-    int pad0[34];
+    int n_live;           // 32-triangle clusters the setup processes (k_frame_init's cluster culling)
+    int pad0[35];
     int n_small3;         // stored small-triangle records (pass 2 input)
     int pad1[63];
     int n_large3;         // compact large-triangle records (stored from the back of the record array)

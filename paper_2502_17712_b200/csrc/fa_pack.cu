@@ -619,6 +619,62 @@ __device__ bool pack_candidate(const DimT* __restrict__ ow, const DimT* __restri
 // cand record: [accept, num, den, used, slot]
 #define CAND_REC FA_CAND_REC
 
+__global__ void __launch_bounds__(PK_THREADS) k_pack(const long long* __restrict__ ow, const long long* __restrict__ oh,
+                                                     int n_max, const int* __restrict__ n_dev, long long omega,
+                                                     int kbits, long long n_scales, long long first,
+                                                     long long explicit_num, long long explicit_den, long long min_dim,
+                                                     long long pad, long long* __restrict__ cand,
+                                                     long long* __restrict__ cand_p, int* __restrict__ cand_w,
+                                                     int* __restrict__ cand_h, int* __restrict__ cand_y,
+                                                     int* __restrict__ rowstart, int* __restrict__ gfront,
+                                                     fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
+    extern __shared__ int dyn_front[];
+    __shared__ PackSmem sm;
+    int n = n_dev ? *n_dev : n_max;
+    if (n > n_max) {
+        if (st && threadIdx.x == 0) atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW);
+        return;
+    }
+    long long i = first - blockIdx.x;  // candidates descending within a batch
+    if (i < 1) return;
+    if (st && st->done) return;
+    if (n <= 0) return;
+    if (st && (st->flags & (FA_DFLAG_HEIGHT_OVERFLOW | FA_DFLAG_KEY_RANGE | FA_DFLAG_DUPLICATE_MIN_TRI))) return;
+    long long num, den;
+    if (explicit_den > 0) {
+        long long g = gcd_ll(explicit_num, explicit_den);
+        num = div_by_gcd(explicit_num, g);
+        den = div_by_gcd(explicit_den, g);
+    } else {
+        long long g = gcd_ll(i, n_scales);
+        num = div_by_gcd(i, g);
+        den = div_by_gcd(n_scales, g);
+    }
+    size_t slot = blockIdx.x;
+    int* front = gfront ? gfront + slot * (size_t)(omega + 1) : dyn_front;
+    long long rn = 0, rd = 1, used = 0;
+    bool ok = pack_candidate(ow, oh, n, num, den, omega, kbits, min_dim, pad, cand_w + slot * n_max,
+                             cand_h + slot * n_max, cand_p + slot * n_max, cand_y + slot * n_max,
+                             rowstart + slot * n_max, front, rn, rd, used, sm);
+    if (threadIdx.x == 0) {
+        long long* rec = cand + CAND_REC * (i - 1);
+        rec[0] = ok;
+        rec[1] = rn;
+        rec[2] = rd;
+        rec[3] = used;
+        rec[4] = (long long)slot;
+    }
+}
+
+// after a batch: done |= any accepted in [lo, hi]
+__global__ void k_batch_done(const long long* __restrict__ cand, long long lo, long long hi, fa_dstat* st) {
+    FA_PDL_PROLOGUE();
+    bool any = false;
+    for (long long i = lo + threadIdx.x; i <= hi; i += blockDim.x) any |= cand[CAND_REC * (i - 1)] != 0;
+    if (__syncthreads_or(any) && threadIdx.x == 0) st->done = 1;
+}
+
 // selection (packing.py:327-345) + placements in packing order, by one CTA;
 // red: 33 long longs of shared memory.  Array types are templated so the
 // frame's fused pack (k_pack_frame) can pass its shared-memory copies.
@@ -695,92 +751,6 @@ __device__ void select_body(const OwT* ow, const TwT* tw, const TwT* th, const i
         st->scale_den = rec[2];
         st->texels_allocated = tex;
     }
-}
-
-// selection inputs for the last candidate CTA (k_pack with fused selection)
-struct fa_select_args {
-    const long long *tw, *th, *chart_id;
-    const unsigned char* rot;
-    const int* perm;
-    long long* placements;
-    int4* plc_by_src;
-    unsigned char* accept_out;
-};
-
-__global__ void __launch_bounds__(PK_THREADS) k_pack(const long long* __restrict__ ow, const long long* __restrict__ oh,
-                                                     int n_max, const int* __restrict__ n_dev, long long omega,
-                                                     int kbits, long long n_scales, long long first,
-                                                     long long explicit_num, long long explicit_den, long long min_dim,
-                                                     long long pad, long long* __restrict__ cand,
-                                                     long long* __restrict__ cand_p, int* __restrict__ cand_w,
-                                                     int* __restrict__ cand_h, int* __restrict__ cand_y,
-                                                     int* __restrict__ rowstart, int* __restrict__ gfront,
-                                                     fa_dstat* __restrict__ st, fa_select_args sel) {
-    FA_PDL_PROLOGUE();
-    extern __shared__ int dyn_front[];
-    __shared__ PackSmem sm;
-    __shared__ long long s_best;
-    __shared__ int s_last;
-    int n = n_dev ? *n_dev : n_max;
-    long long i = first - blockIdx.x;  // candidates descending within a batch
-    bool work = true;
-    if (n > n_max) {
-        if (st && threadIdx.x == 0) atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW);
-        work = false;
-    }
-    if (i < 1 || (st && st->done) || n <= 0) work = false;
-    if (st && (st->flags & (FA_DFLAG_HEIGHT_OVERFLOW | FA_DFLAG_KEY_RANGE | FA_DFLAG_DUPLICATE_MIN_TRI))) work = false;
-    if (work) {
-        long long num, den;
-        if (explicit_den > 0) {
-            long long g = gcd_ll(explicit_num, explicit_den);
-            num = div_by_gcd(explicit_num, g);
-            den = div_by_gcd(explicit_den, g);
-        } else {
-            long long g = gcd_ll(i, n_scales);
-            num = div_by_gcd(i, g);
-            den = div_by_gcd(n_scales, g);
-        }
-        size_t slot = blockIdx.x;
-        int* front = gfront ? gfront + slot * (size_t)(omega + 1) : dyn_front;
-        long long rn = 0, rd = 1, used = 0;
-        bool ok = pack_candidate(ow, oh, n, num, den, omega, kbits, min_dim, pad, cand_w + slot * n_max,
-                                 cand_h + slot * n_max, cand_p + slot * n_max, cand_y + slot * n_max,
-                                 rowstart + slot * n_max, front, rn, rd, used, sm);
-        if (threadIdx.x == 0) {
-            long long* rec = cand + CAND_REC * (i - 1);
-            rec[0] = ok;
-            rec[1] = rn;
-            rec[2] = rd;
-            rec[3] = used;
-            rec[4] = (long long)slot;
-        }
-    }
-    if (!sel.placements) return;
-    // fused selection (single batch): the last candidate CTA to finish
-    // selects (packing.py:342-345), saving the selection launch
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        s_last = atomicAdd(&st->pack_done, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    if (st->flags & (FA_DFLAG_HEIGHT_OVERFLOW | FA_DFLAG_KEY_RANGE | FA_DFLAG_DUPLICATE_MIN_TRI |
-                     FA_DFLAG_QUEUE_OVERFLOW))
-        return;
-    select_body(ow, sel.tw, sel.th, (const int*)nullptr, sel.chart_id, sel.rot, sel.perm, n, omega, n_scales, min_dim,
-                pad, cand, cand_p, cand_w, cand_h, cand_y, n_max, sel.placements, sel.plc_by_src, sel.accept_out, st,
-                sm.red, &s_best);
-}
-
-// after a batch: done |= any accepted in [lo, hi]
-__global__ void k_batch_done(const long long* __restrict__ cand, long long lo, long long hi, fa_dstat* st) {
-    FA_PDL_PROLOGUE();
-    bool any = false;
-    for (long long i = lo + threadIdx.x; i <= hi; i += blockDim.x) any |= cand[CAND_REC * (i - 1)] != 0;
-    if (__syncthreads_or(any) && threadIdx.x == 0) st->done = 1;
 }
 
 __global__ void __launch_bounds__(1024) k_select(const long long* __restrict__ ow, const long long* __restrict__ tw,
@@ -942,26 +912,19 @@ int fa_launch_pack(const fa_pack_bufs& b, int n_max, const int* n_dev, long long
     bool smem_front = front_smem(omega) <= kMaxFrontSmem;
     size_t dyn = smem_front ? front_smem(omega) : 0;
     int launches = 0;
-    // one batch (n_scales <= batch, the frame's 64 candidates): the last
-    // candidate CTA selects; otherwise batches, then k_select
-    const bool fused = n_scales <= batch && st != nullptr;
-    const fa_select_args sel = fused ? fa_select_args{b.tw, b.th, b.chart_id, b.rot, b.perm, b.placements, b.plc_by_src,
-                                                      b.accept_out}
-                                     : fa_select_args{};
     for (long long hi = n_scales; hi >= 1; hi -= batch) {
         long long lo = hi - batch + 1;
         if (lo < 1) lo = 1;
         int grid = (int)(hi - lo + 1);
         fa_launch(k_pack, grid, PK_THREADS, dyn, s, b.ow, b.oh, n_max, n_dev, omega, kbits, n_scales, hi, 0, 0, min_dim, pad,
                                              b.cand, b.cand_p, b.cand_w, b.cand_h, b.cand_y, b.rowstart,
-                                             smem_front ? nullptr : b.gfront, st, sel);
+                                             smem_front ? nullptr : b.gfront, st);
         launches++;
         if (lo > 1) {
             fa_launch(k_batch_done, 1, 256, 0, s, b.cand, lo, hi, st);
             launches++;
         }
     }
-    if (fused) return launches;
     fa_launch(k_select, 1, 1024, 0, s, b.ow, b.tw, b.th, b.chart_id, b.rot, b.perm, n_max, n_dev, omega, n_scales, min_dim,
                                 pad, b.cand, b.cand_p, b.cand_w, b.cand_h, b.cand_y, b.placements, b.plc_by_src, b.accept_out, st);
     return launches + 1;
@@ -975,8 +938,7 @@ void fa_launch_pack_at_scale(const long long* ow, const long long* oh, int n, lo
     bool smem_front = front_smem(omega) <= kMaxFrontSmem;
     fa_launch(k_pack, 1, PK_THREADS, smem_front ? front_smem(omega) : 0, s, ow, oh, n, nullptr, omega, kbits, 1, 1, num, den,
                                                                      min_dim, pad, cand, cand_p, cand_w, cand_h, cand_y,
-                                                                     rowstart, smem_front ? nullptr : gfront, nullptr,
-                                                                     fa_select_args{});
+                                                                     rowstart, smem_front ? nullptr : gfront, nullptr);
 }
 
 void fa_launch_xywh(const long long* cand, const long long* cand_p, const int* cand_w, const int* cand_h,
