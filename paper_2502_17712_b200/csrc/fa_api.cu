@@ -118,7 +118,7 @@ void fa_destroy(fa_ctx* c) {
                       &c->target, &c->survived, &c->okey, &c->oidx, &c->ow, &c->oh, &c->orot, &c->sortk, &c->sortv,
                       &c->pinv, &c->cand, &c->cand_p, &c->cand_w, &c->cand_h, &c->cand_y, &c->rowstart,
                       &c->placements, &c->uv, &c->vp_dev, &c->blocks, &c->dstat, &c->aux, &c->in_tw, &c->in_th,
-                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list, &c->hiz, &c->wid, &c->vis_chart, &c->vis_cidx, &c->plc_c, &c->pos_perm, &c->tris_perm, &c->vperm_buf, &c->vis_tris, &c->vslot, &c->vlist, &c->vuv, &c->vblocks, &c->pstat, &c->tperm_buf, &c->tris_sorted_buf, &c->clusters_buf, &c->live_buf};
+                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list, &c->hiz, &c->wid, &c->vis_chart, &c->vis_cidx, &c->plc_c, &c->pos_perm, &c->tris_perm, &c->vperm_buf, &c->vis_tris, &c->vslot, &c->vlist, &c->vuv, &c->vblocks, &c->pstat, &c->tperm_buf, &c->tris_sorted_buf, &c->clusters_buf, &c->live_buf, &c->mesh_first, &c->mesh_scratch, &c->mesh_sort, &c->mesh_tris_s};
     for (fa_buf* b : bufs) free_buf(*b);
     for (cudaEvent_t e : c->fj)
         if (e) cudaEventDestroy(e);
@@ -161,7 +161,11 @@ int fa_set_mesh(fa_ctx* ctx, const double* positions, int64_t n_vertices, const 
         const bool order = fa_env_int("FASTATLAS_TRI_ORDER", 1) != 0;
         const long long T = n_triangles;
         const int V = (int)n_vertices;
-        fa_buf first, scratch, sort_scratch, tris_s;
+        // scratch kept by the context (grow-only): a rebind allocates nothing
+        fa_buf& first = ctx->mesh_first;
+        fa_buf& scratch = ctx->mesh_scratch;
+        fa_buf& sort_scratch = ctx->mesh_sort;
+        fa_buf& tris_s = ctx->mesh_tris_s;
         const size_t vb = (size_t)(n_vertices > 0 ? n_vertices : 1) * 4;
         bool ok = fa_ensure(ctx, first, vb) &&
                   fa_ensure(ctx, scratch, (size_t)fa_mesh_scratch_ints(n_vertices, T) * 4 + vb + 16) &&
@@ -172,13 +176,7 @@ int fa_set_mesh(fa_ctx* ctx, const double* positions, int64_t n_vertices, const 
             ok = fa_ensure(ctx, ctx->tris_perm, (size_t)T * 12) && fa_ensure(ctx, ctx->vperm_buf, vb) &&
                  fa_ensure(ctx, ctx->pos_perm, (size_t)n_vertices * 24 + 8);
         }
-        if (!ok) {
-            free_buf(first);
-            free_buf(scratch);
-            free_buf(sort_scratch);
-            free_buf(tris_s);
-            return set_err(FA_CUDA_ERROR, "out of device memory binding the mesh");
-        }
+        if (!ok) return set_err(FA_CUDA_ERROR, "out of device memory binding the mesh");
         cudaStream_t s = nullptr;
         int* bad = P<int>(scratch);
         int* newidx = P<int>(scratch) + 1 + fa_mesh_scratch_ints(n_vertices, T);
@@ -210,10 +208,6 @@ int fa_set_mesh(fa_ctx* ctx, const double* positions, int64_t n_vertices, const 
             e = cudaGetLastError();
             if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         }
-        free_buf(first);
-        free_buf(scratch);
-        free_buf(sort_scratch);
-        free_buf(tris_s);
         if (e != cudaSuccess) return set_err(FA_CUDA_ERROR, "fa_set_mesh: %s", cudaGetErrorString(e));
         if (hbad) return set_err(FA_VALUE_ERROR, "triangle index out of range");
         if (renumber) {

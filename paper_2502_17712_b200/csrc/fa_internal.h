@@ -87,6 +87,7 @@ struct fa_ctx {
     const int* tris_sorted = nullptr;
     const fa_cluster* clusters = nullptr;
     fa_buf tperm_buf, tris_sorted_buf, clusters_buf, live_buf;
+    fa_buf mesh_first, mesh_scratch, mesh_sort, mesh_tris_s;  // fa_set_mesh scratch
 
     // scratch (grown on demand)
     fa_buf small_rec, clip, depth_keys, depth_f64, flags, vis_list, large, tiles, label, vmin, v2c, cidx;

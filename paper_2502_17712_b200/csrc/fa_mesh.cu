@@ -163,7 +163,7 @@ void fa_launch_mesh_renumber(const double* pos, const int* tris, long long T, in
 // -- are unchanged: the setup reads the original id of each slot.
 // ---------------------------------------------------------------------------
 #define RS_THREADS 256
-#define RS_ITEMS 16
+#define RS_ITEMS 64
 #define RS_TILE (RS_THREADS * RS_ITEMS)
 
 int fa_sort_blocks(long long n) { return (int)((n + RS_TILE - 1) / RS_TILE); }
