@@ -268,7 +268,7 @@ static int ensure_raster(fa_ctx* ctx, int W, int H, bool depth) {
     ENSURE(hiz, (size_t)fa_hiz_dim(W) * fa_hiz_dim(H) * 8);
     ENSURE(flags, ((T + 15) / 16 + 1) * 16);
     ENSURE(clip_list, (T + 1) * 4);
-    ENSURE(small_rec, (T + 1) * sizeof(SmallRec));
+    ENSURE(small_rec, (T + 1) * sizeof(SmallRec) + (T + 1) * 4);  // records + their triangle ids
     long long want_tiles = (long long)W * H / 32;
     if (want_tiles > ctx->max_tiles) ctx->max_tiles = (int)(want_tiles < (1ll << 30) ? want_tiles : (1 << 30));
     ENSURE(large, (size_t)ctx->max_large * sizeof(TriSetup));

@@ -241,7 +241,11 @@ __global__ void __launch_bounds__(SETUP_WARPS * 32) k_raster_setup(const double4
             }
         }
         __syncthreads();
-        if (m1 && kind == 1) store_rec(f, t, recs + s_base[0][warp] + __popc(m1 & lt_mask));
+        if (m1 && kind == 1) {
+            const int idx = s_base[0][warp] + __popc(m1 & lt_mask);
+            store_rec(f, t, recs + idx);
+            small_ids(recs, T)[idx] = t;  // lets the visibility filter skip flagged records unread
+        }
         if (m3 && kind == 3) clip_list[s_base[2][warp] + __popc(m3 & lt_mask)] = t;
         if (m2) {
             // large records are stored downward from index T (small + large
@@ -628,7 +632,7 @@ __global__ void __launch_bounds__(COOP_WARPS * 32, COOP_MIN_BLOCKS) k_small_coop
 // them).  The ~20% that survive are appended (one atomic per block step) to a
 // queue that k_vis_small_sample walks one thread per survivor, so sampling
 // lanes are not spread thinly over warps that are mostly done.
-__global__ void __launch_bounds__(256) k_vis_small_filter(const SmallRec* __restrict__ small_rec,
+__global__ void __launch_bounds__(256) k_vis_small_filter(const SmallRec* __restrict__ small_rec, int T,
                                                           const unsigned long long* __restrict__ hiz, int htx,
                                                           const unsigned char* __restrict__ flags,
                                                           int* __restrict__ queue, fa_dstat* __restrict__ st) {
@@ -636,17 +640,23 @@ __global__ void __launch_bounds__(256) k_vis_small_filter(const SmallRec* __rest
     __shared__ int s_cnt[8], s_base;
     const int n3 = st->n_small3;
     const int lane = lane_id(), warp = threadIdx.x >> 5;
+    const int* __restrict__ ids = small_ids(small_rec, T);
     for (int b0 = (int)blockIdx.x * blockDim.x; b0 < n3; b0 += gridDim.x * blockDim.x) {
         const int i = b0 + threadIdx.x;
         bool need = false;
-        if (i < n3) {
+        // the triangle id first: a record whose triangle is already flagged
+        // (a pass-1 pixel winner) is never read
+        const unsigned char seen = i < n3 ? flags[__ldg(ids + i)] : 1;
+        if (!seen) {
+            const SmallRec* q = small_rec + i;
             Setup3 f;
-            int t;
-            load_rec(small_rec + i, f, t);
+            f.min_x = q->min_x; f.max_x = q->max_x; f.min_y = q->min_y; f.max_y = q->max_y;
+            f.use_plane = (q->flags >> 3) & 1;
+            f.p0x = q->x0; f.p0y = q->y0; f.p0z = q->z0;
+            f.gx = q->g0; f.gy = q->g1; f.zmean = q->g0;
             const int tx0 = f.min_x / FA_HIZ, tx1 = f.max_x / FA_HIZ, ty0 = f.min_y / FA_HIZ, ty1 = f.max_y / FA_HIZ;
             const bool hz = tx1 - tx0 <= 1 && ty1 - ty0 <= 1;
             unsigned long long h00 = 1, h01 = 1, h10 = 1, h11 = 1;
-            const unsigned char seen = flags[t];
             if (hz) {
                 h00 = __ldg(hiz + ty0 * htx + tx0);
                 h01 = __ldg(hiz + ty0 * htx + tx1);
@@ -956,7 +966,7 @@ int fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const
     if (side) fork_to(s, side, ev_fork);
     fa_launch(k_raster_vis_tiles, fa_cap(FA_NUM_SMS * 8), 256, 0, b, small_rec, T, large, tiles, W, depth, hiz, htx, flags, st,
                                                       max_tiles, max_large);
-    fa_launch(k_vis_small_filter, fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s, small_rec, hiz, htx, flags, vis_queue,
+    fa_launch(k_vis_small_filter, fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s, small_rec, T, hiz, htx, flags, vis_queue,
               st);
     fa_launch(k_vis_small_sample, fa_grid(T / 4, 256, FA_NUM_SMS * 8), 256, 0, s, small_rec, W, depth, vis_queue, flags,
               st);

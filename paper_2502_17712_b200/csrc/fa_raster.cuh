@@ -632,6 +632,12 @@ struct __align__(16) SmallRec {
     int flags;                      // bits 0-2 incl, bit 3 use_plane
 };
 
+// triangle id of each small record, stored after the (T + 1) records
+__device__ __forceinline__ int* small_ids(SmallRec* recs, int T) { return reinterpret_cast<int*>(recs + (T + 1)); }
+__device__ __forceinline__ const int* small_ids(const SmallRec* recs, int T) {
+    return reinterpret_cast<const int*>(recs + (T + 1));
+}
+
 __device__ __forceinline__ void store_rec(const Setup3& s, int t, SmallRec* r) {
     SmallRec q;
     q.x0 = s.ax0; q.y0 = s.ay0; q.x1 = s.ax1; q.y1 = s.ay1; q.x2 = s.ax2; q.y2 = s.ay2;
