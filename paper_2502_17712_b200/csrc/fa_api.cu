@@ -118,7 +118,7 @@ void fa_destroy(fa_ctx* c) {
                       &c->target, &c->survived, &c->okey, &c->oidx, &c->ow, &c->oh, &c->orot, &c->sortk, &c->sortv,
                       &c->pinv, &c->cand, &c->cand_p, &c->cand_w, &c->cand_h, &c->cand_y, &c->rowstart,
                       &c->placements, &c->uv, &c->vp_dev, &c->blocks, &c->dstat, &c->aux, &c->in_tw, &c->in_th,
-                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list, &c->hiz, &c->wid, &c->vis_chart, &c->vis_cidx, &c->plc_c, &c->pos_perm, &c->tris_perm, &c->vperm_buf, &c->vis_tris, &c->vslot, &c->vlist, &c->vuv, &c->vblocks, &c->pstat, &c->tperm_buf, &c->tris_sorted_buf, &c->clusters_buf, &c->live_buf, &c->mesh_first, &c->mesh_scratch, &c->mesh_sort, &c->mesh_tris_s};
+                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list, &c->hiz, &c->wid, &c->vis_chart, &c->vis_cidx, &c->plc_c, &c->pos_perm, &c->tris_perm, &c->vperm_buf, &c->vis_tris, &c->vslot, &c->vlist, &c->vuv, &c->vblocks, &c->pstat, &c->tperm_buf, &c->tris_sorted_buf, &c->clusters_buf, &c->live_buf, &c->mesh_first, &c->mesh_scratch, &c->mesh_sort, &c->mesh_tris_s, &c->ord_tw, &c->ord_th, &c->ord_cid};
     for (fa_buf* b : bufs) free_buf(*b);
     for (cudaEvent_t e : c->fj)
         if (e) cudaEventDestroy(e);
@@ -320,6 +320,9 @@ static int ensure_pack(fa_ctx* ctx, int64_t n_cap, int64_t n_scales, int64_t ome
     ENSURE(cand_y, (size_t)batch * n * 4);
     ENSURE(rowstart, (size_t)batch * n * 4);
     ENSURE(placements, n * 64);
+    ENSURE(ord_tw, n * 8);
+    ENSURE(ord_th, n * 8);
+    ENSURE(ord_cid, n * 8);
     ENSURE(plc_c, n * 32);
     if (!fa_front_in_smem(omega)) ENSURE(okey, (size_t)batch * (omega + 1) * 4);
     return FA_OK;
@@ -1075,6 +1078,10 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     fa_pack_bufs b = pack_bufs(ctx, P<long long>(ctx->in_tw), P<long long>(ctx->in_th), P<long long>(ctx->in_cid),
                                P<long long>(ctx->placements), nullptr);
     b.plc_by_src = P<int4>(ctx->plc_c);
+    b.ord_tw = P<long long>(ctx->ord_tw);
+    b.ord_th = P<long long>(ctx->ord_th);
+    b.ord_cid = P<long long>(ctx->ord_cid);
+    b.ord_written = fa_env_int("FASTATLAS_ORDER_ONCHIP", 1) != 0;
     const fa_box_dims_args bd{P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), P<int>(ctx->roots), W, H,
                               p->prescale, P<double>(ctx->ndc), P<int>(ctx->px), P<long long>(ctx->target),
                               P<long long>(ctx->in_tw), P<long long>(ctx->in_th), P<long long>(ctx->in_cid),

@@ -305,7 +305,8 @@ struct fa_box_dims_args {
     int cap;
 };
 
-__device__ __forceinline__ void fa_box_dims_one(const fa_box_dims_args& a, int j, fa_dstat* st) {
+__device__ __forceinline__ void fa_box_dims_one(const fa_box_dims_args& a, int j, fa_dstat* st,
+                                                long long* out_tw = nullptr, long long* out_th = nullptr) {
     if (!a.survived[j]) atomicOr(&st->flags, FA_DFLAG_DEGENERATE_CHART);
     double mnx = key_f64(a.keys[4 * j]), mny = key_f64(a.keys[4 * j + 1]);
     double mxx = key_f64(a.keys[4 * j + 2]), mxy = key_f64(a.keys[4 * j + 3]);
@@ -324,6 +325,7 @@ __device__ __forceinline__ void fa_box_dims_one(const fa_box_dims_args& a, int j
     long long itw = tw < 1.0 ? 1 : (long long)tw, ith = th < 1.0 ? 1 : (long long)th;
     a.target[2 * j] = itw;
     a.target[2 * j + 1] = ith;
+    if (out_tw) { *out_tw = itw; *out_th = ith; }
     if (j >= a.cap) {
         atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW);
         return;

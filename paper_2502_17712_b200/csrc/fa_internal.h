@@ -88,6 +88,7 @@ struct fa_ctx {
     const fa_cluster* clusters = nullptr;
     fa_buf tperm_buf, tris_sorted_buf, clusters_buf, live_buf;
     fa_buf mesh_first, mesh_scratch, mesh_sort, mesh_tris_s;  // fa_set_mesh scratch
+    fa_buf ord_tw, ord_th, ord_cid;  // per packing position (k_order_frame -> k_select)
 
     // scratch (grown on demand)
     fa_buf small_rec, clip, depth_keys, depth_f64, flags, vis_list, large, tiles, label, vmin, v2c, cidx;
@@ -243,6 +244,12 @@ struct fa_pack_bufs {
     int4* plc_by_src;          // optional (n,2) int4 per input box: {x, y, w, h}, {rot, 0, 0, 0}
     unsigned char* accept_out; // optional
     int* gfront;               // global frontline (batch x (omega+1)) when omega is too big for smem
+    // frame path: target dims / chart id per packing position (k_order_frame
+    // writes them when ord_written, k_select reads them without perm)
+    long long* ord_tw = nullptr;
+    long long* ord_th = nullptr;
+    long long* ord_cid = nullptr;
+    bool ord_written = false;
 };
 // bd (optional): compute the per-chart box dims (k_box_dims' work) first, in the same launch
 void fa_launch_orient_sort(const fa_pack_bufs& b, int n_max, const int* n_dev, long long max_h, fa_dstat* st,

@@ -284,6 +284,114 @@ __global__ void __launch_bounds__(SORT_THREADS) k_orient_sort(const long long* t
     }
 }
 
+// ---- the frame's order: box dims + orient + order, in shared memory -------
+// The frame path of k_orient_sort (box dims at the head, charts in
+// ascending-root order, so a stable radix sort on the height alone gives
+// (-h, min_tri), packing.py:109-130) with every intermediate kept on chip:
+// the dims stay in shared memory instead of a global write-and-read-back, the
+// radix ping-pong arrays are shared memory (up to `cap` charts; beyond it the
+// global scratch), and the outputs are fire-and-forget stores -- one global
+// round trip (the bounds' keys) instead of about six.  Also writes the target
+// dims and chart id of each packing position (ord_*), so the selection reads
+// them without the perm indirection.
+size_t fa_order_frame_smem(int cap) { return (size_t)cap * (4 + 4 + 8 + 8 + 4 + 4) + 64; }
+
+__global__ void __launch_bounds__(SORT_THREADS) k_order_frame(fa_box_dims_args bd, const int* __restrict__ n_dev,
+                                                              int n_max, int cap, long long max_h,
+                                                              long long* __restrict__ ow, long long* __restrict__ oh,
+                                                              unsigned char* __restrict__ rot, int* __restrict__ perm,
+                                                              int* __restrict__ pinv, unsigned long long* sk, int* sv,
+                                                              long long* __restrict__ ord_tw,
+                                                              long long* __restrict__ ord_th,
+                                                              long long* __restrict__ ord_cid,
+                                                              fa_dstat* __restrict__ st) {
+    FA_PDL_PROLOGUE();
+    extern __shared__ __align__(16) unsigned char of_dyn[];
+    __shared__ SortSmem sm;
+    const int tid = threadIdx.x;
+    const int n = *n_dev;
+    if (n > n_max) {
+        if (tid == 0) atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW);
+        return;
+    }
+    const bool on_chip = n <= cap;
+    unsigned long long* ka = reinterpret_cast<unsigned long long*>(of_dyn);
+    unsigned long long* kb = ka + cap;
+    int* va = reinterpret_cast<int*>(kb + cap);
+    int* vb = va + cap;
+    int* in_w = vb + cap;
+    int* in_h = in_w + cap;
+    if (!on_chip) {
+        ka = sk;
+        kb = sk + n_max;
+        va = sv;
+        vb = sv + n_max;
+    }
+    long long hmax = 0, nhmin = -0x7fffffffffffffffll;
+    bool overflow = false;
+    for (int j = tid; j < n; j += blockDim.x) {
+        long long itw, ith;
+        fa_box_dims_one(bd, j, st, &itw, &ith);
+        const long long oh_ = itw > ith ? itw : ith;
+        if (oh_ > max_h) overflow = true;
+        hmax = oh_ > hmax ? oh_ : hmax;
+        nhmin = -oh_ > nhmin ? -oh_ : nhmin;
+        if (on_chip) {
+            in_w[j] = (int)(itw < (1ll << 30) ? itw : (1ll << 30));
+            in_h[j] = (int)(ith < (1ll << 30) ? ith : (1ll << 30));
+        }
+    }
+    if (tid == 0) sm.flag = 0;
+    __syncthreads();
+    if (overflow) sm.flag = 1;
+    {
+        // hmax and -hmin in one pair of barriers
+        long long a = warp_max_ll(hmax), b = warp_max_ll(nhmin);
+        const int lane = lane_id(), wid = tid >> 5, nw = blockDim.x >> 5;
+        __shared__ long long r2[2][32];
+        if (lane == 0) { r2[0][wid] = a; r2[1][wid] = b; }
+        __syncthreads();
+        a = lane < nw ? r2[0][lane] : 0;
+        b = lane < nw ? r2[1][lane] : -0x7fffffffffffffffll;
+        hmax = warp_max_ll(a);
+        nhmin = warp_max_ll(b);
+    }
+    if (sm.flag) {  // HeightOverflow (packing.py:127-129)
+        if (tid == 0) atomicOr(&st->flags, FA_DFLAG_HEIGHT_OVERFLOW);
+        return;
+    }
+    if (n == 0) return;
+    if (tid == 0) st->max_h = (int)hmax;
+    const long long hmin = -nhmin;
+    int hbits = 0;
+    while (hbits < 63 && ((hmax - hmin) >> hbits) != 0) hbits++;
+    for (int j = tid; j < n; j += blockDim.x) {
+        const long long w = on_chip ? in_w[j] : bd.otw[j], h = on_chip ? in_h[j] : bd.oth[j];
+        ka[j] = (unsigned long long)(hmax - (w > h ? w : h));
+        va[j] = j;
+    }
+    __syncthreads();
+    for (int q = 0; q < (hbits + 7) / 8; q++) {
+        radix_pass(ka, va, kb, vb, n, 8 * q, sm);
+        unsigned long long* tk = ka; ka = kb; kb = tk;
+        int* tv = va; va = vb; vb = tv;
+    }
+    __syncthreads();
+    for (int j = tid; j < n; j += blockDim.x) {
+        const int i = va[j];
+        const long long w = on_chip ? in_w[i] : bd.otw[i], h = on_chip ? in_h[i] : bd.oth[i];
+        const bool r = w > h;
+        perm[j] = i;
+        pinv[i] = j;
+        ow[j] = r ? h : w;
+        oh[j] = r ? w : h;
+        rot[j] = r;
+        ord_tw[j] = w;
+        ord_th[j] = h;
+        ord_cid[j] = bd.roots[i];
+    }
+}
+
 // ============================================================================
 // packing candidates
 // ============================================================================
@@ -686,7 +794,9 @@ __device__ void select_body(const OwT* ow, const TwT* tw, const TwT* th, const i
                             const int* __restrict__ cand_w, const int* __restrict__ cand_h,
                             const int* __restrict__ cand_y, int n_max, long long* __restrict__ placements,
                             int4* __restrict__ plc_by_src, unsigned char* __restrict__ accept_out,
-                            fa_dstat* __restrict__ st, long long* red, long long* s_best) {
+                            fa_dstat* __restrict__ st, long long* red, long long* s_best,
+                            const long long* __restrict__ ord_tw = nullptr, const long long* __restrict__ ord_th = nullptr,
+                            const long long* __restrict__ ord_cid = nullptr) {
     const int tid = threadIdx.x;
     if (n <= 0) {
         if (tid == 0) { st->scale_num = 1; st->scale_den = 1; st->best = -1; }
@@ -729,14 +839,20 @@ __device__ void select_body(const OwT* ow, const TwT* tw, const TwT* th, const i
         long long x = (r % FA_DIRECTION_PERIOD == 0) ? q : omega - q - w[j];
         int src = perm[j];
         long long* P = placements + 8 * (long long)j;
-        P[0] = chart_id_i ? (long long)chart_id_i[src] : (chart_id ? chart_id[src] : src);
+        if (ord_tw) {  // packing-order copies (k_order_frame): no dependent load through perm
+            P[0] = ord_cid[j];
+            P[6] = ord_tw[j];
+            P[7] = ord_th[j];
+        } else {
+            P[0] = chart_id_i ? (long long)chart_id_i[src] : (chart_id ? chart_id[src] : src);
+            P[6] = tw[src];
+            P[7] = th[src];
+        }
         P[1] = x;
         P[2] = y[j];
         P[3] = w[j];
         P[4] = h[j];
         P[5] = rot[j];
-        P[6] = tw[src];
-        P[7] = th[src];
         if (plc_by_src) {  // k_uv reads its chart's placement directly (x, y, w, h < 2^31)
             plc_by_src[2 * src] = make_int4((int)x, y[j], w[j], h[j]);
             plc_by_src[2 * src + 1] = make_int4(rot[j], 0, 0, 0);
@@ -762,7 +878,9 @@ __global__ void __launch_bounds__(1024) k_select(const long long* __restrict__ o
                                                  const int* __restrict__ cand_w, const int* __restrict__ cand_h,
                                                  const int* __restrict__ cand_y, long long* __restrict__ placements,
                                                  int4* __restrict__ plc_by_src, unsigned char* __restrict__ accept_out,
-                                                 fa_dstat* __restrict__ st) {
+                                                 fa_dstat* __restrict__ st, const long long* __restrict__ ord_tw,
+                                                 const long long* __restrict__ ord_th,
+                                                 const long long* __restrict__ ord_cid) {
     FA_PDL_PROLOGUE();
     __shared__ long long red[33];
     __shared__ long long s_best;
@@ -771,7 +889,8 @@ __global__ void __launch_bounds__(1024) k_select(const long long* __restrict__ o
                      FA_DFLAG_QUEUE_OVERFLOW))
         return;
     select_body(ow, tw, th, (const int*)nullptr, chart_id, rot, perm, n, omega, n_scales, min_dim, pad, cand, cand_p,
-                cand_w, cand_h, cand_y, n_max, placements, plc_by_src, accept_out, st, red, &s_best);
+                cand_w, cand_h, cand_y, n_max, placements, plc_by_src, accept_out, st, red, &s_best, ord_tw, ord_th,
+                ord_cid);
 }
 
 // ---- standalone fold (packing.py:133-158) --------------------------------
@@ -891,6 +1010,18 @@ static void ensure_smem_attr() {
 
 void fa_launch_orient_sort(const fa_pack_bufs& b, int n_max, const int* n_dev, long long max_h, fa_dstat* st,
                            cudaStream_t s, const fa_box_dims_args* bd) {
+    if (bd && b.ord_tw && fa_env_int("FASTATLAS_ORDER_ONCHIP", 1)) {
+        const int cap = n_max < 4096 ? n_max : 4096;
+        const size_t smem = fa_order_frame_smem(cap);
+        static size_t attr = 0;
+        if (smem > attr) {
+            cudaFuncSetAttribute(k_order_frame, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr = smem;
+        }
+        fa_launch(k_order_frame, 1, SORT_THREADS, smem, s, *bd, n_dev, n_max, cap, max_h, b.ow, b.oh, b.rot, b.perm,
+                  b.pinv, b.sortk, b.sortv, b.ord_tw, b.ord_th, b.ord_cid, st);
+        return;
+    }
     fa_box_dims_args none{};
     fa_launch(k_orient_sort, 1, SORT_THREADS, 0, s, b.tw, b.th, nullptr, n_max, n_dev, max_h, b.ow, b.oh, b.rot, b.perm,
               b.pinv, b.sortk, b.sortv, 0, st, bd ? *bd : none);
@@ -925,8 +1056,11 @@ int fa_launch_pack(const fa_pack_bufs& b, int n_max, const int* n_dev, long long
             launches++;
         }
     }
+    const bool ord = b.ord_tw && b.ord_written;
     fa_launch(k_select, 1, 1024, 0, s, b.ow, b.tw, b.th, b.chart_id, b.rot, b.perm, n_max, n_dev, omega, n_scales, min_dim,
-                                pad, b.cand, b.cand_p, b.cand_w, b.cand_h, b.cand_y, b.placements, b.plc_by_src, b.accept_out, st);
+                                pad, b.cand, b.cand_p, b.cand_w, b.cand_h, b.cand_y, b.placements, b.plc_by_src, b.accept_out, st,
+                                ord ? (const long long*)b.ord_tw : nullptr, ord ? (const long long*)b.ord_th : nullptr,
+                                ord ? (const long long*)b.ord_cid : nullptr);
     return launches + 1;
 }
 
