@@ -15,6 +15,7 @@
 #include <string>
 #include <vector>
 
+#define FA_TU_ID 1  // trace builds (FA_TRACE): kernel key = TU id + line
 #include "fa_internal.h"
 #include "fa_raster.cuh"
 
@@ -1503,3 +1504,49 @@ int fa_orient(fa_ctx* ctx, const int64_t* target_w, const int64_t* target_h, int
 }
 
 }  // extern "C"
+
+FA_TRACE_TU(api)
+
+#ifdef FA_TRACE
+// ---- debug trace (FA_TRACE builds): per-kernel device timestamps ------------
+void fa_trace_bind_raster(void*);
+void fa_trace_bind_charts(void*);
+void fa_trace_bind_bounds(void*);
+void fa_trace_bind_pack(void*);
+void fa_trace_bind_uv(void*);
+void fa_trace_bind_baselines(void*);
+void fa_trace_bind_mesh(void*);
+static fa_trace_rec* g_trace_dev = nullptr;
+
+extern "C" int fa_debug_trace_reset(void) {
+    if (!g_trace_dev && cudaMalloc(&g_trace_dev, 128 * sizeof(fa_trace_rec)) != cudaSuccess) return -1;
+    fa_trace_rec init[128];
+    for (auto& r : init) r = {0ull, ~0ull, 0ull, 0ull};
+    cudaMemcpy(g_trace_dev, init, sizeof(init), cudaMemcpyHostToDevice);
+    void* p = g_trace_dev;
+    fa_trace_bind_raster(p); fa_trace_bind_charts(p); fa_trace_bind_bounds(p); fa_trace_bind_pack(p);
+    fa_trace_bind_uv(p); fa_trace_bind_baselines(p); fa_trace_bind_mesh(p); fa_trace_bind_api(p);
+    return 0;
+}
+
+// n records: kernel key (decimal string, names[64*i]), first start, last end (ns), launches
+extern "C" int fa_debug_trace_read(char* names, unsigned long long* start, unsigned long long* end,
+                                   unsigned long long* hits, int max) {
+    if (!g_trace_dev) return 0;
+    cudaDeviceSynchronize();
+    fa_trace_rec rec[128];
+    cudaMemcpy(rec, g_trace_dev, sizeof(rec), cudaMemcpyDeviceToHost);
+    int n = 0;
+    for (int i = 0; i < 128 && n < max; i++) {
+        if (!rec[i].name) continue;
+        char buf[64] = {0};
+        snprintf(buf, sizeof(buf), "%llu", rec[i].name);
+        memcpy(names + 64 * n, buf, 64);
+        start[n] = rec[i].start;
+        end[n] = rec[i].end;
+        hits[n] = rec[i].hits;
+        n++;
+    }
+    return n;
+}
+#endif

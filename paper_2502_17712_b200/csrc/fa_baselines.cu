@@ -14,6 +14,7 @@
 //   places boxes in order, its lanes testing 32 blocks at a time for the
 //   first-fit block (ballot), the winning lane updating that block's shelves.
 //   The result is the first (largest-block) level that places every box.
+#define FA_TU_ID 7  // trace builds (FA_TRACE): kernel key = TU id + line
 #include "fa_internal.h"
 #include "fa_pack.cuh"
 
@@ -365,3 +366,5 @@ void fa_launch_superblock(const long long* ow, const long long* oh, const long l
     fa_launch(k_superblock_select, 1, 256, 0, s, tw, th, cid, rot, perm, n, n_levels, xywh, out_stride, level_ok, placements,
                                           out);
 }
+
+FA_TRACE_TU(baselines)

@@ -10,6 +10,7 @@
 // materialised — min/max are order independent).  Lanes holding the same
 // chart form runs in the (ascending) visible list, so a segmented warp scan
 // reduces each run and only the run tail issues the four u64 key atomics.
+#define FA_TU_ID 4  // trace builds (FA_TRACE): kernel key = TU id + line
 #include "fa_internal.h"
 
 struct NBox {
@@ -311,3 +312,5 @@ void fa_launch_chart_bbox_world(const double* xyz, int n, const double* vp, unsi
 void fa_launch_viewport_box(const double* box, int n, int W, int H, long long* out, cudaStream_t s) {
     fa_launch(k_viewport_box, fa_grid(n, 256, FA_NUM_SMS * 4), 256, 0, s, box, n, W, H, out);
 }
+
+FA_TRACE_TU(bounds)

@@ -10,6 +10,7 @@
 // three vertices.  Hooking always puts the larger root under the smaller
 // (atomicCAS), so each component's root is its minimum triangle index —
 // the reference's canonical chart id (charts.py:335-340, 394-402).
+#define FA_TU_ID 3  // trace builds (FA_TRACE): kernel key = TU id + line
 #include "fa_internal.h"
 
 #define CMP_THREADS 256
@@ -663,3 +664,5 @@ void fa_launch_compact_roots(const int* vis_list, const int* label, int T, int* 
     fa_launch(k_count_roots, nb, CMP_THREADS, 0, s, vis_list, label, blocks, st);
     fa_launch(k_scatter_roots, nb, CMP_THREADS, 0, s, vis_list, label, blocks, nb, roots, cidx, ndc_keys, survived, st);
 }
+
+FA_TRACE_TU(charts)

@@ -237,11 +237,56 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 // no-ops when the kernel was launched without the attribute.
 __device__ __forceinline__ void fa_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void fa_pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#ifdef FA_TRACE
+// Debug builds only (tools/trace_frame.py): each kernel's first block start
+// and last block-0-thread exit per frame, from %globaltimer, into a
+// host-bound buffer (one pointer per translation unit, bound by
+// fa_debug_trace_reset); a kernel is keyed by FA_TU_ID * 100000 + the line of
+// its FA_PDL_PROLOGUE.
+struct fa_trace_rec {
+    unsigned long long name, start, end, hits;
+};
+static __device__ fa_trace_rec* g_fa_trace;
+__device__ __forceinline__ unsigned long long fa_gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#ifndef FA_TU_ID
+#define FA_TU_ID 0
+#endif
+struct FaTraceGuard {
+    int slot = -1;
+    __device__ FaTraceGuard(unsigned long long key) {
+        if (!g_fa_trace || threadIdx.x != 0) return;
+        int h = (int)(((key >> 4) * 2654435761ull) & 127);
+        for (int k = 0; k < 128; k++, h = (h + 1) & 127) {
+            unsigned long long cur = atomicCAS(&g_fa_trace[h].name, 0ull, key);
+            if (cur == 0ull || cur == key) { slot = h; break; }
+        }
+        if (slot >= 0) {
+            atomicMin(&g_fa_trace[slot].start, fa_gtime());
+            if (blockIdx.x == 0 && blockIdx.y == 0) atomicAdd(&g_fa_trace[slot].hits, 1ull);
+        }
+    }
+    __device__ ~FaTraceGuard() {
+        if (slot >= 0) atomicMax(&g_fa_trace[slot].end, fa_gtime());
+    }
+};
+#define FA_TRACE_TU(tu) \
+    void fa_trace_bind_##tu(void* p) { cudaMemcpyToSymbol(g_fa_trace, &p, sizeof(p)); }
+#define FA_PDL_PROLOGUE() \
+    fa_pdl_wait();        \
+    fa_pdl_trigger();     \
+    FaTraceGuard _fa_trace_guard((unsigned long long)FA_TU_ID * 100000ull + __LINE__)
+#else
+#define FA_TRACE_TU(tu)
 #define FA_PDL_PROLOGUE() \
     do {                  \
         fa_pdl_wait();    \
         fa_pdl_trigger(); \
     } while (0)
+#endif
 
 bool fa_pdl_enabled();  // FASTATLAS_PDL=0 disables (fa_api.cu)
 int fa_env_int(const char* name, int dflt);  // integer knob from the environment (fa_api.cu)

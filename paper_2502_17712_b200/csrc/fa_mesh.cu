@@ -17,6 +17,7 @@
 //
 // Each compaction is count -> one-CTA scan of the per-tile counts ->
 // scatter, so the whole rebinding is O(3T + V) work in eight launches.
+#define FA_TU_ID 8  // trace builds (FA_TRACE): kernel key = TU id + line
 #include "fa_internal.h"
 
 #define MS_THREADS 256
@@ -419,3 +420,5 @@ void fa_launch_cluster_build(const double* pos, const int* tris_sorted, int T, f
     fa_launch(k_cluster_build, fa_grid((long long)((T + 31) / 32) * 32, 256, FA_NUM_SMS * 8), 256, 0, s, pos,
               tris_sorted, T, out);
 }
+
+FA_TRACE_TU(mesh)

@@ -16,6 +16,7 @@
 //   * selection (packing.py:342-345): the largest accepted candidate index.
 // All scale arithmetic is exact integer arithmetic with numpy int64
 // semantics; the snap uses 128-bit intermediates.
+#define FA_TU_ID 5  // trace builds (FA_TRACE): kernel key = TU id + line
 #include "fa_internal.h"
 
 #ifndef PK_THREADS
@@ -1113,3 +1114,5 @@ void fa_launch_orient(const long long* tw, const long long* th, int n, long long
                       unsigned char* rot, cudaStream_t s) {
     fa_launch(k_orient, fa_grid(n, 256, FA_NUM_SMS * 4), 256, 0, s, tw, th, n, ow, oh, rot);
 }
+
+FA_TRACE_TU(pack)

@@ -13,6 +13,7 @@
 // pixel winner.  Pass 2 (visibility) skips the winners, rejects occluded
 // records with an 8x8 hierarchical Z, and replays the stored records.
 // DESIGN.md §2.1 has the full picture.
+#define FA_TU_ID 2  // trace builds (FA_TRACE): kernel key = TU id + line
 #include "fa_internal.h"
 #include "fa_raster.cuh"
 
@@ -988,3 +989,5 @@ void fa_launch_decode_depth(const unsigned long long* keys, double* out, long lo
 void fa_launch_encode_depth(const double* in, unsigned long long* keys, long long n, cudaStream_t s) {
     fa_launch(k_encode_depth, fa_grid(n, 256, FA_NUM_SMS * 8), 256, 0, s, in, keys, n);
 }
+
+FA_TRACE_TU(raster)

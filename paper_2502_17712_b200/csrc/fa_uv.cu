@@ -5,6 +5,7 @@
 // (the CTA's output slab starts at a multiple of 16 bytes).  Rows of
 // triangles with a corner at or behind the camera plane (w <= W_EPSILON,
 // cli.py:433-435) are NaN, as are rows of charts without a placement.
+#define FA_TU_ID 6  // trace builds (FA_TRACE): kernel key = TU id + line
 #include "fa_internal.h"
 
 #define UV_THREADS 256
@@ -188,3 +189,5 @@ void fa_launch_uv(const double4* clip, const int* tris, const int* vis_list, con
         fa_launch(k_uv<float>, grid, UV_THREADS, 0, s, clip, tris, vis_list, label, cidx, pinv, ndc, px, placements, W, H,
                                                 pad, (float*)uv, vis_chart, vis_cidx, plc_c, vis_tris, vslot, vuv, st);
 }
+
+FA_TRACE_TU(uv)
