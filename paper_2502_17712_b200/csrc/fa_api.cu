@@ -119,7 +119,7 @@ void fa_destroy(fa_ctx* c) {
                       &c->target, &c->survived, &c->okey, &c->oidx, &c->ow, &c->oh, &c->orot, &c->sortk, &c->sortv,
                       &c->pinv, &c->cand, &c->cand_p, &c->cand_w, &c->cand_h, &c->cand_y, &c->rowstart,
                       &c->placements, &c->uv, &c->vp_dev, &c->blocks, &c->dstat, &c->aux, &c->in_tw, &c->in_th,
-                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list, &c->hiz, &c->wid, &c->vis_chart, &c->vis_cidx, &c->plc_c, &c->pos_perm, &c->tris_perm, &c->vperm_buf, &c->vis_tris, &c->vslot, &c->vlist, &c->vuv, &c->vblocks, &c->pstat, &c->tperm_buf, &c->tris_sorted_buf, &c->clusters_buf, &c->live_buf, &c->mesh_first, &c->mesh_scratch, &c->mesh_sort, &c->mesh_tris_s, &c->ord_tw, &c->ord_th, &c->ord_cid};
+                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list, &c->hiz, &c->wid, &c->vis_chart, &c->vis_cidx, &c->plc_c, &c->pos_perm, &c->tris_perm, &c->vperm_buf, &c->vis_tris, &c->vslot, &c->vlist, &c->vuv, &c->vblocks, &c->pstat, &c->tperm_buf, &c->tris_sorted_buf, &c->clusters_buf, &c->live_buf, &c->mesh_first, &c->mesh_scratch, &c->mesh_sort, &c->mesh_tris_s, &c->ord_tw, &c->ord_th, &c->ord_cid, &c->ndc2};
     for (fa_buf* b : bufs) free_buf(*b);
     for (cudaEvent_t e : c->fj)
         if (e) cudaEventDestroy(e);
@@ -264,6 +264,7 @@ static int ensure_raster(fa_ctx* ctx, int W, int H, bool depth) {
     int64_t T = ctx->T, V = ctx->V;
     ENSURE(clip, (V > 0 ? V : 1) * sizeof(double4));
     ENSURE(scr, (V > 0 ? V : 1) * sizeof(double4));
+    ENSURE(ndc2, (V > 0 ? V : 1) * sizeof(double2));
     if (depth) ENSURE(depth_keys, (size_t)W * H * 8);
     if (depth && T < (1 << 24)) ENSURE(wid, (size_t)W * H * 8);
     ENSURE(hiz, (size_t)fa_hiz_dim(W) * fa_hiz_dim(H) * 8);
@@ -1027,7 +1028,7 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     const fa_setup_order ord = setup_order(ctx);
     fa_launch_cluster_cull(P<double>(ctx->vp_dev), W, H, cull_args(ctx, p->backface_cull), s);
     fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), P<double4>(ctx->scr), W, H,
-                         P<int>(ctx->vmin), nullptr, nullptr, 0, flags, T, s);
+                         P<int>(ctx->vmin), nullptr, nullptr, 0, flags, T, s, 0, P<double2>(ctx->ndc2));
     nl += ord.live ? 3 : 2;
     mark();  // 1: project + clears
     nl += fa_launch_depth_pass(true, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, W, H,
@@ -1073,7 +1074,7 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     mark();  // 6: chart roots (+ flatten)
     fa_launch_chart_bounds(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->label),
                            P<int>(ctx->cidx), T, P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), st, s,
-                           P<int>(ctx->vis_cidx), P<int4>(ctx->vis_tris));
+                           P<int>(ctx->vis_cidx), P<int4>(ctx->vis_tris), P<double2>(ctx->ndc2));
     nl += 1;
     mark();  // 7: chart bounds (the box dims run at the head of the order kernel)
     fa_pack_bufs b = pack_bufs(ctx, P<long long>(ctx->in_tw), P<long long>(ctx->in_th), P<long long>(ctx->in_cid),
@@ -1102,7 +1103,7 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
                  P<int>(ctx->pinv), P<double>(ctx->ndc), P<int>(ctx->px), P<long long>(ctx->placements), T, W, H,
                  p->padding, p->uv_f64 != 0, ctx->uv.p, P<int>(ctx->vis_chart), P<int>(ctx->vis_cidx),
                  p->packer == FA_PACKER_FASTATLAS ? P<int4>(ctx->plc_c) : nullptr, st, s, P<int4>(ctx->vis_tris),
-                 P<int>(ctx->vslot), P<float2>(ctx->vuv));
+                 P<int>(ctx->vslot), P<float2>(ctx->vuv), P<double2>(ctx->ndc2));
     nl += 1;
     mark();  // 10: uv
     if (p->want_depth) {

@@ -128,7 +128,8 @@ __global__ void __launch_bounds__(256) k_chart_bounds(const double4* __restrict_
                                                       const int* __restrict__ cidx,
                                                       unsigned long long* __restrict__ keys,
                                                       int* __restrict__ survived, const fa_dstat* __restrict__ st,
-                                                      int* __restrict__ vis_cidx, const int4* __restrict__ vis_tris) {
+                                                      int* __restrict__ vis_cidx, const int4* __restrict__ vis_tris,
+                                                      const double2* __restrict__ ndc2) {
     FA_PDL_PROLOGUE();
     int n = st->n_vis;
     int lane = lane_id();
@@ -140,23 +141,45 @@ __global__ void __launch_bounds__(256) k_chart_bounds(const double4* __restrict_
         unsigned long long k0 = FA_KEY_POS_INF, k1 = FA_KEY_POS_INF, k2 = FA_KEY_NEG_INF, k3 = FA_KEY_NEG_INF;
         int surv = 0;
         if (k < n) {
-            double4 cc[3];
             int t;
+            NBox b = empty_box();
+            bool got = false;
             if (vis_tris) {  // vertex indices next to the id: one dependent load fewer
                 const int4 q = vis_tris[k];
                 t = q.w;
-                cc[0] = ldg4(clip + q.x);
-                cc[1] = ldg4(clip + q.y);
-                cc[2] = ldg4(clip + q.z);
+                c = cidx[label[t]];
+                if (ndc2) {
+                    // every vertex strictly inside the frustum (vertex_ndc not
+                    // NaN): no side plane is crossed and the Blinn clamp is the
+                    // plain division, so the box is the vertices' NDC, added in
+                    // the same order and comparisons as tri_box's blinn_add
+                    const double2 n0 = __ldg(ndc2 + q.x), n1 = __ldg(ndc2 + q.y), n2 = __ldg(ndc2 + q.z);
+                    if (!isnan(n0.x) && !isnan(n1.x) && !isnan(n2.x)) {
+                        const double2 nn[3] = {n0, n1, n2};
+#pragma unroll
+                        for (int i = 0; i < 3; i++) {
+                            if (nn[i].x < b.mnx) b.mnx = nn[i].x;
+                            if (nn[i].y < b.mny) b.mny = nn[i].y;
+                            if (nn[i].x > b.mxx) b.mxx = nn[i].x;
+                            if (nn[i].y > b.mxy) b.mxy = nn[i].y;
+                        }
+                        got = true;
+                    }
+                }
+                if (!got) {
+                    double4 cc[3] = {ldg4(clip + q.x), ldg4(clip + q.y), ldg4(clip + q.z)};
+                    got = tri_box(cc, b);
+                }
             } else {
                 t = vis_list[k];
+                double4 cc[3];
 #pragma unroll
                 for (int j = 0; j < 3; j++) cc[j] = ldg4(clip + __ldg(tris + 3 * t + j));
+                c = cidx[label[t]];
+                got = tri_box(cc, b);
             }
-            c = cidx[label[t]];
             if (vis_cidx) vis_cidx[k] = c;  // k_uv's chart index (saves it two dependent loads)
-            NBox b = empty_box();
-            if (tri_box(cc, b)) {
+            if (got) {
                 surv = 1;
                 k0 = f64_key(b.mnx);
                 k1 = f64_key(b.mny);
@@ -214,9 +237,9 @@ __global__ void k_box_dims(const unsigned long long* __restrict__ keys, const in
 
 void fa_launch_chart_bounds(const double4* clip, const int* tris, const int* vis_list, const int* label,
                             const int* cidx, int T, unsigned long long* ndc_keys, int* survived, const fa_dstat* st,
-                            cudaStream_t s, int* vis_cidx, const int4* vis_tris) {
+                            cudaStream_t s, int* vis_cidx, const int4* vis_tris, const double2* ndc2) {
     fa_launch(k_chart_bounds, fa_grid(T, 256, FA_NUM_SMS * 8), 256, 0, s, clip, tris, vis_list, label, cidx, ndc_keys,
-              survived, st, vis_cidx, vis_tris);
+              survived, st, vis_cidx, vis_tris, vis_tris ? ndc2 : nullptr);
 }
 
 void fa_launch_box_dims(const unsigned long long* ndc_keys, const int* survived, const int* roots, int T, int W, int H,

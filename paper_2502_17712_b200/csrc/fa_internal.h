@@ -89,6 +89,7 @@ struct fa_ctx {
     fa_buf tperm_buf, tris_sorted_buf, clusters_buf, live_buf;
     fa_buf mesh_first, mesh_scratch, mesh_sort, mesh_tris_s;  // fa_set_mesh scratch
     fa_buf ord_tw, ord_th, ord_cid;  // per packing position (k_order_frame -> k_select)
+    fa_buf ndc2;                     // per-vertex NDC of the inside vertices (vertex_ndc), for bounds and UVs
 
     // scratch (grown on demand)
     fa_buf small_rec, clip, depth_keys, depth_f64, flags, vis_list, large, tiles, label, vmin, v2c, cidx;
@@ -141,7 +142,8 @@ bool fa_ensure(fa_ctx* ctx, fa_buf& b, size_t bytes);
 // wid (may be null): pass-1 winner buffer, cleared to all ones with depth
 void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* clip, double4* scr, int W, int H,
                           int* vmin, unsigned long long* depth, unsigned long long* wid, long long npx,
-                          unsigned char* flags, int T, cudaStream_t s, int max_blocks = 0);
+                          unsigned char* flags, int T, cudaStream_t s, int max_blocks = 0,
+                          double2* ndc2 = nullptr);
 // the setup's live-cluster list (no-op when cu.clusters is null)
 void fa_launch_cluster_cull(const double* vp, int W, int H, const fa_cull_args& cu, cudaStream_t s);
 // side == nullptr: everything on s; otherwise fork/join through the events.
@@ -217,7 +219,7 @@ void fa_launch_cluster_build(const double* pos, const int* tris_sorted, int T, f
 // ---- bounds (fa_bounds.cu) -----------------------------------------------
 void fa_launch_chart_bounds(const double4* clip, const int* tris, const int* vis_list, const int* label,
                             const int* cidx, int T, unsigned long long* ndc_keys, int* survived, const fa_dstat* st,
-                            cudaStream_t s, int* vis_cidx = nullptr, const int4* vis_tris = nullptr);
+                            cudaStream_t s, int* vis_cidx = nullptr, const int4* vis_tris = nullptr, const double2* ndc2 = nullptr);
 void fa_launch_box_dims(const unsigned long long* ndc_keys, const int* survived, const int* roots, int T, int W, int H,
                         double prescale, double* ndc, int* px, long long* target, long long* tw, long long* th,
                         long long* cid, int cap, fa_dstat* st, cudaStream_t s);
@@ -277,7 +279,7 @@ void fa_launch_uv(const double4* clip, const int* tris, const int* vis_list, con
                   const int* pinv, const double* ndc, const int* px, const long long* placements, int T, int W, int H,
                   long long pad, bool f64, void* uv, int* vis_chart, const int* vis_cidx, const int4* plc_c,
                   fa_dstat* st, cudaStream_t s, const int4* vis_tris = nullptr, const int* vslot = nullptr,
-                  float2* vuv = nullptr);
+                  float2* vuv = nullptr, const double2* ndc2 = nullptr);
 
 // ---- comparison packers (fa_baselines.cu) -----------------------------------
 void fa_launch_seq_search(const long long* ow, const long long* oh, int n, long long omega, long long n_scales,

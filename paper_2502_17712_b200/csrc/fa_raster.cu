@@ -67,7 +67,7 @@ __global__ void k_frame_init(const double* __restrict__ pos, int V, const double
                              double4* __restrict__ clip, double4* __restrict__ scr, int W, int H,
                              int* __restrict__ vmin, unsigned long long* __restrict__ depth,
                              unsigned long long* __restrict__ wid, long long npx,
-                             unsigned int* __restrict__ flags32, int nflag32) {
+                             unsigned int* __restrict__ flags32, int nflag32, double2* __restrict__ ndc2) {
     FA_PDL_PROLOGUE();
     long long stride = (long long)gridDim.x * blockDim.x;
     long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -78,6 +78,7 @@ __global__ void k_frame_init(const double* __restrict__ pos, int V, const double
         double x = pos[3 * v], y = pos[3 * v + 1], z = pos[3 * v + 2];
         double4 c = project_point(x, y, z, m);
         clip[v] = c;
+        if (ndc2) ndc2[v] = vertex_ndc(c);
         if (scr) scr[v] = vertex_screen(c, W, H);
         if (vmin) vmin[v] = 0x7fffffff;
     }
@@ -897,13 +898,13 @@ __global__ void __launch_bounds__(256) k_raster_vis_tiles(const SmallRec* __rest
 // ---- host launchers -------------------------------------------------------
 void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* clip, double4* scr, int W, int H,
                           int* vmin, unsigned long long* depth, unsigned long long* wid, long long npx,
-                          unsigned char* flags, int T, cudaStream_t s, int max_blocks) {
+                          unsigned char* flags, int T, cudaStream_t s, int max_blocks, double2* ndc2) {
     long long work = V;
     if (depth && npx / 2 > work) work = npx / 2;
     int nflag32 = flags ? (T + 3) / 4 : 0;
     if (nflag32 > work) work = nflag32;
     fa_launch(k_frame_init, fa_grid(work, 256, max_blocks > 0 ? max_blocks : FA_NUM_SMS * 8), 256, 0, s, 
-        pos, V, vp, clip, scr, W, H, vmin, depth, wid, npx, reinterpret_cast<unsigned int*>(flags), nflag32);
+        pos, V, vp, clip, scr, W, H, vmin, depth, wid, npx, reinterpret_cast<unsigned int*>(flags), nflag32, ndc2);
 }
 
 // fork `side` off `s` (side waits for everything issued on s so far)

@@ -452,6 +452,22 @@ __device__ __forceinline__ double4 vertex_screen(double4 c, int W, int H) {
     return o;
 }
 
+// Per-vertex NDC (x/w, y/w) of a vertex strictly inside every frustum plane
+// (w - W_EPSILON > 0 and all six d >= 0), NaN otherwise.  For such a vertex
+// the chart-bounds Blinn clamp (geometry.py:185-200) is the plain division
+// and the UV emission's ndc (cli.py:436-439) is the same division, so both
+// read these bits instead of dividing again per triangle.
+__device__ __forceinline__ double2 vertex_ndc(double4 c) {
+    const bool inside = __dsub_rn(c.w, FA_W_EPSILON) > 0 && __dadd_rn(c.w, c.x) >= 0 && __dsub_rn(c.w, c.x) >= 0 &&
+                        __dadd_rn(c.w, c.y) >= 0 && __dsub_rn(c.w, c.y) >= 0 && __dadd_rn(c.w, c.z) >= 0 &&
+                        __dsub_rn(c.w, c.z) >= 0;
+    if (!inside) {
+        const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+        return make_double2(qnan, qnan);
+    }
+    return make_double2(__ddiv_rn(c.x, c.w), __ddiv_rn(c.y, c.w));
+}
+
 // 1 = Setup3 filled, 0 = no samples, 2 = needs the generic (clipping) path.
 // Same decisions as tri_setup3 below, from the per-vertex screen records.
 __device__ __forceinline__ int tri_setup3s(const double4* __restrict__ scr, int ia, int ib, int ic, int W, int H,

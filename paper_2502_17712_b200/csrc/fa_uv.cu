@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
                                                    int* __restrict__ vis_chart, const int* __restrict__ vis_cidx,
                                                    const int4* __restrict__ plc_c, const int4* __restrict__ vis_tris,
                                                    const int* __restrict__ vslot, float2* __restrict__ vuv,
-                                                   fa_dstat* __restrict__ st) {
+                                                   fa_dstat* __restrict__ st, const double2* __restrict__ ndc2) {
     FA_PDL_PROLOGUE();
     __shared__ __align__(16) OutT stage[UV_THREADS * 6];
     __shared__ double red_w[UV_THREADS / 32], red_a[UV_THREADS / 32], red_m[UV_THREADS / 32];
@@ -66,12 +66,30 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
             // chart index and placement straight from the bounds / select
             // side outputs when present (two dependent loads instead of four)
             int c = vis_cidx ? vis_cidx[k] : cidx[label[t]];
+            double nxs[3], nys[3];
+            bool behind = false, fast = false;
+            if (ndc2 && vis_tris) {
+                // all three vertices strictly inside the frustum: their NDC
+                // divisions were done once per vertex (vertex_ndc, same bits)
+                const double2 n0 = __ldg(ndc2 + vq.x), n1 = __ldg(ndc2 + vq.y), n2 = __ldg(ndc2 + vq.z);
+                fast = !isnan(n0.x) && !isnan(n1.x) && !isnan(n2.x);
+                nxs[0] = n0.x; nxs[1] = n1.x; nxs[2] = n2.x;
+                nys[0] = n0.y; nys[1] = n1.y; nys[2] = n2.y;
+            }
             double4 v[3];
-            bool behind = false;
+            if (!fast) {
 #pragma unroll
-            for (int i = 0; i < 3; i++) {
-                v[i] = ldg4(clip + (vis_tris ? (i == 0 ? vq.x : (i == 1 ? vq.y : vq.z)) : __ldg(tris + 3 * t + i)));
-                if (v[i].w <= FA_W_EPSILON) behind = true;
+                for (int i = 0; i < 3; i++) {
+                    v[i] = ldg4(clip + (vis_tris ? (i == 0 ? vq.x : (i == 1 ? vq.y : vq.z)) : __ldg(tris + 3 * t + i)));
+                    if (v[i].w <= FA_W_EPSILON) behind = true;
+                }
+                if (!behind) {
+#pragma unroll
+                    for (int i = 0; i < 3; i++) {
+                        nxs[i] = __ddiv_rn(v[i].x, v[i].w);
+                        nys[i] = __ddiv_rn(v[i].y, v[i].w);
+                    }
+                }
             }
             if (behind && vuv) {
                 // a vertex at or behind the camera plane makes every row it is
@@ -103,7 +121,7 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
                 double scr[6];
 #pragma unroll
                 for (int i = 0; i < 3; i++) {
-                    double nx = __ddiv_rn(v[i].x, v[i].w), ny = __ddiv_rn(v[i].y, v[i].w);
+                    const double nx = nxs[i], ny = nys[i];
                     double u = __dmul_rn(__dmul_rn(__dsub_rn(nx, mnx), 0.5), (double)W);
                     double vv = __dmul_rn(__dmul_rn(__dsub_rn(ny, mny), 0.5), (double)H);
                     out[2 * i] = __dadd_rn(bx, __dmul_rn(rot ? vv : u, rx));
@@ -179,15 +197,16 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
 void fa_launch_uv(const double4* clip, const int* tris, const int* vis_list, const int* label, const int* cidx,
                   const int* pinv, const double* ndc, const int* px, const long long* placements, int T, int W, int H,
                   long long pad, bool f64, void* uv, int* vis_chart, const int* vis_cidx, const int4* plc_c,
-                  fa_dstat* st, cudaStream_t s, const int4* vis_tris, const int* vslot, float2* vuv) {
+                  fa_dstat* st, cudaStream_t s, const int4* vis_tris, const int* vslot, float2* vuv,
+                  const double2* ndc2) {
     if (!vis_tris) vuv = nullptr;  // the compact UVs index vertices through vis_tris
     int grid = fa_grid(T, UV_THREADS, FA_NUM_SMS * 8);
     if (f64)
         fa_launch(k_uv<double>, grid, UV_THREADS, 0, s, clip, tris, vis_list, label, cidx, pinv, ndc, px, placements, W, H,
-                                                 pad, (double*)uv, vis_chart, vis_cidx, plc_c, vis_tris, vslot, vuv, st);
+                                                 pad, (double*)uv, vis_chart, vis_cidx, plc_c, vis_tris, vslot, vuv, st, ndc2);
     else
         fa_launch(k_uv<float>, grid, UV_THREADS, 0, s, clip, tris, vis_list, label, cidx, pinv, ndc, px, placements, W, H,
-                                                pad, (float*)uv, vis_chart, vis_cidx, plc_c, vis_tris, vslot, vuv, st);
+                                                pad, (float*)uv, vis_chart, vis_cidx, plc_c, vis_tris, vslot, vuv, st, ndc2);
 }
 
 FA_TRACE_TU(uv)
