@@ -524,24 +524,25 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const SmallRec* __re
 // window averages ~20 samples for ~1.5 covered ones.  Depth pass only
 // (RED.MIN.64 per covered sample).
 #define COOP_WARPS 4
-#ifndef COOP_MIN_BLOCKS
-#define COOP_MIN_BLOCKS 6
+#ifndef COOP_GRID_MULT
+#define COOP_GRID_MULT 3  // one wave: the resident CTAs loop (persistent)
 #endif
-struct CoopWarp {
-    SmallRec rec[2][32];  // double buffer: the next 32 records stream in (cp.async) during the current ones
+#ifndef COOP_MIN_BLOCKS
+#define COOP_MIN_BLOCKS 3
+#endif
+struct __align__(16) CoopWarp {
+    SmallRec rec[2][32];  // double buffer: the next 32 records stream in (one bulk copy) during the current ones
+    unsigned long long bar[2];  // bulk-copy completion, one mbarrier per buffer
     int prefix[33];
     SpanEdges se[32];     // each record's span reciprocals, computed once by the lane that owns it
 };
 
 
-__device__ __forceinline__ void coop_issue(const SmallRec* __restrict__ recs, int base, int n, SmallRec* dst) {
-    const int lane = lane_id();
-    if (base + lane < n) {
-        const char* src = reinterpret_cast<const char*>(recs + base + lane);
-        char* d = reinterpret_cast<char*>(dst + lane);
-#pragma unroll
-        for (int q = 0; q < (int)(sizeof(SmallRec) / 16); q++) cp_async16(d + 16 * q, src + 16 * q);
-    }
+// records [base, base + 32) (clipped to n) -> dst: one bulk copy by lane 0
+__device__ __forceinline__ void coop_issue(const SmallRec* __restrict__ recs, int base, int n, SmallRec* dst,
+                                           unsigned long long* bar) {
+    if (lane_id() == 0 && base < n)
+        bulk_g2s(dst, recs + base, (unsigned)(min(32, n - base) * sizeof(SmallRec)), bar);
 }
 
 __global__ void __launch_bounds__(COOP_WARPS * 32, COOP_MIN_BLOCKS) k_small_coop(const SmallRec* __restrict__ recs, int W,
@@ -556,13 +557,16 @@ __global__ void __launch_bounds__(COOP_WARPS * 32, COOP_MIN_BLOCKS) k_small_coop
     const int stride = gridDim.x * COOP_WARPS * 32;
     int base = ((int)blockIdx.x * COOP_WARPS + warp) * 32;
     int buf = 0;
-    coop_issue(recs, base, n, cw.rec[0]);
-    cp_async_commit();
-    for (; base < n; base += stride, buf ^= 1) {
-        coop_issue(recs, base + stride, n, cw.rec[buf ^ 1]);
-        cp_async_commit();
-        cp_async_wait1();
-        __syncwarp();
+    if (lane == 0) {
+        mbar_init(&cw.bar[0], 1);
+        mbar_init(&cw.bar[1], 1);
+        fence_async_shared();
+    }
+    __syncwarp();
+    coop_issue(recs, base, n, cw.rec[0], &cw.bar[0]);
+    for (int it = 0; base < n; base += stride, buf ^= 1, it++) {
+        coop_issue(recs, base + stride, n, cw.rec[buf ^ 1], &cw.bar[buf ^ 1]);
+        mbar_wait(&cw.bar[buf], (it >> 1) & 1);  // use it>>1 of this buffer
         const SmallRec* rb = cw.rec[buf];
         const int cnt = min(32, n - base);
         int np = 0;
@@ -944,8 +948,8 @@ int fa_launch_depth_pass(bool write_depth, const double4* clip, const double4* s
                   large, max_large, tiles, max_tiles, st);
         fa_launch(k_raster_depth_tiles, fa_cap(FA_NUM_SMS * 4), 256, 0, b2, small_rec, large, tiles, W, depth, wid, st,
                   max_tiles, 0, 1, 1);
-        fa_launch(k_small_coop, fa_grid((long long)T, COOP_WARPS * 32 * 2, FA_NUM_SMS * 12), COOP_WARPS * 32, 0, s,
-                  small_rec, W, depth, wid, st);
+        fa_launch(k_small_coop, fa_grid((long long)T, COOP_WARPS * 32 * 2, FA_NUM_SMS * COOP_GRID_MULT), COOP_WARPS * 32, 0,
+                  s, small_rec, W, depth, wid, st);
         n = 5;
     } else {
         fa_launch(k_raster_clipped<false>, fa_cap(FA_NUM_SMS * 2), 256, 0, b, clip, tris, W, H, cull, clip_list, depth,
