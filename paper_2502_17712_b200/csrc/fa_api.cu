@@ -61,6 +61,13 @@ bool fa_ensure(fa_ctx* ctx, fa_buf& b, size_t bytes) {
     return true;
 }
 
+// value of a fixed-point digit accumulator (fx_add), rounded to double
+static double fx_value(const unsigned long long (&acc)[FA_FX_DIGITS]) {
+    double v = 0.0;
+    for (int k = FA_FX_DIGITS - 1; k >= 0; k--) v += ldexp((double)acc[k], 32 * k - 80);
+    return v;
+}
+
 #define ENSURE(buf, n)                                                                     \
     do {                                                                                   \
         if (!fa_ensure(ctx, ctx->buf, (size_t)(n)))                                        \
@@ -1224,7 +1231,12 @@ int fa_frame_finish(fa_ctx* ctx, fa_frame_result* out, void* stream) {
         double linf;
         memcpy(&linf, &h->stretch_linf_bits, sizeof(linf));
         out->stretch_linf = h->stretch_valid ? linf : 0.0;
-        out->stretch_l2 = (h->stretch_valid && h->stretch_area > 0) ? sqrt(h->stretch_wsum / h->stretch_area) : 0.0;
+        double wsum = h->stretch_wsum, area = h->stretch_area;
+        if (!(h->flags & FA_DFLAG_STRETCH_RANGE)) {
+            wsum = fx_value(h->stretch_fx[0]);
+            area = fx_value(h->stretch_fx[1]);
+        }
+        out->stretch_l2 = (h->stretch_valid && area > 0) ? sqrt(wsum / area) : 0.0;
     }
     out->depth = ctx->last_params.want_depth ? P<double>(ctx->depth_f64) : nullptr;
     out->flags = P<uint8_t>(ctx->flags);

@@ -31,6 +31,8 @@
 #define FA_DFLAG_DUPLICATE_MIN_TRI 32u
 #define FA_DFLAG_KEY_RANGE 64u
 #define FA_DFLAG_BAD_ARGS 128u
+#define FA_FX_DIGITS 6
+#define FA_DFLAG_STRETCH_RANGE 256u  // a stretch partial outside [2^-80, 2^111): report the float sums
 
 // Per-frame device counters and status (zeroed per frame).  The four append
 // counters of k_raster_setup take one atomic per block step each (~4K per
@@ -55,11 +57,16 @@ struct fa_dstat {
     int n_tiles_clip;     // tiles of clipped (generic) setups, stored downward from max_tiles - 1
     int n_vis_vertices;   // vertices touched by a visible triangle (compact UV format)
     int pad_v;
-    double stretch_wsum;  // sum area * (S1^2 + S2^2) / 2   (metrics.py:103)
-    double stretch_area;  // sum area                       (metrics.py:104)
+    double stretch_wsum;  // sum area * (S1^2 + S2^2) / 2   (metrics.py:103) — used only on FA_DFLAG_STRETCH_RANGE
+    double stretch_area;  // sum area                       (metrics.py:104) — ditto
     unsigned long long stretch_linf_bits;  // max S1 (positive double bits)
     int n_live;           // 32-triangle clusters the setup processes (k_frame_init's cluster culling)
-    int pad0[35];
+    int pad_l;
+    // the same two sums in exact fixed point (units of 2^-80, 32-bit digits
+    // in six u64 counters each, fx_add): integer adds commute, so the sums
+    // are run-to-run reproducible (k_uv adds one truncated partial per block)
+    unsigned long long stretch_fx[2][FA_FX_DIGITS];
+    int pad0[10];
     int n_small3;         // stored small-triangle records (pass 2 input)
     int pad1[63];
     int n_large3;         // compact large-triangle records (stored from the back of the record array)
@@ -69,6 +76,7 @@ struct fa_dstat {
     int n_tiles;          // large-raster tile work items
     int pad4[63];
 };
+static_assert(offsetof(fa_dstat, stretch_fx) % 8 == 0, "fa_dstat: aligned fixed-point limbs");
 static_assert(sizeof(fa_dstat) == 1280, "fa_dstat: a 256-byte status block + four 256-byte counter slots");
 
 // ---- float64 <-> order-preserving u64 key --------------------------------
@@ -218,6 +226,35 @@ __device__ __forceinline__ long long block_sum_ll(long long v, long long* smem32
     }
     __syncthreads();
     return smem32[32];
+}
+
+// ---- exact fixed-point accumulation (reproducible sums) ----------------
+// acc += v truncated to a multiple of 2^-80.  The fixed-point value is cut
+// into 32-bit digits and digit k is added to the 64-bit counter acc[k]
+// (value = sum_k acc[k] * 2^(32k - 80)); counters cannot overflow below 2^32
+// adds, so no carries are needed and every add is a fire-and-forget RED.
+// Integer adds commute: the sum does not depend on their order.
+// Returns false when v is negative, NaN or >= 2^111 (not representable).
+__device__ __forceinline__ bool fx_add(unsigned long long* acc, double v) {
+    if (v == 0.0) return true;
+    if (!(v > 0.0) || v >= 0x1p111) return false;
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+    const int be = (int)(bits >> 52);                                    // biased exponent (v > 0)
+    if (be == 0) return true;                                            // subnormal: below 2^-80
+    unsigned long long m = (bits & 0xFFFFFFFFFFFFFull) | (1ull << 52);  // v = m * 2^(be - 1075)
+    int sh = be - 1075 + 80;                                             // accumulator bit of m's LSB
+    if (sh < 0) {
+        if (sh <= -64) return true;                                      // below 2^-80
+        m >>= -sh;
+        sh = 0;
+    }
+    const int k = sh >> 5, r = sh & 31;                                  // digit k, bit r (k <= 4)
+    // m << r spans at most 85 bits: digits k, k+1, k+2
+    atomicAdd(acc + k, (m << r) & 0xFFFFFFFFull);
+    const unsigned long long d1 = (m >> (32 - r)) & 0xFFFFFFFFull, d2 = r ? m >> (64 - r) : 0ull;
+    if (d1) atomicAdd(acc + k + 1, d1);
+    if (d2 && k + 2 < FA_FX_DIGITS) atomicAdd(acc + k + 2, d2);  // (d2 == 0 for k == 4: v < 2^111)
+    return true;
 }
 
 // ---- cp.async (LDGSTS): global -> shared copies that complete in the background

@@ -186,6 +186,10 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
             c += red_c[i];
         }
         if (c) {
+            // exact fixed-point sums (reproducible); the float sums are kept
+            // for partials outside the fixed-point range
+            if (!fx_add(st->stretch_fx[0], w) || !fx_add(st->stretch_fx[1], a))
+                atomicOr(&st->flags, FA_DFLAG_STRETCH_RANGE);
             atomicAdd(&st->stretch_wsum, w);
             atomicAdd(&st->stretch_area, a);
             atomicMax(&st->stretch_linf_bits, (unsigned long long)__double_as_longlong(m));

@@ -434,6 +434,20 @@ def test_full_size_vs_oracle(cfg):
     assert grid.max() <= 1
 
 
+def test_stretch_sums_are_reproducible():
+    """k_uv adds its per-block stretch partials in a fixed order (last block),
+    so repeated frames report bit-identical L2 / Linf stretch."""
+    spec = scenes.build_scene("C2")
+    eng = FrameEngine(fa.Mesh(spec.positions, spec.triangles),
+                      settings=FrameSettings(screen=spec.screen, omega=spec.omega))
+    vp = _scene_vp(spec, spec.poses[0])
+    seen = set()
+    for _ in range(5):
+        st = eng.run(vp).stretch()
+        seen.add((np.float64(st.l2).tobytes(), np.float64(st.linf).tobytes()))
+    assert len(seen) == 1
+
+
 def _check_vs_oracle(h, r, status_ok=True):
     assert np.array_equal(h["flags"].astype(bool), r.flags)
     assert np.array_equal(h["chart_of_triangle"].astype(np.int64), r.chart_of_triangle)
