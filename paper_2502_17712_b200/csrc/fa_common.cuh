@@ -66,7 +66,8 @@ struct fa_dstat {
     // in six u64 counters each, fx_add): integer adds commute, so the sums
     // are run-to-run reproducible (k_uv adds one truncated partial per block)
     unsigned long long stretch_fx[2][FA_FX_DIGITS];
-    int pad0[10];
+    int n_vis_q2;         // larger small records the visibility filter left for warp sampling
+    int pad0[9];
     int n_small3;         // stored small-triangle records (pass 2 input)
     int pad1[63];
     int n_large3;         // compact large-triangle records (stored from the back of the record array)

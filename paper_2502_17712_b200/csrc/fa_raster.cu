@@ -17,8 +17,11 @@
 #include "fa_internal.h"
 #include "fa_raster.cuh"
 
+#ifndef FA_VIS_WARP_PX
+#define FA_VIS_WARP_PX 48  // pass-2 survivors with larger windows are sampled a warp per record
+#endif
 #ifndef FA_SMALL_PX
-#define FA_SMALL_PX 48
+#define FA_SMALL_PX 96
 #endif
 #define TILE_W 16
 #define TILE_H 8
@@ -643,13 +646,13 @@ __global__ void __launch_bounds__(256) k_vis_small_filter(const SmallRec* __rest
                                                           const unsigned char* __restrict__ flags,
                                                           int* __restrict__ queue, fa_dstat* __restrict__ st) {
     FA_PDL_PROLOGUE();
-    __shared__ int s_cnt[8], s_base;
+    __shared__ int s_cnt[2][8], s_base[2];
     const int n3 = st->n_small3;
     const int lane = lane_id(), warp = threadIdx.x >> 5;
     const int* __restrict__ ids = small_ids(small_rec, T);
     for (int b0 = (int)blockIdx.x * blockDim.x; b0 < n3; b0 += gridDim.x * blockDim.x) {
         const int i = b0 + threadIdx.x;
-        bool need = false;
+        bool need = false, wide = false;
         // the triangle id first: a record whose triangle is already flagged
         // (a pass-1 pixel winner) is never read
         const unsigned char seen = i < n3 ? flags[__ldg(ids + i)] : 1;
@@ -670,33 +673,48 @@ __global__ void __launch_bounds__(256) k_vis_small_filter(const SmallRec* __rest
                 h11 = __ldg(hiz + ty1 * htx + tx1);
             }
             const double zlb = depth_lower_bound(f, f.min_x, f.max_x, f.min_y, f.max_y);
-            need = !seen && !(hz && hiz_tile_rejects(h00, zlb) && hiz_tile_rejects(h01, zlb) &&
-                              hiz_tile_rejects(h10, zlb) && hiz_tile_rejects(h11, zlb));
+            if (hz)
+                need = !(hiz_tile_rejects(h00, zlb) && hiz_tile_rejects(h01, zlb) && hiz_tile_rejects(h10, zlb) &&
+                         hiz_tile_rejects(h11, zlb));
+            else  // windows over more than 2x2 hi-Z tiles: up to 3x3 tested, else sampled
+                need = tx1 - tx0 > 2 || ty1 - ty0 > 2 ||
+                       !hiz_rejects(hiz, htx, f.min_x, f.max_x, f.min_y, f.max_y, zlb);
+            wide = (f.max_x - f.min_x + 1) * (f.max_y - f.min_y + 1) > FA_VIS_WARP_PX;
 #ifdef FA_HIZ_STATS
             if (!seen) atomicAdd(&g_hiz_stats[need ? 1 : 0], 1ull);
 #endif
         }
-        const unsigned m = __ballot_sync(0xffffffffu, need);
-        if (lane == 0) s_cnt[warp] = __popc(m);
+        const unsigned m = __ballot_sync(0xffffffffu, need && !wide);
+        const unsigned m2 = __ballot_sync(0xffffffffu, need && wide);
+        if (lane == 0) {
+            s_cnt[0][warp] = __popc(m);
+            s_cnt[1][warp] = __popc(m2);
+        }
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if (threadIdx.x < 2) {
             int tot = 0;
-            for (int w = 0; w < 8; w++) tot += s_cnt[w];
-            s_base = tot ? atomicAdd(&st->n_vis_q, tot) : 0;
+            for (int w = 0; w < 8; w++) tot += s_cnt[threadIdx.x][w];
+            s_base[threadIdx.x] = tot ? atomicAdd(threadIdx.x ? &st->n_vis_q2 : &st->n_vis_q, tot) : 0;
         }
         __syncthreads();
         if (need) {
-            int off = s_base + __popc(m & ((1u << lane) - 1u));
-            for (int w = 0; w < warp; w++) off += s_cnt[w];
-            queue[off] = i;
+            // thread-sampled survivors from the front of the queue, warp-sampled
+            // ones downward from index T (together at most n_small3 <= T)
+            const unsigned mm = wide ? m2 : m;
+            int off = s_base[wide] + __popc(mm & ((1u << lane) - 1u));
+            for (int w = 0; w < warp; w++) off += s_cnt[wide][w];
+            queue[wide ? T - off : off] = i;
         }
         __syncthreads();
     }
 }
 
-// Survivors of the filter, one thread each: sample the row spans, stopping
-// at the first passing sample; up to 4 covered samples per batch of depth loads.
-__global__ void __launch_bounds__(256) k_vis_small_sample(const SmallRec* __restrict__ small_rec, int W,
+// Survivors of the filter.  Thread queue: one thread each, sample the row
+// spans, stopping at the first passing sample; up to 4 covered samples per
+// batch of depth loads.  Warp queue (windows above FA_VIS_WARP_PX): one warp
+// per record, the window's samples dealt over the lanes (<= FA_SMALL_PX / 32
+// each, their depth loads issued together).
+__global__ void __launch_bounds__(256) k_vis_small_sample(const SmallRec* __restrict__ small_rec, int T, int W,
                                                           const unsigned long long* __restrict__ depth,
                                                           const int* __restrict__ queue,
                                                           unsigned char* __restrict__ flags,
@@ -742,6 +760,33 @@ __global__ void __launch_bounds__(256) k_vis_small_sample(const SmallRec* __rest
                   (nq > 2 && depth_passes(z2, key_f64(k2)));
         }
         if (vis) flags[t] = 1;
+    }
+    // the warp queue
+    const int nq2 = st->n_vis_q2;
+    const int lane = lane_id();
+    constexpr int PER_LANE = (FA_SMALL_PX + 31) / 32;
+    for (int wi = (int)(blockIdx.x * blockDim.x + threadIdx.x) / 32; wi < nq2; wi += gridDim.x * blockDim.x / 32) {
+        Setup3 f;
+        int t;
+        load_rec(small_rec + queue[T - wi], f, t);
+        const int bw = f.max_x - f.min_x + 1, n = bw * (f.max_y - f.min_y + 1);
+        bool in[PER_LANE];
+        double zq[PER_LANE];
+        unsigned long long kq[PER_LANE];
+#pragma unroll
+        for (int j = 0; j < PER_LANE; j++) {
+            const int k = lane + 32 * j;
+            const int dy = k / bw;
+            const int iy = f.min_y + dy, ix = f.min_x + (k - dy * bw);
+            const double px = (double)ix + 0.5, py = (double)iy + 0.5;
+            in[j] = k < n && sample_inside3(f, px, py);
+            zq[j] = in[j] ? sample_depth3(f, px, py) : 0.0;
+            kq[j] = in[j] ? depth[(long long)iy * W + ix] : 0ull;
+        }
+        bool vis = false;
+#pragma unroll
+        for (int j = 0; j < PER_LANE; j++) vis = vis || (in[j] && depth_passes(zq[j], key_f64(kq[j])));
+        if (__any_sync(0xffffffffu, vis) && lane == 0) flags[t] = 1;
     }
 }
 
@@ -974,8 +1019,8 @@ int fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const
                                                       max_tiles, max_large);
     fa_launch(k_vis_small_filter, fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s, small_rec, T, hiz, htx, flags, vis_queue,
               st);
-    fa_launch(k_vis_small_sample, fa_grid(T / 4, 256, FA_NUM_SMS * 8), 256, 0, s, small_rec, W, depth, vis_queue, flags,
-              st);
+    fa_launch(k_vis_small_sample, fa_grid(T / 4, 256, FA_NUM_SMS * 8), 256, 0, s, small_rec, T, W, depth, vis_queue,
+              flags, st);
     if (side) fork_to(side, s, ev_join);
     return 3;
 }
