@@ -528,10 +528,13 @@ __global__ void __launch_bounds__(256) k_raster_depth_tiles(const SmallRec* __re
 // (RED.MIN.64 per covered sample).
 #define COOP_WARPS 4
 #ifndef COOP_GRID_MULT
-#define COOP_GRID_MULT 3  // one wave: the resident CTAs loop (persistent)
+#define COOP_GRID_MULT 5  // one wave: the resident CTAs loop (persistent)
+#endif
+#ifndef COOP_UNROLL
+#define COOP_UNROLL 2  // samples of a row span in flight per lane
 #endif
 #ifndef COOP_MIN_BLOCKS
-#define COOP_MIN_BLOCKS 3
+#define COOP_MIN_BLOCKS 5
 #endif
 struct __align__(16) CoopWarp {
     SmallRec rec[2][32];  // double buffer: the next 32 records stream in (one bulk copy) during the current ones
@@ -622,6 +625,8 @@ __global__ void __launch_bounds__(COOP_WARPS * 32, COOP_MIN_BLOCKS) k_small_coop
                 row_span_cert(f, rt, se, xa, xb, ca, cb);
                 const long long rowoff = (long long)iy * W;
                 double px = (double)xa + 0.5;  // px += 1 below is exact (half-integers < 2^52)
+                constexpr int kUnroll = COOP_UNROLL;
+#pragma unroll kUnroll
                 for (int ix = xa; ix <= xb; ix++, px += 1.0) {
                     // the edge test only near a crossing (row_span_cert)
                     const double z = depth_row(f, rt, px);
