@@ -17,6 +17,7 @@
 
 #define FA_TU_ID 1  // trace builds (FA_TRACE): kernel key = TU id + line
 #include "fa_internal.h"
+#include <cuda_profiler_api.h>
 #include "fa_raster.cuh"
 
 static thread_local std::string g_err;
@@ -1011,7 +1012,21 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     nl = 0;
     bool prof = p->profile && !p->use_graph;
     ctx->n_stage_marks = 0;
+    // debug knob for ncu range replay (tools/frame_traffic.py):
+    // FASTATLAS_PROFILE_STAGE=k brackets stage k (between marks k and k + 1
+    // below) of the FASTATLAS_PROFILE_FRAME-th non-graph frame (default 4)
+    // with cudaProfilerStart/Stop
+    static const int prof_stage = fa_env_int("FASTATLAS_PROFILE_STAGE", -1);
+    static const int prof_frame = fa_env_int("FASTATLAS_PROFILE_FRAME", 4);
+    static int frame_no = 0;
+    const bool prof_this = prof_stage >= 0 && !p->use_graph && frame_no++ == prof_frame;
+    int n_marks = 0;
     auto mark = [&]() -> int {
+        if (prof_this) {
+            if (n_marks == prof_stage) cudaProfilerStart();
+            if (n_marks == prof_stage + 1) cudaProfilerStop();
+        }
+        n_marks++;
         if (!prof) return FA_OK;
         if (!ctx->ev[ctx->n_stage_marks]) CK(cudaEventCreate(&ctx->ev[ctx->n_stage_marks]));
         CK(cudaEventRecord(ctx->ev[ctx->n_stage_marks], s));
