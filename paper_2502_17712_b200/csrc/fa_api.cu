@@ -433,6 +433,12 @@ static fa_cull_args cull_args(fa_ctx* ctx, int cull) {
     return c;
 }
 
+// clip-space vertices: the array k_frame_init wrote (the standalone entry
+// points), or recomputed from the positions where needed (the frame, whose
+// k_frame_init skips the (V,4) array)
+static ClipSrc clip_stored(fa_ctx* ctx) { return ClipSrc{P<double4>(ctx->clip), nullptr, nullptr}; }
+static ClipSrc clip_recomputed(fa_ctx* ctx) { return ClipSrc{nullptr, ctx->pos, P<double>(ctx->vp_dev)}; }
+
 // depth pass (shared by fa_depth_prepass and the frame)
 static int launch_depth(fa_ctx* ctx, int W, int H, int cull, unsigned char* flags_out, cudaStream_t s, int& nl) {
     int T = (int)ctx->T, V = (int)ctx->V;
@@ -442,7 +448,7 @@ static int launch_depth(fa_ctx* ctx, int W, int H, int cull, unsigned char* flag
                          P<int>(ctx->vmin), P<unsigned long long>(ctx->depth_keys), nullptr, (long long)W * H,
                          flags_out, T, s);
     if (ord.live) nl += 1;
-    nl += 1 + fa_launch_depth_pass(true, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, W, H, cull,
+    nl += 1 + fa_launch_depth_pass(true, clip_stored(ctx), P<double4>(ctx->scr), ctx->tris, T, W, H, cull,
                                    P<unsigned long long>(ctx->depth_keys), nullptr, P<SmallRec>(ctx->small_rec),
                                    P<int>(ctx->clip_list), P<TriSetup>(ctx->large), ctx->max_large,
                                    P<int4>(ctx->tiles), ctx->max_tiles, P<fa_dstat>(ctx->dstat), s, nullptr, nullptr,
@@ -635,7 +641,7 @@ int fa_mark_visible(fa_ctx* ctx, const double* vp_host, const double* depth, int
         fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), P<double4>(ctx->scr), width,
                              height, nullptr, nullptr, nullptr, 0, P<unsigned char>(ctx->flags), T, s);
         fa_launch_encode_depth(depth, P<unsigned long long>(ctx->depth_keys), (long long)width * height, s);
-        fa_launch_depth_pass(false, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, width, height,
+        fa_launch_depth_pass(false, clip_stored(ctx), P<double4>(ctx->scr), ctx->tris, T, width, height,
                              backface_cull, nullptr, nullptr, P<SmallRec>(ctx->small_rec), P<int>(ctx->clip_list),
                              P<TriSetup>(ctx->large), ctx->max_large, P<int4>(ctx->tiles), ctx->max_tiles,
                              P<fa_dstat>(ctx->dstat), s, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, ord);
@@ -758,7 +764,7 @@ int fa_chart_boxes(fa_ctx* ctx, const double* vp_host, const int32_t* labels, in
     fa_launch_compact_visible(fl, T, P<int>(ctx->blocks), P<int>(ctx->vis_list), P<int>(ctx->aux), st, s);
     fa_launch_compact_roots(P<int>(ctx->vis_list), labels, T, P<int>(ctx->blocks), P<int>(ctx->roots),
                             P<int>(ctx->cidx), P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), st, s);
-    fa_launch_chart_bounds(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->vis_list), labels, P<int>(ctx->cidx), T,
+    fa_launch_chart_bounds(clip_stored(ctx), ctx->tris, P<int>(ctx->vis_list), labels, P<int>(ctx->cidx), T,
                            P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), st, s);
     fa_launch_box_dims(P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), P<int>(ctx->roots), T, width,
                        height, prescale, P<double>(ctx->ndc), P<int>(ctx->px), P<long long>(ctx->target),
@@ -1049,11 +1055,11 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     CK(cudaEventRecord(ctx->fj[10], ctx->side));
     const fa_setup_order ord = setup_order(ctx);
     fa_launch_cluster_cull(P<double>(ctx->vp_dev), W, H, cull_args(ctx, p->backface_cull), s);
-    fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), P<double4>(ctx->clip), P<double4>(ctx->scr), W, H,
+    fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), nullptr, P<double4>(ctx->scr), W, H,
                          P<int>(ctx->vmin), nullptr, nullptr, 0, flags, T, s, 0, P<double2>(ctx->ndc2));
     nl += ord.live ? 3 : 2;
     mark();  // 1: project + clears
-    nl += fa_launch_depth_pass(true, P<double4>(ctx->clip), P<double4>(ctx->scr), ctx->tris, T, W, H,
+    nl += fa_launch_depth_pass(true, clip_recomputed(ctx), P<double4>(ctx->scr), ctx->tris, T, W, H,
                                p->backface_cull, P<unsigned long long>(ctx->depth_keys), wid,
                                P<SmallRec>(ctx->small_rec), P<int>(ctx->clip_list), P<TriSetup>(ctx->large),
                                ctx->max_large, P<int4>(ctx->tiles), ctx->max_tiles, st, s,
@@ -1074,6 +1080,14 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
                               ctx->tris, P<int>(ctx->vmin), P<int4>(ctx->vis_tris));
     nl += 2;
     mark();  // 4: visible compaction
+    // debug knob (results invalid): end the frame after the raster passes
+    // and the visible compaction,
+    // to measure what the rest of the frame costs the pipelined throughput
+    static const int dbg_stop = fa_env_int("FASTATLAS_DEBUG_STOP_AFTER_RASTER", 0);
+    if (dbg_stop) {
+        CK(cudaMemcpyAsync(ctx->hstat, ctx->dstat.p, sizeof(fa_dstat), cudaMemcpyDeviceToHost, s));
+        return FA_OK;
+    }
     nl += fa_launch_uf_vertex(ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->vmin), P<int>(ctx->label), T, st, s,
                               true, P<int4>(ctx->vis_tris));
     mark();  // 5: union-find charts (hooking)
@@ -1094,7 +1108,7 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     nl += 2;
     CK(cudaStreamWaitEvent(s, ctx->fj[5], 0));  // bounds read the flattened labels
     mark();  // 6: chart roots (+ flatten)
-    fa_launch_chart_bounds(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->label),
+    fa_launch_chart_bounds(clip_recomputed(ctx), ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->label),
                            P<int>(ctx->cidx), T, P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), st, s,
                            P<int>(ctx->vis_cidx), P<int4>(ctx->vis_tris), P<double2>(ctx->ndc2));
     nl += 1;
@@ -1121,7 +1135,7 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     }
     mark();  // 9: candidate pack + select
     CK(cudaStreamWaitEvent(s, ctx->fj[6], 0));  // vertex -> chart map and the visible-vertex slots
-    fa_launch_uv(P<double4>(ctx->clip), ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->label), P<int>(ctx->cidx),
+    fa_launch_uv(clip_recomputed(ctx), ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->label), P<int>(ctx->cidx),
                  P<int>(ctx->pinv), P<double>(ctx->ndc), P<int>(ctx->px), P<long long>(ctx->placements), T, W, H,
                  p->padding, p->uv_f64 != 0, ctx->uv.p, P<int>(ctx->vis_chart), P<int>(ctx->vis_cidx),
                  p->packer == FA_PACKER_FASTATLAS ? P<int4>(ctx->plc_c) : nullptr, st, s, P<int4>(ctx->vis_tris),

@@ -123,7 +123,7 @@ __device__ __forceinline__ bool tri_box(const double4 (&c)[3], NBox& b) {
     return false;
 }
 
-__global__ void __launch_bounds__(256) k_chart_bounds(const double4* __restrict__ clip, const int* __restrict__ tris,
+__global__ void __launch_bounds__(256) k_chart_bounds(const ClipSrc clip, const int* __restrict__ tris,
                                                       const int* __restrict__ vis_list, const int* __restrict__ label,
                                                       const int* __restrict__ cidx,
                                                       unsigned long long* __restrict__ keys,
@@ -167,14 +167,14 @@ __global__ void __launch_bounds__(256) k_chart_bounds(const double4* __restrict_
                     }
                 }
                 if (!got) {
-                    double4 cc[3] = {ldg4(clip + q.x), ldg4(clip + q.y), ldg4(clip + q.z)};
+                    double4 cc[3] = {clip(q.x), clip(q.y), clip(q.z)};
                     got = tri_box(cc, b);
                 }
             } else {
                 t = vis_list[k];
                 double4 cc[3];
 #pragma unroll
-                for (int j = 0; j < 3; j++) cc[j] = ldg4(clip + __ldg(tris + 3 * t + j));
+                for (int j = 0; j < 3; j++) cc[j] = clip(__ldg(tris + 3 * t + j));
                 c = cidx[label[t]];
                 got = tri_box(cc, b);
             }
@@ -235,7 +235,7 @@ __global__ void k_box_dims(const unsigned long long* __restrict__ keys, const in
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) fa_box_dims_one(a, j, st);
 }
 
-void fa_launch_chart_bounds(const double4* clip, const int* tris, const int* vis_list, const int* label,
+void fa_launch_chart_bounds(const ClipSrc clip, const int* tris, const int* vis_list, const int* label,
                             const int* cidx, int T, unsigned long long* ndc_keys, int* survived, const fa_dstat* st,
                             cudaStream_t s, int* vis_cidx, const int4* vis_tris, const double2* ndc2) {
     fa_launch(k_chart_bounds, fa_grid(T, 256, FA_NUM_SMS * 8), 256, 0, s, clip, tris, vis_list, label, cidx, ndc_keys,

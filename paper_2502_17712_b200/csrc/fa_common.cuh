@@ -396,6 +396,24 @@ __device__ __forceinline__ double4 ldg4(const double4* p) {
     return make_double4(a.x, a.y, b.x, b.y);
 }
 
+// Clip-space vertices for the paths that need them (clipping, and the bounds /
+// UV fallbacks of triangles with a vertex outside the frustum): read from a
+// stored array, or recomputed from the positions with the projection's own
+// FMA chain (same bits), so the frame never writes the (V,4) clip array.
+struct ClipSrc {
+    const double4* clip;  // stored clip coordinates, or nullptr:
+    const double* pos;    // (V,3) positions and
+    const double* vp;     // the device view-projection matrix (row-major)
+    __device__ __forceinline__ double4 operator()(int v) const {
+        if (clip) return ldg4(clip + v);
+        double m[16];
+#pragma unroll
+        for (int i = 0; i < 16; i++) m[i] = __ldg(vp + i);
+        return project_point(__ldg(pos + 3 * (long long)v), __ldg(pos + 3 * (long long)v + 1),
+                             __ldg(pos + 3 * (long long)v + 2), m);
+    }
+};
+
 // ---- per-chart box dims (geometry.py:352-362 viewport_box + cli.py:379-384) --
 // NDC box -> (w_px, h_px) = max(1, ceil(extent/2 * W)) -> target dims
 // max(1, ceil(prescale * dim)); the packer's inputs for j < cap.  Shared by

@@ -148,7 +148,7 @@ void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* c
 void fa_launch_cluster_cull(const double* vp, int W, int H, const fa_cull_args& cu, cudaStream_t s);
 // side == nullptr: everything on s; otherwise fork/join through the events.
 // Both return the number of kernels launched.  wid: see depth_min (may be null).
-int fa_launch_depth_pass(bool write_depth, const double4* clip, const double4* scr, const int* tris, int T, int W,
+int fa_launch_depth_pass(bool write_depth, const ClipSrc clip, const double4* scr, const int* tris, int T, int W,
                          int H, int cull, unsigned long long* depth, unsigned long long* wid, SmallRec* small_rec,
                          int* clip_list, TriSetup* large, int max_large, int4* tiles, int max_tiles, fa_dstat* st,
                          cudaStream_t s, cudaStream_t side, cudaStream_t side2, cudaEvent_t ev_fork,
@@ -217,7 +217,7 @@ void fa_launch_mesh_remap(const int* tris, long long T, const int* newidx, int* 
 void fa_launch_cluster_build(const double* pos, const int* tris_sorted, int T, fa_cluster* out, cudaStream_t s);
 
 // ---- bounds (fa_bounds.cu) -----------------------------------------------
-void fa_launch_chart_bounds(const double4* clip, const int* tris, const int* vis_list, const int* label,
+void fa_launch_chart_bounds(const ClipSrc clip, const int* tris, const int* vis_list, const int* label,
                             const int* cidx, int T, unsigned long long* ndc_keys, int* survived, const fa_dstat* st,
                             cudaStream_t s, int* vis_cidx = nullptr, const int4* vis_tris = nullptr, const double2* ndc2 = nullptr);
 void fa_launch_box_dims(const unsigned long long* ndc_keys, const int* survived, const int* roots, int T, int W, int H,
@@ -275,7 +275,7 @@ void fa_launch_fold(const long long* w, int n, long long omega, long long* rows,
                     cudaStream_t s);
 
 // ---- uv (fa_uv.cu) -------------------------------------------------------
-void fa_launch_uv(const double4* clip, const int* tris, const int* vis_list, const int* label, const int* cidx,
+void fa_launch_uv(const ClipSrc clip, const int* tris, const int* vis_list, const int* label, const int* cidx,
                   const int* pinv, const double* ndc, const int* px, const long long* placements, int T, int W, int H,
                   long long pad, bool f64, void* uv, int* vis_chart, const int* vis_cidx, const int4* plc_c,
                   fa_dstat* st, cudaStream_t s, const int4* vis_tris = nullptr, const int* vslot = nullptr,

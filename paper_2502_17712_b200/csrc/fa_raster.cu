@@ -80,7 +80,7 @@ __global__ void k_frame_init(const double* __restrict__ pos, int V, const double
     for (long long v = i0; v < V; v += stride) {
         double x = pos[3 * v], y = pos[3 * v + 1], z = pos[3 * v + 2];
         double4 c = project_point(x, y, z, m);
-        clip[v] = c;
+        if (clip) clip[v] = c;
         if (ndc2) ndc2[v] = vertex_ndc(c);
         if (scr) scr[v] = vertex_screen(c, W, H);
         if (vmin) vmin[v] = 0x7fffffff;
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(SETUP_WARPS * 32) k_raster_setup(const double4
 // pass only) or writes the descriptors of its 16x8 tiles (negative ids).
 // The visibility pass finds every stored setup through the queue.
 template <bool WRITE_DEPTH>
-__global__ void __launch_bounds__(256) k_raster_clipped(const double4* __restrict__ clip, const int* __restrict__ tris,
+__global__ void __launch_bounds__(256) k_raster_clipped(const ClipSrc clip, const int* __restrict__ tris,
                                                         int W, int H, int cull, const int* __restrict__ clip_list,
                                                         unsigned long long* __restrict__ depth,
                                                         unsigned long long* __restrict__ wid,
@@ -972,7 +972,7 @@ static void fork_to(cudaStream_t s, cudaStream_t side, cudaEvent_t ev) {
 // tiles on side} || {clipped polygons -> their tiles on side2}, joined back
 // into s.  Every branch only lowers depth keys with atomicMin, so their order
 // does not matter.
-int fa_launch_depth_pass(bool write_depth, const double4* clip, const double4* scr, const int* tris, int T, int W,
+int fa_launch_depth_pass(bool write_depth, const ClipSrc clip, const double4* scr, const int* tris, int T, int W,
                          int H, int cull, unsigned long long* depth, unsigned long long* wid, SmallRec* small_rec,
                          int* clip_list, TriSetup* large, int max_large, int4* tiles, int max_tiles, fa_dstat* st,
                          cudaStream_t s, cudaStream_t side, cudaStream_t side2, cudaEvent_t ev_fork,

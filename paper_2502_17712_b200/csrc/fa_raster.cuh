@@ -373,12 +373,12 @@ __device__ __forceinline__ bool clip_step_warp(double4& v, int& n, double d, Cli
 
 // 1 = setup filled (on every lane's return; `s` in shared memory), 0 = no
 // samples, -1 = polygon capacity overflow.  Call with the whole warp.
-static __device__ __noinline__ int tri_setup_warp(const double4* __restrict__ clip, const int* __restrict__ tris, int t,
+static __device__ __noinline__ int tri_setup_warp(const ClipSrc clip, const int* __restrict__ tris, int t,
                                            int W, int H, bool cull, TriSetup& s, ClipScratch& cs) {
     const int lane = lane_id();
     int n = 3;
     double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
-    if (lane < 3) v = ldg4(clip + __ldg(tris + 3 * t + lane));
+    if (lane < 3) v = clip(__ldg(tris + 3 * t + lane));
     // charts.py:163-167: the w >= eps plane
     double d = __dsub_rn(v.w, FA_W_EPSILON);
     if (!__any_sync(0xffffffffu, lane < n && d > 0)) return 0;

@@ -34,7 +34,7 @@ __device__ __forceinline__ bool tri_stretch(const double (&s)[6], const double (
 }
 
 template <typename OutT>
-__global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ clip, const int* __restrict__ tris,
+__global__ void __launch_bounds__(UV_THREADS) k_uv(const ClipSrc clip, const int* __restrict__ tris,
                                                    const int* __restrict__ vis_list, const int* __restrict__ label,
                                                    const int* __restrict__ cidx, const int* __restrict__ pinv,
                                                    const double* __restrict__ ndc, const int* __restrict__ px,
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
             if (!fast) {
 #pragma unroll
                 for (int i = 0; i < 3; i++) {
-                    v[i] = ldg4(clip + (vis_tris ? (i == 0 ? vq.x : (i == 1 ? vq.y : vq.z)) : __ldg(tris + 3 * t + i)));
+                    v[i] = clip(vis_tris ? (i == 0 ? vq.x : (i == 1 ? vq.y : vq.z)) : __ldg(tris + 3 * t + i));
                     if (v[i].w <= FA_W_EPSILON) behind = true;
                 }
                 if (!behind) {
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const double4* __restrict__ c
     }
 }
 
-void fa_launch_uv(const double4* clip, const int* tris, const int* vis_list, const int* label, const int* cidx,
+void fa_launch_uv(const ClipSrc clip, const int* tris, const int* vis_list, const int* label, const int* cidx,
                   const int* pinv, const double* ndc, const int* px, const long long* placements, int T, int W, int H,
                   long long pad, bool f64, void* uv, int* vis_chart, const int* vis_cidx, const int4* plc_c,
                   fa_dstat* st, cudaStream_t s, const int4* vis_tris, const int* vslot, float2* vuv,

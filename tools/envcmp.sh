@@ -2,7 +2,7 @@
 # Compare environment settings on the bench (3 runs each, 32 views):
 #   bash tools/envcmp.sh "FASTATLAS_PDL=0" "FASTATLAS_PDL=1"
 for setting in "$@"; do
-  for i in 1 2 3; do
+  for i in $(seq 1 ${REPS:-3}); do
     env $setting timeout 300 python bench.py --steps 32 --warmup 3 --no-cpu-baseline --profile-frames 3 \
       2>/dev/null | python -c "
 import json,sys
