@@ -279,7 +279,9 @@ static int ensure_raster(fa_ctx* ctx, int W, int H, bool depth) {
     ENSURE(flags, ((T + 15) / 16 + 1) * 16);
     ENSURE(clip_list, (T + 1) * 4);
     ENSURE(small_rec, (T + 1) * sizeof(SmallRec) + (T + 1) * 4);  // records + their triangle ids
-    long long want_tiles = (long long)W * H / 32;
+    // tile descriptors: 16 B each; a queue overflow costs a rerun of the
+    // frame, so start at one descriptor per 8 pixels (C2 views use up to ~1/30)
+    long long want_tiles = (long long)W * H / 8;
     if (want_tiles > ctx->max_tiles) ctx->max_tiles = (int)(want_tiles < (1ll << 30) ? want_tiles : (1 << 30));
     ENSURE(large, (size_t)ctx->max_large * sizeof(TriSetup));
     ENSURE(tiles, (size_t)ctx->max_tiles * sizeof(int4));
@@ -1237,6 +1239,9 @@ int fa_frame_launch(fa_ctx* ctx, const double* vp_host, const fa_frame_params* p
         if (e != cudaSuccess) return set_err(FA_CUDA_ERROR, "graph instantiate: %s", cudaGetErrorString(e));
         ctx->graph_key = key;
         ctx->last_launches = nl;
+        static const int dbg_cap = fa_env_int("FASTATLAS_DEBUG_CAPTURE", 0);
+        if (dbg_cap) fprintf(stderr, "fastatlas: frame graph captured (ctx %p, gen %llu)\n", (void*)ctx,
+                             (unsigned long long)ctx->gen);
     }
     CK(cudaGraphLaunch(ctx->graph_exec, s));
     return FA_OK;

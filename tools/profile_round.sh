@@ -20,5 +20,12 @@ python tools/ncu_summary.py gpurun_out/${tag}_full.ncu-rep > gpurun_out/${tag}_n
 python tools/bench_configs.py gpurun_out/${tag}_configs.json > gpurun_out/${tag}_configs.log 2>&1
 python tools/set_mesh_time.py C3 5 > gpurun_out/${tag}_set_mesh.txt 2>&1
 python tools/frame_counters.py C2 4 > gpurun_out/${tag}_counters.txt 2>&1
+# whole-frame DRAM traffic in the real cache state (ncu range replay)
+bash tools/frame_traffic.sh > /dev/null 2>&1 && cp gpurun_out/traffic.txt gpurun_out/${tag}_frame_traffic.txt
+# device-side timeline of graphed frames (FA_TRACE build, tools/lib_trace.so)
+if [ -f tools/lib_trace.so ]; then
+  FASTATLAS_LIB=tools/lib_trace.so python tools/trace_frame.py C2 16 > gpurun_out/${tag}_trace_c2.txt 2>&1
+  FASTATLAS_LIB=tools/lib_trace.so python tools/trace_frame.py C1 16 > gpurun_out/${tag}_trace_c1.txt 2>&1
+fi
 tail -3 gpurun_out/${tag}_launches.txt
 cat gpurun_out/${tag}_ncu_summary.txt | head -40
