@@ -1099,7 +1099,6 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     CK(cudaEventRecord(ctx->fj[4], s));
     CK(cudaStreamWaitEvent(ctx->side, ctx->fj[4], 0));
     fa_launch_uf_compress(P<int>(ctx->vis_list), P<int>(ctx->label), T, st, ctx->side);
-    CK(cudaEventRecord(ctx->fj[5], ctx->side));
     fa_launch_v2c(P<int>(ctx->vmin), P<int>(ctx->label), P<int>(ctx->v2c), V, ctx->side, ctx->vperm);
     fa_launch_visible_vertices(P<int>(ctx->vmin), V, ctx->vperm, P<int>(ctx->vblocks), P<int>(ctx->vslot),
                                P<int>(ctx->vlist), st, ctx->side, P<float2>(ctx->vuv));
@@ -1108,7 +1107,7 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     fa_launch_compact_roots(P<int>(ctx->vis_list), P<int>(ctx->label), T, P<int>(ctx->blocks), P<int>(ctx->roots),
                             P<int>(ctx->cidx), P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), st, s);
     nl += 2;
-    CK(cudaStreamWaitEvent(s, ctx->fj[5], 0));  // bounds read the flattened labels
+    // (the bounds find each triangle's root themselves, beside the flattening)
     mark();  // 6: chart roots (+ flatten)
     fa_launch_chart_bounds(clip_recomputed(ctx), ctx->tris, P<int>(ctx->vis_list), P<int>(ctx->label),
                            P<int>(ctx->cidx), T, P<unsigned long long>(ctx->ndc_keys), P<int>(ctx->survived), st, s,

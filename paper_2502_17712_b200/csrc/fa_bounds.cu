@@ -123,8 +123,22 @@ __device__ __forceinline__ bool tri_box(const double4 (&c)[3], NBox& b) {
     return false;
 }
 
+// Root of t's set after the hooking: the frame's bounds run beside the
+// flattening (k_compress, another stream), which only rewrites non-roots to
+// their root, so every value read here is t's parent or its root -- both lead
+// to the root.  L2 loads (not the read-only path: the array is being written).
+__device__ __forceinline__ int uf_root(const int* label, int t) {
+    int r = __ldcg(label + t);
+    if (r == t) return t;
+    for (;;) {
+        const int p = __ldcg(label + r);
+        if (p == r) return r;
+        r = p;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_chart_bounds(const ClipSrc clip, const int* __restrict__ tris,
-                                                      const int* __restrict__ vis_list, const int* __restrict__ label,
+                                                      const int* __restrict__ vis_list, const int* label,
                                                       const int* __restrict__ cidx,
                                                       unsigned long long* __restrict__ keys,
                                                       int* __restrict__ survived, const fa_dstat* __restrict__ st,
@@ -147,7 +161,7 @@ __global__ void __launch_bounds__(256) k_chart_bounds(const ClipSrc clip, const 
             if (vis_tris) {  // vertex indices next to the id: one dependent load fewer
                 const int4 q = vis_tris[k];
                 t = q.w;
-                c = cidx[label[t]];
+                c = cidx[uf_root(label, t)];
                 if (ndc2) {
                     // every vertex strictly inside the frustum (vertex_ndc not
                     // NaN): no side plane is crossed and the Blinn clamp is the
@@ -175,7 +189,7 @@ __global__ void __launch_bounds__(256) k_chart_bounds(const ClipSrc clip, const 
                 double4 cc[3];
 #pragma unroll
                 for (int j = 0; j < 3; j++) cc[j] = clip(__ldg(tris + 3 * t + j));
-                c = cidx[label[t]];
+                c = cidx[uf_root(label, t)];
                 got = tri_box(cc, b);
             }
             if (vis_cidx) vis_cidx[k] = c;  // k_uv's chart index (saves it two dependent loads)
@@ -238,7 +252,7 @@ __global__ void k_box_dims(const unsigned long long* __restrict__ keys, const in
 void fa_launch_chart_bounds(const ClipSrc clip, const int* tris, const int* vis_list, const int* label,
                             const int* cidx, int T, unsigned long long* ndc_keys, int* survived, const fa_dstat* st,
                             cudaStream_t s, int* vis_cidx, const int4* vis_tris, const double2* ndc2) {
-    fa_launch(k_chart_bounds, fa_grid(T, 256, FA_NUM_SMS * 8), 256, 0, s, clip, tris, vis_list, label, cidx, ndc_keys,
+    fa_launch(k_chart_bounds, fa_wave_grid(k_chart_bounds, 256, 0, ((long long)T + 255) / 256, FA_NUM_SMS * 8), 256, 0, s, clip, tris, vis_list, label, cidx, ndc_keys,
               survived, st, vis_cidx, vis_tris, vis_tris ? ndc2 : nullptr);
 }
 

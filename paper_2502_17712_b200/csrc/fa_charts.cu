@@ -476,7 +476,7 @@ void fa_launch_build_adjacency(const int* tris, int T, unsigned long long* keys,
 int fa_launch_uf_vertex(const int* tris, const int* vis_list, int* vmin, int* label, int T, const fa_dstat* st,
                         cudaStream_t s, bool vmin_ready, const int4* vis_tris) {
     if (!vmin_ready) fa_launch(k_vmin, uf_grid(T), 256, 0, s, tris, vis_list, vmin, st);
-    fa_launch(k_hook_multi, uf_grid(T), 256, 0, s, tris, vis_list, vmin, label, st, vis_tris);
+    fa_launch(k_hook_multi, fa_wave_grid(k_hook_multi, 256, 0, ((long long)T + 255) / 256, FA_NUM_SMS * 8), 256, 0, s, tris, vis_list, vmin, label, st, vis_tris);
     return vmin_ready ? 1 : 2;
 }
 
@@ -495,7 +495,7 @@ void fa_launch_uf_labels(const int* labels_in, const int* vis_list, int* label, 
 }
 
 void fa_launch_uf_compress(const int* vis_list, int* label, int T, const fa_dstat* st, cudaStream_t s) {
-    fa_launch(k_compress, uf_grid(T), 256, 0, s, vis_list, label, st);
+    fa_launch(k_compress, fa_wave_grid(k_compress, 256, 0, ((long long)T + 255) / 256, FA_NUM_SMS * 8), 256, 0, s, vis_list, label, st);
 }
 
 void fa_launch_canonicalize(const int* vis_list, int* label, int* tmp, int T, const fa_dstat* st, cudaStream_t s) {

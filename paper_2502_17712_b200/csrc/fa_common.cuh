@@ -356,6 +356,22 @@ struct FaTraceGuard {
 bool fa_pdl_enabled();  // FASTATLAS_PDL=0 disables (fa_api.cu)
 int fa_env_int(const char* name, int dflt);  // integer knob from the environment (fa_api.cu)
 
+// Grid for a grid-stride kernel over device-counted work (the visible
+// triangles): one resident wave -- every CTA fits on the GPU at once, so under
+// PDL the whole grid is already resident when its predecessor finishes -- or,
+// with FASTATLAS_WAVES=0, the former cap of `cap` CTAs.
+template <typename... KArgs>
+static inline int fa_wave_grid(void (*k)(KArgs...), int threads, size_t smem, long long max_blocks, int cap) {
+    static const int waves = fa_env_int("FASTATLAS_WAVES", 1);
+    if (waves <= 0) return (int)(max_blocks < cap ? max_blocks : cap);
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    long long g = (long long)FA_NUM_SMS * per_sm * waves;
+    if (g > max_blocks) g = max_blocks;
+    return (int)(g < 1 ? 1 : g);
+}
+
 template <typename... KArgs, typename... Args>
 static inline void fa_launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                              Args... args) {

@@ -204,7 +204,9 @@ void fa_launch_uv(const ClipSrc clip, const int* tris, const int* vis_list, cons
                   fa_dstat* st, cudaStream_t s, const int4* vis_tris, const int* vslot, float2* vuv,
                   const double2* ndc2) {
     if (!vis_tris) vuv = nullptr;  // the compact UVs index vertices through vis_tris
-    int grid = fa_grid(T, UV_THREADS, FA_NUM_SMS * 8);
+    const long long nblk = ((long long)T + UV_THREADS - 1) / UV_THREADS;
+    const int grid = f64 ? fa_wave_grid(k_uv<double>, UV_THREADS, 0, nblk, FA_NUM_SMS * 8)
+                         : fa_wave_grid(k_uv<float>, UV_THREADS, 0, nblk, FA_NUM_SMS * 8);
     if (f64)
         fa_launch(k_uv<double>, grid, UV_THREADS, 0, s, clip, tris, vis_list, label, cidx, pinv, ndc, px, placements, W, H,
                                                  pad, (double*)uv, vis_chart, vis_cidx, plc_c, vis_tris, vslot, vuv, st, ndc2);
