@@ -579,7 +579,7 @@ void fa_launch_visible_vertices(const int* vmin, int V, const int* vperm, int* b
 }
 
 void fa_launch_v2c(const int* vmin, const int* label, int* v2c, int V, cudaStream_t s, const int* vperm) {
-    fa_launch(k_v2c, fa_grid(V, 256, FA_NUM_SMS * 8), 256, 0, s, vmin, label, v2c, V, vperm);
+    fa_launch(k_v2c, fa_wave_grid(k_v2c, 256, 0, ((long long)V + 255) / 256, FA_NUM_SMS * 8), 256, 0, s, vmin, label, v2c, V, vperm);
 }
 
 void fa_launch_flags_from_labels(const int* labels, unsigned char* flags, int T, cudaStream_t s) {

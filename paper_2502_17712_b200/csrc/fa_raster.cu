@@ -1020,11 +1020,11 @@ int fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const
     cudaStream_t b = side ? side : s;
     const int htx = fa_hiz_dim(W);
     if (side) fork_to(s, side, ev_fork);
-    fa_launch(k_raster_vis_tiles, fa_cap(FA_NUM_SMS * 8), 256, 0, b, small_rec, T, large, tiles, W, depth, hiz, htx, flags, st,
+    fa_launch(k_raster_vis_tiles, fa_wave_grid(k_raster_vis_tiles, 256, 0, FA_NUM_SMS * 8, FA_NUM_SMS * 8), 256, 0, b, small_rec, T, large, tiles, W, depth, hiz, htx, flags, st,
                                                       max_tiles, max_large);
-    fa_launch(k_vis_small_filter, fa_grid(T, 256, FA_NUM_SMS * 16), 256, 0, s, small_rec, T, hiz, htx, flags, vis_queue,
+    fa_launch(k_vis_small_filter, fa_wave_grid(k_vis_small_filter, 256, 0, ((long long)T + 255) / 256, FA_NUM_SMS * 16), 256, 0, s, small_rec, T, hiz, htx, flags, vis_queue,
               st);
-    fa_launch(k_vis_small_sample, fa_grid(T / 4, 256, FA_NUM_SMS * 8), 256, 0, s, small_rec, T, W, depth, vis_queue,
+    fa_launch(k_vis_small_sample, fa_wave_grid(k_vis_small_sample, 256, 0, ((long long)T / 4 + 255) / 256, FA_NUM_SMS * 8), 256, 0, s, small_rec, T, W, depth, vis_queue,
               flags, st);
     if (side) fork_to(side, s, ev_join);
     return 3;
@@ -1033,7 +1033,7 @@ int fa_launch_raster_vis(const SmallRec* small_rec, const TriSetup* large, const
 void fa_launch_depth_hiz(const unsigned long long* depth, const unsigned long long* wid, int W, int H,
                          unsigned long long* hiz, unsigned char* flags, fa_dstat* st, cudaStream_t s) {
     int htx = fa_hiz_dim(W), hty = fa_hiz_dim(H);
-    fa_launch(k_depth_hiz, fa_grid((long long)htx * FA_HIZ * hty, 256, FA_NUM_SMS * 8), 256, 0, s, depth, wid, W, H, hiz, htx,
+    fa_launch(k_depth_hiz, fa_wave_grid(k_depth_hiz, 256, 0, ((long long)htx * FA_HIZ * hty + 255) / 256, FA_NUM_SMS * 8), 256, 0, s, depth, wid, W, H, hiz, htx,
                                                                                            hty, flags, st);
 }
 
