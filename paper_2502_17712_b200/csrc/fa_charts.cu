@@ -17,9 +17,13 @@
 // flags per thread of the visible compaction (one 32-bit load) and visible
 // triangles per thread of the roots compaction: few items per thread, so the
 // latency-bound gathers have many threads in flight
-#define CMP_ITEMS 4
+#ifndef CMP_ITEMS
+#define CMP_ITEMS 4  // a multiple of 4
+#endif
 #define CMP_TILE (CMP_THREADS * CMP_ITEMS)
+#ifndef ROOT_ITEMS
 #define ROOT_ITEMS 2
+#endif
 #define ROOT_TILE (CMP_THREADS * ROOT_ITEMS)
 
 // per-block count slots for n items (sized for the smaller tile)
@@ -48,24 +52,38 @@ __device__ __forceinline__ int block_prefix_of(const int* blocks, int b, int* sm
 }
 
 // ---- visible compaction ----------------------------------------------------
+// The compactions run a wave-sized grid; CTA b handles the contiguous tiles
+// [b * per, (b + 1) * per) of the fixed tile partition (vb = tile index).
+__device__ __forceinline__ void tile_range(int ntiles, int& vb0, int& vb1) {
+    const int per = (ntiles + (int)gridDim.x - 1) / (int)gridDim.x;
+    vb0 = min(ntiles, (int)blockIdx.x * per);
+    vb1 = min(ntiles, vb0 + per);
+}
+
 __global__ void __launch_bounds__(CMP_THREADS) k_count_flags(const unsigned char* __restrict__ flags, int T,
-                                                             int* __restrict__ blocks) {
+                                                             int* __restrict__ blocks, int ntiles) {
     FA_PDL_PROLOGUE();
     __shared__ int sm[32];
-    int base = blockIdx.x * CMP_TILE + threadIdx.x * CMP_ITEMS;
-    int c = 0;
-    if (base + CMP_ITEMS <= T) {
-        c = byte_sum4(*reinterpret_cast<const unsigned int*>(flags + base));
-    } else {
-        for (int i = base; i < T; i++) c += flags[i] != 0;
-    }
-    c = warp_sum(c);
-    if (lane_id() == 0) sm[threadIdx.x >> 5] = c;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int s = 0;
-        for (int i = 0; i < CMP_THREADS / 32; i++) s += sm[i];
-        blocks[blockIdx.x] = s;
+    int vb0, vb1;
+    tile_range(ntiles, vb0, vb1);
+    for (int vb = vb0; vb < vb1; vb++) {
+        int base = vb * CMP_TILE + threadIdx.x * CMP_ITEMS;
+        int c = 0;
+        if (base + CMP_ITEMS <= T) {
+#pragma unroll
+            for (int q = 0; q < CMP_ITEMS / 4; q++) c += byte_sum4(reinterpret_cast<const unsigned int*>(flags + base)[q]);
+        } else {
+            for (int i = base; i < T; i++) c += flags[i] != 0;
+        }
+        c = warp_sum(c);
+        if (lane_id() == 0) sm[threadIdx.x >> 5] = c;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int s = 0;
+            for (int i = 0; i < CMP_THREADS / 32; i++) s += sm[i];
+            blocks[vb] = s;
+        }
+        __syncthreads();
     }
 }
 
@@ -79,13 +97,19 @@ __global__ void __launch_bounds__(CMP_THREADS) k_scatter_visible(const unsigned 
                                                                  fa_dstat* __restrict__ st) {
     FA_PDL_PROLOGUE();
     __shared__ int sm[32];
-    int offset = block_prefix_of(blocks, blockIdx.x, sm);
-    int base = blockIdx.x * CMP_TILE + threadIdx.x * CMP_ITEMS;
+    int vb0, vb1;
+    tile_range(nblocks, vb0, vb1);
+    int offset = block_prefix_of(blocks, vb0, sm);
+    for (int vb = vb0; vb < vb1; vb++) {
+    int base = vb * CMP_TILE + threadIdx.x * CMP_ITEMS;
     unsigned char f[CMP_ITEMS];
     if (base + CMP_ITEMS <= T) {
-        const unsigned int w = *reinterpret_cast<const unsigned int*>(flags + base);
 #pragma unroll
-        for (int i = 0; i < CMP_ITEMS; i++) f[i] = (w >> (8 * i)) & 0xffu;
+        for (int q = 0; q < CMP_ITEMS / 4; q++) {
+            const unsigned int w = reinterpret_cast<const unsigned int*>(flags + base)[q];
+#pragma unroll
+            for (int i = 0; i < 4; i++) f[4 * q + i] = (w >> (8 * i)) & 0xffu;
+        }
     } else {
 #pragma unroll
         for (int i = 0; i < CMP_ITEMS; i++) f[i] = (base + i < T) ? flags[base + i] : 0;
@@ -130,14 +154,19 @@ __global__ void __launch_bounds__(CMP_THREADS) k_scatter_visible(const unsigned 
             vis_list[pos++] = t;
         }
     }
-    if (blockIdx.x == nblocks - 1 && threadIdx.x == 0) st->n_vis = offset + total;
+    if (vb == nblocks - 1 && threadIdx.x == 0) st->n_vis = offset + total;
+    offset += total;
+    __syncthreads();  // sm is reused by the next tile's scan
+    }
 }
 
 void fa_launch_compact_visible(const unsigned char* flags, int T, int* blocks, int* vis_list, int* label,
                                fa_dstat* st, cudaStream_t s, const int* tris, int* vmin, int4* vis_tris) {
     int nb = blocks_for(T, CMP_TILE);
-    fa_launch(k_count_flags, nb, CMP_THREADS, 0, s, flags, T, blocks);
-    fa_launch(k_scatter_visible, nb, CMP_THREADS, 0, s, flags, T, blocks, nb, vis_list, label, tris, vmin,
+    fa_launch(k_count_flags, fa_wave_grid(k_count_flags, CMP_THREADS, 0, nb, nb), CMP_THREADS, 0, s, flags, T, blocks,
+              nb);
+    fa_launch(k_scatter_visible, fa_wave_grid(k_scatter_visible, CMP_THREADS, 0, nb, nb), CMP_THREADS, 0, s, flags, T,
+              blocks, nb, vis_list, label, tris, vmin,
               tris ? vis_tris : nullptr, st);
 }
 
@@ -595,23 +624,28 @@ __global__ void __launch_bounds__(CMP_THREADS) k_count_roots(const int* __restri
     FA_PDL_PROLOGUE();
     __shared__ int sm[32];
     int n = st->n_vis;
-    int base = blockIdx.x * ROOT_TILE + threadIdx.x * ROOT_ITEMS;
-    int c = 0;
+    int vb0, vb1;
+    tile_range((n + ROOT_TILE - 1) / ROOT_TILE, vb0, vb1);
+    for (int vb = vb0; vb < vb1; vb++) {
+        int base = vb * ROOT_TILE + threadIdx.x * ROOT_ITEMS;
+        int c = 0;
 #pragma unroll
-    for (int i = 0; i < ROOT_ITEMS; i++) {
-        int k = base + i;
-        if (k < n) {
-            int t = vis_list[k];
-            c += label[t] == t;
+        for (int i = 0; i < ROOT_ITEMS; i++) {
+            int k = base + i;
+            if (k < n) {
+                int t = vis_list[k];
+                c += label[t] == t;
+            }
         }
-    }
-    c = warp_sum(c);
-    if (lane_id() == 0) sm[threadIdx.x >> 5] = c;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int s = 0;
-        for (int i = 0; i < CMP_THREADS / 32; i++) s += sm[i];
-        blocks[blockIdx.x] = s;
+        c = warp_sum(c);
+        if (lane_id() == 0) sm[threadIdx.x >> 5] = c;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int s = 0;
+            for (int i = 0; i < CMP_THREADS / 32; i++) s += sm[i];
+            blocks[vb] = s;
+        }
+        __syncthreads();
     }
 }
 
@@ -624,11 +658,13 @@ __global__ void __launch_bounds__(CMP_THREADS) k_scatter_roots(const int* __rest
     FA_PDL_PROLOGUE();
     __shared__ int sm[32];
     int n = st->n_vis;
-    int last = (n + ROOT_TILE - 1) / ROOT_TILE - 1;
-    if (last < 0) last = 0;
-    if ((int)blockIdx.x > last) return;
-    int offset = block_prefix_of(blocks, blockIdx.x, sm);
-    int base = blockIdx.x * ROOT_TILE + threadIdx.x * ROOT_ITEMS;
+    int ntiles = (n + ROOT_TILE - 1) / ROOT_TILE;
+    if (ntiles < 1) ntiles = 1;  // (tile 0 reports n_charts = 0)
+    int vb0, vb1;
+    tile_range(ntiles, vb0, vb1);
+    int offset = block_prefix_of(blocks, vb0, sm);
+    for (int vb = vb0; vb < vb1; vb++) {
+    int base = vb * ROOT_TILE + threadIdx.x * ROOT_ITEMS;
     int tv[ROOT_ITEMS];
     int c = 0;
 #pragma unroll
@@ -655,14 +691,19 @@ __global__ void __launch_bounds__(CMP_THREADS) k_scatter_roots(const int* __rest
             pos++;
         }
     }
-    if ((int)blockIdx.x == last && threadIdx.x == 0) st->n_charts = offset + total;
+    if (vb == ntiles - 1 && threadIdx.x == 0) st->n_charts = offset + total;
+    offset += total;
+    __syncthreads();  // sm is reused by the next tile's scan
+    }
 }
 
 void fa_launch_compact_roots(const int* vis_list, const int* label, int T, int* blocks, int* roots, int* cidx,
                              unsigned long long* ndc_keys, int* survived, fa_dstat* st, cudaStream_t s) {
     int nb = blocks_for(T, ROOT_TILE);
-    fa_launch(k_count_roots, nb, CMP_THREADS, 0, s, vis_list, label, blocks, st);
-    fa_launch(k_scatter_roots, nb, CMP_THREADS, 0, s, vis_list, label, blocks, nb, roots, cidx, ndc_keys, survived, st);
+    fa_launch(k_count_roots, fa_wave_grid(k_count_roots, CMP_THREADS, 0, nb, nb), CMP_THREADS, 0, s, vis_list, label,
+              blocks, st);
+    fa_launch(k_scatter_roots, fa_wave_grid(k_scatter_roots, CMP_THREADS, 0, nb, nb), CMP_THREADS, 0, s, vis_list,
+              label, blocks, nb, roots, cidx, ndc_keys, survived, st);
 }
 
 FA_TRACE_TU(charts)
