@@ -957,7 +957,9 @@ void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* c
     if (depth && npx / 2 > work) work = npx / 2;
     int nflag32 = flags ? (T + 3) / 4 : 0;
     if (nflag32 > work) work = nflag32;
-    fa_launch(k_frame_init, fa_grid(work, 256, max_blocks > 0 ? max_blocks : FA_NUM_SMS * 8), 256, 0, s, 
+    fa_launch(k_frame_init, max_blocks > 0 ? fa_grid(work, 256, max_blocks)
+                                           : fa_wave_grid(k_frame_init, 256, 0, (work + 255) / 256, FA_NUM_SMS * 8),
+              256, 0, s, 
         pos, V, vp, clip, scr, W, H, vmin, depth, wid, npx, reinterpret_cast<unsigned int*>(flags), nflag32, ndc2);
 }
 
@@ -972,6 +974,14 @@ static void fork_to(cudaStream_t s, cudaStream_t side, cudaEvent_t ev) {
 // tiles on side} || {clipped polygons -> their tiles on side2}, joined back
 // into s.  Every branch only lowers depth keys with atomicMin, so their order
 // does not matter.
+#ifndef TILES_WAVE
+#define TILES_WAVE 1
+#endif
+#if TILES_WAVE
+#define TILES_GRID(cap) fa_wave_grid(k_raster_depth_tiles, 256, 0, (cap), (cap))
+#else
+#define TILES_GRID(cap) fa_cap(cap)
+#endif
 int fa_launch_depth_pass(bool write_depth, const ClipSrc clip, const double4* scr, const int* tris, int T, int W,
                          int H, int cull, unsigned long long* depth, unsigned long long* wid, SmallRec* small_rec,
                          int* clip_list, TriSetup* large, int max_large, int4* tiles, int max_tiles, fa_dstat* st,
@@ -992,11 +1002,11 @@ int fa_launch_depth_pass(bool write_depth, const ClipSrc clip, const double4* sc
         //   s:     small unclipped records (warp-cooperative)
         //   side:  the unclipped large records' tiles
         //   side2: clipped polygons -> their tiles
-        fa_launch(k_raster_depth_tiles, fa_cap(FA_NUM_SMS * 8), 256, 0, b, small_rec, large, tiles, W, depth, wid, st,
+        fa_launch(k_raster_depth_tiles, TILES_GRID(FA_NUM_SMS * 8), 256, 0, b, small_rec, large, tiles, W, depth, wid, st,
                   max_tiles, 0, 1, 0);
         fa_launch(k_raster_clipped<true>, fa_cap(FA_NUM_SMS * 2), 256, 0, b2, clip, tris, W, H, cull, clip_list, depth, wid,
                   large, max_large, tiles, max_tiles, st);
-        fa_launch(k_raster_depth_tiles, fa_cap(FA_NUM_SMS * 4), 256, 0, b2, small_rec, large, tiles, W, depth, wid, st,
+        fa_launch(k_raster_depth_tiles, TILES_GRID(FA_NUM_SMS * 4), 256, 0, b2, small_rec, large, tiles, W, depth, wid, st,
                   max_tiles, 0, 1, 1);
         fa_launch(k_small_coop, fa_grid((long long)T, COOP_WARPS * 32 * 2, FA_NUM_SMS * COOP_GRID_MULT), COOP_WARPS * 32, 0,
                   s, small_rec, W, depth, wid, st);
