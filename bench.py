@@ -423,7 +423,7 @@ def measure_gpu(args, rank: int, world: int, local: int, view_ids: list) -> dict
     for kind, outputs in (("compact", ("visible", "visible_chart", "vertex_uv", "placements")),
                           ("dense", ("chart_of_triangle", "visible", "uv", "placements"))):
         pipe = fa.FramePipeline(mesh, device=local, settings=settings, depth=args.depth, outputs=outputs,
-                                mesh_replicas=replicas)
+                                mesh_replicas=replicas, packed=not os.environ.get("FA_BENCH_UNPACKED"))
         d2h = [0]
 
         def count(hf):

@@ -257,6 +257,31 @@ int fa_frame_download_visible(fa_ctx *ctx, const fa_frame_result *res, int32_t *
 int fa_frame_download_compact(fa_ctx *ctx, const fa_frame_result *res, int32_t *visible, int32_t *visible_chart,
                               int32_t *visible_vertices, float *vertex_uv, int64_t *placements, void *stream);
 
+/* Packed wire format (about half the bytes of the compact one, for the
+ * same information):
+ *   visible_mask  ceil(T/32) uint32: bit t % 32 of word t / 32 set for each
+ *                 visible triangle (the reference's mark_visible flags,
+ *                 charts.py:302-313, packed; visible = flatnonzero),
+ *   visible_cidx  n_visible uint16: the index of each visible triangle's
+ *                 chart in `roots` (chart id = roots[visible_cidx[i]]),
+ *   roots         n_charts int32: the chart ids (root triangle ids, ascending),
+ *   vertex_mask   ceil(V/32) uint32: bit i set for the i-th vertex of the
+ *                 context's vertex order (fa_vertex_order) that a visible
+ *                 triangle touches, and
+ *   vertex_uv     n_visible_vertices x 2 float32 in that same order (as in
+ *                 fa_frame_download_compact), placements as above.
+ * FA_VALUE_ERROR when the frame has more than 65535 charts (use
+ * fa_frame_download_compact).  Same conventions as fa_frame_download. */
+int fa_frame_download_packed(fa_ctx *ctx, const fa_frame_result *res, uint32_t *visible_mask,
+                             uint16_t *visible_cidx, int32_t *roots, uint32_t *vertex_mask, float *vertex_uv,
+                             int64_t *placements, void *stream);
+
+/* The context's vertex order (V int32 caller vertex ids; the identity when the
+ * mesh was bound without renumbering): entry i is the caller id of the i-th
+ * bit of fa_frame_download_packed's vertex_mask.  Changes only with
+ * fa_set_mesh.  Synchronises `stream`. */
+int fa_vertex_order(fa_ctx *ctx, int32_t *out, void *stream);
+
 /* Number of kernels the last fa_frame_launch enqueued (benchmark accounting). */
 int fa_last_launch_count(fa_ctx *ctx);
 

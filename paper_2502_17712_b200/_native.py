@@ -40,7 +40,7 @@ EXPORTS = (
     "fa_depth_prepass", "fa_mark_visible", "fa_build_adjacency", "fa_connected_charts", "fa_merge_shared_vertices",
     "fa_chart_boxes", "fa_blinn_clamped_ndc", "fa_select_side_plane", "fa_chart_bbox",
     "fa_viewport_box", "fa_orient", "fa_orient_order", "fa_fold", "fa_push_up", "fa_pack_at_scale",
-    "fa_pack", "fa_frame_launch", "fa_frame_finish", "fa_frame", "fa_frame_download", "fa_frame_download_visible", "fa_frame_download_compact", "fa_last_launch_count",
+    "fa_pack", "fa_frame_launch", "fa_frame_finish", "fa_frame", "fa_frame_download", "fa_frame_download_visible", "fa_frame_download_compact", "fa_frame_download_packed", "fa_vertex_order", "fa_last_launch_count",
     "fa_stage_times", "fa_stage_name", "fa_frame_counters", "fa_sequential_scale_search", "fa_sequential_pack", "fa_superblock_pack",
 )
 
@@ -134,6 +134,8 @@ def load_library():
             "fa_frame_download": ([vp, ctypes.POINTER(FrameResult), vp, vp, vp, vp, vp], ci),
             "fa_frame_download_visible": ([vp, ctypes.POINTER(FrameResult), vp, vp, vp, vp, vp], ci),
             "fa_frame_download_compact": ([vp, ctypes.POINTER(FrameResult), vp, vp, vp, vp, vp, vp], ci),
+            "fa_frame_download_packed": ([vp, ctypes.POINTER(FrameResult), vp, vp, vp, vp, vp, vp, vp], ci),
+            "fa_vertex_order": ([vp, vp, vp], ci),
             "fa_last_launch_count": ([vp], ci),
             "fa_stage_times": ([vp, ctypes.POINTER(ctypes.c_float), ci, vp], ci),
             "fa_stage_name": ([ci], ctypes.c_char_p),

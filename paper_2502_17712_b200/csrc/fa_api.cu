@@ -127,7 +127,7 @@ void fa_destroy(fa_ctx* c) {
                       &c->target, &c->survived, &c->okey, &c->oidx, &c->ow, &c->oh, &c->orot, &c->sortk, &c->sortv,
                       &c->pinv, &c->cand, &c->cand_p, &c->cand_w, &c->cand_h, &c->cand_y, &c->rowstart,
                       &c->placements, &c->uv, &c->vp_dev, &c->blocks, &c->dstat, &c->aux, &c->in_tw, &c->in_th,
-                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list, &c->hiz, &c->wid, &c->vis_chart, &c->vis_cidx, &c->plc_c, &c->pos_perm, &c->tris_perm, &c->vperm_buf, &c->vis_tris, &c->vslot, &c->vlist, &c->vuv, &c->vblocks, &c->pstat, &c->tperm_buf, &c->tris_sorted_buf, &c->clusters_buf, &c->live_buf, &c->mesh_first, &c->mesh_scratch, &c->mesh_sort, &c->mesh_tris_s, &c->ord_tw, &c->ord_th, &c->ord_cid, &c->ndc2};
+                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list, &c->hiz, &c->wid, &c->vis_chart, &c->vis_cidx, &c->plc_c, &c->pos_perm, &c->tris_perm, &c->vperm_buf, &c->vis_tris, &c->vslot, &c->vlist, &c->vuv, &c->vblocks, &c->pstat, &c->tperm_buf, &c->tris_sorted_buf, &c->clusters_buf, &c->live_buf, &c->mesh_first, &c->mesh_scratch, &c->mesh_sort, &c->mesh_tris_s, &c->ord_tw, &c->ord_th, &c->ord_cid, &c->ndc2, &c->vis_mask, &c->vvis_mask, &c->cidx16};
     for (fa_buf* b : bufs) free_buf(*b);
     for (cudaEvent_t e : c->fj)
         if (e) cudaEventDestroy(e);
@@ -1079,7 +1079,7 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     mark();  // 3: visibility pass
     // the compaction also lowers vmin (frame_init filled it with INT_MAX)
     fa_launch_compact_visible(flags, T, P<int>(ctx->blocks), P<int>(ctx->vis_list), P<int>(ctx->label), st, s,
-                              ctx->tris, P<int>(ctx->vmin), P<int4>(ctx->vis_tris));
+                              ctx->tris, P<int>(ctx->vmin), P<int4>(ctx->vis_tris), P<unsigned int>(ctx->vis_mask));
     nl += 2;
     mark();  // 4: visible compaction
     // debug knob (results invalid): end the frame after the raster passes
@@ -1101,7 +1101,7 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
     fa_launch_uf_compress(P<int>(ctx->vis_list), P<int>(ctx->label), T, st, ctx->side);
     fa_launch_v2c(P<int>(ctx->vmin), P<int>(ctx->label), P<int>(ctx->v2c), V, ctx->side, ctx->vperm);
     fa_launch_visible_vertices(P<int>(ctx->vmin), V, ctx->vperm, P<int>(ctx->vblocks), P<int>(ctx->vslot),
-                               P<int>(ctx->vlist), st, ctx->side, P<float2>(ctx->vuv));
+                               P<int>(ctx->vlist), st, ctx->side, P<float2>(ctx->vuv), P<unsigned int>(ctx->vvis_mask));
     CK(cudaEventRecord(ctx->fj[6], ctx->side));
     nl += 4;
     fa_launch_compact_roots(P<int>(ctx->vis_list), P<int>(ctx->label), T, P<int>(ctx->blocks), P<int>(ctx->roots),
@@ -1140,7 +1140,7 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
                  P<int>(ctx->pinv), P<double>(ctx->ndc), P<int>(ctx->px), P<long long>(ctx->placements), T, W, H,
                  p->padding, p->uv_f64 != 0, ctx->uv.p, P<int>(ctx->vis_chart), P<int>(ctx->vis_cidx),
                  p->packer == FA_PACKER_FASTATLAS ? P<int4>(ctx->plc_c) : nullptr, st, s, P<int4>(ctx->vis_tris),
-                 P<int>(ctx->vslot), P<float2>(ctx->vuv), P<double2>(ctx->ndc2));
+                 P<int>(ctx->vslot), P<float2>(ctx->vuv), P<double2>(ctx->ndc2), P<unsigned short>(ctx->cidx16));
     nl += 1;
     mark();  // 10: uv
     if (p->want_depth) {
@@ -1174,6 +1174,9 @@ static int frame_prepare(fa_ctx* ctx, const fa_frame_params* p) {
     ENSURE(uv, (size_t)(ctx->T + 1) * 6 * (p->uv_f64 ? 8 : 4));
     ENSURE(vis_chart, (size_t)(ctx->T + 1) * 4);
     ENSURE(vis_cidx, (size_t)(ctx->T + 1) * 4);
+    ENSURE(vis_mask, (size_t)(ctx->T / 32 + 1) * 4);
+    ENSURE(vvis_mask, (size_t)(ctx->V / 32 + 1) * 4);
+    ENSURE(cidx16, (size_t)(ctx->T + 1) * 2);
     ENSURE(vslot, (size_t)(ctx->V + 1) * 4);
     ENSURE(vlist, (size_t)(ctx->V + 1) * 4);
     ENSURE(vuv, (size_t)(ctx->V + 1) * 8);
@@ -1360,6 +1363,40 @@ int fa_frame_download_compact(fa_ctx* ctx, const fa_frame_result* res, int32_t* 
         CK(cudaMemcpyAsync(visible_vertices, res->visible_vertices, nvv * 4, cudaMemcpyDefault, s));
     if (vertex_uv && nvv) CK(cudaMemcpyAsync(vertex_uv, res->vertex_uv, nvv * 8, cudaMemcpyDefault, s));
     if (placements && C) CK(cudaMemcpyAsync(placements, res->placements, C * 64, cudaMemcpyDefault, s));
+    return FA_OK;
+}
+
+int fa_frame_download_packed(fa_ctx* ctx, const fa_frame_result* res, uint32_t* visible_mask,
+                             uint16_t* visible_cidx, int32_t* roots, uint32_t* vertex_mask, float* vertex_uv,
+                             int64_t* placements, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || !res) return set_err(FA_VALUE_ERROR, "bad arguments");
+    if (res->status != FA_OK) return set_err(FA_VALUE_ERROR, "frame result has no outputs (status %d)", res->status);
+    if (res->n_charts > 65535) return set_err(FA_VALUE_ERROR, "more than 65535 charts: use fa_frame_download_compact");
+    if (!ctx->vis_mask.p || !ctx->cidx16.p) return set_err(FA_VALUE_ERROR, "no frame outputs");
+    CK(cudaSetDevice(ctx->device));
+    size_t nv = (size_t)res->n_visible, C = (size_t)res->n_charts, nvv = (size_t)res->n_visible_vertices;
+    if (visible_mask && ctx->T)
+        CK(cudaMemcpyAsync(visible_mask, ctx->vis_mask.p, (size_t)((ctx->T + 31) / 32) * 4, cudaMemcpyDefault, s));
+    if (visible_cidx && nv) CK(cudaMemcpyAsync(visible_cidx, ctx->cidx16.p, nv * 2, cudaMemcpyDefault, s));
+    if (roots && C) CK(cudaMemcpyAsync(roots, res->roots, C * 4, cudaMemcpyDefault, s));
+    if (vertex_mask && ctx->V)
+        CK(cudaMemcpyAsync(vertex_mask, ctx->vvis_mask.p, (size_t)((ctx->V + 31) / 32) * 4, cudaMemcpyDefault, s));
+    if (vertex_uv && nvv) CK(cudaMemcpyAsync(vertex_uv, res->vertex_uv, nvv * 8, cudaMemcpyDefault, s));
+    if (placements && C) CK(cudaMemcpyAsync(placements, res->placements, C * 64, cudaMemcpyDefault, s));
+    return FA_OK;
+}
+
+int fa_vertex_order(fa_ctx* ctx, int32_t* out, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || !out) return set_err(FA_VALUE_ERROR, "bad arguments");
+    CK(cudaSetDevice(ctx->device));
+    if (ctx->vperm) {
+        CK(cudaMemcpyAsync(out, ctx->vperm, (size_t)ctx->V * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    } else {
+        for (int64_t v = 0; v < ctx->V; v++) out[v] = (int32_t)v;
+    }
     return FA_OK;
 }
 

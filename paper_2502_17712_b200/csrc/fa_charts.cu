@@ -51,6 +51,17 @@ __device__ __forceinline__ int block_prefix_of(const int* blocks, int b, int* sm
     return tot;
 }
 
+// Bit mask of 4 items per lane, lanes in order (lane l holds items 4l..4l+3
+// of the warp's 128): the 8 lanes of a group OR their nibbles into one 32-bit
+// word, which the group's first lane returns (others return 0).
+__device__ __forceinline__ unsigned int nibble_word(unsigned int nib) {
+    unsigned int v = (nib & 15u) << (4 * (lane_id() & 7));
+    v |= __shfl_xor_sync(0xffffffffu, v, 1);
+    v |= __shfl_xor_sync(0xffffffffu, v, 2);
+    v |= __shfl_xor_sync(0xffffffffu, v, 4);
+    return v;
+}
+
 // ---- visible compaction ----------------------------------------------------
 // The compactions run a wave-sized grid; CTA b handles the contiguous tiles
 // [b * per, (b + 1) * per) of the fixed tile partition (vb = tile index).
@@ -94,7 +105,8 @@ __global__ void __launch_bounds__(CMP_THREADS) k_scatter_visible(const unsigned 
                                                                  int* __restrict__ vis_list, int* __restrict__ label,
                                                                  const int* __restrict__ tris, int* __restrict__ vmin,
                                                                  int4* __restrict__ vis_tris,
-                                                                 fa_dstat* __restrict__ st) {
+                                                                 fa_dstat* __restrict__ st,
+                                                                 unsigned int* __restrict__ vis_mask) {
     FA_PDL_PROLOGUE();
     __shared__ int sm[32];
     int vb0, vb1;
@@ -117,6 +129,13 @@ __global__ void __launch_bounds__(CMP_THREADS) k_scatter_visible(const unsigned 
     int c = 0;
 #pragma unroll
     for (int i = 0; i < CMP_ITEMS; i++) c += f[i] != 0;
+    if (vis_mask) {
+        // the visibility flags as a bit mask (the packed download format):
+        // bit t of word t / 32
+        static_assert(CMP_ITEMS == 4, "one nibble per thread");
+        const unsigned int w = nibble_word((f[0] != 0) | ((f[1] != 0) << 1) | ((f[2] != 0) << 2) | ((f[3] != 0) << 3));
+        if ((lane_id() & 7) == 0 && base < T) vis_mask[base >> 5] = w;
+    }
     int total;
     int pos = offset + block_exclusive_scan(c, sm, &total);
     if (base + CMP_ITEMS <= T) {
@@ -161,13 +180,14 @@ __global__ void __launch_bounds__(CMP_THREADS) k_scatter_visible(const unsigned 
 }
 
 void fa_launch_compact_visible(const unsigned char* flags, int T, int* blocks, int* vis_list, int* label,
-                               fa_dstat* st, cudaStream_t s, const int* tris, int* vmin, int4* vis_tris) {
+                               fa_dstat* st, cudaStream_t s, const int* tris, int* vmin, int4* vis_tris,
+                               unsigned int* vis_mask) {
     int nb = blocks_for(T, CMP_TILE);
     fa_launch(k_count_flags, fa_wave_grid(k_count_flags, CMP_THREADS, 0, nb, nb), CMP_THREADS, 0, s, flags, T, blocks,
               nb);
     fa_launch(k_scatter_visible, fa_wave_grid(k_scatter_visible, CMP_THREADS, 0, nb, nb), CMP_THREADS, 0, s, flags, T,
               blocks, nb, vis_list, label, tris, vmin,
-              tris ? vis_tris : nullptr, st);
+              tris ? vis_tris : nullptr, st, vis_mask);
 }
 
 // ---- union-find ---------------------------------------------------------------
@@ -566,7 +586,8 @@ __global__ void __launch_bounds__(CMP_THREADS) k_vert_scatter(const int* __restr
                                                               const int* __restrict__ blocks, int nblocks,
                                                               const int* __restrict__ vperm, int* __restrict__ vslot,
                                                               int* __restrict__ vlist, float2* __restrict__ vuv,
-                                                              fa_dstat* __restrict__ st) {
+                                                              fa_dstat* __restrict__ st,
+                                                              unsigned int* __restrict__ vvis_mask) {
     FA_PDL_PROLOGUE();
     __shared__ int sm[32];
     const int offset = block_prefix_of(blocks, blockIdx.x, sm);
@@ -577,6 +598,14 @@ __global__ void __launch_bounds__(CMP_THREADS) k_vert_scatter(const int* __restr
     for (int i = 0; i < VTX_ITEMS; i++) {
         vis[i] = base + i < V && vmin[base + i] != 0x7fffffff;
         c += vis[i];
+    }
+    if (vvis_mask) {
+        // the visible vertices as a bit mask over the context's vertex order
+        // (the order of vlist / vuv; the host maps it through the vertex
+        // order once per mesh)
+        static_assert(VTX_ITEMS == 4, "one nibble per thread");
+        const unsigned int w = nibble_word(vis[0] | (vis[1] << 1) | (vis[2] << 2) | (vis[3] << 3));
+        if ((lane_id() & 7) == 0 && base < V) vvis_mask[base >> 5] = w;
     }
     int total;
     int pos = offset + block_exclusive_scan(c, sm, &total);
@@ -601,10 +630,10 @@ int fa_vertex_blocks(long long V) {
 }
 
 void fa_launch_visible_vertices(const int* vmin, int V, const int* vperm, int* blocks, int* vslot, int* vlist,
-                                fa_dstat* st, cudaStream_t s, float2* vuv) {
+                                fa_dstat* st, cudaStream_t s, float2* vuv, unsigned int* vvis_mask) {
     const int nb = fa_vertex_blocks(V);
     fa_launch(k_vert_count, nb, CMP_THREADS, 0, s, vmin, V, blocks);
-    fa_launch(k_vert_scatter, nb, CMP_THREADS, 0, s, vmin, V, blocks, nb, vperm, vslot, vlist, vuv, st);
+    fa_launch(k_vert_scatter, nb, CMP_THREADS, 0, s, vmin, V, blocks, nb, vperm, vslot, vlist, vuv, st, vvis_mask);
 }
 
 void fa_launch_v2c(const int* vmin, const int* label, int* v2c, int V, cudaStream_t s, const int* vperm) {

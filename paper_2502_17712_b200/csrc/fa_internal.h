@@ -101,6 +101,9 @@ struct fa_ctx {
     fa_buf hiz;             // 8x8 hierarchical-Z max keys of the final depth
     fa_buf wid;             // pass-1 pixel winners (truncated key | triangle id)
     fa_buf vis_chart;       // chart id of each visible triangle (written by k_uv)
+    fa_buf vis_mask;        // packed download format: visibility bit per triangle (k_scatter_visible)
+    fa_buf vvis_mask;       //   bit per vertex in the context's order (k_vert_scatter)
+    fa_buf cidx16;          //   16-bit chart index per visible triangle (k_uv)
     fa_buf vis_cidx;        // chart index of each visible triangle (written by k_chart_bounds, read by k_uv)
     fa_buf plc_c;           // placements by chart index (2 x int4 each; written by k_select, read by k_uv)
     fa_buf vis_tris;        // (a, b, c, t) of each visible triangle (written by the compaction)
@@ -174,7 +177,8 @@ size_t fa_trisetup_bytes();
 // non-null) and vmin lowering (when non-null)
 void fa_launch_compact_visible(const unsigned char* flags, int T, int* blocks, int* vis_list, int* label,
                                fa_dstat* st, cudaStream_t s, const int* tris = nullptr, int* vmin = nullptr,
-                               int4* vis_tris = nullptr);
+                               int4* vis_tris = nullptr,
+                               unsigned int* vis_mask = nullptr);
 int fa_compact_blocks(long long n);
 // vmin_ready: vmin already holds the per-vertex minima (computed by the
 // visible compaction); otherwise it must hold INT_MAX and is computed here
@@ -194,7 +198,8 @@ void fa_launch_v2c(const int* vmin, const int* label, int* v2c, int V, cudaStrea
 // blocks holds fa_vertex_blocks(V) ints
 int fa_vertex_blocks(long long V);
 void fa_launch_visible_vertices(const int* vmin, int V, const int* vperm, int* blocks, int* vslot, int* vlist,
-                                fa_dstat* st, cudaStream_t s, float2* vuv = nullptr);
+                                fa_dstat* st, cudaStream_t s, float2* vuv = nullptr,
+                                unsigned int* vvis_mask = nullptr);
 // out[v] = pos[vperm[v]] (3 doubles each)
 void fa_launch_permute_pos(const double* pos, const int* vperm, double* out, int V, cudaStream_t s);
 void fa_launch_flags_from_labels(const int* labels, unsigned char* flags, int T, cudaStream_t s);
@@ -279,7 +284,7 @@ void fa_launch_uv(const ClipSrc clip, const int* tris, const int* vis_list, cons
                   const int* pinv, const double* ndc, const int* px, const long long* placements, int T, int W, int H,
                   long long pad, bool f64, void* uv, int* vis_chart, const int* vis_cidx, const int4* plc_c,
                   fa_dstat* st, cudaStream_t s, const int4* vis_tris = nullptr, const int* vslot = nullptr,
-                  float2* vuv = nullptr, const double2* ndc2 = nullptr);
+                  float2* vuv = nullptr, const double2* ndc2 = nullptr, unsigned short* cidx16 = nullptr);
 
 // ---- comparison packers (fa_baselines.cu) -----------------------------------
 void fa_launch_seq_search(const long long* ow, const long long* oh, int n, long long omega, long long n_scales,

@@ -43,7 +43,8 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const ClipSrc clip, const int
                                                    int* __restrict__ vis_chart, const int* __restrict__ vis_cidx,
                                                    const int4* __restrict__ plc_c, const int4* __restrict__ vis_tris,
                                                    const int* __restrict__ vslot, float2* __restrict__ vuv,
-                                                   fa_dstat* __restrict__ st, const double2* __restrict__ ndc2) {
+                                                   fa_dstat* __restrict__ st, const double2* __restrict__ ndc2,
+                                                   unsigned short* __restrict__ cidx16) {
     FA_PDL_PROLOGUE();
     __shared__ __align__(16) OutT stage[UV_THREADS * 6];
     __shared__ double red_w[UV_THREADS / 32], red_a[UV_THREADS / 32], red_m[UV_THREADS / 32];
@@ -61,6 +62,9 @@ __global__ void __launch_bounds__(UV_THREADS) k_uv(const ClipSrc clip, const int
         int4 vq = make_int4(0, 0, 0, -1);
         if (k < n && vis_tris) vq = vis_tris[k];
         if (k < n && vis_chart) vis_chart[k] = label[vis_tris ? vq.w : vis_list[k]];  // sparse chart_of_triangle
+        // packed download format: the chart's index (roots[index] = its id),
+        // 16 bits when the frame has < 2^16 charts (else the host takes vis_chart)
+        if (k < n && cidx16 && vis_cidx && st->n_charts <= 65535) cidx16[k] = (unsigned short)vis_cidx[k];
         if (k < n && !failed) {
             int t = vis_tris ? vq.w : vis_list[k];
             // chart index and placement straight from the bounds / select
@@ -202,17 +206,17 @@ void fa_launch_uv(const ClipSrc clip, const int* tris, const int* vis_list, cons
                   const int* pinv, const double* ndc, const int* px, const long long* placements, int T, int W, int H,
                   long long pad, bool f64, void* uv, int* vis_chart, const int* vis_cidx, const int4* plc_c,
                   fa_dstat* st, cudaStream_t s, const int4* vis_tris, const int* vslot, float2* vuv,
-                  const double2* ndc2) {
+                  const double2* ndc2, unsigned short* cidx16) {
     if (!vis_tris) vuv = nullptr;  // the compact UVs index vertices through vis_tris
     const long long nblk = ((long long)T + UV_THREADS - 1) / UV_THREADS;
     const int grid = f64 ? fa_wave_grid(k_uv<double>, UV_THREADS, 0, nblk, FA_NUM_SMS * 8)
                          : fa_wave_grid(k_uv<float>, UV_THREADS, 0, nblk, FA_NUM_SMS * 8);
     if (f64)
         fa_launch(k_uv<double>, grid, UV_THREADS, 0, s, clip, tris, vis_list, label, cidx, pinv, ndc, px, placements, W, H,
-                                                 pad, (double*)uv, vis_chart, vis_cidx, plc_c, vis_tris, vslot, vuv, st, ndc2);
+                                                 pad, (double*)uv, vis_chart, vis_cidx, plc_c, vis_tris, vslot, vuv, st, ndc2, cidx16);
     else
         fa_launch(k_uv<float>, grid, UV_THREADS, 0, s, clip, tris, vis_list, label, cidx, pinv, ndc, px, placements, W, H,
-                                                pad, (float*)uv, vis_chart, vis_cidx, plc_c, vis_tris, vslot, vuv, st, ndc2);
+                                                pad, (float*)uv, vis_chart, vis_cidx, plc_c, vis_tris, vslot, vuv, st, ndc2, cidx16);
 }
 
 FA_TRACE_TU(uv)

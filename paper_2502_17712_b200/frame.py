@@ -233,8 +233,8 @@ class HostFrame:
     is the downloaded rows when the pipeline asked for "uv")."""
 
     __slots__ = ("index", "status", "error", "n_visible", "n_charts", "scale", "screen_fragments",
-                 "texels_allocated", "_cot", "_T", "visible", "visible_chart", "_uv", "_uv_copied", "placements",
-                 "visible_vertices", "vertex_uv", "_tris", "_V")
+                 "texels_allocated", "_cot", "_T", "_visible", "_visible_chart", "_uv", "_uv_copied", "placements",
+                 "_visible_vertices", "vertex_uv", "_tris", "_V", "_packed")
 
     def __init__(self, index: int, n_triangles: int = 0, triangles=None, n_vertices: int = 0):
         self.index = index
@@ -243,12 +243,49 @@ class HostFrame:
         self.n_visible = self.n_charts = 0
         self.scale = None
         self.screen_fragments = self.texels_allocated = 0
-        self._cot = self.visible = self.visible_chart = self._uv = self.placements = None
-        self.visible_vertices = self.vertex_uv = None
+        self._cot = self._visible = self._visible_chart = self._uv = self.placements = None
+        self._visible_vertices = self.vertex_uv = None
         self._uv_copied = False
         self._T = n_triangles
         self._tris = triangles
         self._V = n_vertices
+        # packed wire format (fa_frame_download_packed): (visible bit mask,
+        # 16-bit chart index per visible triangle, chart ids, vertex bit mask,
+        # vertex order); the lists below are decoded from it on first access
+        self._packed = None
+
+    @property
+    def visible(self):
+        if self._visible is None and self._packed is not None:
+            m = self._packed[0]
+            self._visible = np.flatnonzero(np.unpackbits(m.view(np.uint8), bitorder="little",
+                                                         count=self._T)).astype(np.int32)
+        return self._visible
+
+    @visible.setter
+    def visible(self, v):
+        self._visible = v
+
+    @property
+    def visible_chart(self):
+        if self._visible_chart is None and self._packed is not None:
+            self._visible_chart = self._packed[2][self._packed[1]].astype(np.int32)
+        return self._visible_chart
+
+    @visible_chart.setter
+    def visible_chart(self, v):
+        self._visible_chart = v
+
+    @property
+    def visible_vertices(self):
+        if self._visible_vertices is None and self._packed is not None:
+            bits = np.unpackbits(self._packed[3].view(np.uint8), bitorder="little", count=self._V)
+            self._visible_vertices = self._packed[4][np.flatnonzero(bits)]
+        return self._visible_vertices
+
+    @visible_vertices.setter
+    def visible_vertices(self, v):
+        self._visible_vertices = v
 
     @property
     def uv(self):
@@ -271,8 +308,11 @@ class HostFrame:
     def d2h_bytes(self) -> int:
         """Bytes copied device -> host for this view (a rebuilt dense chart
         array is host work, not a copy)."""
-        arrs = (self.visible, self.visible_chart, self._uv if self._uv_copied else None, self.placements,
-                self.visible_vertices, self.vertex_uv)
+        if self._packed is not None:
+            arrs = self._packed[:4] + (self.vertex_uv, self.placements)
+        else:
+            arrs = (self._visible, self._visible_chart, self._uv if self._uv_copied else None, self.placements,
+                    self._visible_vertices, self.vertex_uv)
         n = sum(a.nbytes for a in arrs if a is not None)
         if self._cot is not None and self.visible_chart is None:
             n += self._cot.nbytes
@@ -286,11 +326,15 @@ class FramePipeline:
     SMs its latency-bound stages leave idle and the copy engines return the
     finished frames' chart ids, visible list, UVs and placements to pinned
     host memory.  Results are delivered in view order through
-    `on_frame(HostFrame)`."""
+    `on_frame(HostFrame)`.  With the default compact outputs the copies use
+    the packed wire format (fa_frame_download_packed: visibility and vertex
+    bit masks, 16-bit chart indices; about half the bytes), decoded into the
+    same HostFrame lists on first access; packed=False copies the int32
+    lists."""
 
     def __init__(self, mesh: Mesh, device: int | None = None, settings: FrameSettings | None = None,
                  depth: int = 4, outputs: tuple = ("visible", "visible_chart", "vertex_uv", "placements"),
-                 mesh_replicas: bool = False):
+                 mesh_replicas: bool = False, packed: bool = True):
         torch = nat.require_device()
         if depth < 1:
             raise ValueError("depth must be >= 1")
@@ -316,10 +360,22 @@ class FramePipeline:
             elif "vertex_uv" in outputs:
                 h["visible_vertices"] = torch.empty(mesh.n_vertices, dtype=torch.int32).pin_memory()
                 h["vertex_uv"] = torch.empty((mesh.n_vertices, 2), dtype=torch.float32).pin_memory()
+                if packed and "visible" in outputs and "visible_chart" in outputs and "chart_of_triangle" not in outputs:
+                    # the packed wire format (about half the bytes); the int32
+                    # lists above stay for frames with more than 65535 charts
+                    h["p_vis_mask"] = torch.empty(T // 32 + 1, dtype=torch.int32).pin_memory()
+                    h["p_cidx"] = torch.empty(T + 1, dtype=torch.int16).pin_memory()
+                    h["p_roots"] = torch.empty(T + 1, dtype=torch.int32).pin_memory()
+                    h["p_vtx_mask"] = torch.empty(mesh.n_vertices // 32 + 1, dtype=torch.int32).pin_memory()
             if "placements" in outputs:
                 h["placements"] = torch.empty((T + 1, 8), dtype=torch.int64).pin_memory()
             self._host.append(h)
         self._np = [{k: t.numpy() for k, t in h.items()} for h in self._host]
+        for h in self._np:  # unsigned views of the packed arrays
+            for k, dt in (("p_vis_mask", np.uint32), ("p_cidx", np.uint16), ("p_vtx_mask", np.uint32)):
+                if k in h:
+                    h[k] = h[k].view(dt)
+        self._vorder = [None] * depth  # each slot context's vertex order (fa_vertex_order), fetched once
         self._tris = np.asarray(mesh.triangles)
         self._V = mesh.n_vertices
 
@@ -358,6 +414,23 @@ class FramePipeline:
         ptr = {k: ctypes.c_void_p(t.data_ptr()) if k in h else None
                for k, t in ((k, h.get(k)) for k in ("chart_of_triangle", "visible", "visible_chart", "uv",
                                                      "placements", "visible_vertices", "vertex_uv"))}
+        if "p_vis_mask" in h and C <= 65535:
+            if self._vorder[slot] is None:
+                vo = np.empty(self._V, dtype=np.int32)
+                nat.raise_for_status(L.fa_vertex_order(h_ctx, ctypes.c_void_p(vo.ctypes.data), sp))
+                self._vorder[slot] = vo
+            pp = {k: ctypes.c_void_p(h[k].data_ptr()) for k in ("p_vis_mask", "p_cidx", "p_roots", "p_vtx_mask")}
+            nat.raise_for_status(L.fa_frame_download_packed(h_ctx, ctypes.byref(res), pp["p_vis_mask"], pp["p_cidx"],
+                                                            pp["p_roots"], pp["p_vtx_mask"], ptr["vertex_uv"],
+                                                            ptr["placements"], sp))
+            n = self._np[slot]
+            nvv = int(res.n_visible_vertices)
+            hf._packed = (n["p_vis_mask"][:(self._tris.shape[0] + 31) // 32], n["p_cidx"][:nv], n["p_roots"][:C],
+                          n["p_vtx_mask"][:(self._V + 31) // 32], self._vorder[slot])
+            hf.vertex_uv = n["vertex_uv"][:nvv]
+            if "placements" in h:
+                hf.placements = n["placements"][:C]
+            return hf
         if ptr["vertex_uv"] is not None:
             nat.raise_for_status(L.fa_frame_download_compact(h_ctx, ctypes.byref(res), ptr["visible"],
                                                              ptr["visible_chart"], ptr["visible_vertices"],

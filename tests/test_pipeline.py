@@ -29,9 +29,9 @@ def _vps(spec, poses):
     return out
 
 
-@pytest.mark.parametrize("depth,outputs", [(1, None), (3, None),
-                                           (2, ("chart_of_triangle", "visible", "uv", "placements"))])
-def test_pipeline_matches_sequential(depth, outputs):
+@pytest.mark.parametrize("depth,outputs,packed", [(1, None, True), (3, None, True), (3, None, False),
+                                                  (2, ("chart_of_triangle", "visible", "uv", "placements"), True)])
+def test_pipeline_matches_sequential(depth, outputs, packed):
     """Sparse chart ids (default: visible_chart, dense array rebuilt on the
     host) and the dense download give the sequential engine's outputs."""
     spec = scenes.build_scene("C5")
@@ -50,9 +50,11 @@ def test_pipeline_matches_sequential(depth, outputs):
     def on_frame(hf):
         assert hf.error is None, hf.error
         got.append((hf.index, {"chart": hf.chart_of_triangle.copy(), "vis": hf.visible.copy(), "uv": hf.uv.copy(),
-                               "plc": hf.placements.copy(), "scale": hf.scale, "frag": hf.screen_fragments}))
+                               "plc": hf.placements.copy(), "scale": hf.scale, "frag": hf.screen_fragments,
+                               "vchart": None if hf.visible_chart is None else hf.visible_chart.copy(),
+                               "vv": None if hf.visible_vertices is None else np.sort(hf.visible_vertices)}))
 
-    kw = {} if outputs is None else {"outputs": outputs}
+    kw = {"packed": packed} if outputs is None else {"outputs": outputs}
     pipe = FramePipeline(mesh, settings=settings, depth=depth, **kw)
     assert pipe.run(vps, on_frame) == len(vps)
     assert [i for i, _ in got] == list(range(len(vps)))
@@ -62,6 +64,10 @@ def test_pipeline_matches_sequential(depth, outputs):
         assert np.array_equal(g["uv"].view(np.uint32), w["uv"].view(np.uint32))
         assert np.array_equal(g["plc"], w["plc"])
         assert g["scale"] == w["scale"] and g["frag"] == w["frag"]
+        if g["vchart"] is not None:
+            assert np.array_equal(g["vchart"], w["chart"][w["vis"]])
+        if g["vv"] is not None:  # every vertex of a visible triangle, once
+            assert np.array_equal(g["vv"], np.unique(spec.triangles[w["vis"]]))
 
 
 def test_pipeline_reports_failures_in_order():
