@@ -568,17 +568,22 @@ __global__ void __launch_bounds__(CMP_THREADS) k_vert_count(const int* __restric
                                                             int* __restrict__ blocks) {
     FA_PDL_PROLOGUE();
     __shared__ int sm[32];
-    const int base = blockIdx.x * VTX_TILE + threadIdx.x * VTX_ITEMS;
-    int c = 0;
+    int vb0, vb1;
+    tile_range((V + VTX_TILE - 1) / VTX_TILE, vb0, vb1);
+    for (int vb = vb0; vb < vb1; vb++) {
+        const int base = vb * VTX_TILE + threadIdx.x * VTX_ITEMS;
+        int c = 0;
 #pragma unroll
-    for (int i = 0; i < VTX_ITEMS; i++) c += (base + i < V && vmin[base + i] != 0x7fffffff);
-    c = warp_sum(c);
-    if (lane_id() == 0) sm[threadIdx.x >> 5] = c;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int s = 0;
-        for (int i = 0; i < CMP_THREADS / 32; i++) s += sm[i];
-        blocks[blockIdx.x] = s;
+        for (int i = 0; i < VTX_ITEMS; i++) c += (base + i < V && vmin[base + i] != 0x7fffffff);
+        c = warp_sum(c);
+        if (lane_id() == 0) sm[threadIdx.x >> 5] = c;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int s = 0;
+            for (int i = 0; i < CMP_THREADS / 32; i++) s += sm[i];
+            blocks[vb] = s;
+        }
+        __syncthreads();
     }
 }
 
@@ -590,8 +595,11 @@ __global__ void __launch_bounds__(CMP_THREADS) k_vert_scatter(const int* __restr
                                                               unsigned int* __restrict__ vvis_mask) {
     FA_PDL_PROLOGUE();
     __shared__ int sm[32];
-    const int offset = block_prefix_of(blocks, blockIdx.x, sm);
-    const int base = blockIdx.x * VTX_TILE + threadIdx.x * VTX_ITEMS;
+    int vb0, vb1;
+    tile_range(nblocks, vb0, vb1);
+    int offset = block_prefix_of(blocks, vb0, sm);
+    for (int vb = vb0; vb < vb1; vb++) {
+    const int base = vb * VTX_TILE + threadIdx.x * VTX_ITEMS;
     bool vis[VTX_ITEMS];
     int c = 0;
 #pragma unroll
@@ -621,7 +629,10 @@ __global__ void __launch_bounds__(CMP_THREADS) k_vert_scatter(const int* __restr
             pos++;
         }
     }
-    if (blockIdx.x == nblocks - 1 && threadIdx.x == 0) st->n_vis_vertices = offset + total;
+    if (vb == nblocks - 1 && threadIdx.x == 0) st->n_vis_vertices = offset + total;
+    offset += total;
+    __syncthreads();  // sm is reused by the next tile's scan
+    }
 }
 
 int fa_vertex_blocks(long long V) {
@@ -632,8 +643,9 @@ int fa_vertex_blocks(long long V) {
 void fa_launch_visible_vertices(const int* vmin, int V, const int* vperm, int* blocks, int* vslot, int* vlist,
                                 fa_dstat* st, cudaStream_t s, float2* vuv, unsigned int* vvis_mask) {
     const int nb = fa_vertex_blocks(V);
-    fa_launch(k_vert_count, nb, CMP_THREADS, 0, s, vmin, V, blocks);
-    fa_launch(k_vert_scatter, nb, CMP_THREADS, 0, s, vmin, V, blocks, nb, vperm, vslot, vlist, vuv, st, vvis_mask);
+    fa_launch(k_vert_count, fa_wave_grid(k_vert_count, CMP_THREADS, 0, nb, nb), CMP_THREADS, 0, s, vmin, V, blocks);
+    fa_launch(k_vert_scatter, fa_wave_grid(k_vert_scatter, CMP_THREADS, 0, nb, nb), CMP_THREADS, 0, s, vmin, V, blocks,
+              nb, vperm, vslot, vlist, vuv, st, vvis_mask);
 }
 
 void fa_launch_v2c(const int* vmin, const int* label, int* v2c, int V, cudaStream_t s, const int* vperm) {

@@ -974,6 +974,14 @@ static void fork_to(cudaStream_t s, cudaStream_t side, cudaEvent_t ev) {
 // tiles on side} || {clipped polygons -> their tiles on side2}, joined back
 // into s.  Every branch only lowers depth keys with atomicMin, so their order
 // does not matter.
+#ifndef CLIPPED_WAVE
+#define CLIPPED_WAVE 0
+#endif
+#if CLIPPED_WAVE
+#define CLIPPED_GRID(k) fa_wave_grid(k, 256, 0, FA_NUM_SMS * 8, FA_NUM_SMS * 8)
+#else
+#define CLIPPED_GRID(k) fa_cap(FA_NUM_SMS * 2)
+#endif
 #ifndef TILES_WAVE
 #define TILES_WAVE 1
 #endif
@@ -1004,7 +1012,7 @@ int fa_launch_depth_pass(bool write_depth, const ClipSrc clip, const double4* sc
         //   side2: clipped polygons -> their tiles
         fa_launch(k_raster_depth_tiles, TILES_GRID(FA_NUM_SMS * 8), 256, 0, b, small_rec, large, tiles, W, depth, wid, st,
                   max_tiles, 0, 1, 0);
-        fa_launch(k_raster_clipped<true>, fa_cap(FA_NUM_SMS * 2), 256, 0, b2, clip, tris, W, H, cull, clip_list, depth, wid,
+        fa_launch(k_raster_clipped<true>, CLIPPED_GRID(k_raster_clipped<true>), 256, 0, b2, clip, tris, W, H, cull, clip_list, depth, wid,
                   large, max_large, tiles, max_tiles, st);
         fa_launch(k_raster_depth_tiles, TILES_GRID(FA_NUM_SMS * 4), 256, 0, b2, small_rec, large, tiles, W, depth, wid, st,
                   max_tiles, 0, 1, 1);
