@@ -157,7 +157,7 @@ __global__ void k_encode_depth(const double* __restrict__ in, unsigned long long
 #ifndef SETUP_WARPS
 #define SETUP_WARPS 8
 #endif
-__global__ void __launch_bounds__(SETUP_WARPS * 32) k_raster_setup(const double4* __restrict__ scr,
+__global__ void __launch_bounds__(SETUP_WARPS * 32, 32 / SETUP_WARPS) k_raster_setup(const double4* __restrict__ scr,
                                                       const int* __restrict__ tris,
                                                       int T, int W, int H, int cull,
                                                       SmallRec* __restrict__ recs, int* __restrict__ clip_list,

@@ -470,6 +470,43 @@ __device__ __forceinline__ double2 vertex_ndc(double4 c) {
 
 // 1 = Setup3 filled, 0 = no samples, 2 = needs the generic (clipping) path.
 // Same decisions as tri_setup3 below, from the per-vertex screen records.
+// ---- provably empty windows (no record for triangles that cover no sample) -
+// About a quarter of the C2 small triangles cover no sample centre.  A sample
+// the reference accepts (all three rounded edge values >= 0) lies within
+// d < 1e-11 px of the triangle its rounded vertices and edge vectors define
+// (the edge values' rounding over windows of a few hundred pixels); the
+// vertices of that inflated triangle move by at most 2d / sin(min angle), and
+// sin(min angle) >= area2 / Lmax^2.  So when area2 >= 1e-5 Lmax^2, every
+// accepted sample centre is within 2e-6 px -- inside the margin m = 1e-4 -- of
+// the vertices' bounding box:
+//  * no centre within the box (+ m) in x or in y -> no sample;
+//  * at most 4 centres there -> each is tested with the reference's own edge
+//    arithmetic (sample_inside3); none inside -> no sample.
+// Otherwise (slivers, NaN) the triangle keeps its record.
+#ifndef FA_EMPTY_CULL
+#define FA_EMPTY_CULL 1
+#endif
+#ifndef FA_EMPTY_MAXC
+#define FA_EMPTY_MAXC 4  // candidate centres tested exactly (more: keep the record)
+#endif
+__device__ __forceinline__ bool sample_inside3(const Setup3& s, double px, double py);
+__device__ __forceinline__ bool empty_window(const Setup3& s, double mnx, double mxx, double mny, double mxy,
+                                             double area2) {
+    const double l0 = s.dx0 * s.dx0 + s.dy0 * s.dy0, l1 = s.dx1 * s.dx1 + s.dy1 * s.dy1,
+                 l2 = s.dx2 * s.dx2 + s.dy2 * s.dy2;
+    const double lmax = fmax(l0, fmax(l1, l2));
+    if (!(fabs(area2) >= 1e-5 * lmax)) return false;  // sliver (or NaN): keep
+    const double m = 1e-4;
+    const int xl = max(s.min_x, (int)ceil(mnx - m - 0.5)), xh = min(s.max_x, (int)floor(mxx + m - 0.5));
+    const int yl = max(s.min_y, (int)ceil(mny - m - 0.5)), yh = min(s.max_y, (int)floor(mxy + m - 0.5));
+    if (xl > xh || yl > yh) return true;
+    if ((xh - xl + 1) * (yh - yl + 1) > FA_EMPTY_MAXC) return false;
+    for (int iy = yl; iy <= yh; iy++)
+        for (int ix = xl; ix <= xh; ix++)
+            if (sample_inside3(s, (double)ix + 0.5, (double)iy + 0.5)) return false;
+    return true;
+}
+
 __device__ __forceinline__ int tri_setup3s(const double4* __restrict__ scr, int ia, int ib, int ic, int W, int H,
                                            bool cull, Setup3& s) {
     double4 v0 = ldg4(scr + ia), v1 = ldg4(scr + ib), v2 = ldg4(scr + ic);
@@ -519,6 +556,9 @@ __device__ __forceinline__ int tri_setup3s(const double4* __restrict__ scr, int 
     s.ax2 = x2; s.ay2 = y2; s.dx2 = __dsub_rn(x0, x2); s.dy2 = __dsub_rn(y0, y2);
     s.incl = ((s.dy0 > 0 || (s.dy0 == 0 && s.dx0 < 0)) ? 1 : 0) | ((s.dy1 > 0 || (s.dy1 == 0 && s.dx1 < 0)) ? 2 : 0) |
              ((s.dy2 > 0 || (s.dy2 == 0 && s.dx2 < 0)) ? 4 : 0);
+#if FA_EMPTY_CULL
+    if (empty_window(s, mnx, mxx, mny, mxy, area2)) return 0;
+#endif
     double a1x = s.dx0, a1y = s.dy0, a1z = __dsub_rn(z1, z0);
     double a2x = __dsub_rn(x2, x0), a2y = __dsub_rn(y2, y0), a2z = __dsub_rn(z2, z0);
     double det = __dsub_rn(__dmul_rn(a1x, a2y), __dmul_rn(a2x, a1y));
