@@ -26,6 +26,18 @@
 #define TILE_W 16
 #define TILE_H 8
 
+#ifdef FA_COOP_STATS
+// debug builds only (tools/debug_coopstats.py): small records by window size
+// (<=4, <=9, <=16, <=48, more) x (no / some covered sample)
+__device__ unsigned long long g_coop_stats[5][2];
+extern "C" void fa_debug_coop_stats(unsigned long long* out, int reset) {
+    cudaMemcpyFromSymbol(out, g_coop_stats, sizeof(g_coop_stats));
+    if (reset) {
+        unsigned long long z[10] = {};
+        cudaMemcpyToSymbol(g_coop_stats, z, sizeof(z));
+    }
+}
+#endif
 #ifdef FA_HIZ_STATS
 // debug build only: [small records rejected by the hierarchical Z, small
 // records sampled, tiles tested, tiles rejected, tiles skipped (visible)]
@@ -560,6 +572,11 @@ __global__ void __launch_bounds__(COOP_WARPS * 32, COOP_MIN_BLOCKS) k_small_coop
     const int warp = threadIdx.x >> 5, lane = lane_id();
     CoopWarp& cw = sh[warp];
     const int n = st->n_small3;
+#ifdef FA_COOP_STATS
+    __shared__ int cw_cov[COOP_WARPS][32];
+    cw_cov[warp][lane] = 0;
+    __syncwarp();
+#endif
     const int stride = gridDim.x * COOP_WARPS * 32;
     int base = ((int)blockIdx.x * COOP_WARPS + warp) * 32;
     int buf = 0;
@@ -630,12 +647,26 @@ __global__ void __launch_bounds__(COOP_WARPS * 32, COOP_MIN_BLOCKS) k_small_coop
                 for (int ix = xa; ix <= xb; ix++, px += 1.0) {
                     // the edge test only near a crossing (row_span_cert)
                     const double z = depth_row(f, rt, px);
-                    if ((ix >= ca && ix <= cb) || inside_row(f, rt, px))
+                    if ((ix >= ca && ix <= cb) || inside_row(f, rt, px)) {
                         depth_min(depth, wid, rowoff + ix, f64_key(z), t, false);
+#ifdef FA_COOP_STATS
+                        cw_cov[warp][r] = 1;
+#endif
+                    }
                 }
             }
         }
         __syncwarp();
+#ifdef FA_COOP_STATS
+        if (lane < cnt) {
+            const SmallRec& q = rb[lane];
+            const int area = (q.max_x - q.min_x + 1) * (q.max_y - q.min_y + 1);
+            const int bucket = area <= 4 ? 0 : area <= 9 ? 1 : area <= 16 ? 2 : area <= 48 ? 3 : 4;
+            atomicAdd(&g_coop_stats[bucket][cw_cov[warp][lane]], 1ull);
+            cw_cov[warp][lane] = 0;
+        }
+        __syncwarp();
+#endif
     }
 }
 
