@@ -178,7 +178,7 @@ int fa_set_mesh(fa_ctx* ctx, const double* positions, int64_t n_vertices, const 
         const size_t vb = (size_t)(n_vertices > 0 ? n_vertices : 1) * 4;
         bool ok = fa_ensure(ctx, first, vb) &&
                   fa_ensure(ctx, scratch, (size_t)fa_mesh_scratch_ints(n_vertices, T) * 4 + vb + 16) &&
-                  fa_ensure(ctx, ctx->clusters_buf, (size_t)((T + 31) / 32) * sizeof(fa_cluster)) &&
+                  fa_ensure(ctx, ctx->clusters_buf, (size_t)((T + FA_CLUSTER - 1) / FA_CLUSTER) * sizeof(fa_cluster)) &&
                   fa_ensure(ctx, ctx->tris_sorted_buf, (size_t)T * 12) && fa_ensure(ctx, ctx->tperm_buf, (size_t)T * 4);
         if (ok && order) ok = fa_ensure(ctx, sort_scratch, fa_mesh_sort_scratch_bytes(T)) && fa_ensure(ctx, tris_s, (size_t)T * 12);
         if (ok && renumber) {
@@ -287,7 +287,7 @@ static int ensure_raster(fa_ctx* ctx, int W, int H, bool depth) {
     ENSURE(tiles, (size_t)ctx->max_tiles * sizeof(int4));
     ENSURE(dstat, sizeof(fa_dstat));
     ENSURE(vp_dev, 16 * sizeof(double));
-    ENSURE(live_buf, (size_t)((T + 31) / 32 + 1) * 4);
+    ENSURE(live_buf, (size_t)((T + FA_CLUSTER - 1) / FA_CLUSTER + 1) * 4);
     return FA_OK;
 }
 
@@ -427,7 +427,7 @@ static fa_cull_args cull_args(fa_ctx* ctx, int cull) {
     fa_cull_args c{};
     if (ctx->clusters && ctx->live_buf.p && fa_env_int("FASTATLAS_CLUSTER_CULL", 1)) {
         c.clusters = ctx->clusters;
-        c.n_clusters = (int)((ctx->T + 31) / 32);
+        c.n_clusters = (int)((ctx->T + FA_CLUSTER - 1) / FA_CLUSTER);
         c.cull = cull;
         c.live = P<int>(ctx->live_buf);
         c.st = P<fa_dstat>(ctx->dstat);

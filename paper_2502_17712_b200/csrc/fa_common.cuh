@@ -23,6 +23,10 @@
 #define FA_HIZ 8                // hierarchical-Z tile edge (pixels)
 
 // device status bits (fa_ctx::dstat->flags)
+// triangles per culling cluster (consecutive in the setup order; 32 or 16)
+#ifndef FA_CLUSTER
+#define FA_CLUSTER 32
+#endif
 #define FA_DFLAG_POLY_OVERFLOW 1u
 #define FA_DFLAG_HEIGHT_OVERFLOW 2u
 #define FA_DFLAG_DEGENERATE_CHART 4u

@@ -351,10 +351,14 @@ __global__ void k_cluster_build(const double* __restrict__ pos, const int* __res
                                 fa_cluster* __restrict__ out) {
     FA_PDL_PROLOGUE();
     const int lane = lane_id();
-    const int nc = (T + 31) / 32;
-    for (int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < nc; c += (gridDim.x * blockDim.x) >> 5) {
-        const int i = c * 32 + lane;
-        const bool act = i < T;
+    // one warp per 32 / FA_CLUSTER clusters; reductions stay within a cluster's lanes
+    constexpr int CS = FA_CLUSTER;
+    const int nc = (T + CS - 1) / CS;
+    const int nw = (nc + 32 / CS - 1) / (32 / CS);
+    for (int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < nw; wi += (gridDim.x * blockDim.x) >> 5) {
+        const int c = wi * (32 / CS) + lane / CS;
+        const int i = c * CS + (lane % CS);
+        const bool act = c < nc && i < T;
         double p[3][3];
 #pragma unroll
         for (int k = 0; k < 3; k++)
@@ -365,7 +369,7 @@ __global__ void k_cluster_build(const double* __restrict__ pos, const int* __res
         for (int d = 0; d < 3; d++) {
             lo[d] = act ? fmin(fmin(p[0][d], p[1][d]), p[2][d]) : INFINITY;
             hi[d] = act ? fmax(fmax(p[0][d], p[1][d]), p[2][d]) : -INFINITY;
-            for (int o = 16; o > 0; o >>= 1) {
+            for (int o = CS / 2; o > 0; o >>= 1) {
                 lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
                 hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
             }
@@ -386,22 +390,24 @@ __global__ void k_cluster_build(const double* __restrict__ pos, const int* __res
         const bool good = !act || (nl > 0 && isfinite(nl));
         double ax = good && act ? nx / nl : 0.0, ay = good && act ? ny / nl : 0.0, az = good && act ? nz / nl : 0.0;
         const double mx = ax, my = ay, mz = az;
-        for (int o = 16; o > 0; o >>= 1) {
+        for (int o = CS / 2; o > 0; o >>= 1) {
             r2 = fmax(r2, __shfl_xor_sync(0xffffffffu, r2, o));
             area = fmin(area, __shfl_xor_sync(0xffffffffu, area, o));
             ax += __shfl_xor_sync(0xffffffffu, ax, o);
             ay += __shfl_xor_sync(0xffffffffu, ay, o);
             az += __shfl_xor_sync(0xffffffffu, az, o);
         }
-        const bool all_good = __all_sync(0xffffffffu, good);
+        const unsigned seg = (CS == 32 ? 0xffffffffu : ((1u << CS) - 1u)) << (lane & ~(CS - 1) & 31);
+        const bool all_good = (__ballot_sync(0xffffffffu, good) & seg) == seg;
         const double al = sqrt(ax * ax + ay * ay + az * az);
         double cmin = 1.0;
         if (al > 0) {
             ax /= al; ay /= al; az /= al;
             cmin = act ? mx * ax + my * ay + mz * az : 1.0;
-            for (int o = 16; o > 0; o >>= 1) cmin = fmin(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
         }
-        if (lane == 0) {
+        // (unconditional: `al` differs between the warp's clusters)
+        for (int o = CS / 2; o > 0; o >>= 1) cmin = fmin(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
+        if ((lane % CS) == 0 && c < nc) {
             fa_cluster q;
             q.c[0] = cx; q.c[1] = cy; q.c[2] = cz;
             q.r = sqrt(r2) * (1.0 + 1e-12) + 1e-300;

@@ -192,11 +192,16 @@ __global__ void __launch_bounds__(SETUP_WARPS * 32, 32 / SETUP_WARPS) k_raster_s
     // consecutive slots.  t is the slot's triangle id.
     const int* ts = ord.tris_sorted ? ord.tris_sorted : tris;
     const int* live = ord.live;
-    const int n_items = live ? *ord.n_live : (T + 31) >> 5;  // warp items (32 slots each)
+    // warp items of 32 slots: 32 / FA_CLUSTER live clusters, or 32 consecutive slots
+    constexpr int CPW = 32 / FA_CLUSTER;
+    const int n_items = live ? (*ord.n_live + CPW - 1) / CPW : (T + 31) >> 5;
+    const int n_live_c = live ? *ord.n_live : 0;
     const int istep = gridDim.x * SETUP_WARPS;
     auto slot_of = [&](int item) -> int {
         if (item >= n_items) return T;
-        return (live ? __ldg(live + item) : item) * 32 + lane;
+        if (!live) return item * 32 + lane;
+        const int ci = item * CPW + lane / FA_CLUSTER;
+        return ci < n_live_c ? __ldg(live + ci) * FA_CLUSTER + (lane % FA_CLUSTER) : T;
     };
     int nslot = slot_of(blockIdx.x * SETUP_WARPS + warp);
     int na = 0, nb = 0, nc = 0, nt_id = T;
