@@ -131,6 +131,7 @@ void fa_destroy(fa_ctx* c) {
     for (fa_buf* b : bufs) free_buf(*b);
     for (cudaEvent_t e : c->fj)
         if (e) cudaEventDestroy(e);
+    if (c->copy_done) cudaEventDestroy(c->copy_done);
     for (cudaEvent_t e : c->ev)
         if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : c->vp_ev)
@@ -464,6 +465,7 @@ static int ensure_side(fa_ctx* ctx) {
     if (!ctx->side2) CK(cudaStreamCreateWithFlags(&ctx->side2, cudaStreamNonBlocking));
     for (cudaEvent_t& e : ctx->fj)
         if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    if (!ctx->copy_done) CK(cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming));
     return FA_OK;
 }
 
@@ -1077,6 +1079,16 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
                                P<unsigned long long>(ctx->hiz), flags, P<int>(ctx->clip_list), st, s, ctx->side,
                                ctx->fj[2], ctx->fj[3]);
     mark();  // 3: visibility pass
+    // the previous frame's downloads must be done before this frame rewrites
+    // the downloaded buffers (the compaction is the first writer; in a graph
+    // an external event-wait node)
+    {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        CK(cudaStreamIsCapturing(s, &cs));
+        static const bool no_wait = fa_env_int("FASTATLAS_DEBUG_NO_COPY_WAIT", 0) != 0;  // (tests only)
+        if (!no_wait)
+            CK(cudaStreamWaitEvent(s, ctx->copy_done, cs == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0));
+    }
     // the compaction also lowers vmin (frame_init filled it with INT_MAX)
     fa_launch_compact_visible(flags, T, P<int>(ctx->blocks), P<int>(ctx->vis_list), P<int>(ctx->label), st, s,
                               ctx->tris, P<int>(ctx->vmin), P<int4>(ctx->vis_tris), P<unsigned int>(ctx->vis_mask));
@@ -1347,6 +1359,7 @@ int fa_frame_download(fa_ctx* ctx, const fa_frame_result* res, int32_t* chart_of
     if (visible && nv) CK(cudaMemcpyAsync(visible, res->visible, nv * 4, cudaMemcpyDefault, s));
     if (uv && nv) CK(cudaMemcpyAsync(uv, res->uv, nv * 6 * uv_elem, cudaMemcpyDefault, s));
     if (placements && C) CK(cudaMemcpyAsync(placements, res->placements, C * 64, cudaMemcpyDefault, s));
+    if (ctx->copy_done) CK(cudaEventRecord(ctx->copy_done, s));
     return FA_OK;
 }
 
@@ -1363,7 +1376,19 @@ int fa_frame_download_compact(fa_ctx* ctx, const fa_frame_result* res, int32_t* 
         CK(cudaMemcpyAsync(visible_vertices, res->visible_vertices, nvv * 4, cudaMemcpyDefault, s));
     if (vertex_uv && nvv) CK(cudaMemcpyAsync(vertex_uv, res->vertex_uv, nvv * 8, cudaMemcpyDefault, s));
     if (placements && C) CK(cudaMemcpyAsync(placements, res->placements, C * 64, cudaMemcpyDefault, s));
+    if (ctx->copy_done) CK(cudaEventRecord(ctx->copy_done, s));
     return FA_OK;
+}
+
+// debug knob (tests/test_pipeline.py): FASTATLAS_DEBUG_COPY_DELAY=us spins on
+// the download stream before the copies, so a missing copy_done wait in the
+// next frame would let it overwrite the buffers first
+__global__ void k_debug_spin(long long ns) {
+    long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < ns);
 }
 
 int fa_frame_download_packed(fa_ctx* ctx, const fa_frame_result* res, uint32_t* visible_mask,
@@ -1375,6 +1400,8 @@ int fa_frame_download_packed(fa_ctx* ctx, const fa_frame_result* res, uint32_t* 
     if (res->n_charts > 65535) return set_err(FA_VALUE_ERROR, "more than 65535 charts: use fa_frame_download_compact");
     if (!ctx->vis_mask.p || !ctx->cidx16.p) return set_err(FA_VALUE_ERROR, "no frame outputs");
     CK(cudaSetDevice(ctx->device));
+    static const int dbg_delay = fa_env_int("FASTATLAS_DEBUG_COPY_DELAY", 0);
+    if (dbg_delay > 0) k_debug_spin<<<1, 1, 0, s>>>((long long)dbg_delay * 1000);
     size_t nv = (size_t)res->n_visible, C = (size_t)res->n_charts, nvv = (size_t)res->n_visible_vertices;
     if (visible_mask && ctx->T)
         CK(cudaMemcpyAsync(visible_mask, ctx->vis_mask.p, (size_t)((ctx->T + 31) / 32) * 4, cudaMemcpyDefault, s));
@@ -1384,6 +1411,7 @@ int fa_frame_download_packed(fa_ctx* ctx, const fa_frame_result* res, uint32_t* 
         CK(cudaMemcpyAsync(vertex_mask, ctx->vvis_mask.p, (size_t)((ctx->V + 31) / 32) * 4, cudaMemcpyDefault, s));
     if (vertex_uv && nvv) CK(cudaMemcpyAsync(vertex_uv, res->vertex_uv, nvv * 8, cudaMemcpyDefault, s));
     if (placements && C) CK(cudaMemcpyAsync(placements, res->placements, C * 64, cudaMemcpyDefault, s));
+    if (ctx->copy_done) CK(cudaEventRecord(ctx->copy_done, s));
     return FA_OK;
 }
 
@@ -1413,6 +1441,7 @@ int fa_frame_download_visible(fa_ctx* ctx, const fa_frame_result* res, int32_t* 
         CK(cudaMemcpyAsync(visible_chart, res->visible_chart, nv * 4, cudaMemcpyDefault, s));
     if (uv && nv) CK(cudaMemcpyAsync(uv, res->uv, nv * 6 * uv_elem, cudaMemcpyDefault, s));
     if (placements && C) CK(cudaMemcpyAsync(placements, res->placements, C * 64, cudaMemcpyDefault, s));
+    if (ctx->copy_done) CK(cudaEventRecord(ctx->copy_done, s));
     return FA_OK;
 }
 

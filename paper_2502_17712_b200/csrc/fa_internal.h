@@ -136,6 +136,10 @@ struct fa_ctx {
     // side stream + fork/join events for the independent raster branches
     cudaStream_t side = nullptr, side2 = nullptr;
     cudaEvent_t fj[12] = {};
+    // recorded after a frame's downloads (fa_frame_download*): the next frame
+    // waits on it before its first write to a downloaded buffer, so the copies
+    // may run on another stream, overlapping the next frame's start
+    cudaEvent_t copy_done = nullptr;
 };
 
 // growth helper: ensures buf has >= bytes; returns false on allocation failure

@@ -342,6 +342,7 @@ class FramePipeline:
         self.engines = [FrameEngine(mesh, device, self.settings, private_mesh=mesh_replicas) for _ in range(depth)]
         self.device = self.engines[0].device
         self.streams = [torch.cuda.Stream(device=self.device) for _ in range(depth)]
+        self._cstreams = [torch.cuda.Stream(device=self.device) for _ in range(depth)]  # D2H copies
         self.outputs = tuple(outputs)
         T = mesh.n_triangles
         uv_dt = torch.float64 if self.settings.uv_f64 else torch.float32
@@ -389,6 +390,11 @@ class FramePipeline:
         eng, st = self.engines[slot], self.streams[slot]
         L, h_ctx, res = eng.ctx.L, eng.ctx.h, eng._res
         sp = ctypes.c_void_p(st.cuda_stream)
+        # the copies go on the slot's copy stream: the frame is complete here
+        # (fa_frame_finish synchronised it), and the slot's next frame waits
+        # on the device for them only before it rewrites the downloaded
+        # buffers (the context's copy_done event), so the two overlap
+        spc = ctypes.c_void_p(self._cstreams[slot].cuda_stream)
         hf = HostFrame(index, self.engines[slot].n_triangles, self._tris, self._V)
         for _ in range(4):
             code = L.fa_frame_finish(h_ctx, ctypes.byref(res), sp)
@@ -417,12 +423,12 @@ class FramePipeline:
         if "p_vis_mask" in h and C <= 65535:
             if self._vorder[slot] is None:
                 vo = np.empty(self._V, dtype=np.int32)
-                nat.raise_for_status(L.fa_vertex_order(h_ctx, ctypes.c_void_p(vo.ctypes.data), sp))
+                nat.raise_for_status(L.fa_vertex_order(h_ctx, ctypes.c_void_p(vo.ctypes.data), spc))
                 self._vorder[slot] = vo
             pp = {k: ctypes.c_void_p(h[k].data_ptr()) for k in ("p_vis_mask", "p_cidx", "p_roots", "p_vtx_mask")}
             nat.raise_for_status(L.fa_frame_download_packed(h_ctx, ctypes.byref(res), pp["p_vis_mask"], pp["p_cidx"],
                                                             pp["p_roots"], pp["p_vtx_mask"], ptr["vertex_uv"],
-                                                            ptr["placements"], sp))
+                                                            ptr["placements"], spc))
             n = self._np[slot]
             nvv = int(res.n_visible_vertices)
             hf._packed = (n["p_vis_mask"][:(self._tris.shape[0] + 31) // 32], n["p_cidx"][:nv], n["p_roots"][:C],
@@ -434,17 +440,17 @@ class FramePipeline:
         if ptr["vertex_uv"] is not None:
             nat.raise_for_status(L.fa_frame_download_compact(h_ctx, ctypes.byref(res), ptr["visible"],
                                                              ptr["visible_chart"], ptr["visible_vertices"],
-                                                             ptr["vertex_uv"], ptr["placements"], sp))
+                                                             ptr["vertex_uv"], ptr["placements"], spc))
             if ptr["chart_of_triangle"] is not None:
                 nat.raise_for_status(L.fa_frame_download(h_ctx, ctypes.byref(res), ptr["chart_of_triangle"],
-                                                         None, None, None, sp))
+                                                         None, None, None, spc))
         elif ptr["chart_of_triangle"] is not None:
             nat.raise_for_status(L.fa_frame_download(h_ctx, ctypes.byref(res), ptr["chart_of_triangle"],
-                                                     ptr["visible"], ptr["uv"], ptr["placements"], sp))
+                                                     ptr["visible"], ptr["uv"], ptr["placements"], spc))
         elif any(p is not None for p in ptr.values()):
             nat.raise_for_status(L.fa_frame_download_visible(h_ctx, ctypes.byref(res), ptr["visible"],
                                                              ptr["visible_chart"], ptr["uv"], ptr["placements"],
-                                                             sp))
+                                                             spc))
         if "chart_of_triangle" in h:
             hf._cot = self._np[slot]["chart_of_triangle"]
         if "visible_chart" in h:
@@ -488,7 +494,7 @@ class FramePipeline:
                 idx, v = inflight[slot]
                 copied[slot] = self._finish(slot, idx, v)
                 ev = torch.cuda.Event()
-                ev.record(self.streams[slot])
+                ev.record(self._cstreams[slot])
                 done_ev[slot] = ev
                 inflight[slot] = None
 

@@ -130,3 +130,27 @@ def test_compact_uv_rows_match_engine_rows():
     for g in got:
         assert g.dtype == np.float32 and g.shape == want.shape
         assert np.array_equal(g.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("no_wait", [False, True])
+def test_copies_overlap_next_frame_safely(no_wait):
+    """The slot's downloads run on a copy stream beside its next frame; the
+    frame waits (device side, the context's copy_done event) before it
+    rewrites the downloaded buffers.  With the copies delayed 2 ms, results
+    stay exact -- and without the wait (debug knob) they would not, which
+    shows the test exercises the race."""
+    import subprocess
+    import sys
+    env = dict(__import__("os").environ, FASTATLAS_DEBUG_COPY_DELAY="2000")
+    if no_wait:
+        env["FASTATLAS_DEBUG_NO_COPY_WAIT"] = "1"
+    code = (
+        "import sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+        "import numpy as np, test_pipeline as tp;"
+        "tp.test_pipeline_matches_sequential(2, None, True)"
+    )
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    if no_wait:
+        assert r.returncode != 0, "the unprotected overlap was expected to corrupt a delayed download"
+    else:
+        assert r.returncode == 0, r.stderr[-2000:]
