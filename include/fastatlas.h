@@ -235,7 +235,11 @@ int fa_frame(fa_ctx *ctx, const double *vp_host, const fa_frame_params *params, 
  * chart_of_triangle T int32, visible n_visible int32, uv n_visible x 6
  * (float32, or float64 when the frame ran with uv_f64), placements n_charts
  * x 8 int64.  The caller synchronises `stream` before reading.  Replaces the
- * per-array `.cpu()` reads of SceneResult (reference cli.py:404-406). */
+ * per-array `.cpu()` reads of SceneResult (reference cli.py:404-406).
+ * Every fa_frame_download* call records a context event after its copies, and
+ * the context's next frame waits for it on the device before it rewrites any
+ * downloaded buffer -- so the copies may run on another stream, overlapping
+ * the start of the next frame (FramePipeline does this). */
 int fa_frame_download(fa_ctx *ctx, const fa_frame_result *res, int32_t *chart_of_triangle, int32_t *visible,
                       void *uv, int64_t *placements, void *stream);
 
