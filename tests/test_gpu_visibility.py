@@ -181,3 +181,42 @@ def test_edges_through_sample_centres(seed):
     pos, tris = _screen_tris(None, pts, depths)
     r = _check(pos, tris, _camera().view_proj)
     assert r.flags.sum() > 100
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_subpixel_triangles(seed):
+    """Sub-pixel triangles, most covering no sample centre: the setup drops
+    provably empty windows (no centre within the vertex box + 1e-4 px, or <= 4
+    centres failing the edge test, slivers excepted -- fa_raster.cuh
+    empty_window).  Boxes end at centres + {0, +-1e-12, +-1e-6, +-1e-4 +- 1e-8}
+    and include near-degenerate slivers, so every branch of the test meets
+    the reference's own edge arithmetic at its boundary."""
+    rng = np.random.default_rng(300 + seed)
+    offs = np.array([0.0, 1e-12, -1e-12, 1e-6, -1e-6, 1e-4, -1e-4, 1e-4 + 1e-8, -1e-4 - 1e-8, 1e-4 - 1e-8])
+    pts, depths = [], []
+    W, H = SCREEN
+    for _ in range(4000):
+        cx, cy = rng.integers(4, W - 8), rng.integers(4, H - 8)
+        kind = rng.integers(0, 3)
+        if kind == 0:    # tiny triangle anywhere in a pixel
+            base = rng.uniform(0.0, 1.0, size=2)
+            c = base + rng.uniform(-0.6, 0.6, size=(3, 2))
+        elif kind == 1:  # a corner on a centre +- offsets, the others within a pixel
+            c = np.array([[0.5, 0.5], [0.5, 0.5], [0.5, 0.5]]) + rng.uniform(-0.9, 0.9, size=(3, 2))
+            c[0] = 0.5 + rng.choice(offs, size=2)
+        else:            # near-degenerate sliver through / beside a centre
+            a = np.array([0.5, 0.5]) + rng.choice(offs, size=2)
+            d = rng.uniform(-1, 1, size=2)
+            d /= np.linalg.norm(d)
+            c = np.array([a - 0.8 * d, a + 0.9 * d, a + rng.choice([1e-7, 1e-5, 1e-3]) * np.array([-d[1], d[0]])])
+        c[:, 0] += cx
+        c[:, 1] += cy
+        a2 = (c[1, 0] - c[0, 0]) * (c[2, 1] - c[0, 1]) - (c[2, 0] - c[0, 0]) * (c[1, 1] - c[0, 1])
+        tri = [tuple(p) for p in c]
+        if a2 < 0:
+            tri = [tri[0], tri[2], tri[1]]
+        pts.append(tri)
+        depths.append(rng.uniform(3.0, 9.0))
+    pos, tris = _screen_tris(None, pts, depths)
+    r = _check(pos, tris, _camera().view_proj)
+    assert r.flags.sum() > 50
