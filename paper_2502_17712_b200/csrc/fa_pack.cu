@@ -429,9 +429,10 @@ __device__ __forceinline__ void block_max2_ll(long long& a, long long& b, long l
     b = red2[32];
 }
 
-// boxes per thread kept in registers by the fold rounds (n <= PK_KREG * PK_THREADS)
-#ifndef PK_KREG
-#define PK_KREG 4
+// boxes per thread kept in registers by the fold rounds (n <= KREG * PK_THREADS):
+// pack_candidate<4> and, for larger frames, pack_candidate<PK_KREG_WIDE>
+#ifndef PK_KREG_WIDE
+#define PK_KREG_WIDE 8
 #endif
 
 #ifdef FA_PACK_PROF
@@ -464,7 +465,7 @@ __device__ __forceinline__ void span_fill(int* f, int a, int b, int v) {
 }
 
 // One candidate: returns accept; fills cand_w/h/p/y/rowstart for the CTA.
-template <typename DimT>
+template <int PK_KREG, typename DimT>
 __device__ bool pack_candidate(const DimT* __restrict__ ow, const DimT* __restrict__ oh, int n,
                                long long num, long long den, long long omega, int kbits, long long min_dim,
                                long long pad, int* cw, int* ch, long long* cp, int* cy, int* rowstart, int* front,
@@ -763,9 +764,16 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack(const long long* __restrict
     size_t slot = blockIdx.x;
     int* front = gfront ? gfront + slot * (size_t)(omega + 1) : dyn_front;
     long long rn = 0, rd = 1, used = 0;
-    bool ok = pack_candidate(ow, oh, n, num, den, omega, kbits, min_dim, pad, cand_w + slot * n_max,
-                             cand_h + slot * n_max, cand_p + slot * n_max, cand_y + slot * n_max,
-                             rowstart + slot * n_max, front, rn, rd, used, sm);
+    // boxes per thread in registers: 4 up to 4 * blockDim boxes (the C2
+    // frames), 8 beyond (C3's ~4000 charts), else the global-memory rounds
+    const int K = (n + (int)blockDim.x - 1) / (int)blockDim.x;
+    bool ok = K <= 4 ? pack_candidate<4>(ow, oh, n, num, den, omega, kbits, min_dim, pad, cand_w + slot * n_max,
+                                         cand_h + slot * n_max, cand_p + slot * n_max, cand_y + slot * n_max,
+                                         rowstart + slot * n_max, front, rn, rd, used, sm)
+                     : pack_candidate<PK_KREG_WIDE>(ow, oh, n, num, den, omega, kbits, min_dim, pad,
+                                                    cand_w + slot * n_max, cand_h + slot * n_max,
+                                                    cand_p + slot * n_max, cand_y + slot * n_max,
+                                                    rowstart + slot * n_max, front, rn, rd, used, sm);
     if (threadIdx.x == 0) {
         long long* rec = cand + CAND_REC * (i - 1);
         rec[0] = ok;
