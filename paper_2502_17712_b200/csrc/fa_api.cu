@@ -127,7 +127,7 @@ void fa_destroy(fa_ctx* c) {
                       &c->target, &c->survived, &c->okey, &c->oidx, &c->ow, &c->oh, &c->orot, &c->sortk, &c->sortv,
                       &c->pinv, &c->cand, &c->cand_p, &c->cand_w, &c->cand_h, &c->cand_y, &c->rowstart,
                       &c->placements, &c->uv, &c->vp_dev, &c->blocks, &c->dstat, &c->aux, &c->in_tw, &c->in_th,
-                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list, &c->hiz, &c->wid, &c->vis_chart, &c->vis_cidx, &c->plc_c, &c->pos_perm, &c->tris_perm, &c->vperm_buf, &c->vis_tris, &c->vslot, &c->vlist, &c->vuv, &c->vblocks, &c->pstat, &c->tperm_buf, &c->tris_sorted_buf, &c->clusters_buf, &c->live_buf, &c->mesh_first, &c->mesh_scratch, &c->mesh_sort, &c->mesh_tris_s, &c->ord_tw, &c->ord_th, &c->ord_cid, &c->ndc2, &c->vis_mask, &c->vvis_mask, &c->cidx16};
+                      &c->in_cid, &c->in_mt, &c->scr, &c->clip_list, &c->hiz, &c->wid, &c->vis_chart, &c->vis_cidx, &c->plc_c, &c->pos_perm, &c->tris_perm, &c->vperm_buf, &c->vis_tris, &c->vslot, &c->vlist, &c->vuv, &c->vblocks, &c->pstat, &c->tperm_buf, &c->tris_sorted_buf, &c->clusters_buf, &c->live_buf, &c->mesh_first, &c->mesh_scratch, &c->mesh_sort, &c->mesh_tris_s, &c->ord_tw, &c->ord_th, &c->ord_cid, &c->ndc2, &c->vis_mask, &c->vvis_mask, &c->cidx16, &c->slots4_buf};
     for (fa_buf* b : bufs) free_buf(*b);
     for (cudaEvent_t e : c->fj)
         if (e) cudaEventDestroy(e);
@@ -180,7 +180,8 @@ int fa_set_mesh(fa_ctx* ctx, const double* positions, int64_t n_vertices, const 
         bool ok = fa_ensure(ctx, first, vb) &&
                   fa_ensure(ctx, scratch, (size_t)fa_mesh_scratch_ints(n_vertices, T) * 4 + vb + 16) &&
                   fa_ensure(ctx, ctx->clusters_buf, (size_t)((T + FA_CLUSTER - 1) / FA_CLUSTER) * sizeof(fa_cluster)) &&
-                  fa_ensure(ctx, ctx->tris_sorted_buf, (size_t)T * 12) && fa_ensure(ctx, ctx->tperm_buf, (size_t)T * 4);
+                  fa_ensure(ctx, ctx->tris_sorted_buf, (size_t)T * 12) && fa_ensure(ctx, ctx->tperm_buf, (size_t)T * 4) &&
+                  fa_ensure(ctx, ctx->slots4_buf, (size_t)T * 16);
         if (ok && order) ok = fa_ensure(ctx, sort_scratch, fa_mesh_sort_scratch_bytes(T)) && fa_ensure(ctx, tris_s, (size_t)T * 12);
         if (ok && renumber) {
             ok = fa_ensure(ctx, ctx->tris_perm, (size_t)T * 12) && fa_ensure(ctx, ctx->vperm_buf, vb) &&
@@ -215,6 +216,8 @@ int fa_set_mesh(fa_ctx* ctx, const double* positions, int64_t n_vertices, const 
                 cudaMemcpyAsync(ctx->tris_sorted_buf.p, tri_src, (size_t)T * 12, cudaMemcpyDeviceToDevice, s);
             }
             fa_launch_cluster_build(pos_k, P<int>(ctx->tris_sorted_buf), (int)T, P<fa_cluster>(ctx->clusters_buf), s);
+            fa_launch_make_slots4(P<int>(ctx->tris_sorted_buf), order ? P<int>(ctx->tperm_buf) : nullptr, (int)T,
+                                  P<int4>(ctx->slots4_buf), s);
             e = cudaGetLastError();
             if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         }
@@ -416,6 +419,7 @@ static fa_setup_order setup_order(fa_ctx* ctx) {
     fa_setup_order o{};
     o.tperm = ctx->tperm;
     o.tris_sorted = ctx->tris_sorted;
+    o.slots4 = ctx->tris_sorted && ctx->slots4_buf.p ? P<int4>(ctx->slots4_buf) : nullptr;
     if (ctx->clusters && ctx->live_buf.p && fa_env_int("FASTATLAS_CLUSTER_CULL", 1)) {
         o.live = P<int>(ctx->live_buf);
         o.n_live = &P<fa_dstat>(ctx->dstat)->n_live;

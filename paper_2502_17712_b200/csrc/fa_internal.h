@@ -22,6 +22,7 @@ struct fa_cluster {
 struct fa_setup_order {
     const int* tperm;
     const int* tris_sorted;
+    const int4* slots4;  // (a, b, c, triangle id) per setup slot: one 16-byte load (or null)
     const int* live;    // live clusters (k_frame_init), or null: every slot
     const int* n_live;
 };
@@ -86,7 +87,7 @@ struct fa_ctx {
     const int* tperm = nullptr;
     const int* tris_sorted = nullptr;
     const fa_cluster* clusters = nullptr;
-    fa_buf tperm_buf, tris_sorted_buf, clusters_buf, live_buf;
+    fa_buf tperm_buf, tris_sorted_buf, clusters_buf, live_buf, slots4_buf;
     fa_buf mesh_first, mesh_scratch, mesh_sort, mesh_tris_s;  // fa_set_mesh scratch
     fa_buf ord_tw, ord_th, ord_cid;  // per packing position (k_order_frame -> k_select)
     fa_buf ndc2;                     // per-vertex NDC of the inside vertices (vertex_ndc), for bounds and UVs
@@ -223,6 +224,7 @@ size_t fa_mesh_sort_scratch_bytes(long long T);
 void fa_launch_mesh_order(const double* pos, const int* tris, int T, int V, void* scratch, int* order,
                           int* tris_sorted, cudaStream_t s);
 void fa_launch_mesh_remap(const int* tris, long long T, const int* newidx, int* out, cudaStream_t s);
+void fa_launch_make_slots4(const int* tris_sorted, const int* tperm, int T, int4* out, cudaStream_t s);
 void fa_launch_cluster_build(const double* pos, const int* tris_sorted, int T, fa_cluster* out, cudaStream_t s);
 
 // ---- bounds (fa_bounds.cu) -----------------------------------------------

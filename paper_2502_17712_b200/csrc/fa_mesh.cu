@@ -422,6 +422,18 @@ __global__ void k_cluster_build(const double* __restrict__ pos, const int* __res
     }
 }
 
+// the setup's per-slot record: vertex indices and triangle id in one int4
+__global__ void k_make_slots4(const int* __restrict__ tris_sorted, const int* __restrict__ tperm, int T,
+                              int4* __restrict__ out) {
+    FA_PDL_PROLOGUE();
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < T; i += gridDim.x * blockDim.x)
+        out[i] = make_int4(tris_sorted[3 * i], tris_sorted[3 * i + 1], tris_sorted[3 * i + 2], tperm ? tperm[i] : i);
+}
+
+void fa_launch_make_slots4(const int* tris_sorted, const int* tperm, int T, int4* out, cudaStream_t s) {
+    fa_launch(k_make_slots4, fa_grid(T, 256, FA_NUM_SMS * 8), 256, 0, s, tris_sorted, tperm, T, out);
+}
+
 void fa_launch_cluster_build(const double* pos, const int* tris_sorted, int T, fa_cluster* out, cudaStream_t s) {
     fa_launch(k_cluster_build, fa_grid((long long)((T + 31) / 32) * 32, 256, FA_NUM_SMS * 8), 256, 0, s, pos,
               tris_sorted, T, out);

@@ -203,20 +203,24 @@ __global__ void __launch_bounds__(SETUP_WARPS * 32, 32 / SETUP_WARPS) k_raster_s
         const int ci = item * CPW + lane / FA_CLUSTER;
         return ci < n_live_c ? __ldg(live + ci) * FA_CLUSTER + (lane % FA_CLUSTER) : T;
     };
+    const int4* __restrict__ s4 = ord.slots4;
+    auto load_slot = [&](int sl, int& a, int& b, int& c, int& id) {
+        if (s4) {
+            const int4 q = __ldg(s4 + sl);
+            a = q.x, b = q.y, c = q.z, id = q.w;
+        } else {
+            a = __ldg(ts + 3 * sl), b = __ldg(ts + 3 * sl + 1), c = __ldg(ts + 3 * sl + 2);
+            id = ord.tperm ? __ldg(ord.tperm + sl) : sl;
+        }
+    };
     int nslot = slot_of(blockIdx.x * SETUP_WARPS + warp);
     int na = 0, nb = 0, nc = 0, nt_id = T;
-    if (nslot < T) {
-        na = __ldg(ts + 3 * nslot), nb = __ldg(ts + 3 * nslot + 1), nc = __ldg(ts + 3 * nslot + 2);
-        nt_id = ord.tperm ? __ldg(ord.tperm + nslot) : nslot;
-    }
+    if (nslot < T) load_slot(nslot, na, nb, nc, nt_id);
     for (int ibase = blockIdx.x * SETUP_WARPS; ibase < n_items; ibase += istep) {
         const int slot = nslot;
         const int ia = na, ib = nb, ic = nc, t = nt_id;
         nslot = slot_of(ibase + istep + warp);
-        if (nslot < T) {
-            na = __ldg(ts + 3 * nslot), nb = __ldg(ts + 3 * nslot + 1), nc = __ldg(ts + 3 * nslot + 2);
-            nt_id = ord.tperm ? __ldg(ord.tperm + nslot) : nslot;
-        }
+        if (nslot < T) load_slot(nslot, na, nb, nc, nt_id);
         Setup3 f;
         int kind = 0;  // 0 none, 1 small record, 2 large record, 3 generic path
         int nt = 0;
