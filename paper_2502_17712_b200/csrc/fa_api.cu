@@ -109,7 +109,7 @@ int fa_create(fa_ctx** out, int device) {
     c->max_tiles = 1 << 18;
     c->pack_batch = 148;
     if (cudaMallocHost(&c->hstat, sizeof(fa_dstat)) != cudaSuccess ||
-        cudaMallocHost(&c->hvp, fa_ctx::kVpSlots * 16 * sizeof(double)) != cudaSuccess) {
+        cudaMallocHost(&c->hvp, fa_ctx::kVpSlots * FA_VP_DOUBLES * sizeof(double)) != cudaSuccess) {
         delete c;
         return set_err(FA_CUDA_ERROR, "cudaMallocHost failed");
     }
@@ -290,7 +290,7 @@ static int ensure_raster(fa_ctx* ctx, int W, int H, bool depth) {
     ENSURE(large, (size_t)ctx->max_large * sizeof(TriSetup));
     ENSURE(tiles, (size_t)ctx->max_tiles * sizeof(int4));
     ENSURE(dstat, sizeof(fa_dstat));
-    ENSURE(vp_dev, 16 * sizeof(double));
+    ENSURE(vp_dev, FA_VP_DOUBLES * sizeof(double));
     ENSURE(live_buf, (size_t)((T + FA_CLUSTER - 1) / FA_CLUSTER + 1) * 4);
     return FA_OK;
 }
@@ -397,7 +397,8 @@ static int read_stat(fa_ctx* ctx, cudaStream_t s) {
     return FA_OK;
 }
 
-static int upload_vp(fa_ctx* ctx, const double* vp_host, cudaStream_t s) {
+static_assert(FA_VC_OFF * 8 + sizeof(fa_view_consts) <= FA_VP_DOUBLES * 8, "camera slot too small");
+static int upload_vp(fa_ctx* ctx, const double* vp_host, cudaStream_t s, int W = 0, int H = 0) {
     // The 16 doubles are copied into a context-owned pinned slot before the
     // call returns, so the caller may reuse or refill its matrix at once (a
     // pinned caller buffer would otherwise be read asynchronously).  A slot
@@ -406,9 +407,12 @@ static int upload_vp(fa_ctx* ctx, const double* vp_host, cudaStream_t s) {
     ctx->vp_next = (k + 1) % fa_ctx::kVpSlots;
     if (!ctx->vp_ev[k]) CK(cudaEventCreateWithFlags(&ctx->vp_ev[k], cudaEventDisableTiming));
     else CK(cudaEventSynchronize(ctx->vp_ev[k]));
-    double* slot = ctx->hvp + 16 * k;
+    double* slot = ctx->hvp + FA_VP_DOUBLES * k;
     memcpy(slot, vp_host, 16 * sizeof(double));
-    CK(cudaMemcpyAsync(ctx->vp_dev.p, slot, 16 * sizeof(double), cudaMemcpyHostToDevice, s));
+    // the cluster culling's view constants, computed here once per frame
+    // (the culling's margins dwarf any host/device rounding difference)
+    compute_view_consts(slot, W, H, reinterpret_cast<fa_view_consts*>(slot + FA_VC_OFF));
+    CK(cudaMemcpyAsync(ctx->vp_dev.p, slot, FA_VP_DOUBLES * sizeof(double), cudaMemcpyHostToDevice, s));
     CK(cudaEventRecord(ctx->vp_ev[k], s));
     return FA_OK;
 }
@@ -593,7 +597,7 @@ int fa_project(fa_ctx* ctx, const double* vp_host, double* clip_out, void* strea
     cudaStream_t s = (cudaStream_t)stream;
     if (!ctx || !vp_host || (!clip_out && ctx->V)) return set_err(FA_VALUE_ERROR, "bad arguments");
     CK(cudaSetDevice(ctx->device));
-    ENSURE(vp_dev, 16 * sizeof(double));
+    ENSURE(vp_dev, FA_VP_DOUBLES * sizeof(double));
     int r = upload_vp(ctx, vp_host, s);
     if (r) return r;
     fa_launch_frame_init(ctx->pos_user, (int)ctx->V, P<double>(ctx->vp_dev), (double4*)clip_out, nullptr, 0, 0, nullptr,
@@ -613,7 +617,7 @@ int fa_depth_prepass(fa_ctx* ctx, const double* vp_host, int width, int height, 
         if (!r) r = ensure_charts(ctx);
         if (r) return r;
         CK(cudaMemsetAsync(ctx->dstat.p, 0, sizeof(fa_dstat), s));
-        r = upload_vp(ctx, vp_host, s);
+        r = upload_vp(ctx, vp_host, s, width, height);
         if (r) return r;
         int nl = 0;
         launch_depth(ctx, width, height, backface_cull, nullptr, s, nl);
@@ -642,7 +646,7 @@ int fa_mark_visible(fa_ctx* ctx, const double* vp_host, const double* depth, int
         if (!r) r = ensure_charts(ctx);
         if (r) return r;
         CK(cudaMemsetAsync(ctx->dstat.p, 0, sizeof(fa_dstat), s));
-        r = upload_vp(ctx, vp_host, s);
+        r = upload_vp(ctx, vp_host, s, width, height);
         if (r) return r;
         const fa_setup_order ord = setup_order(ctx);
         fa_launch_cluster_cull(P<double>(ctx->vp_dev), width, height, cull_args(ctx, backface_cull), s);
@@ -1062,10 +1066,12 @@ static int frame_sequence(fa_ctx* ctx, const fa_frame_params* p, cudaStream_t s,
                          fa_env_int("FASTATLAS_CLEAR_BLOCKS", FA_NUM_SMS));  // a slice of the GPU: the setup keeps the rest
     CK(cudaEventRecord(ctx->fj[10], ctx->side));
     const fa_setup_order ord = setup_order(ctx);
-    fa_launch_cluster_cull(P<double>(ctx->vp_dev), W, H, cull_args(ctx, p->backface_cull), s);
+    // the cluster culling runs in the projection's launch (its first blocks):
+    // beside it, with no launch or join of its own
+    const fa_cull_args cua = cull_args(ctx, p->backface_cull);
     fa_launch_frame_init(ctx->pos, V, P<double>(ctx->vp_dev), nullptr, P<double4>(ctx->scr), W, H,
-                         P<int>(ctx->vmin), nullptr, nullptr, 0, flags, T, s, 0, P<double2>(ctx->ndc2));
-    nl += ord.live ? 3 : 2;
+                         P<int>(ctx->vmin), nullptr, nullptr, 0, flags, T, s, 0, P<double2>(ctx->ndc2), &cua);
+    nl += 2;
     mark();  // 1: project + clears
     nl += fa_launch_depth_pass(true, clip_recomputed(ctx), P<double4>(ctx->scr), ctx->tris, T, W, H,
                                p->backface_cull, P<unsigned long long>(ctx->depth_keys), wid,
@@ -1210,7 +1216,7 @@ int fa_frame_launch(fa_ctx* ctx, const double* vp_host, const fa_frame_params* p
     int r = frame_prepare(ctx, p);
     if (r) return r;
     ctx->last_params = *p;
-    r = upload_vp(ctx, vp_host, s);
+    r = upload_vp(ctx, vp_host, s, p->width, p->height);
     if (r) return r;
     if (!p->use_graph || p->profile || p->packer != FA_PACKER_FASTATLAS) {
         fa_frame_params q = *p;
@@ -1514,7 +1520,7 @@ int fa_chart_bbox(fa_ctx* ctx, const double* vp_host, const double* tris_xyz, in
     if (!ctx || !vp_host || n < 0 || n >= (1ll << 31)) return set_err(FA_VALUE_ERROR, "bad arguments");
     if (n == 0) return set_err(FA_DEGENERATE_CHART, "chart has no triangles");
     CK(cudaSetDevice(ctx->device));
-    ENSURE(vp_dev, 16 * sizeof(double));
+    ENSURE(vp_dev, FA_VP_DOUBLES * sizeof(double));
     ENSURE(aux, 128);
     int r = upload_vp(ctx, vp_host, s);
     if (r) return r;

@@ -23,6 +23,8 @@
 #define FA_HIZ 8                // hierarchical-Z tile edge (pixels)
 
 // device status bits (fa_ctx::dstat->flags)
+#define FA_VC_OFF 16  // vp_dev: 16 doubles of VP, then the frame's fa_view_consts (host-computed)
+#define FA_VP_DOUBLES 64  // per uploaded camera (VP + view constants)
 // triangles per culling cluster (consecutive in the setup order; 32 or 16)
 #ifndef FA_CLUSTER
 #define FA_CLUSTER 32

@@ -37,7 +37,7 @@ struct fa_cull_args {
 };
 
 // Per-frame view constants derived from the camera matrix (k_frame_init)
-struct fa_view_consts {
+struct fa_view_consts {  // (FA_VP_DOUBLES - FA_VC_OFF doubles at most)
     double plane[7][4];    // L, R, B, T, N, F (w +- x, y, z) and w - W_EPSILON, as rows over (x, y, z, 1)
     double pn[7];          // |plane normal|
     double cam[3];         // projection centre (x = y = w = 0)
@@ -119,7 +119,7 @@ struct fa_ctx {
     // pinned camera staging: a ring of 16-double slots, each reused only
     // after the event recorded behind its upload has completed
     static const int kVpSlots = 8;
-    double* hvp = nullptr;      // kVpSlots x 16 doubles
+    double* hvp = nullptr;      // kVpSlots x FA_VP_DOUBLES doubles
     cudaEvent_t vp_ev[kVpSlots] = {};
     int vp_next = 0;
     fa_frame_params last_params{};
@@ -151,7 +151,8 @@ bool fa_ensure(fa_ctx* ctx, fa_buf& b, size_t bytes);
 void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* clip, double4* scr, int W, int H,
                           int* vmin, unsigned long long* depth, unsigned long long* wid, long long npx,
                           unsigned char* flags, int T, cudaStream_t s, int max_blocks = 0,
-                          double2* ndc2 = nullptr);
+                          double2* ndc2 = nullptr,
+                          const fa_cull_args* cull = nullptr);
 // the setup's live-cluster list (no-op when cu.clusters is null)
 void fa_launch_cluster_cull(const double* vp, int W, int H, const fa_cull_args& cu, cudaStream_t s);
 // side == nullptr: everything on s; otherwise fork/join through the events.

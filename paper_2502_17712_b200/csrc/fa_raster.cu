@@ -78,14 +78,49 @@ __device__ __forceinline__ int active_append1(int* counter) {
 }
 
 // ---- frame init: projection + buffer clears ------------------------------
-__global__ void k_frame_init(const double* __restrict__ pos, int V, const double* __restrict__ vp_dev,
-                             double4* __restrict__ clip, double4* __restrict__ scr, int W, int H,
-                             int* __restrict__ vmin, unsigned long long* __restrict__ depth,
-                             unsigned long long* __restrict__ wid, long long npx,
-                             unsigned int* __restrict__ flags32, int nflag32, double2* __restrict__ ndc2) {
+// the live-cluster list: one thread per cluster, warp-aggregated appends.
+// `vc` (shared memory) holds the frame's view constants, uploaded with the
+// camera (compute_view_consts on the host).
+__device__ __forceinline__ void cull_clusters(const fa_view_consts& vc, const fa_cull_args& cu, long long t0,
+                                              long long stride) {
+    const long long n_pad = ((long long)cu.n_clusters + 31) & ~31ll;
+    for (long long c = t0; c < n_pad; c += stride) {
+        const bool live = c < cu.n_clusters && !cluster_culled(cu.clusters[c], vc, cu.cull != 0);
+        const unsigned mk = __ballot_sync(0xffffffffu, live);
+        int base = 0;
+        if (lane_id() == 0 && mk) base = atomicAdd(&cu.st->n_live, __popc(mk));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (live) cu.live[base + __popc(mk & ((1u << lane_id()) - 1u))] = (int)c;
+    }
+}
+
+__device__ __forceinline__ void load_view_consts(const double* vp_dev, fa_view_consts* s_vc) {
+    const double* src = vp_dev + FA_VC_OFF;
+    double* dst = reinterpret_cast<double*>(s_vc);
+    for (int i = threadIdx.x; i < (int)(sizeof(fa_view_consts) / 8); i += blockDim.x) dst[i] = __ldg(src + i);
+    __syncthreads();
+}
+
+// Blocks [0, cull_blocks) cull the clusters (k_cluster_cull's work, so the
+// culling runs beside the projection with no extra launch or join); the rest
+// project the vertices / clear.
+__global__ void __launch_bounds__(256, 4) k_frame_init(const double* __restrict__ pos, int V,
+                                                       const double* __restrict__ vp_dev,
+                                                       double4* __restrict__ clip, double4* __restrict__ scr, int W,
+                                                       int H, int* __restrict__ vmin,
+                                                       unsigned long long* __restrict__ depth,
+                                                       unsigned long long* __restrict__ wid, long long npx,
+                                                       unsigned int* __restrict__ flags32, int nflag32,
+                                                       double2* __restrict__ ndc2, fa_cull_args cu, int cull_blocks) {
     FA_PDL_PROLOGUE();
-    long long stride = (long long)gridDim.x * blockDim.x;
-    long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if ((int)blockIdx.x < cull_blocks) {
+        __shared__ fa_view_consts s_vc;
+        load_view_consts(vp_dev, &s_vc);
+        cull_clusters(s_vc, cu, (long long)blockIdx.x * blockDim.x + threadIdx.x, (long long)cull_blocks * blockDim.x);
+        return;
+    }
+    long long stride = (long long)(gridDim.x - cull_blocks) * blockDim.x;
+    long long i0 = (long long)(blockIdx.x - cull_blocks) * blockDim.x + threadIdx.x;
     double m[16];
 #pragma unroll
     for (int i = 0; i < 16; i++) m[i] = V > 0 ? __ldg(vp_dev + i) : 0.0;  // (clear-only launches pass no matrix)
@@ -120,21 +155,8 @@ __global__ void k_frame_init(const double* __restrict__ pos, int V, const double
 __global__ void __launch_bounds__(256) k_cluster_cull(const double* __restrict__ vp_dev, int W, int H, fa_cull_args cu) {
     FA_PDL_PROLOGUE();
     __shared__ fa_view_consts s_vc;
-    if (threadIdx.x == 0) {
-        double m[16];
-        for (int i = 0; i < 16; i++) m[i] = vp_dev[i];
-        compute_view_consts(m, W, H, &s_vc);
-    }
-    __syncthreads();
-    const long long n_pad = ((long long)cu.n_clusters + 31) & ~31ll;
-    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n_pad; c += (long long)gridDim.x * blockDim.x) {
-        const bool live = c < cu.n_clusters && !cluster_culled(cu.clusters[c], s_vc, cu.cull != 0);
-        const unsigned mk = __ballot_sync(0xffffffffu, live);
-        int base = 0;
-        if (lane_id() == 0 && mk) base = atomicAdd(&cu.st->n_live, __popc(mk));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (live) cu.live[base + __popc(mk & ((1u << lane_id()) - 1u))] = (int)c;
-    }
+    load_view_consts(vp_dev, &s_vc);
+    cull_clusters(s_vc, cu, (long long)blockIdx.x * blockDim.x + threadIdx.x, (long long)gridDim.x * blockDim.x);
 }
 
 void fa_launch_cluster_cull(const double* vp, int W, int H, const fa_cull_args& cu, cudaStream_t s) {
@@ -992,15 +1014,22 @@ __global__ void __launch_bounds__(256) k_raster_vis_tiles(const SmallRec* __rest
 // ---- host launchers -------------------------------------------------------
 void fa_launch_frame_init(const double* pos, int V, const double* vp, double4* clip, double4* scr, int W, int H,
                           int* vmin, unsigned long long* depth, unsigned long long* wid, long long npx,
-                          unsigned char* flags, int T, cudaStream_t s, int max_blocks, double2* ndc2) {
+                          unsigned char* flags, int T, cudaStream_t s, int max_blocks, double2* ndc2,
+                          const fa_cull_args* cull) {
     long long work = V;
     if (depth && npx / 2 > work) work = npx / 2;
     int nflag32 = flags ? (T + 3) / 4 : 0;
     if (nflag32 > work) work = nflag32;
-    fa_launch(k_frame_init, max_blocks > 0 ? fa_grid(work, 256, max_blocks)
-                                           : fa_wave_grid(k_frame_init, 256, 0, (work + 255) / 256, FA_NUM_SMS * 8),
-              256, 0, s, 
-        pos, V, vp, clip, scr, W, H, vmin, depth, wid, npx, reinterpret_cast<unsigned int*>(flags), nflag32, ndc2);
+    const int g = max_blocks > 0 ? fa_grid(work, 256, max_blocks)
+                                 : fa_wave_grid(k_frame_init, 256, 0, (work + 255) / 256, FA_NUM_SMS * 8);
+    fa_cull_args cu{};
+    int cull_blocks = 0;
+    if (cull && cull->clusters) {
+        cu = *cull;
+        cull_blocks = fa_grid(cu.n_clusters, 256, FA_NUM_SMS);
+    }
+    fa_launch(k_frame_init, g + cull_blocks, 256, 0, s, pos, V, vp, clip, scr, W, H, vmin, depth, wid, npx,
+              reinterpret_cast<unsigned int*>(flags), nflag32, ndc2, cu, cull_blocks);
 }
 
 // fork `side` off `s` (side waits for everything issued on s so far)

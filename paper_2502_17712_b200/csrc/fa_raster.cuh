@@ -282,7 +282,7 @@ __device__ __forceinline__ bool cluster_culled(const fa_cluster& cl, const fa_vi
 }
 
 // view constants of the camera matrix m (row-major VP), screen W x H
-__device__ __forceinline__ void compute_view_consts(const double* m, int W, int H, fa_view_consts* vc) {
+__host__ __device__ inline void compute_view_consts(const double* m, int W, int H, fa_view_consts* vc) {
     const double* X = m;
     const double* Y = m + 4;
     const double* Z = m + 8;
