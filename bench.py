@@ -255,6 +255,8 @@ def parse_args(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-frames", type=int, default=5)
     ap.add_argument("--depth", type=int, default=6, help="concurrent views per GPU (FramePipeline slots)")
+    ap.add_argument("--e2e-depth", type=int, default=5,
+                    help="FramePipeline slots of the e2e runs (their copies and host hand-offs favour one fewer)")
     ap.add_argument("--l2", default="replicas", choices=["replicas", "flush"],
                     help="pipelined L2 policy: per-slot mesh replicas (inputs > L2) or a 256 MiB flush per view")
     args = ap.parse_args(argv)
@@ -422,7 +424,7 @@ def measure_gpu(args, rank: int, world: int, local: int, view_ids: list) -> dict
     e2e = {}
     for kind, outputs in (("compact", ("visible", "visible_chart", "vertex_uv", "placements")),
                           ("dense", ("chart_of_triangle", "visible", "uv", "placements"))):
-        pipe = fa.FramePipeline(mesh, device=local, settings=settings, depth=args.depth, outputs=outputs,
+        pipe = fa.FramePipeline(mesh, device=local, settings=settings, depth=args.e2e_depth, outputs=outputs,
                                 mesh_replicas=replicas, packed=not os.environ.get("FA_BENCH_UNPACKED"))
         d2h = [0]
 
@@ -527,10 +529,12 @@ def main(argv=None, measure=None):
                        "ms_per_frame_is": "single-view latency, one engine, mean of K event pairs"},
             "e2e": {"value": views_total / (e2e_c * 1e-3), "unit": "atlases/s", "h2d_bytes_per_step": 128,
                     "d2h_bytes_per_step": int(r["e2e"]["compact"][1]),
-                    "what": "FramePipeline.run over pinned camera matrices (H2D per view) with the visible list, "
-                            "the chart id of each visible triangle (sparse chart_of_triangle), the f32 UV of each "
-                            "visible vertex (compact form of the per-triangle f32 UV rows, rebuilt bit-identically "
-                            "on access) and the placements copied into pinned host buffers (D2H per view)",
+                    "concurrent_views_per_gpu": args.e2e_depth,
+                    "what": "FramePipeline.run over pinned camera matrices (H2D per view) with the visible triangles, "
+                            "the chart of each, the f32 UV of each visible vertex and the placements copied into "
+                            "pinned host buffers (D2H per view, the packed wire format: visibility and vertex bit "
+                            "masks, 16-bit chart indices + chart ids, f32 vertex UVs; decoded on access into the "
+                            "visible list, sparse chart ids and the per-triangle f32 UV rows, bit-identical)",
                     "dense": {"value": views_total / (e2e_d * 1e-3), "unit": "atlases/s",
                               "h2d_bytes_per_step": 128, "d2h_bytes_per_step": int(r["e2e"]["dense"][1]),
                               "what": "the reference's output shapes: dense (T,) chart_of_triangle, (n_visible, 6) "
