@@ -14,6 +14,9 @@
 #include "fa_internal.h"
 
 #define CMP_THREADS 256
+#ifndef UF_HALVE_AFTER
+#define UF_HALVE_AFTER 16  // k_hook_multi: find rounds before path halving starts
+#endif
 // flags per thread of the visible compaction (one 32-bit load) and visible
 // triangles per thread of the roots compaction: few items per thread, so the
 // latency-bound gathers have many threads in flight
@@ -322,10 +325,22 @@ __global__ void k_hook_multi(const int* __restrict__ tris, const int* __restrict
         if (r0 == t) r0 = m0;
         // lock-free: every lost CAS moves a node strictly down, so this ends
         while (true) {
-            // joint find: one parent load per node per round
+            // joint find: one parent load per node per round; past UF_HALVE_AFTER
+            // rounds (long paths: few, large charts) each non-root is also
+            // pointed at its grandparent (path halving: labels only point at
+            // smaller ids, so a grandparent is always an ancestor and the racy
+            // plain stores keep every path intact; roots are never written)
+            int hops = 0;
             while (true) {
                 int p0 = label[r0], p1 = label[r1], p2 = label[r2], p3 = label[r3];
                 bool roots = (p0 == r0) & (p1 == r1) & (p2 == r2) & (p3 == r3);
+                if (!roots && ++hops > UF_HALVE_AFTER) {
+                    const int g0 = label[p0], g1 = label[p1], g2 = label[p2], g3 = label[p3];
+                    if (g0 != p0) label[r0] = g0, p0 = g0;
+                    if (g1 != p1) label[r1] = g1, p1 = g1;
+                    if (g2 != p2) label[r2] = g2, p2 = g2;
+                    if (g3 != p3) label[r3] = g3, p3 = g3;
+                }
                 r0 = p0;
                 r1 = p1;
                 r2 = p2;
