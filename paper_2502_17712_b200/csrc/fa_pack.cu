@@ -469,7 +469,8 @@ template <int PK_KREG, typename DimT>
 __device__ bool pack_candidate(const DimT* __restrict__ ow, const DimT* __restrict__ oh, int n,
                                long long num, long long den, long long omega, int kbits, long long min_dim,
                                long long pad, int* cw, int* ch, long long* cp, int* cy, int* rowstart, int* front,
-                               long long& out_num, long long& out_den, long long& out_used, PackSmem& sm) {
+                               long long& out_num, long long& out_den, long long& out_used, PackSmem& sm,
+                               int* sbox = nullptr, int n_sbox = 0) {
     int tid = threadIdx.x;
     bool have_fold = false;
     long long m = 0;
@@ -488,11 +489,15 @@ __device__ bool pack_candidate(const DimT* __restrict__ ow, const DimT* __restri
         // widths, the running fold offset and the overflow stay in registers,
         // so a round is the divisions + one block scan + one paired max.
         const int b0 = tid * K;
-        long long owr[PK_KREG], wr[PK_KREG];
+        long long owr[PK_KREG], ohr[PK_KREG], wr[PK_KREG];
         long long owmax = -1, negmin = 0;
+        // the fast tail (heights + push-up from shared memory) needs the
+        // heights too: loaded with the widths, off the critical path
+        const bool fast_tail = sbox != nullptr && n <= n_sbox && omega < (1ll << 30);
 #pragma unroll
         for (int k = 0; k < PK_KREG; k++) {
             owr[k] = (k < K && b0 + k < n) ? ow[b0 + k] : 0;
+            ohr[k] = (fast_tail && k < K && b0 + k < n) ? oh[b0 + k] : 0;
             owmax = owr[k] > owmax ? owr[k] : owmax;
             negmin = -owr[k] > negmin ? -owr[k] : negmin;
         }
@@ -501,6 +506,7 @@ __device__ bool pack_candidate(const DimT* __restrict__ ow, const DimT* __restri
         // 32-bit values, REDUX max, and one barrier per block reduction
         // (every thread combines the per-warp partials itself).
         block_max2_ll(owmax, negmin, sm.red, sm.red2);
+        PACK_MARK(10, clock64() - t0);
         const long long wb = (owmax > min_dim ? owmax : min_dim) + 2 * pad;
         const bool narrow = negmin <= 0 && owmax >= 0 && owmax < (1ll << 31) && wb < (1ll << 31) &&
                             (long long)n * wb < (1ll << 31);
@@ -600,6 +606,9 @@ __device__ bool pack_candidate(const DimT* __restrict__ ow, const DimT* __restri
                 m = mloc > 0 ? mloc : 0;
                 have_fold = true;
             }
+#ifdef FA_PACK_PROF
+            if (it == 0) PACK_MARK(11, clock64() - t0);
+#endif
             if (m == 0) break;
             have_fold = false;
             snap_scale(num, den, omega, m);
@@ -608,13 +617,94 @@ __device__ bool pack_candidate(const DimT* __restrict__ ow, const DimT* __restri
 #endif
         }
         long long p = base;
+        long long pr[PK_KREG];
 #pragma unroll
         for (int k = 0; k < PK_KREG; k++) {
+            pr[k] = p;
             if (k < K && b0 + k < n) {
                 cw[b0 + k] = (int)wr[k];
                 cp[b0 + k] = p;
                 p += wr[k];
             }
+        }
+        if (fast_tail) {
+            // Fast tail: the heights come from registers and the push-up
+            // reads its boxes from shared memory (x, w, h and the row
+            // starts), so a row costs shared-memory round trips and one
+            // barrier instead of dependent global loads.  With m == 0 no box
+            // straddles a row boundary, so box b starts row r exactly when
+            // its fold offset is a multiple of omega.
+            PACK_MARK(0, clock64() - t0);
+            if (!have_fold || m != 0) return false;  // block-uniform
+            int* sx = sbox;
+            int* sw = sx + n_sbox;
+            int* sh = sw + n_sbox;
+            int* srs = sh + n_sbox;
+            const double rdh = 1.0 / (double)den;
+            unsigned long long area = 0;
+#pragma unroll
+            for (int k = 0; k < PK_KREG; k++) {
+                const int b = b0 + k;
+                if (k < K && b < n) {
+                    const long long h = scaled_dim_rcp(ohr[k], num, den, rdh, min_dim, pad);
+                    ch[b] = (int)h;
+                    area += (unsigned long long)wr[k] * (unsigned long long)h;
+                    const long long q = pr[k] & (omega - 1);
+                    const int r = (int)(pr[k] >> kbits);
+                    const bool left = (r % FA_DIRECTION_PERIOD) == 0;
+                    sx[b] = left ? (int)q : (int)(omega - q - wr[k]);
+                    sw[b] = (int)wr[k];
+                    sh[b] = h > omega ? (int)(omega + 1) : (int)h;  // taller boxes reject anyway (saturated)
+                    if (q == 0) srs[r] = b;
+                    if (b == n - 1) sm.flag = r + 1;
+                }
+            }
+            for (int c = tid; c <= omega; c += blockDim.x) front[c] = 0;
+            area = (unsigned long long)block_sum_ll((long long)area, sm.red);  // its barriers publish sx..srs
+            PACK_MARK(1, clock64() - t0);
+            if ((long long)area > omega * omega) return false;
+            const int n_rows = sm.flag;
+            PACK_MARK(2, clock64() - t0);
+            PACK_MARK(5, n_rows);
+            int used = 0;
+            for (int r = 0; r < n_rows; r++) {
+                const int rb0 = srs[r];
+                const int nb = ((r + 1 < n_rows) ? srs[r + 1] : n) - rb0;
+                int G = 32;
+                while (G > 1 && G * nb > (int)blockDim.x) G >>= 1;
+                const int groups = blockDim.x / G;
+                const int g = tid / G, gl = tid % G;
+                for (int gbase = 0; gbase < nb; gbase += groups) {
+                    const int gb = gbase + g;
+                    const bool act = gb < nb;
+                    const int b = rb0 + (act ? gb : 0);
+                    const int x = sx[b], w = act ? sw[b] : 0, h = sh[b];
+                    int rest = 0;
+                    if (G == 1) rest = span_max(front, x, x + w);
+                    else
+                        for (int c = x + gl; c < x + w; c += G) rest = max(rest, front[c]);
+                    for (int o = G >> 1; o > 0; o >>= 1) rest = max(rest, __shfl_xor_sync(0xffffffffu, rest, o, G));
+                    // saturate above omega: any such top already rejects the candidate
+                    const int top = min(rest + h, (int)omega + 1);
+                    if (act) {
+                        if (G == 1) span_fill(front, x, x + w, top);
+                        else
+                            for (int c = x + gl; c < x + w; c += G) front[c] = top;
+                        if (gl == 0) cy[b] = rest;
+                        used = max(used, top);
+                    }
+                }
+                __syncthreads();
+            }
+            const long long used_b = block_max_ll((long long)used, sm.red);
+            PACK_MARK(3, clock64() - t0);
+            out_used = used_b;
+            if (used_b > omega) return false;
+            long long g2 = gcd_ll(num, den);
+            if (g2 == 0) g2 = 1;
+            out_num = div_by_gcd(num, g2);
+            out_den = div_by_gcd(den, g2);
+            return true;
         }
         __syncthreads();
     } else
@@ -737,8 +827,11 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack(const long long* __restrict
                                                      long long* __restrict__ cand_p, int* __restrict__ cand_w,
                                                      int* __restrict__ cand_h, int* __restrict__ cand_y,
                                                      int* __restrict__ rowstart, int* __restrict__ gfront,
-                                                     fa_dstat* __restrict__ st) {
+                                                     fa_dstat* __restrict__ st, int n_sbox) {
     FA_PDL_PROLOGUE();
+    // dynamic shared memory: the frontline (omega + 1 ints, unless it lives
+    // in gfront), then the push-up's box arrays (x, w, h, row starts: n_sbox
+    // each) when n_sbox > 0
     extern __shared__ int dyn_front[];
     __shared__ PackSmem sm;
     int n = n_dev ? *n_dev : n_max;
@@ -763,17 +856,27 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack(const long long* __restrict
     }
     size_t slot = blockIdx.x;
     int* front = gfront ? gfront + slot * (size_t)(omega + 1) : dyn_front;
+    int* sbox = n_sbox > 0 ? dyn_front + (gfront ? 0 : ((omega + 1 + 3) & ~3ll)) : nullptr;
     long long rn = 0, rd = 1, used = 0;
     // boxes per thread in registers: 4 up to 4 * blockDim boxes (the C2
     // frames), 8 beyond (C3's ~4000 charts), else the global-memory rounds
     const int K = (n + (int)blockDim.x - 1) / (int)blockDim.x;
+#ifdef FA_PACK_TWICE
+    // debug: a first, discarded run warms the instruction cache; the timed
+    // (second) run then shows the per-phase cost without cold-code misses
+    if (K <= 4)
+        pack_candidate<4>(ow, oh, n, num, den, omega, kbits, min_dim, pad, cand_w + slot * n_max,
+                          cand_h + slot * n_max, cand_p + slot * n_max, cand_y + slot * n_max,
+                          rowstart + slot * n_max, front, rn, rd, used, sm, sbox, n_sbox);
+    __syncthreads();
+#endif
     bool ok = K <= 4 ? pack_candidate<4>(ow, oh, n, num, den, omega, kbits, min_dim, pad, cand_w + slot * n_max,
                                          cand_h + slot * n_max, cand_p + slot * n_max, cand_y + slot * n_max,
-                                         rowstart + slot * n_max, front, rn, rd, used, sm)
+                                         rowstart + slot * n_max, front, rn, rd, used, sm, sbox, n_sbox)
                      : pack_candidate<PK_KREG_WIDE>(ow, oh, n, num, den, omega, kbits, min_dim, pad,
                                                     cand_w + slot * n_max, cand_h + slot * n_max,
                                                     cand_p + slot * n_max, cand_y + slot * n_max,
-                                                    rowstart + slot * n_max, front, rn, rd, used, sm);
+                                                    rowstart + slot * n_max, front, rn, rd, used, sm, sbox, n_sbox);
     if (threadIdx.x == 0) {
         long long* rec = cand + CAND_REC * (i - 1);
         rec[0] = ok;
@@ -1009,6 +1112,35 @@ __global__ void k_xywh(const long long* __restrict__ cand, const long long* __re
 static size_t front_smem(long long omega) { return (size_t)(omega + 1) * sizeof(int); }
 static const size_t kMaxFrontSmem = 200 * 1024;
 
+// k_pack's dynamic shared memory: the frontline when it fits, then the
+// push-up box arrays for up to the register path's box count (4 ints each)
+struct PackSmemPlan {
+    bool smem_front;
+    int n_sbox;
+    size_t dyn;
+};
+static PackSmemPlan pack_smem_plan(long long omega, int n_max) {
+    PackSmemPlan pl{};
+    const int cap = n_max < PK_KREG_WIDE * PK_THREADS ? n_max : PK_KREG_WIDE * PK_THREADS;
+    const size_t boxes = (size_t)4 * cap * sizeof(int);
+    const size_t front = ((size_t)(omega + 1 + 3) & ~(size_t)3) * sizeof(int);
+    pl.smem_front = front_smem(omega) <= kMaxFrontSmem;
+    if (pl.smem_front && front + boxes <= kMaxFrontSmem) {
+        pl.n_sbox = cap;
+        pl.dyn = front + boxes;
+    } else if (pl.smem_front) {
+        pl.dyn = front_smem(omega);
+    } else if (boxes <= kMaxFrontSmem) {
+        pl.n_sbox = cap;
+        pl.dyn = boxes;
+    }
+    if (!fa_env_int("FASTATLAS_PACK_SMEM_TAIL", 1)) {
+        pl.n_sbox = 0;
+        pl.dyn = pl.smem_front ? front_smem(omega) : 0;
+    }
+    return pl;
+}
+
 static void ensure_smem_attr() {
     static bool done = false;
     if (done) return;
@@ -1049,8 +1181,9 @@ int fa_launch_pack(const fa_pack_bufs& b, int n_max, const int* n_dev, long long
                    long long min_dim, long long pad, int batch, fa_dstat* st, cudaStream_t s) {
     ensure_smem_attr();
     int kbits = 63 - __builtin_clzll((unsigned long long)omega);
-    bool smem_front = front_smem(omega) <= kMaxFrontSmem;
-    size_t dyn = smem_front ? front_smem(omega) : 0;
+    const PackSmemPlan pl = pack_smem_plan(omega, n_max);
+    const bool smem_front = pl.smem_front;
+    const size_t dyn = pl.dyn;
     int launches = 0;
     for (long long hi = n_scales; hi >= 1; hi -= batch) {
         long long lo = hi - batch + 1;
@@ -1058,7 +1191,7 @@ int fa_launch_pack(const fa_pack_bufs& b, int n_max, const int* n_dev, long long
         int grid = (int)(hi - lo + 1);
         fa_launch(k_pack, grid, PK_THREADS, dyn, s, b.ow, b.oh, n_max, n_dev, omega, kbits, n_scales, hi, 0, 0, min_dim, pad,
                                              b.cand, b.cand_p, b.cand_w, b.cand_h, b.cand_y, b.rowstart,
-                                             smem_front ? nullptr : b.gfront, st);
+                                             smem_front ? nullptr : b.gfront, st, pl.n_sbox);
         launches++;
         if (lo > 1) {
             fa_launch(k_batch_done, 1, 256, 0, s, b.cand, lo, hi, st);
@@ -1078,10 +1211,9 @@ void fa_launch_pack_at_scale(const long long* ow, const long long* oh, int n, lo
                              int* cand_w, int* cand_h, int* cand_y, int* rowstart, int* gfront, cudaStream_t s) {
     ensure_smem_attr();
     int kbits = 63 - __builtin_clzll((unsigned long long)omega);
-    bool smem_front = front_smem(omega) <= kMaxFrontSmem;
-    fa_launch(k_pack, 1, PK_THREADS, smem_front ? front_smem(omega) : 0, s, ow, oh, n, nullptr, omega, kbits, 1, 1, num, den,
-                                                                     min_dim, pad, cand, cand_p, cand_w, cand_h, cand_y,
-                                                                     rowstart, smem_front ? nullptr : gfront, nullptr);
+    const PackSmemPlan pl = pack_smem_plan(omega, n);
+    fa_launch(k_pack, 1, PK_THREADS, pl.dyn, s, ow, oh, n, nullptr, omega, kbits, 1, 1, num, den, min_dim, pad, cand,
+              cand_p, cand_w, cand_h, cand_y, rowstart, pl.smem_front ? nullptr : gfront, nullptr, pl.n_sbox);
 }
 
 void fa_launch_xywh(const long long* cand, const long long* cand_p, const int* cand_w, const int* cand_h,

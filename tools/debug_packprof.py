@@ -26,5 +26,5 @@ print("charts", out.n_charts, "scale", out.scale)
 for i in range(64):
     r = buf[i]
     print(i, "fold %.1f us  heights %.1f  rowstart %.1f  rows %.1f  iters %d  n_rows %d | round 2: widths %d cyc, "
-          "+scan %d cyc +max2 %d +snap %d" % (r[0] / 1920, r[1] / 1920, r[2] / 1920, r[3] / 1920, r[4], r[5], r[6], r[7],
-                                    r[8], r[9]))
+          "+scan %d cyc +max2 %d +snap %d | loaded %d cyc, round 1 done %d cyc" % (r[0] / 1920, r[1] / 1920, r[2] / 1920,
+                                    r[3] / 1920, r[4], r[5], r[6], r[7], r[8], r[9], r[10], r[11]))
