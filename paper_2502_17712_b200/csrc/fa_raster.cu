@@ -191,7 +191,13 @@ __global__ void k_encode_depth(const double* __restrict__ in, unsigned long long
 #ifndef SETUP_WARPS
 #define SETUP_WARPS 8
 #endif
-__global__ void __launch_bounds__(SETUP_WARPS * 32, 32 / SETUP_WARPS) k_raster_setup(const double4* __restrict__ scr,
+#ifndef SETUP_DEFER
+#define SETUP_DEFER 1
+#endif
+#ifndef SETUP_MIN_BLOCKS
+#define SETUP_MIN_BLOCKS (32 / SETUP_WARPS)
+#endif
+__global__ void __launch_bounds__(SETUP_WARPS * 32, SETUP_MIN_BLOCKS) k_raster_setup(const double4* __restrict__ scr,
                                                       const int* __restrict__ tris,
                                                       int T, int W, int H, int cull,
                                                       SmallRec* __restrict__ recs, int* __restrict__ clip_list,
@@ -200,8 +206,8 @@ __global__ void __launch_bounds__(SETUP_WARPS * 32, 32 / SETUP_WARPS) k_raster_s
     FA_PDL_PROLOGUE();
     // per-warp counts -> per-warp bases; one atomic per counter per block step
     // (a same-address atomic per warp serialises ~30K times in the L2)
-    __shared__ int s_cnt[4][SETUP_WARPS];
-    __shared__ int s_base[4][SETUP_WARPS];
+    __shared__ int s_cnt[2][4][SETUP_WARPS];
+    __shared__ int s_base[2][4][SETUP_WARPS];
     const int lane = lane_id(), warp = threadIdx.x >> 5;
     const bool rec_ok = W <= 32767 && H <= 32767;
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -238,6 +244,54 @@ __global__ void __launch_bounds__(SETUP_WARPS * 32, 32 / SETUP_WARPS) k_raster_s
     int nslot = slot_of(blockIdx.x * SETUP_WARPS + warp);
     int na = 0, nb = 0, nc = 0, nt_id = T;
     if (nslot < T) load_slot(nslot, na, nb, nc, nt_id);
+#if SETUP_DEFER
+    // deferred publication (see the loop): the records of a step wait in
+    // shared memory until the next step's barrier has published their bases
+    __shared__ SmallRec s_stage[SETUP_WARPS][32];
+    int step = 0, resv = 0;
+    unsigned pm1 = 0, pm2 = 0, pm3 = 0;
+    int p_kind = 0, p_t = 0, p_nt = 0, p_incl = 0, p_total = 0;
+    // leader thread c: per-warp bases of counter c for the step of parity q
+    auto publish_bases = [&](int q, int b) {
+        const int c = threadIdx.x;
+        for (int w = 0; w < SETUP_WARPS; w++) {
+            s_base[q][c][w] = b;
+            b += s_cnt[q][c][w];
+        }
+    };
+    // write out the warp's staged step (parity q): small records to
+    // [sb, sb + n1), large ones downward from T - lb, their ids, clip list
+    // entries and tile descriptors
+    auto flush = [&](int q) {
+        const int sb = s_base[q][0][warp], lb = s_base[q][1][warp], cb = s_base[q][2][warp],
+                  tb = s_base[q][3][warp];
+        const int n1 = __popc(pm1), n2 = __popc(pm2);
+        const int4* src = reinterpret_cast<const int4*>(s_stage[warp]);
+        constexpr int C16 = sizeof(SmallRec) / 16;
+        for (int j = lane; j < (n1 + n2) * C16; j += 32) {
+            const int r = j / C16, c = j - r * C16;
+            SmallRec* dst = r < n1 ? recs + sb + r : recs + (T - (lb + (r - n1)));
+            reinterpret_cast<int4*>(dst)[c] = src[j];
+        }
+        if (p_kind == 1) small_ids(recs, T)[sb + __popc(pm1 & lt_mask)] = p_t;
+        if (p_kind == 3) clip_list[cb + __popc(pm3 & lt_mask)] = p_t;
+        if (pm2) {
+            const int ri = T - (lb + __popc(pm2 & lt_mask));
+            if (tb + p_total > max_tiles && lane == 0) atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW);
+            unsigned m = pm2;
+            while (m) {
+                int srcl = __ffs(m) - 1;
+                m &= m - 1;
+                int r_src = __shfl_sync(0xffffffffu, ri, srcl);
+                int n_src = __shfl_sync(0xffffffffu, p_nt, srcl);
+                int t_src = __shfl_sync(0xffffffffu, p_t, srcl);
+                int e_src = tb + __shfl_sync(0xffffffffu, p_incl, srcl) - n_src;
+                for (int k = lane; k < n_src; k += 32)
+                    if (e_src + k < max_tiles) tiles[e_src + k] = make_int4(r_src, k, t_src, 0);
+            }
+        }
+    };
+#endif
     for (int ibase = blockIdx.x * SETUP_WARPS; ibase < n_items; ibase += istep) {
         const int slot = nslot;
         const int ia = na, ib = nb, ic = nc, t = nt_id;
@@ -270,35 +324,74 @@ __global__ void __launch_bounds__(SETUP_WARPS * 32, 32 / SETUP_WARPS) k_raster_s
             if (lane >= o) incl += y;
         }
         const int total = __shfl_sync(0xffffffffu, incl, 31);
+#if SETUP_DEFER
+        // One barrier per step.  The counts of this step are published; the
+        // leader threads then (1) write the PREVIOUS step's per-warp bases
+        // from the global reservation they issued one step ago -- so the
+        // atomic's round trip overlaps a whole step of setup work -- and (2)
+        // issue this step's reservation.  Each warp stages this step's
+        // records in shared memory and writes them out (coalesced) one step
+        // later, once their bases are known.
+        const int par = step & 1;
         if (lane == 0) {
-            s_cnt[0][warp] = __popc(m1);
-            s_cnt[1][warp] = __popc(m2);
-            s_cnt[2][warp] = __popc(m3);
-            s_cnt[3][warp] = total;
+            s_cnt[par][0][warp] = __popc(m1);
+            s_cnt[par][1][warp] = __popc(m2);
+            s_cnt[par][2][warp] = __popc(m3);
+            s_cnt[par][3][warp] = total;
+        }
+        if (step > 0 && threadIdx.x < 4) publish_bases(par ^ 1, resv);
+        __syncthreads();
+        if (threadIdx.x < 4) {
+            const int c = threadIdx.x;
+            int sum = 0;
+            for (int w = 0; w < SETUP_WARPS; w++) sum += s_cnt[par][c][w];
+            int* ctr = c == 0 ? &st->n_small3 : c == 1 ? &st->n_large3 : c == 2 ? &st->n_clip : &st->n_tiles;
+            resv = sum ? atomicAdd(ctr, sum) : 0;  // consumed at the next step's publish
+        }
+        if (step > 0) flush(par ^ 1);
+        // stage this step (the flush above read the staging area: same warp)
+        __syncwarp();
+        if (kind == 1) store_rec(f, t, s_stage[warp] + __popc(m1 & lt_mask));
+        else if (kind == 2) store_rec(f, t, s_stage[warp] + __popc(m1) + __popc(m2 & lt_mask));
+        __syncwarp();
+        pm1 = m1, pm2 = m2, pm3 = m3, p_kind = kind, p_t = t, p_nt = nt, p_incl = incl, p_total = total;
+        step++;
+    }
+    if (step > 0) {
+        if (threadIdx.x < 4) publish_bases((step - 1) & 1, resv);
+        __syncthreads();
+        flush((step - 1) & 1);
+    }
+#else
+        if (lane == 0) {
+            s_cnt[0][0][warp] = __popc(m1);
+            s_cnt[0][1][warp] = __popc(m2);
+            s_cnt[0][2][warp] = __popc(m3);
+            s_cnt[0][3][warp] = total;
         }
         __syncthreads();
         if (threadIdx.x < 4) {
             const int c = threadIdx.x;
             int sum = 0;
-            for (int w = 0; w < SETUP_WARPS; w++) sum += s_cnt[c][w];
+            for (int w = 0; w < SETUP_WARPS; w++) sum += s_cnt[0][c][w];
             int* ctr = c == 0 ? &st->n_small3 : c == 1 ? &st->n_large3 : c == 2 ? &st->n_clip : &st->n_tiles;
             int b = sum ? atomicAdd(ctr, sum) : 0;
             for (int w = 0; w < SETUP_WARPS; w++) {
-                s_base[c][w] = b;
-                b += s_cnt[c][w];
+                s_base[0][c][w] = b;
+                b += s_cnt[0][c][w];
             }
         }
         __syncthreads();
         if (m1 && kind == 1) {
-            const int idx = s_base[0][warp] + __popc(m1 & lt_mask);
+            const int idx = s_base[0][0][warp] + __popc(m1 & lt_mask);
             store_rec(f, t, recs + idx);
             small_ids(recs, T)[idx] = t;  // lets the visibility filter skip flagged records unread
         }
-        if (m3 && kind == 3) clip_list[s_base[2][warp] + __popc(m3 & lt_mask)] = t;
+        if (m3 && kind == 3) clip_list[s_base[0][2][warp] + __popc(m3 & lt_mask)] = t;
         if (m2) {
             // large records are stored downward from index T (small + large
             // records <= T, so the two ends never meet)
-            const int rb = s_base[1][warp], tb = s_base[3][warp];
+            const int rb = s_base[0][1][warp], tb = s_base[0][3][warp];
             int ri = T - (rb + __popc(m2 & lt_mask));
             if (kind == 2) store_rec(f, t, recs + ri);
             if (tb + total > max_tiles && lane == 0) atomicOr(&st->flags, FA_DFLAG_QUEUE_OVERFLOW);
@@ -316,6 +409,7 @@ __global__ void __launch_bounds__(SETUP_WARPS * 32, 32 / SETUP_WARPS) k_raster_s
             }
         }
     }
+#endif
 }
 
 // ---- pass 1, generic path: clipped polygons (and oversize screens) --------
@@ -1064,7 +1158,7 @@ int fa_launch_depth_pass(bool write_depth, const ClipSrc clip, const double4* sc
                          int* clip_list, TriSetup* large, int max_large, int4* tiles, int max_tiles, fa_dstat* st,
                          cudaStream_t s, cudaStream_t side, cudaStream_t side2, cudaEvent_t ev_fork,
                          cudaEvent_t ev_join, cudaEvent_t ev_join2, cudaEvent_t ev_clear, fa_setup_order ord) {
-    fa_launch(k_raster_setup, fa_grid(T, SETUP_WARPS * 32, FA_NUM_SMS * (32 / SETUP_WARPS)), SETUP_WARPS * 32, 0, s, scr, tris, T, W, H, cull, small_rec,
+    fa_launch(k_raster_setup, fa_grid(T, SETUP_WARPS * 32, FA_NUM_SMS * SETUP_MIN_BLOCKS), SETUP_WARPS * 32, 0, s, scr, tris, T, W, H, cull, small_rec,
               clip_list, tiles, max_tiles, st, ord);
     // the depth/winner clears ran beside the setup: every raster branch
     // (forked from here) needs them

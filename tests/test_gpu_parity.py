@@ -150,6 +150,13 @@ STATUS_EXC = {"PackFailure": fa.PackFailure, "ValueError": ValueError, "HeightOv
 
 
 class TestPack:
+    @pytest.fixture(autouse=True, params=["smem_tail", "global_tail"])
+    def _tail(self, request, monkeypatch):
+        """Both push-up tails of k_pack: boxes in shared memory (default) and
+        the global-memory rows (FASTATLAS_PACK_SMEM_TAIL=0, the path of frames
+        with more than 4096 charts)."""
+        monkeypatch.setenv("FASTATLAS_PACK_SMEM_TAIL", "1" if request.param == "smem_tail" else "0")
+
     @pytest.mark.parametrize("idx", range(len(pack_cases()["pack"])))
     def test_pack_vs_reference(self, idx):
         c = pack_cases()["pack"][idx]
