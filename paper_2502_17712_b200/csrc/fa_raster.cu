@@ -802,6 +802,9 @@ __global__ void __launch_bounds__(COOP_WARPS * 32, COOP_MIN_BLOCKS) k_small_coop
 // them).  The ~20% that survive are appended (one atomic per block step) to a
 // queue that k_vis_small_sample walks one thread per survivor, so sampling
 // lanes are not spread thinly over warps that are mostly done.
+#ifndef FILTER_WARP_ATOMICS
+#define FILTER_WARP_ATOMICS 1  // measured: visibility stage -2 us vs the block-aggregated reservation
+#endif
 __global__ void __launch_bounds__(256) k_vis_small_filter(const SmallRec* __restrict__ small_rec, int T,
                                                           const unsigned long long* __restrict__ hiz, int htx,
                                                           const unsigned char* __restrict__ flags,
@@ -847,6 +850,25 @@ __global__ void __launch_bounds__(256) k_vis_small_filter(const SmallRec* __rest
         }
         const unsigned m = __ballot_sync(0xffffffffu, need && !wide);
         const unsigned m2 = __ballot_sync(0xffffffffu, need && wide);
+#if FILTER_WARP_ATOMICS
+        // per-warp reservations: no block barrier (warps do not wait on the
+        // block's slowest record loads)
+        int wb0 = 0, wb1 = 0;
+        if (lane == 0) {
+            if (m) wb0 = atomicAdd(&st->n_vis_q, __popc(m));
+            if (m2) wb1 = atomicAdd(&st->n_vis_q2, __popc(m2));
+        }
+        if (m | m2) {
+            wb0 = __shfl_sync(0xffffffffu, wb0, 0);
+            wb1 = __shfl_sync(0xffffffffu, wb1, 0);
+            if (need) {
+                const unsigned mm = wide ? m2 : m;
+                const int off = (wide ? wb1 : wb0) + __popc(mm & ((1u << lane) - 1u));
+                queue[wide ? T - off : off] = i;
+            }
+        }
+        continue;
+#endif
         if (lane == 0) {
             s_cnt[0][warp] = __popc(m);
             s_cnt[1][warp] = __popc(m2);
