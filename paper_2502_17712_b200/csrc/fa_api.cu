@@ -107,6 +107,10 @@ int fa_create(fa_ctx** out, int device) {
     c->device = device;
     c->max_large = 1 << 16;
     c->max_tiles = 1 << 18;
+    // test knob: tiny initial work queues, so frames take the overflow ->
+    // grow -> rerun path (tests/test_gpu_parity.py::test_queue_overflow_reruns)
+    c->queue_init = fa_env_int("FASTATLAS_QUEUE_INIT", 0);
+    if (c->queue_init > 0) c->max_large = c->max_tiles = c->queue_init;
     c->pack_batch = 148;
     if (cudaMallocHost(&c->hstat, sizeof(fa_dstat)) != cudaSuccess ||
         cudaMallocHost(&c->hvp, fa_ctx::kVpSlots * FA_VP_DOUBLES * sizeof(double)) != cudaSuccess) {
@@ -285,7 +289,7 @@ static int ensure_raster(fa_ctx* ctx, int W, int H, bool depth) {
     ENSURE(small_rec, (T + 1) * sizeof(SmallRec) + (T + 1) * 4);  // records + their triangle ids
     // tile descriptors: 16 B each; a queue overflow costs a rerun of the
     // frame, so start at one descriptor per 8 pixels (C2 views use up to ~1/30)
-    long long want_tiles = (long long)W * H / 8;
+    long long want_tiles = ctx->queue_init > 0 ? 0 : (long long)W * H / 8;
     if (want_tiles > ctx->max_tiles) ctx->max_tiles = (int)(want_tiles < (1ll << 30) ? want_tiles : (1 << 30));
     ENSURE(large, (size_t)ctx->max_large * sizeof(TriSetup));
     ENSURE(tiles, (size_t)ctx->max_tiles * sizeof(int4));

@@ -111,6 +111,7 @@ struct fa_ctx {
     fa_buf vslot, vlist, vuv, vblocks;  // visible vertices: slot per vertex, caller ids, f32 UV pairs, block counts
     size_t gen = 0;
     int max_large = 0, max_tiles = 0;
+    int queue_init = 0;  // FASTATLAS_QUEUE_INIT (tests): initial large/tile queue capacity
     int pack_batch = 0;  // candidates per pack launch
     int64_t pack_cap = 0;  // boxes the pack scratch holds
     bool needs_rerun = false;

@@ -154,3 +154,42 @@ def test_copies_overlap_next_frame_safely(no_wait):
         assert r.returncode != 0, "the unprotected overlap was expected to corrupt a delayed download"
     else:
         assert r.returncode == 0, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("use_graph", [True, False])
+def test_queue_overflow_reruns(use_graph, monkeypatch):
+    """Frames whose large-triangle and tile queues overflow (contexts created
+    with FASTATLAS_QUEUE_INIT=32) grow the queues and rerun; the results equal
+    a default context's, through the engine and through the pipeline (whose
+    slots rerun inside FramePipeline._finish)."""
+    spec = scenes.build_scene("C5")
+    mesh = fa.Mesh(spec.positions, spec.triangles)
+    settings = FrameSettings(screen=spec.screen, omega=spec.omega, use_graph=use_graph)
+    vps = _vps(spec, spec.poses[:4])
+    ref = FrameEngine(mesh, settings=settings)
+    want = [{"chart": o.chart_of_triangle.cpu().numpy(), "uv": o.uv.cpu().numpy(), "plc": o.placements.cpu().numpy(),
+             "scale": o.scale, "counters": ref.counters()} for o in (ref.run(vp) for vp in vps)]
+    assert all(w["counters"]["tiles"] > 32 and w["counters"]["large_records"] > 32 for w in want)
+    monkeypatch.setenv("FASTATLAS_QUEUE_INIT", "32")
+    eng = FrameEngine(mesh, settings=settings)
+    # the first launch really overflows (and asks for a rerun)
+    import ctypes
+    from paper_2502_17712_b200 import _native as nat
+    eng.launch(vps[0])
+    code = eng.ctx.L.fa_frame_finish(eng.ctx.h, ctypes.byref(eng._res), eng._stream)
+    assert code == nat.FA_INTERNAL_ERROR and "rerun" in nat.last_error()
+    for vp, w in zip(vps, want):
+        o = eng.run(vp)
+        assert np.array_equal(o.chart_of_triangle.cpu().numpy(), w["chart"])
+        assert np.array_equal(o.uv.cpu().numpy().view(np.uint32), w["uv"].view(np.uint32))
+        assert np.array_equal(o.placements.cpu().numpy(), w["plc"]) and o.scale == w["scale"]
+    got = []
+    pipe = FramePipeline(mesh, settings=settings, depth=2,
+                         outputs=("chart_of_triangle", "visible", "uv", "placements"))
+    assert pipe.run(vps, lambda hf: got.append((hf.error, hf.chart_of_triangle.copy(), hf.uv.copy(),
+                                                hf.placements.copy(), hf.scale))) == len(vps)
+    for (err, chart, uv, plc, scale), w in zip(got, want):
+        assert err is None, err
+        assert np.array_equal(chart, w["chart"])
+        assert np.array_equal(uv.view(np.uint32), w["uv"].view(np.uint32))
+        assert np.array_equal(plc, w["plc"]) and scale == w["scale"]
