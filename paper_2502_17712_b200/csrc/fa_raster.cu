@@ -1008,15 +1008,25 @@ __global__ void __launch_bounds__(256) k_raster_vis_tiles(const SmallRec* __rest
             if (wi < n_front) rec0 = tiles[wi];
             else if (wi < n_tiles) rec0 = tiles[max_tiles - 1 - (wi - n_front)];
             else rec0 = make_int4(-(wi - n_tiles) - 1, -1, -1, 0);
-            if (rec0.x < 0) {
-                need = true;  // generic setup: decided by the sampling phase
+            if (rec0.x < 0 && rec0.y < 0) {
+                need = true;  // generic setup item (small clipped window): decided by the sampling phase
             } else if (!flags[rec0.z]) {
-                const SmallRec* q = recs + rec0.x;
+                // a record's tile, or a generic (clipped) setup's tile: the
+                // same plane / bbox fields, so the same hi-Z test
                 Setup3 f;
-                f.min_x = q->min_x; f.max_x = q->max_x; f.min_y = q->min_y; f.max_y = q->max_y;
-                f.use_plane = (q->flags >> 3) & 1;
-                f.p0x = q->x0; f.p0y = q->y0; f.p0z = q->z0;
-                f.gx = q->g0; f.gy = q->g1; f.zmean = q->g0;
+                if (rec0.x >= 0) {
+                    const SmallRec* q = recs + rec0.x;
+                    f.min_x = q->min_x; f.max_x = q->max_x; f.min_y = q->min_y; f.max_y = q->max_y;
+                    f.use_plane = (q->flags >> 3) & 1;
+                    f.p0x = q->x0; f.p0y = q->y0; f.p0z = q->z0;
+                    f.gx = q->g0; f.gy = q->g1; f.zmean = q->g0;
+                } else {
+                    const TriSetup* g = large + (-rec0.x - 1);
+                    f.min_x = g->min_x; f.max_x = g->max_x; f.min_y = g->min_y; f.max_y = g->max_y;
+                    f.use_plane = g->use_plane;
+                    f.p0x = g->p0x; f.p0y = g->p0y; f.p0z = g->p0z;
+                    f.gx = g->gx; f.gy = g->gy; f.zmean = g->zmean;
+                }
                 const int ntx = (f.max_x - f.min_x + 1 + TILE_W - 1) / TILE_W;
                 const int xa = f.min_x + (rec0.y % ntx) * TILE_W, ya = f.min_y + (rec0.y / ntx) * TILE_H;
                 const int xb = min(xa + TILE_W - 1, f.max_x), yb = min(ya + TILE_H - 1, f.max_y);
@@ -1111,16 +1121,21 @@ __global__ void __launch_bounds__(256) k_raster_vis_tiles(const SmallRec* __rest
         int x = s.min_x + (rec.y % tx) * TILE_W + (lane & 15);
         int y0 = s.min_y + (rec.y / tx) * TILE_H + (lane >> 4);
         if (x <= s.max_x) {
-            double px = (double)x + 0.5;
+            // the inside tests first, then every covered sample's depth load
+            // in flight together, then the slack tests
+            const double px = (double)x + 0.5;
+            bool in[TILE_H / 2];
+            unsigned long long kq[TILE_H / 2];
+#pragma unroll
             for (int k = 0; k < TILE_H / 2; k++) {
-                int y = y0 + 2 * k;
-                if (y > s.max_y) break;
-                double py = (double)y + 0.5;
-                if (!sample_inside(s, px, py)) continue;
-                double z = sample_depth(s, px, py);
-                double stored = key_f64(depth[(long long)y * W + x]);
-                if (depth_passes(z, stored)) { vis = true; break; }
+                const int y = y0 + 2 * k;
+                in[k] = y <= s.max_y && sample_inside(s, px, (double)y + 0.5);
             }
+#pragma unroll
+            for (int k = 0; k < TILE_H / 2; k++) kq[k] = in[k] ? depth[(long long)(y0 + 2 * k) * W + x] : 0ull;
+#pragma unroll
+            for (int k = 0; k < TILE_H / 2; k++)
+                vis = vis || (in[k] && depth_passes(sample_depth(s, px, (double)(y0 + 2 * k) + 0.5), key_f64(kq[k])));
         }
         if (__any_sync(0xffffffffu, vis) && lane == 0) flags[t] = 1;
         }
