@@ -646,3 +646,36 @@ def test_invalid_mesh_leaves_no_mesh_bound():
         code = ctx.L.fa_frame(ctx.h, vp.ctypes.data_as(ctypes.c_void_p), ctypes.byref(p), ctypes.byref(res),
                               ctx.stream_ptr())
         assert code == nat.FA_NOTHING_VISIBLE
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_frames_vs_oracle(seed):
+    """Seeded random frames: sphere fields (icosphere level 1-2, jittered by
+    the seed) over a ground plane, a random camera (sometimes inside the field
+    or grazing the plane, so the near plane and the frustum sides clip), a
+    random screen and atlas, cull on/off, min_dim/padding; the whole CUDA
+    frame against the C oracle (status, depth, flags, charts, placements, f64
+    UVs)."""
+    rng = np.random.default_rng(1000 + seed)
+    fpos, ftris, frng = scenes.sphere_field(int(rng.integers(1, 3)), seed=seed)
+    pos, tris = scenes._merge((fpos, ftris), scenes.ground_plane(int(rng.integers(4, 24)), int(rng.integers(4, 24)),
+                                                                 rng=frng))
+    W, H = int(rng.integers(48, 700)), int(rng.integers(48, 500))
+    omega = int(2 ** rng.integers(7, 12))
+    eye = np.array([rng.uniform(-7, 7), rng.uniform(-1.2, 4.0), rng.uniform(-12, 6)])
+    target = np.array([rng.uniform(-5, 5), rng.uniform(-1.3, 0.5), rng.uniform(-12, -3)])
+    if np.linalg.norm(target - eye) < 1e-3:
+        target = eye + np.array([0.0, 0.0, -1.0])
+    near = float(rng.choice([0.01, 0.1, 0.5, 1.5]))
+    cam = fa.CameraFrame.from_params(math.radians(rng.uniform(25, 110)), W / H, near, near + rng.uniform(5, 60),
+                                     position=eye, look_at=target, up=(0.0, 1.0, 0.0))
+    cull = bool(rng.integers(0, 4) > 0)
+    min_dim, padding = int(rng.integers(1, 4)), int(rng.integers(0, 3))
+    eng = FrameEngine(fa.Mesh(pos, tris), settings=FrameSettings(screen=(W, H), omega=omega, uv_f64=True,
+                                                                 backface_cull=cull, padding=padding, min_dim=min_dim))
+    out = eng.run(cam.view_proj, check=False)
+    r = oracle.run_frame(pos, tris, cam.view_proj, (W, H), omega, min_dim=min_dim, padding=padding, cull=cull)
+    assert out.status == r.status
+    if r.status == oracle.NOTHING_VISIBLE:
+        return
+    _check_vs_oracle(out.to_host(), r, status_ok=r.status == oracle.OK)
