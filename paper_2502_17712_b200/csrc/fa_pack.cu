@@ -906,7 +906,7 @@ __device__ void select_body(const OwT* ow, const TwT* tw, const TwT* th, const i
                             const int* __restrict__ cand_w, const int* __restrict__ cand_h,
                             const int* __restrict__ cand_y, int n_max, long long* __restrict__ placements,
                             int4* __restrict__ plc_by_src, unsigned char* __restrict__ accept_out,
-                            fa_dstat* __restrict__ st, long long* red, long long* s_best,
+                            fa_dstat* __restrict__ st, long long* red, long long* red2,
                             const long long* __restrict__ ord_tw = nullptr, const long long* __restrict__ ord_th = nullptr,
                             const long long* __restrict__ ord_cid = nullptr) {
     const int tid = threadIdx.x;
@@ -914,25 +914,35 @@ __device__ void select_body(const OwT* ow, const TwT* tw, const TwT* th, const i
         if (tid == 0) { st->scale_num = 1; st->scale_den = 1; st->best = -1; }
         return;
     }
-    // floor-scale width check (packing.py:327-332)
+    // this thread's first output item's selection-independent inputs, loaded
+    // before the reductions so they are in flight beside them
+    int src0 = 0, rot0 = 0;
+    long long cid0 = 0, tw0 = 0, th0 = 0;
+    if (tid < n) {
+        src0 = perm[tid];
+        rot0 = rot[tid];
+        if (ord_tw) {
+            cid0 = ord_cid[tid];
+            tw0 = ord_tw[tid];
+            th0 = ord_th[tid];
+        }
+    }
+    // floor-scale width check (packing.py:327-332) and the largest accepted
+    // candidate, reduced together (one pair of barriers; every thread gets both)
     long long fmax = 0;
     const double rdn = 1.0 / (double)n_scales;
     for (int b = tid; b < n; b += blockDim.x) {
         long long f = scaled_dim_rcp((long long)ow[b], 1, n_scales, rdn, min_dim, pad);
         fmax = f > fmax ? f : fmax;
     }
-    fmax = block_max_ll(fmax, red);
     long long best = 0;
     for (long long i = tid + 1; i <= n_scales; i += blockDim.x) {
         bool acc = cand[CAND_REC * (i - 1)] != 0 && cand[CAND_REC * (i - 1) + 4] >= 0;
         if (accept_out) accept_out[i - 1] = acc;
         if (acc && i > best) best = i;
     }
-    best = block_max_ll(best, red);
+    block_max2_ll(fmax, best, red, red2);
     if (fmax > omega) best = 0;
-    if (tid == 0) *s_best = best;
-    __syncthreads();
-    best = *s_best;
     if (best == 0) {
         if (tid == 0) { atomicOr(&st->flags, FA_DFLAG_PACK_FAILURE); st->best = 0; }
         return;
@@ -949,12 +959,13 @@ __device__ void select_body(const OwT* ow, const TwT* tw, const TwT* th, const i
         long long q = p[j] & (omega - 1);
         int r = (int)(p[j] >> kbits);  // row index < n <= 2^31
         long long x = (r % FA_DIRECTION_PERIOD == 0) ? q : omega - q - w[j];
-        int src = perm[j];
+        const bool first = j == tid;
+        int src = first ? src0 : perm[j];
         long long* P = placements + 8 * (long long)j;
         if (ord_tw) {  // packing-order copies (k_order_frame): no dependent load through perm
-            P[0] = ord_cid[j];
-            P[6] = ord_tw[j];
-            P[7] = ord_th[j];
+            P[0] = first ? cid0 : ord_cid[j];
+            P[6] = first ? tw0 : ord_tw[j];
+            P[7] = first ? th0 : ord_th[j];
         } else {
             P[0] = chart_id_i ? (long long)chart_id_i[src] : (chart_id ? chart_id[src] : src);
             P[6] = tw[src];
@@ -964,10 +975,11 @@ __device__ void select_body(const OwT* ow, const TwT* tw, const TwT* th, const i
         P[2] = y[j];
         P[3] = w[j];
         P[4] = h[j];
-        P[5] = rot[j];
+        const int rj = first ? rot0 : rot[j];
+        P[5] = rj;
         if (plc_by_src) {  // k_uv reads its chart's placement directly (x, y, w, h < 2^31)
             plc_by_src[2 * src] = make_int4((int)x, y[j], w[j], h[j]);
-            plc_by_src[2 * src + 1] = make_int4(rot[j], 0, 0, 0);
+            plc_by_src[2 * src + 1] = make_int4(rj, 0, 0, 0);
         }
         long long cw = w[j] - 2 * pad, chh = h[j] - 2 * pad;
         tex += (cw > 0 ? cw : 0) * (chh > 0 ? chh : 0);
@@ -995,13 +1007,13 @@ __global__ void __launch_bounds__(1024) k_select(const long long* __restrict__ o
                                                  const long long* __restrict__ ord_cid) {
     FA_PDL_PROLOGUE();
     __shared__ long long red[33];
-    __shared__ long long s_best;
+    __shared__ long long red2[33];
     int n = n_dev ? *n_dev : n_max;
     if (st->flags & (FA_DFLAG_HEIGHT_OVERFLOW | FA_DFLAG_KEY_RANGE | FA_DFLAG_DUPLICATE_MIN_TRI |
                      FA_DFLAG_QUEUE_OVERFLOW))
         return;
     select_body(ow, tw, th, (const int*)nullptr, chart_id, rot, perm, n, omega, n_scales, min_dim, pad, cand, cand_p,
-                cand_w, cand_h, cand_y, n_max, placements, plc_by_src, accept_out, st, red, &s_best, ord_tw, ord_th,
+                cand_w, cand_h, cand_y, n_max, placements, plc_by_src, accept_out, st, red, red2, ord_tw, ord_th,
                 ord_cid);
 }
 
