@@ -137,7 +137,10 @@ __device__ __forceinline__ int uf_root(const int* label, int t) {
     }
 }
 
-__global__ void __launch_bounds__(256) k_chart_bounds(const ClipSrc clip, const int* __restrict__ tris,
+#ifndef BOUNDS_MIN_BLOCKS
+#define BOUNDS_MIN_BLOCKS 1  // minimum resident CTAs per SM (register cap)
+#endif
+__global__ void __launch_bounds__(256, BOUNDS_MIN_BLOCKS) k_chart_bounds(const ClipSrc clip, const int* __restrict__ tris,
                                                       const int* __restrict__ vis_list, const int* label,
                                                       const int* __restrict__ cidx,
                                                       unsigned long long* __restrict__ keys,

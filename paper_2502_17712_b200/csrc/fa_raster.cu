@@ -897,7 +897,10 @@ __global__ void __launch_bounds__(256) k_vis_small_filter(const SmallRec* __rest
 // batch of depth loads.  Warp queue (windows above FA_VIS_WARP_PX): one warp
 // per record, the window's samples dealt over the lanes (<= FA_SMALL_PX / 32
 // each, their depth loads issued together).
-__global__ void __launch_bounds__(256) k_vis_small_sample(const SmallRec* __restrict__ small_rec, int T, int W,
+#ifndef VSAMPLE_MIN_BLOCKS
+#define VSAMPLE_MIN_BLOCKS 1  // minimum resident CTAs per SM (register cap)
+#endif
+__global__ void __launch_bounds__(256, VSAMPLE_MIN_BLOCKS) k_vis_small_sample(const SmallRec* __restrict__ small_rec, int T, int W,
                                                           const unsigned long long* __restrict__ depth,
                                                           const int* __restrict__ queue,
                                                           unsigned char* __restrict__ flags,

@@ -33,8 +33,11 @@ __device__ __forceinline__ bool tri_stretch(const double (&s)[6], const double (
     return true;
 }
 
+#ifndef UV_MIN_BLOCKS
+#define UV_MIN_BLOCKS 1  // minimum resident CTAs per SM (register cap)
+#endif
 template <typename OutT>
-__global__ void __launch_bounds__(UV_THREADS) k_uv(const ClipSrc clip, const int* __restrict__ tris,
+__global__ void __launch_bounds__(UV_THREADS, UV_MIN_BLOCKS) k_uv(const ClipSrc clip, const int* __restrict__ tris,
                                                    const int* __restrict__ vis_list, const int* __restrict__ label,
                                                    const int* __restrict__ cidx, const int* __restrict__ pinv,
                                                    const double* __restrict__ ndc, const int* __restrict__ px,
