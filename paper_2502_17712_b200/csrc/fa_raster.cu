@@ -248,6 +248,8 @@ __global__ void __launch_bounds__(SETUP_WARPS * 32, SETUP_MIN_BLOCKS) k_raster_s
     // deferred publication (see the loop): the records of a step wait in
     // shared memory until the next step's barrier has published their bases
     __shared__ SmallRec s_stage[SETUP_WARPS][32];
+    static_assert(SETUP_WARPS * 32 * sizeof(SmallRec) <= 40 * 1024,
+                  "SETUP_DEFER stages 3 KB per warp in static shared memory: at most 13 warps per block");
     int step = 0, resv = 0;
     unsigned pm1 = 0, pm2 = 0, pm3 = 0;
     int p_kind = 0, p_t = 0, p_nt = 0, p_incl = 0, p_total = 0;
