@@ -467,7 +467,18 @@ def main(argv=None, measure=None):
     import torch
     import torch.distributed as dist
 
-    if world > 1:
+    # under torchrun the process group is set up even for one rank, so the
+    # NCCL barrier / reduction path is the one a multi-GPU run takes
+    use_pg = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ
+    json_out = sys.stdout
+    if use_pg:
+        if sys.stdout is sys.__stdout__:
+            # stdout carries the one JSON line only: NCCL (and anything else
+            # native) prints to file descriptor 1, so that descriptor goes to
+            # stderr and the line is written to a saved copy of the original
+            sys.stdout.flush()
+            json_out = os.fdopen(os.dup(1), "w")
+            os.dup2(2, 1)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         backend = os.environ.get("FA_BENCH_BACKEND", "nccl")
         if backend == "nccl":
@@ -547,8 +558,8 @@ def main(argv=None, measure=None):
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_sample()
-        print(json.dumps(line), flush=True)
-    if world > 1:
+        print(json.dumps(line), file=json_out, flush=True)
+    if use_pg:
         dist.barrier()
         dist.destroy_process_group()
 

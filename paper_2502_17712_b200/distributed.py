@@ -40,7 +40,7 @@ def max_over_ranks(values, device=None):
     import torch
     import torch.distributed as dist
     t = torch.tensor([float(v) for v in values], dtype=torch.float64, device=device)
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+    if dist.is_available() and dist.is_initialized():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return [float(v) for v in t.cpu()]
 
@@ -50,7 +50,7 @@ def sum_over_ranks(values, device=None):
     import torch
     import torch.distributed as dist
     t = torch.tensor([float(v) for v in values], dtype=torch.float64, device=device)
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+    if dist.is_available() and dist.is_initialized():
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return [float(v) for v in t.cpu()]
 
@@ -58,7 +58,7 @@ def sum_over_ranks(values, device=None):
 def barrier(device=None):
     import torch
     import torch.distributed as dist
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+    if dist.is_available() and dist.is_initialized():
         dist.barrier()
     if device is not None and torch.cuda.is_available():
         torch.cuda.synchronize(device)
